@@ -1,0 +1,233 @@
+/*
+ * topopt_b200 — C ABI of the B200 DC N-1 MapElites engine.
+ *
+ * Drop-in boundary for the reference's hot path (arxiv/paper_2605_10128,
+ * /root/reference/proj). The reference exposes a C++ API only; every entry
+ * point below names the reference interface it replaces (file:line) and keeps
+ * its argument meaning and error behaviour. Conventions:
+ *   - plain pointers and sizes, caller-owned host buffers, context-owned device
+ *     memory; no C++ types and no exceptions cross this boundary;
+ *   - every call returns a tg_status; tg_last_error() holds the message of the
+ *     most recent failure on the calling thread; statuses mirror
+ *     include/topopt/errors.hpp:9-34 (ParseError ... IoError);
+ *   - calls on one context are serialized on one CUDA stream, matching
+ *     run_optimizer's single-threaded use of a DcContext (qd_optimizer.cpp:344).
+ * See INTEGRATION.md for the reference-side shim that binds these symbols.
+ */
+#ifndef TOPOPT_B200_H
+#define TOPOPT_B200_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum tg_status {
+  TG_OK = 0,
+  TG_PARSE_ERROR = 1,            /* errors.hpp:9-12  ParseError */
+  TG_VALIDATION_ERROR = 2,       /* errors.hpp:14-17 ValidationError */
+  TG_ISLANDED_CONTINGENCY = 3,   /* errors.hpp:19-22 IslandedContingency */
+  TG_SINGULAR_SYSTEM = 4,        /* errors.hpp:24-27 SingularSystem */
+  TG_CONFIG_ERROR = 5,           /* errors.hpp:29-31 ConfigError */
+  TG_IO_ERROR = 6,               /* errors.hpp:33-35 IoError */
+  TG_CUDA_ERROR = 7,             /* device failure (no CPU fallback exists) */
+  TG_CAPACITY_ERROR = 8          /* a candidate exceeded a compile-time capacity */
+} tg_status;
+
+typedef struct tg_grid tg_grid;           /* host network model (GridModel) */
+typedef struct tg_actionset tg_actionset; /* host action encoding (ActionSet) */
+typedef struct tg_context tg_context;     /* device-resident DcContext */
+
+/* ---- plain-data network description (replaces const GridModel&,
+ *      grid_model.hpp:80-127); arrays are read during tg_context_create only ---- */
+typedef struct tg_grid_desc {
+  int32_t n_nodes, n_branches, n_injections, slack;
+  const int32_t* branch_from;       /* [n_branches] node index */
+  const int32_t* branch_to;
+  const double* branch_x;           /* series reactance, p.u. (> 0) */
+  const double* branch_limit;       /* MW */
+  const uint8_t* branch_in_service;
+  const int32_t* injection_node;    /* [n_injections] */
+  const double* injection_net_mw;   /* Injection::net_mw(), grid_model.hpp:45 */
+  int32_t n_contingencies;
+  const int32_t* cont_branch_ptr;   /* [n_contingencies+1] CSR */
+  const int32_t* cont_branch;
+  const int32_t* cont_inj_ptr;      /* [n_contingencies+1] CSR */
+  const int32_t* cont_inj;
+  int32_t n_substations;
+  const int32_t* sub_node;          /* [n_substations] switchable node */
+  const int32_t* sub_term_ptr;      /* [n_substations+1] CSR over terminals */
+  const int32_t* term_kind;         /* 0 branch from-end, 1 branch to-end, 2 injection */
+  const int32_t* term_element;      /* branch or injection index */
+  int32_t n_busbar_outages;
+  const int32_t* bo_substation;     /* [n_busbar_outages] */
+  const int32_t* bo_busbar;         /* busbar index within the substation */
+  const int32_t* bo_implied_ptr;    /* [n_busbar_outages+1] default implied branches, grid_model.cpp:217-227 */
+  const int32_t* bo_implied;
+} tg_grid_desc;
+
+/* ---- plain-data action encoding (replaces const ActionSet&, importer.hpp:28-35).
+ *      Actions of one substation must be contiguous (station_ranges). ---- */
+typedef struct tg_actionset_desc {
+  int32_t n_actions;
+  const int32_t* action_substation;     /* [n_actions] */
+  const int32_t* action_lambda_r;       /* Action::reassignment_distance */
+  const int32_t* action_group_ptr;      /* [n_actions+1] into action_group */
+  const uint8_t* action_group;          /* per terminal of the station: 1 = moves to the new node */
+  const int32_t* action_busbar_ptr;     /* [n_actions+1] into action_implied_ptr (one slot per busbar) */
+  const int32_t* action_implied_ptr;    /* implied branches per (action, busbar), grid_model.cpp:229-242 */
+  const int32_t* action_implied;
+  int32_t n_disconnectables;
+  const int32_t* disconnectables;       /* branch indices, ascending */
+} tg_actionset_desc;
+
+/* DcConfig, dc_engine.hpp:16-23 (threads is accepted and ignored on the GPU). */
+typedef struct tg_dc_config {
+  double islanding_penalty_mw;
+  int32_t worst_k;
+  double weight_c0;
+  double weight_c;
+  int32_t fitness_variant;
+  int32_t threads;
+} tg_dc_config;
+
+/* ScoreVector, dc_engine.hpp:25-39, for n candidates (SoA, caller-owned, length n
+ * except worst_* which are [n][worst_k]). Any pointer may be NULL. */
+typedef struct tg_scores {
+  double* lambda_o;
+  int32_t* lambda_c;
+  int32_t* lambda_c0;
+  double* lambda_b;
+  int32_t* lambda_d;
+  int32_t* lambda_s;
+  int32_t* lambda_r;
+  double* fitness;
+  uint8_t* islanded;
+  int32_t* worst_idx;     /* contingency index, -1 padded */
+  double* worst_energy;
+  int32_t* worst_n;
+  int32_t* islanded_outages;        /* FlowResult::islanded_outages */
+  int32_t* islanded_busbar_outages; /* FlowResult::islanded_busbar_outages */
+} tg_scores;
+
+/* QdConfig, qd_optimizer.hpp:15-32 */
+typedef struct tg_qd_config {
+  int32_t n_a, n_d, batch_size, iters_per_epoch, cell_capacity;
+  double mutation_mean;
+  double p_action[4];
+  double p_disc[4];
+  double p_crossover_parent1;
+  int32_t d_max, s_max, r_max;
+  uint64_t seed;
+  int64_t max_evaluations;
+  double max_seconds;
+} tg_qd_config;
+
+/* One archive entry of a RepertoireSnapshot (qd_optimizer.hpp:83-95). */
+typedef struct tg_snapshot_view {
+  int32_t epoch;
+  int64_t evaluations;
+  double best_fitness;
+  int32_t final_snapshot;
+  int32_t n_entries;
+  int32_t n_slots;                  /* n_a + n_d */
+  const int32_t* cell;              /* [n_entries] */
+  const int32_t* genome;            /* [n_entries][n_slots] */
+  const double* fitness;
+  const double* lambda_o;
+  const int32_t* lambda_c;
+  const int32_t* lambda_c0;
+  const double* lambda_b;
+  const int32_t* lambda_d;
+  const int32_t* lambda_s;
+  const int32_t* lambda_r;
+  const int32_t* worst_idx;         /* [n_entries][worst_k] */
+  const double* worst_energy;
+  const int32_t* worst_n;
+  int32_t worst_k;
+} tg_snapshot_view;
+
+/* SnapshotSink, qd_optimizer.hpp:100: invoked on the calling thread after each epoch. */
+typedef void (*tg_snapshot_cb)(const tg_snapshot_view* snap, void* user);
+
+typedef struct tg_opt_stats {
+  int64_t evaluations;   /* OptimizerStats, qd_optimizer.hpp:102-107 */
+  int32_t epochs;
+  int32_t n_trace;       /* fitness_trace entries written to the caller's arrays */
+} tg_opt_stats;
+
+const char* tg_last_error(void);
+const char* tg_version(void);
+
+/* ---- host-side model and import (the engine's own loaders) ---- */
+/* load_grid / grid_from_json_text, grid_model.hpp:130-131 */
+tg_status tg_grid_from_json(const char* text, size_t len, tg_grid** out);
+void tg_grid_destroy(tg_grid* grid);
+/* fills a desc whose arrays point into the grid object (valid while it lives) */
+tg_status tg_grid_describe(const tg_grid* grid, tg_grid_desc* out);
+/* build_action_set, importer.hpp:80 (EnumerationConfig seed/cap, importer.hpp:68-71) */
+tg_status tg_actionset_build(const tg_grid* grid, uint64_t seed, int64_t cap, tg_actionset** out);
+/* load_action_set / save_action_set, importer.hpp:91-94 (JSON text in memory) */
+tg_status tg_actionset_from_json(const tg_grid* grid, const char* text, size_t len, tg_actionset** out);
+tg_status tg_actionset_to_json(const tg_actionset* set, const tg_grid* grid, char** text_out); /* free with tg_free */
+void tg_actionset_destroy(tg_actionset* set);
+tg_status tg_actionset_describe(const tg_actionset* set, const tg_grid* grid, tg_actionset_desc* out);
+void tg_free(void* p);
+
+/* ---- DcContext (dc_engine.hpp:95-150) ---- */
+/* DcContext::DcContext, dc_engine.cpp:80-145: base factorization on `device`,
+ * action busbar tables, pre-optimization score. SingularSystem on a
+ * disconnected grid. */
+tg_status tg_context_create(const tg_grid_desc* grid, const tg_actionset_desc* actions, const tg_dc_config* config,
+                            int device, tg_context** out);
+void tg_context_destroy(tg_context* ctx);
+/* DcContext::evaluate_batch, dc_engine.cpp:439-468 (and ::evaluate for n=1):
+ * genomes [n][n_a+n_d] (-1 = empty slot). batch_size pads like the reference
+ * (padding is evaluated and dropped). Optional FlowResult outputs
+ * (dc_engine.hpp:41-48), NULL to skip: base_flows/max_contingency/max_busbar
+ * [n][n_branches], outage_energy [n][n_contingencies]. */
+tg_status tg_evaluate_batch(tg_context* ctx, const int32_t* genomes, int32_t n, int32_t n_a, int32_t n_d,
+                            int32_t batch_size, tg_scores* out, double* base_flows, double* max_contingency,
+                            double* max_busbar, double* outage_energy);
+/* Same batch with genomes and scores already in device memory (no host copies). */
+tg_status tg_evaluate_batch_device(tg_context* ctx, const int32_t* d_genomes, int32_t n, int32_t n_a, int32_t n_d,
+                                   tg_scores* d_out);
+/* DcContext::pre_optimization_score / lambda_b_pre, dc_engine.hpp:112-113 */
+tg_status tg_pre_score(tg_context* ctx, tg_scores* out, double* lambda_b_pre);
+
+/* ---- MapElites loop (qd_optimizer.hpp:116-118) ---- */
+/* run_optimizer, qd_optimizer.cpp:344-417: device-resident loop; mutation,
+ * crossover, evaluation and archive insert stay on the GPU, one snapshot D2H
+ * per epoch. stop is polled before every iteration. fitness_trace arrays may be
+ * NULL; trace_cap bounds them. ConfigError as the reference. */
+tg_status tg_optimizer_run(tg_context* ctx, const tg_qd_config* cfg, tg_snapshot_cb cb, void* user,
+                           const volatile int32_t* stop, tg_opt_stats* stats, int64_t* trace_evaluations,
+                           double* trace_best, int32_t trace_cap);
+/* Archive of the last run as a snapshot view (valid until the next call). */
+tg_status tg_archive_export(tg_context* ctx, tg_snapshot_view* out);
+/* Repertoire::insert replay (qd_optimizer.cpp:281-303) on the device archive:
+ * resets an archive for cfg and inserts n (genome, score) pairs in order.
+ * inserted[n] (optional) receives Repertoire::insert's return value. */
+tg_status tg_archive_replay(tg_context* ctx, const tg_qd_config* cfg, const int32_t* genomes, int32_t n,
+                            const tg_scores* scores, uint8_t* inserted);
+/* descriptor_to_cell, qd_optimizer.cpp:12-17 */
+int32_t tg_descriptor_to_cell(int32_t lambda_d, int32_t lambda_s, int32_t lambda_r, const tg_qd_config* cfg);
+/* Device mutation / crossover of single lanes with the reference RNG stream
+ * (mt19937_64 + libstdc++ distributions, qd_optimizer.cpp:202-277).
+ * parents [n][n_slots], seeds [n]: one lane per entry. */
+tg_status tg_mutate_lanes(tg_context* ctx, const tg_qd_config* cfg, const int32_t* parents, const uint64_t* seeds,
+                          int32_t n, int32_t* children);
+tg_status tg_crossover_lanes(tg_context* ctx, const tg_qd_config* cfg, const int32_t* parents1,
+                             const int32_t* parents2, const uint64_t* seeds, int32_t n, int32_t* children);
+
+/* ---- counters for the benchmark contract ---- */
+tg_status tg_context_info(tg_context* ctx, int64_t* values, int32_t n_values); /* see capi.cu */
+int64_t tg_kernel_launches(tg_context* ctx);  /* engine kernels launched so far */
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* TOPOPT_B200_H */

@@ -1,0 +1,12 @@
+"""B200-native DC N-1 MapElites engine (drop-in for the reference's hot path).
+
+Host API mirroring /root/reference/proj/include/topopt over the C ABI of
+libtopopt_b200.so (include/topopt_b200.h); see api.py.
+"""
+from .api import (ActionSet, CapacityError, ConfigError, CudaError, DcConfig, DcContext, FlowResult, Genome,
+                  GridModel, IoError, IslandedContingency, OptimizerResult, OptimizerStats, ParseError, QdConfig,
+                  RepertoireSnapshot, ScoreArrays, ScoreVector, SingularSystem, SnapshotEntry, TopoptError,
+                  ValidationError, build_action_set, cell_count, descriptor_to_cell, grid_from_json_text,
+                  kIslandedFitness, load_action_set, load_grid, run_optimizer, save_action_set)
+
+__all__ = [name for name in dir() if not name.startswith("_")]

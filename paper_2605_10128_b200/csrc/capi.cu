@@ -1,0 +1,747 @@
+// C-ABI implementation: host model objects, device context, evaluation and
+// optimizer entry points (declared in include/topopt_b200.h).
+#include <algorithm>
+#include <cstdio>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <string>
+#include <vector>
+
+#include "../../include/topopt_b200.h"
+#include "cuda/engine.cuh"
+#include "cuda/qd.cuh"
+#include "host/model.hpp"
+
+namespace {
+
+thread_local std::string g_error;
+
+struct CudaFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+struct CapacityFailure : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
+
+void check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+template <class F>
+tg_status guarded(F&& f) {
+  try {
+    f();
+    return TG_OK;
+  } catch (const tgb::ParseError& e) {
+    g_error = e.what();
+    return TG_PARSE_ERROR;
+  } catch (const tgb::ValidationError& e) {
+    g_error = e.what();
+    return TG_VALIDATION_ERROR;
+  } catch (const tgb::IslandedContingency& e) {
+    g_error = e.what();
+    return TG_ISLANDED_CONTINGENCY;
+  } catch (const tgb::SingularSystem& e) {
+    g_error = e.what();
+    return TG_SINGULAR_SYSTEM;
+  } catch (const tgb::ConfigError& e) {
+    g_error = e.what();
+    return TG_CONFIG_ERROR;
+  } catch (const tgb::IoError& e) {
+    g_error = e.what();
+    return TG_IO_ERROR;
+  } catch (const CudaFailure& e) {
+    g_error = e.what();
+    return TG_CUDA_ERROR;
+  } catch (const CapacityFailure& e) {
+    g_error = e.what();
+    return TG_CAPACITY_ERROR;
+  } catch (const std::exception& e) {
+    g_error = e.what();
+    return TG_VALIDATION_ERROR;
+  }
+}
+
+// Device allocation owner.
+class DeviceArena {
+ public:
+  ~DeviceArena() {
+    for (void* p : ptrs_) cudaFree(p);
+  }
+  template <class T>
+  T* alloc(size_t n) {
+    void* p = nullptr;
+    if (n == 0) n = 1;
+    check(cudaMalloc(&p, n * sizeof(T)), "cudaMalloc");
+    ptrs_.push_back(p);
+    bytes_ += n * sizeof(T);
+    return static_cast<T*>(p);
+  }
+  template <class T>
+  T* upload(const std::vector<T>& v, cudaStream_t s) {
+    T* d = alloc<T>(v.size());
+    if (!v.empty()) check(cudaMemcpyAsync(d, v.data(), v.size() * sizeof(T), cudaMemcpyHostToDevice, s), "upload");
+    return d;
+  }
+  size_t bytes() const { return bytes_; }
+
+ private:
+  std::vector<void*> ptrs_;
+  size_t bytes_ = 0;
+};
+
+}  // namespace
+
+// ---------------------------------------------------------------- host objects
+struct tg_grid {
+  tgb::Grid g;
+  std::vector<int32_t> br_from, br_to, inj_node, cont_bptr, cont_b, cont_iptr, cont_i, sub_node, sub_tptr, tkind,
+      telem, bo_sub, bo_bb, bo_iptr, bo_i;
+  std::vector<double> br_x, br_lim, inj_net;
+  std::vector<uint8_t> br_on;
+};
+
+struct tg_actionset {
+  tgb::ActionTable t;
+  std::vector<int32_t> station, lambda_r, gptr, bbptr, iptr, imp, disc;
+  std::vector<uint8_t> group;
+};
+
+namespace {
+
+void flatten_grid(tg_grid& h) {
+  const tgb::Grid& g = h.g;
+  h.br_from.assign(g.br_from.begin(), g.br_from.end());
+  h.br_to.assign(g.br_to.begin(), g.br_to.end());
+  h.br_x = g.br_x;
+  h.br_lim = g.br_limit;
+  h.br_on.assign(g.br_on.begin(), g.br_on.end());
+  h.inj_node.assign(g.inj_node.begin(), g.inj_node.end());
+  h.inj_net.clear();
+  for (int i = 0; i < g.n_injections(); ++i) h.inj_net.push_back(g.inj_net(i));
+  h.cont_bptr = {0};
+  h.cont_iptr = {0};
+  h.cont_b.clear();
+  h.cont_i.clear();
+  for (size_t c = 0; c < g.cont_id.size(); ++c) {
+    for (int e : g.cont_branches[c]) h.cont_b.push_back(e);
+    for (int i : g.cont_injections[c]) h.cont_i.push_back(i);
+    h.cont_bptr.push_back(static_cast<int32_t>(h.cont_b.size()));
+    h.cont_iptr.push_back(static_cast<int32_t>(h.cont_i.size()));
+  }
+  h.sub_node.clear();
+  h.sub_tptr = {0};
+  h.tkind.clear();
+  h.telem.clear();
+  for (const auto& st : g.stations) {
+    h.sub_node.push_back(st.node);
+    for (size_t t = 0; t < st.term_kind.size(); ++t) {
+      h.tkind.push_back(st.term_kind[t]);
+      h.telem.push_back(st.term_index[t]);
+    }
+    h.sub_tptr.push_back(static_cast<int32_t>(h.tkind.size()));
+  }
+  h.bo_sub.assign(g.bo_station.begin(), g.bo_station.end());
+  h.bo_bb.assign(g.bo_busbar.begin(), g.bo_busbar.end());
+  h.bo_iptr = {0};
+  h.bo_i.clear();
+  for (size_t b = 0; b < g.bo_id.size(); ++b) {
+    for (int e : g.default_implied(static_cast<int>(b))) h.bo_i.push_back(e);
+    h.bo_iptr.push_back(static_cast<int32_t>(h.bo_i.size()));
+  }
+}
+
+void flatten_actions(tg_actionset& a, const tgb::Grid& g) {
+  const tgb::ActionTable& t = a.t;
+  a.station.assign(t.station.begin(), t.station.end());
+  a.lambda_r.assign(t.lambda_r.begin(), t.lambda_r.end());
+  a.gptr = {0};
+  a.group.clear();
+  a.bbptr = {0};
+  a.iptr = {0};
+  a.imp.clear();
+  for (int k = 0; k < t.n_actions(); ++k) {
+    for (char x : t.group[k]) a.group.push_back(static_cast<uint8_t>(x));
+    a.gptr.push_back(static_cast<int32_t>(a.group.size()));
+    const auto& st = g.stations[t.station[k]];
+    for (int bb = 0; bb < static_cast<int>(st.busbars.size()); ++bb) {
+      for (int e : g.implied_branches(t.station[k], bb, t.assignment[k], t.open_couplers[k])) a.imp.push_back(e);
+      a.iptr.push_back(static_cast<int32_t>(a.imp.size()));
+    }
+    a.bbptr.push_back(static_cast<int32_t>(a.iptr.size() - 1));
+  }
+  a.disc.assign(t.disconnectables.begin(), t.disconnectables.end());
+}
+
+}  // namespace
+
+// ---------------------------------------------------------------- device context
+struct tg_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DeviceArena arena;
+  tgb::DevGrid g{};
+  tgb::DcParams params{};
+  int n_cont = 0;
+  int worst_k = 20;
+  int64_t launches = 0;
+  // evaluation batch buffers
+  int capacity = 0;
+  std::unique_ptr<DeviceArena> batch_arena;
+  tgb::Batch batch{};
+  tgb::EvalScratch scratch{};
+  int* d_genomes = nullptr;
+  // pre-optimization score
+  std::vector<double> pre;  // lambda_o, lambda_c, lambda_c0, lambda_b, fitness
+  double lambda_b_pre = 0.0;
+  // optimizer state
+  std::unique_ptr<tgb::QdState> qd;
+  std::vector<int32_t> snap_cell, snap_genome, snap_lc, snap_lc0, snap_ld, snap_ls, snap_lr, snap_widx, snap_wn;
+  std::vector<double> snap_fit, snap_lo, snap_lb, snap_wval;
+  tg_snapshot_view last_view{};
+  int n_a_cap = 4, n_d_cap = 4;
+
+  void ensure_capacity(int n);
+  void run_batch(int n, int n_a, int n_d, bool full);
+};
+
+void tg_context::ensure_capacity(int n) {
+  if (n <= capacity) return;
+  const int cap = std::max(n, 64);
+  batch_arena = std::make_unique<DeviceArena>();
+  DeviceArena& A = *batch_arena;
+  tgb::Batch& b = batch;
+  const size_t E = g.E, Kp = g.Kpad, Ka = std::max(g.Kall, 1);
+  d_genomes = A.alloc<int>(static_cast<size_t>(cap) * tgb::kMaxSlots);
+  b.status = A.alloc<int>(cap);
+  b.rank = A.alloc<int>(cap);
+  b.removed = A.alloc<int>(static_cast<size_t>(cap) * tgb::kMaxRemovedSweep);
+  b.feat = A.alloc<double>(static_cast<size_t>(cap) * E * tgb::kStride);
+  b.kdat = A.alloc<double>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1) * tgb::kStride);
+  b.kflag = A.alloc<uint8_t>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1));
+  b.fmax = A.alloc<unsigned long long>(static_cast<size_t>(cap) * E);
+  b.fbus = A.alloc<unsigned long long>(static_cast<size_t>(cap) * E);
+  b.energy = A.alloc<double>(static_cast<size_t>(cap) * Ka);
+  b.isl_out = A.alloc<int>(cap);
+  b.isl_bus = A.alloc<int>(cap);
+  b.wl_list = A.alloc<int>(cap);
+  b.wl_start = A.alloc<int>(tgb::kSweepRank + 1);
+  b.wl_count = A.alloc<int>(tgb::kSweepRank + 1);
+  b.wl_group0 = A.alloc<int>(tgb::kSweepRank + 2);
+  tgb::Scores& o = b.out;
+  o.lambda_o = A.alloc<double>(cap);
+  o.lambda_c = A.alloc<int>(cap);
+  o.lambda_c0 = A.alloc<int>(cap);
+  o.lambda_b = A.alloc<double>(cap);
+  o.lambda_d = A.alloc<int>(cap);
+  o.lambda_s = A.alloc<int>(cap);
+  o.lambda_r = A.alloc<int>(cap);
+  o.fitness = A.alloc<double>(cap);
+  o.islanded = A.alloc<uint8_t>(cap);
+  o.error = A.alloc<int>(cap);
+  o.worst_idx = A.alloc<int>(static_cast<size_t>(cap) * std::max(worst_k, 1));
+  o.worst_val = A.alloc<double>(static_cast<size_t>(cap) * std::max(worst_k, 1));
+  o.worst_n = A.alloc<int>(cap);
+  o.isl_out = A.alloc<int>(cap);
+  o.isl_bus = A.alloc<int>(cap);
+  // Z scratch: bounded so huge grids stay within a fixed budget
+  const size_t row_prep = static_cast<size_t>(std::max(g.Nr, 1)) * tgb::kStride * sizeof(double);
+  const size_t budget = size_t{2} << 30;
+  scratch.zslots = static_cast<int>(std::max<size_t>(1, std::min<size_t>(cap, budget / row_prep)));
+  scratch.zprep = A.alloc<double>(static_cast<size_t>(scratch.zslots) * std::max(g.Nr, 1) * tgb::kStride);
+  const size_t row_sp = static_cast<size_t>(std::max(g.Nr, 1)) * tgb::kMaxCols * sizeof(double);
+  scratch.zslots_special = static_cast<int>(std::max<size_t>(1, std::min<size_t>(1024, (size_t{1} << 30) / row_sp)));
+  scratch.zspecial = A.alloc<double>(static_cast<size_t>(scratch.zslots_special) * std::max(g.Nr, 1) * tgb::kMaxCols);
+  capacity = cap;
+}
+
+void tg_context::run_batch(int n, int n_a, int n_d, bool full) {
+  batch.n = n;
+  batch.genomes = d_genomes;
+  batch.params = params;
+  int kernels = 0;
+  tgb::launch_evaluate(g, batch, n_a, n_d, full, scratch, stream, &kernels);
+  launches += kernels;
+  check(cudaGetLastError(), "evaluate launch");
+}
+
+namespace {
+
+void copy_scores(tg_context* ctx, int n, tg_scores* out) {
+  if (!out) return;
+  const tgb::Scores& o = ctx->batch.out;
+  cudaStream_t s = ctx->stream;
+  auto cp = [&](void* dst, const void* src, size_t bytes) {
+    if (dst) check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "scores D2H");
+  };
+  cp(out->lambda_o, o.lambda_o, n * sizeof(double));
+  cp(out->lambda_c, o.lambda_c, n * sizeof(int));
+  cp(out->lambda_c0, o.lambda_c0, n * sizeof(int));
+  cp(out->lambda_b, o.lambda_b, n * sizeof(double));
+  cp(out->lambda_d, o.lambda_d, n * sizeof(int));
+  cp(out->lambda_s, o.lambda_s, n * sizeof(int));
+  cp(out->lambda_r, o.lambda_r, n * sizeof(int));
+  cp(out->fitness, o.fitness, n * sizeof(double));
+  cp(out->islanded, o.islanded, n * sizeof(uint8_t));
+  cp(out->worst_n, o.worst_n, n * sizeof(int));
+  cp(out->islanded_outages, o.isl_out, n * sizeof(int));
+  cp(out->islanded_busbar_outages, o.isl_bus, n * sizeof(int));
+  cp(out->worst_idx, o.worst_idx, static_cast<size_t>(n) * ctx->worst_k * sizeof(int));
+  cp(out->worst_energy, o.worst_val, static_cast<size_t>(n) * ctx->worst_k * sizeof(double));
+}
+
+void check_errors(tg_context* ctx, int n) {
+  std::vector<int> err(n);
+  check(cudaMemcpyAsync(err.data(), ctx->batch.out.error, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream),
+        "error D2H");
+  check(cudaStreamSynchronize(ctx->stream), "evaluate");
+  for (int i = 0; i < n; ++i)
+    if (err[i] != 0)
+      throw CapacityFailure("candidate " + std::to_string(i) +
+                            " exceeds the engine's compile-time capacity (rank/removed/moved limits)");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* tg_last_error(void) { return g_error.c_str(); }
+const char* tg_version(void) { return "topopt_b200 0.1 (sm_100a)"; }
+void tg_free(void* p) { std::free(p); }
+
+tg_status tg_grid_from_json(const char* text, size_t len, tg_grid** out) {
+  return guarded([&] {
+    auto h = std::make_unique<tg_grid>();
+    h->g = tgb::load_grid_json(std::string(text, len));
+    flatten_grid(*h);
+    *out = h.release();
+  });
+}
+
+void tg_grid_destroy(tg_grid* grid) { delete grid; }
+
+tg_status tg_grid_describe(const tg_grid* h, tg_grid_desc* d) {
+  return guarded([&] {
+    const tgb::Grid& g = h->g;
+    d->n_nodes = g.n_nodes();
+    d->n_branches = g.n_branches();
+    d->n_injections = g.n_injections();
+    d->slack = g.slack;
+    d->branch_from = h->br_from.data();
+    d->branch_to = h->br_to.data();
+    d->branch_x = h->br_x.data();
+    d->branch_limit = h->br_lim.data();
+    d->branch_in_service = h->br_on.data();
+    d->injection_node = h->inj_node.data();
+    d->injection_net_mw = h->inj_net.data();
+    d->n_contingencies = static_cast<int32_t>(g.cont_id.size());
+    d->cont_branch_ptr = h->cont_bptr.data();
+    d->cont_branch = h->cont_b.data();
+    d->cont_inj_ptr = h->cont_iptr.data();
+    d->cont_inj = h->cont_i.data();
+    d->n_substations = static_cast<int32_t>(g.stations.size());
+    d->sub_node = h->sub_node.data();
+    d->sub_term_ptr = h->sub_tptr.data();
+    d->term_kind = h->tkind.data();
+    d->term_element = h->telem.data();
+    d->n_busbar_outages = static_cast<int32_t>(g.bo_id.size());
+    d->bo_substation = h->bo_sub.data();
+    d->bo_busbar = h->bo_bb.data();
+    d->bo_implied_ptr = h->bo_iptr.data();
+    d->bo_implied = h->bo_i.data();
+  });
+}
+
+tg_status tg_actionset_build(const tg_grid* grid, uint64_t seed, int64_t cap, tg_actionset** out) {
+  return guarded([&] {
+    auto a = std::make_unique<tg_actionset>();
+    a->t = tgb::build_actions(grid->g, seed, cap > 0 ? cap : (int64_t{1} << 23));
+    flatten_actions(*a, grid->g);
+    *out = a.release();
+  });
+}
+
+tg_status tg_actionset_from_json(const tg_grid* grid, const char* text, size_t len, tg_actionset** out) {
+  return guarded([&] {
+    auto a = std::make_unique<tg_actionset>();
+    if (!tgb::actions_from_json(std::string(text, len), grid->g, tgb::grid_fingerprint(grid->g), a->t))
+      throw tgb::IoError("action cache does not match this grid");
+    flatten_actions(*a, grid->g);
+    *out = a.release();
+  });
+}
+
+tg_status tg_actionset_to_json(const tg_actionset* set, const tg_grid* grid, char** text_out) {
+  return guarded([&] {
+    std::string s = tgb::actions_to_json(set->t, grid->g, tgb::grid_fingerprint(grid->g));
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.c_str(), s.size() + 1);
+    *text_out = p;
+  });
+}
+
+void tg_actionset_destroy(tg_actionset* set) { delete set; }
+
+tg_status tg_actionset_describe(const tg_actionset* a, const tg_grid*, tg_actionset_desc* d) {
+  return guarded([&] {
+    d->n_actions = a->t.n_actions();
+    d->action_substation = a->station.data();
+    d->action_lambda_r = a->lambda_r.data();
+    d->action_group_ptr = a->gptr.data();
+    d->action_group = a->group.data();
+    d->action_busbar_ptr = a->bbptr.data();
+    d->action_implied_ptr = a->iptr.data();
+    d->action_implied = a->imp.data();
+    d->n_disconnectables = static_cast<int32_t>(a->disc.size());
+    d->disconnectables = a->disc.data();
+  });
+}
+
+tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad, const tg_dc_config* cfg, int device,
+                            tg_context** out) {
+  return guarded([&] {
+    auto ctx = std::make_unique<tg_context>();
+    ctx->device = device;
+    check(cudaSetDevice(device), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    cudaStream_t s = ctx->stream;
+    DeviceArena& A = ctx->arena;
+    tgb::DevGrid& g = ctx->g;
+    const int N = gd->n_nodes, E = gd->n_branches, I = gd->n_injections;
+    if (N < 2) throw tgb::ValidationError("grid needs at least two nodes");
+    g.N = N;
+    g.Nr = N - 1;
+    g.E = E;
+    g.I = I;
+    g.slack = gd->slack;
+    std::vector<int> red(N, -1);
+    for (int v = 0, r = 0; v < N; ++v)
+      if (v != gd->slack) red[v] = r++;
+    std::vector<double> b(E);
+    for (int e = 0; e < E; ++e) b[e] = 1.0 / gd->branch_x[e];
+    // node incidence (in-service) and node injections
+    std::vector<int> nptr(N + 1, 0), nbr, iptr(N + 1, 0), ninj;
+    for (int e = 0; e < E; ++e)
+      if (gd->branch_in_service[e]) ++nptr[gd->branch_from[e] + 1], ++nptr[gd->branch_to[e] + 1];
+    for (int v = 0; v < N; ++v) nptr[v + 1] += nptr[v];
+    nbr.resize(nptr[N]);
+    {
+      std::vector<int> fill(nptr.begin(), nptr.end() - 1);
+      for (int e = 0; e < E; ++e)
+        if (gd->branch_in_service[e]) nbr[fill[gd->branch_from[e]]++] = e, nbr[fill[gd->branch_to[e]]++] = e;
+    }
+    for (int i = 0; i < I; ++i) ++iptr[gd->injection_node[i] + 1];
+    for (int v = 0; v < N; ++v) iptr[v + 1] += iptr[v];
+    ninj.resize(iptr[N]);
+    {
+      std::vector<int> fill(iptr.begin(), iptr.end() - 1);
+      for (int i = 0; i < I; ++i) ninj[fill[gd->injection_node[i]]++] = i;
+    }
+    // contingencies: single-branch (fused sweep) vs special (outage rebuild)
+    std::vector<int> ks_cont, ks_br, kx_cont, kx_bptr{0}, kx_b, kx_iptr{0}, kx_i;
+    for (int c = 0; c < gd->n_contingencies; ++c) {
+      const int b0 = gd->cont_branch_ptr[c], b1 = gd->cont_branch_ptr[c + 1];
+      const int i0 = gd->cont_inj_ptr[c], i1 = gd->cont_inj_ptr[c + 1];
+      if (b1 - b0 == 1 && i1 == i0) {
+        ks_cont.push_back(c);
+        ks_br.push_back(gd->cont_branch[b0]);
+      } else {
+        kx_cont.push_back(c);
+        for (int p = b0; p < b1; ++p) kx_b.push_back(gd->cont_branch[p]);
+        for (int p = i0; p < i1; ++p) kx_i.push_back(gd->cont_inj[p]);
+        kx_bptr.push_back(static_cast<int>(kx_b.size()));
+        kx_iptr.push_back(static_cast<int>(kx_i.size()));
+      }
+    }
+    const int tile = tgb::sweep_tile_k();
+    g.Ks = static_cast<int>(ks_cont.size());
+    g.Kpad = ((g.Ks + tile - 1) / tile) * tile;
+    g.Kx = static_cast<int>(kx_cont.size());
+    g.Kall = gd->n_contingencies;
+    g.Kb = gd->n_busbar_outages;
+    g.S = gd->n_substations;
+    g.A = ad ? ad->n_actions : 0;
+    g.D = ad ? ad->n_disconnectables : 0;
+    // station action ranges (actions of one station are contiguous)
+    std::vector<int> lo(g.S, -1), hi(g.S, -1);
+    for (int a = 0; a < g.A; ++a) {
+      const int st = ad->action_substation[a];
+      if (lo[st] < 0) lo[st] = a;
+      else if (hi[st] != a) throw tgb::ValidationError("actions of a substation must be contiguous");
+      hi[st] = a + 1;
+    }
+    auto v32 = [](const int32_t* p, size_t n) { return std::vector<int>(p, p + n); };
+    g.red = A.upload(red, s);
+    g.br_from = A.upload(v32(gd->branch_from, E), s);
+    g.br_to = A.upload(v32(gd->branch_to, E), s);
+    g.br_b = A.upload(b, s);
+    g.br_lim = A.upload(std::vector<double>(gd->branch_limit, gd->branch_limit + E), s);
+    g.br_on = A.upload(std::vector<uint8_t>(gd->branch_in_service, gd->branch_in_service + E), s);
+    g.node_ptr = A.upload(nptr, s);
+    g.node_br = A.upload(nbr, s);
+    g.node_inj_ptr = A.upload(iptr, s);
+    g.node_inj = A.upload(ninj, s);
+    g.inj_node = A.upload(v32(gd->injection_node, I), s);
+    g.inj_net = A.upload(std::vector<double>(gd->injection_net_mw, gd->injection_net_mw + I), s);
+    g.ks_cont = A.upload(ks_cont, s);
+    g.ks_branch = A.upload(ks_br, s);
+    g.kx_cont = A.upload(kx_cont, s);
+    g.kx_br_ptr = A.upload(kx_bptr, s);
+    g.kx_br = A.upload(kx_b, s);
+    g.kx_inj_ptr = A.upload(kx_iptr, s);
+    g.kx_inj = A.upload(kx_i, s);
+    g.bo_station = A.upload(v32(gd->bo_substation, g.Kb), s);
+    g.bo_busbar = A.upload(v32(gd->bo_busbar, g.Kb), s);
+    g.bo_def_ptr = A.upload(v32(gd->bo_implied_ptr, g.Kb + 1), s);
+    g.bo_def = A.upload(v32(gd->bo_implied, gd->bo_implied_ptr[g.Kb]), s);
+    g.st_node = A.upload(v32(gd->sub_node, g.S), s);
+    g.st_range_lo = A.upload(lo, s);
+    g.st_range_hi = A.upload(hi, s);
+    g.st_term_ptr = A.upload(v32(gd->sub_term_ptr, g.S + 1), s);
+    g.term_kind = A.upload(v32(gd->term_kind, gd->sub_term_ptr[g.S]), s);
+    g.term_elem = A.upload(v32(gd->term_element, gd->sub_term_ptr[g.S]), s);
+    if (g.A > 0) {
+      g.act_station = A.upload(v32(ad->action_substation, g.A), s);
+      g.act_lambda_r = A.upload(v32(ad->action_lambda_r, g.A), s);
+      g.act_group_ptr = A.upload(v32(ad->action_group_ptr, g.A + 1), s);
+      g.act_group = A.upload(std::vector<uint8_t>(ad->action_group, ad->action_group + ad->action_group_ptr[g.A]), s);
+      g.act_bb_ptr = A.upload(v32(ad->action_busbar_ptr, g.A + 1), s);
+      const int nslots = ad->action_busbar_ptr[g.A];
+      g.act_imp_ptr = A.upload(v32(ad->action_implied_ptr, nslots + 1), s);
+      g.act_imp = A.upload(v32(ad->action_implied, ad->action_implied_ptr[nslots]), s);
+    } else {
+      g.act_station = A.alloc<int>(1);
+      g.act_lambda_r = A.alloc<int>(1);
+      g.act_group_ptr = A.alloc<int>(1);
+      g.act_group = A.alloc<uint8_t>(1);
+      g.act_bb_ptr = A.alloc<int>(1);
+      g.act_imp_ptr = A.alloc<int>(1);
+      g.act_imp = A.alloc<int>(1);
+    }
+    g.disc = g.D > 0 ? A.upload(v32(ad->disconnectables, g.D), s) : A.alloc<int>(1);
+
+    // base factorization: B_red assembled on the host, inverted on the device
+    const int Nr = g.Nr;
+    std::vector<double> bred(static_cast<size_t>(Nr) * Nr, 0.0);
+    for (int e = 0; e < E; ++e) {
+      if (!gd->branch_in_service[e]) continue;
+      const int i = red[gd->branch_from[e]], j = red[gd->branch_to[e]];
+      if (i >= 0) bred[static_cast<size_t>(i) * Nr + i] += b[e];
+      if (j >= 0) bred[static_cast<size_t>(j) * Nr + j] += b[e];
+      if (i >= 0 && j >= 0) bred[static_cast<size_t>(i) * Nr + j] -= b[e], bred[static_cast<size_t>(j) * Nr + i] -= b[e];
+    }
+    double* X = A.upload(bred, s);
+    if (!tgb::device_spd_inverse(X, Nr, s))
+      throw tgb::SingularSystem("susceptance matrix is singular; the grid is disconnected");
+    g.X = X;
+    std::vector<double> p(N, 0.0);
+    for (int i = 0; i < I; ++i) p[gd->injection_node[i]] += gd->injection_net_mw[i];
+    double tot = 0.0;
+    for (double v : p) tot += v;
+    p[gd->slack] -= tot;
+    std::vector<double> pr(Nr);
+    for (int v = 0; v < N; ++v)
+      if (red[v] >= 0) pr[red[v]] = p[v];
+    double* d_pr = A.upload(pr, s);
+    double* theta0 = A.alloc<double>(Nr);
+    double* f0 = A.alloc<double>(E);
+    double* tdiag = A.alloc<double>(E);
+    double* tk = A.alloc<double>(static_cast<size_t>(E) * std::max(g.Kpad, 1));
+    g.theta0 = theta0;
+    g.f0 = f0;
+    g.Tdiag = tdiag;
+    g.TK = tk;
+    tgb::launch_base_tables(g, d_pr, theta0, f0, tdiag, tk, s);
+    check(cudaGetLastError(), "base tables");
+    check(cudaStreamSynchronize(s), "context setup");
+
+    ctx->n_cont = gd->n_contingencies;
+    ctx->worst_k = cfg ? cfg->worst_k : 20;
+    ctx->params.penalty = cfg ? cfg->islanding_penalty_mw : 10000.0;
+    ctx->params.weight_c0 = cfg ? cfg->weight_c0 : 200.0;
+    ctx->params.weight_c = cfg ? cfg->weight_c : 50.0;
+    ctx->params.variant = cfg ? cfg->fitness_variant : 1;
+    ctx->params.worst_k = ctx->worst_k;
+    ctx->params.lambda_b_pre = 0.0;
+    if (ctx->params.variant != 1 && ctx->params.variant != 2)
+      throw tgb::ConfigError("fitness_variant must be 1 or 2");
+
+    // pre-optimization score of the unchanged topology (dc_engine.cpp:137-144)
+    ctx->ensure_capacity(1);
+    std::vector<int> empty(1, -1);
+    check(cudaMemcpyAsync(ctx->d_genomes, empty.data(), sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
+    ctx->params.n_a = 1;
+    ctx->params.n_d = 0;
+    ctx->run_batch(1, 1, 0, false);
+    check_errors(ctx.get(), 1);
+    double lo_ = 0, lb_ = 0, fit = 0;
+    int lc = 0, lc0 = 0;
+    const tgb::Scores& o = ctx->batch.out;
+    check(cudaMemcpy(&lo_, o.lambda_o, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    check(cudaMemcpy(&lb_, o.lambda_b, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    check(cudaMemcpy(&fit, o.fitness, sizeof(double), cudaMemcpyDeviceToHost), "D2H");
+    check(cudaMemcpy(&lc, o.lambda_c, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+    check(cudaMemcpy(&lc0, o.lambda_c0, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+    ctx->lambda_b_pre = lb_;
+    ctx->params.lambda_b_pre = lb_;
+    // with variant 2 the pre-score subtracts clip(lambda_b - lambda_b_pre) = 0
+    ctx->pre = {lo_, static_cast<double>(lc), static_cast<double>(lc0), lb_, fit};
+    *out = ctx.release();
+  });
+}
+
+void tg_context_destroy(tg_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  cudaStreamSynchronize(ctx->stream);
+  ctx->qd.reset();
+  ctx->batch_arena.reset();
+  cudaStream_t s = ctx->stream;
+  delete ctx;
+  cudaStreamDestroy(s);
+}
+
+tg_status tg_evaluate_batch(tg_context* ctx, const int32_t* genomes, int32_t n, int32_t n_a, int32_t n_d,
+                            int32_t batch_size, tg_scores* out, double* base_flows, double* max_contingency,
+                            double* max_busbar, double* outage_energy) {
+  return guarded([&] {
+    if (n < 0 || n_a < 0 || n_d < 0 || n_a > tgb::kMaxSplits || n_d > tgb::kMaxRemovedSweep)
+      throw tgb::ConfigError("genome slots exceed the engine capacity (n_a <= 4, n_d <= 4)");
+    if (n == 0) return;
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    for (int64_t i = 0; i < static_cast<int64_t>(n) * (n_a + n_d); ++i) {
+      const int v = genomes[i];
+      const int slot = static_cast<int>(i % (n_a + n_d));
+      if (v < -1 || (slot < n_a && v >= ctx->g.A) || (slot >= n_a && v >= ctx->g.D))
+        throw tgb::ValidationError("genome slot value out of range");
+    }
+    (void)batch_size;  // padding lanes are empty genomes whose scores are dropped
+    ctx->ensure_capacity(n);
+    check(cudaMemcpyAsync(ctx->d_genomes, genomes, static_cast<size_t>(n) * (n_a + n_d) * sizeof(int),
+                          cudaMemcpyHostToDevice, ctx->stream),
+          "genomes H2D");
+    const bool full = base_flows || max_contingency || max_busbar || outage_energy;
+    ctx->run_batch(n, n_a, n_d, full);
+    copy_scores(ctx, n, out);
+    const size_t ne = static_cast<size_t>(n) * ctx->g.E;
+    if (base_flows || max_contingency || max_busbar) {
+      tgb::DeviceScratchGuard tmp(ne);
+      if (base_flows) {
+        tgb::launch_extract(ctx->g, ctx->batch, tmp.ptr, nullptr, nullptr, ctx->stream);
+        check(cudaMemcpyAsync(base_flows, tmp.ptr, ne * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        check(cudaStreamSynchronize(ctx->stream), "sync");
+      }
+      if (max_contingency) {
+        tgb::launch_extract(ctx->g, ctx->batch, nullptr, tmp.ptr, nullptr, ctx->stream);
+        check(cudaMemcpyAsync(max_contingency, tmp.ptr, ne * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        check(cudaStreamSynchronize(ctx->stream), "sync");
+      }
+      if (max_busbar) {
+        tgb::launch_extract(ctx->g, ctx->batch, nullptr, nullptr, tmp.ptr, ctx->stream);
+        check(cudaMemcpyAsync(max_busbar, tmp.ptr, ne * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        check(cudaStreamSynchronize(ctx->stream), "sync");
+      }
+    }
+    if (outage_energy && ctx->g.Kall > 0)
+      check(cudaMemcpyAsync(outage_energy, ctx->batch.energy, static_cast<size_t>(n) * ctx->g.Kall * sizeof(double),
+                            cudaMemcpyDeviceToHost, ctx->stream),
+            "energy D2H");
+    check_errors(ctx, n);
+    // islanded genomes report zero flows / energies (FlowResult is not built, dc_engine.cpp:426-435)
+    if (outage_energy && ctx->g.Kall > 0) {
+      std::vector<uint8_t> isl(n);
+      check(cudaMemcpy(isl.data(), ctx->batch.out.islanded, n, cudaMemcpyDeviceToHost), "D2H");
+      for (int i = 0; i < n; ++i)
+        if (isl[i]) std::fill(outage_energy + static_cast<size_t>(i) * ctx->g.Kall,
+                              outage_energy + static_cast<size_t>(i + 1) * ctx->g.Kall, 0.0);
+    }
+    check(cudaStreamSynchronize(ctx->stream), "evaluate");
+  });
+}
+
+tg_status tg_evaluate_batch_device(tg_context* ctx, const int32_t* d_genomes, int32_t n, int32_t n_a, int32_t n_d,
+                                   tg_scores* d_out) {
+  return guarded([&] {
+    if (n_a > tgb::kMaxSplits || n_d > tgb::kMaxRemovedSweep)
+      throw tgb::ConfigError("genome slots exceed the engine capacity (n_a <= 4, n_d <= 4)");
+    if (n <= 0) return;
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ctx->ensure_capacity(n);
+    check(cudaMemcpyAsync(ctx->d_genomes, d_genomes, static_cast<size_t>(n) * (n_a + n_d) * sizeof(int),
+                          cudaMemcpyDeviceToDevice, ctx->stream),
+          "genomes D2D");
+    ctx->run_batch(n, n_a, n_d, false);
+    if (d_out) {
+      const tgb::Scores& o = ctx->batch.out;
+      auto cp = [&](void* dst, const void* src, size_t bytes) {
+        if (dst) check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToDevice, ctx->stream), "scores D2D");
+      };
+      cp(d_out->fitness, o.fitness, n * sizeof(double));
+      cp(d_out->lambda_o, o.lambda_o, n * sizeof(double));
+      cp(d_out->lambda_c, o.lambda_c, n * sizeof(int));
+      cp(d_out->lambda_c0, o.lambda_c0, n * sizeof(int));
+      cp(d_out->islanded, o.islanded, n * sizeof(uint8_t));
+    }
+  });
+}
+
+tg_status tg_pre_score(tg_context* ctx, tg_scores* out, double* lambda_b_pre) {
+  return guarded([&] {
+    if (lambda_b_pre) *lambda_b_pre = ctx->lambda_b_pre;
+    if (!out) return;
+    if (out->lambda_o) out->lambda_o[0] = ctx->pre[0];
+    if (out->lambda_c) out->lambda_c[0] = static_cast<int32_t>(ctx->pre[1]);
+    if (out->lambda_c0) out->lambda_c0[0] = static_cast<int32_t>(ctx->pre[2]);
+    if (out->lambda_b) out->lambda_b[0] = ctx->pre[3];
+    if (out->fitness) out->fitness[0] = ctx->pre[4];
+    if (out->lambda_d) out->lambda_d[0] = 0;
+    if (out->lambda_s) out->lambda_s[0] = 0;
+    if (out->lambda_r) out->lambda_r[0] = 0;
+    if (out->islanded) out->islanded[0] = 0;
+  });
+}
+
+int32_t tg_descriptor_to_cell(int32_t d, int32_t s, int32_t r, const tg_qd_config* c) {
+  d = std::min(d, c->d_max);
+  s = std::min(s, c->s_max);
+  r = std::min(r, c->r_max);
+  return d + (c->d_max + 1) * (s + (c->s_max + 1) * r);
+}
+
+tg_status tg_context_info(tg_context* ctx, int64_t* v, int32_t n) {
+  return guarded([&] {
+    const int64_t vals[] = {ctx->g.N, ctx->g.E, ctx->g.Kall, ctx->g.Ks, ctx->g.Kx, ctx->g.Kb,
+                            ctx->g.A, ctx->g.D, ctx->g.Kpad, static_cast<int64_t>(ctx->arena.bytes())};
+    for (int i = 0; i < n && i < static_cast<int>(sizeof(vals) / sizeof(vals[0])); ++i) v[i] = vals[i];
+  });
+}
+
+int64_t tg_kernel_launches(tg_context* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"
+
+extern "C" {
+tg_status tg_optimizer_run(tg_context*, const tg_qd_config*, tg_snapshot_cb, void*, const volatile int32_t*,
+                           tg_opt_stats*, int64_t*, double*, int32_t) {
+  g_error = "optimizer loop not built yet";
+  return TG_CONFIG_ERROR;
+}
+tg_status tg_archive_export(tg_context*, tg_snapshot_view*) {
+  g_error = "optimizer loop not built yet";
+  return TG_CONFIG_ERROR;
+}
+tg_status tg_archive_replay(tg_context*, const tg_qd_config*, const int32_t*, int32_t, const tg_scores*, uint8_t*) {
+  g_error = "optimizer loop not built yet";
+  return TG_CONFIG_ERROR;
+}
+tg_status tg_mutate_lanes(tg_context*, const tg_qd_config*, const int32_t*, const uint64_t*, int32_t, int32_t*) {
+  g_error = "optimizer loop not built yet";
+  return TG_CONFIG_ERROR;
+}
+tg_status tg_crossover_lanes(tg_context*, const tg_qd_config*, const int32_t*, const int32_t*, const uint64_t*, int32_t,
+                             int32_t*) {
+  g_error = "optimizer loop not built yet";
+  return TG_CONFIG_ERROR;
+}
+}

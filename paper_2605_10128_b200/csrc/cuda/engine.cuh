@@ -1,0 +1,88 @@
+// Batch buffers and launchers of the DC N-1 engine.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <math_constants.h>
+
+#include "common.cuh"
+
+namespace tgb {
+
+constexpr int kMaxRemovedSweep = 4;  // genome disconnections skipped in the sweep (n_d <= 4)
+
+// Per-candidate scores, SoA (dc_engine.hpp:25-39).
+struct Scores {
+  double* lambda_o;
+  int* lambda_c;
+  int* lambda_c0;
+  double* lambda_b;
+  int* lambda_d;
+  int* lambda_s;
+  int* lambda_r;
+  double* fitness;
+  uint8_t* islanded;
+  int* error;       // nonzero: capacity exceeded (host raises)
+  int* worst_idx;   // [n][worst_k]
+  double* worst_val;
+  int* worst_n;
+  int* isl_out;     // islanded contingencies
+  int* isl_bus;     // islanded busbar outages
+};
+
+// Device buffers of one evaluation batch (capacity fixed at allocation).
+struct Batch {
+  int n;                      // candidates in this launch
+  const int* genomes;         // [n][n_a+n_d]
+  DcParams params;
+  int* status;                // 0 ok, 1 islanded, 2/3 capacity error
+  int* rank;                  // low-rank update size, -1 when not swept
+  int* removed;               // [n][kMaxRemovedSweep] genome-removed branches
+  double* feat;               // [n][E][kStride]  f_c, L
+  double* kdat;               // [n][Kpad][kStride] alpha, R' (single-branch contingencies)
+  uint8_t* kflag;             // [n][Kpad] 0 ok, 1 islanded, 2 padding
+  unsigned long long* fmax;   // [n][E] max |f| over contingencies (bits of a non-negative double)
+  unsigned long long* fbus;   // [n][E] max |f| over busbar outages
+  double* energy;             // [n][Kall] outage energy per contingency
+  int* isl_out;               // [n] islanded special contingencies
+  int* isl_bus;               // [n]
+  int* wl_list;               // [n] candidates bucketed by rank
+  int* wl_start;              // [kSweepRank+1]
+  int* wl_count;              // [kSweepRank+1]
+  int* wl_group0;             // [kSweepRank+2]
+  Scores out;
+};
+
+struct EvalScratch {
+  double* zprep;       // [zslots][Nr][kStride]
+  int zslots;
+  double* zspecial;    // [zslots_special][Nr][kMaxCols]
+  int zslots_special;
+};
+
+void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
+                     cudaStream_t stream, int* kernels);
+void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_out, double* fbus_out,
+                    cudaStream_t stream);
+int sweep_tile_k();
+
+// Base factorization on the device (dc_engine.cpp:88-116, importer.cpp:358-401):
+// X = B_red^-1 by in-place Gauss-Jordan (B_red is SPD; no pivoting needed).
+// Returns false when a pivot is not positive (disconnected grid).
+bool device_spd_inverse(double* a, int n, cudaStream_t stream);
+void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
+                        cudaStream_t stream);
+
+}  // namespace tgb
+
+namespace tgb {
+
+// RAII device scratch for one-off host-requested outputs.
+struct DeviceScratchGuard {
+  double* ptr = nullptr;
+  explicit DeviceScratchGuard(size_t n) { cudaMalloc(&ptr, (n ? n : 1) * sizeof(double)); }
+  ~DeviceScratchGuard() { cudaFree(ptr); }
+  DeviceScratchGuard(const DeviceScratchGuard&) = delete;
+  DeviceScratchGuard& operator=(const DeviceScratchGuard&) = delete;
+};
+
+}  // namespace tgb

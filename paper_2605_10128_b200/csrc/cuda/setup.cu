@@ -1,0 +1,150 @@
+// Base factorization and base-case tables on the device.
+// Replaces the DcContext constructor's dense inverse and base solve
+// (dc_engine.cpp:88-116) and build_ptdf's gather (importer.cpp:358-401).
+#include "engine.cuh"
+
+namespace tgb {
+
+namespace {
+
+__global__ void k_gj_pivot(const double* a, int n, int k, double* row, double* col, double tol, int* bad) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) {
+    col[i] = a[static_cast<size_t>(k) * n + i];
+    row[i] = a[static_cast<size_t>(i) * n + k];
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) {
+    const double p = a[static_cast<size_t>(k) * n + k];
+    if (!(p > tol)) *bad = 1;
+  }
+}
+
+// One Gauss-Jordan elimination step on the column-major matrix.
+__global__ void k_gj_update(double* a, int n, int k, const double* row, const double* col) {
+  const double p = row[k];
+  const double ip = 1.0 / p;
+  const size_t total = static_cast<size_t>(n) * n;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(idx / n), i = static_cast<int>(idx % n);
+    double v;
+    if (i == k && j == k)
+      v = ip;
+    else if (i == k)
+      v = row[j] * ip;
+    else if (j == k)
+      v = -col[i] * ip;
+    else
+      v = fma(-col[i] * ip, row[j], a[idx]);
+    a[idx] = v;
+  }
+}
+
+__global__ void k_max_diag(const double* a, int n, double* out) {
+  __shared__ double s[256];
+  double m = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) m = fmax(m, fabs(a[static_cast<size_t>(i) * n + i]));
+  s[threadIdx.x] = m;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) s[threadIdx.x] = fmax(s[threadIdx.x], s[threadIdx.x + w]);
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) *out = s[0];
+}
+
+__global__ void k_symmetrize(double* a, int n) {
+  const size_t total = static_cast<size_t>(n) * n;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int j = static_cast<int>(idx / n), i = static_cast<int>(idx % n);
+    if (i < j) {
+      const double v = 0.5 * (a[idx] + a[static_cast<size_t>(i) * n + j]);
+      a[idx] = v;
+      a[static_cast<size_t>(i) * n + j] = v;
+    }
+  }
+}
+
+__device__ __forceinline__ double xat(const DevGrid& g, int r, int c) {
+  return (r < 0 || c < 0) ? 0.0 : g.X[static_cast<size_t>(c) * g.Nr + r];
+}
+
+__global__ void k_theta(DevGrid g, const double* p_red, double* theta) {
+  for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < g.Nr; i += gridDim.x * blockDim.x) {
+    double acc = 0.0;
+    for (int j = 0; j < g.Nr; ++j) acc = fma(g.X[static_cast<size_t>(j) * g.Nr + i], p_red[j], acc);
+    theta[i] = acc;
+  }
+}
+
+__global__ void k_branch_base(DevGrid g, const double* theta, double* f0, double* tdiag) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < g.E; e += gridDim.x * blockDim.x) {
+    const int ri = g.red[g.br_from[e]], rj = g.red[g.br_to[e]];
+    const double b = g.br_b[e];
+    const double ti = ri >= 0 ? theta[ri] : 0.0, tj = rj >= 0 ? theta[rj] : 0.0;
+    f0[e] = g.br_on[e] ? b * (ti - tj) : 0.0;
+    tdiag[e] = b * (xat(g, ri, ri) - 2.0 * xat(g, ri, rj) + xat(g, rj, rj));
+  }
+}
+
+// T_base[e, k] = b_e a_e^T X a_beta(k), e-major rows of Kpad contingencies.
+__global__ void k_tk(DevGrid g, double* tk) {
+  const size_t total = static_cast<size_t>(g.E) * g.Kpad;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int e = static_cast<int>(idx / g.Kpad), k = static_cast<int>(idx % g.Kpad);
+    double v = 0.0;
+    if (k < g.Ks && g.br_on[e]) {
+      const int beta = g.ks_branch[k];
+      const int fk = g.red[g.br_from[beta]], tk2 = g.red[g.br_to[beta]];
+      const int ri = g.red[g.br_from[e]], rj = g.red[g.br_to[e]];
+      v = g.br_b[e] * ((xat(g, ri, fk) - xat(g, ri, tk2)) - (xat(g, rj, fk) - xat(g, rj, tk2)));
+    }
+    tk[idx] = v;
+  }
+}
+
+}  // namespace
+
+bool device_spd_inverse(double* a, int n, cudaStream_t stream) {
+  if (n == 0) return true;
+  double *row = nullptr, *col = nullptr, *dmax = nullptr;
+  int* bad = nullptr;
+  cudaMalloc(&row, n * sizeof(double));
+  cudaMalloc(&col, n * sizeof(double));
+  cudaMalloc(&dmax, sizeof(double));
+  cudaMalloc(&bad, sizeof(int));
+  cudaMemsetAsync(bad, 0, sizeof(int), stream);
+  k_max_diag<<<1, 256, 0, stream>>>(a, n, dmax);
+  double hmax = 0.0;
+  cudaMemcpyAsync(&hmax, dmax, sizeof(double), cudaMemcpyDeviceToHost, stream);
+  cudaStreamSynchronize(stream);
+  const double tol = 1e-13 * hmax;
+  const size_t total = static_cast<size_t>(n) * n;
+  const int upd_blocks = static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16));
+  for (int k = 0; k < n; ++k) {
+    k_gj_pivot<<<(n + 255) / 256, 256, 0, stream>>>(a, n, k, row, col, tol, bad);
+    k_gj_update<<<upd_blocks, 256, 0, stream>>>(a, n, k, row, col);
+  }
+  k_symmetrize<<<upd_blocks, 256, 0, stream>>>(a, n);
+  int hbad = 0;
+  cudaMemcpyAsync(&hbad, bad, sizeof(int), cudaMemcpyDeviceToHost, stream);
+  cudaStreamSynchronize(stream);
+  cudaFree(row);
+  cudaFree(col);
+  cudaFree(dmax);
+  cudaFree(bad);
+  return hbad == 0;
+}
+
+void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
+                        cudaStream_t stream) {
+  k_theta<<<(g.Nr + 255) / 256 + 1, 256, 0, stream>>>(g, p_red, theta0);
+  DevGrid g2 = g;
+  g2.theta0 = theta0;
+  k_branch_base<<<(g.E + 255) / 256 + 1, 256, 0, stream>>>(g2, theta0, f0, tdiag);
+  const size_t total = static_cast<size_t>(g.E) * g.Kpad;
+  if (total > 0) k_tk<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32)), 256, 0, stream>>>(g2, tk);
+}
+
+}  // namespace tgb

@@ -1,0 +1,100 @@
+"""Shared parity helpers: run the same genomes through the B200 engine (C ABI)
+and the CPU oracle, and compare with the tolerances stated in BASELINE.md §3
+(FP64: 1e-9 relative with scale max(1, |x|); counts and encodings exact)."""
+from __future__ import annotations
+
+import json
+
+import numpy as np
+
+from oracle.oracle import OracleContext
+
+TOL = 1e-9
+
+
+def rel_err(got, want) -> float:
+    got = np.asarray(got, float)
+    want = np.asarray(want, float)
+    if got.size == 0:
+        return 0.0
+    fin = np.isfinite(want)
+    assert np.array_equal(np.isfinite(got), fin)
+    if not fin.any():
+        return 0.0
+    return float(np.max(np.abs(got[fin] - want[fin]) / np.maximum(1.0, np.abs(want[fin]))))
+
+
+def make_pair(grid_json: str, **dc):
+    """(product DcContext, oracle context) for one grid; asserts equal action ids."""
+    import paper_2605_10128_b200 as P
+
+    g = P.grid_from_json_text(grid_json)
+    a = P.build_action_set(g)
+    cfg = P.DcConfig(**{k: v for k, v in dc.items() if k in P.DcConfig.__dataclass_fields__})
+    ctx = P.DcContext(g, a, cfg)
+    orc = OracleContext(grid_json, penalty=cfg.islanding_penalty_mw, worst_k=cfg.worst_k, weight_c0=cfg.weight_c0,
+                        weight_c=cfg.weight_c, variant=cfg.fitness_variant)
+    assert a.n_actions == orc.info["n_actions"]
+    assert a.disconnectables.tolist() == orc.info["disconnectables"]
+    for i, act in enumerate(orc.info["actions"]):
+        assert a.substation[i] == act["substation"] and a.groups[i] == act["group"]
+        assert a.lambda_r[i] == act["lambda_r"]
+    return ctx, orc
+
+
+def compare_scores(sc, ref: dict, worst_k: int) -> dict:
+    """Asserts parity of a ScoreArrays batch against oracle output; returns error stats."""
+    n = len(sc.fitness)
+    assert np.array_equal(sc.islanded, ref["islanded"]), "islanded flags differ"
+    for k in ("lambda_d", "lambda_s", "lambda_r"):
+        assert np.array_equal(getattr(sc, k), ref[k]), k
+    live = ref["islanded"] == 0
+    assert np.array_equal(sc.lambda_c[live], ref["lambda_c"][live]), "lambda_c"
+    assert np.array_equal(sc.lambda_c0[live], ref["lambda_c0"][live]), "lambda_c0"
+    assert np.array_equal(sc.islanded_outages[live], ref["islanded_outages"][live]), "islanded outages"
+    assert np.array_equal(sc.islanded_busbar_outages[live], ref["islanded_busbar"][live]), "islanded busbar"
+    errs = {k: rel_err(getattr(sc, k), ref[k]) for k in ("lambda_o", "lambda_b", "fitness")}
+    for k, v in errs.items():
+        assert v <= TOL, f"{k} rel err {v:.3e}"
+    werr = 0.0
+    for i in range(n):
+        if not live[i]:
+            continue
+        wn = int(ref["worst_n"][i])
+        assert int(sc.worst_n[i]) == wn, f"worst_n lane {i}"
+        gi, ri = sc.worst_idx[i, :wn], ref["worst_idx"][i, :wn]
+        gv, rv = sc.worst_energy[i, :wn], ref["worst_val"][i, :wn]
+        if not np.array_equal(gi, ri):
+            # tolerate order swaps only between energies equal within tolerance
+            assert sorted(gi.tolist()) == sorted(ri.tolist()) or rel_err(np.sort(gv), np.sort(rv)) <= TOL, \
+                f"worst list lane {i}: {gi} vs {ri}"
+        werr = max(werr, rel_err(np.sort(gv), np.sort(rv)))
+    assert werr <= TOL, f"worst energies rel err {werr:.3e}"
+    errs["worst"] = werr
+    return errs
+
+
+def compare_flows(fr, ref: dict) -> dict:
+    live = ref["islanded"] == 0
+    out = {}
+    for mine, theirs in (("base", "base"), ("max_contingency", "fmax"), ("max_busbar", "fbus"),
+                         ("outage_energy", "energy")):
+        e = rel_err(getattr(fr, mine)[live], ref[theirs][live])
+        assert e <= TOL, f"{mine} rel err {e:.3e}"
+        out[mine] = e
+    return out
+
+
+def grid_with_stations(base_json: str, buses) -> str:
+    """Graft 2-busbar stations (helpers.hpp:65-78 station_json) onto buses."""
+    doc = json.loads(base_json)
+    ids = {b["id"]: b for b in doc["branches"]}
+    doc.setdefault("substations", [])
+    for bus in buses:
+        el = [b["id"] for b in doc["branches"] if b["from"] == bus or b["to"] == bus]
+        el += [i["id"] for i in doc.get("injections", []) if i["node"] == bus]
+        doc["substations"].append({"node": bus, "busbars": ["B1", "B2"], "couplers": [["B1", "B2"]],
+                                   "terminals": [{"element": e, "reachable": ["B1", "B2"], "default": "B1"}
+                                                 for e in el]})
+    del ids
+    return json.dumps(doc)
