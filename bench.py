@@ -1,0 +1,333 @@
+"""Benchmark: N-1-evaluated topologies/s of the device-resident MapElites loop.
+
+Workload (BASELINE.json configs[1]): synthetic 1k-bus / 1.5k-branch grid, a
+4096-candidate batch per generation, full single-branch N-1 over every
+listed contingency, 1 timestep. One step = one MapElites generation: device
+mutation/crossover of 4096 lanes, DC N-1 evaluation of every lane, archive
+insert (qd_optimizer.cpp:376-401), launched as one CUDA graph.
+
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg4|cfg1] [--impl b200|reference]
+
+Multi-GPU (torchrun): one island per rank (own seed, own archive), weak
+scaling, device time = max over ranks. --impl reference times the reference's
+CPU algorithm (the oracle restatement, oracle/, threaded like
+dc_engine.cpp:446-465) on this host on the same workload.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+L2_BYTES = 126 * 2 ** 20
+
+CONFIGS = {
+    "cfg1": dict(workload="grid14_congested (bundled), batch 64, full N-1, 1 busbar outage", batch=64),
+    "cfg2": dict(workload="synthetic 1k-bus/1.5k-branch grid, 4096-candidate batch, full N-1, 1 timestep",
+                 batch=4096),
+    "cfg4": dict(workload="synthetic TSO-scale 7k-bus/10.5k-branch grid, 500 splittable stations, "
+                          "16384-candidate batch, full N-1", batch=16384),
+}
+
+
+def grid_text(cfg: str) -> str:
+    if cfg == "cfg1":
+        return open(os.path.join(ROOT, "tests", "golden", "data", "grid14_congested.json")).read()
+    from tools.synth_grid import config_json
+    return config_json(cfg)
+
+
+def dist_setup():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl")
+    return world, rank, local
+
+
+class ClockSampler:
+    """nvidia-smi clocks and throttle reasons sampled during the timed region."""
+
+    def __init__(self, device: int):
+        self.device = device
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        q = ("clocks.sm,clocks.max.sm,clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+             "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap,power.draw")
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.device), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.thread = threading.Thread(target=self._read, daemon=True)
+            self.thread.start()
+        except OSError:
+            self.proc = None
+        return self
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def __exit__(self, *exc):
+        if self.proc:
+            self.proc.terminate()
+            try:
+                self.proc.wait(timeout=5)
+            except subprocess.TimeoutExpired:
+                self.proc.kill()
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            parts = [p.strip() for p in ln.split(",")]
+            if len(parts) < 7:
+                continue
+            try:
+                sm.append(float(parts[0]))
+                mx.append(float(parts[1]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, parts[2:6]):
+                if v.lower().startswith("active"):
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": [], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+def cpu_baseline(text: str, n_target_s: float = 12.0, world: int = 1):
+    """The reference algorithm (oracle restatement) on this host's cores: a
+    bounded sample of the same workload's genomes through
+    DcContext::evaluate_batch with threads = hardware concurrency."""
+    from oracle.oracle import OracleContext
+    orc = OracleContext(text)
+    cores = os.cpu_count() or 1
+    probe = orc.random_genomes(32, 3, 2, seed=11)
+    t = orc.time_evaluate_batch(probe, 3, 2, 1)
+    n = int(max(32, min(20000, 32 * n_target_s / max(t, 1e-6))))
+    sample = orc.random_genomes(n, 3, 2, seed=12)
+    dt = orc.time_evaluate_batch(sample, 3, 2, 1)
+    return {"value": n / dt, "unit": "topologies/s", "cores": cores, "kind": "port",
+            "sample": f"{n} random genomes (helpers.hpp random_genome, n_a=3, n_d=2) of this workload's grid, "
+                      f"full N-1, DcContext::evaluate_batch on {cores} threads, {dt:.1f} s"}
+
+
+def run_reference(args, world, rank):
+    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    if rank != 0:
+        return
+    text = grid_text(args.config)
+    from oracle.oracle import OracleContext
+    orc = OracleContext(text)
+    cores = os.cpu_count() or 1
+    probe = orc.random_genomes(16, 3, 2, seed=21)
+    t = orc.time_evaluate_batch(probe, 3, 2, 1)
+    per_step = int(max(16, min(CONFIGS[args.config]["batch"], 16 * 2.0 / max(t, 1e-6))))
+    for w in range(args.warmup):
+        orc.time_evaluate_batch(orc.random_genomes(per_step, 3, 2, seed=100 + w), 3, 2, 1)
+    total_n, total_t = 0, 0.0
+    for k in range(args.steps):
+        g = orc.random_genomes(per_step, 3, 2, seed=1000 + k)
+        total_t += orc.time_evaluate_batch(g, 3, 2, 1)
+        total_n += per_step
+    value = total_n / total_t
+    line = {"metric": "N-1-evaluated topologies/sec (DC)", "value": value, "unit": "topologies/s",
+            "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+            "ms_per_step": 1000.0 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, reference JSON format)",
+            "impl": "reference",
+            "config": {"workload": CONFIGS[args.config]["workload"], "batch_per_step": per_step,
+                       "note": "each step is a bounded sample of the workload's batch"},
+            "cpu_baseline": {"value": value, "unit": "topologies/s", "cores": cores, "kind": "port",
+                             "sample": f"{per_step} genomes per step x {args.steps} steps, DcContext::evaluate_batch "
+                                       f"(threads = {cores})"},
+            "e2e": {"value": value, "unit": "topologies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3)
+    world, rank, local = dist_setup()
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+            dist.destroy_process_group()
+        return
+
+    import torch
+    import paper_2605_10128_b200 as P
+
+    dev = local
+    torch.cuda.set_device(dev)
+    text = grid_text(args.config)
+    B = CONFIGS[args.config]["batch"]
+    grid = P.grid_from_json_text(text)
+    actions = P.build_action_set(grid)
+    ctx = P.DcContext(grid, actions, P.DcConfig(), device=dev)
+    info = ctx.info()
+    cfg = P.QdConfig(batch_size=B, iters_per_epoch=1 << 30, seed=1 + rank)  # one island per rank
+    sess = P.QdSession(ctx, cfg)
+    stream = torch.cuda.ExternalStream(P.context_stream(ctx), device=dev)
+
+    def barrier():
+        if world > 1:
+            import torch.distributed as dist
+            dist.barrier()
+
+    # warm-up generations
+    sess.step(args.warmup)
+    torch.cuda.synchronize()
+    barrier()
+
+    # ---- timed region: exactly K generations, device time, max over ranks
+    launches0 = ctx.kernel_launches()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with ClockSampler(dev) as clk:
+        torch.cuda.synchronize()
+        barrier()
+        e0.record(stream)
+        sess.step(args.steps)
+        e1.record(stream)
+        torch.cuda.synchronize()
+        barrier()
+    ms = e0.elapsed_time(e1)
+    launches = ctx.kernel_launches() - launches0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([ms], device=f"cuda:{dev}")
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    total = B * args.steps * world
+    value = total / (ms / 1000.0)
+    snap = sess.fetch()
+
+    # ---- live roofline of the fused sweep (same loop, sweep bracketed by events)
+    P.sweep_timing(ctx, True)
+    flops = 0.0
+    E, Ks = info["n_branches"], info["n_single"]
+    n_prof = 5
+    isl = 0
+    for _ in range(n_prof):
+        sess.step(1)
+        r = P.batch_ranks(ctx, B)
+        live = r[r >= 0]
+        isl += int((r < 0).sum())
+        flops += float(E) * Ks * float(np.sum(2.0 + 2.0 * live))
+    sweep_ms, sweep_n = P.sweep_timing(ctx, False)
+    torch.cuda.synchronize()
+    avg_ms = sweep_ms / max(sweep_n, 1)
+    achieved_tflops = flops / n_prof / (avg_ms * 1e-3) / 1e12
+    peak = P.fp64_peak_tflops(dev)
+    mean_rank = float(flops / n_prof / (E * Ks) / B / 2.0 - 1.0) if B else 0.0
+    traffic = None
+    prof_json = os.path.join(ROOT, "profiles", "sweep_ncu_summary.json")
+    if os.path.exists(prof_json):
+        try:
+            traffic = json.load(open(prof_json)).get(args.config, {}).get("dram_bytes_per_launch")
+        except (OSError, ValueError):
+            traffic = None
+
+    # ---- end to end through the reference-facing call with pinned host buffers
+    #      (DcContext::evaluate_batch: H2D genomes, evaluate, D2H scores each step)
+    rng = np.random.default_rng(7 + rank)
+    pool = np.array([e.genome.action_slots + e.genome.disconnection_slots for e in snap.entries], np.int32)
+    parents = pool[rng.integers(0, len(pool), B)]
+    genomes = P.mutate_lanes(ctx, cfg, parents, rng.integers(1, 2 ** 62, B, dtype=np.uint64))
+    g_pin = torch.from_numpy(genomes.reshape(-1)).pin_memory()
+    wk = ctx.config.worst_k
+    outs = {k: torch.zeros(B * m, dtype=t).pin_memory() for k, t, m in [
+        ("lambda_o", torch.float64, 1), ("lambda_c", torch.int32, 1), ("lambda_c0", torch.int32, 1),
+        ("lambda_b", torch.float64, 1), ("lambda_d", torch.int32, 1), ("lambda_s", torch.int32, 1),
+        ("lambda_r", torch.int32, 1), ("fitness", torch.float64, 1), ("islanded", torch.uint8, 1),
+        ("worst_idx", torch.int32, wk), ("worst_energy", torch.float64, wk), ("worst_n", torch.int32, 1),
+        ("islanded_outages", torch.int32, 1), ("islanded_busbar_outages", torch.int32, 1)]}
+    import ctypes as C
+    sc = P.api.L.ScoresC(*[C.cast(C.c_void_p(outs[f].data_ptr()), t) for f, t in P.api.L.ScoresC._fields_])
+    d2h = sum(v.numel() * v.element_size() for v in outs.values())
+    h2d = g_pin.numel() * 4
+    for _ in range(2):
+        P.evaluate_raw(ctx, g_pin.data_ptr(), B, 3, 2, sc)
+    torch.cuda.synchronize()
+    barrier()
+    t0 = time.perf_counter()
+    e2e_steps = max(3, min(args.steps, 20))
+    for _ in range(e2e_steps):
+        P.evaluate_raw(ctx, g_pin.data_ptr(), B, 3, 2, sc)
+    torch.cuda.synchronize()
+    e2e_s = time.perf_counter() - t0
+    if world > 1:
+        import torch.distributed as dist
+        t = torch.tensor([e2e_s], device=f"cuda:{dev}", dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        e2e_s = float(t.item())
+    e2e_value = B * e2e_steps * world / e2e_s
+
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        base = cpu_baseline(text)
+
+    work_bytes = B * (E * 64 + info["k_padded"] * 64)  # per-step candidate rows (feat + contingency rows)
+    if rank == 0:
+        line = {
+            "metric": "N-1-evaluated topologies/sec (DC)", "value": value, "unit": "topologies/s",
+            "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
+            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "data": "synthetic grid (seeded generator tools/synth_grid.py, reference JSON); genomes from the "
+                    "device MapElites loop",
+            "config": {"workload": CONFIGS[args.config]["workload"], "batch_per_gpu": B,
+                       "n_nodes": info["n_nodes"], "n_branches": E, "n_contingencies": info["n_contingencies"],
+                       "n_actions": info["n_actions"], "n_disconnectables": info["n_disconnectables"],
+                       "parallelism": f"islands x{world} (independent archives, seed 1+rank)",
+                       "l2": f"per-step candidate working set {work_bytes / 2**20:.0f} MiB > 126 MiB L2 "
+                             "(no flush needed)",
+                       "step": "one MapElites generation: mutate/crossover + full N-1 evaluation + archive insert",
+                       "archive_entries": len(snap.entries), "best_fitness": snap.best_fitness},
+            "gpu_launches": int(launches),
+            "roofline": {"bound": "fp64", "kernel": "k_sweep (fused N-1 sweep)", "achieved": achieved_tflops,
+                         "peak": peak, "unit": "TFLOP/s", "frac": achieved_tflops / peak if peak else None,
+                         "traffic": traffic, "peak_source": "DFMA microbenchmark on this GPU in this run "
+                                                            "(MEASURED_PEAKS.json has no FP64 figure)",
+                         "flops_per_launch": flops / n_prof, "avg_launch_ms": avg_ms,
+                         "mean_rank": mean_rank, "islanded_fraction": isl / (n_prof * B),
+                         "algorithmic": "E*K_single*(2+2r) per non-islanded candidate (SURVEY.md 8(d))"},
+            "e2e": {"value": e2e_value, "unit": "topologies/s", "h2d_bytes_per_step": int(h2d),
+                    "d2h_bytes_per_step": int(d2h),
+                    "call": "tg_evaluate_batch (DcContext::evaluate_batch) on pinned host buffers"},
+            "clocks": clk.summary(),
+        }
+        if base is not None:
+            line["cpu_baseline"] = base
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        import torch.distributed as dist
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

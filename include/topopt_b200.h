@@ -205,6 +205,13 @@ tg_status tg_pre_score(tg_context* ctx, tg_scores* out, double* lambda_b_pre);
 tg_status tg_optimizer_run(tg_context* ctx, const tg_qd_config* cfg, tg_snapshot_cb cb, void* user,
                            const volatile int32_t* stop, tg_opt_stats* stats, int64_t* trace_evaluations,
                            double* trace_best, int32_t trace_cap);
+/* Step-wise form of the same loop (what run_optimizer does between snapshots):
+ * begin = validate + seed the archive (1 evaluation); step = enqueue n
+ * generations asynchronously (one CUDA graph launch each, no host sync);
+ * fetch = synchronize and copy the archive out as a snapshot view. */
+tg_status tg_qd_begin(tg_context* ctx, const tg_qd_config* cfg);
+tg_status tg_qd_step(tg_context* ctx, int32_t n_iters);
+tg_status tg_qd_fetch(tg_context* ctx, int32_t final_snapshot, tg_snapshot_view* out);
 /* Archive of the last run as a snapshot view (valid until the next call). */
 tg_status tg_archive_export(tg_context* ctx, tg_snapshot_view* out);
 /* Repertoire::insert replay (qd_optimizer.cpp:281-303) on the device archive:
@@ -222,7 +229,15 @@ tg_status tg_mutate_lanes(tg_context* ctx, const tg_qd_config* cfg, const int32_
 tg_status tg_crossover_lanes(tg_context* ctx, const tg_qd_config* cfg, const int32_t* parents1,
                              const int32_t* parents2, const uint64_t* seeds, int32_t n, int32_t* children);
 
-/* ---- counters for the benchmark contract ---- */
+/* ---- counters and timing for the benchmark contract ---- */
+void* tg_context_stream(tg_context* ctx);   /* the context's cudaStream_t (for caller-side events) */
+/* Enables/disables CUDA-event timing of the fused sweep on evaluate calls and
+ * returns (then resets) the accumulated milliseconds and launch count. */
+tg_status tg_sweep_timing(tg_context* ctx, int32_t enable, double* total_ms, int64_t* launches);
+/* Low-rank update size of each candidate of the last evaluated batch (-1 = not swept). */
+tg_status tg_batch_ranks(tg_context* ctx, int32_t n, int32_t* ranks);
+/* Measured FP64 FMA throughput of `device` (TFLOP/s) from a DFMA microbenchmark. */
+tg_status tg_fp64_peak(int device, double* tflops);
 tg_status tg_context_info(tg_context* ctx, int64_t* values, int32_t n_values); /* see capi.cu */
 int64_t tg_kernel_launches(tg_context* ctx);  /* engine kernels launched so far */
 

@@ -107,6 +107,13 @@ SIGNATURES = [
     ("tg_crossover_lanes", C.c_int, [C.c_void_p, C.POINTER(QdConfigC), i32p, i32p, u64p, C.c_int32, i32p]),
     ("tg_context_info", C.c_int, [C.c_void_p, i64p, C.c_int32]),
     ("tg_kernel_launches", C.c_int64, [C.c_void_p]),
+    ("tg_qd_begin", C.c_int, [C.c_void_p, C.POINTER(QdConfigC)]),
+    ("tg_qd_step", C.c_int, [C.c_void_p, C.c_int32]),
+    ("tg_qd_fetch", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(SnapshotView)]),
+    ("tg_context_stream", C.c_void_p, [C.c_void_p]),
+    ("tg_sweep_timing", C.c_int, [C.c_void_p, C.c_int32, f64p, i64p]),
+    ("tg_batch_ranks", C.c_int, [C.c_void_p, C.c_int32, i32p]),
+    ("tg_fp64_peak", C.c_int, [C.c_int, f64p]),
 ]
 
 

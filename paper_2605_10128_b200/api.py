@@ -511,3 +511,94 @@ def run_optimizer(ctx: DcContext, cfg: QdConfig, sink: Optional[Callable[[Repert
     rep = _snapshot_from_view(view, cfg.n_a)
     trace = [(int(tev[i]), float(tbest[i])) for i in range(stats.n_trace)]
     return OptimizerResult(rep, OptimizerStats(int(stats.evaluations), int(stats.epochs), trace))
+
+
+# ---------------------------------------------------------------- device operator access (parity tests)
+def mutate_lanes(ctx: DcContext, cfg: QdConfig, parents: np.ndarray, seeds: np.ndarray) -> np.ndarray:
+    """mutate() (qd_optimizer.cpp:202-210) on the device, one lane per (parent, seed)."""
+    par = np.ascontiguousarray(parents, np.int32).reshape(-1, cfg.n_a + cfg.n_d)
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    out = np.zeros_like(par)
+    c = cfg.to_c()
+    _check(LIB.tg_mutate_lanes(ctx._h, C.byref(c), _ptr(par, C.c_int32), _ptr(sd, C.c_uint64), par.shape[0],
+                               _ptr(out, C.c_int32)))
+    return out
+
+
+def crossover_lanes(ctx: DcContext, cfg: QdConfig, p1: np.ndarray, p2: np.ndarray, seeds: np.ndarray) -> np.ndarray:
+    """crossover() (qd_optimizer.cpp:235-277) on the device, one lane per entry."""
+    a = np.ascontiguousarray(p1, np.int32).reshape(-1, cfg.n_a + cfg.n_d)
+    b = np.ascontiguousarray(p2, np.int32).reshape(-1, cfg.n_a + cfg.n_d)
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    out = np.zeros_like(a)
+    c = cfg.to_c()
+    _check(LIB.tg_crossover_lanes(ctx._h, C.byref(c), _ptr(a, C.c_int32), _ptr(b, C.c_int32),
+                                  _ptr(sd, C.c_uint64), a.shape[0], _ptr(out, C.c_int32)))
+    return out
+
+
+def archive_replay(ctx: DcContext, cfg: QdConfig, genomes: np.ndarray, scores: ScoreArrays):
+    """Repertoire::insert (qd_optimizer.cpp:281-303) replayed on the device archive;
+    returns (per-insert results, snapshot of the archive)."""
+    g = np.ascontiguousarray(genomes, np.int32).reshape(-1, cfg.n_a + cfg.n_d)
+    n = g.shape[0]
+    ins = np.zeros(n, np.uint8)
+    c = cfg.to_c()
+    _check(LIB.tg_archive_replay(ctx._h, C.byref(c), _ptr(g, C.c_int32), n, C.byref(scores.to_c()),
+                                 _ptr(ins, C.c_uint8)))
+    view = L.SnapshotView()
+    _check(LIB.tg_archive_export(ctx._h, C.byref(view)))
+    return ins.astype(bool), _snapshot_from_view(view, cfg.n_a)
+
+
+class QdSession:
+    """Step-wise run_optimizer (tg_qd_begin / tg_qd_step / tg_qd_fetch): the
+    loop the reference runs between two snapshots, with generations enqueued on
+    the device without host synchronization."""
+
+    def __init__(self, ctx: DcContext, cfg: QdConfig):
+        self.ctx = ctx
+        self.cfg = cfg
+        self._c = cfg.to_c()
+        _check(LIB.tg_qd_begin(ctx._h, C.byref(self._c)))
+
+    def step(self, n_iters: int = 1) -> None:
+        _check(LIB.tg_qd_step(self.ctx._h, n_iters))
+
+    def fetch(self, final: bool = False) -> RepertoireSnapshot:
+        view = L.SnapshotView()
+        _check(LIB.tg_qd_fetch(self.ctx._h, int(final), C.byref(view)))
+        return _snapshot_from_view(view, self.cfg.n_a)
+
+
+def context_stream(ctx: DcContext) -> int:
+    """cudaStream_t of the context (for caller-side CUDA events)."""
+    return int(LIB.tg_context_stream(ctx._h) or 0)
+
+
+def sweep_timing(ctx: DcContext, enable: bool) -> Tuple[float, int]:
+    """Toggle live event timing of the fused sweep; returns (ms, launches) so far."""
+    ms = C.c_double()
+    n = C.c_int64()
+    _check(LIB.tg_sweep_timing(ctx._h, int(enable), C.byref(ms), C.byref(n)))
+    return ms.value, n.value
+
+
+def batch_ranks(ctx: DcContext, n: int) -> np.ndarray:
+    out = np.zeros(n, np.int32)
+    _check(LIB.tg_batch_ranks(ctx._h, n, _ptr(out, C.c_int32)))
+    return out
+
+
+def fp64_peak_tflops(device: int = 0) -> float:
+    v = C.c_double()
+    _check(LIB.tg_fp64_peak(device, C.byref(v)))
+    return v.value
+
+
+def evaluate_raw(ctx: DcContext, genomes_ptr: int, n: int, n_a: int, n_d: int, scores: "L.ScoresC") -> None:
+    """tg_evaluate_batch on caller-owned host buffers given as raw pointers
+    (e.g. pinned memory): H2D genomes, evaluate, D2H scores."""
+    nullp = C.POINTER(C.c_double)()
+    _check(LIB.tg_evaluate_batch(ctx._h, C.cast(C.c_void_p(genomes_ptr), C.POINTER(C.c_int32)), n, n_a, n_d, n,
+                                 C.byref(scores), nullp, nullp, nullp, nullp))

@@ -1,6 +1,8 @@
 // C-ABI implementation: host model objects, device context, evaluation and
 // optimizer entry points (declared in include/topopt_b200.h).
 #include <algorithm>
+#include <chrono>
+#include <cmath>
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
@@ -201,6 +203,14 @@ struct tg_context {
   std::vector<double> snap_fit, snap_lo, snap_lb, snap_wval;
   tg_snapshot_view last_view{};
   int n_a_cap = 4, n_d_cap = 4;
+  // live timing of the fused sweep (bench.py roofline)
+  bool time_sweep = false;
+  cudaEvent_t sw0 = nullptr, sw1 = nullptr;
+  double sweep_ms = 0.0;
+  int64_t sweep_launches = 0;
+  // step-wise optimizer state
+  int64_t qd_evaluations = 0;
+  int qd_epoch = 0;
 
   void ensure_capacity(int n);
   void run_batch(int n, int n_a, int n_d, bool full);
@@ -209,6 +219,10 @@ struct tg_context {
 void tg_context::ensure_capacity(int n) {
   if (n <= capacity) return;
   const int cap = std::max(n, 64);
+  if (qd && qd->graph) {  // the captured iteration points at the old buffers
+    cudaGraphExecDestroy(qd->graph);
+    qd->graph = nullptr;
+  }
   batch_arena = std::make_unique<DeviceArena>();
   DeviceArena& A = *batch_arena;
   tgb::Batch& b = batch;
@@ -261,7 +275,20 @@ void tg_context::run_batch(int n, int n_a, int n_d, bool full) {
   batch.genomes = d_genomes;
   batch.params = params;
   int kernels = 0;
-  tgb::launch_evaluate(g, batch, n_a, n_d, full, scratch, stream, &kernels);
+  if (time_sweep && g.Ks > 0) {
+    if (!sw0) {
+      check(cudaEventCreate(&sw0), "event");
+      check(cudaEventCreate(&sw1), "event");
+    }
+    tgb::launch_evaluate(g, batch, n_a, n_d, full, scratch, stream, &kernels, sw0, sw1);
+    check(cudaEventSynchronize(sw1), "sweep timing");
+    float ms = 0.f;
+    check(cudaEventElapsedTime(&ms, sw0, sw1), "sweep timing");
+    sweep_ms += ms;
+    ++sweep_launches;
+  } else {
+    tgb::launch_evaluate(g, batch, n_a, n_d, full, scratch, stream, &kernels);
+  }
   launches += kernels;
   check(cudaGetLastError(), "evaluate launch");
 }
@@ -571,9 +598,12 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     ctx->ensure_capacity(1);
     std::vector<int> empty(1, -1);
     check(cudaMemcpyAsync(ctx->d_genomes, empty.data(), sizeof(int), cudaMemcpyHostToDevice, s), "H2D");
-    ctx->params.n_a = 1;
-    ctx->params.n_d = 0;
+    // lambda_b_pre is not known yet: score with variant 1, whose fitness equals the
+    // variant-2 pre-score (clip(lambda_b - lambda_b_pre) = 0 for the unchanged topology)
+    const int variant = ctx->params.variant;
+    ctx->params.variant = 1;
     ctx->run_batch(1, 1, 0, false);
+    ctx->params.variant = variant;
     check_errors(ctx.get(), 1);
     double lo_ = 0, lb_ = 0, fit = 0;
     int lc = 0, lc0 = 0;
@@ -585,7 +615,6 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     check(cudaMemcpy(&lc0, o.lambda_c0, sizeof(int), cudaMemcpyDeviceToHost), "D2H");
     ctx->lambda_b_pre = lb_;
     ctx->params.lambda_b_pre = lb_;
-    // with variant 2 the pre-score subtracts clip(lambda_b - lambda_b_pre) = 0
     ctx->pre = {lo_, static_cast<double>(lc), static_cast<double>(lc0), lb_, fit};
     *out = ctx.release();
   });
@@ -595,9 +624,14 @@ void tg_context_destroy(tg_context* ctx) {
   if (!ctx) return;
   cudaSetDevice(ctx->device);
   cudaStreamSynchronize(ctx->stream);
-  ctx->qd.reset();
+  if (ctx->qd) {
+    if (ctx->qd->graph) cudaGraphExecDestroy(ctx->qd->graph);
+    delete static_cast<DeviceArena*>(ctx->qd->arena);
+    ctx->qd.reset();
+  }
   ctx->batch_arena.reset();
   cudaStream_t s = ctx->stream;
+  if (ctx->sw0) cudaEventDestroy(ctx->sw0), cudaEventDestroy(ctx->sw1);
   delete ctx;
   cudaStreamDestroy(s);
 }
@@ -721,27 +755,432 @@ int64_t tg_kernel_launches(tg_context* ctx) { return ctx ? ctx->launches : 0; }
 
 }  // extern "C"
 
+// ---------------------------------------------------------------- MapElites loop
+namespace {
+
+tgb::QdParams qd_params(tg_context* ctx, const tg_qd_config* c) {
+  if (c->batch_size <= 0) throw tgb::ConfigError("batch size must be positive");
+  if (c->n_a < 0 || c->n_d < 0 || c->n_a > tgb::kMaxSplits || c->n_d > tgb::kMaxRemovedSweep)
+    throw tgb::ConfigError("n_a and n_d must lie in [0, 4] on the device");
+  if (c->cell_capacity <= 0 || c->cell_capacity > tgb::kMaxCellCap)
+    throw tgb::ConfigError("cell_capacity must lie in [1, 16] on the device");
+  if (!(c->mutation_mean < 12.0))
+    throw tgb::ConfigError("mutation_mean >= 12 (libstdc++ rejection sampler) is not replayed on the device");
+  if (c->d_max < 0 || c->s_max < 0 || c->r_max < 0) throw tgb::ConfigError("descriptor bounds must be >= 0");
+  tgb::QdParams p{};
+  p.n_a = c->n_a;
+  p.n_d = c->n_d;
+  p.batch = c->batch_size;
+  p.cap = c->cell_capacity;
+  p.d_max = c->d_max;
+  p.s_max = c->s_max;
+  p.r_max = c->r_max;
+  p.cells = (c->d_max + 1) * (c->s_max + 1) * (c->r_max + 1);
+  for (int i = 0; i < 4; ++i) p.p_action[i] = c->p_action[i], p.p_disc[i] = c->p_disc[i];
+  p.p_c1 = c->p_crossover_parent1;
+  p.poisson_thr = std::exp(-c->mutation_mean);  // poisson_distribution::param_type::_M_initialize
+  p.seed = c->seed;
+  p.n_actions = ctx->g.A;
+  p.n_disc = ctx->g.D;
+  return p;
+}
+
+void qd_setup(tg_context* ctx, const tgb::QdParams& p) {
+  auto& q = ctx->qd;
+  const bool same = q && q->p.cells == p.cells && q->p.cap == p.cap && q->p.n_a == p.n_a && q->p.n_d == p.n_d &&
+                    q->p.batch >= p.batch;
+  if (!same) {
+    if (q && q->graph) cudaGraphExecDestroy(q->graph);
+    delete static_cast<DeviceArena*>(q ? q->arena : nullptr);
+    q = std::make_unique<tgb::QdState>();
+    auto* A = new DeviceArena();
+    q->arena = A;
+    const size_t slots = static_cast<size_t>(p.cells) * p.cap;
+    const int ns = p.n_a + p.n_d, wk = std::max(ctx->worst_k, 1);
+    tgb::Archive& a = q->a;
+    a.count = A->alloc<int>(p.cells);
+    a.flat_start = A->alloc<int>(p.cells + 1);
+    a.genome = A->alloc<int>(slots * std::max(ns, 1));
+    a.key = A->alloc<int>(slots * std::max(ns, 1));
+    a.fitness = A->alloc<double>(slots);
+    a.lambda_o = A->alloc<double>(slots);
+    a.lambda_c = A->alloc<int>(slots);
+    a.lambda_c0 = A->alloc<int>(slots);
+    a.lambda_b = A->alloc<double>(slots);
+    a.lambda_d = A->alloc<int>(slots);
+    a.lambda_s = A->alloc<int>(slots);
+    a.lambda_r = A->alloc<int>(slots);
+    a.worst_idx = A->alloc<int>(slots * wk);
+    a.worst_val = A->alloc<double>(slots * wk);
+    a.worst_n = A->alloc<int>(slots);
+    a.iter = A->alloc<long long>(1);
+    q->inserted = A->alloc<uint8_t>(std::max(p.batch, 1));
+    q->lane_cell = A->alloc<int>(std::max(p.batch, 1));
+    q->graph_batch = 0;
+  }
+  if (q->graph && std::memcmp(&q->p, &p, sizeof(p)) != 0) {
+    cudaGraphExecDestroy(q->graph);
+    q->graph = nullptr;
+  }
+  q->p = p;
+  q->n_slots = p.n_a + p.n_d;
+  q->worst_k = ctx->worst_k;
+}
+
+// Host view of the device archive (make_snapshot, qd_optimizer.cpp:331-342).
+void fetch_archive(tg_context* ctx, int epoch, int64_t evaluations, bool fin) {
+  const tgb::QdState& q = *ctx->qd;
+  const tgb::Archive& a = q.a;
+  const int cells = q.p.cells, cap = q.p.cap, ns = q.n_slots, wk = std::max(q.worst_k, 1);
+  const size_t slots = static_cast<size_t>(cells) * cap;
+  std::vector<int> cnt(cells), gen(slots * std::max(ns, 1)), lc(slots), lc0(slots), ld(slots), ls(slots), lr(slots),
+      widx(slots * wk), wn(slots);
+  std::vector<double> fit(slots), lo(slots), lb(slots), wval(slots * wk);
+  cudaStream_t s = ctx->stream;
+  auto d2h = [&](void* dst, const void* src, size_t bytes) {
+    check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "archive D2H");
+  };
+  d2h(cnt.data(), a.count, cells * sizeof(int));
+  d2h(gen.data(), a.genome, gen.size() * sizeof(int));
+  d2h(fit.data(), a.fitness, slots * sizeof(double));
+  d2h(lo.data(), a.lambda_o, slots * sizeof(double));
+  d2h(lc.data(), a.lambda_c, slots * sizeof(int));
+  d2h(lc0.data(), a.lambda_c0, slots * sizeof(int));
+  d2h(lb.data(), a.lambda_b, slots * sizeof(double));
+  d2h(ld.data(), a.lambda_d, slots * sizeof(int));
+  d2h(ls.data(), a.lambda_s, slots * sizeof(int));
+  d2h(lr.data(), a.lambda_r, slots * sizeof(int));
+  d2h(widx.data(), a.worst_idx, widx.size() * sizeof(int));
+  d2h(wval.data(), a.worst_val, wval.size() * sizeof(double));
+  d2h(wn.data(), a.worst_n, slots * sizeof(int));
+  check(cudaStreamSynchronize(s), "archive fetch");
+  ctx->snap_cell.clear();
+  ctx->snap_genome.clear();
+  ctx->snap_fit.clear();
+  ctx->snap_lo.clear();
+  ctx->snap_lc.clear();
+  ctx->snap_lc0.clear();
+  ctx->snap_lb.clear();
+  ctx->snap_ld.clear();
+  ctx->snap_ls.clear();
+  ctx->snap_lr.clear();
+  ctx->snap_widx.clear();
+  ctx->snap_wval.clear();
+  ctx->snap_wn.clear();
+  double best = -INFINITY;
+  for (int c = 0; c < cells; ++c)
+    for (int i = 0; i < cnt[c]; ++i) {
+      const size_t at = static_cast<size_t>(c) * cap + i;
+      ctx->snap_cell.push_back(c);
+      for (int k = 0; k < ns; ++k) ctx->snap_genome.push_back(gen[at * ns + k]);
+      ctx->snap_fit.push_back(fit[at]);
+      ctx->snap_lo.push_back(lo[at]);
+      ctx->snap_lc.push_back(lc[at]);
+      ctx->snap_lc0.push_back(lc0[at]);
+      ctx->snap_lb.push_back(lb[at]);
+      ctx->snap_ld.push_back(ld[at]);
+      ctx->snap_ls.push_back(ls[at]);
+      ctx->snap_lr.push_back(lr[at]);
+      ctx->snap_wn.push_back(wn[at]);
+      for (int k = 0; k < wk; ++k) {
+        ctx->snap_widx.push_back(widx[at * wk + k]);
+        ctx->snap_wval.push_back(wval[at * wk + k]);
+      }
+      if (i == 0) best = std::max(best, fit[at]);
+    }
+  tg_snapshot_view& v = ctx->last_view;
+  v.epoch = epoch;
+  v.evaluations = evaluations;
+  v.best_fitness = best;
+  v.final_snapshot = fin ? 1 : 0;
+  v.n_entries = static_cast<int32_t>(ctx->snap_cell.size());
+  v.n_slots = ns;
+  v.cell = ctx->snap_cell.data();
+  v.genome = ctx->snap_genome.data();
+  v.fitness = ctx->snap_fit.data();
+  v.lambda_o = ctx->snap_lo.data();
+  v.lambda_c = ctx->snap_lc.data();
+  v.lambda_c0 = ctx->snap_lc0.data();
+  v.lambda_b = ctx->snap_lb.data();
+  v.lambda_d = ctx->snap_ld.data();
+  v.lambda_s = ctx->snap_ls.data();
+  v.lambda_r = ctx->snap_lr.data();
+  v.worst_idx = ctx->snap_widx.data();
+  v.worst_energy = ctx->snap_wval.data();
+  v.worst_n = ctx->snap_wn.data();
+  v.worst_k = wk;
+}
+
+// One MapElites iteration: offspring -> DC N-1 evaluation -> archive insert.
+int enqueue_iteration(tg_context* ctx) {
+  tgb::QdState& q = *ctx->qd;
+  const int B = q.p.batch;
+  tgb::launch_offspring(ctx->g, q, ctx->d_genomes, ctx->stream);
+  ctx->batch.n = B;
+  ctx->batch.genomes = ctx->d_genomes;
+  ctx->batch.params = ctx->params;
+  int kernels = 0;
+  tgb::launch_evaluate(ctx->g, ctx->batch, q.p.n_a, q.p.n_d, false, ctx->scratch, ctx->stream, &kernels);
+  tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, B, ctx->worst_k, true, ctx->stream);
+  return 1 + kernels + 2;
+}
+
+}  // namespace
+
 extern "C" {
-tg_status tg_optimizer_run(tg_context*, const tg_qd_config*, tg_snapshot_cb, void*, const volatile int32_t*,
-                           tg_opt_stats*, int64_t*, double*, int32_t) {
-  g_error = "optimizer loop not built yet";
-  return TG_CONFIG_ERROR;
+
+tg_status tg_qd_begin(tg_context* ctx, const tg_qd_config* cfg) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    if (ctx->g.A == 0 && ctx->g.D == 0)
+      throw tgb::ConfigError("nothing to optimize: no actions and no disconnectable branches");
+    const tgb::QdParams p = qd_params(ctx, cfg);
+    qd_setup(ctx, p);
+    tgb::QdState& q = *ctx->qd;
+    ctx->ensure_capacity(p.batch);
+    cudaStream_t s = ctx->stream;
+    // seed the archive with the unchanged topology (qd_optimizer.cpp:361-363)
+    tgb::launch_archive_reset(q, s);
+    check(cudaMemsetAsync(ctx->d_genomes, 0xff, static_cast<size_t>(q.n_slots) * sizeof(int), s), "seed genome");
+    ctx->run_batch(1, p.n_a, p.n_d, false);
+    tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, 1, ctx->worst_k, false, s);
+    ctx->launches += 2;
+    ctx->qd_evaluations = 1;
+    ctx->qd_epoch = 0;
+    // the whole iteration as one CUDA graph (no host round trip per generation)
+    if (!q.graph || q.graph_batch != p.batch) {
+      if (q.graph) cudaGraphExecDestroy(q.graph);
+      cudaGraph_t graph;
+      check(cudaStreamBeginCapture(s, cudaStreamCaptureModeThreadLocal), "capture");
+      q.kernels_per_iter = enqueue_iteration(ctx);
+      check(cudaStreamEndCapture(s, &graph), "capture end");
+      check(cudaGraphInstantiate(&q.graph, graph, 0), "graph instantiate");
+      cudaGraphDestroy(graph);
+      q.graph_batch = p.batch;
+    }
+  });
 }
-tg_status tg_archive_export(tg_context*, tg_snapshot_view*) {
-  g_error = "optimizer loop not built yet";
-  return TG_CONFIG_ERROR;
+
+tg_status tg_qd_step(tg_context* ctx, int32_t n_iters) {
+  return guarded([&] {
+    if (!ctx->qd || !ctx->qd->graph) throw tgb::ConfigError("call tg_qd_begin first");
+    if (ctx->time_sweep) {
+      // instrumented path: same kernels launched directly, sweep bracketed by events
+      tgb::QdState& q = *ctx->qd;
+      for (int i = 0; i < n_iters; ++i) {
+        tgb::launch_offspring(ctx->g, q, ctx->d_genomes, ctx->stream);
+        ctx->run_batch(q.p.batch, q.p.n_a, q.p.n_d, false);
+        tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, q.p.batch, ctx->worst_k, true, ctx->stream);
+        ctx->launches += 3;
+      }
+      ctx->qd_evaluations += static_cast<int64_t>(n_iters) * q.p.batch;
+      return;
+    }
+    for (int i = 0; i < n_iters; ++i) check(cudaGraphLaunch(ctx->qd->graph, ctx->stream), "graph launch");
+    ctx->launches += static_cast<int64_t>(n_iters) * ctx->qd->kernels_per_iter;
+    ctx->qd_evaluations += static_cast<int64_t>(n_iters) * ctx->qd->p.batch;
+  });
 }
-tg_status tg_archive_replay(tg_context*, const tg_qd_config*, const int32_t*, int32_t, const tg_scores*, uint8_t*) {
-  g_error = "optimizer loop not built yet";
-  return TG_CONFIG_ERROR;
+
+tg_status tg_qd_fetch(tg_context* ctx, int32_t final_snapshot, tg_snapshot_view* out) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    fetch_archive(ctx, ctx->qd_epoch, ctx->qd_evaluations, final_snapshot != 0);
+    if (out) *out = ctx->last_view;
+  });
 }
-tg_status tg_mutate_lanes(tg_context*, const tg_qd_config*, const int32_t*, const uint64_t*, int32_t, int32_t*) {
-  g_error = "optimizer loop not built yet";
-  return TG_CONFIG_ERROR;
+
+void* tg_context_stream(tg_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
+
+tg_status tg_sweep_timing(tg_context* ctx, int32_t enable, double* total_ms, int64_t* launches) {
+  return guarded([&] {
+    if (total_ms) *total_ms = ctx->sweep_ms;
+    if (launches) *launches = ctx->sweep_launches;
+    ctx->time_sweep = enable != 0;
+    ctx->sweep_ms = 0.0;
+    ctx->sweep_launches = 0;
+  });
 }
-tg_status tg_crossover_lanes(tg_context*, const tg_qd_config*, const int32_t*, const int32_t*, const uint64_t*, int32_t,
-                             int32_t*) {
-  g_error = "optimizer loop not built yet";
-  return TG_CONFIG_ERROR;
+
+tg_status tg_batch_ranks(tg_context* ctx, int32_t n, int32_t* ranks) {
+  return guarded([&] {
+    check(cudaMemcpyAsync(ranks, ctx->batch.rank, static_cast<size_t>(n) * sizeof(int), cudaMemcpyDeviceToHost,
+                          ctx->stream), "ranks D2H");
+    check(cudaStreamSynchronize(ctx->stream), "ranks");
+  });
 }
+
+tg_status tg_optimizer_run(tg_context* ctx, const tg_qd_config* cfg, tg_snapshot_cb cb, void* user,
+                           const volatile int32_t* stop, tg_opt_stats* stats, int64_t* trace_ev, double* trace_best,
+                           int32_t trace_cap) {
+  const auto t0 = std::chrono::steady_clock::now();
+  tg_status st = tg_qd_begin(ctx, cfg);
+  if (st != TG_OK) return st;
+  return guarded([&] {
+    tgb::QdState& q = *ctx->qd;
+    cudaStream_t s = ctx->stream;
+    auto elapsed = [&] { return std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count(); };
+    auto exhausted = [&] {
+      if (stop && *stop) return true;
+      if (cfg->max_evaluations >= 0 && ctx->qd_evaluations >= cfg->max_evaluations) return true;
+      if (cfg->max_seconds >= 0.0 && elapsed() >= cfg->max_seconds) return true;
+      return false;
+    };
+    // at most kInFlight generations queued ahead of the device, so stop /
+    // max_seconds act within a few generations (qd_optimizer.cpp:365-376)
+    constexpr int kInFlight = 4;
+    cudaEvent_t ev[kInFlight];
+    for (auto& e : ev) check(cudaEventCreateWithFlags(&e, cudaEventDisableTiming), "event");
+    int n_trace = 0;
+    int64_t launched = 0;
+    bool emitted_final = false;
+    while (!exhausted()) {
+      for (int it = 0; it < cfg->iters_per_epoch && !exhausted(); ++it) {
+        if (launched >= kInFlight) check(cudaEventSynchronize(ev[launched % kInFlight]), "throttle");
+        check(cudaGraphLaunch(q.graph, s), "graph launch");
+        check(cudaEventRecord(ev[launched % kInFlight], s), "event record");
+        ++launched;
+        ctx->launches += q.kernels_per_iter;
+        ctx->qd_evaluations += q.p.batch;
+      }
+      ++ctx->qd_epoch;
+      const bool fin = exhausted();
+      fetch_archive(ctx, ctx->qd_epoch, ctx->qd_evaluations, fin);
+      if (trace_ev && trace_best && n_trace < trace_cap) {
+        trace_ev[n_trace] = ctx->qd_evaluations;
+        trace_best[n_trace] = ctx->last_view.best_fitness;
+      }
+      ++n_trace;
+      if (cb) cb(&ctx->last_view, user);
+      if (fin) {
+        emitted_final = true;
+        break;
+      }
+    }
+    if (!emitted_final) {
+      fetch_archive(ctx, ctx->qd_epoch, ctx->qd_evaluations, true);
+      if (cb) cb(&ctx->last_view, user);
+    }
+    for (auto& e : ev) cudaEventDestroy(e);
+    // capacity errors raised inside the loop surface here
+    std::vector<int> err(q.p.batch);
+    check(cudaMemcpy(err.data(), ctx->batch.out.error, q.p.batch * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
+    for (int e : err)
+      if (e) throw CapacityFailure("a candidate exceeded the engine's compile-time capacity during the run");
+    if (stats) {
+      stats->evaluations = ctx->qd_evaluations;
+      stats->epochs = ctx->qd_epoch;
+      stats->n_trace = std::min(n_trace, trace_cap);
+    }
+  });
+}
+
+tg_status tg_archive_export(tg_context* ctx, tg_snapshot_view* out) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("no archive: run the optimizer or a replay first");
+    *out = ctx->last_view;
+  });
+}
+
+tg_status tg_archive_replay(tg_context* ctx, const tg_qd_config* cfg, const int32_t* genomes, int32_t n,
+                            const tg_scores* sc, uint8_t* inserted) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    tg_qd_config c2 = *cfg;
+    c2.batch_size = std::max(n, 1);
+    const tgb::QdParams p = qd_params(ctx, &c2);
+    qd_setup(ctx, p);
+    tgb::QdState& q = *ctx->qd;
+    ctx->ensure_capacity(std::max(n, 1));
+    cudaStream_t s = ctx->stream;
+    tgb::launch_archive_reset(q, s);
+    if (n > 0) {
+      const tgb::Scores& o = ctx->batch.out;
+      auto h2d = [&](void* dst, const void* src, size_t bytes) {
+        if (!src) throw tgb::ConfigError("replay needs fitness, lambda_d/s/r and worst lists");
+        check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "replay H2D");
+      };
+      const int wk = ctx->worst_k;
+      h2d(ctx->d_genomes, genomes, static_cast<size_t>(n) * q.n_slots * sizeof(int));
+      h2d(o.fitness, sc->fitness, n * sizeof(double));
+      h2d(o.lambda_d, sc->lambda_d, n * sizeof(int));
+      h2d(o.lambda_s, sc->lambda_s, n * sizeof(int));
+      h2d(o.lambda_r, sc->lambda_r, n * sizeof(int));
+      std::vector<double> zd(n, 0.0);
+      std::vector<int> zi(static_cast<size_t>(n) * std::max(wk, 1), 0);
+      std::vector<double> zw(static_cast<size_t>(n) * std::max(wk, 1), 0.0);
+      h2d(o.lambda_o, sc->lambda_o ? sc->lambda_o : zd.data(), n * sizeof(double));
+      h2d(o.lambda_b, sc->lambda_b ? sc->lambda_b : zd.data(), n * sizeof(double));
+      h2d(o.lambda_c, sc->lambda_c ? sc->lambda_c : zi.data(), n * sizeof(int));
+      h2d(o.lambda_c0, sc->lambda_c0 ? sc->lambda_c0 : zi.data(), n * sizeof(int));
+      h2d(o.worst_n, sc->worst_n ? sc->worst_n : zi.data(), n * sizeof(int));
+      h2d(o.worst_idx, sc->worst_idx ? sc->worst_idx : zi.data(), zi.size() * sizeof(int));
+      h2d(o.worst_val, sc->worst_energy ? sc->worst_energy : zw.data(), zw.size() * sizeof(double));
+      tgb::launch_insert(q, ctx->d_genomes, o, n, wk, false, s);
+      ctx->launches += 2;
+      if (inserted) check(cudaMemcpyAsync(inserted, q.inserted, n, cudaMemcpyDeviceToHost, s), "inserted D2H");
+    }
+    fetch_archive(ctx, 0, n, true);
+  });
+}
+
+tg_status tg_mutate_lanes(tg_context* ctx, const tg_qd_config* cfg, const int32_t* parents, const uint64_t* seeds,
+                          int32_t n, int32_t* children) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    tg_qd_config c2 = *cfg;
+    c2.batch_size = std::max(n, 1);
+    const tgb::QdParams p = qd_params(ctx, &c2);
+    tgb::QdState tmp;
+    tmp.p = p;
+    const size_t ns = p.n_a + p.n_d;
+    DeviceArena A;
+    int* dp = A.alloc<int>(n * ns);
+    int* dc = A.alloc<int>(n * ns);
+    auto* ds = A.alloc<unsigned long long>(n);
+    check(cudaMemcpyAsync(dp, parents, n * ns * sizeof(int), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    check(cudaMemcpyAsync(ds, seeds, n * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    tgb::launch_mutate_lanes(ctx->g, tmp, dp, ds, n, dc, ctx->stream);
+    ctx->launches += 1;
+    check(cudaMemcpyAsync(children, dc, n * ns * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    check(cudaStreamSynchronize(ctx->stream), "mutate");
+  });
+}
+
+tg_status tg_crossover_lanes(tg_context* ctx, const tg_qd_config* cfg, const int32_t* p1, const int32_t* p2,
+                             const uint64_t* seeds, int32_t n, int32_t* children) {
+  return guarded([&] {
+    check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    tg_qd_config c2 = *cfg;
+    c2.batch_size = std::max(n, 1);
+    const tgb::QdParams p = qd_params(ctx, &c2);
+    tgb::QdState tmp;
+    tmp.p = p;
+    const size_t ns = p.n_a + p.n_d;
+    DeviceArena A;
+    int* d1 = A.alloc<int>(n * ns);
+    int* d2 = A.alloc<int>(n * ns);
+    int* dc = A.alloc<int>(n * ns);
+    auto* ds = A.alloc<unsigned long long>(n);
+    check(cudaMemcpyAsync(d1, p1, n * ns * sizeof(int), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    check(cudaMemcpyAsync(d2, p2, n * ns * sizeof(int), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    check(cudaMemcpyAsync(ds, seeds, n * sizeof(uint64_t), cudaMemcpyHostToDevice, ctx->stream), "H2D");
+    tgb::launch_crossover_lanes(ctx->g, tmp, d1, d2, ds, n, dc, ctx->stream);
+    ctx->launches += 1;
+    check(cudaMemcpyAsync(children, dc, n * ns * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+    check(cudaStreamSynchronize(ctx->stream), "crossover");
+  });
+}
+
+}  // extern "C"
+
+namespace tgb {
+double measure_fp64_peak(int device);
+}
+
+extern "C" tg_status tg_fp64_peak(int device, double* tflops) {
+  return guarded([&] {
+    *tflops = tgb::measure_fp64_peak(device);
+    check(cudaGetLastError(), "fp64 peak");
+  });
 }

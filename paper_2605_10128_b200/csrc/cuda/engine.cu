@@ -531,7 +531,7 @@ __global__ void k_bits_to_double(const unsigned long long* in, double* out, size
 
 // ---------------------------------------------------------------- launcher
 void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
-                     cudaStream_t stream, int* kernels) {
+                     cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin, cudaEvent_t sweep_end) {
   int launched = 0;
   const int words = (g.E + 31) >> 5;
   const size_t bits_bytes = 2 * static_cast<size_t>(words) * sizeof(uint32_t);
@@ -547,11 +547,13 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
     k_bucket<<<1, 1024, 0, stream>>>(b);
     ++launched;
     dim3 grid(g.Kpad / kTileK, (b.n + kCandPerCta - 1) / kCandPerCta + kSweepRank + 1);
+    if (sweep_begin) cudaEventRecord(sweep_begin, stream);
     if (full)
       k_sweep<true><<<grid, kSweepThreads, 0, stream>>>(g, b);
     else
       k_sweep<false><<<grid, kSweepThreads, 0, stream>>>(g, b);
     ++launched;
+    if (sweep_end) cudaEventRecord(sweep_end, stream);
   }
   if (g.Kx + g.Kb > 0) {
     const long total = static_cast<long>(b.n) * (g.Kx + g.Kb);

@@ -59,8 +59,10 @@ struct EvalScratch {
   int zslots_special;
 };
 
+// sweep_begin / sweep_end (optional) bracket the fused sweep launch for live timing.
 void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
-                     cudaStream_t stream, int* kernels);
+                     cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin = nullptr,
+                     cudaEvent_t sweep_end = nullptr);
 void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_out, double* fbus_out,
                     cudaStream_t stream);
 int sweep_tile_k();

@@ -1,3 +1,558 @@
-// MapElites device loop (qd_optimizer.cpp:12-417). Entry points are defined
-// in capi.cu; the kernels live here.
+// MapElites on the device (qd_optimizer.cpp:12-417).
+//
+// Offspring lanes replay the reference's RNG stream bit for bit: each lane
+// seeds its own std::mt19937_64 (derive_seed(seed, iter, lane+1),
+// qd_optimizer.cpp:382) and draws through restatements of the libstdc++-13
+// distributions the reference calls (uniform_int_distribution's Lemire
+// downscale, generate_canonical<double,53>, the mean<12 Poisson method). The
+// engine state is generated lazily in place, so a lane only pays for the draws
+// it makes. The archive insert replays the sequential per-lane insert order
+// exactly with one warp per descriptor cell.
 #include "qd.cuh"
+
+namespace tgb {
+
+namespace {
+
+// ---------------------------------------------------------------- RNG (rng.hpp:9-21)
+__device__ __forceinline__ unsigned long long mix64(unsigned long long x) {
+  x += 0x9e3779b97f4a7c15ull;
+  x = (x ^ (x >> 30)) * 0xbf58476d1ce4e5b9ull;
+  x = (x ^ (x >> 27)) * 0x94d049bb133111ebull;
+  return x ^ (x >> 31);
+}
+__device__ __forceinline__ unsigned long long derive_seed(unsigned long long m, unsigned long long a,
+                                                          unsigned long long b) {
+  return mix64(mix64(m ^ mix64(a)) ^ mix64(b + 0x632be59bd9b4e019ull));
+}
+
+// std::mt19937_64 with the twist computed lazily, one word per draw, in place.
+struct Mt64 {
+  static constexpr int kN = 312, kM = 156;
+  unsigned long long mt[kN];
+  int i;
+  __device__ void seed(unsigned long long s) {
+    mt[0] = s;
+    for (int k = 1; k < kN; ++k) mt[k] = 6364136223846793005ull * (mt[k - 1] ^ (mt[k - 1] >> 62)) + k;
+    i = 0;
+  }
+  __device__ unsigned long long next() {
+    const int k = i;
+    const unsigned long long x = (mt[k] & 0xFFFFFFFF80000000ull) | (mt[k + 1 < kN ? k + 1 : 0] & 0x7FFFFFFFull);
+    unsigned long long y = mt[k + kM < kN ? k + kM : k + kM - kN] ^ (x >> 1) ^ ((x & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
+    mt[k] = y;
+    i = k + 1 < kN ? k + 1 : 0;
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= y >> 43;
+    return y;
+  }
+};
+
+// uniform_int_distribution<int>(a, b) over a 64-bit engine (uniform_int_dist.h:257-320)
+__device__ int uniform_int(Mt64& r, int a, int b) {
+  const unsigned long long urange =
+      static_cast<unsigned long long>(static_cast<long long>(b)) - static_cast<unsigned long long>(static_cast<long long>(a));
+  const unsigned long long range = urange + 1ull;
+  unsigned long long x = r.next();
+  unsigned long long low = x * range;
+  unsigned long long high = __umul64hi(x, range);
+  if (low < range) {
+    const unsigned long long threshold = (0ull - range) % range;
+    while (low < threshold) {
+      x = r.next();
+      low = x * range;
+      high = __umul64hi(x, range);
+    }
+  }
+  return static_cast<int>(high + static_cast<unsigned long long>(static_cast<long long>(a)));
+}
+
+// generate_canonical<double, 53> (random.tcc:3349-3381): one 64-bit draw / 2^64
+__device__ __forceinline__ double canonical(Mt64& r) {
+  double v = __dmul_rn(__ull2double_rn(r.next()), 0x1p-64);
+  if (v >= 1.0) v = 1.0 - 0x1p-53;
+  return v;
+}
+
+// uniform_real_distribution<double>(a, b): (u * (b - a)) + a, no contraction (random.h:1909)
+__device__ __forceinline__ double uniform_real(Mt64& r, double a, double b) {
+  return __dadd_rn(__dmul_rn(canonical(r), __dsub_rn(b, a)), a);
+}
+
+// poisson_distribution<int>, mean < 12 branch (random.tcc:1401-1411)
+__device__ int poisson(Mt64& r, double thr) {
+  int x = 0;
+  double prod = 1.0;
+  do {
+    prod = __dmul_rn(prod, canonical(r));
+    x += 1;
+  } while (prod > thr);
+  return x - 1;
+}
+
+// ---------------------------------------------------------------- operators
+struct Ops {
+  const DevGrid& g;
+  const QdParams& p;
+  __device__ int station(int a) const { return g.act_station[a]; }
+  __device__ int lo(int a) const { return g.st_range_lo[station(a)]; }
+  __device__ int hi(int a) const { return g.st_range_hi[station(a)]; }
+};
+
+// choose_feasible_op, qd_optimizer.cpp:100-113
+__device__ int choose_op(const double* w, const bool* ok, Mt64& r) {
+  double total = 0.0;
+  for (int i = 0; i < 4; ++i)
+    if (ok[i]) total = __dadd_rn(total, w[i]);
+  if (total <= 0.0) return 3;
+  double draw = uniform_real(r, 0.0, total);
+  for (int i = 0; i < 4; ++i) {
+    if (!ok[i]) continue;
+    if (draw < w[i]) return i;
+    draw = __dsub_rn(draw, w[i]);
+  }
+  return 3;
+}
+
+__device__ void sort_small(int* v, int n) {
+  for (int i = 1; i < n; ++i) {
+    int x = v[i], j = i - 1;
+    while (j >= 0 && v[j] > x) v[j + 1] = v[j], --j;
+    v[j + 1] = x;
+  }
+}
+
+// qd_optimizer.cpp:115-155
+__device__ void mutate_actions_once(const Ops& o, int* g, Mt64& r, int* trace) {
+  const int na = o.p.n_a;
+  // AddActionPool: excluded station ranges, sorted as pairs
+  int elo[kMaxSplits], ehi[kMaxSplits], nex = 0, excluded = 0;
+  for (int k = 0; k < na; ++k) {
+    const int a = g[k];
+    if (a < 0) continue;
+    elo[nex] = o.lo(a);
+    ehi[nex] = o.hi(a);
+    excluded += ehi[nex] - elo[nex];
+    ++nex;
+  }
+  for (int i = 1; i < nex; ++i) {
+    const int xl = elo[i], xh = ehi[i];
+    int j = i - 1;
+    while (j >= 0 && (elo[j] > xl || (elo[j] == xl && ehi[j] > xh))) elo[j + 1] = elo[j], ehi[j + 1] = ehi[j], --j;
+    elo[j + 1] = xl;
+    ehi[j + 1] = xh;
+  }
+  const int add_size = o.p.n_actions - excluded;
+  int empties[kMaxSplits], filled[kMaxSplits], ne = 0, nf = 0;
+  for (int k = 0; k < na; ++k) (g[k] < 0 ? empties[ne++] : filled[nf++]) = k;
+  // change pool: per filled slot (slot order), its station range minus the current set
+  int cur[kMaxSplits], ncur = 0;
+  for (int k = 0; k < na; ++k) {
+    bool dup = false;
+    for (int q = 0; q < ncur; ++q) dup = dup || cur[q] == g[k];
+    if (!dup) cur[ncur++] = g[k];
+  }
+  sort_small(cur, ncur);
+  int change_size = 0;
+  for (int k = 0; k < na; ++k) {
+    const int a = g[k];
+    if (a < 0) continue;
+    int in = 0;
+    for (int q = 0; q < ncur; ++q) in += cur[q] >= o.lo(a) && cur[q] < o.hi(a);
+    change_size += o.hi(a) - o.lo(a) - in;
+  }
+  const bool ok[4] = {ne > 0 && add_size > 0, nf > 0, change_size > 0, true};
+  const int op = choose_op(o.p.p_action, ok, r);
+  if (trace) *trace = op;
+  if (op == 0) {
+    const int slot = empties[uniform_int(r, 0, ne - 1)];
+    int rank = uniform_int(r, 0, add_size - 1);
+    int cursor = 0, pick = -1;
+    for (int i = 0; i < nex && pick < 0; ++i) {
+      const int gap = elo[i] - cursor;
+      if (rank < gap) pick = cursor + rank;
+      else rank -= gap, cursor = ehi[i];
+    }
+    g[slot] = pick >= 0 ? pick : cursor + rank;
+  } else if (op == 1) {
+    g[filled[uniform_int(r, 0, nf - 1)]] = -1;
+  } else if (op == 2) {
+    int idx = uniform_int(r, 0, change_size - 1), pick = -1;
+    for (int k = 0; k < na && pick < 0; ++k) {
+      const int a = g[k];
+      if (a < 0) continue;
+      const int lo = o.lo(a), hi = o.hi(a);
+      int in = 0;
+      for (int q = 0; q < ncur; ++q) in += cur[q] >= lo && cur[q] < hi;
+      const int cnt = hi - lo - in;
+      if (idx < cnt) {
+        int cand = lo + idx;
+        for (int q = 0; q < ncur; ++q)
+          if (cur[q] >= lo && cur[q] < hi && cur[q] <= cand) ++cand;
+        pick = cand;
+      } else {
+        idx -= cnt;
+      }
+    }
+    const int st = o.station(pick);
+    for (int k = 0; k < na; ++k)
+      if (g[k] >= 0 && o.station(g[k]) == st) {
+        g[k] = pick;
+        break;
+      }
+  }
+}
+
+// qd_optimizer.cpp:157-198
+__device__ void mutate_disconnections_once(const Ops& o, int* g, Mt64& r, int* trace) {
+  const int na = o.p.n_a, nd = o.p.n_d;
+  int* d = g + na;
+  int used[kMaxRemovedSweep], nu = 0;
+  for (int k = 0; k < nd; ++k)
+    if (d[k] >= 0) used[nu++] = d[k];
+  sort_small(used, nu);
+  const int pool = o.p.n_disc - nu;
+  int empties[kMaxRemovedSweep], filled[kMaxRemovedSweep], ne = 0, nf = 0;
+  for (int k = 0; k < nd; ++k) (d[k] < 0 ? empties[ne++] : filled[nf++]) = k;
+  const bool ok[4] = {ne > 0 && pool > 0, nf > 0, nf > 0 && pool > 0, true};
+  bool genome_empty = nf == 0;
+  for (int k = 0; k < na; ++k) genome_empty = genome_empty && g[k] < 0;
+  const int op = (genome_empty && ok[0]) ? 0 : choose_op(o.p.p_disc, ok, r);
+  if (trace) *trace = 10 + op;
+  auto pick_rank = [&](int rank) {
+    for (int q = 0; q < nu; ++q)
+      if (rank >= used[q]) ++rank;
+    return rank;
+  };
+  if (op == 0) {
+    const int slot = empties[uniform_int(r, 0, ne - 1)];
+    d[slot] = pick_rank(uniform_int(r, 0, pool - 1));
+  } else if (op == 1) {
+    d[filled[uniform_int(r, 0, nf - 1)]] = -1;
+  } else if (op == 2) {
+    const int pick = pick_rank(uniform_int(r, 0, pool - 1));
+    const int slot = filled[uniform_int(r, 0, nf - 1)];
+    d[slot] = pick;
+  }
+}
+
+// qd_optimizer.cpp:202-210
+__device__ void mutate(const Ops& o, int* g, Mt64& r, int* trace, int* n_trace) {
+  int n = poisson(r, o.p.poisson_thr);
+  const int hi = o.p.n_a > 1 ? o.p.n_a : 1;
+  n = n < 1 ? 1 : (n > hi ? hi : n);
+  int t = 0;
+  for (int k = 0; k < n; ++k) mutate_actions_once(o, g, r, trace ? trace + t++ : nullptr);
+  mutate_disconnections_once(o, g, r, trace ? trace + t++ : nullptr);
+  if (n_trace) *n_trace = t;
+}
+
+// qd_optimizer.cpp:217-231
+__device__ int union_draw(const int* p1, int n1, const int* p2, int n2, double pc1, Mt64& r) {
+  const double w1 = n1 == 0 ? 0.0 : pc1;
+  const double w2 = n2 == 0 ? 0.0 : __dsub_rn(1.0, pc1);
+  if (__dadd_rn(w1, w2) <= 0.0) return -1;
+  bool first;
+  if (w1 == 0.0)
+    first = false;
+  else if (w2 == 0.0)
+    first = true;
+  else
+    first = uniform_real(r, 0.0, __dadd_rn(w1, w2)) < w1;
+  return first ? p1[uniform_int(r, 0, n1 - 1)] : p2[uniform_int(r, 0, n2 - 1)];
+}
+
+__device__ bool contains(const int* v, int n, int x) {
+  for (int i = 0; i < n; ++i)
+    if (v[i] == x) return true;
+  return false;
+}
+
+// qd_optimizer.cpp:235-277
+__device__ void crossover(const Ops& o, const int* g1, const int* g2, int* child, Mt64& r) {
+  const int na = o.p.n_a, nd = o.p.n_d;
+  for (int k = 0; k < na + nd; ++k) child[k] = -1;
+  int a1[kMaxSplits], a2[kMaxSplits], n1 = 0, n2 = 0;
+  for (int k = 0; k < na; ++k) {
+    if (g1[k] >= 0) a1[n1++] = g1[k];
+    if (g2[k] >= 0) a2[n2++] = g2[k];
+  }
+  sort_small(a1, n1);
+  sort_small(a2, n2);
+  int used_st[kMaxSplits], placed[kMaxSplits], nus = 0, npl = 0;
+  for (int i = 0; i < na; ++i) {
+    int q1[kMaxSplits], q2[kMaxSplits], m1 = 0, m2 = 0;
+    for (int k = 0; k < n1; ++k)
+      if (!contains(placed, npl, a1[k]) && !contains(used_st, nus, o.station(a1[k]))) q1[m1++] = a1[k];
+    for (int k = 0; k < n2; ++k)
+      if (!contains(placed, npl, a2[k]) && !contains(used_st, nus, o.station(a2[k])) && !contains(a1, n1, a2[k]))
+        q2[m2++] = a2[k];
+    const int pick = union_draw(q1, m1, q2, m2, o.p.p_c1, r);
+    if (pick < 0) break;
+    child[i] = pick;
+    placed[npl++] = pick;
+    used_st[nus++] = o.station(pick);
+  }
+  int d1[kMaxRemovedSweep], d2[kMaxRemovedSweep], e1 = 0, e2 = 0;
+  for (int k = 0; k < nd; ++k) {
+    if (g1[na + k] >= 0) d1[e1++] = g1[na + k];
+    if (g2[na + k] >= 0) d2[e2++] = g2[na + k];
+  }
+  sort_small(d1, e1);
+  sort_small(d2, e2);
+  int pd[kMaxRemovedSweep], npd = 0;
+  for (int i = 0; i < nd; ++i) {
+    int q1[kMaxRemovedSweep], q2[kMaxRemovedSweep], m1 = 0, m2 = 0;
+    for (int k = 0; k < e1; ++k)
+      if (!contains(pd, npd, d1[k])) q1[m1++] = d1[k];
+    for (int k = 0; k < e2; ++k)
+      if (!contains(pd, npd, d2[k]) && !contains(d1, e1, d2[k])) q2[m2++] = d2[k];
+    const int pick = union_draw(q1, m1, q2, m2, o.p.p_c1, r);
+    if (pick < 0) break;
+    child[na + i] = pick;
+    pd[npd++] = pick;
+  }
+}
+
+// Repertoire::member (qd_optimizer.cpp:305-315): flat cell-major index -> (cell, pos)
+__device__ const int* member(const Archive& a, const QdParams& p, int ns, int flat) {
+  int lo = 0, hi = p.cells;  // last cell with flat_start <= flat
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a.flat_start[mid] <= flat) lo = mid;
+    else hi = mid;
+  }
+  const int pos = flat - a.flat_start[lo];
+  return a.genome + (static_cast<size_t>(lo) * p.cap + pos) * ns;
+}
+
+__global__ void k_offspring(DevGrid g, QdParams p, Archive a, int* genomes) {
+  __shared__ int b_mc;
+  const long long it = a.iter[0];
+  if (threadIdx.x == 0) {
+    Mt64 ir;
+    ir.seed(derive_seed(p.seed, 0x17e7ull, static_cast<unsigned long long>(it)));
+    b_mc = uniform_int(ir, 0, p.batch);
+  }
+  __syncthreads();
+  const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lane >= p.batch) return;
+  const int ns = p.n_a + p.n_d;
+  Ops o{g, p};
+  Mt64 r;
+  r.seed(derive_seed(p.seed, static_cast<unsigned long long>(it), static_cast<unsigned long long>(lane) + 1ull));
+  const int total = a.flat_start[p.cells];
+  int child[kMaxSlots];
+  if (lane < b_mc) {
+    const int* par = member(a, p, ns, uniform_int(r, 0, total - 1));
+    for (int k = 0; k < ns; ++k) child[k] = par[k];
+    mutate(o, child, r, nullptr, nullptr);
+  } else {
+    const int* p1 = member(a, p, ns, uniform_int(r, 0, total - 1));
+    const int* p2 = member(a, p, ns, uniform_int(r, 0, total - 1));
+    crossover(o, p1, p2, child, r);
+  }
+  for (int k = 0; k < ns; ++k) genomes[static_cast<size_t>(lane) * ns + k] = child[k];
+}
+
+__global__ void k_mutate_lanes(DevGrid g, QdParams p, const int* parents, const unsigned long long* seeds, int n,
+                               int* children) {
+  const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lane >= n) return;
+  const int ns = p.n_a + p.n_d;
+  Ops o{g, p};
+  Mt64 r;
+  r.seed(seeds[lane]);
+  int child[kMaxSlots];
+  for (int k = 0; k < ns; ++k) child[k] = parents[static_cast<size_t>(lane) * ns + k];
+  mutate(o, child, r, nullptr, nullptr);
+  for (int k = 0; k < ns; ++k) children[static_cast<size_t>(lane) * ns + k] = child[k];
+}
+
+__global__ void k_crossover_lanes(DevGrid g, QdParams p, const int* p1, const int* p2,
+                                  const unsigned long long* seeds, int n, int* children) {
+  const int lane = blockIdx.x * blockDim.x + threadIdx.x;
+  if (lane >= n) return;
+  const int ns = p.n_a + p.n_d;
+  Ops o{g, p};
+  Mt64 r;
+  r.seed(seeds[lane]);
+  int child[kMaxSlots];
+  crossover(o, p1 + static_cast<size_t>(lane) * ns, p2 + static_cast<size_t>(lane) * ns, child, r);
+  for (int k = 0; k < ns; ++k) children[static_cast<size_t>(lane) * ns + k] = child[k];
+}
+
+// ---------------------------------------------------------------- archive insert
+__device__ void canonical_key(const int* g, int na, int nd, int* key) {
+  int n = 0;
+  for (int k = 0; k < na; ++k)
+    if (g[k] >= 0) key[n++] = g[k];
+  sort_small(key, n);
+  for (int k = n; k < na; ++k) key[k] = -1;
+  n = 0;
+  for (int k = 0; k < nd; ++k)
+    if (g[na + k] >= 0) key[na + n++] = g[na + k];
+  sort_small(key + na, n);
+  for (int k = n; k < nd; ++k) key[na + k] = -1;
+}
+
+__device__ __forceinline__ int cell_of(const QdParams& p, int d, int s, int r) {
+  d = d < p.d_max ? d : p.d_max;
+  s = s < p.s_max ? s : p.s_max;
+  r = r < p.r_max ? r : p.r_max;
+  return d + (p.d_max + 1) * (s + (p.s_max + 1) * r);
+}
+
+// One warp per cell replays Repertoire::insert (qd_optimizer.cpp:281-303) over
+// the batch in lane order; cells are independent, so this equals the
+// reference's sequential loop.
+__global__ void k_insert(QdParams p, Archive a, const int* genomes, Scores sc, int n, int worst_k, uint8_t* inserted) {
+  const int cell = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (cell >= p.cells) return;
+  const int ns = p.n_a + p.n_d;
+  for (int c0 = 0; c0 < n; c0 += 32) {
+    const int c = c0 + lane;
+    bool mine = false;
+    if (c < n) {
+      const double f = sc.fitness[c];
+      const bool fin = isfinite(f);
+      mine = fin && cell_of(p, sc.lambda_d[c], sc.lambda_s[c], sc.lambda_r[c]) == cell;
+      if (!fin && cell == 0 && inserted) inserted[c] = 0;
+    }
+    unsigned m = __ballot_sync(0xffffffffu, mine);
+    while (m) {
+      const int bit = __ffs(m) - 1;
+      m &= m - 1;
+      if (lane == 0) {
+        const int cand = c0 + bit;
+        const int* gg = genomes + static_cast<size_t>(cand) * ns;
+        int key[kMaxSlots];
+        canonical_key(gg, p.n_a, p.n_d, key);
+        const double fit = sc.fitness[cand];
+        const int cnt = a.count[cell];
+        const size_t base = static_cast<size_t>(cell) * p.cap;
+        bool ok = true;
+        for (int i = 0; i < cnt && ok; ++i) {
+          bool same = true;
+          for (int k = 0; k < ns; ++k) same = same && a.key[(base + i) * ns + k] == key[k];
+          ok = !same;
+        }
+        if (ok && cnt >= p.cap && fit <= a.fitness[base + cnt - 1]) ok = false;
+        if (ok) {
+          int pos = 0;
+          while (pos < cnt && !(fit > a.fitness[base + pos])) ++pos;
+          const int last = cnt < p.cap ? cnt : p.cap - 1;
+          for (int i = last; i > pos; --i) {
+            const size_t dst = base + i, src = base + i - 1;
+            for (int k = 0; k < ns; ++k) {
+              a.genome[dst * ns + k] = a.genome[src * ns + k];
+              a.key[dst * ns + k] = a.key[src * ns + k];
+            }
+            a.fitness[dst] = a.fitness[src];
+            a.lambda_o[dst] = a.lambda_o[src];
+            a.lambda_c[dst] = a.lambda_c[src];
+            a.lambda_c0[dst] = a.lambda_c0[src];
+            a.lambda_b[dst] = a.lambda_b[src];
+            a.lambda_d[dst] = a.lambda_d[src];
+            a.lambda_s[dst] = a.lambda_s[src];
+            a.lambda_r[dst] = a.lambda_r[src];
+            a.worst_n[dst] = a.worst_n[src];
+            for (int k = 0; k < worst_k; ++k) {
+              a.worst_idx[dst * worst_k + k] = a.worst_idx[src * worst_k + k];
+              a.worst_val[dst * worst_k + k] = a.worst_val[src * worst_k + k];
+            }
+          }
+          const size_t at = base + pos;
+          for (int k = 0; k < ns; ++k) {
+            a.genome[at * ns + k] = gg[k];
+            a.key[at * ns + k] = key[k];
+          }
+          a.fitness[at] = fit;
+          a.lambda_o[at] = sc.lambda_o[cand];
+          a.lambda_c[at] = sc.lambda_c[cand];
+          a.lambda_c0[at] = sc.lambda_c0[cand];
+          a.lambda_b[at] = sc.lambda_b[cand];
+          a.lambda_d[at] = sc.lambda_d[cand];
+          a.lambda_s[at] = sc.lambda_s[cand];
+          a.lambda_r[at] = sc.lambda_r[cand];
+          a.worst_n[at] = sc.worst_n[cand];
+          for (int k = 0; k < worst_k; ++k) {
+            a.worst_idx[at * worst_k + k] = sc.worst_idx[static_cast<size_t>(cand) * worst_k + k];
+            a.worst_val[at * worst_k + k] = sc.worst_val[static_cast<size_t>(cand) * worst_k + k];
+          }
+          a.count[cell] = cnt < p.cap ? cnt + 1 : p.cap;
+        }
+        if (inserted) inserted[cand] = ok ? 1 : 0;
+      }
+      __syncwarp();
+    }
+  }
+}
+
+// Exclusive prefix of cell counts (member order) and the iteration counter.
+__global__ void k_archive_prefix(QdParams p, Archive a, int advance) {
+  __shared__ int part[1024];
+  const int per = (p.cells + blockDim.x - 1) / blockDim.x;
+  const int lo = threadIdx.x * per, hi = min(lo + per, p.cells);
+  int s = 0;
+  for (int c = lo; c < hi; ++c) s += a.count[c];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    int run = 0;
+    for (int t = 0; t < static_cast<int>(blockDim.x); ++t) {
+      const int v = part[t];
+      part[t] = run;
+      run += v;
+    }
+    a.flat_start[p.cells] = run;
+    if (advance) a.iter[0] += 1;
+  }
+  __syncthreads();
+  int run = part[threadIdx.x];
+  for (int c = lo; c < hi; ++c) {
+    a.flat_start[c] = run;
+    run += a.count[c];
+  }
+}
+
+__global__ void k_archive_clear(QdParams p, Archive a) {
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= p.cells; c += gridDim.x * blockDim.x) {
+    if (c < p.cells) a.count[c] = 0;
+    a.flat_start[c] = 0;
+  }
+  if (blockIdx.x == 0 && threadIdx.x == 0) a.iter[0] = 0;
+}
+
+}  // namespace
+
+void launch_archive_reset(const QdState& q, cudaStream_t s) {
+  k_archive_clear<<<(q.p.cells + 256) / 256, 256, 0, s>>>(q.p, q.a);
+}
+
+void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStream_t s) {
+  constexpr int kThreads = 64;  // lanes carry a 2.5 KB engine state in local memory
+  k_offspring<<<(q.p.batch + kThreads - 1) / kThreads, kThreads, 0, s>>>(g, q.p, q.a, genomes);
+}
+
+void launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
+                   cudaStream_t s) {
+  constexpr int kWarps = 8;
+  k_insert<<<(q.p.cells + kWarps - 1) / kWarps, 32 * kWarps, 0, s>>>(q.p, q.a, genomes, sc, n, worst_k, q.inserted);
+  k_archive_prefix<<<1, 256, 0, s>>>(q.p, q.a, advance_iter ? 1 : 0);
+}
+
+void launch_mutate_lanes(const DevGrid& g, const QdState& q, const int* parents, const unsigned long long* seeds, int n,
+                         int* children, cudaStream_t s) {
+  k_mutate_lanes<<<(n + 63) / 64, 64, 0, s>>>(g, q.p, parents, seeds, n, children);
+}
+
+void launch_crossover_lanes(const DevGrid& g, const QdState& q, const int* p1, const int* p2,
+                            const unsigned long long* seeds, int n, int* children, cudaStream_t s) {
+  k_crossover_lanes<<<(n + 63) / 64, 64, 0, s>>>(g, q.p, p1, p2, seeds, n, children);
+}
+
+}  // namespace tgb
