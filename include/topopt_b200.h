@@ -212,6 +212,12 @@ tg_status tg_optimizer_run(tg_context* ctx, const tg_qd_config* cfg, tg_snapshot
 tg_status tg_qd_begin(tg_context* ctx, const tg_qd_config* cfg);
 tg_status tg_qd_step(tg_context* ctx, int32_t n_iters);
 tg_status tg_qd_fetch(tg_context* ctx, int32_t final_snapshot, tg_snapshot_view* out);
+/* Lockstep halves of one generation (parity replay, qd_optimizer.cpp:377-401):
+ * offspring = the current iteration's lanes (mutation / crossover from the
+ * archive, no evaluation); insert = Repertoire::insert of caller-provided
+ * scores for those lanes in lane order, then the iteration counter advances. */
+tg_status tg_qd_offspring(tg_context* ctx, int32_t* genomes_out);
+tg_status tg_qd_insert(tg_context* ctx, const int32_t* genomes, const tg_scores* scores);
 /* Archive of the last run as a snapshot view (valid until the next call). */
 tg_status tg_archive_export(tg_context* ctx, tg_snapshot_view* out);
 /* Repertoire::insert replay (qd_optimizer.cpp:281-303) on the device archive:

@@ -72,6 +72,8 @@ def lib() -> C.CDLL:
         L.oc_crossover.argtypes = [vp, C.POINTER(QdConfigC), i32p, i32p, C.c_uint64, i32p]
         L.oc_run_optimizer.argtypes = [vp, C.POINTER(QdConfigC), C.c_int]
         L.oc_run_optimizer.restype = vp
+        L.oc_run_optimizer_trace.argtypes = [vp, C.POINTER(QdConfigC)]
+        L.oc_run_optimizer_trace.restype = vp
         L.oc_random_grid_json.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
         L.oc_random_grid_json.restype = vp
         L.oc_random_genomes.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_int, i32p]
@@ -182,6 +184,10 @@ class OracleContext:
 
     def run_optimizer(self, cfg: QdConfigC, all_snapshots: bool = False) -> dict:
         return json.loads(_take_string(lib().oc_run_optimizer(self.h, C.byref(cfg), int(all_snapshots))))
+
+    def run_optimizer_trace(self, cfg: QdConfigC) -> dict:
+        """run_optimizer with each iteration's offspring and scores (lockstep parity)."""
+        return json.loads(_take_string(lib().oc_run_optimizer_trace(self.h, C.byref(cfg))))
 
     def rebuild_flows(self, genome, n_a: int, n_d: int):
         g = np.ascontiguousarray(genome, np.int32)

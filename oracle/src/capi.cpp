@@ -2,6 +2,7 @@
 // extern "C" surface so pytest / bench.py (cpu_baseline) can drive the oracle
 // through ctypes. Structured results are returned as JSON text (oc_free them).
 #include <chrono>
+#include <cmath>
 #include <cstdlib>
 #include <cstring>
 #include <memory>
@@ -280,6 +281,47 @@ char* oc_run_optimizer(void* h, const oc_qd_config* cfg, int all_snapshots) {
     json j;
     j["stats"] = {{"evaluations", r.stats.evaluations}, {"epochs", r.stats.epochs}, {"fitness_trace", r.stats.fitness_trace}};
     j["snapshots"] = snaps;
+    out = dup_str(j.dump());
+  });
+  return rc == 0 ? out : nullptr;
+}
+
+// run_optimizer with a per-iteration trace: JSON {"iters":[{"it":i,"genomes":[[..]..],
+// "scores":[[fitness,ld,ls,lr,lo,lc,lc0,lb,worst_n,[idx..],[val..]]..]}], "stats":{...},
+// "final":[[cell,[genome],fitness]...]}
+char* oc_run_optimizer_trace(void* h, const oc_qd_config* cfg) {
+  char* out = nullptr;
+  int rc = guarded([&] {
+    auto* c = static_cast<Ctx*>(h);
+    QdConfig q = to_qd(cfg);
+    json iters = json::array();
+    IterationTrace tr = [&](std::int64_t it, const std::vector<Genome>& kids, const std::vector<ScoreVector>& sc) {
+      json gs = json::array(), ss = json::array();
+      for (std::size_t i = 0; i < kids.size(); ++i) {
+        std::vector<int> g = kids[i].action_slots;
+        g.insert(g.end(), kids[i].disconnection_slots.begin(), kids[i].disconnection_slots.end());
+        gs.push_back(g);
+        std::vector<int> wi;
+        std::vector<double> wv;
+        for (const auto& [k, v] : sc[i].worst_contingencies) wi.push_back(k), wv.push_back(v);
+        const double fit = std::isfinite(sc[i].fitness) ? sc[i].fitness : -1e300;
+        ss.push_back({fit, sc[i].lambda_d, sc[i].lambda_s, sc[i].lambda_r, sc[i].lambda_o, sc[i].lambda_c,
+                      sc[i].lambda_c0, sc[i].lambda_b, static_cast<int>(wi.size()), wi, wv});
+      }
+      iters.push_back({{"it", it}, {"genomes", gs}, {"scores", ss}});
+    };
+    auto r = run_optimizer(*c->dc, q, nullptr, nullptr, &tr);
+    json fin = json::array();
+    for (int cell = 0; cell < r.repertoire.n_cells(); ++cell)
+      for (const auto& e : r.repertoire.cell(cell)) {
+        std::vector<int> g = e.genome.action_slots;
+        g.insert(g.end(), e.genome.disconnection_slots.begin(), e.genome.disconnection_slots.end());
+        fin.push_back({cell, g, e.score.fitness});
+      }
+    json j;
+    j["iters"] = iters;
+    j["final"] = fin;
+    j["stats"] = {{"evaluations", r.stats.evaluations}, {"epochs", r.stats.epochs}};
     out = dup_str(j.dump());
   });
   return rc == 0 ? out : nullptr;

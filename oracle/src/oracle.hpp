@@ -396,7 +396,10 @@ struct OptimizerResult {
   Repertoire repertoire;
   OptimizerStats stats;
 };
+// Test hook (not in the reference): called after each iteration's evaluation
+// with the iteration index, offspring and their scores.
+using IterationTrace = std::function<void(std::int64_t, const std::vector<Genome>&, const std::vector<ScoreVector>&)>;
 OptimizerResult run_optimizer(const DcContext& ctx, const QdConfig& cfg, const SnapshotSink& sink,
-                              const std::atomic<bool>* stop = nullptr);
+                              const std::atomic<bool>* stop = nullptr, const IterationTrace* trace = nullptr);
 
 }  // namespace oracle

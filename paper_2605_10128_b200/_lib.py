@@ -110,6 +110,8 @@ SIGNATURES = [
     ("tg_qd_begin", C.c_int, [C.c_void_p, C.POINTER(QdConfigC)]),
     ("tg_qd_step", C.c_int, [C.c_void_p, C.c_int32]),
     ("tg_qd_fetch", C.c_int, [C.c_void_p, C.c_int32, C.POINTER(SnapshotView)]),
+    ("tg_qd_offspring", C.c_int, [C.c_void_p, i32p]),
+    ("tg_qd_insert", C.c_int, [C.c_void_p, i32p, C.POINTER(ScoresC)]),
     ("tg_context_stream", C.c_void_p, [C.c_void_p]),
     ("tg_sweep_timing", C.c_int, [C.c_void_p, C.c_int32, f64p, i64p]),
     ("tg_batch_ranks", C.c_int, [C.c_void_p, C.c_int32, i32p]),

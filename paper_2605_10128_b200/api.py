@@ -565,6 +565,17 @@ class QdSession:
     def step(self, n_iters: int = 1) -> None:
         _check(LIB.tg_qd_step(self.ctx._h, n_iters))
 
+    def offspring(self) -> np.ndarray:
+        """This generation's lanes (device mutation / crossover), without evaluating them."""
+        out = np.zeros((self.cfg.batch_size, self.cfg.n_a + self.cfg.n_d), np.int32)
+        _check(LIB.tg_qd_offspring(self.ctx._h, _ptr(out, C.c_int32)))
+        return out
+
+    def insert(self, genomes: np.ndarray, scores: ScoreArrays) -> None:
+        """Insert externally scored lanes in lane order and advance the generation."""
+        g = np.ascontiguousarray(genomes, np.int32)
+        _check(LIB.tg_qd_insert(self.ctx._h, _ptr(g, C.c_int32), C.byref(scores.to_c())))
+
     def fetch(self, final: bool = False) -> RepertoireSnapshot:
         view = L.SnapshotView()
         _check(LIB.tg_qd_fetch(self.ctx._h, int(final), C.byref(view)))

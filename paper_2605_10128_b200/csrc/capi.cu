@@ -503,7 +503,12 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     g.br_from = A.upload(v32(gd->branch_from, E), s);
     g.br_to = A.upload(v32(gd->branch_to, E), s);
     g.br_b = A.upload(b, s);
-    g.br_lim = A.upload(std::vector<double>(gd->branch_limit, gd->branch_limit + E), s);
+    {
+      // padded to whole sweep chunks: the sweep streams limits in 16-byte bulk copies
+      std::vector<double> lim(gd->branch_limit, gd->branch_limit + E);
+      lim.resize(E + tgb::sweep_chunk(), 0.0);
+      g.br_lim = A.upload(lim, s);
+    }
     g.br_on = A.upload(std::vector<uint8_t>(gd->branch_in_service, gd->branch_in_service + E), s);
     g.node_ptr = A.upload(nptr, s);
     g.node_br = A.upload(nbr, s);
@@ -987,6 +992,49 @@ tg_status tg_qd_fetch(tg_context* ctx, int32_t final_snapshot, tg_snapshot_view*
     if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
     fetch_archive(ctx, ctx->qd_epoch, ctx->qd_evaluations, final_snapshot != 0);
     if (out) *out = ctx->last_view;
+  });
+}
+
+tg_status tg_qd_offspring(tg_context* ctx, int32_t* genomes_out) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    tgb::QdState& q = *ctx->qd;
+    tgb::launch_offspring(ctx->g, q, ctx->d_genomes, ctx->stream);
+    ctx->launches += 1;
+    check(cudaMemcpyAsync(genomes_out, ctx->d_genomes, static_cast<size_t>(q.p.batch) * q.n_slots * sizeof(int),
+                          cudaMemcpyDeviceToHost, ctx->stream),
+          "offspring D2H");
+    check(cudaStreamSynchronize(ctx->stream), "offspring");
+  });
+}
+
+tg_status tg_qd_insert(tg_context* ctx, const int32_t* genomes, const tg_scores* sc) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    tgb::QdState& q = *ctx->qd;
+    const int n = q.p.batch, wk = ctx->worst_k;
+    const tgb::Scores& o = ctx->batch.out;
+    cudaStream_t s = ctx->stream;
+    auto h2d = [&](void* dst, const void* src, size_t bytes) {
+      if (!src) throw tgb::ConfigError("insert needs every score field");
+      check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, s), "insert H2D");
+    };
+    h2d(ctx->d_genomes, genomes, static_cast<size_t>(n) * q.n_slots * sizeof(int));
+    h2d(o.fitness, sc->fitness, n * sizeof(double));
+    h2d(o.lambda_o, sc->lambda_o, n * sizeof(double));
+    h2d(o.lambda_c, sc->lambda_c, n * sizeof(int));
+    h2d(o.lambda_c0, sc->lambda_c0, n * sizeof(int));
+    h2d(o.lambda_b, sc->lambda_b, n * sizeof(double));
+    h2d(o.lambda_d, sc->lambda_d, n * sizeof(int));
+    h2d(o.lambda_s, sc->lambda_s, n * sizeof(int));
+    h2d(o.lambda_r, sc->lambda_r, n * sizeof(int));
+    h2d(o.worst_n, sc->worst_n, n * sizeof(int));
+    h2d(o.worst_idx, sc->worst_idx, static_cast<size_t>(n) * wk * sizeof(int));
+    h2d(o.worst_val, sc->worst_energy, static_cast<size_t>(n) * wk * sizeof(double));
+    tgb::launch_insert(q, ctx->d_genomes, o, n, wk, true, s);
+    ctx->launches += 2;
+    ctx->qd_evaluations += n;
+    check(cudaStreamSynchronize(s), "insert");
   });
 }
 

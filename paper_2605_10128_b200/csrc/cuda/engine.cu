@@ -12,14 +12,6 @@ namespace tgb {
 namespace {
 
 constexpr int kPrepThreads = 256;
-constexpr int kKpl = 4;                    // contingencies per lane in the sweep
-constexpr int kTileK = 32 * kKpl;          // contingencies per CTA tile
-constexpr int kCandPerCta = 8;             // one candidate per warp
-constexpr int kSweepThreads = 32 * kCandPerCta;
-
-__device__ __forceinline__ uint32_t hi_abs(double x) {
-  return static_cast<uint32_t>(__double2hiint(x)) & 0x7fffffffu;
-}
 
 // ---------------------------------------------------------------- K2 prep
 // One CTA per candidate (grid-stride over candidates; Z scratch per CTA slot).
@@ -139,134 +131,6 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       for (int i = 0; i < kMaxRemovedSweep; ++i) rem[i] = i < t.nrem ? t.rem[i] : -1;
     }
     __syncthreads();
-  }
-}
-
-// ---------------------------------------------------------------- bucketing
-// Single CTA: stable per-rank lists of non-islanded candidates, each bucket
-// padded to whole sweep groups.
-__global__ void k_bucket(Batch b) {
-  __shared__ int cnt[kSweepRank + 1];
-  __shared__ int warp_tot[32];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  int base = 0;
-  int group_base = 0;
-  for (int r = 0; r <= kSweepRank; ++r) {
-    int running = 0;
-    for (int c0 = 0; c0 < b.n; c0 += blockDim.x) {
-      const int c = c0 + threadIdx.x;
-      const bool mine = c < b.n && b.rank[c] == r;
-      const unsigned m = __ballot_sync(0xffffffffu, mine);
-      if (lane == 0) warp_tot[wid] = __popc(m);
-      __syncthreads();
-      int off = 0;
-      for (int w = 0; w < wid; ++w) off += warp_tot[w];
-      if (mine) b.wl_list[base + running + off + __popc(m & ((1u << lane) - 1))] = c;
-      int tot = 0;
-      for (int w = 0; w < nw; ++w) tot += warp_tot[w];
-      running += tot;
-      __syncthreads();
-    }
-    if (threadIdx.x == 0) {
-      cnt[r] = running;
-      b.wl_start[r] = base;
-      b.wl_count[r] = running;
-      b.wl_group0[r] = group_base;
-    }
-    base += running;
-    group_base += (running + kCandPerCta - 1) / kCandPerCta;
-  }
-  if (threadIdx.x == 0) b.wl_group0[kSweepRank + 1] = group_base;
-}
-
-// ---------------------------------------------------------------- K3 sweep
-template <int R, bool FULL>
-__device__ __forceinline__ void sweep_body(const DevGrid& g, const Batch& b, int c, int k0) {
-  const int lane = threadIdx.x & 31;
-  const int kb = k0 + lane * kKpl;
-  double alpha[kKpl], rr[kKpl][R > 0 ? R : 1], energy[kKpl];
-  bool kval[kKpl];
-  int kbr[kKpl];
-  const double* kd = b.kdat + (static_cast<size_t>(c) * g.Kpad + kb) * kStride;
-  const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad + kb;
-#pragma unroll
-  for (int i = 0; i < kKpl; ++i) {
-    alpha[i] = kd[i * kStride];
-#pragma unroll
-    for (int q = 0; q < R; ++q) rr[i][q] = kd[i * kStride + 1 + q];
-    energy[i] = 0.0;
-    kval[i] = kf[i] == 0;
-    kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
-  }
-  const int* rem = b.removed + static_cast<size_t>(c) * kMaxRemovedSweep;
-  const int rem0 = rem[0], rem1 = rem[1], rem2 = rem[2], rem3 = rem[3];
-  const double* feat = b.feat + static_cast<size_t>(c) * g.E * kStride;
-  unsigned long long* fmx = b.fmax + static_cast<size_t>(c) * g.E;
-  const double* tk = g.TK + kb;
-  for (int e = 0; e < g.E; ++e) {
-    const double2 t01 = __ldg(reinterpret_cast<const double2*>(tk + static_cast<size_t>(e) * g.Kpad));
-    const double2 t23 = __ldg(reinterpret_cast<const double2*>(tk + static_cast<size_t>(e) * g.Kpad + 2));
-    const double tv[kKpl] = {t01.x, t01.y, t23.x, t23.y};
-    const double* fr = feat + static_cast<size_t>(e) * kStride;
-    double fe[R + 1];
-#pragma unroll
-    for (int q = 0; q <= R; ++q) fe[q] = fr[q];
-    const double lim = __ldg(g.br_lim + e);
-    const uint32_t limhi = hi_abs(lim);
-    double f1[kKpl];
-    bool hot = false;
-#pragma unroll
-    for (int i = 0; i < kKpl; ++i) {
-      double acc = fma(tv[i], alpha[i], fe[0]);
-#pragma unroll
-      for (int q = 0; q < R; ++q) acc = fma(fe[1 + q], rr[i][q], acc);
-      f1[i] = acc;
-      hot |= hi_abs(acc) >= limhi;
-    }
-    if (FULL || hot) {
-      const bool skip_row = e == rem0 || e == rem1 || e == rem2 || e == rem3;
-      double m = 0.0;
-#pragma unroll
-      for (int i = 0; i < kKpl; ++i) {
-        if (!kval[i] || skip_row || e == kbr[i]) continue;  // the outaged branch carries 0
-        const double a = fabs(f1[i]);
-        if (a > lim) energy[i] += a - lim;
-        m = fmax(m, a);
-      }
-      if (FULL) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0 && m > 0.0) atomic_max_pos(fmx + e, m);
-      } else if (m > lim) {
-        atomic_max_pos(fmx + e, m);
-      }
-    }
-  }
-  double* en = b.energy + static_cast<size_t>(c) * g.Kall;
-#pragma unroll
-  for (int i = 0; i < kKpl; ++i)
-    if (kval[i] && kb + i < g.Ks) en[g.ks_cont[kb + i]] = energy[i];
-}
-
-template <bool FULL>
-__global__ void __launch_bounds__(kSweepThreads) k_sweep(DevGrid g, Batch b) {
-  const int group = blockIdx.y;
-  if (group >= b.wl_group0[kSweepRank + 1]) return;
-  int r = 0;
-  while (r < kSweepRank && group >= b.wl_group0[r + 1]) ++r;
-  const int slot = (group - b.wl_group0[r]) * kCandPerCta + (threadIdx.x >> 5);
-  if (slot >= b.wl_count[r]) return;
-  const int c = b.wl_list[b.wl_start[r] + slot];
-  const int k0 = blockIdx.x * kTileK;
-  switch (r) {
-    case 0: sweep_body<0, FULL>(g, b, c, k0); break;
-    case 1: sweep_body<1, FULL>(g, b, c, k0); break;
-    case 2: sweep_body<2, FULL>(g, b, c, k0); break;
-    case 3: sweep_body<3, FULL>(g, b, c, k0); break;
-    case 4: sweep_body<4, FULL>(g, b, c, k0); break;
-    case 5: sweep_body<5, FULL>(g, b, c, k0); break;
-    case 6: sweep_body<6, FULL>(g, b, c, k0); break;
-    default: sweep_body<7, FULL>(g, b, c, k0); break;
   }
 }
 
@@ -543,18 +407,7 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
   k_prep<<<prep_grid, kPrepThreads, bits_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots);
   ++launched;
-  if (g.Ks > 0) {
-    k_bucket<<<1, 1024, 0, stream>>>(b);
-    ++launched;
-    dim3 grid(g.Kpad / kTileK, (b.n + kCandPerCta - 1) / kCandPerCta + kSweepRank + 1);
-    if (sweep_begin) cudaEventRecord(sweep_begin, stream);
-    if (full)
-      k_sweep<true><<<grid, kSweepThreads, 0, stream>>>(g, b);
-    else
-      k_sweep<false><<<grid, kSweepThreads, 0, stream>>>(g, b);
-    ++launched;
-    if (sweep_end) cudaEventRecord(sweep_end, stream);
-  }
+  if (g.Ks > 0) launch_sweep(g, b, full, stream, sweep_begin, sweep_end, &launched);
   if (g.Kx + g.Kb > 0) {
     const long total = static_cast<long>(b.n) * (g.Kx + g.Kb);
     const int grid = static_cast<int>(total < s.zslots_special ? total : s.zslots_special);
@@ -574,6 +427,5 @@ void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_o
   if (fbus_out) k_bits_to_double<<<512, 256, 0, stream>>>(b.fbus, fbus_out, n);
 }
 
-int sweep_tile_k() { return kTileK; }
 
 }  // namespace tgb

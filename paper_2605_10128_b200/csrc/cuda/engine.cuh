@@ -66,6 +66,9 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
 void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_out, double* fbus_out,
                     cudaStream_t stream);
 int sweep_tile_k();
+int sweep_chunk();
+void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1,
+                  int* launched);
 
 // Base factorization on the device (dc_engine.cpp:88-116, importer.cpp:358-401):
 // X = B_red^-1 by in-place Gauss-Jordan (B_red is SPD; no pivoting needed).

@@ -87,12 +87,15 @@ __global__ void k_branch_base(DevGrid g, const double* theta, double* f0, double
   }
 }
 
-// T_base[e, k] = b_e a_e^T X a_beta(k), e-major rows of Kpad contingencies.
-__global__ void k_tk(DevGrid g, double* tk) {
+// T_base[e, k] = b_e a_e^T X a_beta(k), stored in sweep tiles [k / W][e][k % W]
+// (W = sweep_tile_k()) so one pipeline stage of the sweep is one contiguous block.
+__global__ void k_tk(DevGrid g, double* tk, int W) {
   const size_t total = static_cast<size_t>(g.E) * g.Kpad;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
        idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
-    const int e = static_cast<int>(idx / g.Kpad), k = static_cast<int>(idx % g.Kpad);
+    const int kk = static_cast<int>(idx % W);
+    const size_t rest = idx / W;
+    const int e = static_cast<int>(rest % g.E), k = static_cast<int>(rest / g.E) * W + kk;
     double v = 0.0;
     if (k < g.Ks && g.br_on[e]) {
       const int beta = g.ks_branch[k];
@@ -144,7 +147,7 @@ void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, d
   g2.theta0 = theta0;
   k_branch_base<<<(g.E + 255) / 256 + 1, 256, 0, stream>>>(g2, theta0, f0, tdiag);
   const size_t total = static_cast<size_t>(g.E) * g.Kpad;
-  if (total > 0) k_tk<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32)), 256, 0, stream>>>(g2, tk);
+  if (total > 0) k_tk<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32)), 256, 0, stream>>>(g2, tk, sweep_tile_k());
 }
 
 }  // namespace tgb

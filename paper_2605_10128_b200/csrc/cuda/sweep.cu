@@ -1,0 +1,303 @@
+// K3: the fused N-1 contingency sweep (dc_engine.cpp:294-371 for single-branch
+// contingencies, all candidates of a batch at once).
+//
+// For candidate c, monitored branch e and contingency k (branch beta_k):
+//   f1[e,k] = f_c[e] + T_base[e,k] * alpha_k + sum_r L[e,r] * R'[r,k]
+// (topo.cuh: T_cand = T_base + L R, alpha_k = f_c[beta]/(1 - T_cand[beta,beta]),
+// R' = R * alpha). The E x K x B tensor is never written: each element is
+// tested against the branch limit in registers; only elements with
+// |f1| > limit touch the per-(c,k) energy accumulators (registers, summed in
+// branch order) and the per-(c,e) max (atomicMax on the ordered bit pattern).
+//
+// Dataflow (one CTA = one 128-contingency tile x 8*NC candidates):
+//   * T_base tiles ([tile][E][128], 32 branches = 32 KB per stage), the
+//     candidates' branch rows (f_c, L) and the branch limits are streamed into
+//     shared memory by TMA bulk copies (cp.async.bulk + mbarrier complete_tx),
+//     3-stage pipeline, one elected producer thread;
+//   * each lane owns 4 contingencies: alpha / R' live in registers for the
+//     whole sweep; each warp processes NC candidates so one T load feeds NC
+//     candidates' FMAs;
+//   * per element: (1 + R) DFMA + a 2-op hi-word test; the exact path runs only
+//     where |f1| can exceed the limit.
+#include <cstdint>
+
+#include "engine.cuh"
+
+namespace tgb {
+
+namespace {
+
+constexpr int kKpl = 4;                  // contingencies per lane
+constexpr int kTileK = 32 * kKpl;        // contingencies per CTA tile
+constexpr int kWarps = 8;
+constexpr int kThreads = 32 * kWarps;
+constexpr int kChunk = 32;               // branches per pipeline stage
+constexpr int kStages = 3;
+constexpr int kMaxCand = 2 * kWarps;     // candidates per CTA at NC = 2
+
+// candidates per warp for a given rank (register budget)
+__host__ __device__ constexpr int nc_for_rank(int r) { return r <= 5 ? 2 : 1; }
+__host__ __device__ constexpr int cand_per_cta(int r) { return kWarps * nc_for_rank(r); }
+
+constexpr size_t kStageT = static_cast<size_t>(kChunk) * kTileK;           // doubles
+constexpr size_t kStageF = static_cast<size_t>(kMaxCand) * kChunk * kStride;  // doubles
+constexpr size_t kStageL = kChunk;                                         // doubles
+constexpr size_t kStageDoubles = kStageT + kStageF + kStageL;
+constexpr size_t kSmemBytes = kStages * kStageDoubles * sizeof(double) + 64;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count) : "memory");
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+// TMA bulk copy global -> shared, completion counted on the mbarrier
+__device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(smem_u32(dst)),
+      "l"(src), "r"(bytes), "r"(smem_u32(bar))
+      : "memory");
+}
+
+__device__ __forceinline__ uint32_t hi_abs(double x) {
+  return static_cast<uint32_t>(__double2hiint(x)) & 0x7fffffffu;
+}
+
+struct CtaWork {
+  int cand[kMaxCand];
+  int ncand;
+};
+
+// Producer: stage `s` <- chunk `i` (T tile rows, candidate rows, limits).
+__device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, int i,
+                                           double* stage, uint64_t* bar) {
+  const int e0 = i * kChunk;
+  const int rows = min(kChunk, g.E - e0);
+  const uint32_t bt = rows * kTileK * sizeof(double);
+  const uint32_t bf = rows * kStride * sizeof(double);
+  const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
+  mbar_expect_tx(bar, bt + w.ncand * bf + bl);
+  bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
+  double* sf = stage + kStageT;
+  for (int j = 0; j < w.ncand; ++j)
+    bulk_g2s(sf + static_cast<size_t>(j) * kChunk * kStride, b.feat + (static_cast<size_t>(w.cand[j]) * g.E + e0) * kStride,
+             bf, bar);
+  bulk_g2s(stage + kStageT + kStageF, g.br_lim + e0, bl, bar);
+}
+
+template <int R, int NC, bool FULL>
+__device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
+                                          uint64_t* bars) {
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = tile * kTileK + lane * kKpl;
+  // per-(candidate, contingency) operands in registers
+  double alpha[NC][kKpl], rr[NC][kKpl][R > 0 ? R : 1], energy[NC][kKpl];
+  bool kval[NC][kKpl];
+  int kbr[kKpl];
+  int cid[NC], rem[NC][kMaxRemovedSweep];
+#pragma unroll
+  for (int i = 0; i < kKpl; ++i) kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    const int slot = warp * NC + j;
+    cid[j] = slot < w.ncand ? w.cand[slot] : -1;
+    const int c = cid[j] >= 0 ? cid[j] : w.cand[0];
+    const double* kd = b.kdat + (static_cast<size_t>(c) * g.Kpad + kb) * kStride;
+    const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad + kb;
+#pragma unroll
+    for (int i = 0; i < kKpl; ++i) {
+      alpha[j][i] = kd[i * kStride];
+#pragma unroll
+      for (int q = 0; q < R; ++q) rr[j][i][q] = kd[i * kStride + 1 + q];
+      energy[j][i] = 0.0;
+      kval[j][i] = cid[j] >= 0 && kf[i] == 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kMaxRemovedSweep; ++q) rem[j][q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
+  }
+
+  const int nchunks = (g.E + kChunk - 1) / kChunk;
+  if (threadIdx.x == 0)
+    for (int s = 0; s < kStages && s < nchunks; ++s)
+      issue_chunk(g, b, w, tile, s, smem + s * kStageDoubles, bars + s);
+
+  for (int i = 0; i < nchunks; ++i) {
+    const int s = i % kStages;
+    const double* st = smem + s * kStageDoubles;
+    mbar_wait(bars + s, (i / kStages) & 1);
+    const int e0 = i * kChunk;
+    const int rows = min(kChunk, g.E - e0);
+    const double* sT = st + lane * kKpl;
+    const double* sF = st + kStageT + static_cast<size_t>(warp) * NC * kChunk * kStride;
+    const double* sL = st + kStageT + kStageF;
+    for (int el = 0; el < rows; ++el) {
+      const double2 t01 = *reinterpret_cast<const double2*>(sT + el * kTileK);
+      const double2 t23 = *reinterpret_cast<const double2*>(sT + el * kTileK + 2);
+      const double tv[kKpl] = {t01.x, t01.y, t23.x, t23.y};
+      const double lim = sL[el];
+      const uint32_t limhi = hi_abs(lim);
+      double f1[NC][kKpl];
+      bool hot = false;
+#pragma unroll
+      for (int j = 0; j < NC; ++j) {
+        const double* fr = sF + (static_cast<size_t>(j) * kChunk + el) * kStride;
+        double fe[R + 1];
+#pragma unroll
+        for (int q = 0; q <= R; ++q) fe[q] = fr[q];
+#pragma unroll
+        for (int k = 0; k < kKpl; ++k) {
+          double acc = fma(tv[k], alpha[j][k], fe[0]);
+#pragma unroll
+          for (int q = 0; q < R; ++q) acc = fma(fe[1 + q], rr[j][k][q], acc);
+          f1[j][k] = acc;
+          hot |= hi_abs(acc) >= limhi;
+        }
+      }
+      if (FULL || hot) {
+        const int e = e0 + el;
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          bool skip_row = false;
+#pragma unroll
+          for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[j][q];
+          double m = 0.0;
+#pragma unroll
+          for (int k = 0; k < kKpl; ++k) {
+            if (!kval[j][k] || skip_row || e == kbr[k]) continue;  // the outaged branch carries 0
+            const double a = fabs(f1[j][k]);
+            if (a > lim) energy[j][k] += a - lim;
+            m = fmax(m, a);
+          }
+          if (cid[j] < 0) continue;
+          unsigned long long* fmx = b.fmax + static_cast<size_t>(cid[j]) * g.E;
+          if (FULL) {
+#pragma unroll
+            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+            if (lane == 0 && m > 0.0) atomicMax(fmx + e, static_cast<unsigned long long>(__double_as_longlong(m)));
+          } else if (m > lim) {
+            atomicMax(fmx + e, static_cast<unsigned long long>(__double_as_longlong(m)));
+          }
+        }
+      }
+    }
+    __syncthreads();  // every warp is done with stage s
+    if (threadIdx.x == 0 && i + kStages < nchunks) issue_chunk(g, b, w, tile, i + kStages, smem + s * kStageDoubles, bars + s);
+  }
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    if (cid[j] < 0) continue;
+    double* en = b.energy + static_cast<size_t>(cid[j]) * g.Kall;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k)
+      if (kval[j][k] && kb + k < g.Ks) en[g.ks_cont[kb + k]] = energy[j][k];
+  }
+}
+
+template <bool FULL>
+__global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ CtaWork w;
+  __shared__ int r_s;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  double* smem = reinterpret_cast<double*>(smem_raw + 64);
+  const int group = blockIdx.y;
+  if (group >= b.wl_group0[kSweepRank + 1]) return;
+  if (threadIdx.x == 0) {
+    int r = 0;
+    while (r < kSweepRank && group >= b.wl_group0[r + 1]) ++r;
+    r_s = r;
+    const int per = cand_per_cta(r);
+    const int first = (group - b.wl_group0[r]) * per;
+    int n = 0;
+    for (int j = 0; j < per; ++j)
+      if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
+    w.ncand = n;
+    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncthreads();
+  const int tile = blockIdx.x;
+  switch (r_s) {
+    case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars); break;
+    case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars); break;
+    case 2: sweep_cta<2, nc_for_rank(2), FULL>(g, b, w, tile, smem, bars); break;
+    case 3: sweep_cta<3, nc_for_rank(3), FULL>(g, b, w, tile, smem, bars); break;
+    case 4: sweep_cta<4, nc_for_rank(4), FULL>(g, b, w, tile, smem, bars); break;
+    case 5: sweep_cta<5, nc_for_rank(5), FULL>(g, b, w, tile, smem, bars); break;
+    case 6: sweep_cta<6, nc_for_rank(6), FULL>(g, b, w, tile, smem, bars); break;
+    default: sweep_cta<7, nc_for_rank(7), FULL>(g, b, w, tile, smem, bars); break;
+  }
+}
+
+// Stable per-rank lists of swept candidates; bucket r is cut into CTA groups
+// of cand_per_cta(r).
+__global__ void k_bucket(Batch b) {
+  __shared__ int warp_tot[32];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  int base = 0, group_base = 0;
+  for (int r = 0; r <= kSweepRank; ++r) {
+    int running = 0;
+    for (int c0 = 0; c0 < b.n; c0 += blockDim.x) {
+      const int c = c0 + threadIdx.x;
+      const bool mine = c < b.n && b.rank[c] == r;
+      const unsigned m = __ballot_sync(0xffffffffu, mine);
+      if (lane == 0) warp_tot[wid] = __popc(m);
+      __syncthreads();
+      int off = 0, tot = 0;
+      for (int x = 0; x < nw; ++x) {
+        if (x < wid) off += warp_tot[x];
+        tot += warp_tot[x];
+      }
+      if (mine) b.wl_list[base + running + off + __popc(m & ((1u << lane) - 1))] = c;
+      running += tot;
+      __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+      b.wl_start[r] = base;
+      b.wl_count[r] = running;
+      b.wl_group0[r] = group_base;
+    }
+    base += running;
+    group_base += (running + cand_per_cta(r) - 1) / cand_per_cta(r);
+  }
+  if (threadIdx.x == 0) b.wl_group0[kSweepRank + 1] = group_base;
+}
+
+}  // namespace
+
+int sweep_tile_k() { return kTileK; }
+int sweep_chunk() { return kChunk; }
+
+void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1,
+                  int* launched) {
+  static bool configured = false;
+  if (!configured) {
+    cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    configured = true;
+  }
+  k_bucket<<<1, 1024, 0, stream>>>(b);
+  // group slots: every bucket rounds up to whole groups of >= kWarps candidates
+  dim3 grid(g.Kpad / kTileK, (b.n + kWarps - 1) / kWarps + kSweepRank + 1);
+  if (ev0) cudaEventRecord(ev0, stream);
+  if (full)
+    k_sweep<true><<<grid, kThreads, kSmemBytes, stream>>>(g, b);
+  else
+    k_sweep<false><<<grid, kThreads, kSmemBytes, stream>>>(g, b);
+  if (ev1) cudaEventRecord(ev1, stream);
+  *launched += 2;
+}
+
+}  // namespace tgb
