@@ -27,12 +27,13 @@ def _all_singles(ctx, n_a=3, n_d=2):
 def _check(ctx, orc, genomes, n_a=3, n_d=2, flows=True):
     sc, fr = ctx.evaluate_arrays(genomes, n_a, n_d, flows=True)
     ref = orc.evaluate(genomes, n_a, n_d, flows=True)
-    errs = compare_scores(sc, ref, ctx.config.worst_k)
+    lim = ctx.grid.branch_limit
+    errs = compare_scores(sc, ref, ctx.config.worst_k, lim)
     if flows:
         errs.update(compare_flows(fr, ref))
     # the fast (scores-only) sweep must agree with the full-flows sweep
     fast = ctx.evaluate_arrays(genomes, n_a, n_d)
-    compare_scores(fast, ref, ctx.config.worst_k)
+    compare_scores(fast, ref, ctx.config.worst_k, lim)
     return errs
 
 

@@ -12,6 +12,7 @@ import pytest
 
 import paper_2605_10128_b200 as P
 from oracle.oracle import OracleContext, qd_config, random_grid_json
+from tests.parity import compare_scores
 
 pytestmark = pytest.mark.gpu
 
@@ -161,20 +162,15 @@ def test_lockstep_loop_matches_reference(data_dir):
         trace = orc.run_optimizer_trace(qd_config(**kw))
         assert len(trace["iters"]) == 50
         sess = P.QdSession(ctx, P.QdConfig(**kw))
-        worst = 0.0
         for it in trace["iters"]:
             ref_g = np.array(it["genomes"], np.int32)
             got_g = sess.offspring()
             assert np.array_equal(got_g, ref_g), f"offspring differ at iteration {it['it']}"
             ref_sc = _scores_from_trace(it["scores"])
+            # device scores of the same lanes: 1e-9, counts exact off the knife edge
             mine = ctx.evaluate_arrays(got_g, 3, 2)
-            fin = np.isfinite(ref_sc.fitness)
-            assert np.array_equal(np.isfinite(mine.fitness), fin)
-            err = np.max(np.abs(mine.fitness[fin] - ref_sc.fitness[fin]) /
-                         np.maximum(1.0, np.abs(ref_sc.fitness[fin])), initial=0.0)
-            worst = max(worst, err)
+            compare_scores(mine, orc.evaluate(got_g, 3, 2, flows=True), 20, ctx.grid.branch_limit)
             sess.insert(got_g, ref_sc)
-        assert worst <= 1e-9
         snap = sess.fetch(final=True)
         got = [[e.cell, e.genome.action_slots + e.genome.disconnection_slots, e.score.fitness] for e in snap.entries]
         want = [[c, g, f] for c, g, f in trace["final"]]
