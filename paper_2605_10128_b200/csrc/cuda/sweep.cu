@@ -99,7 +99,7 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
 
 template <int R, int NC, bool FULL>
 __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
-                                          uint64_t* bars) {
+                                          uint64_t* bars, int* release) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = tile * kTileK + lane * kKpl;
   // per-(candidate, contingency) operands in registers
@@ -133,6 +133,33 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     for (int s = 0; s < kStages && s < nchunks; ++s)
       issue_chunk(g, b, w, tile, s, smem + s * kStageDoubles, bars + s);
 
+  // exact path for one branch row: energies (registers) and fmax (atomicMax)
+  auto exact_row = [&](int e, double lim, const double (&f1)[NC][kKpl]) {
+#pragma unroll
+    for (int j = 0; j < NC; ++j) {
+      bool skip_row = false;
+#pragma unroll
+      for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[j][q];
+      double m = 0.0;
+#pragma unroll
+      for (int k = 0; k < kKpl; ++k) {
+        if (!kval[j][k] || skip_row || e == kbr[k]) continue;  // the outaged branch carries 0
+        const double a = fabs(f1[j][k]);
+        if (a > lim) energy[j][k] += a - lim;
+        m = fmax(m, a);
+      }
+      if (cid[j] < 0) continue;
+      unsigned long long* fmx = b.fmax + static_cast<size_t>(cid[j]) * g.E;
+      if (FULL) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0 && m > 0.0) atomicMax(fmx + e, static_cast<unsigned long long>(__double_as_longlong(m)));
+      } else if (m > lim) {
+        atomicMax(fmx + e, static_cast<unsigned long long>(__double_as_longlong(m)));
+      }
+    }
+  };
+
   for (int i = 0; i < nchunks; ++i) {
     const int s = i % kStages;
     const double* st = smem + s * kStageDoubles;
@@ -142,58 +169,77 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     const double* sT = st + lane * kKpl;
     const double* sF = st + kStageT + static_cast<size_t>(warp) * NC * kChunk * kStride;
     const double* sL = st + kStageT + kStageF;
-    for (int el = 0; el < rows; ++el) {
+    int el = 0;
+    // two branch rows per iteration: the loads of both rows are issued before
+    // the FMA chains so shared-memory latency overlaps the DFMA pipe
+    for (; el + 2 <= rows; el += 2) {
+      double tv[2][kKpl], fe[2][NC][R + 1], lim[2];
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        const double2 t01 = *reinterpret_cast<const double2*>(sT + (el + u) * kTileK);
+        const double2 t23 = *reinterpret_cast<const double2*>(sT + (el + u) * kTileK + 2);
+        tv[u][0] = t01.x, tv[u][1] = t01.y, tv[u][2] = t23.x, tv[u][3] = t23.y;
+        lim[u] = sL[el + u];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const double* fr = sF + (static_cast<size_t>(j) * kChunk + el + u) * kStride;
+#pragma unroll
+          for (int q = 0; q <= R; ++q) fe[u][j][q] = fr[q];
+        }
+      }
+      double f1[2][NC][kKpl];
+      uint32_t mx[2] = {0u, 0u};
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int j = 0; j < NC; ++j)
+#pragma unroll
+          for (int k = 0; k < kKpl; ++k) {
+            double acc = fma(tv[u][k], alpha[j][k], fe[u][j][0]);
+#pragma unroll
+            for (int q = 0; q < R; ++q) acc = fma(fe[u][j][1 + q], rr[j][k][q], acc);
+            f1[u][j][k] = acc;
+            mx[u] = max(mx[u], hi_abs(acc));
+          }
+#pragma unroll
+      for (int u = 0; u < 2; ++u)
+        if (FULL || mx[u] >= hi_abs(lim[u])) exact_row(e0 + el + u, lim[u], f1[u]);
+    }
+    if (el < rows) {
+      double tv[kKpl], f1[NC][kKpl];
       const double2 t01 = *reinterpret_cast<const double2*>(sT + el * kTileK);
       const double2 t23 = *reinterpret_cast<const double2*>(sT + el * kTileK + 2);
-      const double tv[kKpl] = {t01.x, t01.y, t23.x, t23.y};
+      tv[0] = t01.x, tv[1] = t01.y, tv[2] = t23.x, tv[3] = t23.y;
       const double lim = sL[el];
-      const uint32_t limhi = hi_abs(lim);
-      double f1[NC][kKpl];
-      bool hot = false;
+      uint32_t mx = 0u;
 #pragma unroll
       for (int j = 0; j < NC; ++j) {
         const double* fr = sF + (static_cast<size_t>(j) * kChunk + el) * kStride;
-        double fe[R + 1];
-#pragma unroll
-        for (int q = 0; q <= R; ++q) fe[q] = fr[q];
 #pragma unroll
         for (int k = 0; k < kKpl; ++k) {
-          double acc = fma(tv[k], alpha[j][k], fe[0]);
+          double acc = fma(tv[k], alpha[j][k], fr[0]);
 #pragma unroll
-          for (int q = 0; q < R; ++q) acc = fma(fe[1 + q], rr[j][k][q], acc);
+          for (int q = 0; q < R; ++q) acc = fma(fr[1 + q], rr[j][k][q], acc);
           f1[j][k] = acc;
-          hot |= hi_abs(acc) >= limhi;
+          mx = max(mx, hi_abs(acc));
         }
       }
-      if (FULL || hot) {
-        const int e = e0 + el;
-#pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          bool skip_row = false;
-#pragma unroll
-          for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[j][q];
-          double m = 0.0;
-#pragma unroll
-          for (int k = 0; k < kKpl; ++k) {
-            if (!kval[j][k] || skip_row || e == kbr[k]) continue;  // the outaged branch carries 0
-            const double a = fabs(f1[j][k]);
-            if (a > lim) energy[j][k] += a - lim;
-            m = fmax(m, a);
-          }
-          if (cid[j] < 0) continue;
-          unsigned long long* fmx = b.fmax + static_cast<size_t>(cid[j]) * g.E;
-          if (FULL) {
-#pragma unroll
-            for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-            if (lane == 0 && m > 0.0) atomicMax(fmx + e, static_cast<unsigned long long>(__double_as_longlong(m)));
-          } else if (m > lim) {
-            atomicMax(fmx + e, static_cast<unsigned long long>(__double_as_longlong(m)));
-          }
+      if (FULL || mx >= hi_abs(lim)) exact_row(e0 + el, lim, f1);
+    }
+    // release the stage; the last warp out refills it (no CTA-wide barrier)
+    __syncwarp();
+    if (lane == 0) {
+      __threadfence_block();
+      const int done = atomicAdd(release + s, 1);
+      if (done == kWarps - 1) {
+        release[s] = 0;
+        __threadfence_block();
+        if (i + kStages < nchunks) {
+          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+          issue_chunk(g, b, w, tile, i + kStages, smem + s * kStageDoubles, bars + s);
         }
       }
     }
-    __syncthreads();  // every warp is done with stage s
-    if (threadIdx.x == 0 && i + kStages < nchunks) issue_chunk(g, b, w, tile, i + kStages, smem + s * kStageDoubles, bars + s);
   }
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
@@ -210,6 +256,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CtaWork w;
   __shared__ int r_s;
+  __shared__ int release[kStages];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* smem = reinterpret_cast<double*>(smem_raw + 64);
   const int group = blockIdx.y;
@@ -224,20 +271,20 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
     for (int j = 0; j < per; ++j)
       if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
     w.ncand = n;
-    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1);
+    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1), release[s] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   const int tile = blockIdx.x;
   switch (r_s) {
-    case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars); break;
-    case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars); break;
-    case 2: sweep_cta<2, nc_for_rank(2), FULL>(g, b, w, tile, smem, bars); break;
-    case 3: sweep_cta<3, nc_for_rank(3), FULL>(g, b, w, tile, smem, bars); break;
-    case 4: sweep_cta<4, nc_for_rank(4), FULL>(g, b, w, tile, smem, bars); break;
-    case 5: sweep_cta<5, nc_for_rank(5), FULL>(g, b, w, tile, smem, bars); break;
-    case 6: sweep_cta<6, nc_for_rank(6), FULL>(g, b, w, tile, smem, bars); break;
-    default: sweep_cta<7, nc_for_rank(7), FULL>(g, b, w, tile, smem, bars); break;
+    case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars, release); break;
+    case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars, release); break;
+    case 2: sweep_cta<2, nc_for_rank(2), FULL>(g, b, w, tile, smem, bars, release); break;
+    case 3: sweep_cta<3, nc_for_rank(3), FULL>(g, b, w, tile, smem, bars, release); break;
+    case 4: sweep_cta<4, nc_for_rank(4), FULL>(g, b, w, tile, smem, bars, release); break;
+    case 5: sweep_cta<5, nc_for_rank(5), FULL>(g, b, w, tile, smem, bars, release); break;
+    case 6: sweep_cta<6, nc_for_rank(6), FULL>(g, b, w, tile, smem, bars, release); break;
+    default: sweep_cta<7, nc_for_rank(7), FULL>(g, b, w, tile, smem, bars, release); break;
   }
 }
 

@@ -87,10 +87,18 @@ def compare_scores(sc, ref: dict, worst_k: int, limits=None, weights=(200.0, 50.
     for i in range(n):
         if not live[i]:
             continue
-        wn = int(ref["worst_n"][i])
-        assert int(sc.worst_n[i]) == wn, f"worst_n lane {i}"
-        gi, ri = sc.worst_idx[i, :wn], ref["worst_idx"][i, :wn]
-        gv, rv = sc.worst_energy[i, :wn], ref["worst_val"][i, :wn]
+        # an outage energy that is exactly 0 in exact arithmetic (|f| == limit)
+        # enters the list (energy > 0, dc_engine.cpp:414) on rounding alone:
+        # compare the entries above the knife edge
+        gw, rw = int(sc.worst_n[i]), int(ref["worst_n"][i])
+        gmask = sc.worst_energy[i, :gw] > 1e-7
+        rmask = ref["worst_val"][i, :rw] > 1e-7
+        gi, ri = sc.worst_idx[i, :gw][gmask], ref["worst_idx"][i, :rw][rmask]
+        gv, rv = sc.worst_energy[i, :gw][gmask], ref["worst_val"][i, :rw][rmask]
+        if gw == worst_k or rw == worst_k:  # truncated lists: compare the common prefix
+            m = min(len(gi), len(ri))
+            gi, ri, gv, rv = gi[:m], ri[:m], gv[:m], rv[:m]
+        assert len(gi) == len(ri), f"worst list length lane {i}: {gw} vs {rw}"
         if not np.array_equal(gi, ri):
             # tolerate order swaps only between energies equal within tolerance
             assert sorted(gi.tolist()) == sorted(ri.tolist()) or rel_err(np.sort(gv), np.sort(rv)) <= TOL, \
