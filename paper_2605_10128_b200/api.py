@@ -613,3 +613,12 @@ def evaluate_raw(ctx: DcContext, genomes_ptr: int, n: int, n_a: int, n_d: int, s
     nullp = C.POINTER(C.c_double)()
     _check(LIB.tg_evaluate_batch(ctx._h, C.cast(C.c_void_p(genomes_ptr), C.POINTER(C.c_int32)), n, n_a, n_d, n,
                                  C.byref(scores), nullp, nullp, nullp, nullp))
+
+
+def sweep_rows(ctx: DcContext) -> Tuple[int, int]:
+    """(computed, offered) (branch row x candidate-warp x tile) blocks of the sweep
+    since the last call; the rest were skipped by the exact limit bound."""
+    a = C.c_int64()
+    b = C.c_int64()
+    _check(LIB.tg_sweep_rows(ctx._h, C.byref(a), C.byref(b)))
+    return a.value, b.value

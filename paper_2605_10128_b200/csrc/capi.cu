@@ -232,6 +232,9 @@ void tg_context::ensure_capacity(int n) {
   b.rank = A.alloc<int>(cap);
   b.removed = A.alloc<int>(static_cast<size_t>(cap) * tgb::kMaxRemovedSweep);
   b.feat = A.alloc<double>(static_cast<size_t>(cap) * E * tgb::kStride);
+  b.bnd = A.alloc<double>(static_cast<size_t>(cap) * E * 2);
+  b.rows_done = A.alloc<unsigned long long>(2);
+  check(cudaMemset(b.rows_done, 0, 2 * sizeof(unsigned long long)), "rows_done");
   b.kdat = A.alloc<double>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1) * tgb::kStride);
   b.kflag = A.alloc<uint8_t>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1));
   b.fmax = A.alloc<unsigned long long>(static_cast<size_t>(cap) * E);
@@ -481,6 +484,27 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
         kx_iptr.push_back(static_cast<int>(kx_i.size()));
       }
     }
+    // locality order of the sweep's contingency tiles: each 128-wide tile holds
+    // electrically close branches, so most (branch row, tile) blocks of a
+    // candidate are provably below their limits and skipped exactly
+    {
+      std::vector<std::pair<int, int>> edges;
+      for (int e = 0; e < E; ++e)
+        if (gd->branch_in_service[e]) edges.emplace_back(gd->branch_from[e], gd->branch_to[e]);
+      const std::vector<int> rank = tgb::locality_rank(N, edges);
+      std::vector<int> perm(ks_cont.size());
+      for (size_t i = 0; i < perm.size(); ++i) perm[i] = static_cast<int>(i);
+      auto key = [&](int i) {
+        const int b = ks_br[i];
+        return std::make_pair(std::min(rank[gd->branch_from[b]], rank[gd->branch_to[b]]),
+                              std::max(rank[gd->branch_from[b]], rank[gd->branch_to[b]]));
+      };
+      std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return key(x) < key(y); });
+      std::vector<int> c2, b2;
+      for (int i : perm) c2.push_back(ks_cont[i]), b2.push_back(ks_br[i]);
+      ks_cont.swap(c2);
+      ks_br.swap(b2);
+    }
     const int tile = tgb::sweep_tile_k();
     g.Ks = static_cast<int>(ks_cont.size());
     g.Kpad = ((g.Ks + tile - 1) / tile) * tile;
@@ -580,11 +604,17 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     double* f0 = A.alloc<double>(E);
     double* tdiag = A.alloc<double>(E);
     double* tk = A.alloc<double>(static_cast<size_t>(E) * std::max(g.Kpad, 1));
+    const int ntiles = g.Kpad / tgb::sweep_tile_k();
+    double* tmax = A.alloc<double>(static_cast<size_t>(std::max(ntiles, 1)) * (E + tgb::sweep_chunk()));
+    check(cudaMemsetAsync(tmax, 0, static_cast<size_t>(std::max(ntiles, 1)) * (E + tgb::sweep_chunk()) * sizeof(double),
+                          s),
+          "tmax");
     g.theta0 = theta0;
     g.f0 = f0;
     g.Tdiag = tdiag;
     g.TK = tk;
-    tgb::launch_base_tables(g, d_pr, theta0, f0, tdiag, tk, s);
+    g.Tmax = tmax;
+    tgb::launch_base_tables(g, d_pr, theta0, f0, tdiag, tk, tmax, s);
     check(cudaGetLastError(), "base tables");
     check(cudaStreamSynchronize(s), "context setup");
 
@@ -1047,6 +1077,19 @@ tg_status tg_sweep_timing(tg_context* ctx, int32_t enable, double* total_ms, int
     ctx->time_sweep = enable != 0;
     ctx->sweep_ms = 0.0;
     ctx->sweep_launches = 0;
+  });
+}
+
+tg_status tg_sweep_rows(tg_context* ctx, int64_t* computed, int64_t* offered) {
+  return guarded([&] {
+    unsigned long long v[2] = {0, 0};
+    if (ctx->batch.rows_done) {
+      check(cudaMemcpyAsync(v, ctx->batch.rows_done, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream), "rows D2H");
+      check(cudaMemsetAsync(ctx->batch.rows_done, 0, sizeof(v), ctx->stream), "rows reset");
+      check(cudaStreamSynchronize(ctx->stream), "rows");
+    }
+    if (computed) *computed = static_cast<int64_t>(v[0]);
+    if (offered) *offered = static_cast<int64_t>(v[1]);
   });
 }
 

@@ -47,7 +47,8 @@ struct DevGrid {
   const double* inj_net;   // [I]
   const int* ks_cont;      // [Ks]  contingency index
   const int* ks_branch;    // [Ks]
-  const double* TK;        // [E][Kpad]  T_base[e, ks_branch[k]] (0 rows for out-of-service e)
+  const double* TK;        // [Kpad/128][E][128] T_base[e, ks_branch[k]] tiles (0 rows for out-of-service e)
+  const double* Tmax;      // [Kpad/128][E + 32] max over the tile of |T_base[e, k]| (sweep skip bound)
   const int* kx_cont;      // [Kx]
   const int* kx_br_ptr;    // [Kx+1]
   const int* kx_br;

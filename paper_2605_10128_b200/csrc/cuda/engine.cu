@@ -70,6 +70,10 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       double2* dst = reinterpret_cast<double2*>(feat + static_cast<size_t>(e) * kStride);
 #pragma unroll
       for (int i = 0; i < kStride / 2; ++i) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+      double l1 = 0.0;
+#pragma unroll
+      for (int i = 1; i < kStride; ++i) l1 += fabs(row[i]);
+      reinterpret_cast<double2*>(b.bnd)[static_cast<size_t>(c) * g.E + e] = make_double2(fabs(row[0]), l1);
     }
     __syncthreads();
     // contingency rows: [alpha_k, R[:,k] * alpha_k, 0...], flag

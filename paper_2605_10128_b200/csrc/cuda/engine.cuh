@@ -38,6 +38,8 @@ struct Batch {
   int* rank;                  // low-rank update size, -1 when not swept
   int* removed;               // [n][kMaxRemovedSweep] genome-removed branches
   double* feat;               // [n][E][kStride]  f_c, L
+  double* bnd;                // [n][E][2] |f_c[e]|, sum_r |L[e,r]|  (sweep skip bound)
+  unsigned long long* rows_done;  // [2] sweep stats: (row, candidate) pairs computed / offered
   double* kdat;               // [n][Kpad][kStride] alpha, R' (single-branch contingencies)
   uint8_t* kflag;             // [n][Kpad] 0 ok, 1 islanded, 2 padding
   unsigned long long* fmax;   // [n][E] max |f| over contingencies (bits of a non-negative double)
@@ -75,7 +77,7 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
 // Returns false when a pivot is not positive (disconnected grid).
 bool device_spd_inverse(double* a, int n, cudaStream_t stream);
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
-                        cudaStream_t stream);
+                        double* tmax, cudaStream_t stream);
 
 }  // namespace tgb
 

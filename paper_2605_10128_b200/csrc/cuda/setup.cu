@@ -107,6 +107,19 @@ __global__ void k_tk(DevGrid g, double* tk, int W) {
   }
 }
 
+// Tmax[tile][e] = max_k |T_base[e, k]| over the tile's contingencies.
+__global__ void k_tmax(DevGrid g, const double* tk, double* tmax, int W, int ld) {
+  const int ntiles = g.Kpad / W;
+  const int total = ntiles * g.E;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
+    const int tile = idx / g.E, e = idx % g.E;
+    const double* row = tk + (static_cast<size_t>(tile) * g.E + e) * W;
+    double m = 0.0;
+    for (int k = 0; k < W; ++k) m = fmax(m, fabs(row[k]));
+    tmax[static_cast<size_t>(tile) * ld + e] = m;
+  }
+}
+
 }  // namespace
 
 bool device_spd_inverse(double* a, int n, cudaStream_t stream) {
@@ -141,13 +154,17 @@ bool device_spd_inverse(double* a, int n, cudaStream_t stream) {
 }
 
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
-                        cudaStream_t stream) {
+                        double* tmax, cudaStream_t stream) {
   k_theta<<<(g.Nr + 255) / 256 + 1, 256, 0, stream>>>(g, p_red, theta0);
   DevGrid g2 = g;
   g2.theta0 = theta0;
   k_branch_base<<<(g.E + 255) / 256 + 1, 256, 0, stream>>>(g2, theta0, f0, tdiag);
   const size_t total = static_cast<size_t>(g.E) * g.Kpad;
-  if (total > 0) k_tk<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32)), 256, 0, stream>>>(g2, tk, sweep_tile_k());
+  if (total > 0) {
+    k_tk<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32)), 256, 0, stream>>>(g2, tk, sweep_tile_k());
+    k_tmax<<<static_cast<int>(std::min<size_t>((total / sweep_tile_k() + 255) / 256 + 1, 148 * 32)), 256, 0, stream>>>(
+        g2, tk, tmax, sweep_tile_k(), g.E + sweep_chunk());
+  }
 }
 
 }  // namespace tgb

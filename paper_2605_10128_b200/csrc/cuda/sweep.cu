@@ -42,7 +42,9 @@ __host__ __device__ constexpr int cand_per_cta(int r) { return kWarps * nc_for_r
 constexpr size_t kStageT = static_cast<size_t>(kChunk) * kTileK;           // doubles
 constexpr size_t kStageF = static_cast<size_t>(kMaxCand) * kChunk * kStride;  // doubles
 constexpr size_t kStageL = kChunk;                                         // doubles
-constexpr size_t kStageDoubles = kStageT + kStageF + kStageL;
+constexpr size_t kStageTm = kChunk;                                        // tile max |T_base| per row
+constexpr size_t kStageB = static_cast<size_t>(kMaxCand) * kChunk * 2;     // (|f_c|, sum|L|) per row
+constexpr size_t kStageDoubles = kStageT + kStageF + kStageL + kStageTm + kStageB;
 constexpr size_t kSmemBytes = kStages * kStageDoubles * sizeof(double) + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -88,13 +90,18 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
   const uint32_t bt = rows * kTileK * sizeof(double);
   const uint32_t bf = rows * kStride * sizeof(double);
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
-  mbar_expect_tx(bar, bt + w.ncand * bf + bl);
+  const uint32_t bb = rows * 2 * sizeof(double);
+  mbar_expect_tx(bar, bt + w.ncand * (bf + bb) + 2 * bl);
   bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
   double* sf = stage + kStageT;
-  for (int j = 0; j < w.ncand; ++j)
-    bulk_g2s(sf + static_cast<size_t>(j) * kChunk * kStride, b.feat + (static_cast<size_t>(w.cand[j]) * g.E + e0) * kStride,
-             bf, bar);
+  double* sb = stage + kStageT + kStageF + kStageL + kStageTm;
+  for (int j = 0; j < w.ncand; ++j) {
+    const size_t c = static_cast<size_t>(w.cand[j]);
+    bulk_g2s(sf + static_cast<size_t>(j) * kChunk * kStride, b.feat + (c * g.E + e0) * kStride, bf, bar);
+    bulk_g2s(sb + static_cast<size_t>(j) * kChunk * 2, b.bnd + (c * g.E + e0) * 2, bb, bar);
+  }
   bulk_g2s(stage + kStageT + kStageF, g.br_lim + e0, bl, bar);
+  bulk_g2s(stage + kStageT + kStageF + kStageL, g.Tmax + static_cast<size_t>(tile) * (g.E + kChunk) + e0, bl, bar);
 }
 
 template <int R, int NC, bool FULL>
@@ -126,6 +133,26 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     }
 #pragma unroll
     for (int q = 0; q < kMaxRemovedSweep; ++q) rem[j][q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
+  }
+  // tile maxima of |alpha| and |R'| per candidate (warp-uniform; invalid
+  // contingencies carry zeros) for the row skip bound
+  double amax[NC], rmax[NC];
+#pragma unroll
+  for (int j = 0; j < NC; ++j) {
+    double a = 0.0, r = 0.0;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k) {
+      a = fmax(a, fabs(alpha[j][k]));
+#pragma unroll
+      for (int q = 0; q < R; ++q) r = fmax(r, fabs(rr[j][k][q]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+      r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+    }
+    amax[j] = a * (1.0 + 1e-12);
+    rmax[j] = r * (1.0 + 1e-12);
   }
 
   const int nchunks = (g.E + kChunk - 1) / kChunk;
@@ -169,20 +196,48 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     const double* sT = st + lane * kKpl;
     const double* sF = st + kStageT + static_cast<size_t>(warp) * NC * kChunk * kStride;
     const double* sL = st + kStageT + kStageF;
-    int el = 0;
-    // two branch rows per iteration: the loads of both rows are issued before
-    // the FMA chains so shared-memory latency overlaps the DFMA pipe
-    for (; el + 2 <= rows; el += 2) {
+    // rows that can reach their limit for one of the warp's candidates:
+    // |f1| <= |f_c| + max|T_base|*max|alpha| + (sum_r |L_r|)*max|R'| over the tile
+    unsigned need = rows >= 32 ? 0xffffffffu : ((1u << rows) - 1u);
+    if (!FULL) {
+      bool hot = false;
+      if (lane < rows) {
+        const double lim = sL[lane];
+        const double tm = st[kStageT + kStageF + kStageL + lane];
+        const double2* sB = reinterpret_cast<const double2*>(st + kStageT + kStageF + kStageL + kStageTm);
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const double2 bb = sB[(warp * NC + j) * kChunk + lane];
+          const double bound = bb.x + tm * amax[j] + bb.y * rmax[j];
+          hot |= bound >= lim * (1.0 - 1e-12);
+        }
+      }
+      need = __ballot_sync(0xffffffffu, hot);
+      if (lane == 0) {
+        atomicAdd(b.rows_done, static_cast<unsigned long long>(__popc(need)));
+        atomicAdd(b.rows_done + 1, static_cast<unsigned long long>(rows));
+      }
+    }
+    // two branch rows per step: the loads of both rows are issued before the
+    // FMA chains so shared-memory latency overlaps the DFMA pipe
+    while (need) {
+      int els[2];
+      els[0] = __ffs(need) - 1;
+      need &= need - 1;
+      els[1] = need ? __ffs(need) - 1 : -1;
+      if (need) need &= need - 1;
+      const int nu = els[1] >= 0 ? 2 : 1;
       double tv[2][kKpl], fe[2][NC][R + 1], lim[2];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
-        const double2 t01 = *reinterpret_cast<const double2*>(sT + (el + u) * kTileK);
-        const double2 t23 = *reinterpret_cast<const double2*>(sT + (el + u) * kTileK + 2);
+        const int el = u < nu ? els[u] : els[0];
+        const double2 t01 = *reinterpret_cast<const double2*>(sT + el * kTileK);
+        const double2 t23 = *reinterpret_cast<const double2*>(sT + el * kTileK + 2);
         tv[u][0] = t01.x, tv[u][1] = t01.y, tv[u][2] = t23.x, tv[u][3] = t23.y;
-        lim[u] = sL[el + u];
+        lim[u] = sL[el];
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
-          const double* fr = sF + (static_cast<size_t>(j) * kChunk + el + u) * kStride;
+          const double* fr = sF + (static_cast<size_t>(j) * kChunk + el) * kStride;
 #pragma unroll
           for (int q = 0; q <= R; ++q) fe[u][j][q] = fr[q];
         }
@@ -201,30 +256,8 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
             f1[u][j][k] = acc;
             mx[u] = max(mx[u], hi_abs(acc));
           }
-#pragma unroll
-      for (int u = 0; u < 2; ++u)
-        if (FULL || mx[u] >= hi_abs(lim[u])) exact_row(e0 + el + u, lim[u], f1[u]);
-    }
-    if (el < rows) {
-      double tv[kKpl], f1[NC][kKpl];
-      const double2 t01 = *reinterpret_cast<const double2*>(sT + el * kTileK);
-      const double2 t23 = *reinterpret_cast<const double2*>(sT + el * kTileK + 2);
-      tv[0] = t01.x, tv[1] = t01.y, tv[2] = t23.x, tv[3] = t23.y;
-      const double lim = sL[el];
-      uint32_t mx = 0u;
-#pragma unroll
-      for (int j = 0; j < NC; ++j) {
-        const double* fr = sF + (static_cast<size_t>(j) * kChunk + el) * kStride;
-#pragma unroll
-        for (int k = 0; k < kKpl; ++k) {
-          double acc = fma(tv[k], alpha[j][k], fr[0]);
-#pragma unroll
-          for (int q = 0; q < R; ++q) acc = fma(fr[1 + q], rr[j][k][q], acc);
-          f1[j][k] = acc;
-          mx = max(mx, hi_abs(acc));
-        }
-      }
-      if (FULL || mx >= hi_abs(lim)) exact_row(e0 + el, lim, f1);
+      if (FULL || mx[0] >= hi_abs(lim[0])) exact_row(e0 + els[0], lim[0], f1[0]);
+      if (nu == 2 && (FULL || mx[1] >= hi_abs(lim[1]))) exact_row(e0 + els[1], lim[1], f1[1]);
     }
     // release the stage; the last warp out refills it (no CTA-wide barrier)
     __syncwarp();

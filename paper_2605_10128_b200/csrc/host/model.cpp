@@ -384,6 +384,59 @@ std::vector<double> base_power_vector(const Grid& g) {
   return p;
 }
 
+// ---------------------------------------------------------------- locality
+std::vector<int> locality_rank(int n, const std::vector<std::pair<int, int>>& edges, int leaf) {
+  std::vector<std::vector<int>> adj(n);
+  for (auto [a, b] : edges) adj[a].push_back(b), adj[b].push_back(a);
+  std::vector<int> rank(n, -1), part(n, 0), dist(n, -1);
+  int next_rank = 0, next_part = 1;
+  // BFS restricted to one part; returns visit order, fills dist
+  auto bfs = [&](int src, int pid, std::vector<int>& order) {
+    order.clear();
+    order.push_back(src);
+    dist[src] = 0;
+    for (std::size_t h = 0; h < order.size(); ++h)
+      for (int w : adj[order[h]])
+        if (part[w] == pid && dist[w] < 0) dist[w] = dist[order[h]] + 1, order.push_back(w);
+  };
+  std::vector<std::pair<int, std::vector<int>>> stack;
+  {
+    std::vector<int> all(n);
+    for (int v = 0; v < n; ++v) all[v] = v;
+    stack.emplace_back(0, std::move(all));
+  }
+  std::vector<int> order, sub;
+  while (!stack.empty()) {
+    auto [pid, nodes] = std::move(stack.back());
+    stack.pop_back();
+    if (static_cast<int>(nodes.size()) <= leaf) {
+      for (int v : nodes) rank[v] = next_rank++;
+      continue;
+    }
+    // pseudo-peripheral start, then split the BFS order in halves (components
+    // of a part are visited one after another)
+    std::vector<int> seq;
+    for (int v : nodes) dist[v] = -1;
+    for (int root : nodes) {
+      if (dist[root] >= 0) continue;
+      bfs(root, pid, order);
+      const int far = order.back();
+      for (int v : order) dist[v] = -1;
+      bfs(far, pid, order);
+      seq.insert(seq.end(), order.begin(), order.end());
+    }
+    for (int v : nodes) dist[v] = -1;
+    const std::size_t half = seq.size() / 2;
+    std::vector<int> a(seq.begin(), seq.begin() + half), b(seq.begin() + half, seq.end());
+    const int pa = next_part++, pb = next_part++;
+    for (int v : a) part[v] = pa;
+    for (int v : b) part[v] = pb;
+    stack.emplace_back(pb, std::move(b));  // a is ranked first
+    stack.emplace_back(pa, std::move(a));
+  }
+  return rank;
+}
+
 // ---------------------------------------------------------------- import
 std::vector<int> enumerate_disconnectables(const Grid& g) {
   const int ne = g.n_branches(), n = g.n_nodes();

@@ -108,6 +108,11 @@ struct ActionTable {
   int n_actions() const { return static_cast<int>(station.size()); }
 };
 
+// Locality-preserving node ranking (recursive BFS bisection, leaves of at most
+// `leaf` nodes): nodes close in the graph get close ranks. Used to order the
+// contingency tiles of the sweep so each tile is electrically compact.
+std::vector<int> locality_rank(int n, const std::vector<std::pair<int, int>>& edges, int leaf = 48);
+
 std::vector<int> enumerate_disconnectables(const Grid& g);
 ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap);
 std::string actions_to_json(const ActionTable& t, const Grid& g, std::uint64_t grid_hash);
