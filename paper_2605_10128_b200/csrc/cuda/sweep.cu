@@ -156,6 +156,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   }
 
   const int nchunks = (g.E + kChunk - 1) / kChunk;
+  unsigned rows_computed = 0, rows_offered = 0;  // skip statistics, one atomic per warp at the end
   if (threadIdx.x == 0)
     for (int s = 0; s < kStages && s < nchunks; ++s)
       issue_chunk(g, b, w, tile, s, smem + s * kStageDoubles, bars + s);
@@ -213,10 +214,8 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
         }
       }
       need = __ballot_sync(0xffffffffu, hot);
-      if (lane == 0) {
-        atomicAdd(b.rows_done, static_cast<unsigned long long>(__popc(need)));
-        atomicAdd(b.rows_done + 1, static_cast<unsigned long long>(rows));
-      }
+      rows_computed += __popc(need);
+      rows_offered += rows;
     }
     // two branch rows per step: the loads of both rows are issued before the
     // FMA chains so shared-memory latency overlaps the DFMA pipe
@@ -273,6 +272,10 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
         }
       }
     }
+  }
+  if (!FULL && lane == 0) {
+    atomicAdd(b.rows_done, static_cast<unsigned long long>(rows_computed));
+    atomicAdd(b.rows_done + 1, static_cast<unsigned long long>(rows_offered));
   }
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
