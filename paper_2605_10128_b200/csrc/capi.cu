@@ -231,8 +231,10 @@ void tg_context::ensure_capacity(int n) {
   b.status = A.alloc<int>(cap);
   b.rank = A.alloc<int>(cap);
   b.removed = A.alloc<int>(static_cast<size_t>(cap) * tgb::kMaxRemovedSweep);
-  b.feat = A.alloc<double>(static_cast<size_t>(cap) * E * tgb::kStride);
-  b.bnd = A.alloc<double>(static_cast<size_t>(cap) * E * 2);
+  b.nchunks = static_cast<int>((E + tgb::kChunkRows - 1) / tgb::kChunkRows);
+  b.feat = A.alloc<double>(static_cast<size_t>(tgb::max_sweep_groups(cap)) * b.nchunks * tgb::kGroupSlots *
+                           tgb::kChunkRows * tgb::kStride);
+  b.slot = A.alloc<int>(cap);
   b.rows_done = A.alloc<unsigned long long>(2);
   check(cudaMemset(b.rows_done, 0, 2 * sizeof(unsigned long long)), "rows_done");
   b.kdat = A.alloc<double>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1) * tgb::kStride);

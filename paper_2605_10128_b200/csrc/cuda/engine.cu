@@ -13,6 +13,28 @@ namespace {
 
 constexpr int kPrepThreads = 256;
 
+// ---------------------------------------------------------------- K2a analysis
+// Topology analysis only (one CTA per candidate, thread 0): rank of the
+// low-rank update and structural islanding, so the sweep's candidate groups can
+// be formed before the rows are written (k_prep writes straight into them).
+__global__ void __launch_bounds__(kPrepThreads) k_analyze(DevGrid g, Batch b, int n_a, int n_d) {
+  extern __shared__ uint32_t bits[];
+  __shared__ Topo t;
+  const int words = (g.E + 31) >> 5;
+  for (int c = blockIdx.x; c < b.n; c += gridDim.x) {
+    for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = 0u;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+      analyze(g, t, bits, bits + words, b.genomes + static_cast<size_t>(c) * (n_a + n_d), n_a, n_d, nullptr, 0,
+              nullptr, 0);
+      if (!t.islanded && t.ns + t.nv > kSweepRank) t.islanded = 2;
+      b.status[c] = t.islanded;
+      b.rank[c] = t.islanded ? -1 : t.ns + t.nv;
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- K2 prep
 // One CTA per candidate (grid-stride over candidates; Z scratch per CTA slot).
 __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch,
@@ -24,22 +46,13 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
   uint32_t* rm_bits = bits + words;
   double* zbuf = zscratch + static_cast<size_t>(blockIdx.x) * g.Nr * kStride;
   for (int c = blockIdx.x; c < b.n; c += gridDim.x) {
+    const int slot = b.slot[c];
+    if (slot < 0) continue;  // islanded (or over capacity) by the analysis: status already set
     for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = 0u;
     __syncthreads();
     const int* slots = b.genomes + static_cast<size_t>(c) * (n_a + n_d);
-    if (threadIdx.x == 0) {
-      analyze(g, t, mv_bits, rm_bits, slots, n_a, n_d, nullptr, 0, nullptr, 0);
-      if (!t.islanded && t.ns + t.nv > kSweepRank) t.islanded = 2;
-    }
+    if (threadIdx.x == 0) analyze(g, t, mv_bits, rm_bits, slots, n_a, n_d, nullptr, 0, nullptr, 0);
     __syncthreads();
-    if (t.islanded) {
-      if (threadIdx.x == 0) {
-        b.status[c] = t.islanded;
-        b.rank[c] = -1;
-      }
-      __syncthreads();
-      continue;
-    }
     build_z(g, t, zbuf, kStride);
     __syncthreads();
     if (threadIdx.x == 0) small_solve(g, t, zbuf, kStride);
@@ -53,8 +66,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       continue;
     }
     const int ns = t.ns, nv = t.nv, r = ns + nv;
-    // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0...]
-    double* feat = b.feat + static_cast<size_t>(c) * g.E * kStride;
+    // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0..., sum|L| in slot 7 when r <= 6]
     for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
       double phi[kMaxSplits], rho[kMaxCols];
       const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, kStride, e, phi, rho);
@@ -67,13 +79,15 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
         for (int q = 0; q < ns; ++q) row[1 + q] = be * phi[q];
         for (int m = 0; m < nv; ++m) row[1 + ns + m] = be * rho[m];
       }
-      double2* dst = reinterpret_cast<double2*>(feat + static_cast<size_t>(e) * kStride);
+      if (r < kStride - 1) {
+        double l1 = 0.0;
+#pragma unroll
+        for (int i = 1; i < kStride - 1; ++i) l1 += fabs(row[i]);
+        row[kStride - 1] = l1 * (1.0 + 1e-12);
+      }
+      double2* dst = reinterpret_cast<double2*>(b.feat + feat_index(slot, b.nchunks, e));
 #pragma unroll
       for (int i = 0; i < kStride / 2; ++i) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
-      double l1 = 0.0;
-#pragma unroll
-      for (int i = 1; i < kStride; ++i) l1 += fabs(row[i]);
-      reinterpret_cast<double2*>(b.bnd)[static_cast<size_t>(c) * g.E + e] = make_double2(fabs(row[0]), l1);
     }
     __syncthreads();
     // contingency rows: [alpha_k, R[:,k] * alpha_k, 0...], flag
@@ -116,7 +130,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
             }
             flag = stub ? 0 : 1;
           } else {
-            const double alpha = feat[static_cast<size_t>(beta) * kStride] / den;
+            const double alpha = b.feat[feat_index(slot, b.nchunks, beta)] / den;
             row[0] = alpha;
             for (int i = 0; i < r; ++i) row[1 + i] = rk[i] * alpha;
           }
@@ -286,7 +300,7 @@ __global__ void __launch_bounds__(256) k_finish(DevGrid g, Batch b, int n_a, int
     }
     return;
   }
-  const double* feat = b.feat + static_cast<size_t>(c) * g.E * kStride;
+  const int slot = b.slot[c];
   const unsigned long long* fm = b.fmax + static_cast<size_t>(c) * g.E;
   const unsigned long long* fb = b.fbus + static_cast<size_t>(c) * g.E;
   double so = 0.0, sb = 0.0;
@@ -296,7 +310,7 @@ __global__ void __launch_bounds__(256) k_finish(DevGrid g, Batch b, int n_a, int
     const double m = __longlong_as_double(static_cast<long long>(fm[e]));
     const double mb = __longlong_as_double(static_cast<long long>(fb[e]));
     if (m > lim) so += m - lim, ++nc;
-    if (fabs(feat[static_cast<size_t>(e) * kStride]) > lim) ++nc0;
+    if (fabs(b.feat[feat_index(slot, b.nchunks, e)]) > lim) ++nc0;
     if (mb > lim) sb += mb - lim;
   }
   int isl = 0;
@@ -385,7 +399,8 @@ __global__ void k_extract_base(DevGrid g, Batch b, double* out) {
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < total;
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t c = i / g.E;
-    out[i] = b.status[c] == 0 ? b.feat[i * kStride] : 0.0;
+    const int e = static_cast<int>(i % g.E);
+    out[i] = b.status[c] == 0 ? b.feat[feat_index(b.slot[c], b.nchunks, e)] : 0.0;
   }
 }
 
@@ -408,6 +423,9 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
   cudaMemsetAsync(b.energy, 0, static_cast<size_t>(b.n) * g.Kall * sizeof(double), stream);
   cudaMemsetAsync(b.isl_out, 0, b.n * sizeof(int), stream);
   cudaMemsetAsync(b.isl_bus, 0, b.n * sizeof(int), stream);
+  k_analyze<<<b.n < 4096 ? b.n : 4096, kPrepThreads, bits_bytes, stream>>>(g, b, n_a, n_d);
+  ++launched;
+  launch_bucket(b, stream, &launched);
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
   k_prep<<<prep_grid, kPrepThreads, bits_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots);
   ++launched;

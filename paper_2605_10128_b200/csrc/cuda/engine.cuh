@@ -9,6 +9,15 @@
 namespace tgb {
 
 constexpr int kMaxRemovedSweep = 4;  // genome disconnections skipped in the sweep (n_d <= 4)
+constexpr int kGroupSlots = 16;      // candidates per sweep CTA group (8 warps x 2)
+constexpr int kChunkRows = 32;       // branch rows per sweep pipeline stage
+
+// Row e of candidate c in the group-major candidate row array.
+__host__ __device__ inline size_t feat_index(int slot, int nchunks, int e) {
+  const int group = slot / kGroupSlots, pos = slot % kGroupSlots;
+  const int chunk = e / kChunkRows, row = e % kChunkRows;
+  return ((((static_cast<size_t>(group) * nchunks + chunk) * kGroupSlots + pos) * kChunkRows) + row) * kStride;
+}
 
 // Per-candidate scores, SoA (dc_engine.hpp:25-39).
 struct Scores {
@@ -37,8 +46,12 @@ struct Batch {
   int* status;                // 0 ok, 1 islanded, 2/3 capacity error
   int* rank;                  // low-rank update size, -1 when not swept
   int* removed;               // [n][kMaxRemovedSweep] genome-removed branches
-  double* feat;               // [n][E][kStride]  f_c, L
-  double* bnd;                // [n][E][2] |f_c[e]|, sum_r |L[e,r]|  (sweep skip bound)
+  // Candidate branch rows (f_c, L[0..r-1], pad, slot 7 = sum_r |L| for the skip
+  // bound) stored in the sweep's group-major layout so one pipeline stage of a
+  // sweep CTA is one contiguous block: [group][chunk][kGroupSlots][kChunkRows][kStride].
+  double* feat;
+  int* slot;                  // [n] group * kGroupSlots + position, -1 when not swept
+  int nchunks;                // ceil(E / kChunkRows)
   unsigned long long* rows_done;  // [2] sweep stats: (row, candidate) pairs computed / offered
   double* kdat;               // [n][Kpad][kStride] alpha, R' (single-branch contingencies)
   uint8_t* kflag;             // [n][Kpad] 0 ok, 1 islanded, 2 padding
@@ -71,6 +84,10 @@ int sweep_tile_k();
 int sweep_chunk();
 void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1,
                   int* launched);
+// Rank buckets -> sweep groups; assigns every swept candidate its row slot.
+void launch_bucket(Batch& b, cudaStream_t stream, int* launched);
+// Upper bound on sweep groups for n candidates (every rank bucket rounds up).
+inline int max_sweep_groups(int n) { return (n + 7) / 8 + kSweepRank + 1; }
 
 // Base factorization on the device (dc_engine.cpp:88-116, importer.cpp:358-401):
 // X = B_red^-1 by in-place Gauss-Jordan (B_red is SPD; no pivoting needed).

@@ -43,8 +43,8 @@ constexpr size_t kStageT = static_cast<size_t>(kChunk) * kTileK;           // do
 constexpr size_t kStageF = static_cast<size_t>(kMaxCand) * kChunk * kStride;  // doubles
 constexpr size_t kStageL = kChunk;                                         // doubles
 constexpr size_t kStageTm = kChunk;                                        // tile max |T_base| per row
-constexpr size_t kStageB = static_cast<size_t>(kMaxCand) * kChunk * 2;     // (|f_c|, sum|L|) per row
-constexpr size_t kStageDoubles = kStageT + kStageF + kStageL + kStageTm + kStageB;
+constexpr size_t kStageDoubles = kStageT + kStageF + kStageL + kStageTm;
+static_assert(kMaxCand == kGroupSlots && kChunk == kChunkRows, "sweep tiles must match the row layout");
 constexpr size_t kSmemBytes = kStages * kStageDoubles * sizeof(double) + 64;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
@@ -80,6 +80,7 @@ __device__ __forceinline__ uint32_t hi_abs(double x) {
 struct CtaWork {
   int cand[kMaxCand];
   int ncand;
+  int group;
 };
 
 // Producer: stage `s` <- chunk `i` (T tile rows, candidate rows, limits).
@@ -88,18 +89,11 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
   const int e0 = i * kChunk;
   const int rows = min(kChunk, g.E - e0);
   const uint32_t bt = rows * kTileK * sizeof(double);
-  const uint32_t bf = rows * kStride * sizeof(double);
+  const uint32_t bf = kStageF * sizeof(double);  // the group's rows of this chunk: one contiguous block
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
-  const uint32_t bb = rows * 2 * sizeof(double);
-  mbar_expect_tx(bar, bt + w.ncand * (bf + bb) + 2 * bl);
+  mbar_expect_tx(bar, bt + bf + 2 * bl);
   bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
-  double* sf = stage + kStageT;
-  double* sb = stage + kStageT + kStageF + kStageL + kStageTm;
-  for (int j = 0; j < w.ncand; ++j) {
-    const size_t c = static_cast<size_t>(w.cand[j]);
-    bulk_g2s(sf + static_cast<size_t>(j) * kChunk * kStride, b.feat + (c * g.E + e0) * kStride, bf, bar);
-    bulk_g2s(sb + static_cast<size_t>(j) * kChunk * 2, b.bnd + (c * g.E + e0) * 2, bb, bar);
-  }
+  bulk_g2s(stage + kStageT, b.feat + feat_index(w.group * kGroupSlots, b.nchunks, e0), bf, bar);
   bulk_g2s(stage + kStageT + kStageF, g.br_lim + e0, bl, bar);
   bulk_g2s(stage + kStageT + kStageF + kStageL, g.Tmax + static_cast<size_t>(tile) * (g.E + kChunk) + e0, bl, bar);
 }
@@ -120,6 +114,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   for (int j = 0; j < NC; ++j) {
     const int slot = warp * NC + j;
     cid[j] = slot < w.ncand ? w.cand[slot] : -1;
+    if (cid[j] >= 0 && b.status[cid[j]] != 0) cid[j] = -1;  // islanded by the small solve in k_prep
     const int c = cid[j] >= 0 ? cid[j] : w.cand[0];
     const double* kd = b.kdat + (static_cast<size_t>(c) * g.Kpad + kb) * kStride;
     const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad + kb;
@@ -200,16 +195,15 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     // rows that can reach their limit for one of the warp's candidates:
     // |f1| <= |f_c| + max|T_base|*max|alpha| + (sum_r |L_r|)*max|R'| over the tile
     unsigned need = rows >= 32 ? 0xffffffffu : ((1u << rows) - 1u);
-    if (!FULL) {
+    if (!FULL && R < kStride - 1) {  // slot kStride-1 carries sum|L| for r <= 6
       bool hot = false;
       if (lane < rows) {
         const double lim = sL[lane];
         const double tm = st[kStageT + kStageF + kStageL + lane];
-        const double2* sB = reinterpret_cast<const double2*>(st + kStageT + kStageF + kStageL + kStageTm);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
-          const double2 bb = sB[(warp * NC + j) * kChunk + lane];
-          const double bound = bb.x + tm * amax[j] + bb.y * rmax[j];
+          const double* fr = sF + (static_cast<size_t>(j) * kChunk + lane) * kStride;
+          const double bound = fabs(fr[0]) + tm * amax[j] + fr[kStride - 1] * rmax[j];
           hot |= bound >= lim * (1.0 - 1e-12);
         }
       }
@@ -307,6 +301,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
     for (int j = 0; j < per; ++j)
       if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
     w.ncand = n;
+    w.group = group;
     for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1), release[s] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
@@ -325,10 +320,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
 }
 
 // Stable per-rank lists of swept candidates; bucket r is cut into CTA groups
-// of cand_per_cta(r).
+// of cand_per_cta(r), and every swept candidate gets its row slot
+// (group * kGroupSlots + position) so k_prep writes straight into the layout
+// the sweep streams.
 __global__ void k_bucket(Batch b) {
   __shared__ int warp_tot[32];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+  for (int c = threadIdx.x; c < b.n; c += blockDim.x) b.slot[c] = -1;
+  __syncthreads();
   int base = 0, group_base = 0;
   for (int r = 0; r <= kSweepRank; ++r) {
     int running = 0;
@@ -343,7 +342,11 @@ __global__ void k_bucket(Batch b) {
         if (x < wid) off += warp_tot[x];
         tot += warp_tot[x];
       }
-      if (mine) b.wl_list[base + running + off + __popc(m & ((1u << lane) - 1))] = c;
+      if (mine) {
+        const int pos = running + off + __popc(m & ((1u << lane) - 1));
+        b.wl_list[base + pos] = c;
+        b.slot[c] = (group_base + pos / cand_per_cta(r)) * kGroupSlots + pos % cand_per_cta(r);
+      }
       running += tot;
       __syncthreads();
     }
@@ -371,16 +374,20 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     configured = true;
   }
-  k_bucket<<<1, 1024, 0, stream>>>(b);
   // group slots: every bucket rounds up to whole groups of >= kWarps candidates
-  dim3 grid(g.Kpad / kTileK, (b.n + kWarps - 1) / kWarps + kSweepRank + 1);
+  dim3 grid(g.Kpad / kTileK, max_sweep_groups(b.n));
   if (ev0) cudaEventRecord(ev0, stream);
   if (full)
     k_sweep<true><<<grid, kThreads, kSmemBytes, stream>>>(g, b);
   else
     k_sweep<false><<<grid, kThreads, kSmemBytes, stream>>>(g, b);
   if (ev1) cudaEventRecord(ev1, stream);
-  *launched += 2;
+  *launched += 1;
+}
+
+void launch_bucket(Batch& b, cudaStream_t stream, int* launched) {
+  k_bucket<<<1, 1024, 0, stream>>>(b);
+  *launched += 1;
 }
 
 }  // namespace tgb
