@@ -230,6 +230,8 @@ void tg_context::ensure_capacity(int n) {
   d_genomes = A.alloc<int>(static_cast<size_t>(cap) * tgb::kMaxSlots);
   b.status = A.alloc<int>(cap);
   b.rank = A.alloc<int>(cap);
+  b.topo = reinterpret_cast<tgb::TopoCore*>(A.alloc<uint8_t>(static_cast<size_t>(cap) * tgb::topo_core_bytes()));
+  b.tbits = A.alloc<uint32_t>(static_cast<size_t>(cap) * 2 * ((E + 31) / 32));
   b.removed = A.alloc<int>(static_cast<size_t>(cap) * tgb::kMaxRemovedSweep);
   b.nchunks = static_cast<int>((E + tgb::kChunkRows - 1) / tgb::kChunkRows);
   b.feat = A.alloc<double>(static_cast<size_t>(tgb::max_sweep_groups(cap)) * b.nchunks * tgb::kGroupSlots *
@@ -958,8 +960,8 @@ int enqueue_iteration(tg_context* ctx) {
   ctx->batch.params = ctx->params;
   int kernels = 0;
   tgb::launch_evaluate(ctx->g, ctx->batch, q.p.n_a, q.p.n_d, false, ctx->scratch, ctx->stream, &kernels);
-  tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, B, ctx->worst_k, true, ctx->stream);
-  return 1 + kernels + 2;
+  const int ins = tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, B, ctx->worst_k, true, ctx->stream);
+  return 1 + kernels + ins;
 }
 
 }  // namespace
@@ -980,8 +982,7 @@ tg_status tg_qd_begin(tg_context* ctx, const tg_qd_config* cfg) {
     tgb::launch_archive_reset(q, s);
     check(cudaMemsetAsync(ctx->d_genomes, 0xff, static_cast<size_t>(q.n_slots) * sizeof(int), s), "seed genome");
     ctx->run_batch(1, p.n_a, p.n_d, false);
-    tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, 1, ctx->worst_k, false, s);
-    ctx->launches += 2;
+    ctx->launches += tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, 1, ctx->worst_k, false, s);
     ctx->qd_evaluations = 1;
     ctx->qd_epoch = 0;
     // the whole iteration as one CUDA graph (no host round trip per generation)
@@ -1007,8 +1008,8 @@ tg_status tg_qd_step(tg_context* ctx, int32_t n_iters) {
       for (int i = 0; i < n_iters; ++i) {
         tgb::launch_offspring(ctx->g, q, ctx->d_genomes, ctx->stream);
         ctx->run_batch(q.p.batch, q.p.n_a, q.p.n_d, false);
-        tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, q.p.batch, ctx->worst_k, true, ctx->stream);
-        ctx->launches += 3;
+        ctx->launches += 1 + tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, q.p.batch, ctx->worst_k, true,
+                                                ctx->stream);
       }
       ctx->qd_evaluations += static_cast<int64_t>(n_iters) * q.p.batch;
       return;
@@ -1063,8 +1064,7 @@ tg_status tg_qd_insert(tg_context* ctx, const int32_t* genomes, const tg_scores*
     h2d(o.worst_n, sc->worst_n, n * sizeof(int));
     h2d(o.worst_idx, sc->worst_idx, static_cast<size_t>(n) * wk * sizeof(int));
     h2d(o.worst_val, sc->worst_energy, static_cast<size_t>(n) * wk * sizeof(double));
-    tgb::launch_insert(q, ctx->d_genomes, o, n, wk, true, s);
-    ctx->launches += 2;
+    ctx->launches += tgb::launch_insert(q, ctx->d_genomes, o, n, wk, true, s);
     ctx->qd_evaluations += n;
     check(cudaStreamSynchronize(s), "insert");
   });
@@ -1209,8 +1209,7 @@ tg_status tg_archive_replay(tg_context* ctx, const tg_qd_config* cfg, const int3
       h2d(o.worst_n, sc->worst_n ? sc->worst_n : zi.data(), n * sizeof(int));
       h2d(o.worst_idx, sc->worst_idx ? sc->worst_idx : zi.data(), zi.size() * sizeof(int));
       h2d(o.worst_val, sc->worst_energy ? sc->worst_energy : zw.data(), zw.size() * sizeof(double));
-      tgb::launch_insert(q, ctx->d_genomes, o, n, wk, false, s);
-      ctx->launches += 2;
+      ctx->launches += tgb::launch_insert(q, ctx->d_genomes, o, n, wk, false, s);
       if (inserted) check(cudaMemcpyAsync(inserted, q.inserted, n, cudaMemcpyDeviceToHost, s), "inserted D2H");
     }
     fetch_archive(ctx, 0, n, true);

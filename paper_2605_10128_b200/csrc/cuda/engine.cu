@@ -14,12 +14,16 @@ namespace {
 constexpr int kPrepThreads = 256;
 
 // ---------------------------------------------------------------- K2a analysis
-// Topology analysis only (one CTA per candidate, thread 0): rank of the
-// low-rank update and structural islanding, so the sweep's candidate groups can
-// be formed before the rows are written (k_prep writes straight into them).
-__global__ void __launch_bounds__(kPrepThreads) k_analyze(DevGrid g, Batch b, int n_a, int n_d) {
+// Topology analysis (one warp-sized CTA per candidate, thread 0 serial, so a
+// whole batch runs in one wave): rank of the low-rank update and structural
+// islanding, so the sweep's candidate groups can be formed before the rows are
+// written (k_prep writes straight into them). The analysis and its bitmaps are
+// stored for k_prep.
+constexpr int kAnalyzeThreads = 32;
+
+__global__ void __launch_bounds__(kAnalyzeThreads) k_analyze(DevGrid g, Batch b, int n_a, int n_d) {
   extern __shared__ uint32_t bits[];
-  __shared__ Topo t;
+  __shared__ TopoCore t;
   const int words = (g.E + 31) >> 5;
   for (int c = blockIdx.x; c < b.n; c += gridDim.x) {
     for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = 0u;
@@ -32,6 +36,12 @@ __global__ void __launch_bounds__(kPrepThreads) k_analyze(DevGrid g, Batch b, in
       b.rank[c] = t.islanded ? -1 : t.ns + t.nv;
     }
     __syncthreads();
+    if (!t.islanded) {
+      copy_block(b.topo + c, &t, sizeof(TopoCore), threadIdx.x, blockDim.x);
+      uint32_t* tb = b.tbits + static_cast<size_t>(c) * 2 * words;
+      for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) tb[i] = bits[i];
+    }
+    __syncthreads();
   }
 }
 
@@ -41,6 +51,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
                                                        int zslots) {
   extern __shared__ uint32_t bits[];
   __shared__ Topo t;
+  __shared__ double gram[kSweepRank * kSweepRank];
+  __shared__ double thv[kSweepRank];
   const int words = (g.E + 31) >> 5;
   uint32_t* mv_bits = bits;
   uint32_t* rm_bits = bits + words;
@@ -48,14 +60,15 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
   for (int c = blockIdx.x; c < b.n; c += gridDim.x) {
     const int slot = b.slot[c];
     if (slot < 0) continue;  // islanded (or over capacity) by the analysis: status already set
-    for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = 0u;
-    __syncthreads();
-    const int* slots = b.genomes + static_cast<size_t>(c) * (n_a + n_d);
-    if (threadIdx.x == 0) analyze(g, t, mv_bits, rm_bits, slots, n_a, n_d, nullptr, 0, nullptr, 0);
+    copy_block(static_cast<TopoCore*>(&t), b.topo + c, sizeof(TopoCore), threadIdx.x, blockDim.x);
+    const uint32_t* tb = b.tbits + static_cast<size_t>(c) * 2 * words;
+    for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = tb[i];
     __syncthreads();
     build_z(g, t, zbuf, kStride);
     __syncthreads();
-    if (threadIdx.x == 0) small_solve(g, t, zbuf, kStride);
+    gram_terms(g, t, zbuf, kStride, gram, kSweepRank, thv);
+    __syncthreads();
+    if (threadIdx.x == 0) small_solve(t, gram, kSweepRank, thv);
     __syncthreads();
     if (t.islanded) {
       if (threadIdx.x == 0) {
@@ -165,7 +178,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_special(DevGrid g, Batch b, in
   __shared__ int omit[kMaxPMod];
   __shared__ int n_extra, n_omit, skip;
   __shared__ double red_sum[kPrepThreads / 32];
-  __shared__ double red_max[kPrepThreads / 32];
+  __shared__ double gram[kMaxCols * kMaxCols];
+  __shared__ double thv[kMaxCols];
   const int words = (g.E + 31) >> 5;
   uint32_t* mv_bits = bits;
   uint32_t* rm_bits = bits + words;
@@ -221,7 +235,9 @@ __global__ void __launch_bounds__(kPrepThreads) k_special(DevGrid g, Batch b, in
     if (!t.islanded) {
       build_z(g, t, zbuf, kMaxCols);
       __syncthreads();
-      if (threadIdx.x == 0) small_solve(g, t, zbuf, kMaxCols);
+      gram_terms(g, t, zbuf, kMaxCols, gram, kMaxCols, thv);
+      __syncthreads();
+      if (threadIdx.x == 0) small_solve(t, gram, kMaxCols, thv);
       __syncthreads();
     }
     const bool is_bus = cs >= g.Kx;
@@ -260,7 +276,6 @@ __global__ void __launch_bounds__(kPrepThreads) k_special(DevGrid g, Batch b, in
         b.energy[static_cast<size_t>(c) * g.Kall + g.kx_cont[cs]] = s;
       }
     }
-    (void)red_max;
     __syncthreads();
   }
 }
@@ -412,6 +427,8 @@ __global__ void k_bits_to_double(const unsigned long long* in, double* out, size
 
 }  // namespace
 
+size_t topo_core_bytes() { return sizeof(TopoCore); }
+
 // ---------------------------------------------------------------- launcher
 void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
                      cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin, cudaEvent_t sweep_end) {
@@ -423,7 +440,12 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
   cudaMemsetAsync(b.energy, 0, static_cast<size_t>(b.n) * g.Kall * sizeof(double), stream);
   cudaMemsetAsync(b.isl_out, 0, b.n * sizeof(int), stream);
   cudaMemsetAsync(b.isl_bus, 0, b.n * sizeof(int), stream);
-  k_analyze<<<b.n < 4096 ? b.n : 4096, kPrepThreads, bits_bytes, stream>>>(g, b, n_a, n_d);
+  static bool carveout = false;
+  if (!carveout) {  // one wave of warp-sized analysis CTAs needs the full shared-memory carveout
+    cudaFuncSetAttribute(k_analyze, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
+    carveout = true;
+  }
+  k_analyze<<<b.n < 65535 ? b.n : 65535, kAnalyzeThreads, bits_bytes, stream>>>(g, b, n_a, n_d);
   ++launched;
   launch_bucket(b, stream, &launched);
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;

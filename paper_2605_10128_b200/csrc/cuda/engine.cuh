@@ -8,6 +8,9 @@
 
 namespace tgb {
 
+struct TopoCore;                     // topo.cuh
+size_t topo_core_bytes();
+
 constexpr int kMaxRemovedSweep = 4;  // genome disconnections skipped in the sweep (n_d <= 4)
 constexpr int kGroupSlots = 16;      // candidates per sweep CTA group (8 warps x 2)
 constexpr int kChunkRows = 32;       // branch rows per sweep pipeline stage
@@ -44,6 +47,8 @@ struct Batch {
   const int* genomes;         // [n][n_a+n_d]
   DcParams params;
   int* status;                // 0 ok, 1 islanded, 2/3 capacity error
+  TopoCore* topo;             // [n] topology analysis of k_analyze, reloaded by k_prep
+  uint32_t* tbits;            // [n][2 * words] moved / removed branch bitmaps of the analysis
   int* rank;                  // low-rank update size, -1 when not swept
   int* removed;               // [n][kMaxRemovedSweep] genome-removed branches
   // Candidate branch rows (f_c, L[0..r-1], pad, slot 7 = sum_r |L| for the skip

@@ -405,91 +405,135 @@ __device__ __forceinline__ int cell_of(const QdParams& p, int d, int s, int r) {
   return d + (p.d_max + 1) * (s + (p.s_max + 1) * r);
 }
 
+// Cell of every finite-fitness lane (-1 otherwise); clears the insert results.
+__global__ void k_lane_cell(QdParams p, Scores sc, int n, int* lane_cell, uint8_t* inserted) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= n) return;
+  const double f = sc.fitness[c];
+  lane_cell[c] = isfinite(f) ? cell_of(p, sc.lambda_d[c], sc.lambda_s[c], sc.lambda_r[c]) : -1;
+  inserted[c] = 0;
+}
+
+// Moves one archive field of a cell after the register-level insert: lane i
+// receives entry i from its source (old entry src >= 0 of the cell, or batch
+// lane -src-1). Old entries only move to higher positions, so every lane reads
+// its source before any lane writes.
+template <typename T>
+__device__ __forceinline__ void move_field(T* arr, const T* cand, size_t base, int width, bool moved, int src,
+                                           int lane) {
+  for (int k = 0; k < width; ++k) {
+    T v{};
+    if (moved) v = src >= 0 ? arr[(base + src) * width + k] : cand[static_cast<size_t>(-src - 1) * width + k];
+    __syncwarp();
+    if (moved) arr[(base + lane) * width + k] = v;
+  }
+  __syncwarp();
+}
+
 // One warp per cell replays Repertoire::insert (qd_optimizer.cpp:281-303) over
 // the batch in lane order; cells are independent, so this equals the
-// reference's sequential loop.
-__global__ void k_insert(QdParams p, Archive a, const int* genomes, Scores sc, int n, int worst_k, uint8_t* inserted) {
+// reference's sequential loop. Lane i of the warp holds entry i of the cell
+// (fitness, canonical key, source) in registers: the duplicate test, the
+// upper_bound position and the shift are warp votes and shuffles, and the
+// payload is written once at the end.
+__global__ void k_insert(QdParams p, Archive a, const int* genomes, Scores sc, const int* lane_cell, int n,
+                         int worst_k, uint8_t* inserted) {
   const int cell = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (cell >= p.cells) return;
   const int ns = p.n_a + p.n_d;
-  for (int c0 = 0; c0 < n; c0 += 32) {
-    const int c = c0 + lane;
-    bool mine = false;
-    if (c < n) {
-      const double f = sc.fitness[c];
-      const bool fin = isfinite(f);
-      mine = fin && cell_of(p, sc.lambda_d[c], sc.lambda_s[c], sc.lambda_r[c]) == cell;
-      if (!fin && cell == 0 && inserted) inserted[c] = 0;
+  const size_t base = static_cast<size_t>(cell) * p.cap;
+  int cnt = a.count[cell];
+  double efit = 0.0;
+  int ekey[kMaxSlots];
+  int esrc = lane;
+#pragma unroll
+  for (int k = 0; k < kMaxSlots; ++k) ekey[k] = -1;
+  if (lane < cnt) {
+    efit = a.fitness[base + lane];
+#pragma unroll
+    for (int k = 0; k < kMaxSlots; ++k)
+      if (k < ns) ekey[k] = a.key[(base + lane) * ns + k];
+  }
+  bool changed = false;
+  for (int c0 = 0; c0 < n; c0 += 128) {
+    int lc[4];
+#pragma unroll
+    for (int j = 0; j < 4; ++j) {
+      const int c = c0 + 32 * j + lane;
+      lc[j] = c < n ? lane_cell[c] : -1;
     }
-    unsigned m = __ballot_sync(0xffffffffu, mine);
-    while (m) {
-      const int bit = __ffs(m) - 1;
-      m &= m - 1;
-      if (lane == 0) {
-        const int cand = c0 + bit;
-        const int* gg = genomes + static_cast<size_t>(cand) * ns;
-        int key[kMaxSlots];
-        canonical_key(gg, p.n_a, p.n_d, key);
-        const double fit = sc.fitness[cand];
-        const int cnt = a.count[cell];
-        const size_t base = static_cast<size_t>(cell) * p.cap;
-        bool ok = true;
-        for (int i = 0; i < cnt && ok; ++i) {
-          bool same = true;
-          for (int k = 0; k < ns; ++k) same = same && a.key[(base + i) * ns + k] == key[k];
-          ok = !same;
-        }
-        if (ok && cnt >= p.cap && fit <= a.fitness[base + cnt - 1]) ok = false;
-        if (ok) {
-          int pos = 0;
-          while (pos < cnt && !(fit > a.fitness[base + pos])) ++pos;
-          const int last = cnt < p.cap ? cnt : p.cap - 1;
-          for (int i = last; i > pos; --i) {
-            const size_t dst = base + i, src = base + i - 1;
-            for (int k = 0; k < ns; ++k) {
-              a.genome[dst * ns + k] = a.genome[src * ns + k];
-              a.key[dst * ns + k] = a.key[src * ns + k];
-            }
-            a.fitness[dst] = a.fitness[src];
-            a.lambda_o[dst] = a.lambda_o[src];
-            a.lambda_c[dst] = a.lambda_c[src];
-            a.lambda_c0[dst] = a.lambda_c0[src];
-            a.lambda_b[dst] = a.lambda_b[src];
-            a.lambda_d[dst] = a.lambda_d[src];
-            a.lambda_s[dst] = a.lambda_s[src];
-            a.lambda_r[dst] = a.lambda_r[src];
-            a.worst_n[dst] = a.worst_n[src];
-            for (int k = 0; k < worst_k; ++k) {
-              a.worst_idx[dst * worst_k + k] = a.worst_idx[src * worst_k + k];
-              a.worst_val[dst * worst_k + k] = a.worst_val[src * worst_k + k];
-            }
-          }
-          const size_t at = base + pos;
-          for (int k = 0; k < ns; ++k) {
-            a.genome[at * ns + k] = gg[k];
-            a.key[at * ns + k] = key[k];
-          }
-          a.fitness[at] = fit;
-          a.lambda_o[at] = sc.lambda_o[cand];
-          a.lambda_c[at] = sc.lambda_c[cand];
-          a.lambda_c0[at] = sc.lambda_c0[cand];
-          a.lambda_b[at] = sc.lambda_b[cand];
-          a.lambda_d[at] = sc.lambda_d[cand];
-          a.lambda_s[at] = sc.lambda_s[cand];
-          a.lambda_r[at] = sc.lambda_r[cand];
-          a.worst_n[at] = sc.worst_n[cand];
-          for (int k = 0; k < worst_k; ++k) {
-            a.worst_idx[at * worst_k + k] = sc.worst_idx[static_cast<size_t>(cand) * worst_k + k];
-            a.worst_val[at * worst_k + k] = sc.worst_val[static_cast<size_t>(cand) * worst_k + k];
-          }
-          a.count[cell] = cnt < p.cap ? cnt + 1 : p.cap;
-        }
-        if (inserted) inserted[cand] = ok ? 1 : 0;
+#pragma unroll 1
+    for (int j = 0; j < 4; ++j) {
+      const bool mine = lc[j] == cell;
+      unsigned m = __ballot_sync(0xffffffffu, mine);
+      if (!m) continue;
+      const int cbase = c0 + 32 * j;
+      double cf = 0.0;
+      int ck[kMaxSlots];
+#pragma unroll
+      for (int k = 0; k < kMaxSlots; ++k) ck[k] = -1;
+      if (mine) {
+        cf = sc.fitness[cbase + lane];
+        canonical_key(genomes + static_cast<size_t>(cbase + lane) * ns, p.n_a, p.n_d, ck);
       }
-      __syncwarp();
+      while (m) {
+        const int bit = __ffs(m) - 1;
+        m &= m - 1;
+        const double fit = __shfl_sync(0xffffffffu, cf, bit);
+        int key[kMaxSlots];
+        bool same = lane < cnt;
+#pragma unroll
+        for (int k = 0; k < kMaxSlots; ++k) {
+          key[k] = __shfl_sync(0xffffffffu, ck[k], bit);
+          same = same && (k >= ns || ekey[k] == key[k]);
+        }
+        bool ok = !__any_sync(0xffffffffu, same);
+        const double worst = __shfl_sync(0xffffffffu, efit, cnt > 0 ? cnt - 1 : 0);
+        if (ok && cnt >= p.cap && fit <= worst) ok = false;
+        if (ok) {
+          const int pos = __popc(__ballot_sync(0xffffffffu, lane < cnt && !(fit > efit)));
+          const double uf = __shfl_up_sync(0xffffffffu, efit, 1);
+          const int us = __shfl_up_sync(0xffffffffu, esrc, 1);
+#pragma unroll
+          for (int k = 0; k < kMaxSlots; ++k) {
+            const int uk = __shfl_up_sync(0xffffffffu, ekey[k], 1);
+            if (lane > pos) ekey[k] = uk;
+            if (lane == pos) ekey[k] = key[k];
+          }
+          if (lane > pos) {
+            efit = uf;
+            esrc = us;
+          }
+          if (lane == pos) {
+            efit = fit;
+            esrc = -(cbase + bit) - 1;
+          }
+          cnt = cnt < p.cap ? cnt + 1 : p.cap;
+          changed = true;
+        }
+        if (lane == 0 && ok) inserted[cbase + bit] = 1;
+      }
     }
   }
+  if (!changed) return;
+  if (lane == 0) a.count[cell] = cnt;
+  const bool moved = lane < cnt && esrc != lane;
+  if (moved) {
+    a.fitness[base + lane] = efit;
+    for (int k = 0; k < ns; ++k) a.key[(base + lane) * ns + k] = ekey[k];
+  }
+  move_field(a.genome, genomes, base, ns, moved, esrc, lane);
+  move_field(a.lambda_o, sc.lambda_o, base, 1, moved, esrc, lane);
+  move_field(a.lambda_c, sc.lambda_c, base, 1, moved, esrc, lane);
+  move_field(a.lambda_c0, sc.lambda_c0, base, 1, moved, esrc, lane);
+  move_field(a.lambda_b, sc.lambda_b, base, 1, moved, esrc, lane);
+  move_field(a.lambda_d, sc.lambda_d, base, 1, moved, esrc, lane);
+  move_field(a.lambda_s, sc.lambda_s, base, 1, moved, esrc, lane);
+  move_field(a.lambda_r, sc.lambda_r, base, 1, moved, esrc, lane);
+  move_field(a.worst_n, sc.worst_n, base, 1, moved, esrc, lane);
+  move_field(a.worst_idx, sc.worst_idx, base, worst_k, moved, esrc, lane);
+  move_field(a.worst_val, sc.worst_val, base, worst_k, moved, esrc, lane);
 }
 
 // Exclusive prefix of cell counts (member order) and the iteration counter.
@@ -538,11 +582,15 @@ void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStre
   k_offspring<<<(q.p.batch + kThreads - 1) / kThreads, kThreads, 0, s>>>(g, q.p, q.a, genomes);
 }
 
-void launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
-                   cudaStream_t s) {
-  constexpr int kWarps = 8;
-  k_insert<<<(q.p.cells + kWarps - 1) / kWarps, 32 * kWarps, 0, s>>>(q.p, q.a, genomes, sc, n, worst_k, q.inserted);
+int launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
+                  cudaStream_t s) {
+  constexpr int kWarps = 4;
+  if (n <= 0) return 0;
+  k_lane_cell<<<(n + 255) / 256, 256, 0, s>>>(q.p, sc, n, q.lane_cell, q.inserted);
+  k_insert<<<(q.p.cells + kWarps - 1) / kWarps, 32 * kWarps, 0, s>>>(q.p, q.a, genomes, sc, q.lane_cell, n, worst_k,
+                                                                    q.inserted);
   k_archive_prefix<<<1, 256, 0, s>>>(q.p, q.a, advance_iter ? 1 : 0);
+  return 3;
 }
 
 void launch_mutate_lanes(const DevGrid& g, const QdState& q, const int* parents, const unsigned long long* seeds, int n,

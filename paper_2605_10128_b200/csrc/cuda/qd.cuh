@@ -58,8 +58,9 @@ struct QdState {
 // Kernels launched by the context (capi.cu).
 void launch_archive_reset(const QdState& q, cudaStream_t s);
 void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStream_t s);
-void launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
-                   cudaStream_t s);
+// Returns the number of kernels launched.
+int launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
+                  cudaStream_t s);
 void launch_mutate_lanes(const DevGrid& g, const QdState& q, const int* parents, const unsigned long long* seeds, int n,
                          int* children, cudaStream_t s);
 void launch_crossover_lanes(const DevGrid& g, const QdState& q, const int* p1, const int* p2,

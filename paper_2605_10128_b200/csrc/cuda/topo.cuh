@@ -24,7 +24,9 @@
 
 namespace tgb {
 
-struct Topo {
+// Result of the topology analysis (thread-serial, shared memory). k_analyze
+// stores it per candidate so k_prep reloads it with a cooperative copy.
+struct alignas(16) TopoCore {
   int islanded;
   int n_new;                        // non-empty action slots (new node index j)
   int action_of_new[kMaxSplits];
@@ -54,18 +56,28 @@ struct Topo {
   double W[kMaxSplits * kMaxSplits];
   double dinv[kMaxCols];            // 1/delta of V columns
   double ppsi[kMaxSplits];          // net injection moved to each live split
+  double thresh_scale;
+};
+
+struct Topo : TopoCore {
   // small-solve results
   double Sinv[kMaxSplits * kMaxSplits];
   double Y[kMaxSplits * kMaxCols];  // S^-1 Phi  (ns x nv), row-major
   double Cinv[kMaxCols * kMaxCols];
   double Rp[kMaxSplits + kMaxCols]; // [S^-1 phi_p ; -C^-1 rho_p]
-  double thresh_scale;
 };
+
+// Cooperative copy of a 16-byte aligned block by the threads [0, nthreads).
+__device__ __forceinline__ void copy_block(void* dst, const void* src, size_t bytes, int tid, int nthreads) {
+  uint4* d = static_cast<uint4*>(dst);
+  const uint4* q = static_cast<const uint4*>(src);
+  for (size_t i = tid; i < bytes / 16; i += nthreads) d[i] = q[i];
+}
 
 __device__ __forceinline__ bool bit_get(const uint32_t* bits, int i) { return (bits[i >> 5] >> (i & 31)) & 1u; }
 __device__ __forceinline__ void bit_set(uint32_t* bits, int i) { bits[i >> 5] |= 1u << (i & 31); }
 
-__device__ inline int moved_slot(const Topo& t, const uint32_t* mv_bits, int e) {
+__device__ inline int moved_slot(const TopoCore& t, const uint32_t* mv_bits, int e) {
   if (!bit_get(mv_bits, e)) return -1;
   for (int i = 0; i < t.nmv; ++i)
     if (t.mv_branch[i] == e) return i;
@@ -76,14 +88,14 @@ __device__ inline bool active_branch(const DevGrid& g, const uint32_t* rm_bits, 
   return g.br_on[e] && !bit_get(rm_bits, e);
 }
 
-__device__ inline bool omitted(const Topo& t, int inj) {
+__device__ inline bool omitted(const TopoCore& t, int inj) {
   for (int i = 0; i < t.nom; ++i)
     if (t.omit[i] == inj) return true;
   return false;
 }
 
 // Candidate endpoint ids: base node, or N + j for the new node of split j.
-__device__ inline int cand_end(const DevGrid& g, const Topo& t, const uint32_t* mv_bits, int e, bool from_end) {
+__device__ inline int cand_end(const DevGrid& g, const TopoCore& t, const uint32_t* mv_bits, int e, bool from_end) {
   const int s = moved_slot(t, mv_bits, e);
   if (s >= 0)
     for (int j = 0; j < t.n_new; ++j)
@@ -92,14 +104,14 @@ __device__ inline int cand_end(const DevGrid& g, const Topo& t, const uint32_t* 
 }
 
 // split j whose station node is v, or -1
-__device__ inline int split_at_node(const DevGrid& g, const Topo& t, int v) {
+__device__ inline int split_at_node(const DevGrid& g, const TopoCore& t, int v) {
   for (int j = 0; j < t.n_new; ++j)
     if (g.st_node[g.act_station[t.action_of_new[j]]] == v) return j;
   return -1;
 }
 
 // Live branches incident to a candidate node (base or new), optionally ignoring one branch.
-__device__ inline int cand_degree(const DevGrid& g, const Topo& t, const uint32_t* mv_bits, const uint32_t* rm_bits,
+__device__ inline int cand_degree(const DevGrid& g, const TopoCore& t, const uint32_t* mv_bits, const uint32_t* rm_bits,
                                   int node) {
   int deg = 0;
   if (node >= g.N) {
@@ -120,7 +132,7 @@ __device__ inline int cand_degree(const DevGrid& g, const Topo& t, const uint32_
   return deg;
 }
 
-__device__ inline bool inj_moved_to(const Topo& t, int inj, int* j_out) {
+__device__ inline bool inj_moved_to(const TopoCore& t, int inj, int* j_out) {
   for (int i = 0; i < t.ninj; ++i)
     if (t.inj_id[i] == inj) {
       *j_out = t.inj_new[i];
@@ -130,7 +142,7 @@ __device__ inline bool inj_moved_to(const Topo& t, int inj, int* j_out) {
 }
 
 // Nonzero, non-omitted injection at a candidate node.
-__device__ inline bool cand_hosts_injection(const DevGrid& g, const Topo& t, int node) {
+__device__ inline bool cand_hosts_injection(const DevGrid& g, const TopoCore& t, int node) {
   if (node >= g.N) {
     const int j = node - g.N;
     for (int i = 0; i < t.ninj; ++i)
@@ -148,7 +160,7 @@ __device__ inline bool cand_hosts_injection(const DevGrid& g, const Topo& t, int
 
 // Thread-0 analysis of one topology: genome slots plus an optional outage
 // (extra removed branches, omitted injections). Bitmaps must be zeroed.
-__device__ inline void analyze(const DevGrid& g, Topo& t, uint32_t* mv_bits, uint32_t* rm_bits, const int* slots,
+__device__ inline void analyze(const DevGrid& g, TopoCore& t, uint32_t* mv_bits, uint32_t* rm_bits, const int* slots,
                                int n_a, int n_d, const int* extra_rem, int n_extra, const int* omit_inj,
                                int n_omit) {
   t.islanded = 0;
@@ -366,7 +378,7 @@ __device__ inline bool small_inverse(double* a, int n, int ld, double scale, dou
 }
 
 // Z = X [U | V]: row v of Z at zrow (stride ldz), all threads of the block.
-__device__ inline void build_z(const DevGrid& g, const Topo& t, double* zbuf, int ldz) {
+__device__ inline void build_z(const DevGrid& g, const TopoCore& t, double* zbuf, int ldz) {
   const int ncol = t.ns + t.nv;
   for (int v = threadIdx.x; v < g.Nr; v += blockDim.x) {
     double* zr = zbuf + static_cast<size_t>(v) * ldz;
@@ -385,7 +397,7 @@ __device__ __forceinline__ double zget(const DevGrid& g, const double* zbuf, int
 }
 
 // column^T y for a Z column (y = Z[:, c2]) or a base vector
-__device__ inline double col_dot_z(const Topo& t, int c, const double* zbuf, int ldz, int c2) {
+__device__ inline double col_dot_z(const TopoCore& t, int c, const double* zbuf, int ldz, int c2) {
   double acc = 0.0;
   for (int p = t.col_ptr[c]; p < t.col_ptr[c + 1]; ++p)
     acc = fma(t.term_coef[p], zbuf[static_cast<size_t>(t.term_idx[p]) * ldz + c2], acc);
@@ -393,7 +405,7 @@ __device__ inline double col_dot_z(const Topo& t, int c, const double* zbuf, int
 }
 
 // theta' = theta0 + sum_omitted (-net_i) X[:, red(node_i)] at reduced index r
-__device__ inline double theta_mod(const DevGrid& g, const Topo& t, int r) {
+__device__ inline double theta_mod(const DevGrid& g, const TopoCore& t, int r) {
   double th = g.theta0[r];
   for (int i = 0; i < t.nom; ++i) {
     const int rv = g.red[g.inj_node[t.omit[i]]];
@@ -402,14 +414,32 @@ __device__ inline double theta_mod(const DevGrid& g, const Topo& t, int r) {
   return th;
 }
 
-// Thread-0 small solve after build_z (block-synchronized by the caller).
+// All threads of the block, after build_z: the Gram entries G = [U|V]^T Z
+// (ncol x ncol, row stride ldg) and th[c] = [U|V]_c^T theta'.
+__device__ inline void gram_terms(const DevGrid& g, const TopoCore& t, const double* zbuf, int ldz, double* G, int ldg,
+                                  double* th) {
+  const int ncol = t.ns + t.nv;
+  for (int i = threadIdx.x; i < ncol * ncol + ncol; i += blockDim.x) {
+    if (i < ncol * ncol) {
+      const int c = i / ncol, c2 = i % ncol;
+      G[c * ldg + c2] = col_dot_z(t, c, zbuf, ldz, c2);
+    } else {
+      const int c = i - ncol * ncol;
+      double acc = 0.0;
+      for (int p = t.col_ptr[c]; p < t.col_ptr[c + 1]; ++p) acc = fma(t.term_coef[p], theta_mod(g, t, t.term_idx[p]), acc);
+      th[c] = acc;
+    }
+  }
+}
+
+// Thread-0 small solve on the Gram entries (block-synchronized by the caller).
 // Sets t.islanded = 1 when S or C is singular.
-__device__ inline void small_solve(const DevGrid& g, Topo& t, const double* zbuf, int ldz) {
+__device__ inline void small_solve(Topo& t, const double* G, int ldg, const double* th) {
   const int ns = t.ns, nv = t.nv;
   constexpr double kRel = 1e-10;  // dc_engine.cpp:258 threshold
   double* S = t.Sinv;
   for (int q = 0; q < ns; ++q)
-    for (int q2 = 0; q2 < ns; ++q2) S[q * kMaxSplits + q2] = t.W[q * kMaxSplits + q2] - col_dot_z(t, q, zbuf, ldz, q2);
+    for (int q2 = 0; q2 < ns; ++q2) S[q * kMaxSplits + q2] = t.W[q * kMaxSplits + q2] - G[q * ldg + q2];
   // symmetrize against rounding (S is symmetric in exact arithmetic)
   for (int q = 0; q < ns; ++q)
     for (int q2 = q + 1; q2 < ns; ++q2) {
@@ -420,14 +450,11 @@ __device__ inline void small_solve(const DevGrid& g, Topo& t, const double* zbuf
     t.islanded = 1;
     return;
   }
-  // Phi = U^T X V (ns x nv);  Y = S^-1 Phi
-  double phi[kMaxSplits * kMaxCols];
-  for (int q = 0; q < ns; ++q)
-    for (int m = 0; m < nv; ++m) phi[q * kMaxCols + m] = col_dot_z(t, q, zbuf, ldz, ns + m);
+  // Phi = U^T X V (ns x nv) = G[q][ns + m];  Y = S^-1 Phi
   for (int q = 0; q < ns; ++q)
     for (int m = 0; m < nv; ++m) {
       double acc = 0.0;
-      for (int q2 = 0; q2 < ns; ++q2) acc += S[q * kMaxSplits + q2] * phi[q2 * kMaxCols + m];
+      for (int q2 = 0; q2 < ns; ++q2) acc += S[q * kMaxSplits + q2] * G[q2 * ldg + ns + m];
       t.Y[q * kMaxCols + m] = acc;
     }
   // C = Delta^-1 + V^T X V + Phi^T Y
@@ -435,8 +462,8 @@ __device__ inline void small_solve(const DevGrid& g, Topo& t, const double* zbuf
   double cscale = 0.0;
   for (int m = 0; m < nv; ++m) {
     for (int m2 = 0; m2 < nv; ++m2) {
-      double v = col_dot_z(t, ns + m, zbuf, ldz, ns + m2);
-      for (int q = 0; q < ns; ++q) v += phi[q * kMaxCols + m] * t.Y[q * kMaxCols + m2];
+      double v = G[(ns + m) * ldg + ns + m2];
+      for (int q = 0; q < ns; ++q) v += G[q * ldg + ns + m] * t.Y[q * kMaxCols + m2];
       C[m * kMaxCols + m2] = v + (m == m2 ? t.dinv[m] : 0.0);
     }
     cscale = fmax(cscale, fabs(t.dinv[m]));
@@ -453,12 +480,10 @@ __device__ inline void small_solve(const DevGrid& g, Topo& t, const double* zbuf
   // injection-side coefficients: phi_p = U^T theta' - p_psi, rho_p = V^T theta' + Y^T phi_p
   double php[kMaxSplits], rhp[kMaxCols];
   for (int c = 0; c < ns + nv; ++c) {
-    double acc = 0.0;
-    for (int p = t.col_ptr[c]; p < t.col_ptr[c + 1]; ++p) acc = fma(t.term_coef[p], theta_mod(g, t, t.term_idx[p]), acc);
     if (c < ns)
-      php[c] = acc - t.ppsi[c];
+      php[c] = th[c] - t.ppsi[c];
     else
-      rhp[c - ns] = acc;
+      rhp[c - ns] = th[c];
   }
   for (int m = 0; m < nv; ++m)
     for (int q = 0; q < ns; ++q) rhp[m] += t.Y[q * kMaxCols + m] * php[q];
@@ -498,7 +523,7 @@ __device__ inline bool branch_features(const DevGrid& g, const Topo& t, const ui
 }
 
 // Base flow of e under the (possibly omitted-injection) base injections.
-__device__ inline double base_flow_mod(const DevGrid& g, const Topo& t, int e) {
+__device__ inline double base_flow_mod(const DevGrid& g, const TopoCore& t, int e) {
   double f = g.f0[e];
   if (t.nom == 0) return f;
   const int rf = g.red[g.br_from[e]], rt = g.red[g.br_to[e]];
