@@ -241,16 +241,19 @@ def main():
         isl += int((r < 0).sum())
         flops += float(E) * Ks * float(np.sum(2.0 + 2.0 * live))
     sweep_ms, sweep_n = P.sweep_timing(ctx, False)
-    rows_done, rows_offered = P.sweep_rows(ctx)
+    rows_done, rows_offered, rows_overloaded, rows_partial = P.sweep_rows(ctx)
     torch.cuda.synchronize()
     avg_ms = sweep_ms / max(sweep_n, 1)
     computed_frac = rows_done / rows_offered if rows_offered else 1.0
+    partial_frac = rows_partial / rows_offered if rows_offered else 1.0
     dense_tflops = flops / n_prof / (avg_ms * 1e-3) / 1e12
-    # executed FP64 work: the exact bound skips (row, tile) blocks whose |f1|
-    # cannot reach the limit; the roofline counts only the blocks computed
-    achieved_tflops = dense_tflops * computed_frac
-    peak = P.fp64_peak_tflops(dev)
     mean_rank = float(flops / n_prof / (E * Ks) / B / 2.0 - 1.0) if B else 0.0
+    # executed FP64 work: blocks past the per-row bound run the first FMA
+    # (f_c + T alpha), blocks past the per-element bound also the R FMAs of L R';
+    # skipped work cannot change any score
+    executed_frac = ((partial_frac + computed_frac * mean_rank) / (1.0 + mean_rank)) if rows_offered else 1.0
+    achieved_tflops = dense_tflops * executed_frac
+    peak = P.fp64_peak_tflops(dev)
     traffic = None
     prof_json = os.path.join(ROOT, "profiles", "sweep_ncu_summary.json")
     if os.path.exists(prof_json):
@@ -319,14 +322,18 @@ def main():
                          "peak": peak, "unit": "TFLOP/s", "frac": achieved_tflops / peak if peak else None,
                          "traffic": traffic, "peak_source": "DFMA microbenchmark on this GPU in this run "
                                                             "(MEASURED_PEAKS.json has no FP64 figure)",
-                         "flops_per_launch": flops / n_prof * computed_frac, "avg_launch_ms": avg_ms,
+                         "flops_per_launch": flops / n_prof * executed_frac, "avg_launch_ms": avg_ms,
                          "dense_flops_per_launch": flops / n_prof, "dense_equivalent_tflops": dense_tflops,
-                         "computed_block_fraction": computed_frac,
-                         "skip": "exact bound |f_c|+max|T|max|alpha|+sum|L|max|R'| < limit per (row, 128-contingency "
-                                 "tile, candidate pair); skipped blocks cannot change any score",
+                         "computed_block_fraction": computed_frac, "first_fma_block_fraction": partial_frac,
+                         "executed_flop_fraction": executed_frac,
+                         "overloaded_block_fraction": rows_overloaded / rows_offered if rows_offered else 0.0,
+                         "skip": "two-stage exact bound per (row, 128-contingency tile, candidate pair): "
+                                 "|f_c|+max|T|max|alpha|+sum_q |L_q|max|R'_q| < limit skips the row; else "
+                                 "|f_c+T alpha|+sum_q |L_q|max|R'_q| < limit skips the R FMAs of L R'; skipped "
+                                 "work cannot change any score",
                          "mean_rank": mean_rank, "islanded_fraction": isl / (n_prof * B),
                          "algorithmic": "E*K_single*(2+2r) per non-islanded candidate (SURVEY.md 8(d)) times the "
-                                        "computed block fraction"},
+                                        "executed flop fraction"},
             "e2e": {"value": e2e_value, "unit": "topologies/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "call": "tg_evaluate_batch (DcContext::evaluate_batch) on pinned host buffers"},

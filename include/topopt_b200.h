@@ -240,9 +240,10 @@ void* tg_context_stream(tg_context* ctx);   /* the context's cudaStream_t (for c
 /* Enables/disables CUDA-event timing of the fused sweep on evaluate calls and
  * returns (then resets) the accumulated milliseconds and launch count. */
 tg_status tg_sweep_timing(tg_context* ctx, int32_t enable, double* total_ms, int64_t* launches);
-/* (branch row, candidate, contingency tile) blocks the sweep computed vs offered
- * since the last call (the rest were skipped by the exact |f1| < limit bound). */
-tg_status tg_sweep_rows(tg_context* ctx, int64_t* computed, int64_t* offered);
+/* (branch row, candidate pair, contingency tile) blocks of the sweep since the
+ * last call: offered, passing the per-row bound (first FMA computed), fully
+ * computed (passing the per-element bound), holding at least one overload. */
+tg_status tg_sweep_rows(tg_context* ctx, int64_t* computed, int64_t* offered, int64_t* overloaded, int64_t* partial);
 /* Low-rank update size of each candidate of the last evaluated batch (-1 = not swept). */
 tg_status tg_batch_ranks(tg_context* ctx, int32_t n, int32_t* ranks);
 /* Measured FP64 FMA throughput of `device` (TFLOP/s) from a DFMA microbenchmark. */

@@ -115,7 +115,7 @@ SIGNATURES = [
     ("tg_context_stream", C.c_void_p, [C.c_void_p]),
     ("tg_sweep_timing", C.c_int, [C.c_void_p, C.c_int32, f64p, i64p]),
     ("tg_batch_ranks", C.c_int, [C.c_void_p, C.c_int32, i32p]),
-    ("tg_sweep_rows", C.c_int, [C.c_void_p, i64p, i64p]),
+    ("tg_sweep_rows", C.c_int, [C.c_void_p, i64p, i64p, i64p, i64p]),
     ("tg_fp64_peak", C.c_int, [C.c_int, f64p]),
 ]
 

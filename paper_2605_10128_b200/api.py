@@ -615,10 +615,14 @@ def evaluate_raw(ctx: DcContext, genomes_ptr: int, n: int, n_a: int, n_d: int, s
                                  C.byref(scores), nullp, nullp, nullp, nullp))
 
 
-def sweep_rows(ctx: DcContext) -> Tuple[int, int]:
-    """(computed, offered) (branch row x candidate-warp x tile) blocks of the sweep
-    since the last call; the rest were skipped by the exact limit bound."""
+def sweep_rows(ctx: DcContext) -> Tuple[int, int, int, int]:
+    """(computed, offered, overloaded, partial) (branch row x candidate-warp x tile)
+    blocks of the sweep since the last call: `partial` passed the per-row bound
+    (first FMA computed), `computed` also passed the per-element bound (all
+    FMAs), `overloaded` took the exact (overload) path."""
     a = C.c_int64()
     b = C.c_int64()
-    _check(LIB.tg_sweep_rows(ctx._h, C.byref(a), C.byref(b)))
-    return a.value, b.value
+    o = C.c_int64()
+    p = C.c_int64()
+    _check(LIB.tg_sweep_rows(ctx._h, C.byref(a), C.byref(b), C.byref(o), C.byref(p)))
+    return a.value, b.value, o.value, p.value

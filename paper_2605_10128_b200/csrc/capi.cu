@@ -237,8 +237,8 @@ void tg_context::ensure_capacity(int n) {
   b.feat = A.alloc<double>(static_cast<size_t>(tgb::max_sweep_groups(cap)) * b.nchunks * tgb::kGroupSlots *
                            tgb::kChunkRows * tgb::kStride);
   b.slot = A.alloc<int>(cap);
-  b.rows_done = A.alloc<unsigned long long>(2);
-  check(cudaMemset(b.rows_done, 0, 2 * sizeof(unsigned long long)), "rows_done");
+  b.rows_done = A.alloc<unsigned long long>(4);
+  check(cudaMemset(b.rows_done, 0, 4 * sizeof(unsigned long long)), "rows_done");
   b.kdat = A.alloc<double>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1) * tgb::kStride);
   b.kflag = A.alloc<uint8_t>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1));
   b.fmax = A.alloc<unsigned long long>(static_cast<size_t>(cap) * E);
@@ -1082,9 +1082,9 @@ tg_status tg_sweep_timing(tg_context* ctx, int32_t enable, double* total_ms, int
   });
 }
 
-tg_status tg_sweep_rows(tg_context* ctx, int64_t* computed, int64_t* offered) {
+tg_status tg_sweep_rows(tg_context* ctx, int64_t* computed, int64_t* offered, int64_t* overloaded, int64_t* partial) {
   return guarded([&] {
-    unsigned long long v[2] = {0, 0};
+    unsigned long long v[4] = {0, 0, 0, 0};
     if (ctx->batch.rows_done) {
       check(cudaMemcpyAsync(v, ctx->batch.rows_done, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream), "rows D2H");
       check(cudaMemsetAsync(ctx->batch.rows_done, 0, sizeof(v), ctx->stream), "rows reset");
@@ -1092,6 +1092,8 @@ tg_status tg_sweep_rows(tg_context* ctx, int64_t* computed, int64_t* offered) {
     }
     if (computed) *computed = static_cast<int64_t>(v[0]);
     if (offered) *offered = static_cast<int64_t>(v[1]);
+    if (overloaded) *overloaded = static_cast<int64_t>(v[2]);
+    if (partial) *partial = static_cast<int64_t>(v[3]);
   });
 }
 

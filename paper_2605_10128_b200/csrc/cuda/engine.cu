@@ -79,7 +79,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       continue;
     }
     const int ns = t.ns, nv = t.nv, r = ns + nv;
-    // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0..., sum|L| in slot 7 when r <= 6]
+    // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0...]
     for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
       double phi[kMaxSplits], rho[kMaxCols];
       const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, kStride, e, phi, rho);
@@ -91,12 +91,6 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
         const double be = g.br_b[e];
         for (int q = 0; q < ns; ++q) row[1 + q] = be * phi[q];
         for (int m = 0; m < nv; ++m) row[1 + ns + m] = be * rho[m];
-      }
-      if (r < kStride - 1) {
-        double l1 = 0.0;
-#pragma unroll
-        for (int i = 1; i < kStride - 1; ++i) l1 += fabs(row[i]);
-        row[kStride - 1] = l1 * (1.0 + 1e-12);
       }
       double2* dst = reinterpret_cast<double2*>(b.feat + feat_index(slot, b.nchunks, e));
 #pragma unroll

@@ -51,13 +51,13 @@ struct Batch {
   uint32_t* tbits;            // [n][2 * words] moved / removed branch bitmaps of the analysis
   int* rank;                  // low-rank update size, -1 when not swept
   int* removed;               // [n][kMaxRemovedSweep] genome-removed branches
-  // Candidate branch rows (f_c, L[0..r-1], pad, slot 7 = sum_r |L| for the skip
-  // bound) stored in the sweep's group-major layout so one pipeline stage of a
-  // sweep CTA is one contiguous block: [group][chunk][kGroupSlots][kChunkRows][kStride].
+  // Candidate branch rows (f_c, L[0..r-1], 0 padding) stored in the sweep's
+  // group-major layout so one pipeline stage of a sweep CTA is one contiguous
+  // block: [group][chunk][kGroupSlots][kChunkRows][kStride].
   double* feat;
   int* slot;                  // [n] group * kGroupSlots + position, -1 when not swept
   int nchunks;                // ceil(E / kChunkRows)
-  unsigned long long* rows_done;  // [2] sweep stats: (row, candidate) pairs computed / offered
+  unsigned long long* rows_done;  // [4] sweep stats: blocks computed / offered / overloaded / first FMA only
   double* kdat;               // [n][Kpad][kStride] alpha, R' (single-branch contingencies)
   uint8_t* kflag;             // [n][Kpad] 0 ok, 1 islanded, 2 padding
   unsigned long long* fmax;   // [n][E] max |f| over contingencies (bits of a non-negative double)

@@ -17,8 +17,11 @@
 //   * each lane owns 4 contingencies: alpha / R' live in registers for the
 //     whole sweep; each warp processes NC candidates so one T load feeds NC
 //     candidates' FMAs;
-//   * per element: (1 + R) DFMA + a 2-op hi-word test; the exact path runs only
-//     where |f1| can exceed the limit.
+//   * two-stage exact skip: a per-row bound over the whole tile (no element
+//     work), then the exact first FMA f_c + T alpha per element with the L R'
+//     part bounded; only rows passing both run the remaining R DFMA per
+//     element and a 2-op hi-word test; the exact path runs only where |f1| can
+//     exceed the limit.
 #include <cstdint>
 
 #include "engine.cuh"
@@ -29,14 +32,14 @@ namespace {
 
 constexpr int kKpl = 4;                  // contingencies per lane
 constexpr int kTileK = 32 * kKpl;        // contingencies per CTA tile
-constexpr int kWarps = 8;
+constexpr int kWarps = 16;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kChunk = 32;               // branches per pipeline stage
 constexpr int kStages = 3;
-constexpr int kMaxCand = 2 * kWarps;     // candidates per CTA at NC = 2
+constexpr int kMaxCand = kWarps;         // one candidate per warp
 
 // candidates per warp for a given rank (register budget)
-__host__ __device__ constexpr int nc_for_rank(int r) { return r <= 5 ? 2 : 1; }
+__host__ __device__ constexpr int nc_for_rank(int) { return 1; }
 __host__ __device__ constexpr int cand_per_cta(int r) { return kWarps * nc_for_rank(r); }
 
 constexpr size_t kStageT = static_cast<size_t>(kChunk) * kTileK;           // doubles
@@ -100,7 +103,7 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
 
 template <int R, int NC, bool FULL>
 __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
-                                          uint64_t* bars, int* release) {
+                                          uint64_t* bars, int* release, double* rmax_s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = tile * kTileK + lane * kKpl;
   // per-(candidate, contingency) operands in registers
@@ -129,56 +132,64 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
 #pragma unroll
     for (int q = 0; q < kMaxRemovedSweep; ++q) rem[j][q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
   }
-  // tile maxima of |alpha| and |R'| per candidate (warp-uniform; invalid
-  // contingencies carry zeros) for the row skip bound
-  double amax[NC], rmax[NC];
+  // tile maxima of |alpha| and of each |R'_q| per candidate (warp-uniform;
+  // invalid contingencies carry zeros) for the row skip bound; the R' maxima
+  // live in shared memory as a row weight vector w[j][slot] (0 for f_c and
+  // padding) to spare registers
+  double amax[NC];
+  double* rms = rmax_s + warp * NC * kStride;
+  if (lane < NC * kStride) rms[lane] = 0.0;
+  __syncwarp();
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
-    double a = 0.0, r = 0.0;
+    double a = 0.0;
 #pragma unroll
-    for (int k = 0; k < kKpl; ++k) {
-      a = fmax(a, fabs(alpha[j][k]));
+    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[j][k]));
 #pragma unroll
-      for (int q = 0; q < R; ++q) r = fmax(r, fabs(rr[j][k][q]));
-    }
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-      r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
-    }
+    for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
     amax[j] = a * (1.0 + 1e-12);
-    rmax[j] = r * (1.0 + 1e-12);
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      double r = 0.0;
+#pragma unroll
+      for (int k = 0; k < kKpl; ++k) r = fmax(r, fabs(rr[j][k][q]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+      if (lane == 0) rms[j * kStride + 1 + q] = r * (1.0 + 1e-12);
+    }
   }
+  __syncwarp();
 
   const int nchunks = (g.E + kChunk - 1) / kChunk;
-  unsigned rows_computed = 0, rows_offered = 0;  // skip statistics, one atomic per warp at the end
+  unsigned rows_computed = 0, rows_offered = 0, rows_exact = 0, rows_partial = 0;  // skip statistics, one atomic per warp at the end
   if (threadIdx.x == 0)
     for (int s = 0; s < kStages && s < nchunks; ++s)
       issue_chunk(g, b, w, tile, s, smem + s * kStageDoubles, bars + s);
 
   // exact path for one branch row: energies (registers) and fmax (atomicMax)
   auto exact_row = [&](int e, double lim, const double (&f1)[NC][kKpl]) {
+    const unsigned long long lim_bits = static_cast<unsigned long long>(__double_as_longlong(lim));
 #pragma unroll
     for (int j = 0; j < NC; ++j) {
       bool skip_row = false;
 #pragma unroll
       for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[j][q];
-      double m = 0.0;
+      unsigned long long m = 0ull;  // max |f1| as the ordered bit pattern of a non-negative double
 #pragma unroll
       for (int k = 0; k < kKpl; ++k) {
         if (!kval[j][k] || skip_row || e == kbr[k]) continue;  // the outaged branch carries 0
         const double a = fabs(f1[j][k]);
         if (a > lim) energy[j][k] += a - lim;
-        m = fmax(m, a);
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
       }
       if (cid[j] < 0) continue;
       unsigned long long* fmx = b.fmax + static_cast<size_t>(cid[j]) * g.E;
       if (FULL) {
 #pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0 && m > 0.0) atomicMax(fmx + e, static_cast<unsigned long long>(__double_as_longlong(m)));
-      } else if (m > lim) {
-        atomicMax(fmx + e, static_cast<unsigned long long>(__double_as_longlong(m)));
+        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+        if (lane == 0 && m > 0ull) atomicMax(fmx + e, m);
+      } else if (m > lim_bits) {
+        atomicMax(fmx + e, m);
       }
     }
   };
@@ -192,27 +203,49 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     const double* sT = st + lane * kKpl;
     const double* sF = st + kStageT + static_cast<size_t>(warp) * NC * kChunk * kStride;
     const double* sL = st + kStageT + kStageF;
-    // rows that can reach their limit for one of the warp's candidates:
-    // |f1| <= |f_c| + max|T_base|*max|alpha| + (sum_r |L_r|)*max|R'| over the tile
+    // Stage 1 (one lane per row): rows that can reach their limit for one of
+    // the warp's candidates,
+    //   |f1| <= |f_c| + max|T_base| max|alpha| + lrb,  lrb = sum_q |L_q| max|R'_q|
+    // over the tile. For stage 2 each lane keeps, per candidate, the high word
+    // of lim (1 - 1e-12) - lrb (0 when that is not positive).
     unsigned need = rows >= 32 ? 0xffffffffu : ((1u << rows) - 1u);
-    if (!FULL && R < kStride - 1) {  // slot kStride-1 carries sum|L| for r <= 6
+    uint32_t thr_lane[NC];
+#pragma unroll
+    for (int j = 0; j < NC; ++j) thr_lane[j] = 0u;
+    if (!FULL) {
       bool hot = false;
       if (lane < rows) {
-        const double lim = sL[lane];
+        const double lim = sL[lane] * (1.0 - 1e-12);
         const double tm = st[kStageT + kStageF + kStageL + lane];
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
-          const double* fr = sF + (static_cast<size_t>(j) * kChunk + lane) * kStride;
-          const double bound = fabs(fr[0]) + tm * amax[j] + fr[kStride - 1] * rmax[j];
-          hot |= bound >= lim * (1.0 - 1e-12);
+          // the row's 4 double2 read in a lane-rotated order (conflict-free),
+          // each weighted by its slots' R' maxima
+          const double2* fr = reinterpret_cast<const double2*>(sF + (static_cast<size_t>(j) * kChunk + lane) * kStride);
+          const double2* wr = reinterpret_cast<const double2*>(rms + j * kStride);
+          double lrb = 0.0, fca = 0.0;
+#pragma unroll
+          for (int i = 0; i < kStride / 2; ++i) {
+            const int idx = (i + (lane >> 1)) & (kStride / 2 - 1);
+            const double2 p2 = fr[idx];
+            const double2 w2 = wr[idx];
+            lrb = fma(fabs(p2.x), w2.x, lrb);
+            lrb = fma(fabs(p2.y), w2.y, lrb);
+            fca = idx == 0 ? fabs(p2.x) : fca;
+          }
+          const double thr = lim - lrb;
+          thr_lane[j] = thr > 0.0 ? hi_abs(thr) : 0u;
+          hot |= fma(tm, amax[j], fca) + lrb >= lim;
         }
       }
       need = __ballot_sync(0xffffffffu, hot);
-      rows_computed += __popc(need);
+      rows_partial += __popc(need);
       rows_offered += rows;
     }
-    // two branch rows per step: the loads of both rows are issued before the
-    // FMA chains so shared-memory latency overlaps the DFMA pipe
+    // Stage 2 (two rows per step, loads issued before the FMA chains): the
+    // first FMA f_c + T alpha of every element is exact; the row goes on to the
+    // remaining R FMAs only when |f_c + T alpha| can reach lim - lrb (tested on
+    // high words: hi(|x|) < hi(t) implies |x| < t for non-negative t).
     while (need) {
       int els[2];
       els[0] = __ffs(need) - 1;
@@ -220,7 +253,8 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       els[1] = need ? __ffs(need) - 1 : -1;
       if (need) need &= need - 1;
       const int nu = els[1] >= 0 ? 2 : 1;
-      double tv[2][kKpl], fe[2][NC][R + 1], lim[2];
+      double tv[2][kKpl], fc[2][NC], lim[2];
+      uint32_t thr[2][NC];
 #pragma unroll
       for (int u = 0; u < 2; ++u) {
         const int el = u < nu ? els[u] : els[0];
@@ -230,27 +264,56 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
         lim[u] = sL[el];
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
-          const double* fr = sF + (static_cast<size_t>(j) * kChunk + el) * kStride;
-#pragma unroll
-          for (int q = 0; q <= R; ++q) fe[u][j][q] = fr[q];
+          fc[u][j] = sF[(static_cast<size_t>(j) * kChunk + el) * kStride];
+          thr[u][j] = __shfl_sync(0xffffffffu, thr_lane[j], el);
         }
       }
       double f1[2][NC][kKpl];
-      uint32_t mx[2] = {0u, 0u};
+      bool hot[2] = {FULL, FULL && nu == 2};
 #pragma unroll
       for (int u = 0; u < 2; ++u)
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          uint32_t m = 0u;
+#pragma unroll
+          for (int k = 0; k < kKpl; ++k) {
+            f1[u][j][k] = fma(tv[u][k], alpha[j][k], fc[u][j]);
+            m = max(m, hi_abs(f1[u][j][k]));
+          }
+          if (!FULL) hot[u] |= m >= thr[u][j];
+        }
+      if (!FULL) {
+        hot[0] = __any_sync(0xffffffffu, hot[0]);
+        hot[1] = __any_sync(0xffffffffu, hot[1]) && nu == 2;
+      }
+#pragma unroll
+      for (int u = 0; u < 2; ++u) {
+        if (!hot[u]) continue;
+        ++rows_computed;
+        const int el = els[u];
+        double fl[NC][R > 0 ? R : 1];
+#pragma unroll
+        for (int j = 0; j < NC; ++j) {
+          const double* fr = sF + (static_cast<size_t>(j) * kChunk + el) * kStride;
+#pragma unroll
+          for (int q = 0; q < R; ++q) fl[j][q] = fr[1 + q];
+        }
+        uint32_t mx = 0u;
 #pragma unroll
         for (int j = 0; j < NC; ++j)
 #pragma unroll
           for (int k = 0; k < kKpl; ++k) {
-            double acc = fma(tv[u][k], alpha[j][k], fe[u][j][0]);
+            double acc = f1[u][j][k];
 #pragma unroll
-            for (int q = 0; q < R; ++q) acc = fma(fe[u][j][1 + q], rr[j][k][q], acc);
+            for (int q = 0; q < R; ++q) acc = fma(fl[j][q], rr[j][k][q], acc);
             f1[u][j][k] = acc;
-            mx[u] = max(mx[u], hi_abs(acc));
+            mx = max(mx, hi_abs(acc));
           }
-      if (FULL || mx[0] >= hi_abs(lim[0])) exact_row(e0 + els[0], lim[0], f1[0]);
-      if (nu == 2 && (FULL || mx[1] >= hi_abs(lim[1]))) exact_row(e0 + els[1], lim[1], f1[1]);
+        if (FULL || mx >= hi_abs(lim[u])) {
+          exact_row(e0 + el, lim[u], f1[u]);
+          ++rows_exact;
+        }
+      }
     }
     // release the stage; the last warp out refills it (no CTA-wide barrier)
     __syncwarp();
@@ -270,6 +333,8 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   if (!FULL && lane == 0) {
     atomicAdd(b.rows_done, static_cast<unsigned long long>(rows_computed));
     atomicAdd(b.rows_done + 1, static_cast<unsigned long long>(rows_offered));
+    atomicAdd(b.rows_done + 2, static_cast<unsigned long long>(rows_exact));
+    atomicAdd(b.rows_done + 3, static_cast<unsigned long long>(rows_partial));
   }
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
@@ -287,6 +352,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
   __shared__ CtaWork w;
   __shared__ int r_s;
   __shared__ int release[kStages];
+  __shared__ __align__(16) double rmax_s[kWarps * kStride];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* smem = reinterpret_cast<double*>(smem_raw + 64);
   const int group = blockIdx.y;
@@ -308,14 +374,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
   __syncthreads();
   const int tile = blockIdx.x;
   switch (r_s) {
-    case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars, release); break;
-    case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars, release); break;
-    case 2: sweep_cta<2, nc_for_rank(2), FULL>(g, b, w, tile, smem, bars, release); break;
-    case 3: sweep_cta<3, nc_for_rank(3), FULL>(g, b, w, tile, smem, bars, release); break;
-    case 4: sweep_cta<4, nc_for_rank(4), FULL>(g, b, w, tile, smem, bars, release); break;
-    case 5: sweep_cta<5, nc_for_rank(5), FULL>(g, b, w, tile, smem, bars, release); break;
-    case 6: sweep_cta<6, nc_for_rank(6), FULL>(g, b, w, tile, smem, bars, release); break;
-    default: sweep_cta<7, nc_for_rank(7), FULL>(g, b, w, tile, smem, bars, release); break;
+    case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
+    case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
+    case 2: sweep_cta<2, nc_for_rank(2), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
+    case 3: sweep_cta<3, nc_for_rank(3), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
+    case 4: sweep_cta<4, nc_for_rank(4), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
+    case 5: sweep_cta<5, nc_for_rank(5), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
+    case 6: sweep_cta<6, nc_for_rank(6), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
+    default: sweep_cta<7, nc_for_rank(7), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
   }
 }
 
