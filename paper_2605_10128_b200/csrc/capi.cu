@@ -609,10 +609,9 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     double* tdiag = A.alloc<double>(E);
     double* tk = A.alloc<double>(static_cast<size_t>(E) * std::max(g.Kpad, 1));
     const int ntiles = g.Kpad / tgb::sweep_tile_k();
-    double* tmax = A.alloc<double>(static_cast<size_t>(std::max(ntiles, 1)) * (E + tgb::sweep_chunk()));
-    check(cudaMemsetAsync(tmax, 0, static_cast<size_t>(std::max(ntiles, 1)) * (E + tgb::sweep_chunk()) * sizeof(double),
-                          s),
-          "tmax");
+    const size_t tmax_n = static_cast<size_t>(std::max(ntiles, 1)) * (E + tgb::sweep_chunk()) * tgb::kTmaxSub;
+    double* tmax = A.alloc<double>(tmax_n);
+    check(cudaMemsetAsync(tmax, 0, tmax_n * sizeof(double), s), "tmax");
     g.theta0 = theta0;
     g.f0 = f0;
     g.Tdiag = tdiag;

@@ -107,16 +107,19 @@ __global__ void k_tk(DevGrid g, double* tk, int W) {
   }
 }
 
-// Tmax[tile][e] = max_k |T_base[e, k]| over the tile's contingencies.
+// Tmax[tile][e][s] = max_k |T_base[e, k]| over sub-tile s of the tile's contingencies.
 __global__ void k_tmax(DevGrid g, const double* tk, double* tmax, int W, int ld) {
   const int ntiles = g.Kpad / W;
   const int total = ntiles * g.E;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const int tile = idx / g.E, e = idx % g.E;
     const double* row = tk + (static_cast<size_t>(tile) * g.E + e) * W;
-    double m = 0.0;
-    for (int k = 0; k < W; ++k) m = fmax(m, fabs(row[k]));
-    tmax[static_cast<size_t>(tile) * ld + e] = m;
+    const int sw = W / kTmaxSub;
+    for (int s = 0; s < kTmaxSub; ++s) {
+      double m = 0.0;
+      for (int k = s * sw; k < (s + 1) * sw; ++k) m = fmax(m, fabs(row[k]));
+      tmax[(static_cast<size_t>(tile) * ld + e) * kTmaxSub + s] = m;
+    }
   }
 }
 

@@ -45,7 +45,9 @@ __host__ __device__ constexpr int cand_per_cta(int r) { return kWarps * nc_for_r
 constexpr size_t kStageT = static_cast<size_t>(kChunk) * kTileK;           // doubles
 constexpr size_t kStageF = static_cast<size_t>(kMaxCand) * kChunk * kStride;  // doubles
 constexpr size_t kStageL = kChunk;                                         // doubles
-constexpr size_t kStageTm = kChunk;                                        // tile max |T_base| per row
+constexpr size_t kStageTm = static_cast<size_t>(kChunk) * kTmaxSub;       // sub-tile max |T_base| per row
+constexpr int kSubLanes = 32 / kTmaxSub;                                   // lanes per sub-tile
+static_assert(kTileK % kTmaxSub == 0 && kSubLanes * kTmaxSub == 32 && kTmaxSub == kStride, "sub-tile layout");
 constexpr size_t kStageDoubles = kStageT + kStageF + kStageL + kStageTm;
 static_assert(kMaxCand == kGroupSlots && kChunk == kChunkRows, "sweep tiles must match the row layout");
 constexpr size_t kSmemBytes = kStages * kStageDoubles * sizeof(double) + 64;
@@ -94,16 +96,18 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
   const uint32_t bt = rows * kTileK * sizeof(double);
   const uint32_t bf = kStageF * sizeof(double);  // the group's rows of this chunk: one contiguous block
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
-  mbar_expect_tx(bar, bt + bf + 2 * bl);
+  const uint32_t bm = rows * kTmaxSub * sizeof(double);
+  mbar_expect_tx(bar, bt + bf + bl + bm);
   bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
   bulk_g2s(stage + kStageT, b.feat + feat_index(w.group * kGroupSlots, b.nchunks, e0), bf, bar);
   bulk_g2s(stage + kStageT + kStageF, g.br_lim + e0, bl, bar);
-  bulk_g2s(stage + kStageT + kStageF + kStageL, g.Tmax + static_cast<size_t>(tile) * (g.E + kChunk) + e0, bl, bar);
+  bulk_g2s(stage + kStageT + kStageF + kStageL, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kTmaxSub,
+           bm, bar);
 }
 
 template <int R, int NC, bool FULL>
 __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
-                                          uint64_t* bars, int* release, double* rmax_s) {
+                                          uint64_t* bars, int* release, double* rmax_s, double* amax_s) {
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = tile * kTileK + lane * kKpl;
   // per-(candidate, contingency) operands in registers
@@ -132,12 +136,11 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
 #pragma unroll
     for (int q = 0; q < kMaxRemovedSweep; ++q) rem[j][q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
   }
-  // tile maxima of |alpha| and of each |R'_q| per candidate (warp-uniform;
-  // invalid contingencies carry zeros) for the row skip bound; the R' maxima
-  // live in shared memory as a row weight vector w[j][slot] (0 for f_c and
-  // padding) to spare registers
-  double amax[NC];
+  // Skip-bound operands in shared memory (invalid contingencies carry zeros):
+  // max |alpha| per sub-tile, asub[j][s], and the tile max of each |R'_q| as a
+  // row weight vector rms[j][slot] (0 for f_c and padding).
   double* rms = rmax_s + warp * NC * kStride;
+  double* asub = amax_s + warp * NC * kTmaxSub;
   if (lane < NC * kStride) rms[lane] = 0.0;
   __syncwarp();
 #pragma unroll
@@ -146,8 +149,8 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
 #pragma unroll
     for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[j][k]));
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-    amax[j] = a * (1.0 + 1e-12);
+    for (int o = kSubLanes / 2; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane % kSubLanes == 0) asub[j * kTmaxSub + lane / kSubLanes] = a * (1.0 + 1e-12);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       double r = 0.0;
@@ -205,8 +208,8 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     const double* sL = st + kStageT + kStageF;
     // Stage 1 (one lane per row): rows that can reach their limit for one of
     // the warp's candidates,
-    //   |f1| <= |f_c| + max|T_base| max|alpha| + lrb,  lrb = sum_q |L_q| max|R'_q|
-    // over the tile. For stage 2 each lane keeps, per candidate, the high word
+    //   |f1| <= |f_c| + max_s max|T_base|_s max|alpha|_s + lrb,  lrb = sum_q |L_q| max|R'_q|
+    // (s: sub-tiles; R' maxima over the tile). For stage 2 each lane keeps, per candidate, the high word
     // of lim (1 - 1e-12) - lrb (0 when that is not positive).
     unsigned need = rows >= 32 ? 0xffffffffu : ((1u << rows) - 1u);
     uint32_t thr_lane[NC];
@@ -216,26 +219,30 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       bool hot = false;
       if (lane < rows) {
         const double lim = sL[lane] * (1.0 - 1e-12);
-        const double tm = st[kStageT + kStageF + kStageL + lane];
+        const double2* tmr = reinterpret_cast<const double2*>(st + kStageT + kStageF + kStageL + lane * kTmaxSub);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
           // the row's 4 double2 read in a lane-rotated order (conflict-free),
           // each weighted by its slots' R' maxima
           const double2* fr = reinterpret_cast<const double2*>(sF + (static_cast<size_t>(j) * kChunk + lane) * kStride);
           const double2* wr = reinterpret_cast<const double2*>(rms + j * kStride);
-          double lrb = 0.0, fca = 0.0;
+          const double2* ar = reinterpret_cast<const double2*>(asub + j * kTmaxSub);
+          double lrb = 0.0, fca = 0.0, ta = 0.0;
 #pragma unroll
           for (int i = 0; i < kStride / 2; ++i) {
             const int idx = (i + (lane >> 1)) & (kStride / 2 - 1);
             const double2 p2 = fr[idx];
             const double2 w2 = wr[idx];
+            const double2 t2 = tmr[idx];
+            const double2 a2 = ar[idx];
             lrb = fma(fabs(p2.x), w2.x, lrb);
             lrb = fma(fabs(p2.y), w2.y, lrb);
             fca = idx == 0 ? fabs(p2.x) : fca;
+            ta = fmax(ta, fmax(t2.x * a2.x, t2.y * a2.y));
           }
           const double thr = lim - lrb;
           thr_lane[j] = thr > 0.0 ? hi_abs(thr) : 0u;
-          hot |= fma(tm, amax[j], fca) + lrb >= lim;
+          hot |= fca + ta + lrb >= lim;
         }
       }
       need = __ballot_sync(0xffffffffu, hot);
@@ -353,6 +360,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
   __shared__ int r_s;
   __shared__ int release[kStages];
   __shared__ __align__(16) double rmax_s[kWarps * kStride];
+  __shared__ __align__(16) double amax_s[kWarps * kTmaxSub];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* smem = reinterpret_cast<double*>(smem_raw + 64);
   const int group = blockIdx.y;
@@ -374,14 +382,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
   __syncthreads();
   const int tile = blockIdx.x;
   switch (r_s) {
-    case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
-    case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
-    case 2: sweep_cta<2, nc_for_rank(2), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
-    case 3: sweep_cta<3, nc_for_rank(3), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
-    case 4: sweep_cta<4, nc_for_rank(4), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
-    case 5: sweep_cta<5, nc_for_rank(5), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
-    case 6: sweep_cta<6, nc_for_rank(6), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
-    default: sweep_cta<7, nc_for_rank(7), FULL>(g, b, w, tile, smem, bars, release, rmax_s); break;
+    case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 2: sweep_cta<2, nc_for_rank(2), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 3: sweep_cta<3, nc_for_rank(3), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 4: sweep_cta<4, nc_for_rank(4), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 5: sweep_cta<5, nc_for_rank(5), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 6: sweep_cta<6, nc_for_rank(6), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    default: sweep_cta<7, nc_for_rank(7), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
   }
 }
 
