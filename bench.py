@@ -8,8 +8,9 @@ insert (qd_optimizer.cpp:376-401), launched as one CUDA graph.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg4|cfg1] [--impl b200|reference]
 
-Multi-GPU (torchrun): one island per rank (own seed, own archive), weak
-scaling, device time = max over ranks. --impl reference times the reference's
+Multi-GPU (torchrun): one island per rank (own seed, own archive), archives
+merged every --merge-every generations (NCCL allgather of the archive blobs +
+device merge kernel, islands.py), weak scaling, device time = max over ranks. --impl reference times the reference's
 CPU algorithm (the oracle restatement, oracle/, threaded like
 dc_engine.cpp:446-465) on this host on the same workload.
 """
@@ -169,6 +170,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--merge-every", type=int, default=1,
+                    help="island archive merge (NCCL allgather + device merge) every M generations when N>1; 0 = never")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
@@ -200,8 +203,26 @@ def main():
             import torch.distributed as dist
             dist.barrier()
 
+    ex = None
+    if world > 1 and args.merge_every > 0:
+        from paper_2605_10128_b200.islands import IslandExchange
+        ex = IslandExchange(sess)
+
+    def generations(n):
+        # n generations of this island; every merge_every-th one ends with the
+        # island exchange (pack -> NCCL allgather -> device merge, on the engine stream)
+        if ex is None:
+            sess.step(n)
+            return
+        for _ in range(n):
+            sess.step(1)
+            generations.count += 1
+            if generations.count % args.merge_every == 0:
+                ex.exchange()
+    generations.count = 0
+
     # warm-up generations
-    sess.step(args.warmup)
+    generations(args.warmup)
     torch.cuda.synchronize()
     barrier()
 
@@ -212,7 +233,7 @@ def main():
         torch.cuda.synchronize()
         barrier()
         e0.record(stream)
-        sess.step(args.steps)
+        generations(args.steps)
         e1.record(stream)
         torch.cuda.synchronize()
         barrier()
@@ -312,7 +333,9 @@ def main():
             "config": {"workload": CONFIGS[args.config]["workload"], "batch_per_gpu": B,
                        "n_nodes": info["n_nodes"], "n_branches": E, "n_contingencies": info["n_contingencies"],
                        "n_actions": info["n_actions"], "n_disconnectables": info["n_disconnectables"],
-                       "parallelism": f"islands x{world} (independent archives, seed 1+rank)",
+                       "parallelism": (f"islands x{world} (seed 1+rank), archives merged every {args.merge_every} "
+                                       "generation(s): NCCL allgather of archive blobs + device Repertoire merge"
+                                       if ex is not None else f"islands x{world} (seed 1+rank)"),
                        "l2": f"per-step candidate working set {work_bytes / 2**20:.0f} MiB > 126 MiB L2 "
                              "(no flush needed)",
                        "step": "one MapElites generation: mutate/crossover + full N-1 evaluation + archive insert",

@@ -225,6 +225,19 @@ tg_status tg_archive_export(tg_context* ctx, tg_snapshot_view* out);
  * inserted[n] (optional) receives Repertoire::insert's return value. */
 tg_status tg_archive_replay(tg_context* ctx, const tg_qd_config* cfg, const int32_t* genomes, int32_t n,
                             const tg_scores* scores, uint8_t* inserted);
+/* ---- island exchange (no reference counterpart: the reference runs one
+ * population, qd_optimizer.cpp:344-417; SURVEY.md 8(e) island mode) ----
+ * blob_bytes = size of one island's archive blob (fixed for a cfg; after
+ * tg_qd_begin). pack writes this archive into the DEVICE buffer d_blob, merge
+ * reads n_islands consecutive blobs from the DEVICE buffer d_blobs (e.g. the
+ * output of an NCCL allgather), clears the cells and re-inserts every entry in
+ * (island, cell, position) order with Repertoire::insert semantics
+ * (qd_optimizer.cpp:281-303): islands merging the same blobs end with
+ * identical archives. Both are enqueued on tg_context_stream(ctx); the caller
+ * orders its collective on that stream. The iteration counter is kept. */
+tg_status tg_archive_blob_bytes(tg_context* ctx, int64_t* bytes);
+tg_status tg_archive_pack(tg_context* ctx, void* d_blob);
+tg_status tg_archive_merge(tg_context* ctx, const void* d_blobs, int32_t n_islands);
 /* descriptor_to_cell, qd_optimizer.cpp:12-17 */
 int32_t tg_descriptor_to_cell(int32_t lambda_d, int32_t lambda_s, int32_t lambda_r, const tg_qd_config* cfg);
 /* Device mutation / crossover of single lanes with the reference RNG stream

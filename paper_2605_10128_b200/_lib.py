@@ -117,6 +117,9 @@ SIGNATURES = [
     ("tg_batch_ranks", C.c_int, [C.c_void_p, C.c_int32, i32p]),
     ("tg_sweep_rows", C.c_int, [C.c_void_p, i64p, i64p, i64p, i64p]),
     ("tg_fp64_peak", C.c_int, [C.c_int, f64p]),
+    ("tg_archive_blob_bytes", C.c_int, [C.c_void_p, i64p]),
+    ("tg_archive_pack", C.c_int, [C.c_void_p, C.c_void_p]),
+    ("tg_archive_merge", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
 ]
 
 

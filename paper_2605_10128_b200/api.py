@@ -581,6 +581,20 @@ class QdSession:
         _check(LIB.tg_qd_fetch(self.ctx._h, int(final), C.byref(view)))
         return _snapshot_from_view(view, self.cfg.n_a)
 
+    # ---- island exchange (islands.py drives these over torch.distributed)
+    def blob_bytes(self) -> int:
+        v = C.c_int64()
+        _check(LIB.tg_archive_blob_bytes(self.ctx._h, C.byref(v)))
+        return v.value
+
+    def pack(self, d_blob: int) -> None:
+        """Enqueue the archive -> island blob copy into device memory at d_blob."""
+        _check(LIB.tg_archive_pack(self.ctx._h, C.c_void_p(d_blob)))
+
+    def merge(self, d_blobs: int, n_islands: int) -> None:
+        """Enqueue the merge of n_islands consecutive device blobs into the archive."""
+        _check(LIB.tg_archive_merge(self.ctx._h, C.c_void_p(d_blobs), n_islands))
+
 
 def context_stream(ctx: DcContext) -> int:
     """cudaStream_t of the context (for caller-side CUDA events)."""

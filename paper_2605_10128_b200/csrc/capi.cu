@@ -208,6 +208,9 @@ struct tg_context {
   cudaEvent_t sw0 = nullptr, sw1 = nullptr;
   double sweep_ms = 0.0;
   int64_t sweep_launches = 0;
+  // island merge buffers (allocated on the first merge)
+  std::unique_ptr<DeviceArena> merge_arena;
+  tgb::MergeBuffers merge{};
   // step-wise optimizer state
   int64_t qd_evaluations = 0;
   int qd_epoch = 0;
@@ -831,6 +834,7 @@ void qd_setup(tg_context* ctx, const tgb::QdParams& p) {
     if (q && q->graph) cudaGraphExecDestroy(q->graph);
     delete static_cast<DeviceArena*>(q ? q->arena : nullptr);
     q = std::make_unique<tgb::QdState>();
+    ctx->merge.capacity = 0;  // merge buffers are sized for the old slot layout
     auto* A = new DeviceArena();
     q->arena = A;
     const size_t slots = static_cast<size_t>(p.cells) * p.cap;
@@ -1066,6 +1070,57 @@ tg_status tg_qd_insert(tg_context* ctx, const int32_t* genomes, const tg_scores*
     ctx->launches += tgb::launch_insert(q, ctx->d_genomes, o, n, wk, true, s);
     ctx->qd_evaluations += n;
     check(cudaStreamSynchronize(s), "insert");
+  });
+}
+
+tg_status tg_archive_blob_bytes(tg_context* ctx, int64_t* bytes) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    const tgb::QdState& q = *ctx->qd;
+    *bytes = static_cast<int64_t>(tgb::BlobLayout(q.p.cells * q.p.cap, q.n_slots, q.worst_k).total);
+  });
+}
+
+tg_status tg_archive_pack(tg_context* ctx, void* d_blob) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    if (!d_blob) throw tgb::ConfigError("null blob");
+    tgb::launch_archive_pack(*ctx->qd, d_blob, ctx->stream);
+    ctx->launches += 1;
+    check(cudaGetLastError(), "archive pack");
+  });
+}
+
+tg_status tg_archive_merge(tg_context* ctx, const void* d_blobs, int32_t n_islands) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    if (n_islands <= 0 || !d_blobs) throw tgb::ConfigError("merge needs at least one island blob");
+    tgb::QdState& q = *ctx->qd;
+    const int n = q.p.cells * q.p.cap * n_islands;
+    tgb::MergeBuffers& m = ctx->merge;
+    if (m.capacity < n) {
+      ctx->merge_arena = std::make_unique<DeviceArena>();
+      DeviceArena& A = *ctx->merge_arena;
+      const size_t wk = std::max(ctx->worst_k, 1);
+      m = tgb::MergeBuffers{};
+      m.capacity = n;
+      m.genomes = A.alloc<int>(static_cast<size_t>(n) * std::max(q.n_slots, 1));
+      m.sc.fitness = A.alloc<double>(n);
+      m.sc.lambda_o = A.alloc<double>(n);
+      m.sc.lambda_b = A.alloc<double>(n);
+      m.sc.lambda_c = A.alloc<int>(n);
+      m.sc.lambda_c0 = A.alloc<int>(n);
+      m.sc.lambda_d = A.alloc<int>(n);
+      m.sc.lambda_s = A.alloc<int>(n);
+      m.sc.lambda_r = A.alloc<int>(n);
+      m.sc.worst_n = A.alloc<int>(n);
+      m.sc.worst_idx = A.alloc<int>(static_cast<size_t>(n) * wk);
+      m.sc.worst_val = A.alloc<double>(static_cast<size_t>(n) * wk);
+      m.lane_cell = A.alloc<int>(n);
+      m.inserted = A.alloc<uint8_t>(n);
+    }
+    ctx->launches += tgb::launch_archive_merge(q, d_blobs, n_islands, m, ctx->stream);
+    check(cudaGetLastError(), "archive merge");
   });
 }
 

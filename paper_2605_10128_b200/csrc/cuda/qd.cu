@@ -563,18 +563,75 @@ __global__ void k_archive_prefix(QdParams p, Archive a, int advance) {
   }
 }
 
-__global__ void k_archive_clear(QdParams p, Archive a) {
+__global__ void k_archive_clear(QdParams p, Archive a, int reset_iter) {
   for (int c = blockIdx.x * blockDim.x + threadIdx.x; c <= p.cells; c += gridDim.x * blockDim.x) {
     if (c < p.cells) a.count[c] = 0;
     a.flat_start[c] = 0;
   }
-  if (blockIdx.x == 0 && threadIdx.x == 0) a.iter[0] = 0;
+  if (reset_iter && blockIdx.x == 0 && threadIdx.x == 0) a.iter[0] = 0;
+}
+
+// ---------------------------------------------------------------- island exchange
+// One thread per archive slot: the slot's entry (or an empty marker with
+// fitness -inf) into the island blob.
+__global__ void k_archive_pack(QdParams p, Archive a, int wk, uint8_t* blob) {
+  const int slots = p.cells * p.cap, ns = p.n_a + p.n_d;
+  const BlobLayout L(slots, ns, wk);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= slots) return;
+  const int cell = i / p.cap, pos = i % p.cap;
+  const bool live = pos < a.count[cell];
+  double* fit = reinterpret_cast<double*>(blob + L.fit);
+  fit[i] = live ? a.fitness[i] : -CUDART_INF;
+  reinterpret_cast<double*>(blob + L.lo)[i] = live ? a.lambda_o[i] : 0.0;
+  reinterpret_cast<double*>(blob + L.lb)[i] = live ? a.lambda_b[i] : 0.0;
+  reinterpret_cast<int*>(blob + L.lc)[i] = live ? a.lambda_c[i] : 0;
+  reinterpret_cast<int*>(blob + L.lc0)[i] = live ? a.lambda_c0[i] : 0;
+  reinterpret_cast<int*>(blob + L.ld)[i] = live ? a.lambda_d[i] : 0;
+  reinterpret_cast<int*>(blob + L.ls)[i] = live ? a.lambda_s[i] : 0;
+  reinterpret_cast<int*>(blob + L.lr)[i] = live ? a.lambda_r[i] : 0;
+  reinterpret_cast<int*>(blob + L.wn)[i] = live ? a.worst_n[i] : 0;
+  for (int k = 0; k < ns; ++k)
+    reinterpret_cast<int*>(blob + L.gen)[static_cast<size_t>(i) * ns + k] =
+        live ? a.genome[static_cast<size_t>(i) * ns + k] : -1;
+  for (int k = 0; k < wk; ++k) {
+    const size_t at = static_cast<size_t>(i) * wk + k;
+    reinterpret_cast<int*>(blob + L.widx)[at] = live ? a.worst_idx[at] : 0;
+    reinterpret_cast<double*>(blob + L.wval)[at] = live ? a.worst_val[at] : 0.0;
+  }
+}
+
+// Gathered blobs [island][BlobLayout] -> one insert batch, lane = island * S + slot.
+__global__ void k_merge_unpack(QdParams p, int wk, const uint8_t* blobs, int n_islands, int* genomes, Scores sc) {
+  const int slots = p.cells * p.cap, ns = p.n_a + p.n_d;
+  const BlobLayout L(slots, ns, wk);
+  const long n = static_cast<long>(slots) * n_islands;
+  for (long lane = blockIdx.x * static_cast<long>(blockDim.x) + threadIdx.x; lane < n;
+       lane += static_cast<long>(gridDim.x) * blockDim.x) {
+    const int isl = static_cast<int>(lane / slots), i = static_cast<int>(lane % slots);
+    const uint8_t* b = blobs + static_cast<size_t>(isl) * L.total;
+    sc.fitness[lane] = reinterpret_cast<const double*>(b + L.fit)[i];
+    sc.lambda_o[lane] = reinterpret_cast<const double*>(b + L.lo)[i];
+    sc.lambda_b[lane] = reinterpret_cast<const double*>(b + L.lb)[i];
+    sc.lambda_c[lane] = reinterpret_cast<const int*>(b + L.lc)[i];
+    sc.lambda_c0[lane] = reinterpret_cast<const int*>(b + L.lc0)[i];
+    sc.lambda_d[lane] = reinterpret_cast<const int*>(b + L.ld)[i];
+    sc.lambda_s[lane] = reinterpret_cast<const int*>(b + L.ls)[i];
+    sc.lambda_r[lane] = reinterpret_cast<const int*>(b + L.lr)[i];
+    sc.worst_n[lane] = reinterpret_cast<const int*>(b + L.wn)[i];
+    for (int k = 0; k < ns; ++k)
+      genomes[lane * ns + k] = reinterpret_cast<const int*>(b + L.gen)[static_cast<size_t>(i) * ns + k];
+    for (int k = 0; k < wk; ++k) {
+      sc.worst_idx[lane * wk + k] = reinterpret_cast<const int*>(b + L.widx)[static_cast<size_t>(i) * wk + k];
+      sc.worst_val[lane * wk + k] = reinterpret_cast<const double*>(b + L.wval)[static_cast<size_t>(i) * wk + k];
+    }
+  }
 }
 
 }  // namespace
 
 void launch_archive_reset(const QdState& q, cudaStream_t s) {
-  k_archive_clear<<<(q.p.cells + 256) / 256, 256, 0, s>>>(q.p, q.a);
+  k_archive_clear<<<(q.p.cells + 256) / 256, 256, 0, s>>>(q.p, q.a, 1);
 }
 
 void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStream_t s) {
@@ -582,15 +639,35 @@ void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStre
   k_offspring<<<(q.p.batch + kThreads - 1) / kThreads, kThreads, 0, s>>>(g, q.p, q.a, genomes);
 }
 
-int launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
-                  cudaStream_t s) {
+namespace {
+int insert_lanes(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
+                 int* lane_cell, uint8_t* inserted, cudaStream_t s) {
   constexpr int kWarps = 4;
   if (n <= 0) return 0;
-  k_lane_cell<<<(n + 255) / 256, 256, 0, s>>>(q.p, sc, n, q.lane_cell, q.inserted);
-  k_insert<<<(q.p.cells + kWarps - 1) / kWarps, 32 * kWarps, 0, s>>>(q.p, q.a, genomes, sc, q.lane_cell, n, worst_k,
-                                                                    q.inserted);
+  k_lane_cell<<<(n + 255) / 256, 256, 0, s>>>(q.p, sc, n, lane_cell, inserted);
+  k_insert<<<(q.p.cells + kWarps - 1) / kWarps, 32 * kWarps, 0, s>>>(q.p, q.a, genomes, sc, lane_cell, n, worst_k,
+                                                                    inserted);
   k_archive_prefix<<<1, 256, 0, s>>>(q.p, q.a, advance_iter ? 1 : 0);
   return 3;
+}
+}  // namespace
+
+int launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
+                  cudaStream_t s) {
+  return insert_lanes(q, genomes, sc, n, worst_k, advance_iter, q.lane_cell, q.inserted, s);
+}
+
+void launch_archive_pack(const QdState& q, void* blob, cudaStream_t s) {
+  const int slots = q.p.cells * q.p.cap;
+  k_archive_pack<<<(slots + 255) / 256, 256, 0, s>>>(q.p, q.a, q.worst_k, static_cast<uint8_t*>(blob));
+}
+
+int launch_archive_merge(const QdState& q, const void* blobs, int n_islands, MergeBuffers& m, cudaStream_t s) {
+  const int n = q.p.cells * q.p.cap * n_islands;
+  k_merge_unpack<<<(n + 255) / 256 < 1024 ? (n + 255) / 256 : 1024, 256, 0, s>>>(
+      q.p, q.worst_k, static_cast<const uint8_t*>(blobs), n_islands, m.genomes, m.sc);
+  k_archive_clear<<<(q.p.cells + 256) / 256, 256, 0, s>>>(q.p, q.a, 0);
+  return 2 + insert_lanes(q, m.genomes, m.sc, n, q.worst_k, false, m.lane_cell, m.inserted, s);
 }
 
 void launch_mutate_lanes(const DevGrid& g, const QdState& q, const int* parents, const unsigned long long* seeds, int n,

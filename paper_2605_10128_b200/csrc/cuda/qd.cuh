@@ -55,12 +55,56 @@ struct QdState {
   void* arena = nullptr;        // owned by the context (DeviceArena*)
 };
 
+// Island exchange blob: one island's whole archive (cells x cap slots) in a
+// fixed byte layout, so an NCCL allgather of equal-sized blobs moves every
+// island's archive. Empty slots carry fitness -inf and are rejected by the
+// merge insert like any non-finite fitness (qd_optimizer.cpp:283).
+// Layout (all sections 8-byte aligned): fitness, lambda_o, lambda_b (f64[S]),
+// worst_val (f64[S*wk]), genome (i32[S*ns]), lambda_c, lambda_c0, lambda_d,
+// lambda_s, lambda_r, worst_n (i32[S]), worst_idx (i32[S*wk]).
+struct BlobLayout {
+  size_t fit, lo, lb, wval, gen, lc, lc0, ld, ls, lr, wn, widx, total;
+  __host__ __device__ static size_t al(size_t x) { return (x + 7) & ~size_t{7}; }
+  __host__ __device__ BlobLayout(int slots, int ns, int wk) {
+    const size_t S = static_cast<size_t>(slots);
+    size_t o = 0;
+    fit = o, o += al(S * 8);
+    lo = o, o += al(S * 8);
+    lb = o, o += al(S * 8);
+    wval = o, o += al(S * wk * 8);
+    gen = o, o += al(S * ns * 4);
+    lc = o, o += al(S * 4);
+    lc0 = o, o += al(S * 4);
+    ld = o, o += al(S * 4);
+    ls = o, o += al(S * 4);
+    lr = o, o += al(S * 4);
+    wn = o, o += al(S * 4);
+    widx = o, o += al(S * wk * 4);
+    total = o;
+  }
+};
+
+// Merge-side buffers: the gathered islands unpacked as one insert batch.
+struct MergeBuffers {
+  int capacity = 0;  // lanes
+  int* genomes = nullptr;
+  Scores sc{};
+  int* lane_cell = nullptr;
+  uint8_t* inserted = nullptr;
+};
+
 // Kernels launched by the context (capi.cu).
 void launch_archive_reset(const QdState& q, cudaStream_t s);
 void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStream_t s);
 // Returns the number of kernels launched.
 int launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n, int worst_k, bool advance_iter,
                   cudaStream_t s);
+// Island exchange: pack this archive into `blob`
+// (BlobLayout bytes); merge = clear the cells and insert the n_islands blobs in
+// (island, cell, position) order with the Repertoire::insert semantics, so
+// every island that merges the same gathered blobs holds the same archive.
+void launch_archive_pack(const QdState& q, void* blob, cudaStream_t s);
+int launch_archive_merge(const QdState& q, const void* blobs, int n_islands, MergeBuffers& m, cudaStream_t s);
 void launch_mutate_lanes(const DevGrid& g, const QdState& q, const int* parents, const unsigned long long* seeds, int n,
                          int* children, cudaStream_t s);
 void launch_crossover_lanes(const DevGrid& g, const QdState& q, const int* p1, const int* p2,

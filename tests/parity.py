@@ -133,3 +133,36 @@ def grid_with_stations(base_json: str, buses) -> str:
                                                  for e in el]})
     del ids
     return json.dumps(doc)
+
+
+def replay_inserts(stream, cfg):
+    """Naive list replay of Repertoire::insert (test_qd_optimizer.cpp:262-277):
+    stream of (genome, {fitness, lambda_d, lambda_s, lambda_r}) -> (inserted
+    flags, {cell: [(key, fitness, genome)]})."""
+    import math
+
+    from paper_2605_10128_b200 import Genome, descriptor_to_cell
+
+    cells = {}
+    results = []
+    for genome, sc in stream:
+        if not math.isfinite(sc["fitness"]):
+            results.append(False)
+            continue
+        cell = descriptor_to_cell(sc["lambda_d"], sc["lambda_s"], sc["lambda_r"], cfg)
+        lst = cells.setdefault(cell, [])
+        key = Genome(list(genome[:cfg.n_a]), list(genome[cfg.n_a:])).canonical_key()
+        if any(k == key for k, _, _ in lst):
+            results.append(False)
+            continue
+        if len(lst) >= cfg.cell_capacity and sc["fitness"] <= lst[-1][1]:
+            results.append(False)
+            continue
+        pos = 0
+        while pos < len(lst) and not (sc["fitness"] > lst[pos][1]):
+            pos += 1
+        lst.insert(pos, (key, sc["fitness"], list(genome)))
+        if len(lst) > cfg.cell_capacity:
+            lst.pop()
+        results.append(True)
+    return results, cells

@@ -12,7 +12,7 @@ import pytest
 
 import paper_2605_10128_b200 as P
 from oracle.oracle import OracleContext, qd_config, random_grid_json
-from tests.parity import compare_scores
+from tests.parity import compare_scores, replay_inserts
 
 pytestmark = pytest.mark.gpu
 
@@ -77,31 +77,7 @@ def test_crossover_replays_reference_stream(data_dir):
                 assert got[i].tolist() == want.tolist(), (i, p1[i], p2[i], got[i], want)
 
 
-def _replay_oracle(stream, cfg):
-    """Naive list replay of Repertoire::insert (test_qd_optimizer.cpp:262-277)."""
-    cells = {}
-    results = []
-    for genome, sc in stream:
-        if not math.isfinite(sc["fitness"]):
-            results.append(False)
-            continue
-        cell = P.descriptor_to_cell(sc["lambda_d"], sc["lambda_s"], sc["lambda_r"], cfg)
-        lst = cells.setdefault(cell, [])
-        key = P.Genome(list(genome[:cfg.n_a]), list(genome[cfg.n_a:])).canonical_key()
-        if any(k == key for k, _, _ in lst):
-            results.append(False)
-            continue
-        if len(lst) >= cfg.cell_capacity and sc["fitness"] <= lst[-1][1]:
-            results.append(False)
-            continue
-        pos = 0
-        while pos < len(lst) and not (sc["fitness"] > lst[pos][1]):
-            pos += 1
-        lst.insert(pos, (key, sc["fitness"], list(genome)))
-        if len(lst) > cfg.cell_capacity:
-            lst.pop()
-        results.append(True)
-    return results, cells
+_replay_oracle = replay_inserts
 
 
 def test_archive_replay_matches_sequential_insert(data_dir):
@@ -217,3 +193,67 @@ def test_optimizer_mini_grid_semantics():
     assert any(e.score.lambda_d >= 1 for e in res.repertoire.entries)
     with pytest.raises(P.ConfigError):
         P.run_optimizer(ctx, P.QdConfig(batch_size=0))
+
+
+def test_island_merge_matches_sequential_insert(data_dir):
+    """Island exchange: two islands (own contexts, own seeds)
+    pack their archives on the device, the blobs are concatenated as an
+    allgather would, and the device merge equals a sequential
+    Repertoire::insert replay of island 0's entries then island 1's (cell
+    order, position order). Both islands end with the same archive; the
+    host mirror of the blob layout decodes the device blob; the loop keeps
+    running after a merge."""
+    import torch
+
+    from paper_2605_10128_b200.islands import BlobLayout, IslandExchange, pack_entries, unpack_blob
+
+    text = open(os.path.join(data_dir, "grid14_congested.json")).read()
+    sess, snaps = [], []
+    for seed in (3, 4):
+        ctx, _ = _ctx(text)
+        s = P.QdSession(ctx, P.QdConfig(seed=seed, batch_size=64, cell_capacity=3))
+        s.step(6)
+        sess.append(s)
+        snaps.append(s.fetch())
+    cfg = sess[0].cfg
+    lay = BlobLayout(P.cell_count(cfg), cfg.cell_capacity, cfg.n_a + cfg.n_d, 20)
+    assert sess[0].blob_bytes() == lay.nbytes
+    blobs = torch.empty(2 * lay.nbytes, dtype=torch.uint8, device="cuda")
+    for i, s in enumerate(sess):
+        s.pack(blobs[i * lay.nbytes:].data_ptr())
+    torch.cuda.synchronize()
+    host = blobs.cpu().numpy()
+    # the host mirror decodes the device blob into the fetched snapshot
+    for i, snap in enumerate(snaps):
+        dec = unpack_blob(lay, host[i * lay.nbytes:(i + 1) * lay.nbytes])
+        assert [(d["cell"], d["genome"], d["fitness"]) for d in dec] == [
+            (e.cell, e.genome.action_slots + e.genome.disconnection_slots, e.score.fitness) for e in snap.entries]
+        assert [d["worst"] for d in dec] == [[(k, v) for k, v in e.score.worst_contingencies] for e in snap.entries]
+        # ... and the host encoder reproduces the device blob byte for byte
+        assert np.array_equal(pack_entries(lay, snap.entries), host[i * lay.nbytes:(i + 1) * lay.nbytes])
+    stream = [(e.genome.action_slots + e.genome.disconnection_slots,
+               dict(fitness=e.score.fitness, lambda_d=e.score.lambda_d, lambda_s=e.score.lambda_s,
+                    lambda_r=e.score.lambda_r)) for snap in snaps for e in snap.entries]
+    _, cells = replay_inserts(stream, cfg)
+    want = {c: v for c, v in cells.items() if v}
+    merged = []
+    for s in sess:
+        s.merge(blobs.data_ptr(), 2)
+        m = s.fetch()
+        got = {}
+        for e in m.entries:
+            got.setdefault(e.cell, []).append((e.genome.canonical_key(), e.score.fitness,
+                                               e.genome.action_slots + e.genome.disconnection_slots))
+        assert got == want
+        merged.append([(e.cell, e.genome.action_slots + e.genome.disconnection_slots, e.score.fitness,
+                        e.score.lambda_o, e.score.worst_contingencies) for e in m.entries])
+    assert merged[0] == merged[1]
+    assert max(snaps[0].best_fitness, snaps[1].best_fitness) == sess[0].fetch().best_fitness
+    # a single island merging its own blob is unchanged; the loop continues after merges
+    ex = IslandExchange(sess[0])
+    before = sess[0].fetch().entries
+    ex.exchange()
+    after = sess[0].fetch().entries
+    assert [(e.cell, e.score.fitness) for e in before] == [(e.cell, e.score.fitness) for e in after]
+    sess[0].step(3)
+    assert sess[0].fetch().best_fitness >= snaps[0].best_fitness
