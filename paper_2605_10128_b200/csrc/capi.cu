@@ -612,15 +612,17 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     double* tdiag = A.alloc<double>(E);
     double* tk = A.alloc<double>(static_cast<size_t>(E) * std::max(g.Kpad, 1));
     const int ntiles = g.Kpad / tgb::sweep_tile_k();
-    const size_t tmax_n = static_cast<size_t>(std::max(ntiles, 1)) * (E + tgb::sweep_chunk()) * tgb::kTmaxSub;
+    const size_t tmax_n = static_cast<size_t>(std::max(ntiles, 1)) * (E + tgb::sweep_chunk()) * tgb::kRec;
     double* tmax = A.alloc<double>(tmax_n);
     check(cudaMemsetAsync(tmax, 0, tmax_n * sizeof(double), s), "tmax");
+    double* alpha0 = A.alloc<double>(std::max(g.Kpad, 1));
     g.theta0 = theta0;
     g.f0 = f0;
     g.Tdiag = tdiag;
     g.TK = tk;
     g.Tmax = tmax;
-    tgb::launch_base_tables(g, d_pr, theta0, f0, tdiag, tk, tmax, s);
+    g.alpha0 = alpha0;
+    tgb::launch_base_tables(g, d_pr, theta0, f0, tdiag, tk, tmax, alpha0, s);
     check(cudaGetLastError(), "base tables");
     check(cudaStreamSynchronize(s), "context setup");
 

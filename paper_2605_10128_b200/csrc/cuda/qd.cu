@@ -590,14 +590,15 @@ __global__ void k_archive_pack(QdParams p, Archive a, int wk, uint8_t* blob) {
   reinterpret_cast<int*>(blob + L.ld)[i] = live ? a.lambda_d[i] : 0;
   reinterpret_cast<int*>(blob + L.ls)[i] = live ? a.lambda_s[i] : 0;
   reinterpret_cast<int*>(blob + L.lr)[i] = live ? a.lambda_r[i] : 0;
-  reinterpret_cast<int*>(blob + L.wn)[i] = live ? a.worst_n[i] : 0;
+  const int wn = live ? min(a.worst_n[i], wk) : 0;
+  reinterpret_cast<int*>(blob + L.wn)[i] = wn;
   for (int k = 0; k < ns; ++k)
     reinterpret_cast<int*>(blob + L.gen)[static_cast<size_t>(i) * ns + k] =
         live ? a.genome[static_cast<size_t>(i) * ns + k] : -1;
   for (int k = 0; k < wk; ++k) {
     const size_t at = static_cast<size_t>(i) * wk + k;
-    reinterpret_cast<int*>(blob + L.widx)[at] = live ? a.worst_idx[at] : 0;
-    reinterpret_cast<double*>(blob + L.wval)[at] = live ? a.worst_val[at] : 0.0;
+    reinterpret_cast<int*>(blob + L.widx)[at] = k < wn ? a.worst_idx[at] : 0;  // canonical: zeros past worst_n
+    reinterpret_cast<double*>(blob + L.wval)[at] = k < wn ? a.worst_val[at] : 0.0;
   }
 }
 

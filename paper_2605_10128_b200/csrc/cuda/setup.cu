@@ -107,19 +107,45 @@ __global__ void k_tk(DevGrid g, double* tk, int W) {
   }
 }
 
-// Tmax[tile][e][s] = max_k |T_base[e, k]| over sub-tile s of the tile's contingencies.
-__global__ void k_tmax(DevGrid g, const double* tk, double* tmax, int W, int ld) {
+// alpha0[k] = f0[beta] / (1 - Tdiag[beta]): the contingency's flow factor in
+// the unchanged topology (0 for padding).
+__global__ void k_alpha0(DevGrid g, double* alpha0) {
+  for (int k = blockIdx.x * blockDim.x + threadIdx.x; k < g.Kpad; k += gridDim.x * blockDim.x) {
+    double a = 0.0;
+    if (k < g.Ks) {
+      const int beta = g.ks_branch[k];
+      const double den = 1.0 - g.Tdiag[beta];
+      a = fabs(den) >= 1e-8 ? g.f0[beta] / den : 0.0;
+    }
+    alpha0[k] = a;
+  }
+}
+
+// Skip record [tile][e][kRec]: max_k |T_base[e, k]| over each sub-tile, then
+// max_k and min_k of T_base[e, k] * alpha0[k] over the tile (the unchanged
+// topology's post-contingency flow change on e).
+__global__ void k_tmax(DevGrid g, const double* tk, const double* alpha0, double* tmax, int W, int ld) {
   const int ntiles = g.Kpad / W;
   const int total = ntiles * g.E;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const int tile = idx / g.E, e = idx % g.E;
     const double* row = tk + (static_cast<size_t>(tile) * g.E + e) * W;
+    const double* a0 = alpha0 + static_cast<size_t>(tile) * W;
+    double* rec = tmax + (static_cast<size_t>(tile) * ld + e) * kRec;
     const int sw = W / kTmaxSub;
+    double dmax = 0.0, dmin = 0.0;
     for (int s = 0; s < kTmaxSub; ++s) {
       double m = 0.0;
-      for (int k = s * sw; k < (s + 1) * sw; ++k) m = fmax(m, fabs(row[k]));
-      tmax[(static_cast<size_t>(tile) * ld + e) * kTmaxSub + s] = m;
+      for (int k = s * sw; k < (s + 1) * sw; ++k) {
+        m = fmax(m, fabs(row[k]));
+        const double d = row[k] * a0[k];
+        dmax = fmax(dmax, d);
+        dmin = fmin(dmin, d);
+      }
+      rec[s] = m;
     }
+    rec[kTmaxSub] = dmax;
+    rec[kTmaxSub + 1] = dmin;
   }
 }
 
@@ -157,7 +183,7 @@ bool device_spd_inverse(double* a, int n, cudaStream_t stream) {
 }
 
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
-                        double* tmax, cudaStream_t stream) {
+                        double* tmax, double* alpha0, cudaStream_t stream) {
   k_theta<<<(g.Nr + 255) / 256 + 1, 256, 0, stream>>>(g, p_red, theta0);
   DevGrid g2 = g;
   g2.theta0 = theta0;
@@ -165,8 +191,11 @@ void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, d
   const size_t total = static_cast<size_t>(g.E) * g.Kpad;
   if (total > 0) {
     k_tk<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 32)), 256, 0, stream>>>(g2, tk, sweep_tile_k());
+    g2.f0 = f0;
+    g2.Tdiag = tdiag;
+    k_alpha0<<<(g.Kpad + 255) / 256 + 1, 256, 0, stream>>>(g2, alpha0);
     k_tmax<<<static_cast<int>(std::min<size_t>((total / sweep_tile_k() + 255) / 256 + 1, 148 * 32)), 256, 0, stream>>>(
-        g2, tk, tmax, sweep_tile_k(), g.E + sweep_chunk());
+        g2, tk, alpha0, tmax, sweep_tile_k(), g.E + sweep_chunk());
   }
 }
 

@@ -22,7 +22,9 @@
 //     part bounded; only rows passing both run the remaining R DFMA per
 //     element and a 2-op hi-word test; the exact path runs only where |f1| can
 //     exceed the limit.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 
 #include "engine.cuh"
 
@@ -37,6 +39,7 @@ constexpr int kThreads = 32 * kWarps;
 constexpr int kChunk = 32;               // branches per pipeline stage
 constexpr int kStages = 3;
 constexpr int kMaxCand = kWarps;         // one candidate per warp
+constexpr int kGroupBlock = 8;           // candidate groups per CTA super-block (L2 reuse of T_base tiles)
 
 // candidates per warp for a given rank (register budget)
 __host__ __device__ constexpr int nc_for_rank(int) { return 1; }
@@ -45,7 +48,7 @@ __host__ __device__ constexpr int cand_per_cta(int r) { return kWarps * nc_for_r
 constexpr size_t kStageT = static_cast<size_t>(kChunk) * kTileK;           // doubles
 constexpr size_t kStageF = static_cast<size_t>(kMaxCand) * kChunk * kStride;  // doubles
 constexpr size_t kStageL = kChunk;                                         // doubles
-constexpr size_t kStageTm = static_cast<size_t>(kChunk) * kTmaxSub;       // sub-tile max |T_base| per row
+constexpr size_t kStageTm = static_cast<size_t>(kChunk) * kRec;           // skip record per row
 constexpr int kSubLanes = 32 / kTmaxSub;                                   // lanes per sub-tile
 static_assert(kTileK % kTmaxSub == 0 && kSubLanes * kTmaxSub == 32 && kTmaxSub == kStride, "sub-tile layout");
 constexpr size_t kStageDoubles = kStageT + kStageF + kStageL + kStageTm;
@@ -96,12 +99,12 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
   const uint32_t bt = rows * kTileK * sizeof(double);
   const uint32_t bf = kStageF * sizeof(double);  // the group's rows of this chunk: one contiguous block
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
-  const uint32_t bm = rows * kTmaxSub * sizeof(double);
+  const uint32_t bm = rows * kRec * sizeof(double);
   mbar_expect_tx(bar, bt + bf + bl + bm);
   bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
   bulk_g2s(stage + kStageT, b.feat + feat_index(w.group * kGroupSlots, b.nchunks, e0), bf, bar);
   bulk_g2s(stage + kStageT + kStageF, g.br_lim + e0, bl, bar);
-  bulk_g2s(stage + kStageT + kStageF + kStageL, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kTmaxSub,
+  bulk_g2s(stage + kStageT + kStageF + kStageL, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kRec,
            bm, bar);
 }
 
@@ -136,18 +139,22 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
 #pragma unroll
     for (int q = 0; q < kMaxRemovedSweep; ++q) rem[j][q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
   }
-  // Skip-bound operands in shared memory (invalid contingencies carry zeros):
-  // max |alpha| per sub-tile, asub[j][s], and the tile max of each |R'_q| as a
-  // row weight vector rms[j][slot] (0 for f_c and padding).
+  // Skip-bound operands in shared memory (invalid contingencies carry alpha 0):
+  // max |alpha - alpha0| per sub-tile, asub[j][s] (the candidate's departure
+  // from the unchanged topology's flow factors), and the tile max of each
+  // |R'_q| as a row weight vector rms[j][slot] (0 for f_c and padding).
   double* rms = rmax_s + warp * NC * kStride;
   double* asub = amax_s + warp * NC * kTmaxSub;
   if (lane < NC * kStride) rms[lane] = 0.0;
   __syncwarp();
+  double a0[kKpl];
+#pragma unroll
+  for (int k = 0; k < kKpl; ++k) a0[k] = g.alpha0[kb + k];
 #pragma unroll
   for (int j = 0; j < NC; ++j) {
     double a = 0.0;
 #pragma unroll
-    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[j][k]));
+    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[j][k] - a0[k]));
 #pragma unroll
     for (int o = kSubLanes / 2; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
     if (lane % kSubLanes == 0) asub[j * kTmaxSub + lane / kSubLanes] = a * (1.0 + 1e-12);
@@ -207,10 +214,15 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     const double* sF = st + kStageT + static_cast<size_t>(warp) * NC * kChunk * kStride;
     const double* sL = st + kStageT + kStageF;
     // Stage 1 (one lane per row): rows that can reach their limit for one of
-    // the warp's candidates,
-    //   |f1| <= |f_c| + max_s max|T_base|_s max|alpha|_s + lrb,  lrb = sum_q |L_q| max|R'_q|
-    // (s: sub-tiles; R' maxima over the tile). For stage 2 each lane keeps, per candidate, the high word
-    // of lim (1 - 1e-12) - lrb (0 when that is not positive).
+    // the warp's candidates. With alpha = alpha0 + delta (alpha0: unchanged
+    // topology) every element of the tile satisfies
+    //   f1 = f_c + T alpha0 + T delta + L R'  in  [f_c + D0min - w, f_c + D0max + w],
+    //   w = max_s max|T_base|_s max|delta|_s + lrb,  lrb = sum_q |L_q| max|R'_q|
+    // (D0max / D0min: max / min of T_base * alpha0 over the tile, precomputed;
+    // s: sub-tiles; R' maxima over the tile). A relative slack of 1e-12 on
+    // every term covers the rounding of the computed f1. For stage 2 each lane
+    // keeps, per candidate, the high word of lim (1 - 1e-12) - lrb (0 when that
+    // is not positive).
     unsigned need = rows >= 32 ? 0xffffffffu : ((1u << rows) - 1u);
     uint32_t thr_lane[NC];
 #pragma unroll
@@ -219,7 +231,9 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       bool hot = false;
       if (lane < rows) {
         const double lim = sL[lane] * (1.0 - 1e-12);
-        const double2* tmr = reinterpret_cast<const double2*>(st + kStageT + kStageF + kStageL + lane * kTmaxSub);
+        const double* rec = st + kStageT + kStageF + kStageL + lane * kRec;
+        const double2* tmr = reinterpret_cast<const double2*>(rec);
+        const double2 d0 = *reinterpret_cast<const double2*>(rec + kTmaxSub);
 #pragma unroll
         for (int j = 0; j < NC; ++j) {
           // the row's 4 double2 read in a lane-rotated order (conflict-free),
@@ -227,7 +241,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
           const double2* fr = reinterpret_cast<const double2*>(sF + (static_cast<size_t>(j) * kChunk + lane) * kStride);
           const double2* wr = reinterpret_cast<const double2*>(rms + j * kStride);
           const double2* ar = reinterpret_cast<const double2*>(asub + j * kTmaxSub);
-          double lrb = 0.0, fca = 0.0, ta = 0.0;
+          double lrb = 0.0, fc = 0.0, ta = 0.0;
 #pragma unroll
           for (int i = 0; i < kStride / 2; ++i) {
             const int idx = (i + (lane >> 1)) & (kStride / 2 - 1);
@@ -237,12 +251,14 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
             const double2 a2 = ar[idx];
             lrb = fma(fabs(p2.x), w2.x, lrb);
             lrb = fma(fabs(p2.y), w2.y, lrb);
-            fca = idx == 0 ? fabs(p2.x) : fca;
+            fc = idx == 0 ? p2.x : fc;
             ta = fmax(ta, fmax(t2.x * a2.x, t2.y * a2.y));
           }
           const double thr = lim - lrb;
           thr_lane[j] = thr > 0.0 ? hi_abs(thr) : 0u;
-          hot |= fca + ta + lrb >= lim;
+          const double w = ta + lrb;
+          const double slack = 1e-12 * (fabs(fc) + fmax(d0.x, -d0.y) + w);
+          hot |= (fc + d0.x + w + slack >= lim) || (fc + d0.y - w - slack <= -lim);
         }
       }
       need = __ballot_sync(0xffffffffu, hot);
@@ -353,8 +369,12 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   }
 }
 
+// CTA order: super-blocks of `gblock` candidate groups x all tiles, tile-major
+// inside a super-block, so the CTAs resident at one time share each T_base
+// tile across gblock groups (one HBM read of a tile per super-block instead of
+// per group) while the super-block's candidate rows stay in L2 across its tiles.
 template <bool FULL>
-__global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
+__global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CtaWork w;
   __shared__ int r_s;
@@ -363,7 +383,10 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
   __shared__ __align__(16) double amax_s[kWarps * kTmaxSub];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* smem = reinterpret_cast<double*>(smem_raw + 64);
-  const int group = blockIdx.y;
+  const int per_sb = gblock * ntiles;
+  const int sb = static_cast<int>(blockIdx.x) / per_sb, rr = static_cast<int>(blockIdx.x) % per_sb;
+  const int g0 = sb * gblock, gg = min(gblock, ngroups - g0);
+  const int tile = rr / gg, group = g0 + rr % gg;
   if (group >= b.wl_group0[kSweepRank + 1]) return;
   if (threadIdx.x == 0) {
     int r = 0;
@@ -380,7 +403,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b) {
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
-  const int tile = blockIdx.x;
   switch (r_s) {
     case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
     case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
@@ -449,12 +471,18 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     configured = true;
   }
   // group slots: every bucket rounds up to whole groups of >= kWarps candidates
-  dim3 grid(g.Kpad / kTileK, max_sweep_groups(b.n));
+  static const int gblock_env = [] {
+    const char* v = std::getenv("TGB_SWEEP_GROUP_BLOCK");
+    return v ? std::max(1, std::atoi(v)) : 0;
+  }();
+  const int ntiles = g.Kpad / kTileK, ngroups = max_sweep_groups(b.n);
+  const int gblock = std::min(ngroups, gblock_env ? gblock_env : kGroupBlock);
+  const unsigned grid = static_cast<unsigned>(ntiles) * ngroups;
   if (ev0) cudaEventRecord(ev0, stream);
   if (full)
-    k_sweep<true><<<grid, kThreads, kSmemBytes, stream>>>(g, b);
+    k_sweep<true><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
   else
-    k_sweep<false><<<grid, kThreads, kSmemBytes, stream>>>(g, b);
+    k_sweep<false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
   if (ev1) cudaEventRecord(ev1, stream);
   *launched += 1;
 }
