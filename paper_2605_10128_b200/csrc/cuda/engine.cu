@@ -78,7 +78,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       __syncthreads();
       continue;
     }
-    const int ns = t.ns, nv = t.nv, r = ns + nv;
+    const int ns = t.ns, nv = t.nv, r = ns + nv, rs = row_stride(r);
     // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0...]
     for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
       double phi[kMaxSplits], rho[kMaxCols];
@@ -92,9 +92,10 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
         for (int q = 0; q < ns; ++q) row[1 + q] = be * phi[q];
         for (int m = 0; m < nv; ++m) row[1 + ns + m] = be * rho[m];
       }
-      double2* dst = reinterpret_cast<double2*>(b.feat + feat_index(slot, b.nchunks, e));
+      double2* dst = reinterpret_cast<double2*>(b.feat + feat_index(slot, b.nchunks, e, r));
 #pragma unroll
-      for (int i = 0; i < kStride / 2; ++i) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+      for (int i = 0; i < kStride / 2; ++i)
+        if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
     }
     __syncthreads();
     // contingency rows: [alpha_k, R[:,k] * alpha_k, 0...], flag
@@ -137,16 +138,17 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
             }
             flag = stub ? 0 : 1;
           } else {
-            const double alpha = b.feat[feat_index(slot, b.nchunks, beta)] / den;
+            const double alpha = b.feat[feat_index(slot, b.nchunks, beta, r)] / den;
             row[0] = alpha;
             for (int i = 0; i < r; ++i) row[1 + i] = rk[i] * alpha;
           }
         }
         if (flag == 1) b.energy[static_cast<size_t>(c) * g.Kall + g.ks_cont[k]] = b.params.penalty;
       }
-      double2* dst = reinterpret_cast<double2*>(kd + static_cast<size_t>(k) * kStride);
+      double2* dst = reinterpret_cast<double2*>(kd + static_cast<size_t>(k) * rs);
 #pragma unroll
-      for (int i = 0; i < kStride / 2; ++i) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+      for (int i = 0; i < kStride / 2; ++i)
+        if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
       kf[k] = flag;
     }
     if (threadIdx.x == 0) {
@@ -319,7 +321,7 @@ __global__ void __launch_bounds__(256) k_finish(DevGrid g, Batch b, int n_a, int
     const double m = __longlong_as_double(static_cast<long long>(fm[e]));
     const double mb = __longlong_as_double(static_cast<long long>(fb[e]));
     if (m > lim) so += m - lim, ++nc;
-    if (fabs(b.feat[feat_index(slot, b.nchunks, e)]) > lim) ++nc0;
+    if (fabs(b.feat[feat_index(slot, b.nchunks, e, b.rank[c])]) > lim) ++nc0;
     if (mb > lim) sb += mb - lim;
   }
   int isl = 0;
@@ -409,7 +411,7 @@ __global__ void k_extract_base(DevGrid g, Batch b, double* out) {
        i += static_cast<size_t>(gridDim.x) * blockDim.x) {
     const size_t c = i / g.E;
     const int e = static_cast<int>(i % g.E);
-    out[i] = b.status[c] == 0 ? b.feat[feat_index(b.slot[c], b.nchunks, e)] : 0.0;
+    out[i] = b.status[c] == 0 ? b.feat[feat_index(b.slot[c], b.nchunks, e, b.rank[c])] : 0.0;
   }
 }
 

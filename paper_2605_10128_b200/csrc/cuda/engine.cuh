@@ -15,11 +15,18 @@ constexpr int kMaxRemovedSweep = 4;  // genome disconnections skipped in the swe
 constexpr int kGroupSlots = 16;      // candidates per sweep CTA group (8 warps x 2)
 constexpr int kChunkRows = 32;       // branch rows per sweep pipeline stage
 
-// Row e of candidate c in the group-major candidate row array.
-__host__ __device__ inline size_t feat_index(int slot, int nchunks, int e) {
+// Doubles per candidate row (branch row f_c, L[0..r-1] or contingency row
+// alpha, R'[0..r-1]) for update rank r, rounded up to whole double2.
+__host__ __device__ constexpr int row_stride(int r) { return (r + 2) & ~1; }
+
+// Row e of candidate c (sweep slot `slot`, update rank r) in the group-major
+// candidate row array: [group][chunk][kGroupSlots][kChunkRows][row_stride(r)],
+// each group owning a block sized for the largest stride.
+__host__ __device__ inline size_t feat_index(int slot, int nchunks, int e, int r) {
   const int group = slot / kGroupSlots, pos = slot % kGroupSlots;
   const int chunk = e / kChunkRows, row = e % kChunkRows;
-  return ((((static_cast<size_t>(group) * nchunks + chunk) * kGroupSlots + pos) * kChunkRows) + row) * kStride;
+  return static_cast<size_t>(group) * nchunks * kGroupSlots * kChunkRows * kStride +
+         ((static_cast<size_t>(chunk) * kGroupSlots + pos) * kChunkRows + row) * row_stride(r);
 }
 
 // Per-candidate scores, SoA (dc_engine.hpp:25-39).
@@ -53,12 +60,13 @@ struct Batch {
   int* removed;               // [n][kMaxRemovedSweep] genome-removed branches
   // Candidate branch rows (f_c, L[0..r-1], 0 padding) stored in the sweep's
   // group-major layout so one pipeline stage of a sweep CTA is one contiguous
-  // block: [group][chunk][kGroupSlots][kChunkRows][kStride].
+  // block: [group][chunk][kGroupSlots][kChunkRows][row_stride(r)] (feat_index).
   double* feat;
   int* slot;                  // [n] group * kGroupSlots + position, -1 when not swept
   int nchunks;                // ceil(E / kChunkRows)
   unsigned long long* rows_done;  // [4] sweep stats: blocks computed / offered / overloaded / first FMA only
-  double* kdat;               // [n][Kpad][kStride] alpha, R' (single-branch contingencies)
+  double* kdat;               // [n][Kpad * kStride]: Kpad rows of row_stride(r) doubles alpha, R'
+                              // (single-branch contingencies)
   uint8_t* kflag;             // [n][Kpad] 0 ok, 1 islanded, 2 padding
   unsigned long long* fmax;   // [n][E] max |f| over contingencies (bits of a non-negative double)
   unsigned long long* fbus;   // [n][E] max |f| over busbar outages

@@ -2,26 +2,35 @@
 // contingencies, all candidates of a batch at once).
 //
 // For candidate c, monitored branch e and contingency k (branch beta_k):
-//   f1[e,k] = f_c[e] + T_base[e,k] * alpha_k + sum_r L[e,r] * R'[r,k]
+//   f1[e,k] = f_c[e] + T_base[e,k] * alpha_k + sum_q L[e,q] * R'[q,k]
 // (topo.cuh: T_cand = T_base + L R, alpha_k = f_c[beta]/(1 - T_cand[beta,beta]),
 // R' = R * alpha). The E x K x B tensor is never written: each element is
 // tested against the branch limit in registers; only elements with
 // |f1| > limit touch the per-(c,k) energy accumulators (registers, summed in
 // branch order) and the per-(c,e) max (atomicMax on the ordered bit pattern).
 //
-// Dataflow (one CTA = one 128-contingency tile x 8*NC candidates):
-//   * T_base tiles ([tile][E][128], 32 branches = 32 KB per stage), the
-//     candidates' branch rows (f_c, L) and the branch limits are streamed into
-//     shared memory by TMA bulk copies (cp.async.bulk + mbarrier complete_tx),
-//     3-stage pipeline, one elected producer thread;
-//   * each lane owns 4 contingencies: alpha / R' live in registers for the
-//     whole sweep; each warp processes NC candidates so one T load feeds NC
-//     candidates' FMAs;
-//   * two-stage exact skip: a per-row bound over the whole tile (no element
-//     work), then the exact first FMA f_c + T alpha per element with the L R'
-//     part bounded; only rows passing both run the remaining R DFMA per
-//     element and a 2-op hi-word test; the exact path runs only where |f1| can
-//     exceed the limit.
+// One CTA = one 128-contingency tile x one group of 16 candidates of equal
+// update rank R (one candidate per warp). Each lane owns 4 contingencies:
+// alpha / R' live in registers for the whole sweep. Candidate rows are
+// row_stride(R) doubles (f_c, L[0..R-1]), contingency rows likewise.
+//
+// Scores-only kernel (k_sweep<false>, the MapElites path): branch rows are
+// streamed in chunks of 32 by TMA bulk copies (cp.async.bulk + mbarrier
+// complete_tx) into a 5-8 stage ring: the group's candidate rows, the limits
+// and the per-(tile, row) skip record (sub-tile max |T_base|, extrema of
+// T_base * alpha0). T_base itself is NOT streamed:
+//   stage 1 (one lane per row, no element work): a rigorous bound of |f1|
+//     over the whole tile proves most (row, candidate) blocks safe;
+//   stage 2 (rows that fail it): the lanes load that row of the T_base tile
+//     (1 KB, coalesced, L2) and evaluate the exact first FMA f_c + T alpha per
+//     element with the L R' part bounded;
+//   stage 3: the remaining R DFMA per element and a hi-word test; the exact
+//     path runs only where |f1| can exceed the limit.
+// Skipped work cannot change any score (tests/test_gpu_evaluate.py compares the
+// two kernels and the oracle).
+//
+// Flows kernel (k_sweep<true>, FlowResult requested): every element computed,
+// T_base tiles streamed with the rows, max |f1| folded for every branch.
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
@@ -37,23 +46,30 @@ constexpr int kTileK = 32 * kKpl;        // contingencies per CTA tile
 constexpr int kWarps = 16;
 constexpr int kThreads = 32 * kWarps;
 constexpr int kChunk = 32;               // branches per pipeline stage
-constexpr int kStages = 3;
 constexpr int kMaxCand = kWarps;         // one candidate per warp
-constexpr int kGroupBlock = 8;           // candidate groups per CTA super-block (L2 reuse of T_base tiles)
-
-// candidates per warp for a given rank (register budget)
-__host__ __device__ constexpr int nc_for_rank(int) { return 1; }
-__host__ __device__ constexpr int cand_per_cta(int r) { return kWarps * nc_for_rank(r); }
-
-constexpr size_t kStageT = static_cast<size_t>(kChunk) * kTileK;           // doubles
-constexpr size_t kStageF = static_cast<size_t>(kMaxCand) * kChunk * kStride;  // doubles
-constexpr size_t kStageL = kChunk;                                         // doubles
-constexpr size_t kStageTm = static_cast<size_t>(kChunk) * kRec;           // skip record per row
-constexpr int kSubLanes = 32 / kTmaxSub;                                   // lanes per sub-tile
-static_assert(kTileK % kTmaxSub == 0 && kSubLanes * kTmaxSub == 32 && kTmaxSub == kStride, "sub-tile layout");
-constexpr size_t kStageDoubles = kStageT + kStageF + kStageL + kStageTm;
+constexpr int kGroupBlock = 8;           // candidate groups per CTA super-block (L2 reuse)
+constexpr int kMaxStages = 8;
+constexpr size_t kStageBudget = 200 * 1024;  // dynamic shared memory for the stage ring
+constexpr int kSubLanes = 32 / kTmaxSub;     // lanes per skip sub-tile
+static_assert(kTileK % kTmaxSub == 0 && kSubLanes * kTmaxSub == 32, "sub-tile layout");
 static_assert(kMaxCand == kGroupSlots && kChunk == kChunkRows, "sweep tiles must match the row layout");
-constexpr size_t kSmemBytes = kStages * kStageDoubles * sizeof(double) + 64;
+
+__host__ __device__ constexpr int cand_per_cta(int) { return kWarps; }
+
+// Stage ring geometry for rank R (doubles per stage, number of stages).
+template <int R, bool FULL>
+struct Ring {
+  static constexpr int S = row_stride(R);
+  static constexpr size_t T = FULL ? static_cast<size_t>(kChunk) * kTileK : 0;  // T_base tile rows
+  static constexpr size_t F = static_cast<size_t>(kMaxCand) * kChunk * S;       // candidate rows
+  static constexpr size_t L = kChunk;                                           // limits
+  static constexpr size_t M = FULL ? 0 : static_cast<size_t>(kChunk) * kRec;    // skip records
+  static constexpr size_t doubles = T + F + L + M;
+  static constexpr size_t fit = kStageBudget / (doubles * sizeof(double));
+  static constexpr int stages = fit < static_cast<size_t>(kMaxStages) ? static_cast<int>(fit) : kMaxStages;
+  static_assert(stages >= 2, "stage ring too small");
+};
+constexpr size_t kSmemBytes = kStageBudget + 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -91,250 +107,234 @@ struct CtaWork {
   int group;
 };
 
-// Producer: stage `s` <- chunk `i` (T tile rows, candidate rows, limits).
+// Producer: stage <- chunk i (T tile rows when FULL, the group's candidate
+// rows, limits, skip records when not FULL).
+template <int R, bool FULL>
 __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, int i,
                                            double* stage, uint64_t* bar) {
+  using Rg = Ring<R, FULL>;
   const int e0 = i * kChunk;
   const int rows = min(kChunk, g.E - e0);
-  const uint32_t bt = rows * kTileK * sizeof(double);
-  const uint32_t bf = kStageF * sizeof(double);  // the group's rows of this chunk: one contiguous block
+  const uint32_t bt = FULL ? rows * kTileK * sizeof(double) : 0;
+  const uint32_t bf = Rg::F * sizeof(double);  // the group's rows of this chunk: one contiguous block
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
-  const uint32_t bm = rows * kRec * sizeof(double);
+  const uint32_t bm = FULL ? 0 : rows * kRec * sizeof(double);
   mbar_expect_tx(bar, bt + bf + bl + bm);
-  bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
-  bulk_g2s(stage + kStageT, b.feat + feat_index(w.group * kGroupSlots, b.nchunks, e0), bf, bar);
-  bulk_g2s(stage + kStageT + kStageF, g.br_lim + e0, bl, bar);
-  bulk_g2s(stage + kStageT + kStageF + kStageL, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kRec,
-           bm, bar);
+  if (FULL) bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
+  bulk_g2s(stage + Rg::T, b.feat + feat_index(w.group * kGroupSlots, b.nchunks, e0, R), bf, bar);
+  bulk_g2s(stage + Rg::T + Rg::F, g.br_lim + e0, bl, bar);
+  if (!FULL)
+    bulk_g2s(stage + Rg::T + Rg::F + Rg::L, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kRec, bm,
+             bar);
 }
 
-template <int R, int NC, bool FULL>
+template <int R, bool FULL>
 __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
                                           uint64_t* bars, int* release, double* rmax_s, double* amax_s) {
+  using Rg = Ring<R, FULL>;
+  constexpr int S = Rg::S, NST = Rg::stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = tile * kTileK + lane * kKpl;
   // per-(candidate, contingency) operands in registers
-  double alpha[NC][kKpl], rr[NC][kKpl][R > 0 ? R : 1], energy[NC][kKpl];
-  bool kval[NC][kKpl];
-  int kbr[kKpl];
-  int cid[NC], rem[NC][kMaxRemovedSweep];
-#pragma unroll
-  for (int i = 0; i < kKpl; ++i) kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    const int slot = warp * NC + j;
-    cid[j] = slot < w.ncand ? w.cand[slot] : -1;
-    if (cid[j] >= 0 && b.status[cid[j]] != 0) cid[j] = -1;  // islanded by the small solve in k_prep
-    const int c = cid[j] >= 0 ? cid[j] : w.cand[0];
-    const double* kd = b.kdat + (static_cast<size_t>(c) * g.Kpad + kb) * kStride;
+  double alpha[kKpl], rr[kKpl][R > 0 ? R : 1], energy[kKpl];
+  bool kval[kKpl];
+  int kbr[kKpl], rem[kMaxRemovedSweep];
+  int cid = warp < w.ncand ? w.cand[warp] : -1;
+  if (cid >= 0 && b.status[cid] != 0) cid = -1;  // islanded by the small solve in k_prep
+  {
+    const int c = cid >= 0 ? cid : w.cand[0];
+    const double* kd = b.kdat + static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(kb) * S;
     const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad + kb;
 #pragma unroll
     for (int i = 0; i < kKpl; ++i) {
-      alpha[j][i] = kd[i * kStride];
+      kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
+      alpha[i] = kd[i * S];
 #pragma unroll
-      for (int q = 0; q < R; ++q) rr[j][i][q] = kd[i * kStride + 1 + q];
-      energy[j][i] = 0.0;
-      kval[j][i] = cid[j] >= 0 && kf[i] == 0;
+      for (int q = 0; q < R; ++q) rr[i][q] = kd[i * S + 1 + q];
+      energy[i] = 0.0;
+      kval[i] = cid >= 0 && kf[i] == 0;
     }
 #pragma unroll
-    for (int q = 0; q < kMaxRemovedSweep; ++q) rem[j][q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
+    for (int q = 0; q < kMaxRemovedSweep; ++q) rem[q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
   }
   // Skip-bound operands in shared memory (invalid contingencies carry alpha 0):
-  // max |alpha - alpha0| per sub-tile, asub[j][s] (the candidate's departure
-  // from the unchanged topology's flow factors), and the tile max of each
-  // |R'_q| as a row weight vector rms[j][slot] (0 for f_c and padding).
-  double* rms = rmax_s + warp * NC * kStride;
-  double* asub = amax_s + warp * NC * kTmaxSub;
-  if (lane < NC * kStride) rms[lane] = 0.0;
-  __syncwarp();
-  double a0[kKpl];
-#pragma unroll
-  for (int k = 0; k < kKpl; ++k) a0[k] = g.alpha0[kb + k];
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
+  // max |alpha - alpha0| per sub-tile, asub[s] (the candidate's departure from
+  // the unchanged topology's flow factors), and the tile max of each |R'_q| as
+  // a row weight vector rms[slot] (0 for f_c and padding).
+  double* rms = rmax_s + warp * kStride;
+  double* asub = amax_s + warp * kTmaxSub;
+  if (!FULL) {
+    if (lane < kStride) rms[lane] = 0.0;
+    __syncwarp();
     double a = 0.0;
 #pragma unroll
-    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[j][k] - a0[k]));
+    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[k] - g.alpha0[kb + k]));
 #pragma unroll
     for (int o = kSubLanes / 2; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-    if (lane % kSubLanes == 0) asub[j * kTmaxSub + lane / kSubLanes] = a * (1.0 + 1e-12);
+    if (lane % kSubLanes == 0) asub[lane / kSubLanes] = a * (1.0 + 1e-12);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       double r = 0.0;
 #pragma unroll
-      for (int k = 0; k < kKpl; ++k) r = fmax(r, fabs(rr[j][k][q]));
+      for (int k = 0; k < kKpl; ++k) r = fmax(r, fabs(rr[k][q]));
 #pragma unroll
       for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
-      if (lane == 0) rms[j * kStride + 1 + q] = r * (1.0 + 1e-12);
+      if (lane == 0) rms[1 + q] = r * (1.0 + 1e-12);
     }
+    __syncwarp();
   }
-  __syncwarp();
 
   const int nchunks = (g.E + kChunk - 1) / kChunk;
-  unsigned rows_computed = 0, rows_offered = 0, rows_exact = 0, rows_partial = 0;  // skip statistics, one atomic per warp at the end
+  unsigned rows_computed = 0, rows_offered = 0, rows_exact = 0, rows_partial = 0;  // skip statistics
   if (threadIdx.x == 0)
-    for (int s = 0; s < kStages && s < nchunks; ++s)
-      issue_chunk(g, b, w, tile, s, smem + s * kStageDoubles, bars + s);
+    for (int s = 0; s < NST && s < nchunks; ++s)
+      issue_chunk<R, FULL>(g, b, w, tile, s, smem + s * Rg::doubles, bars + s);
 
   // exact path for one branch row: energies (registers) and fmax (atomicMax)
-  auto exact_row = [&](int e, double lim, const double (&f1)[NC][kKpl]) {
-    const unsigned long long lim_bits = static_cast<unsigned long long>(__double_as_longlong(lim));
+  auto exact_row = [&](int e, double lim, const double (&f1)[kKpl]) {
+    bool skip_row = false;
 #pragma unroll
-    for (int j = 0; j < NC; ++j) {
-      bool skip_row = false;
+    for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[q];
+    unsigned long long m = 0ull;  // max |f1| as the ordered bit pattern of a non-negative double
 #pragma unroll
-      for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[j][q];
-      unsigned long long m = 0ull;  // max |f1| as the ordered bit pattern of a non-negative double
-#pragma unroll
-      for (int k = 0; k < kKpl; ++k) {
-        if (!kval[j][k] || skip_row || e == kbr[k]) continue;  // the outaged branch carries 0
-        const double a = fabs(f1[j][k]);
-        if (a > lim) energy[j][k] += a - lim;
-        m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
-      }
-      if (cid[j] < 0) continue;
-      unsigned long long* fmx = b.fmax + static_cast<size_t>(cid[j]) * g.E;
-      if (FULL) {
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
-        if (lane == 0 && m > 0ull) atomicMax(fmx + e, m);
-      } else if (m > lim_bits) {
-        atomicMax(fmx + e, m);
-      }
+    for (int k = 0; k < kKpl; ++k) {
+      if (!kval[k] || skip_row || e == kbr[k]) continue;  // the outaged branch carries 0
+      const double a = fabs(f1[k]);
+      if (a > lim) energy[k] += a - lim;
+      m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
     }
+    if (cid < 0) return;
+    unsigned long long* fmx = b.fmax + static_cast<size_t>(cid) * g.E;
+    if (FULL) {
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) m = max(m, __shfl_xor_sync(0xffffffffu, m, o));
+      if (lane == 0 && m > 0ull) atomicMax(fmx + e, m);
+    } else if (m > static_cast<unsigned long long>(__double_as_longlong(lim))) {
+      atomicMax(fmx + e, m);
+    }
+  };
+  // remaining R FMAs of one row (L from shared memory), then the exact path
+  // when `test` is off or some |f1| can exceed the limit (hi-word test)
+  auto finish_row = [&](int e, double lim, const double* fr, double (&f1)[kKpl], bool test) {
+    double fl[R > 0 ? R : 1];
+#pragma unroll
+    for (int q = 0; q < R; ++q) fl[q] = fr[1 + q];
+    uint32_t mx = 0u;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k) {
+      double acc = f1[k];
+#pragma unroll
+      for (int q = 0; q < R; ++q) acc = fma(fl[q], rr[k][q], acc);
+      f1[k] = acc;
+      mx = max(mx, hi_abs(acc));
+    }
+    if (!test || __any_sync(0xffffffffu, mx >= hi_abs(lim))) {
+      exact_row(e, lim, f1);
+      return true;
+    }
+    return false;
   };
 
   for (int i = 0; i < nchunks; ++i) {
-    const int s = i % kStages;
-    const double* st = smem + s * kStageDoubles;
-    mbar_wait(bars + s, (i / kStages) & 1);
+    const int s = i % NST;
+    const double* st = smem + s * Rg::doubles;
+    mbar_wait(bars + s, (i / NST) & 1);
     const int e0 = i * kChunk;
     const int rows = min(kChunk, g.E - e0);
-    const double* sT = st + lane * kKpl;
-    const double* sF = st + kStageT + static_cast<size_t>(warp) * NC * kChunk * kStride;
-    const double* sL = st + kStageT + kStageF;
-    // Stage 1 (one lane per row): rows that can reach their limit for one of
-    // the warp's candidates. With alpha = alpha0 + delta (alpha0: unchanged
-    // topology) every element of the tile satisfies
-    //   f1 = f_c + T alpha0 + T delta + L R'  in  [f_c + D0min - w, f_c + D0max + w],
-    //   w = max_s max|T_base|_s max|delta|_s + lrb,  lrb = sum_q |L_q| max|R'_q|
-    // (D0max / D0min: max / min of T_base * alpha0 over the tile, precomputed;
-    // s: sub-tiles; R' maxima over the tile). A relative slack of 1e-12 on
-    // every term covers the rounding of the computed f1. For stage 2 each lane
-    // keeps, per candidate, the high word of lim (1 - 1e-12) - lrb (0 when that
-    // is not positive).
-    unsigned need = rows >= 32 ? 0xffffffffu : ((1u << rows) - 1u);
-    uint32_t thr_lane[NC];
-#pragma unroll
-    for (int j = 0; j < NC; ++j) thr_lane[j] = 0u;
-    if (!FULL) {
-      bool hot = false;
-      if (lane < rows) {
-        const double lim = sL[lane] * (1.0 - 1e-12);
-        const double* rec = st + kStageT + kStageF + kStageL + lane * kRec;
-        const double2* tmr = reinterpret_cast<const double2*>(rec);
-        const double2 d0 = *reinterpret_cast<const double2*>(rec + kTmaxSub);
-#pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          // the row's 4 double2 read in a lane-rotated order (conflict-free),
-          // each weighted by its slots' R' maxima
-          const double2* fr = reinterpret_cast<const double2*>(sF + (static_cast<size_t>(j) * kChunk + lane) * kStride);
-          const double2* wr = reinterpret_cast<const double2*>(rms + j * kStride);
-          const double2* ar = reinterpret_cast<const double2*>(asub + j * kTmaxSub);
-          double lrb = 0.0, fc = 0.0, ta = 0.0;
-#pragma unroll
-          for (int i = 0; i < kStride / 2; ++i) {
-            const int idx = (i + (lane >> 1)) & (kStride / 2 - 1);
-            const double2 p2 = fr[idx];
-            const double2 w2 = wr[idx];
-            const double2 t2 = tmr[idx];
-            const double2 a2 = ar[idx];
-            lrb = fma(fabs(p2.x), w2.x, lrb);
-            lrb = fma(fabs(p2.y), w2.y, lrb);
-            fc = idx == 0 ? p2.x : fc;
-            ta = fmax(ta, fmax(t2.x * a2.x, t2.y * a2.y));
-          }
-          const double thr = lim - lrb;
-          thr_lane[j] = thr > 0.0 ? hi_abs(thr) : 0u;
-          const double w = ta + lrb;
-          const double slack = 1e-12 * (fabs(fc) + fmax(d0.x, -d0.y) + w);
-          hot |= (fc + d0.x + w + slack >= lim) || (fc + d0.y - w - slack <= -lim);
-        }
-      }
-      need = __ballot_sync(0xffffffffu, hot);
-      rows_partial += __popc(need);
-      rows_offered += rows;
-    }
-    // Stage 2 (two rows per step, loads issued before the FMA chains): the
-    // first FMA f_c + T alpha of every element is exact; the row goes on to the
-    // remaining R FMAs only when |f_c + T alpha| can reach lim - lrb (tested on
-    // high words: hi(|x|) < hi(t) implies |x| < t for non-negative t).
-    while (need) {
-      int els[2];
-      els[0] = __ffs(need) - 1;
-      need &= need - 1;
-      els[1] = need ? __ffs(need) - 1 : -1;
-      if (need) need &= need - 1;
-      const int nu = els[1] >= 0 ? 2 : 1;
-      double tv[2][kKpl], fc[2][NC], lim[2];
-      uint32_t thr[2][NC];
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        const int el = u < nu ? els[u] : els[0];
+    const double* sF = st + Rg::T + static_cast<size_t>(warp) * kChunk * S;
+    const double* sL = st + Rg::T + Rg::F;
+    if (FULL) {
+      const double* sT = st + lane * kKpl;
+      for (int el = 0; el < rows; ++el) {
         const double2 t01 = *reinterpret_cast<const double2*>(sT + el * kTileK);
         const double2 t23 = *reinterpret_cast<const double2*>(sT + el * kTileK + 2);
-        tv[u][0] = t01.x, tv[u][1] = t01.y, tv[u][2] = t23.x, tv[u][3] = t23.y;
-        lim[u] = sL[el];
+        const double tv[kKpl] = {t01.x, t01.y, t23.x, t23.y};
+        const double fc = sF[el * S];
+        double f1[kKpl];
 #pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          fc[u][j] = sF[(static_cast<size_t>(j) * kChunk + el) * kStride];
-          thr[u][j] = __shfl_sync(0xffffffffu, thr_lane[j], el);
-        }
+        for (int k = 0; k < kKpl; ++k) f1[k] = fma(tv[k], alpha[k], fc);
+        finish_row(e0 + el, sL[el], sF + el * S, f1, false);
       }
-      double f1[2][NC][kKpl];
-      bool hot[2] = {FULL, FULL && nu == 2};
+    } else {
+      // Stage 1 (one lane per row). With alpha = alpha0 + delta (alpha0: the
+      // unchanged topology) every element of the tile satisfies
+      //   f1 = f_c + T alpha0 + T delta + L R'  in  [f_c + D0min - w, f_c + D0max + w],
+      //   w = max_s max|T_base|_s max|delta|_s + lrb,  lrb = sum_q |L_q| max|R'_q|
+      // (D0max / D0min: max / min of T_base * alpha0 over the tile, precomputed;
+      // s: sub-tiles; R' maxima over the tile). A relative slack of 1e-12 on
+      // every term covers the rounding of the computed f1. Stage 2 tests
+      // against the high word of lim (1 - 1e-12) - lrb (0 when not positive).
+      bool hot = false;
+      uint32_t thr_lane = 0u;
+      if (lane < rows) {
+        const double lim = sL[lane] * (1.0 - 1e-12);
+        const double* rec = st + Rg::T + Rg::F + Rg::L + lane * kRec;
+        const double2* fr = reinterpret_cast<const double2*>(sF + lane * S);
+        const double2* wr = reinterpret_cast<const double2*>(rms);
+        double lrb = 0.0, fc = 0.0;
 #pragma unroll
-      for (int u = 0; u < 2; ++u)
+        for (int q = 0; q < S / 2; ++q) {
+          const double2 p2 = fr[q];
+          const double2 w2 = wr[q];
+          lrb = fma(fabs(p2.x), w2.x, lrb);
+          lrb = fma(fabs(p2.y), w2.y, lrb);
+          if (q == 0) fc = p2.x;
+        }
+        const double2* tmr = reinterpret_cast<const double2*>(rec);
+        const double2* ar = reinterpret_cast<const double2*>(asub);
+        double ta = 0.0;
 #pragma unroll
-        for (int j = 0; j < NC; ++j) {
+        for (int q = 0; q < kTmaxSub / 2; ++q) {
+          const double2 t2 = tmr[q];
+          const double2 a2 = ar[q];
+          ta = fmax(ta, fmax(t2.x * a2.x, t2.y * a2.y));
+        }
+        const double2 d0 = *reinterpret_cast<const double2*>(rec + kTmaxSub);
+        const double thr = lim - lrb;
+        thr_lane = thr > 0.0 ? hi_abs(thr) : 0u;
+        const double wd = ta + lrb;
+        const double slack = 1e-12 * (fabs(fc) + fmax(d0.x, -d0.y) + wd);
+        hot = (fc + d0.x + wd + slack >= lim) || (fc + d0.y - wd - slack <= -lim);
+      }
+      unsigned need = __ballot_sync(0xffffffffu, hot);
+      rows_partial += __popc(need);
+      rows_offered += rows;
+      // Stage 2: hot rows in batches of NB, T_base row loads issued before use
+      constexpr int NB = R >= 6 ? 1 : (R >= 4 ? 2 : 4);  // register budget (128 per thread at 512 threads)
+      const double* tk_rows = g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK + lane * kKpl;
+      while (need) {
+        int els[NB];
+        int nu = 0;
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          els[u] = need ? __ffs(need) - 1 : -1;
+          if (need) need &= need - 1, ++nu;
+        }
+        double2 t[NB][2];
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          const int el = els[u] >= 0 ? els[u] : els[0];
+          const double2* src = reinterpret_cast<const double2*>(tk_rows + static_cast<size_t>(el) * kTileK);
+          t[u][0] = __ldg(src);
+          t[u][1] = __ldg(src + 1);
+        }
+#pragma unroll
+        for (int u = 0; u < NB; ++u) {
+          if (u >= nu) break;
+          const int el = els[u];
+          const double fc = sF[el * S];
+          const uint32_t thr = __shfl_sync(0xffffffffu, thr_lane, el);
+          const double tv[kKpl] = {t[u][0].x, t[u][0].y, t[u][1].x, t[u][1].y};
+          double f1[kKpl];
           uint32_t m = 0u;
 #pragma unroll
           for (int k = 0; k < kKpl; ++k) {
-            f1[u][j][k] = fma(tv[u][k], alpha[j][k], fc[u][j]);
-            m = max(m, hi_abs(f1[u][j][k]));
+            f1[k] = fma(tv[k], alpha[k], fc);
+            m = max(m, hi_abs(f1[k]));
           }
-          if (!FULL) hot[u] |= m >= thr[u][j];
-        }
-      if (!FULL) {
-        hot[0] = __any_sync(0xffffffffu, hot[0]);
-        hot[1] = __any_sync(0xffffffffu, hot[1]) && nu == 2;
-      }
-#pragma unroll
-      for (int u = 0; u < 2; ++u) {
-        if (!hot[u]) continue;
-        ++rows_computed;
-        const int el = els[u];
-        double fl[NC][R > 0 ? R : 1];
-#pragma unroll
-        for (int j = 0; j < NC; ++j) {
-          const double* fr = sF + (static_cast<size_t>(j) * kChunk + el) * kStride;
-#pragma unroll
-          for (int q = 0; q < R; ++q) fl[j][q] = fr[1 + q];
-        }
-        uint32_t mx = 0u;
-#pragma unroll
-        for (int j = 0; j < NC; ++j)
-#pragma unroll
-          for (int k = 0; k < kKpl; ++k) {
-            double acc = f1[u][j][k];
-#pragma unroll
-            for (int q = 0; q < R; ++q) acc = fma(fl[j][q], rr[j][k][q], acc);
-            f1[u][j][k] = acc;
-            mx = max(mx, hi_abs(acc));
-          }
-        if (FULL || mx >= hi_abs(lim[u])) {
-          exact_row(e0 + el, lim[u], f1[u]);
-          ++rows_exact;
+          if (!__any_sync(0xffffffffu, m >= thr)) continue;
+          ++rows_computed;
+          rows_exact += finish_row(e0 + el, sL[el], sF + el * S, f1, true) ? 1u : 0u;
         }
       }
     }
@@ -346,9 +346,9 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       if (done == kWarps - 1) {
         release[s] = 0;
         __threadfence_block();
-        if (i + kStages < nchunks) {
+        if (i + NST < nchunks) {
           asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_chunk(g, b, w, tile, i + kStages, smem + s * kStageDoubles, bars + s);
+          issue_chunk<R, FULL>(g, b, w, tile, i + NST, smem + s * Rg::doubles, bars + s);
         }
       }
     }
@@ -359,30 +359,28 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     atomicAdd(b.rows_done + 2, static_cast<unsigned long long>(rows_exact));
     atomicAdd(b.rows_done + 3, static_cast<unsigned long long>(rows_partial));
   }
-#pragma unroll
-  for (int j = 0; j < NC; ++j) {
-    if (cid[j] < 0) continue;
-    double* en = b.energy + static_cast<size_t>(cid[j]) * g.Kall;
+  if (cid >= 0) {
+    double* en = b.energy + static_cast<size_t>(cid) * g.Kall;
 #pragma unroll
     for (int k = 0; k < kKpl; ++k)
-      if (kval[j][k] && kb + k < g.Ks) en[g.ks_cont[kb + k]] = energy[j][k];
+      if (kval[k] && kb + k < g.Ks) en[g.ks_cont[kb + k]] = energy[k];
   }
 }
 
 // CTA order: super-blocks of `gblock` candidate groups x all tiles, tile-major
 // inside a super-block, so the CTAs resident at one time share each T_base
-// tile across gblock groups (one HBM read of a tile per super-block instead of
-// per group) while the super-block's candidate rows stay in L2 across its tiles.
+// tile across gblock groups while the super-block's candidate rows stay in L2
+// across its tiles.
 template <bool FULL>
 __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CtaWork w;
   __shared__ int r_s;
-  __shared__ int release[kStages];
+  __shared__ int release[kMaxStages];
   __shared__ __align__(16) double rmax_s[kWarps * kStride];
   __shared__ __align__(16) double amax_s[kWarps * kTmaxSub];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
-  double* smem = reinterpret_cast<double*>(smem_raw + 64);
+  double* smem = reinterpret_cast<double*>(smem_raw + 128);
   const int per_sb = gblock * ntiles;
   const int sb = static_cast<int>(blockIdx.x) / per_sb, rr = static_cast<int>(blockIdx.x) % per_sb;
   const int g0 = sb * gblock, gg = min(gblock, ngroups - g0);
@@ -399,19 +397,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
       if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
     w.ncand = n;
     w.group = group;
-    for (int s = 0; s < kStages; ++s) mbar_init(bars + s, 1), release[s] = 0;
+    for (int s = 0; s < kMaxStages; ++s) mbar_init(bars + s, 1), release[s] = 0;
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   switch (r_s) {
-    case 0: sweep_cta<0, nc_for_rank(0), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 1: sweep_cta<1, nc_for_rank(1), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 2: sweep_cta<2, nc_for_rank(2), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 3: sweep_cta<3, nc_for_rank(3), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 4: sweep_cta<4, nc_for_rank(4), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 5: sweep_cta<5, nc_for_rank(5), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 6: sweep_cta<6, nc_for_rank(6), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    default: sweep_cta<7, nc_for_rank(7), FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 0: sweep_cta<0, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 1: sweep_cta<1, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 2: sweep_cta<2, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 3: sweep_cta<3, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 4: sweep_cta<4, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 5: sweep_cta<5, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 6: sweep_cta<6, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    default: sweep_cta<7, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
   }
 }
 
@@ -470,7 +468,7 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     configured = true;
   }
-  // group slots: every bucket rounds up to whole groups of >= kWarps candidates
+  // group slots: every bucket rounds up to whole groups of kWarps candidates
   static const int gblock_env = [] {
     const char* v = std::getenv("TGB_SWEEP_GROUP_BLOCK");
     return v ? std::max(1, std::atoi(v)) : 0;
