@@ -4,6 +4,8 @@
 // Reference path replaced: DcContext::evaluate_batch -> evaluate ->
 // apply_topology / screen_contingencies / compute_scores
 // (dc_engine.cpp:147-468). See topo.cuh for the low-rank formulation.
+#include <algorithm>
+
 #include "engine.cuh"
 #include "topo.cuh"
 
@@ -12,6 +14,7 @@ namespace tgb {
 namespace {
 
 constexpr int kPrepThreads = 256;
+constexpr size_t kPrepZsmBytes = 0;  // Z = X [U | V] kept in shared memory up to this size
 
 // ---------------------------------------------------------------- K2a analysis
 // Topology analysis (one warp-sized CTA per candidate, thread 0 serial, so a
@@ -46,17 +49,20 @@ __global__ void __launch_bounds__(kAnalyzeThreads) k_analyze(DevGrid g, Batch b,
 }
 
 // ---------------------------------------------------------------- K2 prep
-// One CTA per candidate (grid-stride over candidates; Z scratch per CTA slot).
+// One CTA per candidate (grid-stride over candidates). Z = X [U | V] lives in
+// shared memory (row stride row_stride(r)) when it fits in `zsm_doubles`, else
+// in the CTA's global scratch slot.
 __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch,
-                                                       int zslots) {
-  extern __shared__ uint32_t bits[];
+                                                       int zslots, int zsm_doubles) {
+  extern __shared__ __align__(16) uint32_t bits[];
   __shared__ Topo t;
   __shared__ double gram[kSweepRank * kSweepRank];
   __shared__ double thv[kSweepRank];
   const int words = (g.E + 31) >> 5;
   uint32_t* mv_bits = bits;
   uint32_t* rm_bits = bits + words;
-  double* zbuf = zscratch + static_cast<size_t>(blockIdx.x) * g.Nr * kStride;
+  double* zsm = reinterpret_cast<double*>(bits + ((2 * words + 3) & ~3));
+  double* zglob = zscratch + static_cast<size_t>(blockIdx.x) * g.Nr * kStride;
   for (int c = blockIdx.x; c < b.n; c += gridDim.x) {
     const int slot = b.slot[c];
     if (slot < 0) continue;  // islanded (or over capacity) by the analysis: status already set
@@ -64,9 +70,11 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
     const uint32_t* tb = b.tbits + static_cast<size_t>(c) * 2 * words;
     for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = tb[i];
     __syncthreads();
-    build_z(g, t, zbuf, kStride);
+    const int ldz = row_stride(t.ns + t.nv);
+    double* zbuf = static_cast<size_t>(g.Nr) * ldz <= static_cast<size_t>(zsm_doubles) ? zsm : zglob;
+    build_z(g, t, zbuf, ldz);
     __syncthreads();
-    gram_terms(g, t, zbuf, kStride, gram, kSweepRank, thv);
+    gram_terms(g, t, zbuf, ldz, gram, kSweepRank, thv);
     __syncthreads();
     if (threadIdx.x == 0) small_solve(t, gram, kSweepRank, thv);
     __syncthreads();
@@ -82,7 +90,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
     // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0...]
     for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
       double phi[kMaxSplits], rho[kMaxCols];
-      const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, kStride, e, phi, rho);
+      const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
       double row[kStride];
 #pragma unroll
       for (int i = 0; i < kStride; ++i) row[i] = 0.0;
@@ -109,7 +117,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       if (k < g.Ks) {
         const int beta = g.ks_branch[k];
         double phi[kMaxSplits], rho[kMaxCols];
-        const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, kStride, beta, phi, rho);
+        const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, beta, phi, rho);
         flag = 0;
         if (on) {
           double rk[kSweepRank];
@@ -278,14 +286,24 @@ __global__ void __launch_bounds__(kPrepThreads) k_special(DevGrid g, Batch b, in
 
 // ---------------------------------------------------------------- K5 finish
 // dc_engine.cpp:390-437: metric sums, fitness, worst-k list; islanded genomes
-// get the sentinel score with lambda_d/s/r filled.
-__global__ void __launch_bounds__(256) k_finish(DevGrid g, Batch b, int n_a, int n_d) {
-  __shared__ double s_o[8], s_b[8];
-  __shared__ int s_c[8], s_c0[8], s_isl[8];
-  __shared__ double best_v[8];
-  __shared__ int best_i[8];
-  const int c = blockIdx.x;
+// get the sentinel score with lambda_d/s/r filled. One warp per candidate
+// (warp reductions only). Worst-k (dc_engine.cpp:400-420: energy > 0, sorted
+// by energy desc then index asc, first worst_k): the positive energies are
+// compacted into the warp's shared list, then worst_k selection rounds run on
+// the list (or on all contingencies when it overflows).
+constexpr int kFinishWarps = 8;
+constexpr int kFinishList = 256;
+
+__device__ __forceinline__ bool worst_before(double v, int k, double u, int j) {
+  return v > u || (v == u && k < j);
+}
+
+__global__ void __launch_bounds__(32 * kFinishWarps) k_finish(DevGrid g, Batch b, int n_a, int n_d) {
+  __shared__ double wl_v[kFinishWarps][kFinishList];
+  __shared__ int wl_i[kFinishWarps][kFinishList];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c = blockIdx.x * kFinishWarps + wid;
+  if (c >= b.n) return;
   const int* slots = b.genomes + static_cast<size_t>(c) * (n_a + n_d);
   int ld = 0, ls = 0, lr = 0;
   for (int k = 0; k < n_d; ++k) ld += slots[n_a + k] >= 0;
@@ -294,7 +312,7 @@ __global__ void __launch_bounds__(256) k_finish(DevGrid g, Batch b, int n_a, int
   Scores& o = b.out;
   const int st = b.status[c];
   if (st != 0) {
-    if (threadIdx.x == 0) {
+    if (lane == 0) {
       o.lambda_o[c] = 0.0;
       o.lambda_c[c] = 0;
       o.lambda_c0[c] = 0;
@@ -311,22 +329,22 @@ __global__ void __launch_bounds__(256) k_finish(DevGrid g, Batch b, int n_a, int
     }
     return;
   }
-  const int slot = b.slot[c];
+  const int slot = b.slot[c], rank = b.rank[c];
   const unsigned long long* fm = b.fmax + static_cast<size_t>(c) * g.E;
   const unsigned long long* fb = b.fbus + static_cast<size_t>(c) * g.E;
   double so = 0.0, sb = 0.0;
   int nc = 0, nc0 = 0;
-  for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
+  for (int e = lane; e < g.E; e += 32) {
     const double lim = g.br_lim[e];
     const double m = __longlong_as_double(static_cast<long long>(fm[e]));
     const double mb = __longlong_as_double(static_cast<long long>(fb[e]));
     if (m > lim) so += m - lim, ++nc;
-    if (fabs(b.feat[feat_index(slot, b.nchunks, e, b.rank[c])]) > lim) ++nc0;
+    if (fabs(b.feat[feat_index(slot, b.nchunks, e, rank)]) > lim) ++nc0;
     if (mb > lim) sb += mb - lim;
   }
   int isl = 0;
   const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad;
-  for (int k = threadIdx.x; k < g.Ks; k += blockDim.x) isl += kf[k] == 1;
+  for (int k = lane; k < g.Ks; k += 32) isl += kf[k] == 1;
 #pragma unroll
   for (int d = 16; d > 0; d >>= 1) {
     so += __shfl_xor_sync(0xffffffffu, so, d);
@@ -335,21 +353,15 @@ __global__ void __launch_bounds__(256) k_finish(DevGrid g, Batch b, int n_a, int
     nc0 += __shfl_xor_sync(0xffffffffu, nc0, d);
     isl += __shfl_xor_sync(0xffffffffu, isl, d);
   }
-  if (lane == 0) s_o[wid] = so, s_b[wid] = sb, s_c[wid] = nc, s_c0[wid] = nc0, s_isl[wid] = isl;
-  __syncthreads();
-  const double* en = b.energy + static_cast<size_t>(c) * g.Kall;
-  if (threadIdx.x == 0) {
-    double lo = 0.0, lb = 0.0;
-    int lc = 0, lc0 = 0, iso = b.isl_out[c];
-    for (int w = 0; w < 8; ++w) lo += s_o[w], lb += s_b[w], lc += s_c[w], lc0 += s_c0[w], iso += s_isl[w];
-    const int isb = b.isl_bus[c];
-    lo += b.params.penalty * iso;
-    lb += b.params.penalty * isb;
-    double fit = -(lo + b.params.weight_c0 * lc0 + b.params.weight_c * lc);
+  if (lane == 0) {
+    const int iso = b.isl_out[c] + isl, isb = b.isl_bus[c];
+    const double lo = so + b.params.penalty * iso;
+    const double lb = sb + b.params.penalty * isb;
+    double fit = -(lo + b.params.weight_c0 * nc0 + b.params.weight_c * nc);
     if (b.params.variant == 2) fit -= fmax(lb - b.params.lambda_b_pre, 0.0);
     o.lambda_o[c] = lo;
-    o.lambda_c[c] = lc;
-    o.lambda_c0[c] = lc0;
+    o.lambda_c[c] = nc;
+    o.lambda_c0[c] = nc0;
     o.lambda_b[c] = lb;
     o.lambda_d[c] = ld;
     o.lambda_s[c] = ls;
@@ -360,48 +372,50 @@ __global__ void __launch_bounds__(256) k_finish(DevGrid g, Batch b, int n_a, int
     o.isl_out[c] = iso;
     o.isl_bus[c] = isb;
   }
-  // worst-k: repeated block argmax under the order (energy desc, index asc)
+  // compact the positive energies (ascending contingency order)
+  const double* en = b.energy + static_cast<size_t>(c) * g.Kall;
+  double* lv = wl_v[wid];
+  int* li = wl_i[wid];
+  int npos = 0;
+  for (int k0 = 0; k0 < g.Kall; k0 += 32) {
+    const int k = k0 + lane;
+    const double v = k < g.Kall ? en[k] : 0.0;
+    const unsigned m = __ballot_sync(0xffffffffu, v > 0.0);
+    const int at = npos + __popc(m & ((1u << lane) - 1u));
+    if (v > 0.0 && at < kFinishList) lv[at] = v, li[at] = k;
+    npos += __popc(m);
+  }
+  __syncwarp();
+  const bool listed = npos <= kFinishList;
+  const int n_scan = listed ? npos : g.Kall;
+  const int wk = b.params.worst_k;
   double pv = CUDART_INF;
-  int pi = -1;
-  int nsel = 0;
-  for (int round = 0; round < b.params.worst_k; ++round) {
+  int pi = -1, nsel = 0;
+  for (int round = 0; round < wk; ++round) {
     double bv = 0.0;
     int bi = -1;
-    for (int k = threadIdx.x; k < g.Kall; k += blockDim.x) {
-      const double v = en[k];
-      if (!(v > 0.0)) continue;
-      const bool after = v < pv || (v == pv && k > pi);
-      if (!after) continue;
-      if (bi < 0 || v > bv || (v == bv && k < bi)) bv = v, bi = k;
+    for (int i = lane; i < n_scan; i += 32) {
+      const double v = listed ? lv[i] : en[i];
+      const int k = listed ? li[i] : i;
+      if (!(v > 0.0) || !worst_before(pv, pi, v, k)) continue;  // already selected
+      if (bi < 0 || worst_before(v, k, bv, bi)) bv = v, bi = k;
     }
 #pragma unroll
     for (int d = 16; d > 0; d >>= 1) {
       const double ov = __shfl_xor_sync(0xffffffffu, bv, d);
       const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
-      if (oi >= 0 && (bi < 0 || ov > bv || (ov == bv && oi < bi))) bv = ov, bi = oi;
+      if (oi >= 0 && (bi < 0 || worst_before(ov, oi, bv, bi))) bv = ov, bi = oi;
     }
-    if (lane == 0) best_v[wid] = bv, best_i[wid] = bi;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      double v = 0.0;
-      int i = -1;
-      for (int w = 0; w < 8; ++w)
-        if (best_i[w] >= 0 && (i < 0 || best_v[w] > v || (best_v[w] == v && best_i[w] < i))) v = best_v[w], i = best_i[w];
-      best_v[0] = v;
-      best_i[0] = i;
+    if (bi < 0) break;
+    if (lane == 0) {
+      o.worst_idx[static_cast<size_t>(c) * wk + round] = bi;
+      o.worst_val[static_cast<size_t>(c) * wk + round] = bv;
     }
-    __syncthreads();
-    pv = best_v[0];
-    pi = best_i[0];
-    __syncthreads();
-    if (pi < 0) break;
-    if (threadIdx.x == 0) {
-      o.worst_idx[static_cast<size_t>(c) * b.params.worst_k + round] = pi;
-      o.worst_val[static_cast<size_t>(c) * b.params.worst_k + round] = pv;
-    }
+    pv = bv;
+    pi = bi;
     ++nsel;
   }
-  if (threadIdx.x == 0) o.worst_n[c] = nsel;
+  if (lane == 0) o.worst_n[c] = nsel;
 }
 
 // Dense copy of the candidate base flows (f_c) for callers that ask for them.
@@ -444,8 +458,18 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
   k_analyze<<<b.n < 65535 ? b.n : 65535, kAnalyzeThreads, bits_bytes, stream>>>(g, b, n_a, n_d);
   ++launched;
   launch_bucket(b, stream, &launched);
+  // Z in shared memory up to kPrepZsmBytes (0: Z in the global scratch slots,
+  // measured faster: the small serial solve needs many resident CTAs per SM)
+  const size_t bits_al = (bits_bytes + 15) & ~size_t{15};
+  const size_t zsm_bytes = std::min<size_t>(static_cast<size_t>(g.Nr) * kStride * sizeof(double), kPrepZsmBytes);
+  const int zsm_doubles = static_cast<int>(zsm_bytes / sizeof(double));
+  static size_t prep_smem_set = 0;
+  if (bits_al + zsm_bytes > 48 * 1024 && bits_al + zsm_bytes > prep_smem_set) {
+    cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bits_al + zsm_bytes));
+    prep_smem_set = bits_al + zsm_bytes;
+  }
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
-  k_prep<<<prep_grid, kPrepThreads, bits_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots);
+  k_prep<<<prep_grid, kPrepThreads, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots, zsm_doubles);
   ++launched;
   if (g.Ks > 0) launch_sweep(g, b, full, stream, sweep_begin, sweep_end, &launched);
   if (g.Kx + g.Kb > 0) {
@@ -454,7 +478,7 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
     k_special<<<grid, kPrepThreads, bits_bytes, stream>>>(g, b, n_a, n_d, full ? 1 : 0, s.zspecial);
     ++launched;
   }
-  k_finish<<<b.n, 256, 0, stream>>>(g, b, n_a, n_d);
+  k_finish<<<(b.n + kFinishWarps - 1) / kFinishWarps, 32 * kFinishWarps, 0, stream>>>(g, b, n_a, n_d);
   ++launched;
   if (kernels) *kernels = launched;
 }
