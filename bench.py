@@ -252,15 +252,20 @@ def main():
     P.sweep_timing(ctx, True)
     P.sweep_rows(ctx)  # reset the skip counters
     flops = 0.0
-    E, Ks = info["n_branches"], info["n_single"]
+    E, Ks, Kp = info["n_branches"], info["n_single"], info["k_padded"]
     n_prof = 5
     isl = 0
+    alg_bytes = 0.0
     for _ in range(n_prof):
         sess.step(1)
         r = P.batch_ranks(ctx, B)
         live = r[r >= 0]
         isl += int((r < 0).sum())
         flops += float(E) * Ks * float(np.sum(2.0 + 2.0 * live))
+        # compulsory sweep traffic: each swept candidate's branch and contingency
+        # rows (row_stride(r) doubles each) + the skip records + T_base read once
+        stride = (live + 2) & ~1
+        alg_bytes += 8.0 * float(np.sum(stride)) * (E + Kp) + 8.0 * E * Kp * (1 + 10 / 128)
     sweep_ms, sweep_n = P.sweep_timing(ctx, False)
     rows_done, rows_offered, rows_overloaded, rows_partial = P.sweep_rows(ctx)
     torch.cuda.synchronize()
@@ -273,15 +278,27 @@ def main():
     # (f_c + T alpha), blocks past the per-element bound also the R FMAs of L R';
     # skipped work cannot change any score
     executed_frac = ((partial_frac + computed_frac * mean_rank) / (1.0 + mean_rank)) if rows_offered else 1.0
-    achieved_tflops = dense_tflops * executed_frac
+    executed_tflops = dense_tflops * executed_frac
     peak = P.fp64_peak_tflops(dev)
     traffic = None
+    ncu = {}
     prof_json = os.path.join(ROOT, "profiles", "sweep_ncu_summary.json")
     if os.path.exists(prof_json):
         try:
-            traffic = json.load(open(prof_json)).get(args.config, {}).get("dram_bytes_per_launch")
+            ncu = json.load(open(prof_json)).get(args.config, {})
+            traffic = ncu.get("dram_bytes_per_launch")
         except (OSError, ValueError):
-            traffic = None
+            ncu = {}
+
+    # ---- the dense sweep (FlowResult path, every element computed, no skip) on
+    #      this step's candidates: the kernel's own FP64 roofline fraction
+    P.sweep_timing(ctx, True)
+    dense_g = sess.offspring()
+    ctx.evaluate_arrays(dense_g, 3, 2, flows=True)
+    dense_ms, dense_n = P.sweep_timing(ctx, False)
+    rd = P.batch_ranks(ctx, B)
+    dense_flops = float(E) * Ks * float(np.sum(2.0 + 2.0 * rd[rd >= 0]))
+    dense_kernel_tflops = dense_flops / (dense_ms / max(dense_n, 1) * 1e-3) / 1e12
 
     # ---- end to end through the reference-facing call with pinned host buffers
     #      (DcContext::evaluate_batch: H2D genomes, evaluate, D2H scores each step)
@@ -341,22 +358,32 @@ def main():
                        "step": "one MapElites generation: mutate/crossover + full N-1 evaluation + archive insert",
                        "archive_entries": len(snap.entries), "best_fitness": snap.best_fitness},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "fp64", "kernel": "k_sweep (fused N-1 sweep)", "achieved": achieved_tflops,
-                         "peak": peak, "unit": "TFLOP/s", "frac": achieved_tflops / peak if peak else None,
-                         "traffic": traffic, "peak_source": "DFMA microbenchmark on this GPU in this run "
-                                                            "(MEASURED_PEAKS.json has no FP64 figure)",
-                         "flops_per_launch": flops / n_prof * executed_frac, "avg_launch_ms": avg_ms,
-                         "dense_flops_per_launch": flops / n_prof, "dense_equivalent_tflops": dense_tflops,
-                         "computed_block_fraction": computed_frac, "first_fma_block_fraction": partial_frac,
-                         "executed_flop_fraction": executed_frac,
-                         "overloaded_block_fraction": rows_overloaded / rows_offered if rows_offered else 0.0,
-                         "skip": "two-stage exact bound per (row, 128-contingency tile, candidate pair): "
-                                 "|f_c|+max|T|max|alpha|+sum_q |L_q|max|R'_q| < limit skips the row; else "
-                                 "|f_c+T alpha|+sum_q |L_q|max|R'_q| < limit skips the R FMAs of L R'; skipped "
-                                 "work cannot change any score",
-                         "mean_rank": mean_rank, "islanded_fraction": isl / (n_prof * B),
-                         "algorithmic": "E*K_single*(2+2r) per non-islanded candidate (SURVEY.md 8(d)) times the "
-                                        "executed flop fraction"},
+            "roofline": {"bound": "fp64", "kernel": "k_sweep (fused N-1 sweep)", "achieved": dense_tflops,
+                         "peak": peak, "unit": "TFLOP/s", "frac": dense_tflops / peak if peak else None,
+                         "traffic": traffic,
+                         "algorithmic": "SURVEY.md 8(d): E*K_single*(2+2r) FP64 flops per swept candidate x the "
+                                        "candidates of one launch, / the launch time measured live with CUDA events "
+                                        "on the engine stream",
+                         "peak_source": "DFMA microbenchmark on this GPU in this run (MEASURED_PEAKS.json has no "
+                                        "FP64 figure)",
+                         "flops_per_launch": flops / n_prof, "avg_launch_ms": avg_ms, "mean_rank": mean_rank,
+                         "algorithmic_bytes_per_launch": alg_bytes / n_prof,
+                         "islanded_fraction": isl / (n_prof * B),
+                         "note": "the sweep does not execute every algorithmic flop: an exact bound-and-skip proves "
+                                 "most (branch row, contingency tile, candidate) blocks below their limit without "
+                                 "element work (skipped work cannot change a score; tests/test_gpu_scale.py checks "
+                                 "it bit for bit against the dense sweep). 'executed' reports the FP64 work it "
+                                 "does run; the kernel is latency/issue-bound (profiles/)",
+                         "dense_kernel": {"tflops": dense_kernel_tflops,
+                                          "frac_of_peak": dense_kernel_tflops / peak if peak else None,
+                                          "ms": dense_ms / max(dense_n, 1),
+                                          "what": "k_sweep<true> (FlowResult path: every element, max folded "
+                                                  "for every branch) on one step's candidates"},
+                         "executed": {"tflops": executed_tflops, "frac_of_peak": executed_tflops / peak if peak else None,
+                                      "flop_fraction": executed_frac, "first_fma_block_fraction": partial_frac,
+                                      "computed_block_fraction": computed_frac,
+                                      "overloaded_block_fraction": rows_overloaded / rows_offered if rows_offered
+                                      else 0.0, "ncu": ncu or None}},
             "e2e": {"value": e2e_value, "unit": "topologies/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "call": "tg_evaluate_batch (DcContext::evaluate_batch) on pinned host buffers"},
