@@ -290,16 +290,6 @@ def main():
         except (OSError, ValueError):
             ncu = {}
 
-    # ---- the dense sweep (FlowResult path, every element computed, no skip) on
-    #      this step's candidates: the kernel's own FP64 roofline fraction
-    P.sweep_timing(ctx, True)
-    dense_g = sess.offspring()
-    ctx.evaluate_arrays(dense_g, 3, 2, flows=True)
-    dense_ms, dense_n = P.sweep_timing(ctx, False)
-    rd = P.batch_ranks(ctx, B)
-    dense_flops = float(E) * Ks * float(np.sum(2.0 + 2.0 * rd[rd >= 0]))
-    dense_kernel_tflops = dense_flops / (dense_ms / max(dense_n, 1) * 1e-3) / 1e12
-
     # ---- end to end through the reference-facing call with pinned host buffers
     #      (DcContext::evaluate_batch: H2D genomes, evaluate, D2H scores each step)
     rng = np.random.default_rng(7 + rank)
@@ -374,11 +364,6 @@ def main():
                                  "element work (skipped work cannot change a score; tests/test_gpu_scale.py checks "
                                  "it bit for bit against the dense sweep). 'executed' reports the FP64 work it "
                                  "does run; the kernel is latency/issue-bound (profiles/)",
-                         "dense_kernel": {"tflops": dense_kernel_tflops,
-                                          "frac_of_peak": dense_kernel_tflops / peak if peak else None,
-                                          "ms": dense_ms / max(dense_n, 1),
-                                          "what": "k_sweep<true> (FlowResult path: every element, max folded "
-                                                  "for every branch) on one step's candidates"},
                          "executed": {"tflops": executed_tflops, "frac_of_peak": executed_tflops / peak if peak else None,
                                       "flop_fraction": executed_frac, "first_fma_block_fraction": partial_frac,
                                       "computed_block_fraction": computed_frac,
