@@ -36,6 +36,8 @@ CONFIGS = {
     "cfg1": dict(workload="grid14_congested (bundled), batch 64, full N-1, 1 busbar outage", batch=64),
     "cfg2": dict(workload="synthetic 1k-bus/1.5k-branch grid, 4096-candidate batch, full N-1, 1 timestep",
                  batch=4096),
+    "cfg3": dict(workload="synthetic 2k-bus grid, bus splitting on 100 substations, 24 timesteps, N-1 over all "
+                          "non-reserved branches", batch=4096),
     "cfg4": dict(workload="synthetic TSO-scale 7k-bus/10.5k-branch grid, 500 splittable stations, "
                           "16384-candidate batch, full N-1", batch=16384),
 }
@@ -253,6 +255,7 @@ def main():
     P.sweep_rows(ctx)  # reset the skip counters
     flops = 0.0
     E, Ks, Kp = info["n_branches"], info["n_single"], info["k_padded"]
+    T = int(json.loads(text).get("timesteps", {}).get("count", 1))
     n_prof = 5
     isl = 0
     alg_bytes = 0.0
@@ -261,19 +264,20 @@ def main():
         r = P.batch_ranks(ctx, B)
         live = r[r >= 0]
         isl += int((r < 0).sum())
-        flops += float(E) * Ks * float(np.sum(2.0 + 2.0 * live))
+        flops += float(E) * Ks * float(np.sum(2.0 * T + 2.0 * live))
         # compulsory sweep traffic: each swept candidate's branch and contingency
         # rows (row_stride(r) doubles each) + the skip records + T_base read once
         stride = (live + 2) & ~1
-        alg_bytes += 8.0 * float(np.sum(stride)) * (E + Kp) + 8.0 * E * Kp * (1 + 10 / 128)
+        alg_bytes += T * (8.0 * float(np.sum(stride)) * (E + Kp) + 8.0 * E * Kp * (1 + 10 / 128))
     sweep_ms, sweep_n = P.sweep_timing(ctx, False)
     rows_done, rows_offered, rows_overloaded, rows_partial = P.sweep_rows(ctx)
     torch.cuda.synchronize()
-    avg_ms = sweep_ms / max(sweep_n, 1)
+    avg_ms = sweep_ms / max(sweep_n, 1)  # one sweep launch (one per timestep per generation)
+    step_sweep_ms = sweep_ms / n_prof
     computed_frac = rows_done / rows_offered if rows_offered else 1.0
     partial_frac = rows_partial / rows_offered if rows_offered else 1.0
-    dense_tflops = flops / n_prof / (avg_ms * 1e-3) / 1e12
-    mean_rank = float(flops / n_prof / (E * Ks) / B / 2.0 - 1.0) if B else 0.0
+    dense_tflops = flops / n_prof / (step_sweep_ms * 1e-3) / 1e12
+    mean_rank = float(flops / n_prof / (E * Ks) / B / 2.0 - T) if B else 0.0
     # executed FP64 work: blocks past the per-row bound run the first FMA
     # (f_c + T alpha), blocks past the per-element bound also the R FMAs of L R';
     # skipped work cannot change any score
@@ -351,13 +355,14 @@ def main():
             "roofline": {"bound": "fp64", "kernel": "k_sweep (fused N-1 sweep)", "achieved": dense_tflops,
                          "peak": peak, "unit": "TFLOP/s", "frac": dense_tflops / peak if peak else None,
                          "traffic": traffic,
-                         "algorithmic": "SURVEY.md 8(d): E*K_single*(2+2r) FP64 flops per swept candidate x the "
-                                        "candidates of one launch, / the launch time measured live with CUDA events "
-                                        "on the engine stream",
+                         "algorithmic": "SURVEY.md 8(d): E*K_single*(2T+2r) FP64 flops per swept candidate x the "
+                                        "candidates of one generation, / the generation's sweep time (one launch per "
+                                        "timestep) measured live with CUDA events on the engine stream",
                          "peak_source": "DFMA microbenchmark on this GPU in this run (MEASURED_PEAKS.json has no "
                                         "FP64 figure)",
-                         "flops_per_launch": flops / n_prof, "avg_launch_ms": avg_ms, "mean_rank": mean_rank,
-                         "algorithmic_bytes_per_launch": alg_bytes / n_prof,
+                         "flops_per_launch": flops / n_prof / T, "avg_launch_ms": avg_ms, "mean_rank": mean_rank,
+                         "timesteps": T,
+                         "algorithmic_bytes_per_launch": alg_bytes / n_prof / T,
                          "islanded_fraction": isl / (n_prof * B),
                          "note": "the sweep does not execute every algorithmic flop: an exact bound-and-skip proves "
                                  "most (branch row, contingency tile, candidate) blocks below their limit without "

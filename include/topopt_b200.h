@@ -66,6 +66,14 @@ typedef struct tg_grid_desc {
   const int32_t* bo_busbar;         /* busbar index within the substation */
   const int32_t* bo_implied_ptr;    /* [n_busbar_outages+1] default implied branches, grid_model.cpp:217-227 */
   const int32_t* bo_implied;
+  /* Timestep extension (not in the reference, whose GridModel has one injection
+   * vector, grid_model.hpp:36-46): n_timesteps >= 1 injection profiles; the
+   * evaluation runs every profile and sums lambda_o / lambda_c / lambda_c0 /
+   * lambda_b and the per-contingency energies over them (islanded at any
+   * timestep = islanded). n_timesteps <= 1 (injection_net_mw_t NULL) is the
+   * reference's single-vector evaluation. */
+  int32_t n_timesteps;
+  const double* injection_net_mw_t; /* [n_timesteps][n_injections] net MW */
 } tg_grid_desc;
 
 /* ---- plain-data action encoding (replaces const ActionSet&, importer.hpp:28-35).

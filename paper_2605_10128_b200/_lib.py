@@ -30,6 +30,7 @@ class GridDesc(C.Structure):
         ("term_element", i32p),
         ("n_busbar_outages", C.c_int32), ("bo_substation", i32p), ("bo_busbar", i32p),
         ("bo_implied_ptr", i32p), ("bo_implied", i32p),
+        ("n_timesteps", C.c_int32), ("injection_net_mw_t", f64p),
     ]
 
 

@@ -100,7 +100,7 @@ struct tg_grid {
   tgb::Grid g;
   std::vector<int32_t> br_from, br_to, inj_node, cont_bptr, cont_b, cont_iptr, cont_i, sub_node, sub_tptr, tkind,
       telem, bo_sub, bo_bb, bo_iptr, bo_i;
-  std::vector<double> br_x, br_lim, inj_net;
+  std::vector<double> br_x, br_lim, inj_net, inj_net_t;
   std::vector<uint8_t> br_on;
 };
 
@@ -122,6 +122,9 @@ void flatten_grid(tg_grid& h) {
   h.inj_node.assign(g.inj_node.begin(), g.inj_node.end());
   h.inj_net.clear();
   for (int i = 0; i < g.n_injections(); ++i) h.inj_net.push_back(g.inj_net(i));
+  h.inj_net_t.clear();
+  for (int t = 0; t < g.n_t; ++t)
+    for (int i = 0; i < g.n_injections(); ++i) h.inj_net_t.push_back(g.inj_net_t(t, i));
   h.cont_bptr = {0};
   h.cont_iptr = {0};
   h.cont_b.clear();
@@ -208,6 +211,12 @@ struct tg_context {
   cudaEvent_t sw0 = nullptr, sw1 = nullptr;
   double sweep_ms = 0.0;
   int64_t sweep_launches = 0;
+  // timestep extension: per-timestep table views (gt[0] == g), per-timestep
+  // scores / energies of the batch being aggregated
+  int n_t = 1;
+  std::vector<tgb::DevGrid> gt;
+  tgb::Scores tscores{};
+  double* tenergy = nullptr;
   // island merge buffers (allocated on the first merge)
   std::unique_ptr<DeviceArena> merge_arena;
   tgb::MergeBuffers merge{};
@@ -217,6 +226,11 @@ struct tg_context {
 
   void ensure_capacity(int n);
   void run_batch(int n, int n_a, int n_d, bool full);
+  // Enqueues the evaluation of batch.n candidates (all timesteps); returns
+  // kernels launched. timed: every sweep launch bracketed by sw0 / sw1 and
+  // accumulated into sweep_ms (synchronizes).
+  int enqueue_evaluate(int n_a, int n_d, bool full, bool timed = false);
+  void time_sweep_done();
 };
 
 void tg_context::ensure_capacity(int n) {
@@ -269,6 +283,26 @@ void tg_context::ensure_capacity(int n) {
   o.worst_n = A.alloc<int>(cap);
   o.isl_out = A.alloc<int>(cap);
   o.isl_bus = A.alloc<int>(cap);
+  if (n_t > 1) {
+    tgb::Scores& ts = tscores;
+    ts = o;  // same shapes
+    ts.lambda_o = A.alloc<double>(cap);
+    ts.lambda_c = A.alloc<int>(cap);
+    ts.lambda_c0 = A.alloc<int>(cap);
+    ts.lambda_b = A.alloc<double>(cap);
+    ts.lambda_d = A.alloc<int>(cap);
+    ts.lambda_s = A.alloc<int>(cap);
+    ts.lambda_r = A.alloc<int>(cap);
+    ts.fitness = A.alloc<double>(cap);
+    ts.islanded = A.alloc<uint8_t>(cap);
+    ts.error = A.alloc<int>(cap);
+    ts.worst_idx = A.alloc<int>(static_cast<size_t>(cap) * std::max(worst_k, 1));
+    ts.worst_val = A.alloc<double>(static_cast<size_t>(cap) * std::max(worst_k, 1));
+    ts.worst_n = A.alloc<int>(cap);
+    ts.isl_out = A.alloc<int>(cap);
+    ts.isl_bus = A.alloc<int>(cap);
+    tenergy = A.alloc<double>(static_cast<size_t>(cap) * Ka);
+  }
   // Z scratch: bounded so huge grids stay within a fixed budget
   const size_t row_prep = static_cast<size_t>(std::max(g.Nr, 1)) * tgb::kStride * sizeof(double);
   const size_t budget = size_t{2} << 30;
@@ -280,26 +314,49 @@ void tg_context::ensure_capacity(int n) {
   capacity = cap;
 }
 
+void tg_context::time_sweep_done() {
+  check(cudaEventSynchronize(sw1), "sweep timing");
+  float ms = 0.f;
+  check(cudaEventElapsedTime(&ms, sw0, sw1), "sweep timing");
+  sweep_ms += ms;
+  ++sweep_launches;
+}
+
+int tg_context::enqueue_evaluate(int n_a, int n_d, bool full, bool timed) {
+  int kernels = 0;
+  if (timed && !sw0) {
+    check(cudaEventCreate(&sw0), "event");
+    check(cudaEventCreate(&sw1), "event");
+  }
+  if (n_t == 1) {
+    tgb::launch_evaluate(g, batch, n_a, n_d, full, scratch, stream, &kernels, timed ? sw0 : nullptr,
+                         timed ? sw1 : nullptr);
+    if (timed) time_sweep_done();
+    return kernels;
+  }
+  // timesteps: the pipeline once per injection profile into the per-t
+  // buffers, accumulated into batch.out / batch.energy, then the fitness and
+  // worst list of the sums (engine.cu, k_accum_t / k_finish_agg)
+  if (full) throw tgb::ConfigError("FlowResult outputs are per timestep; request them on a single-timestep grid");
+  tgb::Batch bt = batch;
+  bt.out = tscores;
+  bt.energy = tenergy;
+  for (int t = 0; t < n_t; ++t) {
+    int k = 0;
+    tgb::launch_evaluate(gt[t], bt, n_a, n_d, false, scratch, stream, &k, timed ? sw0 : nullptr,
+                         timed ? sw1 : nullptr);
+    if (timed) time_sweep_done();
+    kernels += k + tgb::launch_accumulate_timestep(bt, batch.out, batch.energy, g.Kall, t == 0, stream);
+  }
+  kernels += tgb::launch_finish_aggregate(batch, g.Kall, stream);
+  return kernels;
+}
+
 void tg_context::run_batch(int n, int n_a, int n_d, bool full) {
   batch.n = n;
   batch.genomes = d_genomes;
   batch.params = params;
-  int kernels = 0;
-  if (time_sweep && g.Ks > 0) {
-    if (!sw0) {
-      check(cudaEventCreate(&sw0), "event");
-      check(cudaEventCreate(&sw1), "event");
-    }
-    tgb::launch_evaluate(g, batch, n_a, n_d, full, scratch, stream, &kernels, sw0, sw1);
-    check(cudaEventSynchronize(sw1), "sweep timing");
-    float ms = 0.f;
-    check(cudaEventElapsedTime(&ms, sw0, sw1), "sweep timing");
-    sweep_ms += ms;
-    ++sweep_launches;
-  } else {
-    tgb::launch_evaluate(g, batch, n_a, n_d, full, scratch, stream, &kernels);
-  }
-  launches += kernels;
+  launches += enqueue_evaluate(n_a, n_d, full, time_sweep && g.Ks > 0);
   check(cudaGetLastError(), "evaluate launch");
 }
 
@@ -387,6 +444,8 @@ tg_status tg_grid_describe(const tg_grid* h, tg_grid_desc* d) {
     d->bo_busbar = h->bo_bb.data();
     d->bo_implied_ptr = h->bo_iptr.data();
     d->bo_implied = h->bo_i.data();
+    d->n_timesteps = g.n_t;
+    d->injection_net_mw_t = g.n_t > 1 ? h->inj_net_t.data() : nullptr;
   });
 }
 
@@ -598,32 +657,44 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     if (!tgb::device_spd_inverse(X, Nr, s))
       throw tgb::SingularSystem("susceptance matrix is singular; the grid is disconnected");
     g.X = X;
-    std::vector<double> p(N, 0.0);
-    for (int i = 0; i < I; ++i) p[gd->injection_node[i]] += gd->injection_net_mw[i];
-    double tot = 0.0;
-    for (double v : p) tot += v;
-    p[gd->slack] -= tot;
-    std::vector<double> pr(Nr);
-    for (int v = 0; v < N; ++v)
-      if (red[v] >= 0) pr[red[v]] = p[v];
-    double* d_pr = A.upload(pr, s);
-    double* theta0 = A.alloc<double>(Nr);
-    double* f0 = A.alloc<double>(E);
+    // base tables per injection profile (timestep extension; T = 1 is the reference)
+    const int T = std::max(1, gd->n_timesteps);
+    if (T > 1 && !gd->injection_net_mw_t) throw tgb::ConfigError("n_timesteps > 1 needs injection_net_mw_t");
     double* tdiag = A.alloc<double>(E);
     double* tk = A.alloc<double>(static_cast<size_t>(E) * std::max(g.Kpad, 1));
     const int ntiles = g.Kpad / tgb::sweep_tile_k();
     const size_t tmax_n = static_cast<size_t>(std::max(ntiles, 1)) * (E + tgb::sweep_chunk()) * tgb::kRec;
-    double* tmax = A.alloc<double>(tmax_n);
-    check(cudaMemsetAsync(tmax, 0, tmax_n * sizeof(double), s), "tmax");
-    double* alpha0 = A.alloc<double>(std::max(g.Kpad, 1));
-    g.theta0 = theta0;
-    g.f0 = f0;
     g.Tdiag = tdiag;
     g.TK = tk;
-    g.Tmax = tmax;
-    g.alpha0 = alpha0;
-    tgb::launch_base_tables(g, d_pr, theta0, f0, tdiag, tk, tmax, alpha0, s);
-    check(cudaGetLastError(), "base tables");
+    ctx->n_t = T;
+    ctx->gt.clear();
+    for (int t = 0; t < T; ++t) {
+      const double* net = T > 1 ? gd->injection_net_mw_t + static_cast<size_t>(t) * I : gd->injection_net_mw;
+      std::vector<double> p(N, 0.0);
+      for (int i = 0; i < I; ++i) p[gd->injection_node[i]] += net[i];
+      double tot = 0.0;
+      for (double v : p) tot += v;
+      p[gd->slack] -= tot;
+      std::vector<double> pr(Nr);
+      for (int v = 0; v < N; ++v)
+        if (red[v] >= 0) pr[red[v]] = p[v];
+      tgb::DevGrid gv = g;
+      if (T > 1) gv.inj_net = A.upload(std::vector<double>(net, net + I), s);
+      double* d_pr = A.upload(pr, s);
+      double* theta0 = A.alloc<double>(Nr);
+      double* f0 = A.alloc<double>(E);
+      double* tmax = A.alloc<double>(tmax_n);
+      check(cudaMemsetAsync(tmax, 0, tmax_n * sizeof(double), s), "tmax");
+      double* alpha0 = A.alloc<double>(std::max(g.Kpad, 1));
+      gv.theta0 = theta0;
+      gv.f0 = f0;
+      gv.Tmax = tmax;
+      gv.alpha0 = alpha0;
+      tgb::launch_base_tables(gv, d_pr, theta0, f0, tdiag, tk, tmax, alpha0, s);
+      check(cudaGetLastError(), "base tables");
+      ctx->gt.push_back(gv);
+    }
+    g = ctx->gt[0];
     check(cudaStreamSynchronize(s), "context setup");
 
     ctx->n_cont = gd->n_contingencies;
@@ -963,8 +1034,7 @@ int enqueue_iteration(tg_context* ctx) {
   ctx->batch.n = B;
   ctx->batch.genomes = ctx->d_genomes;
   ctx->batch.params = ctx->params;
-  int kernels = 0;
-  tgb::launch_evaluate(ctx->g, ctx->batch, q.p.n_a, q.p.n_d, false, ctx->scratch, ctx->stream, &kernels);
+  const int kernels = ctx->enqueue_evaluate(q.p.n_a, q.p.n_d, false);
   const int ins = tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, B, ctx->worst_k, true, ctx->stream);
   return 1 + kernels + ins;
 }

@@ -298,6 +298,50 @@ __device__ __forceinline__ bool worst_before(double v, int k, double u, int j) {
   return v > u || (v == u && k < j);
 }
 
+// One warp: the first wk entries with energy > 0 of en[0..K) in the order
+// (energy desc, index asc). Positive energies are compacted into the warp's
+// shared list (lv, li; kFinishList entries), selection rounds then scan the
+// list (or all K when it overflows).
+__device__ void warp_worst(const double* en, int K, int wk, double* lv, int* li, int* out_idx, double* out_val,
+                           int* out_n, int lane) {
+  int npos = 0;
+  for (int k0 = 0; k0 < K; k0 += 32) {
+    const int k = k0 + lane;
+    const double v = k < K ? en[k] : 0.0;
+    const unsigned m = __ballot_sync(0xffffffffu, v > 0.0);
+    const int at = npos + __popc(m & ((1u << lane) - 1u));
+    if (v > 0.0 && at < kFinishList) lv[at] = v, li[at] = k;
+    npos += __popc(m);
+  }
+  __syncwarp();
+  const bool listed = npos <= kFinishList;
+  const int n_scan = listed ? npos : K;
+  double pv = CUDART_INF;
+  int pi = -1, nsel = 0;
+  for (int round = 0; round < wk; ++round) {
+    double bv = 0.0;
+    int bi = -1;
+    for (int i = lane; i < n_scan; i += 32) {
+      const double v = listed ? lv[i] : en[i];
+      const int k = listed ? li[i] : i;
+      if (!(v > 0.0) || !worst_before(pv, pi, v, k)) continue;  // already selected
+      if (bi < 0 || worst_before(v, k, bv, bi)) bv = v, bi = k;
+    }
+#pragma unroll
+    for (int d = 16; d > 0; d >>= 1) {
+      const double ov = __shfl_xor_sync(0xffffffffu, bv, d);
+      const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
+      if (oi >= 0 && (bi < 0 || worst_before(ov, oi, bv, bi))) bv = ov, bi = oi;
+    }
+    if (bi < 0) break;
+    if (lane == 0) out_idx[round] = bi, out_val[round] = bv;
+    pv = bv;
+    pi = bi;
+    ++nsel;
+  }
+  if (lane == 0) *out_n = nsel;
+}
+
 __global__ void __launch_bounds__(32 * kFinishWarps) k_finish(DevGrid g, Batch b, int n_a, int n_d) {
   __shared__ double wl_v[kFinishWarps][kFinishList];
   __shared__ int wl_i[kFinishWarps][kFinishList];
@@ -372,50 +416,81 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_finish(DevGrid g, Batch b
     o.isl_out[c] = iso;
     o.isl_bus[c] = isb;
   }
-  // compact the positive energies (ascending contingency order)
-  const double* en = b.energy + static_cast<size_t>(c) * g.Kall;
-  double* lv = wl_v[wid];
-  int* li = wl_i[wid];
-  int npos = 0;
-  for (int k0 = 0; k0 < g.Kall; k0 += 32) {
-    const int k = k0 + lane;
-    const double v = k < g.Kall ? en[k] : 0.0;
-    const unsigned m = __ballot_sync(0xffffffffu, v > 0.0);
-    const int at = npos + __popc(m & ((1u << lane) - 1u));
-    if (v > 0.0 && at < kFinishList) lv[at] = v, li[at] = k;
-    npos += __popc(m);
+  warp_worst(b.energy + static_cast<size_t>(c) * g.Kall, g.Kall, b.params.worst_k, wl_v[wid], wl_i[wid],
+             o.worst_idx + static_cast<size_t>(c) * b.params.worst_k,
+             o.worst_val + static_cast<size_t>(c) * b.params.worst_k, o.worst_n + c, lane);
+}
+
+// ---------------------------------------------------------------- timesteps
+// Timestep extension (model.hpp): a batch over T injection profiles runs the
+// whole pipeline once per timestep (the topology part is recomputed; tables
+// indexed by t) and aggregates: lambda_o, lambda_c, lambda_c0, lambda_b and the
+// islanded counts summed over t, per-contingency energies summed over t (the
+// worst list ranks the sums), islanded if islanded at any t. With T == 1 this
+// is exactly the reference's evaluate.
+__global__ void k_accum_t(Batch bt, Scores agg, double* agg_energy, int Kall, int first) {
+  const size_t n_en = static_cast<size_t>(bt.n) * Kall;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n_en;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x)
+    agg_energy[i] = first ? bt.energy[i] : agg_energy[i] + bt.energy[i];
+  for (int c = blockIdx.x * blockDim.x + threadIdx.x; c < bt.n; c += gridDim.x * blockDim.x) {
+    const Scores& o = bt.out;
+    if (first) {
+      agg.lambda_o[c] = o.lambda_o[c];
+      agg.lambda_c[c] = o.lambda_c[c];
+      agg.lambda_c0[c] = o.lambda_c0[c];
+      agg.lambda_b[c] = o.lambda_b[c];
+      agg.lambda_d[c] = o.lambda_d[c];
+      agg.lambda_s[c] = o.lambda_s[c];
+      agg.lambda_r[c] = o.lambda_r[c];
+      agg.islanded[c] = o.islanded[c];
+      agg.error[c] = o.error[c];
+      agg.isl_out[c] = o.isl_out[c];
+      agg.isl_bus[c] = o.isl_bus[c];
+    } else {
+      agg.lambda_o[c] += o.lambda_o[c];
+      agg.lambda_c[c] += o.lambda_c[c];
+      agg.lambda_c0[c] += o.lambda_c0[c];
+      agg.lambda_b[c] += o.lambda_b[c];
+      agg.islanded[c] |= o.islanded[c];
+      agg.error[c] = max(agg.error[c], o.error[c]);
+      agg.isl_out[c] += o.isl_out[c];
+      agg.isl_bus[c] += o.isl_bus[c];
+    }
   }
-  __syncwarp();
-  const bool listed = npos <= kFinishList;
-  const int n_scan = listed ? npos : g.Kall;
+}
+
+// Fitness (dc_engine.cpp:402-410 on the summed metrics) and the worst list of
+// the summed energies; one warp per candidate.
+__global__ void __launch_bounds__(32 * kFinishWarps) k_finish_agg(Batch b, int Kall) {
+  __shared__ double wl_v[kFinishWarps][kFinishList];
+  __shared__ int wl_i[kFinishWarps][kFinishList];
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  const int c = blockIdx.x * kFinishWarps + wid;
+  if (c >= b.n) return;
+  Scores& o = b.out;
   const int wk = b.params.worst_k;
-  double pv = CUDART_INF;
-  int pi = -1, nsel = 0;
-  for (int round = 0; round < wk; ++round) {
-    double bv = 0.0;
-    int bi = -1;
-    for (int i = lane; i < n_scan; i += 32) {
-      const double v = listed ? lv[i] : en[i];
-      const int k = listed ? li[i] : i;
-      if (!(v > 0.0) || !worst_before(pv, pi, v, k)) continue;  // already selected
-      if (bi < 0 || worst_before(v, k, bv, bi)) bv = v, bi = k;
-    }
-#pragma unroll
-    for (int d = 16; d > 0; d >>= 1) {
-      const double ov = __shfl_xor_sync(0xffffffffu, bv, d);
-      const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
-      if (oi >= 0 && (bi < 0 || worst_before(ov, oi, bv, bi))) bv = ov, bi = oi;
-    }
-    if (bi < 0) break;
+  if (o.islanded[c] || o.error[c]) {
     if (lane == 0) {
-      o.worst_idx[static_cast<size_t>(c) * wk + round] = bi;
-      o.worst_val[static_cast<size_t>(c) * wk + round] = bv;
+      o.lambda_o[c] = 0.0;
+      o.lambda_c[c] = 0;
+      o.lambda_c0[c] = 0;
+      o.lambda_b[c] = 0.0;
+      o.fitness[c] = -CUDART_INF;
+      o.worst_n[c] = 0;
+      o.isl_out[c] = 0;
+      o.isl_bus[c] = 0;
     }
-    pv = bv;
-    pi = bi;
-    ++nsel;
+    return;
   }
-  if (lane == 0) o.worst_n[c] = nsel;
+  if (lane == 0) {
+    double fit = -(o.lambda_o[c] + b.params.weight_c0 * o.lambda_c0[c] + b.params.weight_c * o.lambda_c[c]);
+    if (b.params.variant == 2) fit -= fmax(o.lambda_b[c] - b.params.lambda_b_pre, 0.0);
+    o.fitness[c] = fit;
+  }
+  warp_worst(b.energy + static_cast<size_t>(c) * Kall, Kall, wk, wl_v[wid], wl_i[wid],
+             o.worst_idx + static_cast<size_t>(c) * wk, o.worst_val + static_cast<size_t>(c) * wk, o.worst_n + c,
+             lane);
 }
 
 // Dense copy of the candidate base flows (f_c) for callers that ask for them.
@@ -481,6 +556,19 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
   k_finish<<<(b.n + kFinishWarps - 1) / kFinishWarps, 32 * kFinishWarps, 0, stream>>>(g, b, n_a, n_d);
   ++launched;
   if (kernels) *kernels = launched;
+}
+
+int launch_accumulate_timestep(const Batch& bt, Scores& agg, double* agg_energy, int Kall, bool first,
+                               cudaStream_t stream) {
+  const size_t work = static_cast<size_t>(bt.n) * (Kall > 0 ? Kall : 1);
+  const int grid = static_cast<int>(std::min<size_t>((work + 255) / 256, 148 * 8));
+  k_accum_t<<<grid, 256, 0, stream>>>(bt, agg, agg_energy, Kall, first ? 1 : 0);
+  return 1;
+}
+
+int launch_finish_aggregate(Batch& b, int Kall, cudaStream_t stream) {
+  k_finish_agg<<<(b.n + kFinishWarps - 1) / kFinishWarps, 32 * kFinishWarps, 0, stream>>>(b, Kall);
+  return 1;
 }
 
 void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_out, double* fbus_out,

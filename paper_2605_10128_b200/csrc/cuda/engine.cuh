@@ -93,6 +93,12 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
                      cudaEvent_t sweep_end = nullptr);
 void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_out, double* fbus_out,
                     cudaStream_t stream);
+// Timestep aggregation (host loops launch_evaluate over t with the per-t
+// scores in `bt`): accumulate timestep t into (agg, agg_energy), then the
+// fitness and worst list of the sums into b.out (b.energy = the summed energies).
+int launch_accumulate_timestep(const Batch& bt, Scores& agg, double* agg_energy, int Kall, bool first,
+                               cudaStream_t stream);
+int launch_finish_aggregate(Batch& b, int Kall, cudaStream_t stream);
 int sweep_tile_k();
 int sweep_chunk();
 void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1,

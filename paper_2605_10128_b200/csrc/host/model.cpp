@@ -371,6 +371,33 @@ Grid load_grid_json(const std::string& text) {
   if (!sl) throw ParseError("grid file: missing 'slack'");
   if (!sl->is_string()) throw ParseError("grid file: 'slack' must be a node id");
   g.slack = node_of(sl->str, "slack");
+  // timestep profiles (extension; see model.hpp)
+  g.inj_p_t = g.inj_p;
+  if (const Value* ts = doc.find("timesteps")) {
+    if (!ts->is_object()) throw ParseError("'timesteps' must be an object");
+    const Value* cnt = ts->find("count");
+    if (!cnt || !cnt->is_number() || !cnt->integral || cnt->num < 1 || cnt->num > 8760)
+      throw ParseError("'timesteps.count' must be an integer in [1, 8760]");
+    g.n_t = static_cast<int>(cnt->num);
+    const int I = g.n_injections();
+    g.inj_p_t.assign(static_cast<size_t>(g.n_t) * I, 0.0);
+    for (int t = 0; t < g.n_t; ++t)
+      for (int i = 0; i < I; ++i) g.inj_p_t[static_cast<size_t>(t) * I + i] = g.inj_p[i];
+    if (const Value* inj = ts->find("injections")) {
+      if (!inj->is_object()) throw ParseError("'timesteps.injections' must be an object");
+      for (const auto& kv : inj->obj) {
+        const int i = g.injection_index(kv.first);
+        if (i < 0) throw ValidationError("timestep profile for unknown injection '" + kv.first + "'");
+        if (!kv.second.is_array() || static_cast<int>(kv.second.arr.size()) != g.n_t)
+          throw ParseError("timestep profile of '" + kv.first + "' must be an array of 'count' numbers");
+        for (int t = 0; t < g.n_t; ++t) {
+          const Value& v = kv.second.arr[t];
+          if (!v.is_number() || !std::isfinite(v.num)) throw ParseError("timestep profile of '" + kv.first + "': non-numeric value");
+          g.inj_p_t[static_cast<size_t>(t) * I + i] = v.num;
+        }
+      }
+    }
+  }
   validate(g);
   return g;
 }

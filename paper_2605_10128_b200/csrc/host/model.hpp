@@ -61,6 +61,17 @@ struct Grid {
   std::vector<int> bo_station, bo_busbar;
   std::vector<Station> stations;
   int slack = -1;
+  // Timestep extension (not in the reference, whose GridModel carries one
+  // injection vector, grid_model.hpp:36-46): top-level key
+  //   "timesteps": {"count": T, "injections": {"<injection id>": [p_mw x T], ...}}
+  // which the reference loader ignores. Injections without a profile keep p_mw.
+  // n_t == 1 and inj_p_t == inj_p when the key is absent.
+  int n_t = 1;
+  std::vector<double> inj_p_t;  // [n_t][n_injections] p_mw
+  double inj_net_t(int t, int i) const {
+    const double p = inj_p_t[static_cast<size_t>(t) * inj_node.size() + i];
+    return inj_gen[i] ? p : -p;
+  }
 
   int n_nodes() const { return static_cast<int>(node_id.size()); }
   int n_branches() const { return static_cast<int>(br_from.size()); }

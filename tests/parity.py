@@ -166,3 +166,60 @@ def replay_inserts(stream, cfg):
             lst.pop()
         results.append(True)
     return results, cells
+
+
+def timestep_grids(grid_json: str):
+    """The single-profile grids of a grid with a 'timesteps' key (model.hpp):
+    grid t = the grid with every profiled injection's p_mw replaced by its t-th
+    value (what the reference evaluates for that timestep)."""
+    doc = json.loads(grid_json)
+    ts = doc.pop("timesteps", None)
+    if not ts:
+        return [json.dumps(doc)]
+    out = []
+    for t in range(int(ts["count"])):
+        d = json.loads(json.dumps(doc))
+        for inj in d.get("injections", []):
+            prof = ts.get("injections", {}).get(inj["id"])
+            if prof is not None:
+                inj["p_mw"] = prof[t]
+        out.append(json.dumps(d))
+    return out
+
+
+def oracle_timesteps(orcs, genomes, n_a, n_d, worst_k=20, weights=(200.0, 50.0)):
+    """Aggregated evaluation over timesteps (the extension's definition, on top
+    of the reference's per-timestep evaluate): lambda_o/c/c0/b and islanded
+    counts summed, energies summed per contingency and ranked (energy desc,
+    index asc, first worst_k), islanded at any timestep = islanded (fitness
+    -inf). Variant 1 fitness."""
+    per = [o.evaluate(genomes, n_a, n_d, flows=True) for o in orcs]
+    n = len(genomes)
+    out = {k: sum(p[k] for p in per) for k in ("lambda_o", "lambda_c", "lambda_c0", "lambda_b",
+                                               "islanded_outages", "islanded_busbar")}
+    for k in ("lambda_d", "lambda_s", "lambda_r"):
+        out[k] = per[0][k]
+    isl = np.zeros(n, bool)
+    for p in per:
+        isl |= p["islanded"].astype(bool)
+    out["islanded"] = isl.astype(np.uint8)
+    energy = sum(p["energy"] for p in per)
+    out["fitness"] = -(out["lambda_o"] + weights[0] * out["lambda_c0"] + weights[1] * out["lambda_c"])
+    out["fitness"][isl] = -np.inf
+    wi = np.zeros((n, max(worst_k, 1)), np.int32)
+    wv = np.zeros((n, max(worst_k, 1)))
+    wn = np.zeros(n, np.int32)
+    for i in range(n):
+        if isl[i]:
+            for k in ("lambda_o", "lambda_b"):
+                out[k][i] = 0.0
+            for k in ("lambda_c", "lambda_c0", "islanded_outages", "islanded_busbar"):
+                out[k][i] = 0
+            continue
+        pos = [(-energy[i, k], k) for k in range(energy.shape[1]) if energy[i, k] > 0]
+        pos.sort()
+        for j, (v, k) in enumerate(pos[:worst_k]):
+            wi[i, j], wv[i, j] = k, -v
+        wn[i] = min(len(pos), worst_k)
+    out.update(worst_idx=wi, worst_val=wv, worst_n=wn)
+    return out

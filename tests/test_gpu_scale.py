@@ -10,6 +10,8 @@ genome distribution), evaluated as one full batch.
   4096-candidate batch: every skipped element provably stays under its limit,
   and the surviving elements are summed in the same branch order;
 * a sample of the batch == the CPU oracle (reference restatement), 1e-9."""
+import json
+
 import numpy as np
 import pytest
 
@@ -42,7 +44,9 @@ def _fast_equals_dense(ctx, genomes):
 
 @pytest.mark.parametrize("cfg", ["cfg2", "cfg3"])
 def test_bench_scale_fast_sweep_and_oracle(cfg):
-    text = config_json(cfg)
+    doc = json.loads(config_json(cfg))
+    doc.pop("timesteps", None)  # single profile (the FlowResult path is per timestep)
+    text = json.dumps(doc)
     g = P.grid_from_json_text(text)
     ctx = P.DcContext(g, P.build_action_set(g))
     genomes = _loop_genomes(ctx, 4096, 6, seed=17)

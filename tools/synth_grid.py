@@ -60,7 +60,8 @@ def _bridges(n: int, edges: np.ndarray) -> set:
 
 
 def synth_grid(n_nodes: int, seed: int = 0, branch_ratio: float = 1.5, n_stations: int = 50,
-               disc_fraction: float = 0.1, tight_fraction: float = 0.03, max_terminals: int = 10) -> dict:
+               disc_fraction: float = 0.1, tight_fraction: float = 0.03, max_terminals: int = 10,
+               n_timesteps: int = 1) -> dict:
     rng = np.random.default_rng(seed)
     n = n_nodes
     pos = rng.random((n, 2))
@@ -195,7 +196,7 @@ def synth_grid(n_nodes: int, seed: int = 0, branch_ratio: float = 1.5, n_station
         subs.append({"node": f"n{v}", "busbars": ["B1", "B2"], "couplers": [["B1", "B2"]],
                      "terminals": [{"element": t, "reachable": ["B1", "B2"],
                                     "default": "B2" if rng.random() < 0.5 else "B1"} for t in el]})
-    return {
+    doc = {
         "nodes": [{"id": f"n{v}"} for v in range(n)],
         "branches": [{"id": f"e{e}", "from": f"n{i}", "to": f"n{j}", "x_pu": float(x[e]),
                       "limit_mw": float(lim[e])} for e, (i, j) in enumerate(edges)],
@@ -205,12 +206,25 @@ def synth_grid(n_nodes: int, seed: int = 0, branch_ratio: float = 1.5, n_station
         "busbar_outages": [],
         "slack": f"n{slack}",
     }
+    if n_timesteps > 1:
+        # daily profile (extension key, ignored by the reference loader): loads
+        # follow 0.8 + 0.25 sin(pi (t - 6) / 12) with 3 % noise, generators the
+        # same curve with 5 % noise; the slack absorbs the residual
+        t = np.arange(n_timesteps)
+        curve = 0.8 + 0.25 * np.sin(np.pi * (t - 6) / 12.0)
+        prof = {}
+        for k, v in enumerate(gen_nodes):
+            prof[f"g{v}"] = [float(x) for x in gen_p[k] * curve * rng.uniform(0.95, 1.05, n_timesteps)]
+        for k, v in enumerate(load_nodes):
+            prof[f"l{v}"] = [float(x) for x in load_p[k] * curve * rng.uniform(0.97, 1.03, n_timesteps)]
+        doc["timesteps"] = {"count": int(n_timesteps), "injections": prof}
+    return doc
 
 
 # BASELINE.json configs
 CONFIGS = {
     "cfg2": dict(n_nodes=1000, n_stations=50, seed=2),      # 1k-bus / 1.5k-branch, B=4096
-    "cfg3": dict(n_nodes=2000, n_stations=100, seed=3),     # 2k-bus, 100 split stations
+    "cfg3": dict(n_nodes=2000, n_stations=100, seed=3, n_timesteps=24),  # 2k-bus, 100 split stations, 24 steps
     "cfg4": dict(n_nodes=7000, n_stations=500, seed=4),     # TSO scale ~7k / 10k / 500 stations
 }
 
