@@ -56,8 +56,22 @@ def dist_setup():
     local = int(os.environ.get("LOCAL_RANK", "0"))
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl")
+        # NCCL over NVLink/NVSwitch; TGB_DIST_BACKEND=gloo (host-staged exchange,
+        # ranks may share a GPU) is the single-GPU test harness of the N>1 path
+        dist.init_process_group(os.environ.get("TGB_DIST_BACKEND", "nccl"))
     return world, rank, local
+
+
+def max_over_ranks(x: float, world: int, dev: int) -> float:
+    """Max of a per-rank time over all ranks (device tensor for NCCL, host for gloo)."""
+    if world == 1:
+        return x
+    import torch
+    import torch.distributed as dist
+    on_dev = dist.get_backend() == "nccl"
+    t = torch.tensor([x], dtype=torch.float64, device=f"cuda:{dev}" if on_dev else "cpu")
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
 
 
 class ClockSampler:
@@ -188,7 +202,7 @@ def main():
     import torch
     import paper_2605_10128_b200 as P
 
-    dev = local
+    dev = local % max(1, torch.cuda.device_count())
     torch.cuda.set_device(dev)
     text = grid_text(args.config)
     B = CONFIGS[args.config]["batch"]
@@ -241,11 +255,7 @@ def main():
         barrier()
     ms = e0.elapsed_time(e1)
     launches = ctx.kernel_launches() - launches0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([ms], device=f"cuda:{dev}")
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        ms = float(t.item())
+    ms = max_over_ranks(ms, world, dev)
     total = B * args.steps * world
     value = total / (ms / 1000.0)
     snap = sess.fetch()
@@ -322,11 +332,7 @@ def main():
         P.evaluate_raw(ctx, g_pin.data_ptr(), B, 3, 2, sc)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
-    if world > 1:
-        import torch.distributed as dist
-        t = torch.tensor([e2e_s], device=f"cuda:{dev}", dtype=torch.float64)
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        e2e_s = float(t.item())
+    e2e_s = max_over_ranks(e2e_s, world, dev)
     e2e_value = B * e2e_steps * world / e2e_s
 
     base = None

@@ -138,6 +138,9 @@ class IslandExchange:
         self.session = session
         self.group = group
         self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        # NCCL gathers device buffers directly; any other backend (gloo: the
+        # single-GPU test harness of the N>1 path) is staged through host memory
+        self.device_collective = not dist.is_initialized() or dist.get_backend(group) == "nccl"
         self.nbytes = session.blob_bytes()
         dev = torch.device("cuda", torch.cuda.current_device())
         self.send = torch.empty(self.nbytes, dtype=torch.uint8, device=dev)
@@ -151,11 +154,17 @@ class IslandExchange:
 
         with torch.cuda.stream(self.stream):
             self.session.pack(self.send.data_ptr())
-            if self.world > 1:
+            if self.world == 1:
+                self.session.merge(self.send.data_ptr(), 1)
+            elif self.device_collective:
                 dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
                 self.session.merge(self.recv.data_ptr(), self.world)
             else:
-                self.session.merge(self.send.data_ptr(), 1)
+                host = self.send.cpu()
+                gathered = torch.empty(self.world * self.nbytes, dtype=torch.uint8)
+                dist.all_gather_into_tensor(gathered, host, group=self.group)
+                self.recv.copy_(gathered)
+                self.session.merge(self.recv.data_ptr(), self.world)
         self.exchanges += 1
 
 
