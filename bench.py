@@ -186,6 +186,8 @@ def main():
     ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--rng", default="replay", choices=["replay", "philox"],
+                    help="lane RNG: the reference's mt19937_64 stream (default) or counter-based Philox4x32-10")
     ap.add_argument("--merge-every", type=int, default=1,
                     help="island archive merge (NCCL allgather + device merge) every M generations when N>1; 0 = never")
     args = ap.parse_args()
@@ -210,7 +212,7 @@ def main():
     actions = P.build_action_set(grid)
     ctx = P.DcContext(grid, actions, P.DcConfig(), device=dev)
     info = ctx.info()
-    cfg = P.QdConfig(batch_size=B, iters_per_epoch=1 << 30, seed=1 + rank)  # one island per rank
+    cfg = P.QdConfig(batch_size=B, iters_per_epoch=1 << 30, seed=1 + rank, rng=args.rng)  # one island per rank
     sess = P.QdSession(ctx, cfg)
     stream = torch.cuda.ExternalStream(P.context_stream(ctx), device=dev)
 
@@ -356,6 +358,7 @@ def main():
                        "l2": f"per-step candidate working set {work_bytes / 2**20:.0f} MiB > 126 MiB L2 "
                              "(no flush needed)",
                        "step": "one MapElites generation: mutate/crossover + full N-1 evaluation + archive insert",
+                       "rng": args.rng,
                        "archive_entries": len(snap.entries), "best_fitness": snap.best_fitness},
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp64", "kernel": "k_sweep (fused N-1 sweep)", "achieved": dense_tflops,

@@ -131,6 +131,11 @@ typedef struct tg_qd_config {
   uint64_t seed;
   int64_t max_evaluations;
   double max_seconds;
+  /* Lane RNG (extension): 0 = replay of the reference's per-lane
+   * std::mt19937_64 + libstdc++ distributions (qd_optimizer.cpp:377-383; bit
+   * for bit), 1 = counter-based Philox4x32-10 keyed by the same lane seed
+   * (stateless draws, same distributions; not the reference's stream). */
+  int32_t rng;
 } tg_qd_config;
 
 /* One archive entry of a RepertoireSnapshot (qd_optimizer.hpp:83-95). */

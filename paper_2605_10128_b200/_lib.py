@@ -60,7 +60,7 @@ class QdConfigC(C.Structure):
                 ("iters_per_epoch", C.c_int32), ("cell_capacity", C.c_int32), ("mutation_mean", C.c_double),
                 ("p_action", C.c_double * 4), ("p_disc", C.c_double * 4), ("p_crossover_parent1", C.c_double),
                 ("d_max", C.c_int32), ("s_max", C.c_int32), ("r_max", C.c_int32), ("seed", C.c_uint64),
-                ("max_evaluations", C.c_int64), ("max_seconds", C.c_double)]
+                ("max_evaluations", C.c_int64), ("max_seconds", C.c_double), ("rng", C.c_int32)]
 
 
 class SnapshotView(C.Structure):

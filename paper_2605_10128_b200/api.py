@@ -417,6 +417,9 @@ class QdConfig:
     seed: int = 1
     max_evaluations: int = -1
     max_seconds: float = -1.0
+    # lane RNG: "replay" = the reference's per-lane std::mt19937_64 stream bit
+    # for bit; "philox" = counter-based Philox4x32-10 (extension, same distributions)
+    rng: str = "replay"
 
     def to_c(self) -> L.QdConfigC:
         c = L.QdConfigC()
@@ -428,6 +431,9 @@ class QdConfig:
         c.p_crossover_parent1 = self.p_crossover_parent1
         c.d_max, c.s_max, c.r_max = self.d_max, self.s_max, self.r_max
         c.seed, c.max_evaluations, c.max_seconds = self.seed, self.max_evaluations, self.max_seconds
+        if self.rng not in ("replay", "philox"):
+            raise ConfigError(f"rng must be 'replay' or 'philox', not {self.rng!r}")
+        c.rng = 1 if self.rng == "philox" else 0
         return c
 
 

@@ -896,6 +896,8 @@ tgb::QdParams qd_params(tg_context* ctx, const tg_qd_config* c) {
   p.seed = c->seed;
   p.n_actions = ctx->g.A;
   p.n_disc = ctx->g.D;
+  if (c->rng != tgb::kRngReplay && c->rng != tgb::kRngPhilox) throw tgb::ConfigError("rng must be 0 (replay) or 1 (philox)");
+  p.rng = c->rng;
   return p;
 }
 

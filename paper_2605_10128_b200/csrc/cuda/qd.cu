@@ -50,8 +50,46 @@ struct Mt64 {
   }
 };
 
+// Philox4x32-10 (Salmon et al., SC'11): counter-based, stateless per draw; the
+// lane key is the same derive_seed(seed, iter, lane + 1) the replay mode seeds
+// mt19937_64 with, the counter is the draw index. Two 64-bit draws per block.
+struct Philox {
+  uint32_t k0, k1;
+  uint32_t ctr = 0;
+  unsigned long long buf = 0;
+  bool have = false;
+  __device__ void seed(unsigned long long s) {
+    k0 = static_cast<uint32_t>(s);
+    k1 = static_cast<uint32_t>(s >> 32);
+    ctr = 0;
+    have = false;
+  }
+  __device__ unsigned long long next() {
+    if (have) {
+      have = false;
+      return buf;
+    }
+    uint32_t c0 = ctr++, c1 = 0x7f4a7c15u, c2 = 0, c3 = 0, a = k0, b = k1;
+#pragma unroll
+    for (int i = 0; i < 10; ++i) {
+      const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+      const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+      c0 = hi1 ^ c1 ^ a;
+      c1 = lo1;
+      c2 = hi0 ^ c3 ^ b;
+      c3 = lo0;
+      a += 0x9E3779B9u;
+      b += 0xBB67AE85u;
+    }
+    buf = (static_cast<unsigned long long>(c3) << 32) | c2;
+    have = true;
+    return (static_cast<unsigned long long>(c1) << 32) | c0;
+  }
+};
+
 // uniform_int_distribution<int>(a, b) over a 64-bit engine (uniform_int_dist.h:257-320)
-__device__ int uniform_int(Mt64& r, int a, int b) {
+template <class Rng>
+__device__ int uniform_int(Rng& r, int a, int b) {
   const unsigned long long urange =
       static_cast<unsigned long long>(static_cast<long long>(b)) - static_cast<unsigned long long>(static_cast<long long>(a));
   const unsigned long long range = urange + 1ull;
@@ -70,19 +108,22 @@ __device__ int uniform_int(Mt64& r, int a, int b) {
 }
 
 // generate_canonical<double, 53> (random.tcc:3349-3381): one 64-bit draw / 2^64
-__device__ __forceinline__ double canonical(Mt64& r) {
+template <class Rng>
+__device__ __forceinline__ double canonical(Rng& r) {
   double v = __dmul_rn(__ull2double_rn(r.next()), 0x1p-64);
   if (v >= 1.0) v = 1.0 - 0x1p-53;
   return v;
 }
 
 // uniform_real_distribution<double>(a, b): (u * (b - a)) + a, no contraction (random.h:1909)
-__device__ __forceinline__ double uniform_real(Mt64& r, double a, double b) {
+template <class Rng>
+__device__ __forceinline__ double uniform_real(Rng& r, double a, double b) {
   return __dadd_rn(__dmul_rn(canonical(r), __dsub_rn(b, a)), a);
 }
 
 // poisson_distribution<int>, mean < 12 branch (random.tcc:1401-1411)
-__device__ int poisson(Mt64& r, double thr) {
+template <class Rng>
+__device__ int poisson(Rng& r, double thr) {
   int x = 0;
   double prod = 1.0;
   do {
@@ -102,7 +143,8 @@ struct Ops {
 };
 
 // choose_feasible_op, qd_optimizer.cpp:100-113
-__device__ int choose_op(const double* w, const bool* ok, Mt64& r) {
+template <class Rng>
+__device__ int choose_op(const double* w, const bool* ok, Rng& r) {
   double total = 0.0;
   for (int i = 0; i < 4; ++i)
     if (ok[i]) total = __dadd_rn(total, w[i]);
@@ -125,7 +167,8 @@ __device__ void sort_small(int* v, int n) {
 }
 
 // qd_optimizer.cpp:115-155
-__device__ void mutate_actions_once(const Ops& o, int* g, Mt64& r, int* trace) {
+template <class Rng>
+__device__ void mutate_actions_once(const Ops& o, int* g, Rng& r, int* trace) {
   const int na = o.p.n_a;
   // AddActionPool: excluded station ranges, sorted as pairs
   int elo[kMaxSplits], ehi[kMaxSplits], nex = 0, excluded = 0;
@@ -206,7 +249,8 @@ __device__ void mutate_actions_once(const Ops& o, int* g, Mt64& r, int* trace) {
 }
 
 // qd_optimizer.cpp:157-198
-__device__ void mutate_disconnections_once(const Ops& o, int* g, Mt64& r, int* trace) {
+template <class Rng>
+__device__ void mutate_disconnections_once(const Ops& o, int* g, Rng& r, int* trace) {
   const int na = o.p.n_a, nd = o.p.n_d;
   int* d = g + na;
   int used[kMaxRemovedSweep], nu = 0;
@@ -239,7 +283,8 @@ __device__ void mutate_disconnections_once(const Ops& o, int* g, Mt64& r, int* t
 }
 
 // qd_optimizer.cpp:202-210
-__device__ void mutate(const Ops& o, int* g, Mt64& r, int* trace, int* n_trace) {
+template <class Rng>
+__device__ void mutate(const Ops& o, int* g, Rng& r, int* trace, int* n_trace) {
   int n = poisson(r, o.p.poisson_thr);
   const int hi = o.p.n_a > 1 ? o.p.n_a : 1;
   n = n < 1 ? 1 : (n > hi ? hi : n);
@@ -250,7 +295,8 @@ __device__ void mutate(const Ops& o, int* g, Mt64& r, int* trace, int* n_trace) 
 }
 
 // qd_optimizer.cpp:217-231
-__device__ int union_draw(const int* p1, int n1, const int* p2, int n2, double pc1, Mt64& r) {
+template <class Rng>
+__device__ int union_draw(const int* p1, int n1, const int* p2, int n2, double pc1, Rng& r) {
   const double w1 = n1 == 0 ? 0.0 : pc1;
   const double w2 = n2 == 0 ? 0.0 : __dsub_rn(1.0, pc1);
   if (__dadd_rn(w1, w2) <= 0.0) return -1;
@@ -271,7 +317,8 @@ __device__ bool contains(const int* v, int n, int x) {
 }
 
 // qd_optimizer.cpp:235-277
-__device__ void crossover(const Ops& o, const int* g1, const int* g2, int* child, Mt64& r) {
+template <class Rng>
+__device__ void crossover(const Ops& o, const int* g1, const int* g2, int* child, Rng& r) {
   const int na = o.p.n_a, nd = o.p.n_d;
   for (int k = 0; k < na + nd; ++k) child[k] = -1;
   int a1[kMaxSplits], a2[kMaxSplits], n1 = 0, n2 = 0;
@@ -328,11 +375,12 @@ __device__ const int* member(const Archive& a, const QdParams& p, int ns, int fl
   return a.genome + (static_cast<size_t>(lo) * p.cap + pos) * ns;
 }
 
+template <class Rng>
 __global__ void k_offspring(DevGrid g, QdParams p, Archive a, int* genomes) {
   __shared__ int b_mc;
   const long long it = a.iter[0];
   if (threadIdx.x == 0) {
-    Mt64 ir;
+    Rng ir;
     ir.seed(derive_seed(p.seed, 0x17e7ull, static_cast<unsigned long long>(it)));
     b_mc = uniform_int(ir, 0, p.batch);
   }
@@ -341,7 +389,7 @@ __global__ void k_offspring(DevGrid g, QdParams p, Archive a, int* genomes) {
   if (lane >= p.batch) return;
   const int ns = p.n_a + p.n_d;
   Ops o{g, p};
-  Mt64 r;
+  Rng r;
   r.seed(derive_seed(p.seed, static_cast<unsigned long long>(it), static_cast<unsigned long long>(lane) + 1ull));
   const int total = a.flat_start[p.cells];
   int child[kMaxSlots];
@@ -357,13 +405,14 @@ __global__ void k_offspring(DevGrid g, QdParams p, Archive a, int* genomes) {
   for (int k = 0; k < ns; ++k) genomes[static_cast<size_t>(lane) * ns + k] = child[k];
 }
 
+template <class Rng>
 __global__ void k_mutate_lanes(DevGrid g, QdParams p, const int* parents, const unsigned long long* seeds, int n,
                                int* children) {
   const int lane = blockIdx.x * blockDim.x + threadIdx.x;
   if (lane >= n) return;
   const int ns = p.n_a + p.n_d;
   Ops o{g, p};
-  Mt64 r;
+  Rng r;
   r.seed(seeds[lane]);
   int child[kMaxSlots];
   for (int k = 0; k < ns; ++k) child[k] = parents[static_cast<size_t>(lane) * ns + k];
@@ -371,13 +420,14 @@ __global__ void k_mutate_lanes(DevGrid g, QdParams p, const int* parents, const 
   for (int k = 0; k < ns; ++k) children[static_cast<size_t>(lane) * ns + k] = child[k];
 }
 
+template <class Rng>
 __global__ void k_crossover_lanes(DevGrid g, QdParams p, const int* p1, const int* p2,
                                   const unsigned long long* seeds, int n, int* children) {
   const int lane = blockIdx.x * blockDim.x + threadIdx.x;
   if (lane >= n) return;
   const int ns = p.n_a + p.n_d;
   Ops o{g, p};
-  Mt64 r;
+  Rng r;
   r.seed(seeds[lane]);
   int child[kMaxSlots];
   crossover(o, p1 + static_cast<size_t>(lane) * ns, p2 + static_cast<size_t>(lane) * ns, child, r);
@@ -637,7 +687,11 @@ void launch_archive_reset(const QdState& q, cudaStream_t s) {
 
 void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStream_t s) {
   constexpr int kThreads = 64;  // lanes carry a 2.5 KB engine state in local memory
-  k_offspring<<<(q.p.batch + kThreads - 1) / kThreads, kThreads, 0, s>>>(g, q.p, q.a, genomes);
+  const int blocks = (q.p.batch + kThreads - 1) / kThreads;
+  if (q.p.rng == kRngPhilox)
+    k_offspring<Philox><<<blocks, kThreads, 0, s>>>(g, q.p, q.a, genomes);
+  else
+    k_offspring<Mt64><<<blocks, kThreads, 0, s>>>(g, q.p, q.a, genomes);
 }
 
 namespace {
@@ -673,12 +727,18 @@ int launch_archive_merge(const QdState& q, const void* blobs, int n_islands, Mer
 
 void launch_mutate_lanes(const DevGrid& g, const QdState& q, const int* parents, const unsigned long long* seeds, int n,
                          int* children, cudaStream_t s) {
-  k_mutate_lanes<<<(n + 63) / 64, 64, 0, s>>>(g, q.p, parents, seeds, n, children);
+  if (q.p.rng == kRngPhilox)
+    k_mutate_lanes<Philox><<<(n + 63) / 64, 64, 0, s>>>(g, q.p, parents, seeds, n, children);
+  else
+    k_mutate_lanes<Mt64><<<(n + 63) / 64, 64, 0, s>>>(g, q.p, parents, seeds, n, children);
 }
 
 void launch_crossover_lanes(const DevGrid& g, const QdState& q, const int* p1, const int* p2,
                             const unsigned long long* seeds, int n, int* children, cudaStream_t s) {
-  k_crossover_lanes<<<(n + 63) / 64, 64, 0, s>>>(g, q.p, p1, p2, seeds, n, children);
+  if (q.p.rng == kRngPhilox)
+    k_crossover_lanes<Philox><<<(n + 63) / 64, 64, 0, s>>>(g, q.p, p1, p2, seeds, n, children);
+  else
+    k_crossover_lanes<Mt64><<<(n + 63) / 64, 64, 0, s>>>(g, q.p, p1, p2, seeds, n, children);
 }
 
 }  // namespace tgb

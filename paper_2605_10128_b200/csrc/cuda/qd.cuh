@@ -7,6 +7,8 @@
 namespace tgb {
 
 constexpr int kMaxCellCap = 16;  // QdConfig::cell_capacity supported on the device
+constexpr int kRngReplay = 0;    // per-lane std::mt19937_64 + libstdc++ distributions (reference stream)
+constexpr int kRngPhilox = 1;    // counter-based Philox4x32-10, same distributions
 
 // QdConfig (qd_optimizer.hpp:15-32) as passed to kernels.
 struct QdParams {
@@ -18,6 +20,7 @@ struct QdParams {
   double poisson_thr;  // exp(-mutation_mean), computed by the host libm like libstdc++ does
   unsigned long long seed;
   int n_actions, n_disc;
+  int rng;             // kRngReplay (mt19937_64, bit-exact with the reference) or kRngPhilox
 };
 
 // Device archive of cells x cell_capacity entries, cell-major (Repertoire,

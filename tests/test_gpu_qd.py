@@ -257,3 +257,43 @@ def test_island_merge_matches_sequential_insert(data_dir):
     assert [(e.cell, e.score.fitness) for e in before] == [(e.cell, e.score.fitness) for e in after]
     sess[0].step(3)
     assert sess[0].fetch().best_fitness >= snaps[0].best_fitness
+
+
+def _valid(ctx, g, n_a=3):
+    # genome_valid, genome.cpp:49-63
+    acts = [a for a in g[:n_a] if a >= 0]
+    disc = [d for d in g[n_a:] if d >= 0]
+    st = [ctx.actions.substation_of(a) for a in acts]
+    return (len(set(st)) == len(st) and len(set(disc)) == len(disc) and all(a < ctx.actions.n_actions for a in acts)
+            and all(d < len(ctx.actions.disconnectables) for d in disc))
+
+
+def test_philox_mode_valid_and_distributed_like_replay(data_dir):
+    """Counter-based lane RNG (north_star item 1; extension): valid offspring,
+    the same operator statistics as the reference stream (two-sample
+    chi-square on the changed-slot counts), a working optimizer."""
+    text = open(os.path.join(data_dir, "grid14_congested.json")).read()
+    ctx, orc = _ctx(text)
+    par = _parents(orc, 20000, 8)
+    seeds = np.arange(len(par), dtype=np.uint64) * np.uint64(0x9E3779B97F4A7C15) + np.uint64(99)
+    hist = {}
+    for rng in ("replay", "philox"):
+        kids = P.mutate_lanes(ctx, P.QdConfig(rng=rng), par, seeds)
+        assert all(_valid(ctx, k) for k in kids)
+        changed = (kids != par).sum(1)
+        hist[rng] = np.bincount(changed, minlength=6)[:6].astype(float)
+        x = P.crossover_lanes(ctx, P.QdConfig(rng=rng), par, par[::-1].copy(), seeds)
+        assert all(_valid(ctx, k) for k in x)
+    a, b = hist["replay"], hist["philox"]
+    keep = (a + b) > 20
+    chi2 = float((((a - b) ** 2) / (a + b))[keep].sum())
+    assert chi2 < 25.0, (a, b)   # 5 dof, p ~ 1e-4
+    assert not np.array_equal(P.mutate_lanes(ctx, P.QdConfig(rng="philox"), par[:64], seeds[:64]),
+                              P.mutate_lanes(ctx, P.QdConfig(rng="replay"), par[:64], seeds[:64]))
+    kw = dict(seed=3, batch_size=64, iters_per_epoch=50, max_evaluations=1 + 64 * 150)
+    rep = P.run_optimizer(ctx, P.QdConfig(**kw))
+    phi = P.run_optimizer(ctx, P.QdConfig(rng="philox", **kw))
+    assert phi.stats.evaluations == rep.stats.evaluations
+    assert phi.repertoire.best_fitness >= rep.repertoire.best_fitness - 0.05 * abs(rep.repertoire.best_fitness)
+    with pytest.raises(P.ConfigError):
+        P.QdConfig(rng="xorshift").to_c()
