@@ -89,6 +89,9 @@ __device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
       "r"(parity)
       : "memory");
 }
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
 // TMA bulk copy global -> shared, completion counted on the mbarrier
 __device__ __forceinline__ void bulk_g2s(void* dst, const void* src, uint32_t bytes, uint64_t* bar) {
   asm volatile(
@@ -130,7 +133,7 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
 
 template <int R, bool FULL>
 __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
-                                          uint64_t* bars, int* release, double* rmax_s, double* amax_s) {
+                                          uint64_t* bars, double* rmax_s, double* amax_s) {
   using Rg = Ring<R, FULL>;
   constexpr int S = Rg::S, NST = Rg::stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -182,6 +185,16 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       if (lane == 0) rms[1 + q] = r * (1.0 + 1e-12);
     }
     __syncwarp();
+  }
+  // small ranks keep the per-warp skip weights in registers (stage 1 then reads
+  // only the row data from shared memory)
+  constexpr bool kRegW = !FULL && R <= 3;
+  double areg[kRegW ? kTmaxSub : 1], wreg[kRegW ? S : 1];
+  if (kRegW) {
+#pragma unroll
+    for (int q = 0; q < kTmaxSub; ++q) areg[q] = asub[q];
+#pragma unroll
+    for (int q = 0; q < S; ++q) wreg[q] = rms[q];
   }
 
   const int nchunks = (g.E + kChunk - 1) / kChunk;
@@ -275,7 +288,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
 #pragma unroll
         for (int q = 0; q < S / 2; ++q) {
           const double2 p2 = fr[q];
-          const double2 w2 = wr[q];
+          const double2 w2 = kRegW ? make_double2(wreg[kRegW ? 2 * q : 0], wreg[kRegW ? 2 * q + 1 : 0]) : wr[q];
           lrb = fma(fabs(p2.x), w2.x, lrb);
           lrb = fma(fabs(p2.y), w2.y, lrb);
           if (q == 0) fc = p2.x;
@@ -286,7 +299,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
 #pragma unroll
         for (int q = 0; q < kTmaxSub / 2; ++q) {
           const double2 t2 = tmr[q];
-          const double2 a2 = ar[q];
+          const double2 a2 = kRegW ? make_double2(areg[kRegW ? 2 * q : 0], areg[kRegW ? 2 * q + 1 : 0]) : ar[q];
           ta = fmax(ta, fmax(t2.x * a2.x, t2.y * a2.y));
         }
         const double2 d0 = *reinterpret_cast<const double2*>(rec + kTmaxSub);
@@ -338,20 +351,16 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
         }
       }
     }
-    // release the stage; the last warp out refills it (no CTA-wide barrier)
+    // release the stage (arrive on its empty barrier, no return value); thread 0
+    // refills it once all 16 warps have left it (no CTA-wide barrier)
     __syncwarp();
-    if (lane == 0) {
-      __threadfence_block();
-      const int done = atomicAdd(release + s, 1);
-      if (done == kWarps - 1) {
-        release[s] = 0;
-        __threadfence_block();
-        if (i + NST < nchunks) {
-          asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-          issue_chunk<R, FULL>(g, b, w, tile, i + NST, smem + s * Rg::doubles, bars + s);
-        }
-      }
+    if (lane == 0) mbar_arrive(bars + kMaxStages + s);
+    if (threadIdx.x == 0 && i + NST < nchunks) {
+      mbar_wait(bars + kMaxStages + s, (i / NST) & 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue_chunk<R, FULL>(g, b, w, tile, i + NST, smem + s * Rg::doubles, bars + s);
     }
+    __syncwarp();
   }
   if (!FULL && lane == 0) {
     atomicAdd(b.rows_done, static_cast<unsigned long long>(rows_computed));
@@ -376,7 +385,6 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CtaWork w;
   __shared__ int r_s;
-  __shared__ int release[kMaxStages];
   __shared__ __align__(16) double rmax_s[kWarps * kStride];
   __shared__ __align__(16) double amax_s[kWarps * kTmaxSub];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
@@ -397,19 +405,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
       if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
     w.ncand = n;
     w.group = group;
-    for (int s = 0; s < kMaxStages; ++s) mbar_init(bars + s, 1), release[s] = 0;
+    for (int s = 0; s < kMaxStages; ++s) mbar_init(bars + s, 1), mbar_init(bars + kMaxStages + s, kWarps);
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
   __syncthreads();
   switch (r_s) {
-    case 0: sweep_cta<0, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 1: sweep_cta<1, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 2: sweep_cta<2, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 3: sweep_cta<3, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 4: sweep_cta<4, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 5: sweep_cta<5, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    case 6: sweep_cta<6, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
-    default: sweep_cta<7, FULL>(g, b, w, tile, smem, bars, release, rmax_s, amax_s); break;
+    case 0: sweep_cta<0, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 1: sweep_cta<1, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 2: sweep_cta<2, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 3: sweep_cta<3, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 4: sweep_cta<4, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 5: sweep_cta<5, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 6: sweep_cta<6, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    default: sweep_cta<7, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
   }
 }
 

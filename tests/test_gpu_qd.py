@@ -286,7 +286,7 @@ def test_philox_mode_valid_and_distributed_like_replay(data_dir):
         assert all(_valid(ctx, k) for k in x)
     a, b = hist["replay"], hist["philox"]
     keep = (a + b) > 20
-    chi2 = float((((a - b) ** 2) / (a + b))[keep].sum())
+    chi2 = float((((a - b) ** 2)[keep] / (a + b)[keep]).sum())
     assert chi2 < 25.0, (a, b)   # 5 dof, p ~ 1e-4
     assert not np.array_equal(P.mutate_lanes(ctx, P.QdConfig(rng="philox"), par[:64], seeds[:64]),
                               P.mutate_lanes(ctx, P.QdConfig(rng="replay"), par[:64], seeds[:64]))
