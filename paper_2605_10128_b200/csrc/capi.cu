@@ -683,8 +683,8 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
       double* d_pr = A.upload(pr, s);
       double* theta0 = A.alloc<double>(Nr);
       double* f0 = A.alloc<double>(E);
-      double* tmax = A.alloc<double>(tmax_n);
-      check(cudaMemsetAsync(tmax, 0, tmax_n * sizeof(double), s), "tmax");
+      float* tmax = A.alloc<float>(tmax_n);
+      check(cudaMemsetAsync(tmax, 0, tmax_n * sizeof(float), s), "tmax");
       double* alpha0 = A.alloc<double>(std::max(g.Kpad, 1));
       gv.theta0 = theta0;
       gv.f0 = f0;

@@ -20,7 +20,8 @@ constexpr int kMaxTerms = 512;     // sparse coefficients over all Z columns
 constexpr int kMaxPMod = 16;       // omitted injections (p modifications)
 constexpr int kMaxInjMoved = 64;   // injections moved to new nodes
 constexpr int kTmaxSub = 8;        // sub-tiles of a sweep tile carrying their own max |T_base| per row
-constexpr int kRec = kTmaxSub + 2; // per (tile, row) skip record: kTmaxSub sub-tile maxima, max / min of T_base*alpha0
+constexpr int kRec = kTmaxSub + 4; // floats per (tile, row) skip record: kTmaxSub sub-tile maxima of |T_base| (rounded
+                                   // up), max (rounded up) / min (rounded down) of T_base*alpha0, 2 pad (48 B)
 
 // Flat, read-only network tables on the device (built once per context by
 // engine_setup.cu from the host Grid/ActionTable).
@@ -50,7 +51,7 @@ struct DevGrid {
   const int* ks_cont;      // [Ks]  contingency index
   const int* ks_branch;    // [Ks]
   const double* TK;        // [Kpad/128][E][128] T_base[e, ks_branch[k]] tiles (0 rows for out-of-service e)
-  const double* Tmax;      // [Kpad/128][E + 32][kRec] skip record per (tile, row): max over each sub-tile of
+  const float* Tmax;       // [Kpad/128][E + 32][kRec] skip record per (tile, row): max over each sub-tile of
                            // |T_base[e, k]|, then max_k and min_k of T_base[e, k] * alpha0[k] over the tile
   const double* alpha0;    // [Kpad] alpha of the unchanged topology, f0[beta] / (1 - Tdiag[beta]) (0 padding)
   const int* kx_cont;      // [Kx]

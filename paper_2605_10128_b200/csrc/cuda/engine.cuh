@@ -113,7 +113,7 @@ inline int max_sweep_groups(int n) { return (n + 7) / 8 + kSweepRank + 1; }
 // Returns false when a pivot is not positive (disconnected grid).
 bool device_spd_inverse(double* a, int n, cudaStream_t stream);
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
-                        double* tmax, double* alpha0, cudaStream_t stream);
+                        float* tmax, double* alpha0, cudaStream_t stream);
 
 }  // namespace tgb
 

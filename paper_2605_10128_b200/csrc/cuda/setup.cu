@@ -124,14 +124,14 @@ __global__ void k_alpha0(DevGrid g, double* alpha0) {
 // Skip record [tile][e][kRec]: max_k |T_base[e, k]| over each sub-tile, then
 // max_k and min_k of T_base[e, k] * alpha0[k] over the tile (the unchanged
 // topology's post-contingency flow change on e).
-__global__ void k_tmax(DevGrid g, const double* tk, const double* alpha0, double* tmax, int W, int ld) {
+__global__ void k_tmax(DevGrid g, const double* tk, const double* alpha0, float* tmax, int W, int ld) {
   const int ntiles = g.Kpad / W;
   const int total = ntiles * g.E;
   for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < total; idx += gridDim.x * blockDim.x) {
     const int tile = idx / g.E, e = idx % g.E;
     const double* row = tk + (static_cast<size_t>(tile) * g.E + e) * W;
     const double* a0 = alpha0 + static_cast<size_t>(tile) * W;
-    double* rec = tmax + (static_cast<size_t>(tile) * ld + e) * kRec;
+    float* rec = tmax + (static_cast<size_t>(tile) * ld + e) * kRec;
     const int sw = W / kTmaxSub;
     double dmax = 0.0, dmin = 0.0;
     for (int s = 0; s < kTmaxSub; ++s) {
@@ -142,10 +142,12 @@ __global__ void k_tmax(DevGrid g, const double* tk, const double* alpha0, double
         dmax = fmax(dmax, d);
         dmin = fmin(dmin, d);
       }
-      rec[s] = m;
+      rec[s] = __double2float_ru(m);  // rounded up: the bound stays rigorous
     }
-    rec[kTmaxSub] = dmax;
-    rec[kTmaxSub + 1] = dmin;
+    rec[kTmaxSub] = __double2float_ru(dmax);
+    rec[kTmaxSub + 1] = __double2float_rd(dmin);
+    rec[kTmaxSub + 2] = 0.f;
+    rec[kTmaxSub + 3] = 0.f;
   }
 }
 
@@ -183,7 +185,7 @@ bool device_spd_inverse(double* a, int n, cudaStream_t stream) {
 }
 
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
-                        double* tmax, double* alpha0, cudaStream_t stream) {
+                        float* tmax, double* alpha0, cudaStream_t stream) {
   k_theta<<<(g.Nr + 255) / 256 + 1, 256, 0, stream>>>(g, p_red, theta0);
   DevGrid g2 = g;
   g2.theta0 = theta0;

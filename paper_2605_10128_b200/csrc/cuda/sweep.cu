@@ -63,7 +63,7 @@ struct Ring {
   static constexpr size_t T = FULL ? static_cast<size_t>(kChunk) * kTileK : 0;  // T_base tile rows
   static constexpr size_t F = static_cast<size_t>(kMaxCand) * kChunk * S;       // candidate rows
   static constexpr size_t L = kChunk;                                           // limits
-  static constexpr size_t M = FULL ? 0 : static_cast<size_t>(kChunk) * kRec;    // skip records
+  static constexpr size_t M = FULL ? 0 : static_cast<size_t>(kChunk) * kRec / 2;  // skip records (floats)
   static constexpr size_t doubles = T + F + L + M;
   static constexpr size_t fit = kStageBudget / (doubles * sizeof(double));
   static constexpr int stages = fit < static_cast<size_t>(kMaxStages) ? static_cast<int>(fit) : kMaxStages;
@@ -121,7 +121,7 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
   const uint32_t bt = FULL ? rows * kTileK * sizeof(double) : 0;
   const uint32_t bf = Rg::F * sizeof(double);  // the group's rows of this chunk: one contiguous block
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
-  const uint32_t bm = FULL ? 0 : rows * kRec * sizeof(double);
+  const uint32_t bm = FULL ? 0 : rows * kRec * sizeof(float);
   mbar_expect_tx(bar, bt + bf + bl + bm);
   if (FULL) bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
   bulk_g2s(stage + Rg::T, b.feat + feat_index(w.group * kGroupSlots, b.nchunks, e0, R), bf, bar);
@@ -129,6 +129,7 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
   if (!FULL)
     bulk_g2s(stage + Rg::T + Rg::F + Rg::L, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kRec, bm,
              bar);
+  static_assert(kRec % 4 == 0, "skip records are whole float4");
 }
 
 template <int R, bool FULL>
@@ -281,7 +282,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       uint32_t thr_lane = 0u;
       if (lane < rows) {
         const double lim = sL[lane] * (1.0 - 1e-12);
-        const double* rec = st + Rg::T + Rg::F + Rg::L + lane * kRec;
+        const float4* rec = reinterpret_cast<const float4*>(st + Rg::T + Rg::F + Rg::L) + lane * (kRec / 4);
         const double2* fr = reinterpret_cast<const double2*>(sF + lane * S);
         const double2* wr = reinterpret_cast<const double2*>(rms);
         double lrb = 0.0, fc = 0.0;
@@ -293,16 +294,18 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
           lrb = fma(fabs(p2.y), w2.y, lrb);
           if (q == 0) fc = p2.x;
         }
-        const double2* tmr = reinterpret_cast<const double2*>(rec);
         const double2* ar = reinterpret_cast<const double2*>(asub);
         double ta = 0.0;
 #pragma unroll
-        for (int q = 0; q < kTmaxSub / 2; ++q) {
-          const double2 t2 = tmr[q];
-          const double2 a2 = kRegW ? make_double2(areg[kRegW ? 2 * q : 0], areg[kRegW ? 2 * q + 1 : 0]) : ar[q];
-          ta = fmax(ta, fmax(t2.x * a2.x, t2.y * a2.y));
+        for (int q = 0; q < kTmaxSub / 4; ++q) {
+          const float4 t4 = rec[q];
+          const double2 a01 = kRegW ? make_double2(areg[kRegW ? 4 * q : 0], areg[kRegW ? 4 * q + 1 : 0]) : ar[2 * q];
+          const double2 a23 = kRegW ? make_double2(areg[kRegW ? 4 * q + 2 : 0], areg[kRegW ? 4 * q + 3 : 0])
+                                    : ar[2 * q + 1];
+          ta = fmax(ta, fmax(fmax(t4.x * a01.x, t4.y * a01.y), fmax(t4.z * a23.x, t4.w * a23.y)));
         }
-        const double2 d0 = *reinterpret_cast<const double2*>(rec + kTmaxSub);
+        const float4 d4 = rec[kTmaxSub / 4];
+        const double2 d0 = make_double2(d4.x, d4.y);
         const double thr = lim - lrb;
         thr_lane = thr > 0.0 ? hi_abs(thr) : 0u;
         const double wd = ta + lrb;
