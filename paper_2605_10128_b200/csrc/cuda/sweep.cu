@@ -60,10 +60,12 @@ __host__ __device__ constexpr int cand_per_cta(int) { return kWarps; }
 template <int R, bool FULL>
 struct Ring {
   static constexpr int S = row_stride(R);
+  static constexpr int H = FULL ? 1 : 2;                                         // 32-row chunks per stage
+  static constexpr size_t FH = static_cast<size_t>(kMaxCand) * kChunk * S;       // one chunk of candidate rows
   static constexpr size_t T = FULL ? static_cast<size_t>(kChunk) * kTileK : 0;  // T_base tile rows
-  static constexpr size_t F = static_cast<size_t>(kMaxCand) * kChunk * S;       // candidate rows
-  static constexpr size_t L = kChunk;                                           // limits
-  static constexpr size_t M = FULL ? 0 : static_cast<size_t>(kChunk) * kRec / 2;  // skip records (floats)
+  static constexpr size_t F = H * FH;                                           // candidate rows
+  static constexpr size_t L = H * kChunk;                                       // limits
+  static constexpr size_t M = FULL ? 0 : static_cast<size_t>(H) * kChunk * kRec / 2;  // skip records (floats)
   static constexpr size_t doubles = T + F + L + M;
   static constexpr size_t fit = kStageBudget / (doubles * sizeof(double));
   static constexpr int stages = fit < static_cast<size_t>(kMaxStages) ? static_cast<int>(fit) : kMaxStages;
@@ -110,16 +112,17 @@ struct CtaWork {
   int group;
 };
 
-// Producer: stage <- chunk i (T tile rows when FULL, the group's candidate
-// rows, limits, skip records when not FULL).
+// Producer: stage <- stage-chunk i = 32-row chunks [H i, H i + H) (T tile rows
+// when FULL, the group's candidate rows, limits, skip records when not FULL).
 template <int R, bool FULL>
 __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, int i,
                                            double* stage, uint64_t* bar) {
   using Rg = Ring<R, FULL>;
-  const int e0 = i * kChunk;
-  const int rows = min(kChunk, g.E - e0);
+  const int e0 = i * Rg::H * kChunk;
+  const int rows = min(Rg::H * kChunk, g.E - e0);
+  const int nch = (rows + kChunk - 1) / kChunk;
   const uint32_t bt = FULL ? rows * kTileK * sizeof(double) : 0;
-  const uint32_t bf = Rg::F * sizeof(double);  // the group's rows of this chunk: one contiguous block
+  const uint32_t bf = nch * Rg::FH * sizeof(double);  // the group's rows of these chunks: one contiguous block
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
   const uint32_t bm = FULL ? 0 : rows * kRec * sizeof(float);
   mbar_expect_tx(bar, bt + bf + bl + bm);
@@ -198,7 +201,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     for (int q = 0; q < S; ++q) wreg[q] = rms[q];
   }
 
-  const int nchunks = (g.E + kChunk - 1) / kChunk;
+  const int nchunks = (g.E + Rg::H * kChunk - 1) / (Rg::H * kChunk);  // stage-chunks
   unsigned rows_computed = 0, rows_offered = 0, rows_exact = 0, rows_partial = 0;  // skip statistics
   if (threadIdx.x == 0)
     for (int s = 0; s < NST && s < nchunks; ++s)
@@ -253,10 +256,13 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     const int s = i % NST;
     const double* st = smem + s * Rg::doubles;
     mbar_wait(bars + s, (i / NST) & 1);
-    const int e0 = i * kChunk;
+#pragma unroll 1
+    for (int h = 0; h < Rg::H; ++h) {
+    const int e0 = (i * Rg::H + h) * kChunk;
     const int rows = min(kChunk, g.E - e0);
-    const double* sF = st + Rg::T + static_cast<size_t>(warp) * kChunk * S;
-    const double* sL = st + Rg::T + Rg::F;
+    if (rows <= 0) break;
+    const double* sF = st + Rg::T + h * Rg::FH + static_cast<size_t>(warp) * kChunk * S;
+    const double* sL = st + Rg::T + Rg::F + h * kChunk;
     if (FULL) {
       const double* sT = st + lane * kKpl;
       for (int el = 0; el < rows; ++el) {
@@ -282,7 +288,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       uint32_t thr_lane = 0u;
       if (lane < rows) {
         const double lim = sL[lane] * (1.0 - 1e-12);
-        const float4* rec = reinterpret_cast<const float4*>(st + Rg::T + Rg::F + Rg::L) + lane * (kRec / 4);
+        const float4* rec = reinterpret_cast<const float4*>(st + Rg::T + Rg::F + Rg::L) + (h * kChunk + lane) * (kRec / 4);
         const double2* fr = reinterpret_cast<const double2*>(sF + lane * S);
         const double2* wr = reinterpret_cast<const double2*>(rms);
         double lrb = 0.0, fc = 0.0;
@@ -354,6 +360,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
         }
       }
     }
+    }  // h
     // release the stage (arrive on its empty barrier, no return value); thread 0
     // refills it once all 16 warps have left it (no CTA-wide barrier)
     __syncwarp();
