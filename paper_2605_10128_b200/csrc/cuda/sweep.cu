@@ -49,7 +49,7 @@ constexpr int kChunk = 32;               // branches per pipeline stage
 constexpr int kMaxCand = kWarps;         // one candidate per warp
 constexpr int kGroupBlock = 8;           // candidate groups per CTA super-block (L2 reuse)
 constexpr int kMaxStages = 8;
-constexpr size_t kStageBudget = 200 * 1024;  // dynamic shared memory for the stage ring
+constexpr size_t kStageBudget = 216 * 1024;  // dynamic shared memory for the stage ring
 constexpr int kSubLanes = 32 / kTmaxSub;     // lanes per skip sub-tile
 static_assert(kTileK % kTmaxSub == 0 && kSubLanes * kTmaxSub == 32, "sub-tile layout");
 static_assert(kMaxCand == kGroupSlots && kChunk == kChunkRows, "sweep tiles must match the row layout");
@@ -60,7 +60,7 @@ __host__ __device__ constexpr int cand_per_cta(int) { return kWarps; }
 template <int R, bool FULL>
 struct Ring {
   static constexpr int S = row_stride(R);
-  static constexpr int H = FULL ? 1 : 2;                                         // 32-row chunks per stage
+  static constexpr int H = FULL ? 1 : (R <= 3 ? 4 : 2);                          // 32-row chunks per stage
   static constexpr size_t FH = static_cast<size_t>(kMaxCand) * kChunk * S;       // one chunk of candidate rows
   static constexpr size_t T = FULL ? static_cast<size_t>(kChunk) * kTileK : 0;  // T_base tile rows
   static constexpr size_t F = H * FH;                                           // candidate rows
