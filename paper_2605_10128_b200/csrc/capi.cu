@@ -263,6 +263,7 @@ void tg_context::ensure_capacity(int n) {
   b.energy = A.alloc<double>(static_cast<size_t>(cap) * Ka);
   b.isl_out = A.alloc<int>(cap);
   b.isl_bus = A.alloc<int>(cap);
+  b.nc0 = A.alloc<int>(cap);
   b.wl_list = A.alloc<int>(cap);
   b.wl_start = A.alloc<int>(tgb::kSweepRank + 1);
   b.wl_count = A.alloc<int>(tgb::kSweepRank + 1);

@@ -58,6 +58,8 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
   __shared__ Topo t;
   __shared__ double gram[kSweepRank * kSweepRank];
   __shared__ double thv[kSweepRank];
+  __shared__ int nc0_s;
+  if (threadIdx.x == 0) nc0_s = 0;
   const int words = (g.E + 31) >> 5;
   uint32_t* mv_bits = bits;
   uint32_t* rm_bits = bits + words;
@@ -87,7 +89,9 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       continue;
     }
     const int ns = t.ns, nv = t.nv, r = ns + nv, rs = row_stride(r);
-    // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0...]
+    // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0...]; lambda_c0 = #(|f_c| > limit)
+    // (dc_engine.cpp:397) counted on the way
+    int nc0 = 0;
     for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
       double phi[kMaxSplits], rho[kMaxCols];
       const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
@@ -95,6 +99,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
 #pragma unroll
       for (int i = 0; i < kStride; ++i) row[i] = 0.0;
       row[0] = cand_flow(g, t, e, phi, rho, on);
+      nc0 += fabs(row[0]) > g.br_lim[e];
       if (on) {
         const double be = g.br_b[e];
         for (int q = 0; q < ns; ++q) row[1 + q] = be * phi[q];
@@ -105,7 +110,11 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       for (int i = 0; i < kStride / 2; ++i)
         if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
     }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) nc0 += __shfl_xor_sync(0xffffffffu, nc0, o);
+    if ((threadIdx.x & 31) == 0) atomicAdd(&nc0_s, nc0);
     __syncthreads();
+    if (threadIdx.x == 0) b.nc0[c] = nc0_s, nc0_s = 0;
     // contingency rows: [alpha_k, R[:,k] * alpha_k, 0...], flag
     double* kd = b.kdat + static_cast<size_t>(c) * g.Kpad * kStride;
     uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad;
@@ -373,18 +382,18 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_finish(DevGrid g, Batch b
     }
     return;
   }
-  const int slot = b.slot[c], rank = b.rank[c];
   const unsigned long long* fm = b.fmax + static_cast<size_t>(c) * g.E;
   const unsigned long long* fb = b.fbus + static_cast<size_t>(c) * g.E;
   double so = 0.0, sb = 0.0;
-  int nc = 0, nc0 = 0;
+  int nc = 0, nc0 = lane == 0 ? b.nc0[c] : 0;  // counted by k_prep
   for (int e = lane; e < g.E; e += 32) {
     const double lim = g.br_lim[e];
     const double m = __longlong_as_double(static_cast<long long>(fm[e]));
-    const double mb = __longlong_as_double(static_cast<long long>(fb[e]));
     if (m > lim) so += m - lim, ++nc;
-    if (fabs(b.feat[feat_index(slot, b.nchunks, e, rank)]) > lim) ++nc0;
-    if (mb > lim) sb += mb - lim;
+    if (g.Kb > 0) {  // no busbar outages: fbus stays 0
+      const double mb = __longlong_as_double(static_cast<long long>(fb[e]));
+      if (mb > lim) sb += mb - lim;
+    }
   }
   int isl = 0;
   const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad;

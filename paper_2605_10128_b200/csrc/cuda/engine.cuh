@@ -71,6 +71,7 @@ struct Batch {
   unsigned long long* fmax;   // [n][E] max |f| over contingencies (bits of a non-negative double)
   unsigned long long* fbus;   // [n][E] max |f| over busbar outages
   double* energy;             // [n][Kall] outage energy per contingency
+  int* nc0;                   // [n] lambda_c0 of the candidate flows (k_prep)
   int* isl_out;               // [n] islanded special contingencies
   int* isl_bus;               // [n]
   int* wl_list;               // [n] candidates bucketed by rank
