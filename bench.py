@@ -210,7 +210,9 @@ def main():
     B = CONFIGS[args.config]["batch"]
     grid = P.grid_from_json_text(text)
     actions = P.build_action_set(grid)
-    ctx = P.DcContext(grid, actions, P.DcConfig(), device=dev)
+    t_setup = time.perf_counter()
+    ctx = P.DcContext(grid, actions, P.DcConfig(), device=dev)  # DcContext ctor: X, T_base, skip records on device
+    setup_s = time.perf_counter() - t_setup
     info = ctx.info()
     cfg = P.QdConfig(batch_size=B, iters_per_epoch=1 << 30, seed=1 + rank, rng=args.rng)  # one island per rank
     sess = P.QdSession(ctx, cfg)
@@ -359,7 +361,8 @@ def main():
                              "(no flush needed)",
                        "step": "one MapElites generation: mutate/crossover + full N-1 evaluation + archive insert",
                        "rng": args.rng,
-                       "archive_entries": len(snap.entries), "best_fitness": snap.best_fitness},
+                       "archive_entries": len(snap.entries), "best_fitness": snap.best_fitness,
+                       "context_setup_s": setup_s},
             "gpu_launches": int(launches),
             "roofline": {"bound": "fp64", "kernel": "k_sweep (fused N-1 sweep)", "achieved": dense_tflops,
                          "peak": peak, "unit": "TFLOP/s", "frac": dense_tflops / peak if peak else None,
