@@ -140,9 +140,16 @@ def cpu_baseline(text: str, n_target_s: float = 12.0, world: int = 1):
     n = int(max(32, min(20000, 32 * n_target_s / max(t, 1e-6))))
     sample = orc.random_genomes(n, 3, 2, seed=12)
     dt = orc.time_evaluate_batch(sample, 3, 2, 1)
-    return {"value": n / dt, "unit": "topologies/s", "cores": cores, "kind": "port",
+    T = n_timesteps(text)
+    note = (f"; {T} timesteps = {T} reference evaluations per topology (the reference evaluates one injection "
+            f"vector; timed on one profile, rate / {T})") if T > 1 else ""
+    return {"value": n / dt / T, "unit": "topologies/s", "cores": cores, "kind": "port",
             "sample": f"{n} random genomes (helpers.hpp random_genome, n_a=3, n_d=2) of this workload's grid, "
-                      f"full N-1, DcContext::evaluate_batch on {cores} threads, {dt:.1f} s"}
+                      f"full N-1, DcContext::evaluate_batch on {cores} threads, {dt:.1f} s{note}"}
+
+
+def n_timesteps(text: str) -> int:
+    return int(json.loads(text).get("timesteps", {}).get("count", 1))
 
 
 def run_reference(args, world, rank):
@@ -161,7 +168,7 @@ def run_reference(args, world, rank):
     total_n, total_t = 0, 0.0
     for k in range(args.steps):
         g = orc.random_genomes(per_step, 3, 2, seed=1000 + k)
-        total_t += orc.time_evaluate_batch(g, 3, 2, 1)
+        total_t += orc.time_evaluate_batch(g, 3, 2, 1) * n_timesteps(text)  # one reference evaluation per profile
         total_n += per_step
     value = total_n / total_t
     line = {"metric": "N-1-evaluated topologies/sec (DC)", "value": value, "unit": "topologies/s",
@@ -173,7 +180,9 @@ def run_reference(args, world, rank):
                        "note": "each step is a bounded sample of the workload's batch"},
             "cpu_baseline": {"value": value, "unit": "topologies/s", "cores": cores, "kind": "port",
                              "sample": f"{per_step} genomes per step x {args.steps} steps, DcContext::evaluate_batch "
-                                       f"(threads = {cores})"},
+                                       f"(threads = {cores})" + (f", x {n_timesteps(text)} profiles (one reference "
+                                                                  "evaluation per timestep, timed on one)"
+                                                                  if n_timesteps(text) > 1 else "")},
             "e2e": {"value": value, "unit": "topologies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
