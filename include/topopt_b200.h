@@ -261,6 +261,26 @@ tg_status tg_mutate_lanes(tg_context* ctx, const tg_qd_config* cfg, const int32_
 tg_status tg_crossover_lanes(tg_context* ctx, const tg_qd_config* cfg, const int32_t* parents1,
                              const int32_t* parents2, const uint64_t* seeds, int32_t n, int32_t* children);
 
+/* ---- snapshot hand-off to the AC stage ----
+ * SnapshotChannel, channel.hpp:15-79: single-producer single-consumer queue of
+ * RepertoireSnapshots; a bounded channel never blocks the producer, when full
+ * the oldest non-final snapshot is dropped; capacity 0 = unbounded.
+ * tg_channel_sink, a callback of type tg_snapshot_cb with user = the channel, copies each
+ * snapshot of tg_optimizer_run into the channel, so the DC loop feeds the AC
+ * consumer thread with no caller code in between (pipeline.cpp:354-366).
+ * pop: blocking waits until a snapshot arrives or the channel is closed and
+ * drained; returns 1 with *out valid until the next pop / destroy on this
+ * channel, 0 when none. */
+typedef struct tg_channel tg_channel;
+tg_channel* tg_channel_create(int64_t capacity);
+void tg_channel_destroy(tg_channel* ch);
+void tg_channel_push(tg_channel* ch, const tg_snapshot_view* snap); /* deep copy */
+void tg_channel_sink(const tg_snapshot_view* snap, void* channel);
+void tg_channel_close(tg_channel* ch);
+int32_t tg_channel_pop(tg_channel* ch, int32_t blocking, tg_snapshot_view* out);
+int64_t tg_channel_pending(tg_channel* ch);
+int64_t tg_channel_dropped(tg_channel* ch);
+
 /* ---- counters and timing for the benchmark contract ---- */
 void* tg_context_stream(tg_context* ctx);   /* the context's cudaStream_t (for caller-side events) */
 /* Enables/disables CUDA-event timing of the fused sweep on evaluate calls and

@@ -5,7 +5,8 @@ libtopopt_b200.so (include/topopt_b200.h); see api.py.
 """
 from .api import (ActionSet, CapacityError, ConfigError, CudaError, DcConfig, DcContext, FlowResult, Genome,
                   GridModel, IoError, IslandedContingency, OptimizerResult, OptimizerStats, ParseError, QdConfig,
-                  RepertoireSnapshot, ScoreArrays, ScoreVector, SingularSystem, SnapshotEntry, TopoptError,
+                  RepertoireSnapshot, ScoreArrays, ScoreVector, SingularSystem, SnapshotChannel, SnapshotEntry,
+                  TopoptError,
                   ValidationError, build_action_set, cell_count, descriptor_to_cell, grid_from_json_text,
                   kIslandedFitness, load_action_set, load_grid, run_optimizer, save_action_set)
 from .api import (QdSession, archive_replay, batch_ranks, context_stream, crossover_lanes,  # noqa: E402,F401

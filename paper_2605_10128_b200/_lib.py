@@ -118,6 +118,14 @@ SIGNATURES = [
     ("tg_batch_ranks", C.c_int, [C.c_void_p, C.c_int32, i32p]),
     ("tg_sweep_rows", C.c_int, [C.c_void_p, i64p, i64p, i64p, i64p]),
     ("tg_fp64_peak", C.c_int, [C.c_int, f64p]),
+    ("tg_channel_create", C.c_void_p, [C.c_int64]),
+    ("tg_channel_destroy", None, [C.c_void_p]),
+    ("tg_channel_push", None, [C.c_void_p, C.POINTER(SnapshotView)]),
+    ("tg_channel_sink", None, [C.POINTER(SnapshotView), C.c_void_p]),
+    ("tg_channel_close", None, [C.c_void_p]),
+    ("tg_channel_pop", C.c_int32, [C.c_void_p, C.c_int32, C.POINTER(SnapshotView)]),
+    ("tg_channel_pending", C.c_int64, [C.c_void_p]),
+    ("tg_channel_dropped", C.c_int64, [C.c_void_p]),
     ("tg_archive_blob_bytes", C.c_int, [C.c_void_p, i64p]),
     ("tg_archive_pack", C.c_int, [C.c_void_p, C.c_void_p]),
     ("tg_archive_merge", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),

@@ -487,9 +487,83 @@ class OptimizerResult:
     stats: OptimizerStats
 
 
+class SnapshotChannel:
+    """SnapshotChannel (channel.hpp:15-79) in native code: single-producer
+    single-consumer queue; a bounded channel never blocks the producer, when
+    full the oldest non-final snapshot is dropped; capacity 0 = unbounded.
+    Passed to run_optimizer(channel=...), the device loop feeds it from C++
+    (tg_channel_sink) while a consumer thread pops (the AC stage,
+    pipeline.cpp:354-425)."""
+
+    def __init__(self, capacity: int = 0, n_a: int = 3):
+        self._h = LIB.tg_channel_create(int(capacity))
+        if not self._h:
+            raise TopoptError("channel allocation failed")
+        self.n_a = n_a
+
+    def push(self, snap: RepertoireSnapshot) -> None:
+        n = len(snap.entries)
+        ns = len(snap.entries[0].genome.action_slots) + len(snap.entries[0].genome.disconnection_slots) if n else 0
+        wk = max([len(e.score.worst_contingencies) for e in snap.entries] + [0])
+        arr = {
+            "cell": np.array([e.cell for e in snap.entries], np.int32),
+            "genome": np.array([e.genome.action_slots + e.genome.disconnection_slots for e in snap.entries],
+                               np.int32).reshape(-1),
+            "fitness": np.array([e.score.fitness for e in snap.entries]),
+            "lambda_o": np.array([e.score.lambda_o for e in snap.entries]),
+            "lambda_c": np.array([e.score.lambda_c for e in snap.entries], np.int32),
+            "lambda_c0": np.array([e.score.lambda_c0 for e in snap.entries], np.int32),
+            "lambda_b": np.array([e.score.lambda_b for e in snap.entries]),
+            "lambda_d": np.array([e.score.lambda_d for e in snap.entries], np.int32),
+            "lambda_s": np.array([e.score.lambda_s for e in snap.entries], np.int32),
+            "lambda_r": np.array([e.score.lambda_r for e in snap.entries], np.int32),
+            "worst_n": np.array([len(e.score.worst_contingencies) for e in snap.entries], np.int32),
+            "worst_idx": np.zeros(n * wk, np.int32), "worst_energy": np.zeros(n * wk),
+        }
+        for i, e in enumerate(snap.entries):
+            for j, (k, v) in enumerate(e.score.worst_contingencies):
+                arr["worst_idx"][i * wk + j] = k
+                arr["worst_energy"][i * wk + j] = v
+        v = L.SnapshotView()
+        v.epoch, v.evaluations, v.best_fitness = snap.epoch, snap.evaluations, snap.best_fitness
+        v.final_snapshot, v.n_entries, v.n_slots, v.worst_k = int(snap.final), n, ns, wk
+        for name, a in arr.items():
+            setattr(v, name, _ptr(a, C.c_double if a.dtype == np.float64 else C.c_int32))
+        LIB.tg_channel_push(self._h, C.byref(v))
+
+    def close(self) -> None:
+        LIB.tg_channel_close(self._h)
+
+    def _pop(self, blocking: bool) -> Optional[RepertoireSnapshot]:
+        v = L.SnapshotView()
+        if not LIB.tg_channel_pop(self._h, int(blocking), C.byref(v)):
+            return None
+        return _snapshot_from_view(v, self.n_a)
+
+    def pop(self) -> Optional[RepertoireSnapshot]:
+        """Blocks until a snapshot arrives or the channel is closed and drained."""
+        return self._pop(True)
+
+    def try_pop(self) -> Optional[RepertoireSnapshot]:
+        return self._pop(False)
+
+    def has_pending(self) -> bool:
+        return LIB.tg_channel_pending(self._h) > 0
+
+    def dropped(self) -> int:
+        return int(LIB.tg_channel_dropped(self._h))
+
+    def __del__(self):
+        if getattr(self, "_h", None):
+            LIB.tg_channel_destroy(self._h)
+            self._h = None
+
+
 def run_optimizer(ctx: DcContext, cfg: QdConfig, sink: Optional[Callable[[RepertoireSnapshot], None]] = None,
-                  stop=None) -> OptimizerResult:
-    """run_optimizer (qd_optimizer.cpp:344-417) on the device-resident loop."""
+                  stop=None, channel: Optional[SnapshotChannel] = None) -> OptimizerResult:
+    """run_optimizer (qd_optimizer.cpp:344-417) on the device-resident loop.
+    Snapshots go to `sink` (Python callable, called on this thread) or, with
+    `channel`, straight into a native SnapshotChannel."""
     ccfg = cfg.to_c()
     errors: List[BaseException] = []
 
@@ -501,14 +575,21 @@ def run_optimizer(ctx: DcContext, cfg: QdConfig, sink: Optional[Callable[[Repert
         except BaseException as exc:  # surfaced after the run
             errors.append(exc)
 
-    cb = L.SNAPSHOT_CB(_cb)
+    if channel is not None:
+        if sink is not None:
+            raise ConfigError("pass either sink or channel")
+        cb = C.cast(LIB.tg_channel_sink, L.SNAPSHOT_CB)
+        user = C.c_void_p(channel._h)
+    else:
+        cb = L.SNAPSHOT_CB(_cb)
+        user = None
     stats = L.OptStats()
     cap = 1 << 16
     tev = np.zeros(cap, np.int64)
     tbest = np.zeros(cap)
     stop_arr = stop if stop is not None else None
     stop_p = _ptr(stop_arr, C.c_int32) if stop_arr is not None else C.POINTER(C.c_int32)()
-    _check(LIB.tg_optimizer_run(ctx._h, C.byref(ccfg), cb, None, stop_p, C.byref(stats), _ptr(tev, C.c_int64),
+    _check(LIB.tg_optimizer_run(ctx._h, C.byref(ccfg), cb, user, stop_p, C.byref(stats), _ptr(tev, C.c_int64),
                                 _ptr(tbest, C.c_double), cap))
     if errors:
         raise errors[0]

@@ -6,6 +6,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <deque>
 #include <memory>
 #include <string>
 #include <vector>
@@ -14,6 +15,7 @@
 #include "cuda/engine.cuh"
 #include "cuda/qd.cuh"
 #include "host/model.hpp"
+#include "host/snapshot.hpp"
 
 namespace {
 
@@ -202,9 +204,17 @@ struct tg_context {
   double lambda_b_pre = 0.0;
   // optimizer state
   std::unique_ptr<tgb::QdState> qd;
-  std::vector<int32_t> snap_cell, snap_genome, snap_lc, snap_lc0, snap_ld, snap_ls, snap_lr, snap_widx, snap_wn;
-  std::vector<double> snap_fit, snap_lo, snap_lb, snap_wval;
-  tg_snapshot_view last_view{};
+  // snapshots (make_snapshot): archive blob packed on the device, copied to
+  // pinned host memory (ring of kSnapSlots for the asynchronous hand-off of
+  // tg_optimizer_run), decoded on the host
+  static constexpr int kSnapSlots = 2;
+  tgb::HostSnapshot snap;
+  size_t snap_bytes = 0;
+  void* snap_dev[kSnapSlots] = {nullptr, nullptr};
+  uint8_t* snap_host[kSnapSlots] = {nullptr, nullptr};
+  cudaEvent_t snap_ev[kSnapSlots] = {nullptr, nullptr};
+  void snap_buffers(size_t bytes);
+  void free_snap_buffers();
   int n_a_cap = 4, n_d_cap = 4;
   // live timing of the fused sweep (bench.py roofline)
   bool time_sweep = false;
@@ -232,6 +242,30 @@ struct tg_context {
   int enqueue_evaluate(int n_a, int n_d, bool full, bool timed = false);
   void time_sweep_done();
 };
+
+void tg_context::snap_buffers(size_t bytes) {
+  if (bytes <= snap_bytes) return;
+  check(cudaStreamSynchronize(stream), "snapshot buffers");
+  free_snap_buffers();
+  for (int i = 0; i < kSnapSlots; ++i) {
+    check(cudaMalloc(&snap_dev[i], bytes), "cudaMalloc");
+    check(cudaMallocHost(reinterpret_cast<void**>(&snap_host[i]), bytes), "cudaMallocHost");
+    check(cudaEventCreateWithFlags(&snap_ev[i], cudaEventDisableTiming), "event");
+  }
+  snap_bytes = bytes;
+}
+
+void tg_context::free_snap_buffers() {
+  for (int i = 0; i < kSnapSlots; ++i) {
+    if (snap_dev[i]) cudaFree(snap_dev[i]);
+    if (snap_host[i]) cudaFreeHost(snap_host[i]);
+    if (snap_ev[i]) cudaEventDestroy(snap_ev[i]);
+    snap_dev[i] = nullptr;
+    snap_host[i] = nullptr;
+    snap_ev[i] = nullptr;
+  }
+  snap_bytes = 0;
+}
 
 void tg_context::ensure_capacity(int n) {
   if (n <= capacity) return;
@@ -745,6 +779,7 @@ void tg_context_destroy(tg_context* ctx) {
     ctx->qd.reset();
   }
   ctx->batch_arena.reset();
+  ctx->free_snap_buffers();
   cudaStream_t s = ctx->stream;
   if (ctx->sw0) cudaEventDestroy(ctx->sw0), cudaEventDestroy(ctx->sw1);
   delete ctx;
@@ -945,88 +980,29 @@ void qd_setup(tg_context* ctx, const tgb::QdParams& p) {
   q->worst_k = ctx->worst_k;
 }
 
-// Host view of the device archive (make_snapshot, qd_optimizer.cpp:331-342).
-void fetch_archive(tg_context* ctx, int epoch, int64_t evaluations, bool fin) {
+// Snapshot of the device archive (make_snapshot, qd_optimizer.cpp:331-342):
+// enqueue the blob pack + D2H into ring slot `slot`, completion recorded on
+// snap_ev[slot]; decode_snapshot turns the pinned blob into ctx->snap.
+void enqueue_snapshot(tg_context* ctx, int slot) {
   const tgb::QdState& q = *ctx->qd;
-  const tgb::Archive& a = q.a;
-  const int cells = q.p.cells, cap = q.p.cap, ns = q.n_slots, wk = std::max(q.worst_k, 1);
-  const size_t slots = static_cast<size_t>(cells) * cap;
-  std::vector<int> cnt(cells), gen(slots * std::max(ns, 1)), lc(slots), lc0(slots), ld(slots), ls(slots), lr(slots),
-      widx(slots * wk), wn(slots);
-  std::vector<double> fit(slots), lo(slots), lb(slots), wval(slots * wk);
-  cudaStream_t s = ctx->stream;
-  auto d2h = [&](void* dst, const void* src, size_t bytes) {
-    check(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, s), "archive D2H");
-  };
-  d2h(cnt.data(), a.count, cells * sizeof(int));
-  d2h(gen.data(), a.genome, gen.size() * sizeof(int));
-  d2h(fit.data(), a.fitness, slots * sizeof(double));
-  d2h(lo.data(), a.lambda_o, slots * sizeof(double));
-  d2h(lc.data(), a.lambda_c, slots * sizeof(int));
-  d2h(lc0.data(), a.lambda_c0, slots * sizeof(int));
-  d2h(lb.data(), a.lambda_b, slots * sizeof(double));
-  d2h(ld.data(), a.lambda_d, slots * sizeof(int));
-  d2h(ls.data(), a.lambda_s, slots * sizeof(int));
-  d2h(lr.data(), a.lambda_r, slots * sizeof(int));
-  d2h(widx.data(), a.worst_idx, widx.size() * sizeof(int));
-  d2h(wval.data(), a.worst_val, wval.size() * sizeof(double));
-  d2h(wn.data(), a.worst_n, slots * sizeof(int));
-  check(cudaStreamSynchronize(s), "archive fetch");
-  ctx->snap_cell.clear();
-  ctx->snap_genome.clear();
-  ctx->snap_fit.clear();
-  ctx->snap_lo.clear();
-  ctx->snap_lc.clear();
-  ctx->snap_lc0.clear();
-  ctx->snap_lb.clear();
-  ctx->snap_ld.clear();
-  ctx->snap_ls.clear();
-  ctx->snap_lr.clear();
-  ctx->snap_widx.clear();
-  ctx->snap_wval.clear();
-  ctx->snap_wn.clear();
-  double best = -INFINITY;
-  for (int c = 0; c < cells; ++c)
-    for (int i = 0; i < cnt[c]; ++i) {
-      const size_t at = static_cast<size_t>(c) * cap + i;
-      ctx->snap_cell.push_back(c);
-      for (int k = 0; k < ns; ++k) ctx->snap_genome.push_back(gen[at * ns + k]);
-      ctx->snap_fit.push_back(fit[at]);
-      ctx->snap_lo.push_back(lo[at]);
-      ctx->snap_lc.push_back(lc[at]);
-      ctx->snap_lc0.push_back(lc0[at]);
-      ctx->snap_lb.push_back(lb[at]);
-      ctx->snap_ld.push_back(ld[at]);
-      ctx->snap_ls.push_back(ls[at]);
-      ctx->snap_lr.push_back(lr[at]);
-      ctx->snap_wn.push_back(wn[at]);
-      for (int k = 0; k < wk; ++k) {
-        ctx->snap_widx.push_back(widx[at * wk + k]);
-        ctx->snap_wval.push_back(wval[at * wk + k]);
-      }
-      if (i == 0) best = std::max(best, fit[at]);
-    }
-  tg_snapshot_view& v = ctx->last_view;
-  v.epoch = epoch;
-  v.evaluations = evaluations;
-  v.best_fitness = best;
-  v.final_snapshot = fin ? 1 : 0;
-  v.n_entries = static_cast<int32_t>(ctx->snap_cell.size());
-  v.n_slots = ns;
-  v.cell = ctx->snap_cell.data();
-  v.genome = ctx->snap_genome.data();
-  v.fitness = ctx->snap_fit.data();
-  v.lambda_o = ctx->snap_lo.data();
-  v.lambda_c = ctx->snap_lc.data();
-  v.lambda_c0 = ctx->snap_lc0.data();
-  v.lambda_b = ctx->snap_lb.data();
-  v.lambda_d = ctx->snap_ld.data();
-  v.lambda_s = ctx->snap_ls.data();
-  v.lambda_r = ctx->snap_lr.data();
-  v.worst_idx = ctx->snap_widx.data();
-  v.worst_energy = ctx->snap_wval.data();
-  v.worst_n = ctx->snap_wn.data();
-  v.worst_k = wk;
+  ctx->snap_buffers(tgb::BlobLayout(q.p.cells * q.p.cap, q.n_slots, q.worst_k).total);
+  tgb::launch_archive_pack(q, ctx->snap_dev[slot], ctx->stream);
+  ctx->launches += 1;
+  check(cudaMemcpyAsync(ctx->snap_host[slot], ctx->snap_dev[slot], ctx->snap_bytes, cudaMemcpyDeviceToHost,
+                        ctx->stream), "snapshot D2H");
+  check(cudaEventRecord(ctx->snap_ev[slot], ctx->stream), "snapshot event");
+}
+
+void decode_snapshot(tg_context* ctx, int slot, int epoch, int64_t evaluations, bool fin) {
+  const tgb::QdState& q = *ctx->qd;
+  ctx->snap.from_blob(ctx->snap_host[slot], q.p.cells, q.p.cap, q.n_slots, q.worst_k, epoch, evaluations, fin);
+}
+
+// Synchronous snapshot (tg_qd_fetch, tg_archive_replay, run end).
+void fetch_archive(tg_context* ctx, int epoch, int64_t evaluations, bool fin) {
+  enqueue_snapshot(ctx, 0);
+  check(cudaEventSynchronize(ctx->snap_ev[0]), "snapshot");
+  decode_snapshot(ctx, 0, epoch, evaluations, fin);
 }
 
 // One MapElites iteration: offspring -> DC N-1 evaluation -> archive insert.
@@ -1102,7 +1078,7 @@ tg_status tg_qd_fetch(tg_context* ctx, int32_t final_snapshot, tg_snapshot_view*
   return guarded([&] {
     if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
     fetch_archive(ctx, ctx->qd_epoch, ctx->qd_evaluations, final_snapshot != 0);
-    if (out) *out = ctx->last_view;
+    if (out) *out = ctx->snap.view;
   });
 }
 
@@ -1199,6 +1175,41 @@ tg_status tg_archive_merge(tg_context* ctx, const void* d_blobs, int32_t n_islan
   });
 }
 
+struct tg_channel {
+  explicit tg_channel(size_t capacity) : q(capacity) {}
+  tgb::SnapshotChannel q;
+  std::unique_ptr<tgb::HostSnapshot> popped;  // backs the view returned by the last pop
+};
+
+tg_channel* tg_channel_create(int64_t capacity) {
+  try {
+    return new tg_channel(static_cast<size_t>(capacity > 0 ? capacity : 0));
+  } catch (...) {
+    return nullptr;
+  }
+}
+void tg_channel_destroy(tg_channel* ch) { delete ch; }
+void tg_channel_push(tg_channel* ch, const tg_snapshot_view* v) {
+  if (!ch || !v) return;
+  auto s = std::make_unique<tgb::HostSnapshot>();
+  s->from_view(*v);
+  ch->q.push(std::move(s));
+}
+void tg_channel_sink(const tg_snapshot_view* v, void* channel) { tg_channel_push(static_cast<tg_channel*>(channel), v); }
+void tg_channel_close(tg_channel* ch) {
+  if (ch) ch->q.close();
+}
+int32_t tg_channel_pop(tg_channel* ch, int32_t blocking, tg_snapshot_view* out) {
+  if (!ch) return 0;
+  auto s = ch->q.pop(blocking != 0);
+  if (!s) return 0;
+  ch->popped = std::move(s);
+  if (out) *out = ch->popped->view;
+  return 1;
+}
+int64_t tg_channel_pending(tg_channel* ch) { return ch ? static_cast<int64_t>(ch->q.pending()) : 0; }
+int64_t tg_channel_dropped(tg_channel* ch) { return ch ? static_cast<int64_t>(ch->q.dropped()) : 0; }
+
 void* tg_context_stream(tg_context* ctx) { return ctx ? static_cast<void*>(ctx->stream) : nullptr; }
 
 tg_status tg_sweep_timing(tg_context* ctx, int32_t enable, double* total_ms, int64_t* launches) {
@@ -1258,6 +1269,47 @@ tg_status tg_optimizer_run(tg_context* ctx, const tg_qd_config* cfg, tg_snapshot
     int n_trace = 0;
     int64_t launched = 0;
     bool emitted_final = false;
+    // Snapshot hand-off: each epoch's archive is packed
+    // and copied to pinned memory asynchronously; the sink runs on this thread
+    // once the copy has landed, while the device already works on the next
+    // epoch (same content and order as make_snapshot after each epoch,
+    // qd_optimizer.cpp:403-410).
+    struct Pending {
+      int slot, epoch;
+      int64_t evaluations;
+      bool fin;
+    };
+    std::deque<Pending> pending;
+    int next_slot = 0;
+    auto deliver = [&](bool wait_all) {
+      while (!pending.empty()) {
+        const Pending p = pending.front();
+        if (!wait_all) {
+          const cudaError_t r = cudaEventQuery(ctx->snap_ev[p.slot]);
+          if (r == cudaErrorNotReady) return;
+          check(r, "snapshot");
+        } else {
+          check(cudaEventSynchronize(ctx->snap_ev[p.slot]), "snapshot");
+        }
+        decode_snapshot(ctx, p.slot, p.epoch, p.evaluations, p.fin);
+        pending.pop_front();
+        if (trace_ev && trace_best && n_trace < trace_cap) {
+          trace_ev[n_trace] = p.evaluations;
+          trace_best[n_trace] = ctx->snap.view.best_fitness;
+        }
+        ++n_trace;
+        if (cb) cb(&ctx->snap.view, user);
+      }
+    };
+    auto snapshot = [&](bool fin) {
+      if (static_cast<int>(pending.size()) == tg_context::kSnapSlots) {  // ring full: the oldest goes first
+        check(cudaEventSynchronize(ctx->snap_ev[pending.front().slot]), "snapshot");
+        deliver(false);
+      }
+      enqueue_snapshot(ctx, next_slot);
+      pending.push_back({next_slot, ctx->qd_epoch, ctx->qd_evaluations, fin});
+      next_slot = (next_slot + 1) % tg_context::kSnapSlots;
+    };
     while (!exhausted()) {
       for (int it = 0; it < cfg->iters_per_epoch && !exhausted(); ++it) {
         if (launched >= kInFlight) check(cudaEventSynchronize(ev[launched % kInFlight]), "throttle");
@@ -1266,25 +1318,18 @@ tg_status tg_optimizer_run(tg_context* ctx, const tg_qd_config* cfg, tg_snapshot
         ++launched;
         ctx->launches += q.kernels_per_iter;
         ctx->qd_evaluations += q.p.batch;
+        deliver(false);
       }
       ++ctx->qd_epoch;
       const bool fin = exhausted();
-      fetch_archive(ctx, ctx->qd_epoch, ctx->qd_evaluations, fin);
-      if (trace_ev && trace_best && n_trace < trace_cap) {
-        trace_ev[n_trace] = ctx->qd_evaluations;
-        trace_best[n_trace] = ctx->last_view.best_fitness;
-      }
-      ++n_trace;
-      if (cb) cb(&ctx->last_view, user);
+      snapshot(fin);
       if (fin) {
         emitted_final = true;
         break;
       }
     }
-    if (!emitted_final) {
-      fetch_archive(ctx, ctx->qd_epoch, ctx->qd_evaluations, true);
-      if (cb) cb(&ctx->last_view, user);
-    }
+    if (!emitted_final) snapshot(true);
+    deliver(true);
     for (auto& e : ev) cudaEventDestroy(e);
     // capacity errors raised inside the loop surface here
     std::vector<int> err(q.p.batch);
@@ -1302,7 +1347,7 @@ tg_status tg_optimizer_run(tg_context* ctx, const tg_qd_config* cfg, tg_snapshot
 tg_status tg_archive_export(tg_context* ctx, tg_snapshot_view* out) {
   return guarded([&] {
     if (!ctx->qd) throw tgb::ConfigError("no archive: run the optimizer or a replay first");
-    *out = ctx->last_view;
+    *out = ctx->snap.view;
   });
 }
 

@@ -297,3 +297,41 @@ def test_philox_mode_valid_and_distributed_like_replay(data_dir):
     assert phi.repertoire.best_fitness >= rep.repertoire.best_fitness - 0.05 * abs(rep.repertoire.best_fitness)
     with pytest.raises(P.ConfigError):
         P.QdConfig(rng="xorshift").to_c()
+
+
+def test_optimizer_feeds_native_channel_asynchronously(data_dir):
+    """Snapshot -> AC hand-off: epoch snapshots are
+    packed on the device and copied asynchronously; fed into a native
+    SnapshotChannel while a consumer thread pops them, they equal the
+    synchronous sink's snapshots (make_snapshot order, last one final)."""
+    import threading
+
+    text = open(os.path.join(data_dir, "grid14_congested.json")).read()
+    ctx, _ = _ctx(text)
+    kw = dict(seed=9, batch_size=64, iters_per_epoch=5, max_evaluations=1 + 64 * 42)
+    via_sink = []
+    P.run_optimizer(ctx, P.QdConfig(**kw), sink=via_sink.append)
+    ch = P.SnapshotChannel(0)
+    got = []
+
+    def consumer():
+        while (s := ch.pop()) is not None:
+            got.append(s)
+
+    t = threading.Thread(target=consumer)
+    t.start()
+    res = P.run_optimizer(ctx, P.QdConfig(**kw), channel=ch)
+    ch.close()
+    t.join(timeout=60)
+    assert len(got) == len(via_sink) == res.stats.epochs and got[-1].final
+    for a, b in zip(got, via_sink):
+        assert (a.epoch, a.evaluations, a.best_fitness, a.final) == (b.epoch, b.evaluations, b.best_fitness, b.final)
+        assert [(e.cell, e.genome.action_slots + e.genome.disconnection_slots, e.score.fitness,
+                 e.score.worst_contingencies) for e in a.entries] == \
+            [(e.cell, e.genome.action_slots + e.genome.disconnection_slots, e.score.fitness,
+              e.score.worst_contingencies) for e in b.entries]
+    # bounded channel: the producer never blocks, the final snapshot survives
+    ch2 = P.SnapshotChannel(1)
+    P.run_optimizer(ctx, P.QdConfig(**kw), channel=ch2)
+    last = ch2.try_pop()
+    assert last is not None and last.final and ch2.dropped() == res.stats.epochs - 1
