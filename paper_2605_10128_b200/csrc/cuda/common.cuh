@@ -10,8 +10,8 @@ namespace tgb {
 // (qd_optimizer.hpp:16-17); these bound the per-candidate low-rank update.
 constexpr int kMaxSlots = 8;       // n_a + n_d
 constexpr int kMaxSplits = 4;      // n_a
-constexpr int kSweepRank = 7;      // rank r handled by the fused sweep (stride 8 with f_c / alpha)
-constexpr int kStride = 8;         // doubles per branch row (f_c, L[0..6]) and per contingency row
+constexpr int kSweepRank = 11;     // largest update rank r (n_a = n_d = 4 plus grounded dead nodes)
+constexpr int kStride = 12;        // max doubles per branch row (f_c, L[0..10]) and per contingency row
 constexpr int kMaxMoved = 128;     // moved branch ends per candidate
 constexpr int kMaxRemoved = 24;    // removed branches (genome + outage case)
 constexpr int kMaxGround = 8;      // dead base nodes grounded

@@ -107,7 +107,7 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
 // Rank buckets -> sweep groups; assigns every swept candidate its row slot.
 void launch_bucket(Batch& b, cudaStream_t stream, int* launched);
 // Upper bound on sweep groups for n candidates (every rank bucket rounds up).
-inline int max_sweep_groups(int n) { return (n + 7) / 8 + kSweepRank + 1; }
+inline int max_sweep_groups(int n) { return (n + kGroupSlots - 1) / kGroupSlots + kSweepRank + 1; }
 
 // Base factorization on the device (dc_engine.cpp:88-116, importer.cpp:358-401):
 // X = B_red^-1 by in-place Gauss-Jordan (B_red is SPD; no pivoting needed).

@@ -386,10 +386,25 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   }
 }
 
-// CTA order: super-blocks of `gblock` candidate groups x all tiles, tile-major
-// inside a super-block, so the CTAs resident at one time share each T_base
-// tile across gblock groups while the super-block's candidate rows stay in L2
-// across its tiles.
+// Common-rank kernel (ranks 0..kFastRank). CTA order: super-blocks of
+// `gblock` candidate groups x all tiles, tile-major inside a super-block, so
+// the CTAs resident at one time share each T_base tile across gblock groups
+// while the super-block's candidate rows stay in L2 across its tiles.
+constexpr int kFastRank = 7;
+
+// CTA setup for (group, rank r): the candidate list and fresh stage barriers.
+__device__ __forceinline__ void cta_setup(const Batch& b, int group, int r, CtaWork& w, uint64_t* bars) {
+  const int per = cand_per_cta(r);
+  const int first = (group - b.wl_group0[r]) * per;
+  int n = 0;
+  for (int j = 0; j < per; ++j)
+    if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
+  w.ncand = n;
+  w.group = group;
+  for (int s = 0; s < kMaxStages; ++s) mbar_init(bars + s, 1), mbar_init(bars + kMaxStages + s, kWarps);
+  asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+}
+
 template <bool FULL>
 __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
@@ -403,20 +418,12 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
   const int sb = static_cast<int>(blockIdx.x) / per_sb, rr = static_cast<int>(blockIdx.x) % per_sb;
   const int g0 = sb * gblock, gg = min(gblock, ngroups - g0);
   const int tile = rr / gg, group = g0 + rr % gg;
-  if (group >= b.wl_group0[kSweepRank + 1]) return;
+  if (group >= b.wl_group0[kFastRank + 1]) return;  // higher ranks: k_sweep_hi
   if (threadIdx.x == 0) {
     int r = 0;
-    while (r < kSweepRank && group >= b.wl_group0[r + 1]) ++r;
+    while (r < kFastRank && group >= b.wl_group0[r + 1]) ++r;
     r_s = r;
-    const int per = cand_per_cta(r);
-    const int first = (group - b.wl_group0[r]) * per;
-    int n = 0;
-    for (int j = 0; j < per; ++j)
-      if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
-    w.ncand = n;
-    w.group = group;
-    for (int s = 0; s < kMaxStages; ++s) mbar_init(bars + s, 1), mbar_init(bars + kMaxStages + s, kWarps);
-    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    cta_setup(b, group, r, w, bars);
   }
   __syncthreads();
   switch (r_s) {
@@ -430,6 +437,41 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
     default: sweep_cta<7, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
   }
 }
+
+// Ranks kFastRank+1 .. kSweepRank (n_a = n_d = 4 genomes with grounded dead
+// nodes; rare): a persistent kernel over their (tile, group) items, so its
+// register allocation stays out of the common kernel and an empty bucket
+// costs one short launch.
+template <bool FULL>
+__global__ void __launch_bounds__(kThreads, 1) k_sweep_hi(DevGrid g, Batch b, int ntiles) {
+  extern __shared__ __align__(128) unsigned char smem_raw[];
+  __shared__ CtaWork w;
+  __shared__ int r_s;
+  __shared__ __align__(16) double rmax_s[kWarps * kStride];
+  __shared__ __align__(16) double amax_s[kWarps * kTmaxSub];
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
+  double* smem = reinterpret_cast<double*>(smem_raw + 128);
+  const int gbeg = b.wl_group0[kFastRank + 1], gend = b.wl_group0[kSweepRank + 1];
+  const long items = static_cast<long>(gend - gbeg) * ntiles;
+  for (long it = blockIdx.x; it < items; it += gridDim.x) {
+    const int group = gbeg + static_cast<int>(it / ntiles), tile = static_cast<int>(it % ntiles);
+    __syncthreads();  // the previous item is done with the barriers and shared state
+    if (threadIdx.x == 0) {
+      int r = kFastRank + 1;
+      while (r < kSweepRank && group >= b.wl_group0[r + 1]) ++r;
+      r_s = r;
+      cta_setup(b, group, r, w, bars);
+    }
+    __syncthreads();
+    switch (r_s) {
+      case 8: sweep_cta<8, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      case 9: sweep_cta<9, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      case 10: sweep_cta<10, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      default: sweep_cta<11, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    }
+  }
+}
+static_assert(kSweepRank == 11 && kFastRank == 7, "k_sweep / k_sweep_hi rank switches");
 
 // Stable per-rank lists of swept candidates; bucket r is cut into CTA groups
 // of cand_per_cta(r), and every swept candidate gets its row slot
@@ -484,6 +526,8 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
   if (!configured) {
     cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    cudaFuncSetAttribute(k_sweep_hi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    cudaFuncSetAttribute(k_sweep_hi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     configured = true;
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
@@ -495,12 +539,16 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
   const int gblock = std::min(ngroups, gblock_env ? gblock_env : kGroupBlock);
   const unsigned grid = static_cast<unsigned>(ntiles) * ngroups;
   if (ev0) cudaEventRecord(ev0, stream);
-  if (full)
+  constexpr int kHiCtas = 148;  // persistent: one CTA per SM
+  if (full) {
     k_sweep<true><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
-  else
+    k_sweep_hi<true><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+  } else {
     k_sweep<false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_hi<false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+  }
   if (ev1) cudaEventRecord(ev1, stream);
-  *launched += 1;
+  *launched += 2;
 }
 
 void launch_bucket(Batch& b, cudaStream_t stream, int* launched) {

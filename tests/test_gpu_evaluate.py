@@ -155,3 +155,21 @@ def test_batch_purity_and_padding(data_dir):
     for i in range(len(g)):
         one = ctx.evaluate_arrays(g[i:i + 1], 3, 2)
         assert one.fitness[0] == a.fitness[i] and one.lambda_o[0] == a.lambda_o[i]
+
+
+def test_high_rank_genomes_four_splits_four_disconnections():
+    """n_a = n_d = 4 genomes reach update ranks 8..11 (k_sweep_hi); parity with
+    the oracle and no capacity error."""
+    import paper_2605_10128_b200 as P
+    from tools.synth_grid import synth_grid
+
+    text = json.dumps(synth_grid(300, n_stations=24, seed=31))
+    ctx, orc = make_pair(text)
+    g = orc.random_genomes(600, 4, 4, seed=77)
+    sc = ctx.evaluate_arrays(g, 4, 4)
+    ranks = P.batch_ranks(ctx, len(g))
+    assert (ranks >= 8).sum() > 10, np.bincount(ranks[ranks >= 0])
+    compare_scores(sc, orc.evaluate(g, 4, 4, flows=True), ctx.config.worst_k, ctx.grid.branch_limit)
+    fast = ctx.evaluate_arrays(g, 4, 4)
+    dense, _ = ctx.evaluate_arrays(g, 4, 4, flows=True)
+    assert np.array_equal(fast.fitness, dense.fitness) and np.array_equal(fast.worst_idx, dense.worst_idx)
