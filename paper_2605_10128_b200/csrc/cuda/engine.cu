@@ -125,8 +125,16 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       uint8_t flag = 2;  // padding
       if (k < g.Ks) {
         const int beta = g.ks_branch[k];
+        // phi, rho of the outaged branch from its branch row (written above,
+        // L = b_beta [phi; rho]) instead of a second pass over Z
+        const double* fr = b.feat + feat_index(slot, b.nchunks, beta, r);
+        const bool on = g.br_on[beta] && !bit_get(rm_bits, beta);
         double phi[kMaxSplits], rho[kMaxCols];
-        const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, beta, phi, rho);
+        if (on) {
+          const double ib = 1.0 / g.br_b[beta];
+          for (int q = 0; q < ns; ++q) phi[q] = fr[1 + q] * ib;
+          for (int m = 0; m < nv; ++m) rho[m] = fr[1 + ns + m] * ib;
+        }
         flag = 0;
         if (on) {
           double rk[kSweepRank];
@@ -155,7 +163,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
             }
             flag = stub ? 0 : 1;
           } else {
-            const double alpha = b.feat[feat_index(slot, b.nchunks, beta, r)] / den;
+            const double alpha = fr[0] / den;
             row[0] = alpha;
             for (int i = 0; i < r; ++i) row[1 + i] = rk[i] * alpha;
           }
