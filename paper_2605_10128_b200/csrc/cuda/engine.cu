@@ -322,17 +322,88 @@ __device__ __forceinline__ bool worst_before(double v, int k, double u, int j) {
 __device__ void warp_worst(const double* en, int K, int wk, double* lv, int* li, int* out_idx, double* out_val,
                            int* out_n, int lane) {
   int npos = 0;
+  unsigned long long maxbits = 0ull;  // positive doubles order like their bit patterns
   for (int k0 = 0; k0 < K; k0 += 32) {
     const int k = k0 + lane;
     const double v = k < K ? en[k] : 0.0;
     const unsigned m = __ballot_sync(0xffffffffu, v > 0.0);
     const int at = npos + __popc(m & ((1u << lane) - 1u));
-    if (v > 0.0 && at < kFinishList) lv[at] = v, li[at] = k;
+    if (v > 0.0) {
+      if (at < kFinishList) lv[at] = v, li[at] = k;
+      maxbits = max(maxbits, static_cast<unsigned long long>(__double_as_longlong(v)));
+    }
     npos += __popc(m);
   }
   __syncwarp();
-  const bool listed = npos <= kFinishList;
-  const int n_scan = listed ? npos : K;
+  bool listed = npos <= kFinishList;
+  int n_scan = listed ? npos : K;
+  if (!listed) {
+    // Too many positive energies for the list: a histogram over (exponent, 3
+    // mantissa bits) below the maximum finds the bucket holding the wk-th
+    // largest; only entries at or above it are collected (3 passes over K
+    // instead of wk).
+    for (int o = 16; o > 0; o >>= 1) maxbits = max(maxbits, __shfl_xor_sync(0xffffffffu, maxbits, o));
+    const long long maxkey = static_cast<long long>(maxbits >> 49);
+    int* hist = li;  // kFinishList >= 256 buckets
+    for (int i = lane; i < 256; i += 32) hist[i] = 0;
+    __syncwarp();
+    for (int k = lane; k < K; k += 32) {
+      const double v = en[k];
+      if (!(v > 0.0)) continue;
+      const long long d = maxkey - static_cast<long long>(static_cast<unsigned long long>(__double_as_longlong(v)) >> 49);
+      atomicAdd(&hist[d < 255 ? d : 255], 1);
+    }
+    __syncwarp();
+    int local = 0;
+#pragma unroll
+    for (int q = 0; q < 8; ++q) local += hist[lane * 8 + q];
+    int incl = local;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+      const int y = __shfl_up_sync(0xffffffffu, incl, o);
+      if (lane >= o) incl += y;
+    }
+    const int excl = incl - local;
+    int jb = 255, cum = npos;  // bucket of the wk-th largest, count at or above it
+    if (excl < wk && incl >= wk) {
+      int run = excl;
+      for (int q = 0; q < 8; ++q) {
+        run += hist[lane * 8 + q];
+        if (run >= wk) {
+          jb = lane * 8 + q;
+          cum = run;
+          break;
+        }
+      }
+    }
+    const unsigned who = __ballot_sync(0xffffffffu, excl < wk && incl >= wk);
+    if (who) {
+      const int src = __ffs(who) - 1;
+      jb = __shfl_sync(0xffffffffu, jb, src);
+      cum = __shfl_sync(0xffffffffu, cum, src);
+    }
+    __syncwarp();
+    if (cum <= kFinishList) {
+      int n = 0;
+      for (int k0 = 0; k0 < K; k0 += 32) {
+        const int k = k0 + lane;
+        const double v = k < K ? en[k] : 0.0;
+        bool take = false;
+        if (v > 0.0) {
+          const long long d =
+              maxkey - static_cast<long long>(static_cast<unsigned long long>(__double_as_longlong(v)) >> 49);
+          take = (d < 255 ? d : 255) <= jb;
+        }
+        const unsigned m = __ballot_sync(0xffffffffu, take);
+        const int at = n + __popc(m & ((1u << lane) - 1u));
+        if (take) lv[at] = v, li[at] = k;
+        n += __popc(m);
+      }
+      __syncwarp();
+      listed = true;
+      n_scan = n;
+    }
+  }
   double pv = CUDART_INF;
   int pi = -1, nsel = 0;
   for (int round = 0; round < wk; ++round) {

@@ -173,3 +173,21 @@ def test_high_rank_genomes_four_splits_four_disconnections():
     fast = ctx.evaluate_arrays(g, 4, 4)
     dense, _ = ctx.evaluate_arrays(g, 4, 4, flows=True)
     assert np.array_equal(fast.fitness, dense.fitness) and np.array_equal(fast.worst_idx, dense.worst_idx)
+
+
+def test_worst_list_with_many_overloaded_contingencies():
+    """Every contingency overloads something (limits x 0.3): more positive
+    outage energies than k_finish's shared list holds, so the worst-k
+    selection takes its histogram path (dc_engine.cpp:400-420 order: energy
+    desc, index asc)."""
+    from tools.synth_grid import synth_grid
+
+    doc = synth_grid(400, n_stations=10, seed=41)
+    for br in doc["branches"]:
+        br["limit_mw"] *= 0.3
+    for wk in (20, 3):
+        ctx, orc = make_pair(json.dumps(doc), worst_k=wk)
+        g = orc.random_genomes(120, seed=6)
+        ref = orc.evaluate(g, 3, 2, flows=True)
+        assert ((ref["energy"] > 0).sum(1) > 256).sum() > 50
+        compare_scores(ctx.evaluate_arrays(g, 3, 2), ref, wk, ctx.grid.branch_limit)
