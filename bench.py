@@ -197,6 +197,10 @@ def main():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rng", default="replay", choices=["replay", "philox"],
                     help="lane RNG: the reference's mt19937_64 stream (default) or counter-based Philox4x32-10")
+    ap.add_argument("--mode", default="islands", choices=["islands", "shard"],
+                    help="N>1: islands (one population per GPU, archive merge; weak scaling) or shard (one "
+                         "population, each GPU evaluates a slice of every generation; strong scaling, archive "
+                         "bit-identical to one GPU)")
     ap.add_argument("--merge-every", type=int, default=1,
                     help="island archive merge (NCCL allgather + device merge) every M generations when N>1; 0 = never")
     args = ap.parse_args()
@@ -223,7 +227,9 @@ def main():
     ctx = P.DcContext(grid, actions, P.DcConfig(), device=dev)  # DcContext ctor: X, T_base, skip records on device
     setup_s = time.perf_counter() - t_setup
     info = ctx.info()
-    cfg = P.QdConfig(batch_size=B, iters_per_epoch=1 << 30, seed=1 + rank, rng=args.rng)  # one island per rank
+    # islands: one population per rank (seed 1 + rank); shard: one population (seed 1)
+    cfg = P.QdConfig(batch_size=B, iters_per_epoch=1 << 30, seed=1 + (rank if args.mode == "islands" else 0),
+                     rng=args.rng)
     sess = P.QdSession(ctx, cfg)
     stream = torch.cuda.ExternalStream(P.context_stream(ctx), device=dev)
 
@@ -233,11 +239,18 @@ def main():
             dist.barrier()
 
     ex = None
-    if world > 1 and args.merge_every > 0:
+    shard = None
+    if world > 1 and args.mode == "shard":
+        from paper_2605_10128_b200.islands import BatchShard
+        shard = BatchShard(sess)
+    elif world > 1 and args.merge_every > 0:
         from paper_2605_10128_b200.islands import IslandExchange
         ex = IslandExchange(sess)
 
     def generations(n):
+        if shard is not None:
+            shard.step(n)
+            return
         # n generations of this island; every merge_every-th one ends with the
         # island exchange (pack -> NCCL allgather -> device merge, on the engine stream)
         if ex is None:
@@ -269,7 +282,7 @@ def main():
     ms = e0.elapsed_time(e1)
     launches = ctx.kernel_launches() - launches0
     ms = max_over_ranks(ms, world, dev)
-    total = B * args.steps * world
+    total = B * args.steps * (world if shard is None else 1)  # shard: the ranks share one batch
     value = total / (ms / 1000.0)
     snap = sess.fetch()
 
@@ -357,13 +370,17 @@ def main():
         line = {
             "metric": "N-1-evaluated topologies/sec (DC)", "value": value, "unit": "topologies/s",
             "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms / args.steps,
-            "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+            "higher_is_better": True, "scaling": "strong" if shard is not None else "weak", "vs_baseline": None,
+            "dtype": "f64",
             "data": "synthetic grid (seeded generator tools/synth_grid.py, reference JSON); genomes from the "
                     "device MapElites loop",
             "config": {"workload": CONFIGS[args.config]["workload"], "batch_per_gpu": B,
                        "n_nodes": info["n_nodes"], "n_branches": E, "n_contingencies": info["n_contingencies"],
                        "n_actions": info["n_actions"], "n_disconnectables": info["n_disconnectables"],
-                       "parallelism": (f"islands x{world} (seed 1+rank), archives merged every {args.merge_every} "
+                       "parallelism": (f"batch shard x{world}: one population, each rank evaluates {B // world} "
+                                       "lanes per generation, NCCL allgather of score slices, every rank inserts "
+                                       "all lanes (archive identical to one GPU)" if shard is not None else
+                                       f"islands x{world} (seed 1+rank), archives merged every {args.merge_every} "
                                        "generation(s): NCCL allgather of archive blobs + device Repertoire merge"
                                        if ex is not None else f"islands x{world} (seed 1+rank)"),
                        "l2": f"per-step candidate working set {work_bytes / 2**20:.0f} MiB > 126 MiB L2 "

@@ -251,6 +251,20 @@ tg_status tg_archive_replay(tg_context* ctx, const tg_qd_config* cfg, const int3
 tg_status tg_archive_blob_bytes(tg_context* ctx, int64_t* bytes);
 tg_status tg_archive_pack(tg_context* ctx, void* d_blob);
 tg_status tg_archive_merge(tg_context* ctx, const void* d_blobs, int32_t n_islands);
+/* ---- batch-sharded generation (SURVEY.md 8(e) parity mode): one
+ * run_optimizer iteration (qd_optimizer.cpp:376-401) split so that G ranks
+ * share one population: every rank runs generation_begin (the same offspring
+ * on every rank: lane seeds depend only on (seed, iteration, lane)), evaluates
+ * its lane slice, packs it (device blob, scores_blob_bytes(hi - lo)), the
+ * slices are allgathered and unpacked, and generation_end inserts all lanes in
+ * lane order and advances the iteration: the archive is bit-identical to a
+ * one-GPU run. All calls are enqueued on tg_context_stream(ctx). */
+tg_status tg_qd_generation_begin(tg_context* ctx);
+tg_status tg_qd_evaluate_lanes(tg_context* ctx, int32_t lo, int32_t hi);
+tg_status tg_qd_scores_blob_bytes(tg_context* ctx, int32_t n, int64_t* bytes);
+tg_status tg_qd_scores_pack(tg_context* ctx, int32_t lo, int32_t hi, void* d_blob);
+tg_status tg_qd_scores_unpack(tg_context* ctx, int32_t lo, int32_t hi, const void* d_blob);
+tg_status tg_qd_generation_end(tg_context* ctx);
 /* descriptor_to_cell, qd_optimizer.cpp:12-17 */
 int32_t tg_descriptor_to_cell(int32_t lambda_d, int32_t lambda_s, int32_t lambda_r, const tg_qd_config* cfg);
 /* Device mutation / crossover of single lanes with the reference RNG stream

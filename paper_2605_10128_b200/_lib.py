@@ -126,6 +126,12 @@ SIGNATURES = [
     ("tg_channel_pop", C.c_int32, [C.c_void_p, C.c_int32, C.POINTER(SnapshotView)]),
     ("tg_channel_pending", C.c_int64, [C.c_void_p]),
     ("tg_channel_dropped", C.c_int64, [C.c_void_p]),
+    ("tg_qd_generation_begin", C.c_int, [C.c_void_p]),
+    ("tg_qd_evaluate_lanes", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    ("tg_qd_scores_blob_bytes", C.c_int, [C.c_void_p, C.c_int32, i64p]),
+    ("tg_qd_scores_pack", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    ("tg_qd_scores_unpack", C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_void_p]),
+    ("tg_qd_generation_end", C.c_int, [C.c_void_p]),
     ("tg_archive_blob_bytes", C.c_int, [C.c_void_p, i64p]),
     ("tg_archive_pack", C.c_int, [C.c_void_p, C.c_void_p]),
     ("tg_archive_merge", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),

@@ -668,6 +668,27 @@ class QdSession:
         _check(LIB.tg_qd_fetch(self.ctx._h, int(final), C.byref(view)))
         return _snapshot_from_view(view, self.cfg.n_a)
 
+    # ---- batch-sharded generation (islands.py: BatchShard drives these)
+    def generation_begin(self) -> None:
+        _check(LIB.tg_qd_generation_begin(self.ctx._h))
+
+    def evaluate_lanes(self, lo: int, hi: int) -> None:
+        _check(LIB.tg_qd_evaluate_lanes(self.ctx._h, lo, hi))
+
+    def scores_blob_bytes(self, n: int) -> int:
+        v = C.c_int64()
+        _check(LIB.tg_qd_scores_blob_bytes(self.ctx._h, n, C.byref(v)))
+        return v.value
+
+    def scores_pack(self, lo: int, hi: int, d_blob: int) -> None:
+        _check(LIB.tg_qd_scores_pack(self.ctx._h, lo, hi, C.c_void_p(d_blob)))
+
+    def scores_unpack(self, lo: int, hi: int, d_blob: int) -> None:
+        _check(LIB.tg_qd_scores_unpack(self.ctx._h, lo, hi, C.c_void_p(d_blob)))
+
+    def generation_end(self) -> None:
+        _check(LIB.tg_qd_generation_end(self.ctx._h))
+
     # ---- island exchange (islands.py drives these over torch.distributed)
     def blob_bytes(self) -> int:
         v = C.c_int64()

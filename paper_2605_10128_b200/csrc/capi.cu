@@ -239,7 +239,10 @@ struct tg_context {
   // Enqueues the evaluation of batch.n candidates (all timesteps); returns
   // kernels launched. timed: every sweep launch bracketed by sw0 / sw1 and
   // accumulated into sweep_ms (synchronizes).
-  int enqueue_evaluate(int n_a, int n_d, bool full, bool timed = false);
+  int enqueue_evaluate(int n_a, int n_d, bool full, bool timed = false) {
+    return enqueue_evaluate(batch, n_a, n_d, full, timed);
+  }
+  int enqueue_evaluate(tgb::Batch& bv, int n_a, int n_d, bool full, bool timed);
   void time_sweep_done();
 };
 
@@ -357,14 +360,14 @@ void tg_context::time_sweep_done() {
   ++sweep_launches;
 }
 
-int tg_context::enqueue_evaluate(int n_a, int n_d, bool full, bool timed) {
+int tg_context::enqueue_evaluate(tgb::Batch& bv, int n_a, int n_d, bool full, bool timed) {
   int kernels = 0;
   if (timed && !sw0) {
     check(cudaEventCreate(&sw0), "event");
     check(cudaEventCreate(&sw1), "event");
   }
   if (n_t == 1) {
-    tgb::launch_evaluate(g, batch, n_a, n_d, full, scratch, stream, &kernels, timed ? sw0 : nullptr,
+    tgb::launch_evaluate(g, bv, n_a, n_d, full, scratch, stream, &kernels, timed ? sw0 : nullptr,
                          timed ? sw1 : nullptr);
     if (timed) time_sweep_done();
     return kernels;
@@ -373,7 +376,7 @@ int tg_context::enqueue_evaluate(int n_a, int n_d, bool full, bool timed) {
   // buffers, accumulated into batch.out / batch.energy, then the fitness and
   // worst list of the sums (engine.cu, k_accum_t / k_finish_agg)
   if (full) throw tgb::ConfigError("FlowResult outputs are per timestep; request them on a single-timestep grid");
-  tgb::Batch bt = batch;
+  tgb::Batch bt = bv;
   bt.out = tscores;
   bt.energy = tenergy;
   for (int t = 0; t < n_t; ++t) {
@@ -381,9 +384,9 @@ int tg_context::enqueue_evaluate(int n_a, int n_d, bool full, bool timed) {
     tgb::launch_evaluate(gt[t], bt, n_a, n_d, false, scratch, stream, &k, timed ? sw0 : nullptr,
                          timed ? sw1 : nullptr);
     if (timed) time_sweep_done();
-    kernels += k + tgb::launch_accumulate_timestep(bt, batch.out, batch.energy, g.Kall, t == 0, stream);
+    kernels += k + tgb::launch_accumulate_timestep(bt, bv.out, bv.energy, g.Kall, t == 0, stream);
   }
-  kernels += tgb::launch_finish_aggregate(batch, g.Kall, stream);
+  kernels += tgb::launch_finish_aggregate(bv, g.Kall, stream);
   return kernels;
 }
 
@@ -1071,6 +1074,83 @@ tg_status tg_qd_step(tg_context* ctx, int32_t n_iters) {
     for (int i = 0; i < n_iters; ++i) check(cudaGraphLaunch(ctx->qd->graph, ctx->stream), "graph launch");
     ctx->launches += static_cast<int64_t>(n_iters) * ctx->qd->kernels_per_iter;
     ctx->qd_evaluations += static_cast<int64_t>(n_iters) * ctx->qd->p.batch;
+  });
+}
+
+// ---- batch-sharded generation (SURVEY.md 8(e) parity mode)
+namespace {
+tgb::Scores offset_scores(const tgb::Scores& o, int lo, int wk) {
+  tgb::Scores v = o;
+  v.lambda_o += lo, v.lambda_c += lo, v.lambda_c0 += lo, v.lambda_b += lo, v.lambda_d += lo, v.lambda_s += lo;
+  v.lambda_r += lo, v.fitness += lo, v.islanded += lo, v.error += lo, v.worst_n += lo, v.isl_out += lo;
+  v.isl_bus += lo;
+  v.worst_idx += static_cast<size_t>(lo) * wk;
+  v.worst_val += static_cast<size_t>(lo) * wk;
+  return v;
+}
+void check_lane_range(tg_context* ctx, int lo, int hi) {
+  if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+  if (lo < 0 || hi < lo || hi > ctx->qd->p.batch) throw tgb::ConfigError("lane range outside the batch");
+}
+}  // namespace
+
+tg_status tg_qd_generation_begin(tg_context* ctx) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    tgb::launch_offspring(ctx->g, *ctx->qd, ctx->d_genomes, ctx->stream);
+    ctx->launches += 1;
+    check(cudaGetLastError(), "offspring");
+  });
+}
+
+tg_status tg_qd_evaluate_lanes(tg_context* ctx, int32_t lo, int32_t hi) {
+  return guarded([&] {
+    check_lane_range(ctx, lo, hi);
+    if (hi == lo) return;
+    const tgb::QdState& q = *ctx->qd;
+    tgb::Batch bv = ctx->batch;
+    bv.n = hi - lo;
+    bv.genomes = ctx->d_genomes + static_cast<size_t>(lo) * q.n_slots;
+    bv.params = ctx->params;
+    bv.out = offset_scores(ctx->batch.out, lo, std::max(ctx->worst_k, 1));
+    ctx->launches += ctx->enqueue_evaluate(bv, q.p.n_a, q.p.n_d, false, false);
+    check(cudaGetLastError(), "evaluate lanes");
+  });
+}
+
+tg_status tg_qd_scores_blob_bytes(tg_context* ctx, int32_t n, int64_t* bytes) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    *bytes = static_cast<int64_t>(tgb::BlobLayout(n, ctx->qd->n_slots, ctx->qd->worst_k).total);
+  });
+}
+
+tg_status tg_qd_scores_pack(tg_context* ctx, int32_t lo, int32_t hi, void* d_blob) {
+  return guarded([&] {
+    check_lane_range(ctx, lo, hi);
+    tgb::launch_scores_pack(*ctx->qd, ctx->d_genomes, ctx->batch.out, lo, hi - lo, d_blob, ctx->stream);
+    ctx->launches += 1;
+    check(cudaGetLastError(), "scores pack");
+  });
+}
+
+tg_status tg_qd_scores_unpack(tg_context* ctx, int32_t lo, int32_t hi, const void* d_blob) {
+  return guarded([&] {
+    check_lane_range(ctx, lo, hi);
+    tgb::launch_scores_unpack(*ctx->qd, d_blob, lo, hi - lo, ctx->batch.out, ctx->stream);
+    ctx->launches += 1;
+    check(cudaGetLastError(), "scores unpack");
+  });
+}
+
+tg_status tg_qd_generation_end(tg_context* ctx) {
+  return guarded([&] {
+    if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    tgb::QdState& q = *ctx->qd;
+    ctx->launches += tgb::launch_insert(q, ctx->d_genomes, ctx->batch.out, q.p.batch, ctx->worst_k, true,
+                                        ctx->stream);
+    ctx->qd_evaluations += q.p.batch;
+    check(cudaGetLastError(), "insert");
   });
 }
 

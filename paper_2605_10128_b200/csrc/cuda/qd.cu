@@ -652,6 +652,53 @@ __global__ void k_archive_pack(QdParams p, Archive a, int wk, uint8_t* blob) {
   }
 }
 
+// Batch lanes [lo, lo + n) -> BlobLayout(n) blob (one thread per lane).
+__global__ void k_scores_pack(QdParams p, int wk, const int* genomes, Scores sc, int lo, int n, uint8_t* blob) {
+  const int ns = p.n_a + p.n_d;
+  const BlobLayout L(n, ns, wk);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = lo + i;
+  reinterpret_cast<double*>(blob + L.fit)[i] = sc.fitness[c];
+  reinterpret_cast<double*>(blob + L.lo)[i] = sc.lambda_o[c];
+  reinterpret_cast<double*>(blob + L.lb)[i] = sc.lambda_b[c];
+  reinterpret_cast<int*>(blob + L.lc)[i] = sc.lambda_c[c];
+  reinterpret_cast<int*>(blob + L.lc0)[i] = sc.lambda_c0[c];
+  reinterpret_cast<int*>(blob + L.ld)[i] = sc.lambda_d[c];
+  reinterpret_cast<int*>(blob + L.ls)[i] = sc.lambda_s[c];
+  reinterpret_cast<int*>(blob + L.lr)[i] = sc.lambda_r[c];
+  reinterpret_cast<int*>(blob + L.wn)[i] = sc.worst_n[c];
+  for (int k = 0; k < ns; ++k)
+    reinterpret_cast<int*>(blob + L.gen)[static_cast<size_t>(i) * ns + k] = genomes[static_cast<size_t>(c) * ns + k];
+  for (int k = 0; k < wk; ++k) {
+    reinterpret_cast<int*>(blob + L.widx)[static_cast<size_t>(i) * wk + k] = sc.worst_idx[static_cast<size_t>(c) * wk + k];
+    reinterpret_cast<double*>(blob + L.wval)[static_cast<size_t>(i) * wk + k] =
+        sc.worst_val[static_cast<size_t>(c) * wk + k];
+  }
+}
+
+__global__ void k_scores_unpack(QdParams p, int wk, const uint8_t* blob, int lo, int n, Scores sc) {
+  const int ns = p.n_a + p.n_d;
+  const BlobLayout L(n, ns, wk);
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const int c = lo + i;
+  sc.fitness[c] = reinterpret_cast<const double*>(blob + L.fit)[i];
+  sc.lambda_o[c] = reinterpret_cast<const double*>(blob + L.lo)[i];
+  sc.lambda_b[c] = reinterpret_cast<const double*>(blob + L.lb)[i];
+  sc.lambda_c[c] = reinterpret_cast<const int*>(blob + L.lc)[i];
+  sc.lambda_c0[c] = reinterpret_cast<const int*>(blob + L.lc0)[i];
+  sc.lambda_d[c] = reinterpret_cast<const int*>(blob + L.ld)[i];
+  sc.lambda_s[c] = reinterpret_cast<const int*>(blob + L.ls)[i];
+  sc.lambda_r[c] = reinterpret_cast<const int*>(blob + L.lr)[i];
+  sc.worst_n[c] = reinterpret_cast<const int*>(blob + L.wn)[i];
+  for (int k = 0; k < wk; ++k) {
+    sc.worst_idx[static_cast<size_t>(c) * wk + k] = reinterpret_cast<const int*>(blob + L.widx)[static_cast<size_t>(i) * wk + k];
+    sc.worst_val[static_cast<size_t>(c) * wk + k] =
+        reinterpret_cast<const double*>(blob + L.wval)[static_cast<size_t>(i) * wk + k];
+  }
+}
+
 // Gathered blobs [island][BlobLayout] -> one insert batch, lane = island * S + slot.
 __global__ void k_merge_unpack(QdParams p, int wk, const uint8_t* blobs, int n_islands, int* genomes, Scores sc) {
   const int slots = p.cells * p.cap, ns = p.n_a + p.n_d;
@@ -723,6 +770,17 @@ int launch_archive_merge(const QdState& q, const void* blobs, int n_islands, Mer
       q.p, q.worst_k, static_cast<const uint8_t*>(blobs), n_islands, m.genomes, m.sc);
   k_archive_clear<<<(q.p.cells + 256) / 256, 256, 0, s>>>(q.p, q.a, 0);
   return 2 + insert_lanes(q, m.genomes, m.sc, n, q.worst_k, false, m.lane_cell, m.inserted, s);
+}
+
+void launch_scores_pack(const QdState& q, const int* genomes, const Scores& sc, int lo, int n, void* blob,
+                        cudaStream_t s) {
+  if (n > 0)
+    k_scores_pack<<<(n + 255) / 256, 256, 0, s>>>(q.p, q.worst_k, genomes, sc, lo, n, static_cast<uint8_t*>(blob));
+}
+
+void launch_scores_unpack(const QdState& q, const void* blob, int lo, int n, const Scores& sc, cudaStream_t s) {
+  if (n > 0)
+    k_scores_unpack<<<(n + 255) / 256, 256, 0, s>>>(q.p, q.worst_k, static_cast<const uint8_t*>(blob), lo, n, sc);
 }
 
 void launch_mutate_lanes(const DevGrid& g, const QdState& q, const int* parents, const unsigned long long* seeds, int n,

@@ -108,6 +108,12 @@ int launch_insert(const QdState& q, const int* genomes, const Scores& sc, int n,
 // every island that merges the same gathered blobs holds the same archive.
 void launch_archive_pack(const QdState& q, void* blob, cudaStream_t s);
 int launch_archive_merge(const QdState& q, const void* blobs, int n_islands, MergeBuffers& m, cudaStream_t s);
+// Score slices of a batch (lanes [lo, lo + n)) <-> BlobLayout(n) blobs, for
+// the batch-sharded generation (each rank evaluates a slice, slices are
+// allgathered, every rank inserts the whole batch).
+void launch_scores_pack(const QdState& q, const int* genomes, const Scores& sc, int lo, int n, void* blob,
+                        cudaStream_t s);
+void launch_scores_unpack(const QdState& q, const void* blob, int lo, int n, const Scores& sc, cudaStream_t s);
 void launch_mutate_lanes(const DevGrid& g, const QdState& q, const int* parents, const unsigned long long* seeds, int n,
                          int* children, cudaStream_t s);
 void launch_crossover_lanes(const DevGrid& g, const QdState& q, const int* p1, const int* p2,

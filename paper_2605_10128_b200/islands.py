@@ -168,6 +168,59 @@ class IslandExchange:
         self.exchanges += 1
 
 
+class BatchShard:
+    """Batch-sharded generations (SURVEY.md 8(e) parity mode): the ranks of
+    `group` share ONE population. Every rank draws the same offspring (lane
+    seeds depend only on (seed, iteration, lane), qd_optimizer.cpp:377-383),
+    evaluates its slice of lanes, the score slices are allgathered (NCCL, device
+    blobs) and every rank inserts all lanes in lane order: the archive is
+    bit-identical to a one-GPU run (strong scaling of one generation)."""
+
+    def __init__(self, session, group=None):
+        import torch
+        import torch.distributed as dist
+
+        from . import api
+
+        self.session = session
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        B = session.cfg.batch_size
+        if B % self.world:
+            raise api.ConfigError(f"batch {B} does not split evenly over {self.world} ranks")
+        self.per = B // self.world
+        self.lo, self.hi = self.rank * self.per, (self.rank + 1) * self.per
+        self.nbytes = session.scores_blob_bytes(self.per)
+        self.device_collective = not dist.is_initialized() or dist.get_backend(group) == "nccl"
+        dev = torch.device("cuda", torch.cuda.current_device())
+        self.send = torch.empty(self.nbytes, dtype=torch.uint8, device=dev)
+        self.recv = torch.empty(self.nbytes * self.world, dtype=torch.uint8, device=dev)
+        self.stream = torch.cuda.ExternalStream(api.context_stream(session.ctx), device=dev)
+
+    def step(self, n: int = 1) -> None:
+        import torch
+        import torch.distributed as dist
+
+        s = self.session
+        with torch.cuda.stream(self.stream):
+            for _ in range(n):
+                s.generation_begin()
+                s.evaluate_lanes(self.lo, self.hi)
+                if self.world > 1:
+                    s.scores_pack(self.lo, self.hi, self.send.data_ptr())
+                    if self.device_collective:
+                        dist.all_gather_into_tensor(self.recv, self.send, group=self.group)
+                    else:
+                        gathered = torch.empty(self.world * self.nbytes, dtype=torch.uint8)
+                        dist.all_gather_into_tensor(gathered, self.send.cpu(), group=self.group)
+                        self.recv.copy_(gathered)
+                    for r in range(self.world):
+                        if r != self.rank:
+                            s.scores_unpack(r * self.per, (r + 1) * self.per, self.recv[r * self.nbytes:].data_ptr())
+                s.generation_end()
+
+
 def run_islands(session, generations: int, merge_every: int = 1, exchange: Optional[IslandExchange] = None) -> None:
     """`generations` MapElites generations of this island with an archive
     merge every `merge_every` generations (0 = never)."""

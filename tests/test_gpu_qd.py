@@ -335,3 +335,40 @@ def test_optimizer_feeds_native_channel_asynchronously(data_dir):
     P.run_optimizer(ctx, P.QdConfig(**kw), channel=ch2)
     last = ch2.try_pop()
     assert last is not None and last.final and ch2.dropped() == res.stats.epochs - 1
+
+
+def test_batch_sharded_generations_equal_one_gpu(data_dir):
+    """SURVEY.md 8(e) parity mode: two 'ranks' (own contexts, same seed) draw
+    the same offspring, each evaluates half of the lanes, the score slices are
+    exchanged as device blobs and both insert all lanes: after 6 generations
+    both archives equal the unsharded run's bit for bit."""
+    import torch
+
+    text = open(os.path.join(data_dir, "grid14_congested.json")).read()
+    kw = dict(seed=12, batch_size=64, iters_per_epoch=1 << 30)
+    ref_ctx, _ = _ctx(text)
+    ref = P.QdSession(ref_ctx, P.QdConfig(**kw))
+    ref.step(6)
+    want = [(e.cell, e.genome.action_slots + e.genome.disconnection_slots, e.score.fitness, e.score.lambda_o,
+             e.score.worst_contingencies) for e in ref.fetch().entries]
+    ranks = []
+    for _ in range(2):
+        ctx, _ = _ctx(text)
+        ranks.append(P.QdSession(ctx, P.QdConfig(**kw)))
+    half = 32
+    nb = ranks[0].scores_blob_bytes(half)
+    blobs = [torch.empty(nb, dtype=torch.uint8, device="cuda") for _ in range(2)]
+    for _ in range(6):
+        for r, s in enumerate(ranks):
+            s.generation_begin()
+            s.evaluate_lanes(r * half, (r + 1) * half)
+            s.scores_pack(r * half, (r + 1) * half, blobs[r].data_ptr())
+        torch.cuda.synchronize()
+        for r, s in enumerate(ranks):
+            o = 1 - r
+            s.scores_unpack(o * half, (o + 1) * half, blobs[o].data_ptr())
+            s.generation_end()
+    for s in ranks:
+        got = [(e.cell, e.genome.action_slots + e.genome.disconnection_slots, e.score.fitness, e.score.lambda_o,
+                e.score.worst_contingencies) for e in s.fetch().entries]
+        assert got == want
