@@ -1,6 +1,8 @@
 // Device-side tables and helpers shared by every kernel of the DC N-1 engine.
 #pragma once
 
+#include <atomic>
+
 #include <cstdint>
 #include <cuda_runtime.h>
 
@@ -87,6 +89,15 @@ struct DcParams {
   int variant;
   int n_a, n_d;
 };
+
+// Function attributes (shared-memory limits, carveouts) are per device: true
+// the first time the calling thread's current device asks for `flags`.
+inline bool first_use_on_device(std::atomic<unsigned long long>& flags) {
+  int d = 0;
+  cudaGetDevice(&d);
+  const unsigned long long bit = 1ull << (d & 63);
+  return !(flags.fetch_or(bit) & bit);
+}
 
 __device__ __forceinline__ unsigned long long dbits(double x) { return static_cast<unsigned long long>(__double_as_longlong(x)); }
 

@@ -613,11 +613,9 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
   cudaMemsetAsync(b.energy, 0, static_cast<size_t>(b.n) * g.Kall * sizeof(double), stream);
   cudaMemsetAsync(b.isl_out, 0, b.n * sizeof(int), stream);
   cudaMemsetAsync(b.isl_bus, 0, b.n * sizeof(int), stream);
-  static bool carveout = false;
-  if (!carveout) {  // one wave of warp-sized analysis CTAs needs the full shared-memory carveout
+  static std::atomic<unsigned long long> carveout{0};
+  if (first_use_on_device(carveout))  // one wave of warp-sized analysis CTAs needs the full shared-memory carveout
     cudaFuncSetAttribute(k_analyze, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
-    carveout = true;
-  }
   k_analyze<<<b.n < 65535 ? b.n : 65535, kAnalyzeThreads, bits_bytes, stream>>>(g, b, n_a, n_d);
   ++launched;
   launch_bucket(b, stream, &launched);
@@ -626,11 +624,8 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
   const size_t bits_al = (bits_bytes + 15) & ~size_t{15};
   const size_t zsm_bytes = std::min<size_t>(static_cast<size_t>(g.Nr) * kStride * sizeof(double), kPrepZsmBytes);
   const int zsm_doubles = static_cast<int>(zsm_bytes / sizeof(double));
-  static size_t prep_smem_set = 0;
-  if (bits_al + zsm_bytes > 48 * 1024 && bits_al + zsm_bytes > prep_smem_set) {
+  if (bits_al + zsm_bytes > 48 * 1024)  // (per launch: the size depends on the grid)
     cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bits_al + zsm_bytes));
-    prep_smem_set = bits_al + zsm_bytes;
-  }
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
   k_prep<<<prep_grid, kPrepThreads, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots, zsm_doubles);
   ++launched;

@@ -522,13 +522,12 @@ int sweep_chunk() { return kChunk; }
 
 void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1,
                   int* launched) {
-  static bool configured = false;
-  if (!configured) {
+  static std::atomic<unsigned long long> configured{0};
+  if (first_use_on_device(configured)) {
     cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     cudaFuncSetAttribute(k_sweep_hi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
     cudaFuncSetAttribute(k_sweep_hi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-    configured = true;
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
   static const int gblock_env = [] {

@@ -3,11 +3,13 @@
 
 #include <algorithm>
 #include <array>
+#include <atomic>
 #include <cmath>
 #include <cstdio>
 #include <numeric>
 #include <random>
 #include <set>
+#include <thread>
 
 #include "json_lite.hpp"
 
@@ -206,11 +208,18 @@ void validate(const Grid& g) {
   std::vector<int> all(n);
   std::iota(all.begin(), all.end(), 0);
   if (!connected_with(n, edges, all)) throw ValidationError("grid is disconnected in the base case");
+  // grid_model.cpp:108-121 runs a BFS per contingency; a single-branch outage of
+  // a connected grid disconnects it iff the branch is an in-service bridge, so
+  // one bridge pass answers those (same verdicts, O(E) instead of O(K E)).
+  std::vector<char> is_bridge(edges.size(), 0);
+  for (int e : bridges(n, edges)) is_bridge[e] = 1;
   for (std::size_t c = 0; c < g.cont_id.size(); ++c) {
     if (g.cont_branches[c].empty() && g.cont_injections[c].empty())
       throw ValidationError("contingency '" + g.cont_id[c] + "' removes nothing");
-    if (!connected_with(n, edges, all, g.cont_branches[c]))
-      throw IslandedContingency("contingency '" + g.cont_id[c] + "' disconnects the base-case grid");
+    const auto& brs = g.cont_branches[c];
+    const bool islands = brs.size() == 1 ? (edges[brs[0]].on && is_bridge[brs[0]])
+                                         : !brs.empty() && !connected_with(n, edges, all, brs);
+    if (islands) throw IslandedContingency("contingency '" + g.cont_id[c] + "' disconnects the base-case grid");
   }
   for (const Station& st : g.stations) {
     const std::string where = "substation at node '" + g.node_id[st.node] + "'";
@@ -612,6 +621,7 @@ ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap) {
   ActionTable t;
   t.disconnectables = enumerate_disconnectables(g);
   t.station_range.assign(g.stations.size(), {-1, -1});
+  std::vector<std::pair<int, std::vector<char>>> pending;  // (station, group) in enumeration order
   for (int s = 0; s < static_cast<int>(g.stations.size()); ++s) {
     const Station& st = g.stations[s];
     const int nt = static_cast<int>(st.term_kind.size());
@@ -648,18 +658,38 @@ ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap) {
       std::uniform_int_distribution<std::uint64_t> dist(1, (std::uint64_t{1} << free_bits) - 1);
       for (std::int64_t k = 0; k < cap * 2 && static_cast<std::int64_t>(cands.size()) < cap; ++k) consider(dist(rng));
     }
-    const int begin = t.n_actions();
-    for (const auto& grp : cands) {
-      Realized r;
-      if (!realize(st, grp, r)) continue;
-      if (!split_keeps_connected(g, s, grp)) continue;
-      t.station.push_back(s);
-      t.group.push_back(grp);
-      t.assignment.push_back(std::move(r.assignment));
-      t.open_couplers.push_back(std::move(r.open));
-      t.lambda_r.push_back(r.lambda_r);
-    }
-    if (t.n_actions() > begin) t.station_range[s] = {begin, t.n_actions()};
+    for (auto& grp : cands) pending.push_back({s, std::move(grp)});
+  }
+  // realization + islanding validation of every candidate split are
+  // independent (importer.cpp:288-356): fanned out over the host cores, ids
+  // assigned afterwards in (station, enumeration) order as the reference does
+  std::vector<Realized> real(pending.size());
+  std::vector<char> keep(pending.size(), 0);
+  {
+    std::atomic<std::size_t> next{0};
+    auto work = [&] {
+      for (std::size_t i; (i = next.fetch_add(1)) < pending.size();) {
+        const int s = pending[i].first;
+        keep[i] = realize(g.stations[s], pending[i].second, real[i]) && split_keeps_connected(g, s, pending[i].second);
+      }
+    };
+    const unsigned nth = std::max(1u, std::min<unsigned>(std::thread::hardware_concurrency(),
+                                                         static_cast<unsigned>(pending.size() / 8 + 1)));
+    std::vector<std::thread> pool;
+    for (unsigned k = 1; k < nth; ++k) pool.emplace_back(work);
+    work();
+    for (auto& th : pool) th.join();
+  }
+  for (std::size_t i = 0; i < pending.size(); ++i) {
+    if (!keep[i]) continue;
+    const int s = pending[i].first;
+    if (t.station_range[s].first < 0) t.station_range[s].first = t.n_actions();
+    t.station.push_back(s);
+    t.group.push_back(std::move(pending[i].second));
+    t.assignment.push_back(std::move(real[i].assignment));
+    t.open_couplers.push_back(std::move(real[i].open));
+    t.lambda_r.push_back(real[i].lambda_r);
+    t.station_range[s].second = t.n_actions();
   }
   return t;
 }
