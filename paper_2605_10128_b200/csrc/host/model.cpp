@@ -71,15 +71,26 @@ const std::vector<Value>& opt_array(const Value& o, const char* key) {
   return v->arr;
 }
 
-std::vector<std::vector<std::pair<int, int>>> adjacency(int n, const std::vector<Edge>& edges,
-                                                        const std::vector<char>& cut) {
-  std::vector<std::vector<std::pair<int, int>>> adj(n);
-  for (int e = 0; e < static_cast<int>(edges.size()); ++e) {
-    if (!edges[e].on || (!cut.empty() && cut[e])) continue;
-    adj[edges[e].a].emplace_back(edges[e].b, e);
-    adj[edges[e].b].emplace_back(edges[e].a, e);
-  }
-  return adj;
+// Active edges as CSR (offsets, (neighbour, edge) pairs): two flat arrays
+// instead of one vector per node (the import runs these per candidate split).
+struct Csr {
+  std::vector<int> off;
+  std::vector<std::pair<int, int>> nb;
+  int degree(int v) const { return off[v + 1] - off[v]; }
+};
+
+Csr adjacency(int n, const std::vector<Edge>& edges, const std::vector<char>& cut) {
+  Csr c;
+  c.off.assign(n + 1, 0);
+  auto live = [&](int e) { return edges[e].on && (cut.empty() || !cut[e]); };
+  for (int e = 0; e < static_cast<int>(edges.size()); ++e)
+    if (live(e)) ++c.off[edges[e].a + 1], ++c.off[edges[e].b + 1];
+  for (int v = 0; v < n; ++v) c.off[v + 1] += c.off[v];
+  c.nb.resize(c.off[n]);
+  std::vector<int> fill(c.off.begin(), c.off.end() - 1);
+  for (int e = 0; e < static_cast<int>(edges.size()); ++e)  // edge order per node, as push_back would give
+    if (live(e)) c.nb[fill[edges[e].a]++] = {edges[e].b, e}, c.nb[fill[edges[e].b]++] = {edges[e].a, e};
+  return c;
 }
 
 }  // namespace
@@ -87,48 +98,55 @@ std::vector<std::vector<std::pair<int, int>>> adjacency(int n, const std::vector
 // ---------------------------------------------------------------- graph
 bool connected_with(int n, const std::vector<Edge>& edges, const std::vector<int>& must_reach,
                     const std::vector<int>& cut_list) {
-  std::vector<char> cut(edges.size(), 0);
-  for (int e : cut_list) cut[e] = 1;
-  auto adj = adjacency(n, edges, cut);
+  std::vector<char> cut;
+  if (!cut_list.empty()) {
+    cut.assign(edges.size(), 0);
+    for (int e : cut_list) cut[e] = 1;
+  }
+  const Csr adj = adjacency(n, edges, cut);
   std::vector<char> need(n, 0);
   for (int v : must_reach) need[v] = 1;
   int root = must_reach.empty() ? -1 : must_reach.front();
   for (int v = 0; v < n; ++v)
-    if (!adj[v].empty()) {
+    if (adj.degree(v) > 0) {
       need[v] = 1;
       if (root < 0) root = v;
     }
   if (root < 0) return true;
   std::vector<char> seen(n, 0);
-  std::vector<int> q{root};
+  std::vector<int> q;
+  q.reserve(n);
+  q.push_back(root);
   seen[root] = 1;
   for (std::size_t h = 0; h < q.size(); ++h)
-    for (auto [w, e] : adj[q[h]])
+    for (int p = adj.off[q[h]]; p < adj.off[q[h] + 1]; ++p) {
+      const int w = adj.nb[p].first;
       if (!seen[w]) seen[w] = 1, q.push_back(w);
+    }
   for (int v = 0; v < n; ++v)
     if (need[v] && !seen[v]) return false;
   return true;
 }
 
 std::vector<int> bridges(int n, const std::vector<Edge>& edges) {
-  auto adj = adjacency(n, edges, {});
+  const Csr adj = adjacency(n, edges, {});
   std::vector<int> tin(n, -1), low(n, 0), out;
   // explicit stack of (node, entering edge, next neighbour cursor)
   std::vector<std::array<int, 3>> st;
   int t = 0;
   for (int r = 0; r < n; ++r) {
-    if (tin[r] >= 0 || adj[r].empty()) continue;
+    if (tin[r] >= 0 || adj.degree(r) == 0) continue;
     tin[r] = low[r] = t++;
-    st.push_back({r, -1, 0});
+    st.push_back({r, -1, adj.off[r]});
     while (!st.empty()) {
       auto& top = st.back();
       const int v = top[0];
-      if (top[2] < static_cast<int>(adj[v].size())) {
-        auto [w, e] = adj[v][top[2]++];
+      if (top[2] < adj.off[v + 1]) {
+        auto [w, e] = adj.nb[top[2]++];
         if (e == top[1]) continue;
         if (tin[w] < 0) {
           tin[w] = low[w] = t++;
-          st.push_back({w, e, 0});
+          st.push_back({w, e, adj.off[w]});
         } else {
           low[v] = std::min(low[v], tin[w]);
         }
