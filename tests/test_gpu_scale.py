@@ -79,3 +79,23 @@ def test_tso_scale_fast_sweep_equals_dense():
     fast, _, (computed, offered, _, partial) = _fast_equals_dense(ctx, genomes)
     assert offered > 0 and partial < 0.1 * offered
     assert np.isfinite(fast.fitness).mean() > 0.9
+
+
+def test_special_outages_at_scale():
+    """Multi-branch and injection contingencies plus busbar outages (the
+    k_special path, dc_engine.cpp:303-356, 373-386) on a 300-bus grid, 2048
+    loop candidates: skipping == dense sweep bit for bit, a sample == oracle."""
+    from oracle.oracle import random_grid_json
+
+    text = random_grid_json(77, n_nodes=300, extra_edges=250, n_outages=60, n_stations=10, multi=True,
+                            injection=True, busbar=True)
+    g = P.grid_from_json_text(text)
+    ctx = P.DcContext(g, P.build_action_set(g))
+    genomes = _loop_genomes(ctx, 2048, 4, seed=29)
+    fast, _, _ = _fast_equals_dense(ctx, genomes)
+    orc = OracleContext(text)
+    pick = np.random.default_rng(9).choice(len(genomes), 200, replace=False)
+    ref = orc.evaluate(genomes[pick], 3, 2, flows=True)
+    sc, fr = ctx.evaluate_arrays(genomes[pick], 3, 2, flows=True)
+    compare_scores(sc, ref, ctx.config.worst_k, ctx.grid.branch_limit)
+    compare_flows(fr, ref)
