@@ -227,6 +227,18 @@ struct tg_context {
   std::vector<tgb::DevGrid> gt;
   tgb::Scores tscores{};
   double* tenergy = nullptr;
+  // multi-timestep screening (one mask pass over all profiles, then a masked
+  // sweep per profile): needs the same zero pattern of injections in every
+  // profile (then the topology analysis is shared) and room for every
+  // profile's candidate rows
+  bool mt_ok = false;
+  bool mt_pattern_ok = false;  // injection zero pattern identical across profiles
+  tgb::DevGrid g_mt{};          // t = 0 view with the all-profile skip records
+  double* mt_feat = nullptr;    // [n_t] candidate branch rows
+  double* mt_kdat = nullptr;    // [n_t] contingency rows
+  double* mt_energy = nullptr;  // [n_t][cap][Kall]
+  int* mt_nc0 = nullptr;        // [n_t][cap]
+  size_t mt_feat_sz = 0, mt_kdat_sz = 0;
   // island merge buffers (allocated on the first merge)
   std::unique_ptr<DeviceArena> merge_arena;
   tgb::MergeBuffers merge{};
@@ -243,6 +255,7 @@ struct tg_context {
     return enqueue_evaluate(batch, n_a, n_d, full, timed);
   }
   int enqueue_evaluate(tgb::Batch& bv, int n_a, int n_d, bool full, bool timed);
+  int enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed);
   void time_sweep_done();
 };
 
@@ -280,6 +293,8 @@ void tg_context::ensure_capacity(int n) {
   batch_arena = std::make_unique<DeviceArena>();
   DeviceArena& A = *batch_arena;
   tgb::Batch& b = batch;
+  b = tgb::Batch{};  // every pointer below is reallocated or stays null
+  mt_ok = false;
   const size_t E = g.E, Kp = g.Kpad, Ka = std::max(g.Kall, 1);
   d_genomes = A.alloc<int>(static_cast<size_t>(cap) * tgb::kMaxSlots);
   b.status = A.alloc<int>(cap);
@@ -340,6 +355,33 @@ void tg_context::ensure_capacity(int n) {
     ts.isl_out = A.alloc<int>(cap);
     ts.isl_bus = A.alloc<int>(cap);
     tenergy = A.alloc<double>(static_cast<size_t>(cap) * Ka);
+    // multi-timestep screening buffers, when they fit in half of the free memory
+    const size_t feat_sz = static_cast<size_t>(tgb::max_sweep_groups(cap)) * b.nchunks * tgb::kGroupSlots *
+                           tgb::kChunkRows * tgb::kStride;
+    const size_t kdat_sz = static_cast<size_t>(cap) * std::max<size_t>(Kp, 1) * tgb::kStride;
+    const size_t ntiles = std::max<size_t>(Kp / tgb::sweep_tile_k(), 1);
+    const size_t need = sizeof(double) * (static_cast<size_t>(n_t) * (feat_sz + kdat_sz + static_cast<size_t>(cap) * Ka) +
+                                          feat_sz) +
+                        static_cast<size_t>(n_t) * cap * sizeof(int) +
+                        static_cast<size_t>(cap) * ntiles * (tgb::kTmaxSub + tgb::kStride) * 8 +
+                        static_cast<size_t>(cap) * ntiles * b.nchunks * 4;
+    size_t free_b = 0, total_b = 0;
+    cudaMemGetInfo(&free_b, &total_b);
+    static const bool mt_disabled = std::getenv("TGB_NO_MT_SCREEN") != nullptr;  // A/B switch
+    mt_ok = mt_pattern_ok && !mt_disabled && need < free_b / 2;
+    if (mt_ok) {
+      mt_feat_sz = feat_sz;
+      mt_kdat_sz = kdat_sz;
+      mt_feat = A.alloc<double>(static_cast<size_t>(n_t) * feat_sz);
+      mt_kdat = A.alloc<double>(static_cast<size_t>(n_t) * kdat_sz);
+      mt_energy = A.alloc<double>(static_cast<size_t>(n_t) * cap * Ka);
+      mt_nc0 = A.alloc<int>(static_cast<size_t>(n_t) * cap);
+      b.feat_mt = A.alloc<double>(feat_sz);
+      b.amx_mt = A.alloc<unsigned long long>(static_cast<size_t>(cap) * ntiles * tgb::kTmaxSub);
+      b.rmx_mt = A.alloc<unsigned long long>(static_cast<size_t>(cap) * ntiles * tgb::kStride);
+      b.mask = A.alloc<uint32_t>(static_cast<size_t>(cap) * ntiles * b.nchunks);
+      b.topo_sol = A.alloc<double>(static_cast<size_t>(cap) * tgb::kTopoSol);
+    }
   }
   // Z scratch: bounded so huge grids stay within a fixed budget
   const size_t row_prep = static_cast<size_t>(std::max(g.Nr, 1)) * tgb::kStride * sizeof(double);
@@ -376,6 +418,7 @@ int tg_context::enqueue_evaluate(tgb::Batch& bv, int n_a, int n_d, bool full, bo
   // buffers, accumulated into batch.out / batch.energy, then the fitness and
   // worst list of the sums (engine.cu, k_accum_t / k_finish_agg)
   if (full) throw tgb::ConfigError("FlowResult outputs are per timestep; request them on a single-timestep grid");
+  if (mt_ok) return enqueue_evaluate_mt(bv, n_a, n_d, timed);
   tgb::Batch bt = bv;
   bt.out = tscores;
   bt.energy = tenergy;
@@ -385,6 +428,60 @@ int tg_context::enqueue_evaluate(tgb::Batch& bv, int n_a, int n_d, bool full, bo
                          timed ? sw1 : nullptr);
     if (timed) time_sweep_done();
     kernels += k + tgb::launch_accumulate_timestep(bt, bv.out, bv.energy, g.Kall, t == 0, stream);
+  }
+  kernels += tgb::launch_finish_aggregate(bv, g.Kall, stream);
+  return kernels;
+}
+
+// Multi-timestep screening: analysis once (the topology does not depend on the
+// profile), candidate rows of every profile (k_prep folds bounds over all
+// profiles), one mask pass over all profiles (k_sweep mode 1), then per profile
+// the masked sweep (mode 2), special outages, scores, accumulation.
+int tg_context::enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed) {
+  const int n = bv.n, ntiles = std::max(g.Kpad / tgb::sweep_tile_k(), 1);
+  const size_t Ka = std::max(g.Kall, 1);
+  int kernels = 0;
+  auto view = [&](int t) {
+    tgb::Batch b = bv;
+    b.feat = mt_feat + static_cast<size_t>(t) * mt_feat_sz;
+    b.kdat = mt_kdat + static_cast<size_t>(t) * mt_kdat_sz;
+    b.energy = mt_energy + static_cast<size_t>(t) * n * Ka;
+    b.nc0 = mt_nc0 + static_cast<size_t>(t) * n;
+    b.t_index = t;
+    b.prep_lite = t > 0;  // later profiles reuse the first profile's topology factors and L rows
+    b.feat_ref = mt_feat;
+    return b;
+  };
+  tgb::Batch b0 = view(0);
+  b0.feat_mt = nullptr;  // the analysis does not touch the bounds
+  kernels += tgb::launch_analyze(g, b0, n_a, n_d, stream);
+  check(cudaMemsetAsync(bv.amx_mt, 0, static_cast<size_t>(n) * ntiles * tgb::kTmaxSub * 8, stream), "memset");
+  check(cudaMemsetAsync(bv.rmx_mt, 0, static_cast<size_t>(n) * ntiles * tgb::kStride * 8, stream), "memset");
+  check(cudaMemsetAsync(mt_energy, 0, static_cast<size_t>(n_t) * n * Ka * sizeof(double), stream), "memset");
+  for (int t = 0; t < n_t; ++t) {
+    tgb::Batch bt = view(t);
+    kernels += tgb::launch_prep(gt[t], bt, n_a, n_d, scratch, stream);
+  }
+  tgb::Batch bm = view(0);
+  bm.t_mode = 1;
+  if (g.Ks > 0) tgb::launch_sweep(g_mt, bm, false, stream, timed ? sw0 : nullptr, timed ? sw1 : nullptr, &kernels);
+  if (timed && g.Ks > 0) time_sweep_done();
+  for (int t = 0; t < n_t; ++t) {
+    tgb::Batch bt = view(t);
+    bt.out = tscores;
+    bt.t_mode = 2;
+    bt.feat_mt = nullptr;
+    bt.amx_mt = nullptr;
+    bt.rmx_mt = nullptr;
+    check(cudaMemsetAsync(bt.fmax, 0, static_cast<size_t>(n) * g.E * sizeof(unsigned long long), stream), "memset");
+    check(cudaMemsetAsync(bt.fbus, 0, static_cast<size_t>(n) * g.E * sizeof(unsigned long long), stream), "memset");
+    check(cudaMemsetAsync(bt.isl_out, 0, n * sizeof(int), stream), "memset");
+    check(cudaMemsetAsync(bt.isl_bus, 0, n * sizeof(int), stream), "memset");
+    if (g.Ks > 0)
+      tgb::launch_sweep(gt[t], bt, false, stream, timed ? sw0 : nullptr, timed ? sw1 : nullptr, &kernels);
+    if (timed && g.Ks > 0) time_sweep_done();
+    kernels += tgb::launch_special_finish(gt[t], bt, n_a, n_d, false, scratch, stream);
+    kernels += tgb::launch_accumulate_timestep(bt, bv.out, bv.energy, g.Kall, t == 0, stream);
   }
   kernels += tgb::launch_finish_aggregate(bv, g.Kall, stream);
   return kernels;
@@ -706,6 +803,15 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     g.TK = tk;
     ctx->n_t = T;
     ctx->gt.clear();
+    float* tmax_all = A.alloc<float>(static_cast<size_t>(T) * tmax_n);
+    check(cudaMemsetAsync(tmax_all, 0, static_cast<size_t>(T) * tmax_n * sizeof(float), s), "tmax");
+    ctx->mt_pattern_ok = T > 1;
+    for (int t = 1; t < T && ctx->mt_pattern_ok; ++t)
+      for (int i = 0; i < I; ++i)
+        if ((gd->injection_net_mw_t[static_cast<size_t>(t) * I + i] == 0.0) != (gd->injection_net_mw_t[i] == 0.0)) {
+          ctx->mt_pattern_ok = false;
+          break;
+        }
     for (int t = 0; t < T; ++t) {
       const double* net = T > 1 ? gd->injection_net_mw_t + static_cast<size_t>(t) * I : gd->injection_net_mw;
       std::vector<double> p(N, 0.0);
@@ -721,8 +827,7 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
       double* d_pr = A.upload(pr, s);
       double* theta0 = A.alloc<double>(Nr);
       double* f0 = A.alloc<double>(E);
-      float* tmax = A.alloc<float>(tmax_n);
-      check(cudaMemsetAsync(tmax, 0, tmax_n * sizeof(float), s), "tmax");
+      float* tmax = tmax_all + static_cast<size_t>(t) * tmax_n;
       double* alpha0 = A.alloc<double>(std::max(g.Kpad, 1));
       gv.theta0 = theta0;
       gv.f0 = f0;
@@ -733,6 +838,12 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
       ctx->gt.push_back(gv);
     }
     g = ctx->gt[0];
+    ctx->g_mt = g;
+    if (T > 1) {
+      float* rec_mt = A.alloc<float>(tmax_n);
+      tgb::launch_rec_combine(tmax_all, tmax_n, T, rec_mt, s);
+      ctx->g_mt.Tmax = rec_mt;
+    }
     check(cudaStreamSynchronize(s), "context setup");
 
     ctx->n_cont = gd->n_contingencies;

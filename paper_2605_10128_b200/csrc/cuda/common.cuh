@@ -18,6 +18,7 @@ constexpr int kMaxMoved = 128;     // moved branch ends per candidate
 constexpr int kMaxRemoved = 24;    // removed branches (genome + outage case)
 constexpr int kMaxGround = 8;      // dead base nodes grounded
 constexpr int kMaxCols = kMaxSplits + kMaxRemoved + kMaxGround;  // Z columns for the outage rebuild
+constexpr int kTopoSol = kMaxSplits * kMaxSplits + kMaxSplits * kMaxCols + kMaxCols * kMaxCols;  // S^-1, Y, C^-1
 constexpr int kMaxTerms = 512;     // sparse coefficients over all Z columns
 constexpr int kMaxPMod = 16;       // omitted injections (p modifications)
 constexpr int kMaxInjMoved = 64;   // injections moved to new nodes

@@ -72,14 +72,36 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
     const uint32_t* tb = b.tbits + static_cast<size_t>(c) * 2 * words;
     for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = tb[i];
     __syncthreads();
+    if (threadIdx.x == 0) moved_injections(g, t);  // this profile's injections (the analysis may be shared)
+    const bool lite = b.prep_lite != 0;
+    if (lite && b.status[c] != 0) {  // islanded by the first profile's prep (structure only)
+      __syncthreads();
+      continue;
+    }
+    double* sol = b.topo_sol ? b.topo_sol + static_cast<size_t>(c) * kTopoSol : nullptr;
+    if (lite) {
+      // later profiles: the topology factors of the first profile's prep, only
+      // the injection side of the small solve and the rows are recomputed
+      copy_block(t.Sinv, sol, kTopoSol * sizeof(double), threadIdx.x, blockDim.x);
+      __syncthreads();
+      if (threadIdx.x == 0) {
+        theta_terms(g, t, thv);
+        small_rhs(t, thv);
+      }
+      __syncthreads();
+    }
     const int ldz = row_stride(t.ns + t.nv);
     double* zbuf = static_cast<size_t>(g.Nr) * ldz <= static_cast<size_t>(zsm_doubles) ? zsm : zglob;
-    build_z(g, t, zbuf, ldz);
-    __syncthreads();
-    gram_terms(g, t, zbuf, ldz, gram, kSweepRank, thv);
-    __syncthreads();
-    if (threadIdx.x == 0) small_solve(t, gram, kSweepRank, thv);
-    __syncthreads();
+    if (!lite) {
+      __syncthreads();
+      build_z(g, t, zbuf, ldz);
+      __syncthreads();
+      gram_terms(g, t, zbuf, ldz, gram, kSweepRank, thv);
+      __syncthreads();
+      if (threadIdx.x == 0) small_solve(t, gram, kSweepRank, thv);
+      __syncthreads();
+      if (sol && !t.islanded) copy_block(sol, t.Sinv, kTopoSol * sizeof(double), threadIdx.x, blockDim.x);
+    }
     if (t.islanded) {
       if (threadIdx.x == 0) {
         b.status[c] = t.islanded;
@@ -94,7 +116,16 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
     int nc0 = 0;
     for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
       double phi[kMaxSplits], rho[kMaxCols];
-      const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
+      bool on;
+      if (lite) {  // phi, rho from the first profile's branch row (L = b_e [phi; rho])
+        on = g.br_on[e] && !bit_get(rm_bits, e);
+        const double* fr0 = b.feat_ref + feat_index(slot, b.nchunks, e, r);
+        const double ib = 1.0 / g.br_b[e];
+        for (int q = 0; q < ns; ++q) phi[q] = on ? fr0[1 + q] * ib : 0.0;
+        for (int m = 0; m < nv; ++m) rho[m] = on ? fr0[1 + ns + m] * ib : 0.0;
+      } else {
+        on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
+      }
       double row[kStride];
 #pragma unroll
       for (int i = 0; i < kStride; ++i) row[i] = 0.0;
@@ -104,6 +135,19 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
         const double be = g.br_b[e];
         for (int q = 0; q < ns; ++q) row[1 + q] = be * phi[q];
         for (int m = 0; m < nv; ++m) row[1 + ns + m] = be * rho[m];
+      }
+      if (b.feat_mt) {  // multi-timestep bounds: max / min of f_c over profiles, L (profile-independent)
+        unsigned long long* m = reinterpret_cast<unsigned long long*>(b.feat_mt + feat_index(slot, b.nchunks, e, r + 1));
+        const unsigned long long key = order_key(row[0]);
+        if (b.t_index == 0) {
+          m[0] = key;
+          m[1] = key;
+          double* l = reinterpret_cast<double*>(m) + 2;
+          for (int q = 0; q < r; ++q) l[q] = row[1 + q];
+        } else {
+          atomicMax(m, key);
+          atomicMin(m + 1, key);
+        }
       }
       double2* dst = reinterpret_cast<double2*>(b.feat + feat_index(slot, b.nchunks, e, r));
 #pragma unroll
@@ -175,6 +219,24 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
       for (int i = 0; i < kStride / 2; ++i)
         if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
       kf[k] = flag;
+      if (b.amx_mt) {
+        // multi-timestep bounds per (tile, sub-tile): a warp covers 32
+        // consecutive contingencies of one tile (blockDim and tiles are
+        // multiples of 128), half a warp one 16-wide sub-tile
+        const int ntiles = g.Kpad / 128, tile = k >> 7, sub = (k & 127) >> 4;
+        double dl = fabs(row[0] - g.alpha0[k]);
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) dl = fmax(dl, __shfl_xor_sync(0xffffffffu, dl, o));
+        if ((threadIdx.x & 15) == 0)
+          atomicMax(b.amx_mt + (static_cast<size_t>(c) * ntiles + tile) * kTmaxSub + sub, dbits(dl));
+        for (int q = 0; q < r; ++q) {
+          double rq = fabs(row[1 + q]);
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) rq = fmax(rq, __shfl_xor_sync(0xffffffffu, rq, o));
+          if ((threadIdx.x & 31) == 0)
+            atomicMax(b.rmx_mt + (static_cast<size_t>(c) * ntiles + tile) * kStride + 1 + q, dbits(rq));
+        }
+      }
     }
     if (threadIdx.x == 0) {
       b.status[c] = 0;
@@ -603,22 +665,31 @@ __global__ void k_bits_to_double(const unsigned long long* in, double* out, size
 size_t topo_core_bytes() { return sizeof(TopoCore); }
 
 // ---------------------------------------------------------------- launcher
-void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
-                     cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin, cudaEvent_t sweep_end) {
-  int launched = 0;
-  const int words = (g.E + 31) >> 5;
-  const size_t bits_bytes = 2 * static_cast<size_t>(words) * sizeof(uint32_t);
+// Phases of one evaluation (launch_evaluate runs them in order; the
+// multi-timestep path of capi.cu interleaves them across profiles).
+int launch_eval_reset(const DevGrid& g, Batch& b, cudaStream_t stream) {
   cudaMemsetAsync(b.fmax, 0, static_cast<size_t>(b.n) * g.E * sizeof(unsigned long long), stream);
   cudaMemsetAsync(b.fbus, 0, static_cast<size_t>(b.n) * g.E * sizeof(unsigned long long), stream);
   cudaMemsetAsync(b.energy, 0, static_cast<size_t>(b.n) * g.Kall * sizeof(double), stream);
   cudaMemsetAsync(b.isl_out, 0, b.n * sizeof(int), stream);
   cudaMemsetAsync(b.isl_bus, 0, b.n * sizeof(int), stream);
+  return 0;
+}
+
+int launch_analyze(const DevGrid& g, Batch& b, int n_a, int n_d, cudaStream_t stream) {
+  int launched = 0;
+  const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
   static std::atomic<unsigned long long> carveout{0};
   if (first_use_on_device(carveout))  // one wave of warp-sized analysis CTAs needs the full shared-memory carveout
     cudaFuncSetAttribute(k_analyze, cudaFuncAttributePreferredSharedMemoryCarveout, 100);
   k_analyze<<<b.n < 65535 ? b.n : 65535, kAnalyzeThreads, bits_bytes, stream>>>(g, b, n_a, n_d);
   ++launched;
   launch_bucket(b, stream, &launched);
+  return launched;
+}
+
+int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch& s, cudaStream_t stream) {
+  const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
   // Z in shared memory up to kPrepZsmBytes (0: Z in the global scratch slots,
   // measured faster: the small serial solve needs many resident CTAs per SM)
   const size_t bits_al = (bits_bytes + 15) & ~size_t{15};
@@ -628,8 +699,13 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
     cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bits_al + zsm_bytes));
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
   k_prep<<<prep_grid, kPrepThreads, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots, zsm_doubles);
-  ++launched;
-  if (g.Ks > 0) launch_sweep(g, b, full, stream, sweep_begin, sweep_end, &launched);
+  return 1;
+}
+
+int launch_special_finish(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
+                          cudaStream_t stream) {
+  int launched = 0;
+  const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
   if (g.Kx + g.Kb > 0) {
     const long total = static_cast<long>(b.n) * (g.Kx + g.Kb);
     const int grid = static_cast<int>(total < s.zslots_special ? total : s.zslots_special);
@@ -638,6 +714,16 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
   }
   k_finish<<<(b.n + kFinishWarps - 1) / kFinishWarps, 32 * kFinishWarps, 0, stream>>>(g, b, n_a, n_d);
   ++launched;
+  return launched;
+}
+
+void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
+                     cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin, cudaEvent_t sweep_end) {
+  int launched = launch_eval_reset(g, b, stream);
+  launched += launch_analyze(g, b, n_a, n_d, stream);
+  launched += launch_prep(g, b, n_a, n_d, s, stream);
+  if (g.Ks > 0) launch_sweep(g, b, full, stream, sweep_begin, sweep_end, &launched);
+  launched += launch_special_finish(g, b, n_a, n_d, full, s, stream);
   if (kernels) *kernels = launched;
 }
 

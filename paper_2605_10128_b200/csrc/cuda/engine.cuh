@@ -15,6 +15,15 @@ constexpr int kMaxRemovedSweep = 4;  // genome disconnections skipped in the swe
 constexpr int kGroupSlots = 16;      // candidates per sweep CTA group (8 warps x 2)
 constexpr int kChunkRows = 32;       // branch rows per sweep pipeline stage
 
+// Ordered-integer key of a double (any sign): keys compare like the values.
+__device__ inline unsigned long long order_key(double x) {
+  const unsigned long long b = static_cast<unsigned long long>(__double_as_longlong(x));
+  return (b >> 63) ? ~b : (b | 0x8000000000000000ull);
+}
+__device__ inline double order_value(unsigned long long k) {
+  return __longlong_as_double(static_cast<long long>((k >> 63) ? (k & 0x7fffffffffffffffull) : ~k));
+}
+
 // Doubles per candidate row (branch row f_c, L[0..r-1] or contingency row
 // alpha, R'[0..r-1]) for update rank r, rounded up to whole double2.
 __host__ __device__ constexpr int row_stride(int r) { return (r + 2) & ~1; }
@@ -72,6 +81,21 @@ struct Batch {
   unsigned long long* fbus;   // [n][E] max |f| over busbar outages
   double* energy;             // [n][Kall] outage energy per contingency
   int* nc0;                   // [n] lambda_c0 of the candidate flows (k_prep)
+  // Multi-timestep screening (capi.cu, n_t > 1 profiles): k_prep of profile
+  // t_index folds every profile's candidate flows and flow factors into
+  // bounds over all profiles; k_sweep in mask mode (t_mode 1) marks the rows
+  // of each (candidate, tile) that can overload at some profile, k_sweep in
+  // masked mode (t_mode 2) then visits only those rows per profile.
+  int t_mode;                 // 0 single profile, 1 mask generation, 2 masked sweep
+  int t_index;                // profile of this prep pass (0 writes the bounds, > 0 folds)
+  double* feat_mt;            // rows [key(max_t f_c), key(min_t f_c), L...] at row_stride(r + 1), feat_index layout;
+                              // keys are the ordered bit patterns of doubles (order_key)
+  unsigned long long* amx_mt; // [n][ntiles][kTmaxSub] max_t max |alpha_t - alpha0_t| per sub-tile (bits)
+  unsigned long long* rmx_mt; // [n][ntiles][kStride] max_t max_k |R'_t[q, k]| per tile (bits, slot 1 + q)
+  uint32_t* mask;             // [n][ntiles][nchunks] rows that can overload at some profile
+  int prep_lite;              // k_prep reuses topo_sol and feat_ref (profiles after the first)
+  double* topo_sol;           // [n][kTopoSol] S^-1, Y, C^-1 of the first profile's small solve
+  const double* feat_ref;     // the first profile's candidate rows (L)
   int* isl_out;               // [n] islanded special contingencies
   int* isl_bus;               // [n]
   int* wl_list;               // [n] candidates bucketed by rank
@@ -92,6 +116,12 @@ struct EvalScratch {
 void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
                      cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin = nullptr,
                      cudaEvent_t sweep_end = nullptr);
+// The phases launch_evaluate runs (returning kernels launched).
+int launch_eval_reset(const DevGrid& g, Batch& b, cudaStream_t stream);
+int launch_analyze(const DevGrid& g, Batch& b, int n_a, int n_d, cudaStream_t stream);
+int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch& s, cudaStream_t stream);
+int launch_special_finish(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
+                          cudaStream_t stream);
 void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_out, double* fbus_out,
                     cudaStream_t stream);
 // Timestep aggregation (host loops launch_evaluate over t with the per-t
@@ -113,6 +143,9 @@ inline int max_sweep_groups(int n) { return (n + kGroupSlots - 1) / kGroupSlots 
 // X = B_red^-1 by in-place Gauss-Jordan (B_red is SPD; no pivoting needed).
 // Returns false when a pivot is not positive (disconnected grid).
 bool device_spd_inverse(double* a, int n, cudaStream_t stream);
+// Skip records of n_t profiles (contiguous, rec_floats each) combined into
+// bounds over all profiles (multi-timestep screening).
+void launch_rec_combine(const float* recs, size_t rec_floats, int n_t, float* out, cudaStream_t stream);
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
                         float* tmax, double* alpha0, cudaStream_t stream);
 

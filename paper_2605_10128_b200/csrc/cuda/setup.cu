@@ -151,7 +151,33 @@ __global__ void k_tmax(DevGrid g, const double* tk, const double* alpha0, float*
   }
 }
 
+// Skip records over all profiles: the sub-tile maxima of |T_base| are
+// profile-independent, max / min of T_base * alpha0_t over the profiles.
+__global__ void k_rec_combine(const float* recs, size_t rec_floats, int n_t, float* out) {
+  const size_t n = rec_floats / kRec;
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const float* r0 = recs + i * kRec;
+    float* o = out + i * kRec;
+    for (int j = 0; j < kTmaxSub; ++j) o[j] = r0[j];
+    float hi = r0[kTmaxSub], lo = r0[kTmaxSub + 1];
+    for (int t = 1; t < n_t; ++t) {
+      const float* r = recs + static_cast<size_t>(t) * rec_floats + i * kRec;
+      hi = fmaxf(hi, r[kTmaxSub]);
+      lo = fminf(lo, r[kTmaxSub + 1]);
+    }
+    o[kTmaxSub] = hi;
+    o[kTmaxSub + 1] = lo;
+    o[kTmaxSub + 2] = 0.f;
+    o[kTmaxSub + 3] = 0.f;
+  }
+}
+
 }  // namespace
+
+void launch_rec_combine(const float* recs, size_t rec_floats, int n_t, float* out, cudaStream_t stream) {
+  k_rec_combine<<<1024, 256, 0, stream>>>(recs, rec_floats, n_t, out);
+}
 
 bool device_spd_inverse(double* a, int n, cudaStream_t stream) {
   if (n == 0) return true;

@@ -57,10 +57,15 @@ static_assert(kMaxCand == kGroupSlots && kChunk == kChunkRows, "sweep tiles must
 __host__ __device__ constexpr int cand_per_cta(int) { return kWarps; }
 
 // Stage ring geometry for rank R (doubles per stage, number of stages).
-template <int R, bool FULL>
+// Timestep modes (Batch::t_mode): 0 one profile, 1 mask generation over all
+// profiles (k_sweep with rows [max f_c, min f_c, L...], no element work), 2
+// masked sweep of one profile (k_sweep_masked: only the rows marked by mode 1).
+constexpr int kTmSingle = 0, kTmMask = 1, kTmMasked = 2;
+
+template <int R, bool FULL, int TM = kTmSingle>
 struct Ring {
-  static constexpr int S = row_stride(R);
-  static constexpr int H = FULL ? 1 : (R <= 3 ? 4 : 2);                          // 32-row chunks per stage
+  static constexpr int S = row_stride(TM == kTmMask ? R + 1 : R);
+  static constexpr int H = FULL ? 1 : (S <= 4 ? 4 : (S <= 10 ? 2 : 1));          // 32-row chunks per stage
   static constexpr size_t FH = static_cast<size_t>(kMaxCand) * kChunk * S;       // one chunk of candidate rows
   static constexpr size_t T = FULL ? static_cast<size_t>(kChunk) * kTileK : 0;  // T_base tile rows
   static constexpr size_t F = H * FH;                                           // candidate rows
@@ -114,31 +119,33 @@ struct CtaWork {
 
 // Producer: stage <- stage-chunk i = 32-row chunks [H i, H i + H) (T tile rows
 // when FULL, the group's candidate rows, limits, skip records when not FULL).
-template <int R, bool FULL>
+template <int R, bool FULL, int TM>
 __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, int i,
                                            double* stage, uint64_t* bar) {
-  using Rg = Ring<R, FULL>;
+  using Rg = Ring<R, FULL, TM>;
   const int e0 = i * Rg::H * kChunk;
   const int rows = min(Rg::H * kChunk, g.E - e0);
   const int nch = (rows + kChunk - 1) / kChunk;
   const uint32_t bt = FULL ? rows * kTileK * sizeof(double) : 0;
   const uint32_t bf = nch * Rg::FH * sizeof(double);  // the group's rows of these chunks: one contiguous block
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
-  const uint32_t bm = FULL ? 0 : rows * kRec * sizeof(float);
+  const uint32_t bm = Rg::M ? rows * kRec * sizeof(float) : 0;
   mbar_expect_tx(bar, bt + bf + bl + bm);
   if (FULL) bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
-  bulk_g2s(stage + Rg::T, b.feat + feat_index(w.group * kGroupSlots, b.nchunks, e0, R), bf, bar);
+  const double* rows_src = TM == kTmMask ? b.feat_mt : b.feat;
+  bulk_g2s(stage + Rg::T, rows_src + feat_index(w.group * kGroupSlots, b.nchunks, e0, TM == kTmMask ? R + 1 : R), bf,
+           bar);
   bulk_g2s(stage + Rg::T + Rg::F, g.br_lim + e0, bl, bar);
-  if (!FULL)
+  if (Rg::M)
     bulk_g2s(stage + Rg::T + Rg::F + Rg::L, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kRec, bm,
              bar);
   static_assert(kRec % 4 == 0, "skip records are whole float4");
 }
 
-template <int R, bool FULL>
+template <int R, bool FULL, int TM = kTmSingle>
 __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
                                           uint64_t* bars, double* rmax_s, double* amax_s) {
-  using Rg = Ring<R, FULL>;
+  using Rg = Ring<R, FULL, TM>;
   constexpr int S = Rg::S, NST = Rg::stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = tile * kTileK + lane * kKpl;
@@ -148,7 +155,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   int kbr[kKpl], rem[kMaxRemovedSweep];
   int cid = warp < w.ncand ? w.cand[warp] : -1;
   if (cid >= 0 && b.status[cid] != 0) cid = -1;  // islanded by the small solve in k_prep
-  {
+  if (TM != kTmMask) {
     const int c = cid >= 0 ? cid : w.cand[0];
     const double* kd = b.kdat + static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(kb) * S;
     const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad + kb;
@@ -170,7 +177,17 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   // a row weight vector rms[slot] (0 for f_c and padding).
   double* rms = rmax_s + warp * kStride;
   double* asub = amax_s + warp * kTmaxSub;
-  if (!FULL) {
+  const int ntiles = g.Kpad / kTileK;
+  if (TM == kTmMask) {
+    // bounds over all profiles, folded by k_prep (bit patterns of non-negative doubles)
+    const size_t at = (static_cast<size_t>(cid >= 0 ? cid : 0) * ntiles + tile);
+    if (lane < kStride)
+      rms[lane] = lane >= 1 && lane <= R && cid >= 0 ? __longlong_as_double(b.rmx_mt[at * kStride + lane]) * (1.0 + 1e-12)
+                                                     : 0.0;
+    if (lane < kTmaxSub)
+      asub[lane] = cid >= 0 ? __longlong_as_double(b.amx_mt[at * kTmaxSub + lane]) * (1.0 + 1e-12) : 0.0;
+    __syncwarp();
+  } else if (!FULL && TM == kTmSingle) {
     if (lane < kStride) rms[lane] = 0.0;
     __syncwarp();
     double a = 0.0;
@@ -192,7 +209,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   }
   // small ranks keep the per-warp skip weights in registers (stage 1 then reads
   // only the row data from shared memory)
-  constexpr bool kRegW = !FULL && R <= 3;
+  constexpr bool kRegW = !FULL && TM == kTmSingle && R <= 3;
   double areg[kRegW ? kTmaxSub : 1], wreg[kRegW ? S : 1];
   if (kRegW) {
 #pragma unroll
@@ -205,7 +222,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   unsigned rows_computed = 0, rows_offered = 0, rows_exact = 0, rows_partial = 0;  // skip statistics
   if (threadIdx.x == 0)
     for (int s = 0; s < NST && s < nchunks; ++s)
-      issue_chunk<R, FULL>(g, b, w, tile, s, smem + s * Rg::doubles, bars + s);
+      issue_chunk<R, FULL, TM>(g, b, w, tile, s, smem + s * Rg::doubles, bars + s);
 
   // exact path for one branch row: energies (registers) and fmax (atomicMax)
   auto exact_row = [&](int e, double lim, const double (&f1)[kKpl]) {
@@ -286,19 +303,31 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       // against the high word of lim (1 - 1e-12) - lrb (0 when not positive).
       bool hot = false;
       uint32_t thr_lane = 0u;
+      const int chunk32 = i * Rg::H + h;
       if (lane < rows) {
         const double lim = sL[lane] * (1.0 - 1e-12);
         const float4* rec = reinterpret_cast<const float4*>(st + Rg::T + Rg::F + Rg::L) + (h * kChunk + lane) * (kRec / 4);
         const double2* fr = reinterpret_cast<const double2*>(sF + lane * S);
         const double2* wr = reinterpret_cast<const double2*>(rms);
-        double lrb = 0.0, fc = 0.0;
+        double lrb = 0.0, fc = 0.0, flo = 0.0;
+        if (TM == kTmMask) {
+          // rows [key(max_t f_c), key(min_t f_c), L_0..L_{R-1}]; rms slot 1 + q weighs L_q
+          const unsigned long long* kr = reinterpret_cast<const unsigned long long*>(fr);
+          fc = order_value(kr[0]);
+          flo = order_value(kr[1]);
+          const double* l = reinterpret_cast<const double*>(fr) + 2;
 #pragma unroll
-        for (int q = 0; q < S / 2; ++q) {
-          const double2 p2 = fr[q];
-          const double2 w2 = kRegW ? make_double2(wreg[kRegW ? 2 * q : 0], wreg[kRegW ? 2 * q + 1 : 0]) : wr[q];
-          lrb = fma(fabs(p2.x), w2.x, lrb);
-          lrb = fma(fabs(p2.y), w2.y, lrb);
-          if (q == 0) fc = p2.x;
+          for (int q = 0; q < R; ++q) lrb = fma(fabs(l[q]), rms[1 + q], lrb);
+        } else {
+#pragma unroll
+          for (int q = 0; q < S / 2; ++q) {
+            const double2 p2 = fr[q];
+            const double2 w2 = kRegW ? make_double2(wreg[kRegW ? 2 * q : 0], wreg[kRegW ? 2 * q + 1 : 0]) : wr[q];
+            lrb = fma(fabs(p2.x), w2.x, lrb);
+            lrb = fma(fabs(p2.y), w2.y, lrb);
+            if (q == 0) fc = p2.x;
+          }
+          flo = fc;
         }
         const double2* ar = reinterpret_cast<const double2*>(asub);
         double ta = 0.0;
@@ -315,12 +344,16 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
         const double thr = lim - lrb;
         thr_lane = thr > 0.0 ? hi_abs(thr) : 0u;
         const double wd = ta + lrb;
-        const double slack = 1e-12 * (fabs(fc) + fmax(d0.x, -d0.y) + wd);
-        hot = (fc + d0.x + wd + slack >= lim) || (fc + d0.y - wd - slack <= -lim);
+        const double slack = 1e-12 * (fmax(fabs(fc), fabs(flo)) + fmax(d0.x, -d0.y) + wd);
+        hot = (fc + d0.x + wd + slack >= lim) || (flo + d0.y - wd - slack <= -lim);
       }
       unsigned need = __ballot_sync(0xffffffffu, hot);
       rows_partial += __popc(need);
       rows_offered += rows;
+      if (TM == kTmMask) {
+        if (lane == 0 && cid >= 0) b.mask[(static_cast<size_t>(cid) * ntiles + tile) * b.nchunks + chunk32] = need;
+        continue;  // no element work in mask generation
+      }
       // Stage 2: hot rows in batches of NB, T_base row loads issued before use
       constexpr int NB = R >= 6 ? 1 : (R >= 4 ? 2 : 4);  // register budget (128 per thread at 512 threads)
       const double* tk_rows = g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK + lane * kKpl;
@@ -368,7 +401,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     if (threadIdx.x == 0 && i + NST < nchunks) {
       mbar_wait(bars + kMaxStages + s, (i / NST) & 1);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_chunk<R, FULL>(g, b, w, tile, i + NST, smem + s * Rg::doubles, bars + s);
+      issue_chunk<R, FULL, TM>(g, b, w, tile, i + NST, smem + s * Rg::doubles, bars + s);
     }
     __syncwarp();
   }
@@ -405,7 +438,7 @@ __device__ __forceinline__ void cta_setup(const Batch& b, int group, int r, CtaW
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-template <bool FULL>
+template <bool FULL, int TM>
 __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CtaWork w;
@@ -427,14 +460,14 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
   }
   __syncthreads();
   switch (r_s) {
-    case 0: sweep_cta<0, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 1: sweep_cta<1, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 2: sweep_cta<2, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 3: sweep_cta<3, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 4: sweep_cta<4, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 5: sweep_cta<5, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 6: sweep_cta<6, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    default: sweep_cta<7, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 0: sweep_cta<0, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 1: sweep_cta<1, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 2: sweep_cta<2, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 3: sweep_cta<3, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 4: sweep_cta<4, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 5: sweep_cta<5, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 6: sweep_cta<6, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    default: sweep_cta<7, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
   }
 }
 
@@ -442,7 +475,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
 // nodes; rare): a persistent kernel over their (tile, group) items, so its
 // register allocation stays out of the common kernel and an empty bucket
 // costs one short launch.
-template <bool FULL>
+template <bool FULL, int TM>
 __global__ void __launch_bounds__(kThreads, 1) k_sweep_hi(DevGrid g, Batch b, int ntiles) {
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CtaWork w;
@@ -464,14 +497,165 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep_hi(DevGrid g, Batch b, in
     }
     __syncthreads();
     switch (r_s) {
-      case 8: sweep_cta<8, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-      case 9: sweep_cta<9, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-      case 10: sweep_cta<10, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-      default: sweep_cta<11, FULL>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      case 8: sweep_cta<8, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      case 9: sweep_cta<9, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      case 10: sweep_cta<10, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      default: sweep_cta<11, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
     }
   }
 }
 static_assert(kSweepRank == 11 && kFastRank == 7, "k_sweep / k_sweep_hi rank switches");
+
+// Masked sweep of one injection profile (multi-timestep screening,
+// Batch::t_mode 2): no staging ring; each warp visits only the rows its
+// candidate's all-profile mask marks for this tile (a few percent) and gathers
+// their candidate row and T_base row from L2, NB rows at a time.
+template <int R>
+__device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile) {
+  constexpr int S = row_stride(R);
+  constexpr int NB = R <= 3 ? 4 : (R <= 5 ? 2 : 1);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int kb = tile * kTileK + lane * kKpl;
+  double alpha[kKpl], rr[kKpl][R > 0 ? R : 1], energy[kKpl];
+  bool kval[kKpl];
+  int kbr[kKpl], rem[kMaxRemovedSweep];
+  int cid = warp < w.ncand ? w.cand[warp] : -1;
+  if (cid >= 0 && b.status[cid] != 0) cid = -1;
+  {
+    const int c = cid >= 0 ? cid : w.cand[0];
+    const double* kd = b.kdat + static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(kb) * S;
+    const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad + kb;
+#pragma unroll
+    for (int i = 0; i < kKpl; ++i) {
+      kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
+      alpha[i] = kd[i * S];
+#pragma unroll
+      for (int q = 0; q < R; ++q) rr[i][q] = kd[i * S + 1 + q];
+      energy[i] = 0.0;
+      kval[i] = cid >= 0 && kf[i] == 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kMaxRemovedSweep; ++q) rem[q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
+  }
+  if (cid >= 0) {
+    const int ntiles = g.Kpad / kTileK;
+    const uint32_t* mw = b.mask + (static_cast<size_t>(cid) * ntiles + tile) * b.nchunks;
+    const size_t slot = static_cast<size_t>(w.group) * kGroupSlots + warp;
+    unsigned long long* fmx = b.fmax + static_cast<size_t>(cid) * g.E;
+    int pend[NB];
+    int np = 0;
+    // one batch of up to NB marked rows: loads first, then the arithmetic
+    auto flush = [&]() {
+      double2 t[NB][2];
+      double frow[NB][S];
+      double lim[NB];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const int e = u < np ? pend[u] : pend[0];
+        const double2* src = reinterpret_cast<const double2*>(g.TK + (static_cast<size_t>(tile) * g.E + e) * kTileK +
+                                                              lane * kKpl);
+        t[u][0] = __ldg(src);
+        t[u][1] = __ldg(src + 1);
+        const double* fr = b.feat + feat_index(static_cast<int>(slot), b.nchunks, e, R);
+#pragma unroll
+        for (int q = 0; q < S; ++q) frow[u][q] = fr[q];
+        lim[u] = g.br_lim[e];
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        if (u >= np) break;
+        const int e = pend[u];
+        const double tv[kKpl] = {t[u][0].x, t[u][0].y, t[u][1].x, t[u][1].y};
+        double f1[kKpl];
+        uint32_t mx = 0u;
+#pragma unroll
+        for (int k = 0; k < kKpl; ++k) {
+          double acc = fma(tv[k], alpha[k], frow[u][0]);
+#pragma unroll
+          for (int q = 0; q < R; ++q) acc = fma(frow[u][1 + q], rr[k][q], acc);
+          f1[k] = acc;
+          mx = max(mx, hi_abs(acc));
+        }
+        if (!__any_sync(0xffffffffu, mx >= hi_abs(lim[u]))) continue;
+        bool skip_row = false;
+#pragma unroll
+        for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[q];
+        unsigned long long m = 0ull;
+#pragma unroll
+        for (int k = 0; k < kKpl; ++k) {
+          if (!kval[k] || skip_row || e == kbr[k]) continue;
+          const double a = fabs(f1[k]);
+          if (a > lim[u]) energy[k] += a - lim[u];
+          m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+        }
+        if (m > static_cast<unsigned long long>(__double_as_longlong(lim[u]))) atomicMax(fmx + e, m);
+      }
+      np = 0;
+    };
+    for (int c0 = 0; c0 < b.nchunks; c0 += 32) {
+      const unsigned mine = c0 + lane < b.nchunks ? mw[c0 + lane] : 0u;
+      unsigned nz = __ballot_sync(0xffffffffu, mine != 0u);
+      while (nz) {
+        const int j = __ffs(nz) - 1;
+        nz &= nz - 1;
+        unsigned word = __shfl_sync(0xffffffffu, mine, j);
+        while (word) {
+          pend[np++] = (c0 + j) * kChunk + __ffs(word) - 1;
+          word &= word - 1;
+          if (np == NB) flush();
+        }
+      }
+    }
+    if (np) flush();
+    double* en = b.energy + static_cast<size_t>(cid) * g.Kall;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k)
+      if (kval[k] && kb + k < g.Ks) en[g.ks_cont[kb + k]] = energy[k];
+  }
+}
+
+template <int R>
+__device__ __noinline__ void masked_cta_call(const DevGrid& g, const Batch& b, const CtaWork& w, int tile) {
+  masked_cta<R>(g, b, w, tile);
+}
+
+__global__ void __launch_bounds__(kThreads, 1) k_sweep_masked(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
+  __shared__ CtaWork w;
+  __shared__ int r_s;
+  const int per_sb = gblock * ntiles;
+  const int sb = static_cast<int>(blockIdx.x) / per_sb, rr = static_cast<int>(blockIdx.x) % per_sb;
+  const int g0 = sb * gblock, gg = min(gblock, ngroups - g0);
+  const int tile = rr / gg, group = g0 + rr % gg;
+  if (group >= b.wl_group0[kSweepRank + 1]) return;
+  if (threadIdx.x == 0) {
+    int r = 0;
+    while (r < kSweepRank && group >= b.wl_group0[r + 1]) ++r;
+    r_s = r;
+    const int per = cand_per_cta(r);
+    const int first = (group - b.wl_group0[r]) * per;
+    int n = 0;
+    for (int j = 0; j < per; ++j)
+      if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
+    w.ncand = n;
+    w.group = group;
+  }
+  __syncthreads();
+  switch (r_s) {
+    case 0: masked_cta<0>(g, b, w, tile); break;
+    case 1: masked_cta<1>(g, b, w, tile); break;
+    case 2: masked_cta<2>(g, b, w, tile); break;
+    case 3: masked_cta<3>(g, b, w, tile); break;
+    case 4: masked_cta<4>(g, b, w, tile); break;
+    case 5: masked_cta<5>(g, b, w, tile); break;
+    // higher ranks in their own call frames (register pressure of the common ones)
+    case 6: masked_cta_call<6>(g, b, w, tile); break;
+    case 7: masked_cta_call<7>(g, b, w, tile); break;
+    case 8: masked_cta_call<8>(g, b, w, tile); break;
+    case 9: masked_cta_call<9>(g, b, w, tile); break;
+    case 10: masked_cta_call<10>(g, b, w, tile); break;
+    default: masked_cta_call<11>(g, b, w, tile); break;
+  }
+}
 
 // Stable per-rank lists of swept candidates; bucket r is cut into CTA groups
 // of cand_per_cta(r), and every swept candidate gets its row slot
@@ -524,10 +708,13 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
                   int* launched) {
   static std::atomic<unsigned long long> configured{0};
   if (first_use_on_device(configured)) {
-    cudaFuncSetAttribute(k_sweep<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-    cudaFuncSetAttribute(k_sweep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-    cudaFuncSetAttribute(k_sweep_hi<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
-    cudaFuncSetAttribute(k_sweep_hi<false>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kSmemBytes));
+    const int sm = static_cast<int>(kSmemBytes);
+    cudaFuncSetAttribute(k_sweep<true, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep<false, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep<false, kTmMask>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep_hi<true, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep_hi<false, kTmMask>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
   static const int gblock_env = [] {
@@ -540,11 +727,16 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
   if (ev0) cudaEventRecord(ev0, stream);
   constexpr int kHiCtas = 148;  // persistent: one CTA per SM
   if (full) {
-    k_sweep<true><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
-    k_sweep_hi<true><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+    k_sweep<true, kTmSingle><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_hi<true, kTmSingle><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+  } else if (b.t_mode == kTmMask) {
+    k_sweep<false, kTmMask><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_hi<false, kTmMask><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+  } else if (b.t_mode == kTmMasked) {
+    k_sweep_masked<<<grid, kThreads, 0, stream>>>(g, b, ntiles, ngroups, gblock);
   } else {
-    k_sweep<false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
-    k_sweep_hi<false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+    k_sweep<false, kTmSingle><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_hi<false, kTmSingle><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
   }
   if (ev1) cudaEventRecord(ev1, stream);
   *launched += 2;

@@ -60,12 +60,15 @@ struct alignas(16) TopoCore {
 };
 
 struct Topo : TopoCore {
-  // small-solve results
-  double Sinv[kMaxSplits * kMaxSplits];
+  // small-solve results (Sinv, Y, Cinv contiguous: copied as one block of kTopoSol doubles)
+  alignas(16) double Sinv[kMaxSplits * kMaxSplits];
   double Y[kMaxSplits * kMaxCols];  // S^-1 Phi  (ns x nv), row-major
   double Cinv[kMaxCols * kMaxCols];
   double Rp[kMaxSplits + kMaxCols]; // [S^-1 phi_p ; -C^-1 rho_p]
 };
+static_assert(sizeof(Topo::Sinv) + sizeof(Topo::Y) + sizeof(Topo::Cinv) == kTopoSol * sizeof(double) &&
+                  (kTopoSol * 8) % 16 == 0,
+              "the small-solve factors are one 16-byte multiple block");
 
 // Cooperative copy of a 16-byte aligned block by the threads [0, nthreads).
 __device__ __forceinline__ void copy_block(void* dst, const void* src, size_t bytes, int tid, int nthreads) {
@@ -156,6 +159,17 @@ __device__ inline bool cand_hosts_injection(const DevGrid& g, const TopoCore& t,
     if (g.inj_net[i] != 0.0 && !omitted(t, i)) return true;
   }
   return false;
+}
+
+// Net injection moved onto each live split node (the only part of the
+// analysis that depends on the injection values, not just their zero
+// pattern: recomputed per injection profile).
+__device__ inline void moved_injections(const DevGrid& g, TopoCore& t) {
+  for (int q = 0; q < t.ns; ++q) t.ppsi[q] = 0.0;
+  for (int i = 0; i < t.ninj; ++i) {
+    const int q = t.q_of_new[t.inj_new[i]];
+    if (q >= 0 && !omitted(t, t.inj_id[i])) t.ppsi[q] += g.inj_net[t.inj_id[i]];
+  }
 }
 
 // Thread-0 analysis of one topology: genome slots plus an optional outage
@@ -312,12 +326,7 @@ __device__ inline void analyze(const DevGrid& g, TopoCore& t, uint32_t* mv_bits,
   t.col_ptr[col] = nt;
   t.thresh_scale = wmax;  // S pivots are compared with the moved susceptance sum
 
-  // net injection moved onto each live split node
-  for (int q = 0; q < t.ns; ++q) t.ppsi[q] = 0.0;
-  for (int i = 0; i < t.ninj; ++i) {
-    const int q = t.q_of_new[t.inj_new[i]];
-    if (q >= 0 && !omitted(t, t.inj_id[i])) t.ppsi[q] += g.inj_net[t.inj_id[i]];
-  }
+  moved_injections(g, t);
 }
 
 // In-place inverse of a small dense matrix (row-major, leading dim ld) by
@@ -432,6 +441,17 @@ __device__ inline void gram_terms(const DevGrid& g, const TopoCore& t, const dou
   }
 }
 
+__device__ inline void small_rhs(Topo& t, const double* th);
+
+// th[c] = [U|V]_c^T theta' (thread 0; no Z needed).
+__device__ inline void theta_terms(const DevGrid& g, const TopoCore& t, double* th) {
+  for (int c = 0; c < t.ns + t.nv; ++c) {
+    double acc = 0.0;
+    for (int p = t.col_ptr[c]; p < t.col_ptr[c + 1]; ++p) acc = fma(t.term_coef[p], theta_mod(g, t, t.term_idx[p]), acc);
+    th[c] = acc;
+  }
+}
+
 // Thread-0 small solve on the Gram entries (block-synchronized by the caller).
 // Sets t.islanded = 1 when S or C is singular.
 __device__ inline void small_solve(Topo& t, const double* G, int ldg, const double* th) {
@@ -477,7 +497,16 @@ __device__ inline void small_solve(Topo& t, const double* G, int ldg, const doub
     t.islanded = 1;
     return;
   }
-  // injection-side coefficients: phi_p = U^T theta' - p_psi, rho_p = V^T theta' + Y^T phi_p
+  small_rhs(t, th);
+}
+
+// Injection side of the small solve (the only part that depends on the
+// injection profile): phi_p = U^T theta' - p_psi, rho_p = V^T theta' + Y^T phi_p,
+// Rp = [S^-1 phi_p ; -C^-1 rho_p].
+__device__ inline void small_rhs(Topo& t, const double* th) {
+  const int ns = t.ns, nv = t.nv;
+  const double* S = t.Sinv;
+  const double* C = t.Cinv;
   double php[kMaxSplits], rhp[kMaxCols];
   for (int c = 0; c < ns + nv; ++c) {
     if (c < ns)
