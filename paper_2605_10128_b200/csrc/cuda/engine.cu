@@ -52,6 +52,7 @@ __global__ void __launch_bounds__(kAnalyzeThreads) k_analyze(DevGrid g, Batch b,
 // One CTA per candidate (grid-stride over candidates). Z = X [U | V] lives in
 // shared memory (row stride row_stride(r)) when it fits in `zsm_doubles`, else
 // in the CTA's global scratch slot.
+template <bool LITE>  // LITE: a later injection profile reusing the first profile's factors and rows
 __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch,
                                                        int zslots, int zsm_doubles) {
   extern __shared__ __align__(16) uint32_t bits[];
@@ -73,7 +74,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n
     for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = tb[i];
     __syncthreads();
     if (threadIdx.x == 0) moved_injections(g, t);  // this profile's injections (the analysis may be shared)
-    const bool lite = b.prep_lite != 0;
+    constexpr bool lite = LITE;
     if (lite && b.status[c] != 0) {  // islanded by the first profile's prep (structure only)
       __syncthreads();
       continue;
@@ -696,9 +697,15 @@ int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch&
   const size_t zsm_bytes = std::min<size_t>(static_cast<size_t>(g.Nr) * kStride * sizeof(double), kPrepZsmBytes);
   const int zsm_doubles = static_cast<int>(zsm_bytes / sizeof(double));
   if (bits_al + zsm_bytes > 48 * 1024)  // (per launch: the size depends on the grid)
-    cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bits_al + zsm_bytes));
+    cudaFuncSetAttribute(b.prep_lite ? k_prep<true> : k_prep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(bits_al + zsm_bytes));
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
-  k_prep<<<prep_grid, kPrepThreads, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots, zsm_doubles);
+  if (b.prep_lite)
+    k_prep<true><<<prep_grid, kPrepThreads, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
+                                                                           zsm_doubles);
+  else
+    k_prep<false><<<prep_grid, kPrepThreads, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
+                                                                            zsm_doubles);
   return 1;
 }
 
