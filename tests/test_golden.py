@@ -1,0 +1,59 @@
+"""Golden vectors (tests/golden/grid14_congested_golden.json, made by
+tests/golden/make_golden.py from the oracle): 92 genomes on the bundled
+grid14_congested.json -- the unchanged topology, every single action, every
+single disconnection and 48 random genomes -- with their scores and flows.
+The oracle must reproduce them exactly (CPU); the engine within 1e-9 (GPU)."""
+import json
+import os
+
+import numpy as np
+import pytest
+
+from oracle.oracle import OracleContext
+
+HERE = os.path.join(os.path.dirname(__file__), "golden")
+
+
+def _golden():
+    gold = json.load(open(os.path.join(HERE, "grid14_congested_golden.json")))
+    text = open(os.path.join(HERE, gold["grid"])).read()
+    return gold, text, np.array(gold["genomes"], np.int32)
+
+
+def test_oracle_reproduces_golden_vectors():
+    gold, text, g = _golden()
+    ref = OracleContext(text).evaluate(g, gold["n_a"], gold["n_d"], flows=True)
+    for i, s in enumerate(gold["scores"]):
+        assert ref["fitness"][i] == s["fitness"] and ref["lambda_c"][i] == s["lambda_c"]
+        assert ref["lambda_o"][i] == s["lambda_o"] and ref["lambda_b"][i] == s["lambda_b"]
+        assert list(ref["base"][i]) == s["base"] and list(ref["fmax"][i]) == s["fmax"]
+
+
+@pytest.mark.gpu
+def test_engine_matches_golden_vectors():
+    import paper_2605_10128_b200 as P
+
+    gold, text, g = _golden()
+    grid = P.grid_from_json_text(text)
+    ctx = P.DcContext(grid, P.build_action_set(grid))
+    sc, fr = ctx.evaluate_arrays(g, gold["n_a"], gold["n_d"], flows=True)
+    lim = ctx.grid.branch_limit
+    for i, s in enumerate(gold["scores"]):
+        assert bool(sc.islanded[i]) == bool(s["islanded"])
+        for k in ("lambda_d", "lambda_s", "lambda_r"):
+            assert getattr(sc, k)[i] == s[k], (i, k)
+        if s["islanded"]:
+            assert sc.fitness[i] == -np.inf
+            continue
+        scale = max(1.0, abs(s["fitness"]))
+        knife = np.abs(np.array(s["fmax"]) - lim) <= 1e-9 * np.maximum(1.0, lim)
+        if sc.lambda_c[i] == s["lambda_c"] and sc.lambda_c0[i] == s["lambda_c0"]:
+            assert abs(sc.fitness[i] - s["fitness"]) <= 1e-9 * scale, i
+        else:
+            assert knife.any(), f"genome {i}: count difference off the knife edge"
+        assert abs(sc.lambda_o[i] - s["lambda_o"]) <= 1e-9 * max(1.0, abs(s["lambda_o"]))
+        np.testing.assert_allclose(fr.base[i], s["base"], rtol=1e-9, atol=1e-9)
+        np.testing.assert_allclose(fr.max_contingency[i], s["fmax"], rtol=1e-9, atol=1e-9)
+        got = [(int(a), float(b)) for a, b in zip(sc.worst_idx[i, :sc.worst_n[i]], sc.worst_energy[i, :sc.worst_n[i]])]
+        want = [(a, b) for a, b in s["worst"]]
+        assert [a for a, _ in got if _ > 1e-7] == [a for a, b in want if b > 1e-7] or knife.any(), i
