@@ -14,11 +14,13 @@
 // alpha / R' live in registers for the whole sweep. Candidate rows are
 // row_stride(R) doubles (f_c, L[0..R-1]), contingency rows likewise.
 //
-// Scores-only kernel (k_sweep<false>, the MapElites path): branch rows are
-// streamed in chunks of 32 by TMA bulk copies (cp.async.bulk + mbarrier
-// complete_tx) into a 5-8 stage ring: the group's candidate rows, the limits
-// and the per-(tile, row) skip record (sub-tile max |T_base|, extrema of
-// T_base * alpha0). T_base itself is NOT streamed:
+// Scores-only kernel (k_sweep<false, kTmSingle>, the MapElites path): branch
+// rows are streamed in stages of 1-4 chunks of 32 by TMA bulk copies
+// (cp.async.bulk + mbarrier complete_tx) into a 2-8 stage ring: the group's
+// candidate rows, the limits and the per-(tile, row) skip record (sub-tile max
+// |T_base|, extrema of T_base * alpha0, float4 with directed rounding); warps
+// release a stage on its empty mbarrier and thread 0 refills it. T_base itself
+// is NOT streamed:
 //   stage 1 (one lane per row, no element work): a rigorous bound of |f1|
 //     over the whole tile proves most (row, candidate) blocks safe;
 //   stage 2 (rows that fail it): the lanes load that row of the T_base tile
@@ -26,11 +28,14 @@
 //     element with the L R' part bounded;
 //   stage 3: the remaining R DFMA per element and a hi-word test; the exact
 //     path runs only where |f1| can exceed the limit.
-// Skipped work cannot change any score (tests/test_gpu_evaluate.py compares the
-// two kernels and the oracle).
+// Skipped work cannot change any score (tests/test_gpu_scale.py compares the
+// skipping and the dense kernel bit for bit, and both with the oracle).
 //
 // Flows kernel (k_sweep<true>, FlowResult requested): every element computed,
 // T_base tiles streamed with the rows, max |f1| folded for every branch.
+// Ranks 8..11 run in the persistent k_sweep_hi (own register allocation).
+// Timestep grids: k_sweep<false, kTmMask> marks the rows that can overload at
+// some injection profile, k_sweep_masked visits only those per profile.
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
