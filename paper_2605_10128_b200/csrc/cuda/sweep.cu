@@ -149,7 +149,7 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
 
 template <int R, bool FULL, int TM = kTmSingle>
 __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
-                                          uint64_t* bars, double* rmax_s, double* amax_s) {
+                                          uint64_t* bars, double* rmax_s, float* amax_s) {
   using Rg = Ring<R, FULL, TM>;
   constexpr int S = Rg::S, NST = Rg::stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -181,7 +181,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   // the unchanged topology's flow factors), and the tile max of each |R'_q| as
   // a row weight vector rms[slot] (0 for f_c and padding).
   double* rms = rmax_s + warp * kStride;
-  double* asub = amax_s + warp * kTmaxSub;
+  float* asub = amax_s + warp * kTmaxSub;  // rounded up to float: the T_base x delta bound runs in FP32
   const int ntiles = g.Kpad / kTileK;
   if (TM == kTmMask) {
     // bounds over all profiles, folded by k_prep (bit patterns of non-negative doubles)
@@ -190,7 +190,8 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
       rms[lane] = lane >= 1 && lane <= R && cid >= 0 ? __longlong_as_double(b.rmx_mt[at * kStride + lane]) * (1.0 + 1e-12)
                                                      : 0.0;
     if (lane < kTmaxSub)
-      asub[lane] = cid >= 0 ? __longlong_as_double(b.amx_mt[at * kTmaxSub + lane]) * (1.0 + 1e-12) : 0.0;
+      asub[lane] = cid >= 0 ? __double2float_ru(__longlong_as_double(b.amx_mt[at * kTmaxSub + lane]) * (1.0 + 1e-12))
+                            : 0.0f;
     __syncwarp();
   } else if (!FULL && TM == kTmSingle) {
     if (lane < kStride) rms[lane] = 0.0;
@@ -200,7 +201,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[k] - g.alpha0[kb + k]));
 #pragma unroll
     for (int o = kSubLanes / 2; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-    if (lane % kSubLanes == 0) asub[lane / kSubLanes] = a * (1.0 + 1e-12);
+    if (lane % kSubLanes == 0) asub[lane / kSubLanes] = __double2float_ru(a * (1.0 + 1e-12));
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       double r = 0.0;
@@ -215,7 +216,8 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   // small ranks keep the per-warp skip weights in registers (stage 1 then reads
   // only the row data from shared memory)
   constexpr bool kRegW = !FULL && TM == kTmSingle && R <= 3;
-  double areg[kRegW ? kTmaxSub : 1], wreg[kRegW ? S : 1];
+  float areg[kRegW ? kTmaxSub : 1];
+  double wreg[kRegW ? S : 1];
   if (kRegW) {
 #pragma unroll
     for (int q = 0; q < kTmaxSub; ++q) areg[q] = asub[q];
@@ -334,16 +336,20 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
           }
           flo = fc;
         }
-        const double2* ar = reinterpret_cast<const double2*>(asub);
-        double ta = 0.0;
+        // max_s Tmax_s * delta_s in FP32 rounded up (both factors are
+        // non-negative upper bounds already rounded up to float)
+        const float4* ar = reinterpret_cast<const float4*>(asub);
+        float taf = 0.0f;
 #pragma unroll
         for (int q = 0; q < kTmaxSub / 4; ++q) {
           const float4 t4 = rec[q];
-          const double2 a01 = kRegW ? make_double2(areg[kRegW ? 4 * q : 0], areg[kRegW ? 4 * q + 1 : 0]) : ar[2 * q];
-          const double2 a23 = kRegW ? make_double2(areg[kRegW ? 4 * q + 2 : 0], areg[kRegW ? 4 * q + 3 : 0])
-                                    : ar[2 * q + 1];
-          ta = fmax(ta, fmax(fmax(t4.x * a01.x, t4.y * a01.y), fmax(t4.z * a23.x, t4.w * a23.y)));
+          const float4 a4 = kRegW ? make_float4(areg[kRegW ? 4 * q : 0], areg[kRegW ? 4 * q + 1 : 0],
+                                                areg[kRegW ? 4 * q + 2 : 0], areg[kRegW ? 4 * q + 3 : 0])
+                                  : ar[q];
+          taf = fmaxf(taf, fmaxf(fmaxf(__fmul_ru(t4.x, a4.x), __fmul_ru(t4.y, a4.y)),
+                                 fmaxf(__fmul_ru(t4.z, a4.z), __fmul_ru(t4.w, a4.w))));
         }
+        const double ta = taf;
         const float4 d4 = rec[kTmaxSub / 4];
         const double2 d0 = make_double2(d4.x, d4.y);
         const double thr = lim - lrb;
@@ -449,7 +455,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
   __shared__ CtaWork w;
   __shared__ int r_s;
   __shared__ __align__(16) double rmax_s[kWarps * kStride];
-  __shared__ __align__(16) double amax_s[kWarps * kTmaxSub];
+  __shared__ __align__(16) float amax_s[kWarps * kTmaxSub];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* smem = reinterpret_cast<double*>(smem_raw + 128);
   const int per_sb = gblock * ntiles;
@@ -486,7 +492,7 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep_hi(DevGrid g, Batch b, in
   __shared__ CtaWork w;
   __shared__ int r_s;
   __shared__ __align__(16) double rmax_s[kWarps * kStride];
-  __shared__ __align__(16) double amax_s[kWarps * kTmaxSub];
+  __shared__ __align__(16) float amax_s[kWarps * kTmaxSub];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* smem = reinterpret_cast<double*>(smem_raw + 128);
   const int gbeg = b.wl_group0[kFastRank + 1], gend = b.wl_group0[kSweepRank + 1];
