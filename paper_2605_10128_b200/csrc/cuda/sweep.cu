@@ -316,7 +316,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
         const float4* rec = reinterpret_cast<const float4*>(st + Rg::T + Rg::F + Rg::L) + (h * kChunk + lane) * (kRec / 4);
         const double2* fr = reinterpret_cast<const double2*>(sF + lane * S);
         const double2* wr = reinterpret_cast<const double2*>(rms);
-        double lrb = 0.0, fc = 0.0, flo = 0.0;
+        double l0 = 0.0, l1 = 0.0, fc = 0.0, flo = 0.0;  // two accumulators: half the dependent chain
         if (TM == kTmMask) {
           // rows [key(max_t f_c), key(min_t f_c), L_0..L_{R-1}]; rms slot 1 + q weighs L_q
           const unsigned long long* kr = reinterpret_cast<const unsigned long long*>(fr);
@@ -324,18 +324,24 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
           flo = order_value(kr[1]);
           const double* l = reinterpret_cast<const double*>(fr) + 2;
 #pragma unroll
-          for (int q = 0; q < R; ++q) lrb = fma(fabs(l[q]), rms[1 + q], lrb);
+          for (int q = 0; q < R; ++q) {
+            if (q & 1)
+              l1 = fma(fabs(l[q]), rms[1 + q], l1);
+            else
+              l0 = fma(fabs(l[q]), rms[1 + q], l0);
+          }
         } else {
 #pragma unroll
           for (int q = 0; q < S / 2; ++q) {
             const double2 p2 = fr[q];
             const double2 w2 = kRegW ? make_double2(wreg[kRegW ? 2 * q : 0], wreg[kRegW ? 2 * q + 1 : 0]) : wr[q];
-            lrb = fma(fabs(p2.x), w2.x, lrb);
-            lrb = fma(fabs(p2.y), w2.y, lrb);
+            l0 = fma(fabs(p2.x), w2.x, l0);
+            l1 = fma(fabs(p2.y), w2.y, l1);
             if (q == 0) fc = p2.x;
           }
           flo = fc;
         }
+        const double lrb = l0 + l1;
         // max_s Tmax_s * delta_s in FP32 rounded up (both factors are
         // non-negative upper bounds already rounded up to float)
         const float4* ar = reinterpret_cast<const float4*>(asub);
@@ -349,14 +355,19 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
           taf = fmaxf(taf, fmaxf(fmaxf(__fmul_ru(t4.x, a4.x), __fmul_ru(t4.y, a4.y)),
                                  fmaxf(__fmul_ru(t4.z, a4.z), __fmul_ru(t4.w, a4.w))));
         }
-        const double ta = taf;
         const float4 d4 = rec[kTmaxSub / 4];
         const double2 d0 = make_double2(d4.x, d4.y);
         const double thr = lim - lrb;
         thr_lane = thr > 0.0 ? hi_abs(thr) : 0u;
-        const double wd = ta + lrb;
-        const double slack = 1e-12 * (fmax(fabs(fc), fabs(flo)) + fmax(d0.x, -d0.y) + wd);
-        hot = (fc + d0.x + wd + slack >= lim) || (flo + d0.y - wd - slack <= -lim);
+        // some |f1| of the tile can reach lim only if
+        //   fc + D0max + w + slack >= lim  or  flo + D0min - w - slack <= -lim,
+        // i.e. w (1 + 1e-12) + s0 >= lim - max(fc + D0max, -(flo + D0min)), with
+        // slack = 1e-12 (max(|fc|, |flo|) + |D0max| + |D0min| + w); the gap and
+        // s0 do not depend on w (short dependent chain)
+        const double gap = lim - fmax(fc + d0.x, -(flo + d0.y));
+        const double s0 = 1e-12 * (fmax(fabs(fc), fabs(flo)) + fabs(d0.x) + fabs(d0.y));
+        const double wd = static_cast<double>(taf) + lrb;
+        hot = fma(wd, 1.0 + 1e-12, s0) >= gap;
       }
       unsigned need = __ballot_sync(0xffffffffu, hot);
       rows_partial += __popc(need);
