@@ -10,7 +10,8 @@ import ctypes as C
 import os
 
 _HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_HERE, "_lib", "libtopopt_b200.so")
+# TGB_LIB_PATH: an alternative build of the same library (A/B timing of kernel variants)
+LIB_PATH = os.environ.get("TGB_LIB_PATH") or os.path.join(_HERE, "_lib", "libtopopt_b200.so")
 
 i32p = C.POINTER(C.c_int32)
 i64p = C.POINTER(C.c_int64)
