@@ -23,8 +23,8 @@ constexpr int kMaxTerms = 512;     // sparse coefficients over all Z columns
 constexpr int kMaxPMod = 16;       // omitted injections (p modifications)
 constexpr int kMaxInjMoved = 64;   // injections moved to new nodes
 constexpr int kTmaxSub = 8;        // sub-tiles of a sweep tile carrying their own max |T_base| per row
-constexpr int kRec = kTmaxSub + 4; // floats per (tile, row) skip record: kTmaxSub sub-tile maxima of |T_base| (rounded
-                                   // up), max (rounded up) / min (rounded down) of T_base*alpha0, 2 pad (48 B)
+constexpr int kRec = kTmaxSub + 4; // floats per (tile, row) skip record: kTmaxSub sub-tile maxima of |T_base| (float,
+                                   // rounded up), then max / min of T_base*alpha0 as two doubles (48 B)
 
 // Flat, read-only network tables on the device (built once per context by
 // engine_setup.cu from the host Grid/ActionTable).

@@ -144,10 +144,7 @@ __global__ void k_tmax(DevGrid g, const double* tk, const double* alpha0, float*
       }
       rec[s] = __double2float_ru(m);  // rounded up: the bound stays rigorous
     }
-    rec[kTmaxSub] = __double2float_ru(dmax);
-    rec[kTmaxSub + 1] = __double2float_rd(dmin);
-    rec[kTmaxSub + 2] = 0.f;
-    rec[kTmaxSub + 3] = 0.f;
+    *reinterpret_cast<double2*>(rec + kTmaxSub) = make_double2(dmax, dmin);  // exact (read as FP64)
   }
 }
 
@@ -160,16 +157,13 @@ __global__ void k_rec_combine(const float* recs, size_t rec_floats, int n_t, flo
     const float* r0 = recs + i * kRec;
     float* o = out + i * kRec;
     for (int j = 0; j < kTmaxSub; ++j) o[j] = r0[j];
-    float hi = r0[kTmaxSub], lo = r0[kTmaxSub + 1];
+    double2 d = *reinterpret_cast<const double2*>(r0 + kTmaxSub);
     for (int t = 1; t < n_t; ++t) {
-      const float* r = recs + static_cast<size_t>(t) * rec_floats + i * kRec;
-      hi = fmaxf(hi, r[kTmaxSub]);
-      lo = fminf(lo, r[kTmaxSub + 1]);
+      const double2 dt = *reinterpret_cast<const double2*>(recs + static_cast<size_t>(t) * rec_floats + i * kRec + kTmaxSub);
+      d.x = fmax(d.x, dt.x);
+      d.y = fmin(d.y, dt.y);
     }
-    o[kTmaxSub] = hi;
-    o[kTmaxSub + 1] = lo;
-    o[kTmaxSub + 2] = 0.f;
-    o[kTmaxSub + 3] = 0.f;
+    *reinterpret_cast<double2*>(o + kTmaxSub) = d;
   }
 }
 

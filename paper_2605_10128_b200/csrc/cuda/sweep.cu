@@ -18,7 +18,7 @@
 // rows are streamed in stages of 1-4 chunks of 32 by TMA bulk copies
 // (cp.async.bulk + mbarrier complete_tx) into a 2-8 stage ring: the group's
 // candidate rows, the limits and the per-(tile, row) skip record (sub-tile max
-// |T_base|, extrema of T_base * alpha0, float4 with directed rounding); warps
+// |T_base| as floats rounded up, extrema of T_base * alpha0 as doubles); warps
 // release a stage on its empty mbarrier and thread 0 refills it. T_base itself
 // is NOT streamed:
 //   stage 1 (one lane per row, no element work): a rigorous bound of |f1|
@@ -355,8 +355,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
           taf = fmaxf(taf, fmaxf(fmaxf(__fmul_ru(t4.x, a4.x), __fmul_ru(t4.y, a4.y)),
                                  fmaxf(__fmul_ru(t4.z, a4.z), __fmul_ru(t4.w, a4.w))));
         }
-        const float4 d4 = rec[kTmaxSub / 4];
-        const double2 d0 = make_double2(d4.x, d4.y);
+        const double2 d0 = reinterpret_cast<const double2*>(rec)[kTmaxSub / 4];
         const double thr = lim - lrb;
         thr_lane = thr > 0.0 ? hi_abs(thr) : 0u;
         // some |f1| of the tile can reach lim only if
