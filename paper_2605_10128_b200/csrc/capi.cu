@@ -368,7 +368,7 @@ void tg_context::ensure_capacity(int n) {
     size_t free_b = 0, total_b = 0;
     cudaMemGetInfo(&free_b, &total_b);
     static const bool mt_disabled = std::getenv("TGB_NO_MT_SCREEN") != nullptr;  // A/B switch
-    mt_ok = mt_pattern_ok && !mt_disabled && need < free_b / 2;
+    mt_ok = mt_pattern_ok && !mt_disabled && need < free_b / 2 && tgb::masked_sweep_fits(g.E);
     if (mt_ok) {
       mt_feat_sz = feat_sz;
       mt_kdat_sz = kdat_sz;

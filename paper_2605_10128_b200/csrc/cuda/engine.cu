@@ -14,6 +14,7 @@ namespace tgb {
 namespace {
 
 constexpr int kPrepThreads = 256;
+constexpr int kPrepCta = 512;  // k_prep block size (a multiple of 128: the timestep bound folds)
 constexpr size_t kPrepZsmBytes = 0;  // Z = X [U | V] kept in shared memory up to this size
 
 // ---------------------------------------------------------------- K2a analysis
@@ -53,7 +54,7 @@ __global__ void __launch_bounds__(kAnalyzeThreads) k_analyze(DevGrid g, Batch b,
 // shared memory (row stride row_stride(r)) when it fits in `zsm_doubles`, else
 // in the CTA's global scratch slot.
 template <bool LITE>  // LITE: a later injection profile reusing the first profile's factors and rows
-__global__ void __launch_bounds__(kPrepThreads) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch,
+__global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch,
                                                        int zslots, int zsm_doubles) {
   extern __shared__ __align__(16) uint32_t bits[];
   __shared__ Topo t;
@@ -701,10 +702,10 @@ int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch&
                          static_cast<int>(bits_al + zsm_bytes));
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
   if (b.prep_lite)
-    k_prep<true><<<prep_grid, kPrepThreads, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
+    k_prep<true><<<prep_grid, kPrepCta, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
                                                                            zsm_doubles);
   else
-    k_prep<false><<<prep_grid, kPrepThreads, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
+    k_prep<false><<<prep_grid, kPrepCta, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
                                                                             zsm_doubles);
   return 1;
 }

@@ -132,6 +132,7 @@ int launch_accumulate_timestep(const Batch& bt, Scores& agg, double* agg_energy,
 int launch_finish_aggregate(Batch& b, int Kall, cudaStream_t stream);
 int sweep_tile_k();
 int sweep_chunk();
+bool masked_sweep_fits(int E);  // k_sweep_masked's shared-memory plan holds for E rows
 void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1,
                   int* launched);
 // Rank buckets -> sweep groups; assigns every swept candidate its row slot.

@@ -528,14 +528,44 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep_hi(DevGrid g, Batch b, in
 static_assert(kSweepRank == 11 && kFastRank == 7, "k_sweep / k_sweep_hi rank switches");
 
 // Masked sweep of one injection profile (multi-timestep screening,
-// Batch::t_mode 2): no staging ring; each warp visits only the rows its
-// candidate's all-profile mask marks for this tile (a few percent) and gathers
-// their candidate row and T_base row from L2, NB rows at a time.
+// Batch::t_mode 2): each warp visits only the rows its candidate's all-profile
+// mask marks for this tile (a few percent). The CTA's 16 masks are OR-ed into
+// one union row list (rows hot for one candidate tend to be hot for many:
+// ~8x fewer rows than the sum at cfg3); the T_base rows of the union are
+// staged once per CTA by TMA bulk copies (1 KB per row) into a ring of
+// 32-row batches, and each warp gathers only its own marked candidate rows.
+constexpr int kMaskBatch = 32;                               // union rows per ring stage
+constexpr size_t kMaskStageBytes = kMaskBatch * kTileK * 8;  // T_base rows of one stage
+constexpr int kMaskMaxStages = 4;
+
+// shared-memory plan of k_sweep_masked for E rows at row stride S
+struct MaskedPlan {
+  size_t su, ul, scr, ring;  // byte offsets: union words, union rows, per-warp row scratch, ring
+  int stages;
+};
+__host__ __device__ inline MaskedPlan masked_plan(int E, int S) {
+  MaskedPlan p;
+  const int nch = (E + kChunk - 1) / kChunk;
+  p.su = 0;
+  p.ul = (static_cast<size_t>(nch) * 4 + 15) & ~size_t{15};
+  p.scr = (p.ul + static_cast<size_t>(E) * 4 + 15) & ~size_t{15};
+  p.ring = (p.scr + static_cast<size_t>(kWarps) * 32 * S * 8 + 127) & ~size_t{127};
+  const size_t left = kStageBudget > p.ring ? kStageBudget - p.ring : 0;
+  const size_t st = left / kMaskStageBytes;
+  p.stages = static_cast<int>(st < kMaskMaxStages ? st : kMaskMaxStages);
+  return p;
+}
+
 template <int R>
-__device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile) {
+__device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile,
+                                           uint8_t* smem, uint64_t* full_bar, uint64_t* empty_bar, int nunion) {
   constexpr int S = row_stride(R);
-  constexpr int NB = R <= 3 ? 4 : (R <= 5 ? 2 : 1);
+  const MaskedPlan plan = masked_plan(g.E, S);
+  const int NST = plan.stages;
+  const int* ul = reinterpret_cast<const int*>(smem + plan.ul);
+  const double* ring = reinterpret_cast<const double*>(smem + plan.ring);
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  double* scr = reinterpret_cast<double*>(smem + plan.scr) + static_cast<size_t>(warp) * 32 * S;
   const int kb = tile * kTileK + lane * kKpl;
   double alpha[kKpl], rr[kKpl][R > 0 ? R : 1], energy[kKpl];
   bool kval[kKpl];
@@ -558,76 +588,106 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
 #pragma unroll
     for (int q = 0; q < kMaxRemovedSweep; ++q) rem[q] = b.removed[static_cast<size_t>(c) * kMaxRemovedSweep + q];
   }
-  if (cid >= 0) {
-    const int ntiles = g.Kpad / kTileK;
-    const uint32_t* mw = b.mask + (static_cast<size_t>(cid) * ntiles + tile) * b.nchunks;
-    const size_t slot = static_cast<size_t>(w.group) * kGroupSlots + warp;
-    unsigned long long* fmx = b.fmax + static_cast<size_t>(cid) * g.E;
-    int pend[NB];
-    int np = 0;
-    // one batch of up to NB marked rows: loads first, then the arithmetic
-    auto flush = [&]() {
-      double2 t[NB][2];
-      double frow[NB][S];
-      double lim[NB];
+  const int ntiles = g.Kpad / kTileK;
+  const uint32_t* mw = b.mask + (static_cast<size_t>(cid >= 0 ? cid : 0) * ntiles + tile) * b.nchunks;
+  const size_t slot = static_cast<size_t>(w.group) * kGroupSlots + warp;
+  unsigned long long* fmx = b.fmax + static_cast<size_t>(cid >= 0 ? cid : 0) * g.E;
+  const double* tk_tile = g.TK + static_cast<size_t>(tile) * g.E * kTileK;
+  const int nb = (nunion + kMaskBatch - 1) / kMaskBatch;
+  auto issue = [&](int j) {
+    const int s = j % NST, r0 = j * kMaskBatch, nr = min(kMaskBatch, nunion - r0);
+    uint64_t* bar = full_bar + s;
+    mbar_expect_tx(bar, static_cast<uint32_t>(nr * kTileK * 8));
+    double* dst = const_cast<double*>(ring) + static_cast<size_t>(s) * kMaskBatch * kTileK;
+    for (int r = 0; r < nr; ++r)
+      bulk_g2s(dst + r * kTileK, tk_tile + static_cast<size_t>(ul[r0 + r]) * kTileK, kTileK * 8, bar);
+  };
+  if (threadIdx.x == 0)
+    for (int j = 0; j < NST && j < nb; ++j) issue(j);
+  // this lane's union row of batch j: own mask bit, candidate row and limit,
+  // gathered one batch ahead (registers) while the current batch computes
+  int e_n = -1;
+  bool marked_n = false;
+  double lim_n = 0.0;
+  double2 fr_n[S / 2];
+  auto gather = [&](int j) {
+    const int idx = j * kMaskBatch + lane;
+    e_n = j < nb && idx < nunion ? ul[idx] : -1;
+    marked_n = e_n >= 0 && cid >= 0 && ((mw[e_n >> 5] >> (e_n & 31)) & 1u);
+    if (marked_n) {
+      const double2* fr = reinterpret_cast<const double2*>(b.feat + feat_index(static_cast<int>(slot), b.nchunks, e_n, R));
 #pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        const int e = u < np ? pend[u] : pend[0];
-        const double2* src = reinterpret_cast<const double2*>(g.TK + (static_cast<size_t>(tile) * g.E + e) * kTileK +
-                                                              lane * kKpl);
-        t[u][0] = __ldg(src);
-        t[u][1] = __ldg(src + 1);
-        const double* fr = b.feat + feat_index(static_cast<int>(slot), b.nchunks, e, R);
-#pragma unroll
-        for (int q = 0; q < S; ++q) frow[u][q] = fr[q];
-        lim[u] = g.br_lim[e];
-      }
-#pragma unroll
-      for (int u = 0; u < NB; ++u) {
-        if (u >= np) break;
-        const int e = pend[u];
-        const double tv[kKpl] = {t[u][0].x, t[u][0].y, t[u][1].x, t[u][1].y};
-        double f1[kKpl];
-        uint32_t mx = 0u;
-#pragma unroll
-        for (int k = 0; k < kKpl; ++k) {
-          double acc = fma(tv[k], alpha[k], frow[u][0]);
-#pragma unroll
-          for (int q = 0; q < R; ++q) acc = fma(frow[u][1 + q], rr[k][q], acc);
-          f1[k] = acc;
-          mx = max(mx, hi_abs(acc));
-        }
-        if (!__any_sync(0xffffffffu, mx >= hi_abs(lim[u]))) continue;
-        bool skip_row = false;
-#pragma unroll
-        for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[q];
-        unsigned long long m = 0ull;
-#pragma unroll
-        for (int k = 0; k < kKpl; ++k) {
-          if (!kval[k] || skip_row || e == kbr[k]) continue;
-          const double a = fabs(f1[k]);
-          if (a > lim[u]) energy[k] += a - lim[u];
-          m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
-        }
-        if (m > static_cast<unsigned long long>(__double_as_longlong(lim[u]))) atomicMax(fmx + e, m);
-      }
-      np = 0;
-    };
-    for (int c0 = 0; c0 < b.nchunks; c0 += 32) {
-      const unsigned mine = c0 + lane < b.nchunks ? mw[c0 + lane] : 0u;
-      unsigned nz = __ballot_sync(0xffffffffu, mine != 0u);
-      while (nz) {
-        const int j = __ffs(nz) - 1;
-        nz &= nz - 1;
-        unsigned word = __shfl_sync(0xffffffffu, mine, j);
-        while (word) {
-          pend[np++] = (c0 + j) * kChunk + __ffs(word) - 1;
-          word &= word - 1;
-          if (np == NB) flush();
-        }
-      }
+      for (int q = 0; q < S / 2; ++q) fr_n[q] = fr[q];
+      lim_n = g.br_lim[e_n];
     }
-    if (np) flush();
+  };
+  gather(0);
+  for (int j = 0; j < nb; ++j) {
+    const int s = j % NST;
+    const int e_l = e_n;
+    const bool marked = marked_n;
+    const double lim_l = lim_n;
+    if (marked) {
+      double2* dst = reinterpret_cast<double2*>(scr + lane * S);
+#pragma unroll
+      for (int q = 0; q < S / 2; ++q) dst[q] = fr_n[q];
+    }
+    __syncwarp();
+    gather(j + 1);
+    unsigned need = __ballot_sync(0xffffffffu, marked);
+    mbar_wait(full_bar + s, (j / NST) & 1);
+    const double* st = ring + static_cast<size_t>(s) * kMaskBatch * kTileK + lane * kKpl;
+    while (need) {
+      const int u = __ffs(need) - 1;
+      need &= need - 1;
+      const int e = __shfl_sync(0xffffffffu, e_l, u);
+      const double lim = __shfl_sync(0xffffffffu, lim_l, u);
+      const double2 t01 = *reinterpret_cast<const double2*>(st + u * kTileK);
+      const double2 t23 = *reinterpret_cast<const double2*>(st + u * kTileK + 2);
+      const double tv[kKpl] = {t01.x, t01.y, t23.x, t23.y};
+      const double* frow = scr + u * S;
+      double fl[S];
+#pragma unroll
+      for (int q = 0; q < S / 2; ++q) {
+        const double2 v = reinterpret_cast<const double2*>(frow)[q];
+        fl[2 * q] = v.x;
+        fl[2 * q + 1] = v.y;
+      }
+      double f1[kKpl];
+      uint32_t mx = 0u;
+#pragma unroll
+      for (int k = 0; k < kKpl; ++k) {
+        double acc = fma(tv[k], alpha[k], fl[0]);
+#pragma unroll
+        for (int q = 0; q < R; ++q) acc = fma(fl[1 + q], rr[k][q], acc);
+        f1[k] = acc;
+        mx = max(mx, hi_abs(acc));
+      }
+      if (!__any_sync(0xffffffffu, mx >= hi_abs(lim))) continue;
+      bool skip_row = false;
+#pragma unroll
+      for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[q];
+      unsigned long long m = 0ull;
+#pragma unroll
+      for (int k = 0; k < kKpl; ++k) {
+        if (!kval[k] || skip_row || e == kbr[k]) continue;
+        const double a = fabs(f1[k]);
+        if (a > lim) energy[k] += a - lim;
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+      }
+      if (m > static_cast<unsigned long long>(__double_as_longlong(lim))) atomicMax(fmx + e, m);
+    }
+    // release the stage; thread 0 refills it once every warp has left it
+    __syncwarp();
+    if (lane == 0) mbar_arrive(empty_bar + s);
+    if (threadIdx.x == 0 && j + NST < nb) {
+      mbar_wait(empty_bar + s, (j / NST) & 1);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(j + NST);
+    }
+    __syncwarp();
+  }
+  if (cid >= 0) {
     double* en = b.energy + static_cast<size_t>(cid) * g.Kall;
 #pragma unroll
     for (int k = 0; k < kKpl; ++k)
@@ -636,13 +696,17 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
 }
 
 template <int R>
-__device__ __noinline__ void masked_cta_call(const DevGrid& g, const Batch& b, const CtaWork& w, int tile) {
-  masked_cta<R>(g, b, w, tile);
+__device__ __noinline__ void masked_cta_call(const DevGrid& g, const Batch& b, const CtaWork& w, int tile,
+                                             uint8_t* smem, uint64_t* full_bar, uint64_t* empty_bar, int nunion) {
+  masked_cta<R>(g, b, w, tile, smem, full_bar, empty_bar, nunion);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_sweep_masked(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
+  extern __shared__ __align__(128) uint8_t msm[];
   __shared__ CtaWork w;
-  __shared__ int r_s;
+  __shared__ int r_s, nunion_s;
+  __shared__ int wsum[kWarps];
+  __shared__ __align__(8) uint64_t bars[2 * kMaskMaxStages];
   const int per_sb = gblock * ntiles;
   const int sb = static_cast<int>(blockIdx.x) / per_sb, rr = static_cast<int>(blockIdx.x) % per_sb;
   const int g0 = sb * gblock, gg = min(gblock, ngroups - g0);
@@ -659,22 +723,75 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep_masked(DevGrid g, Batch b
       if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
     w.ncand = n;
     w.group = group;
+    for (int s = 0; s < kMaskMaxStages; ++s) {
+      mbar_init(bars + s, 1);
+      mbar_init(bars + kMaskMaxStages + s, kWarps);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  // union of the CTA's masks for this tile, then the union row list
+  const int nch = b.nchunks;
+  uint32_t* su = reinterpret_cast<uint32_t*>(msm);
+  for (int c = threadIdx.x; c < nch; c += blockDim.x) su[c] = 0u;
+  __syncthreads();
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  {
+    int cid = warp < w.ncand ? w.cand[warp] : -1;
+    if (cid >= 0 && b.status[cid] != 0) cid = -1;
+    if (cid >= 0) {
+      const uint32_t* mw = b.mask + (static_cast<size_t>(cid) * ntiles + tile) * nch;
+      for (int c = lane; c < nch; c += 32) {
+        const uint32_t v = mw[c];
+        if (v) atomicOr(su + c, v);
+      }
+    }
   }
   __syncthreads();
+  // block-wide exclusive scan of the per-thread row counts (contiguous word ranges)
+  const int per_t = (nch + blockDim.x - 1) / blockDim.x;
+  const int c_lo = min(nch, static_cast<int>(threadIdx.x) * per_t), c_hi = min(nch, c_lo + per_t);
+  int cnt = 0;
+  for (int c = c_lo; c < c_hi; ++c) cnt += __popc(su[c]);
+  int incl = cnt;
+#pragma unroll
+  for (int o = 1; o < 32; o <<= 1) {
+    const int v = __shfl_up_sync(0xffffffffu, incl, o);
+    if (lane >= o) incl += v;
+  }
+  if (lane == 31) wsum[warp] = incl;
+  __syncthreads();
+  int base = 0;
+  for (int i = 0; i < warp; ++i) base += wsum[i];
+  if (threadIdx.x == blockDim.x - 1) nunion_s = base + incl;
+  const int S = row_stride(r_s);
+  int* ul = reinterpret_cast<int*>(msm + masked_plan(g.E, S).ul);
+  int pos = base + incl - cnt;
+  for (int c = c_lo; c < c_hi; ++c) {
+    uint32_t v = su[c];
+    while (v) {
+      ul[pos++] = c * kChunk + __ffs(v) - 1;
+      v &= v - 1;
+    }
+  }
+  __syncthreads();
+  uint8_t* sm = msm;
+  uint64_t* fb = bars;
+  uint64_t* eb = bars + kMaskMaxStages;
+  const int nu = nunion_s;
   switch (r_s) {
-    case 0: masked_cta<0>(g, b, w, tile); break;
-    case 1: masked_cta<1>(g, b, w, tile); break;
-    case 2: masked_cta<2>(g, b, w, tile); break;
-    case 3: masked_cta<3>(g, b, w, tile); break;
-    case 4: masked_cta<4>(g, b, w, tile); break;
-    case 5: masked_cta<5>(g, b, w, tile); break;
+    case 0: masked_cta<0>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 1: masked_cta<1>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 2: masked_cta<2>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 3: masked_cta<3>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 4: masked_cta<4>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 5: masked_cta<5>(g, b, w, tile, sm, fb, eb, nu); break;
     // higher ranks in their own call frames (register pressure of the common ones)
-    case 6: masked_cta_call<6>(g, b, w, tile); break;
-    case 7: masked_cta_call<7>(g, b, w, tile); break;
-    case 8: masked_cta_call<8>(g, b, w, tile); break;
-    case 9: masked_cta_call<9>(g, b, w, tile); break;
-    case 10: masked_cta_call<10>(g, b, w, tile); break;
-    default: masked_cta_call<11>(g, b, w, tile); break;
+    case 6: masked_cta_call<6>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 7: masked_cta_call<7>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 8: masked_cta_call<8>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 9: masked_cta_call<9>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 10: masked_cta_call<10>(g, b, w, tile, sm, fb, eb, nu); break;
+    default: masked_cta_call<11>(g, b, w, tile, sm, fb, eb, nu); break;
   }
 }
 
@@ -723,6 +840,8 @@ __global__ void k_bucket(Batch b) {
 }  // namespace
 
 int sweep_tile_k() { return kTileK; }
+// the masked timestep sweep needs two ring stages next to its row lists
+bool masked_sweep_fits(int E) { return masked_plan(E, kStride).stages >= 2; }
 int sweep_chunk() { return kChunk; }
 
 void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1,
@@ -736,6 +855,7 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     cudaFuncSetAttribute(k_sweep_hi<true, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmMask>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep_masked, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStageBudget));
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
   static const int gblock_env = [] {
@@ -754,7 +874,7 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     k_sweep<false, kTmMask><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
     k_sweep_hi<false, kTmMask><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
   } else if (b.t_mode == kTmMasked) {
-    k_sweep_masked<<<grid, kThreads, 0, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_masked<<<grid, kThreads, kStageBudget, stream>>>(g, b, ntiles, ngroups, gblock);
   } else {
     k_sweep<false, kTmSingle><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
     k_sweep_hi<false, kTmSingle><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);

@@ -1,0 +1,13 @@
+"""One MapElites generation inside cudaProfilerStart/Stop (ncu --profile-from-start off)."""
+import sys
+sys.path.insert(0, ".")
+import torch
+import paper_2605_10128_b200 as P
+from tools.synth_grid import config_json
+cfg = sys.argv[1]; B = int(sys.argv[2])
+g = P.grid_from_json_text(config_json(cfg)); ctx = P.DcContext(g, P.build_action_set(g))
+sess = P.QdSession(ctx, P.QdConfig(batch_size=B, iters_per_epoch=1 << 30))
+sess.step(2); torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStart()
+sess.step(1); torch.cuda.synchronize()
+torch.cuda.cudart().cudaProfilerStop()
