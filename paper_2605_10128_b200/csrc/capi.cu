@@ -233,6 +233,7 @@ struct tg_context {
   // profile's candidate rows
   bool mt_ok = false;
   bool mt_pattern_ok = false;  // injection zero pattern identical across profiles
+  tgb::MtProfiles mt_prof{};   // per-profile table pointers (device arrays)
   tgb::DevGrid g_mt{};          // t = 0 view with the all-profile skip records
   double* mt_feat = nullptr;    // [n_t] candidate branch rows
   double* mt_kdat = nullptr;    // [n_t] contingency rows
@@ -458,9 +459,16 @@ int tg_context::enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed
   check(cudaMemsetAsync(bv.amx_mt, 0, static_cast<size_t>(n) * ntiles * tgb::kTmaxSub * 8, stream), "memset");
   check(cudaMemsetAsync(bv.rmx_mt, 0, static_cast<size_t>(n) * ntiles * tgb::kStride * 8, stream), "memset");
   check(cudaMemsetAsync(mt_energy, 0, static_cast<size_t>(n_t) * n * Ka * sizeof(double), stream), "memset");
-  for (int t = 0; t < n_t; ++t) {
-    tgb::Batch bt = view(t);
-    kernels += tgb::launch_prep(gt[t], bt, n_a, n_d, scratch, stream);
+  {
+    // profile 0 (factors, L rows, bounds), then every later profile in one pass
+    tgb::Batch b0p = view(0);
+    kernels += tgb::launch_prep(gt[0], b0p, n_a, n_d, scratch, stream);
+    tgb::MtProfiles P = mt_prof;
+    P.feat_stride = mt_feat_sz;
+    P.kdat_stride = mt_kdat_sz;
+    P.energy_stride = static_cast<size_t>(n) * Ka;
+    P.nc0_stride = static_cast<size_t>(n);
+    kernels += tgb::launch_prep_mt(g, b0p, P, stream);
   }
   tgb::Batch bm = view(0);
   bm.t_mode = 1;
@@ -839,6 +847,21 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     }
     g = ctx->gt[0];
     ctx->g_mt = g;
+    {
+      // per-profile table pointers for k_prep_mt
+      std::vector<const double*> f0p, thp, injp, a0p;
+      for (const auto& gv : ctx->gt) {
+        f0p.push_back(gv.f0);
+        thp.push_back(gv.theta0);
+        injp.push_back(gv.inj_net);
+        a0p.push_back(gv.alpha0);
+      }
+      ctx->mt_prof.f0 = A.upload(f0p, s);
+      ctx->mt_prof.theta0 = A.upload(thp, s);
+      ctx->mt_prof.inj_net = A.upload(injp, s);
+      ctx->mt_prof.alpha0 = A.upload(a0p, s);
+      ctx->mt_prof.n_t = T;
+    }
     if (T > 1) {
       float* rec_mt = A.alloc<float>(tmax_n);
       tgb::launch_rec_combine(tmax_all, tmax_n, T, rec_mt, s);

@@ -250,6 +250,175 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
   }
 }
 
+// ---------------------------------------------------------------- K2b prep, profiles 1..n_t-1
+// Multi-timestep screening (capi.cu enqueue_evaluate_mt): the topology factors
+// and the L rows are profile-independent, only f_c and alpha change with the
+// injections. One CTA per candidate computes every later profile's rows in one
+// pass: the per-profile small right-hand sides in parallel (one thread per
+// profile), then each thread reads its branch's L row once (profile 0, written
+// by k_prep) and emits f_c for all profiles; the bounds of the mask pass are
+// folded over the profiles in registers (no per-profile atomics).
+__global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProfiles P) {
+  extern __shared__ __align__(16) uint32_t bits[];
+  __shared__ Topo t;
+  constexpr int kRp = kMaxSplits + kMaxCols;
+  const int words = (g.E + 31) >> 5;
+  uint32_t* rm_bits = bits + words;
+  double* rp_all = reinterpret_cast<double*>(bits + ((2 * words + 3) & ~3));
+  int* nc0_s = reinterpret_cast<int*>(rp_all + static_cast<size_t>(P.n_t) * kRp);
+  const int lane = threadIdx.x & 31;
+  const int ntiles = g.Kpad / 128;
+  for (int c = blockIdx.x; c < b.n; c += gridDim.x) {
+    const int slot = b.slot[c];
+    if (slot < 0 || b.status[c] != 0) continue;  // islanded (analysis or profile 0's small solve)
+    copy_block(static_cast<TopoCore*>(&t), b.topo + c, sizeof(TopoCore), threadIdx.x, blockDim.x);
+    const uint32_t* tb = b.tbits + static_cast<size_t>(c) * 2 * words;
+    for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = tb[i];
+    copy_block(t.Sinv, b.topo_sol + static_cast<size_t>(c) * kTopoSol, kTopoSol * sizeof(double), threadIdx.x,
+               blockDim.x);
+    for (int i = threadIdx.x; i < P.n_t; i += blockDim.x) nc0_s[i] = 0;
+    __syncthreads();
+    const int ns = t.ns, nv = t.nv, r = ns + nv, rs = row_stride(r);
+    // injection side of the small solve, one thread per profile
+    for (int tt = 1 + threadIdx.x; tt < P.n_t; tt += blockDim.x) {
+      double ppsi[kMaxSplits], th[kMaxCols];
+      for (int q = 0; q < ns; ++q) ppsi[q] = 0.0;
+      for (int i = 0; i < t.ninj; ++i) {
+        const int q = t.q_of_new[t.inj_new[i]];
+        if (q >= 0 && !omitted(t, t.inj_id[i])) ppsi[q] += P.inj_net[tt][t.inj_id[i]];
+      }
+      const double* th0 = P.theta0[tt];
+      for (int cc = 0; cc < r; ++cc) {
+        double acc = 0.0;
+        for (int p = t.col_ptr[cc]; p < t.col_ptr[cc + 1]; ++p) acc = fma(t.term_coef[p], th0[t.term_idx[p]], acc);
+        th[cc] = acc;
+      }
+      small_rhs_into(t, th, ppsi, rp_all + static_cast<size_t>(tt) * kRp);
+    }
+    __syncthreads();
+    // branch rows of every later profile from the L row of profile 0
+    const int e_end = (g.E + 31) & ~31;
+    for (int e0 = threadIdx.x; e0 < e_end; e0 += blockDim.x) {
+      const int e = e0 < g.E ? e0 : g.E - 1;
+      const bool valid = e0 < g.E;
+      const size_t fi = feat_index(slot, b.nchunks, e, r);
+      const double* fr0 = b.feat + fi;
+      double row[kStride];
+#pragma unroll
+      for (int i = 0; i < kStride; ++i) row[i] = 0.0;
+      for (int i = 1; i < rs; ++i) row[i] = fr0[i];
+      const bool on = g.br_on[e] && !bit_get(rm_bits, e);
+      double phi[kMaxSplits], rho[kMaxCols];
+      const double be = g.br_b[e], ib = 1.0 / be;
+      for (int q = 0; q < ns; ++q) phi[q] = on ? row[1 + q] * ib : 0.0;
+      for (int m = 0; m < nv; ++m) rho[m] = on ? row[1 + ns + m] * ib : 0.0;
+      unsigned long long* mk = reinterpret_cast<unsigned long long*>(b.feat_mt + feat_index(slot, b.nchunks, e, r + 1));
+      unsigned long long kmax = 0ull, kmin = ~0ull;
+      const double lim = g.br_lim[e];
+      for (int tt = 1; tt < P.n_t; ++tt) {
+        const double* rp = rp_all + static_cast<size_t>(tt) * kRp;
+        double fc = 0.0;
+        if (on) {  // cand_flow (topo.cuh) with this profile's base flow and Rp
+          double acc = 0.0;
+          for (int q = 0; q < ns; ++q) acc = fma(phi[q], rp[q], acc);
+          for (int m = 0; m < nv; ++m) acc = fma(rho[m], rp[ns + m], acc);
+          fc = P.f0[tt][e] + be * acc;
+        }
+        const unsigned cnt = __popc(__ballot_sync(0xffffffffu, valid && fabs(fc) > lim));
+        if (lane == 0 && cnt) atomicAdd(nc0_s + tt, static_cast<int>(cnt));
+        if (valid) {
+          row[0] = fc;
+          const unsigned long long key = order_key(fc);
+          kmax = max(kmax, key);
+          kmin = min(kmin, key);
+          double2* dst = reinterpret_cast<double2*>(b.feat + static_cast<size_t>(tt) * P.feat_stride + fi);
+#pragma unroll
+          for (int i = 0; i < kStride / 2; ++i)
+            if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+        }
+      }
+      if (valid) {
+        mk[0] = max(mk[0], kmax);
+        mk[1] = min(mk[1], kmin);
+      }
+    }
+    __syncthreads();
+    if (threadIdx.x == 0)
+      for (int tt = 1; tt < P.n_t; ++tt) b.nc0[static_cast<size_t>(tt) * P.nc0_stride + c] = nc0_s[tt];
+    // contingency rows: the topology part once, alpha per profile
+    for (int k = threadIdx.x; k < g.Kpad; k += blockDim.x) {
+      double rk[kSweepRank];
+      double den = 1.0;
+      bool live = false;  // regular contingency with an active outaged branch
+      int beta = -1;
+      const uint8_t flag = b.kflag[static_cast<size_t>(c) * g.Kpad + k];  // topology-only, from profile 0
+      if (k < g.Ks && flag == 0) {
+        beta = g.ks_branch[k];
+        const bool on = g.br_on[beta] && !bit_get(rm_bits, beta);
+        if (on) {
+          const double* fr = b.feat + feat_index(slot, b.nchunks, beta, r);
+          const double ib = 1.0 / g.br_b[beta];
+          double phi[kMaxSplits], rho[kMaxCols];
+          for (int q = 0; q < ns; ++q) phi[q] = fr[1 + q] * ib;
+          for (int m = 0; m < nv; ++m) rho[m] = fr[1 + ns + m] * ib;
+          double lr = 0.0;
+          for (int q = 0; q < ns; ++q) {
+            double acc = 0.0;
+            for (int q2 = 0; q2 < ns; ++q2) acc += t.Sinv[q * kMaxSplits + q2] * phi[q2];
+            rk[q] = acc;
+            lr += phi[q] * acc;
+          }
+          for (int m = 0; m < nv; ++m) {
+            double acc = 0.0;
+            for (int m2 = 0; m2 < nv; ++m2) acc += t.Cinv[m * kMaxCols + m2] * rho[m2];
+            rk[ns + m] = -acc;
+            lr -= rho[m] * acc;
+          }
+          den = 1.0 - (g.Tdiag[beta] + g.br_b[beta] * lr);
+          live = !(fabs(den) < 1e-8);  // a bridge with flag 0 is a dead stub: flows unchanged
+        }
+      }
+      double dlmax = 0.0, rqmax[kSweepRank];
+      for (int q = 0; q < r; ++q) rqmax[q] = 0.0;
+      for (int tt = 1; tt < P.n_t; ++tt) {
+        double row[kStride];
+#pragma unroll
+        for (int i = 0; i < kStride; ++i) row[i] = 0.0;
+        if (live) {
+          const double fcb = b.feat[static_cast<size_t>(tt) * P.feat_stride + feat_index(slot, b.nchunks, beta, r)];
+          const double alpha = fcb / den;
+          row[0] = alpha;
+          for (int i = 0; i < r; ++i) row[1 + i] = rk[i] * alpha;
+        }
+        if (k < g.Ks && flag == 1)
+          b.energy[static_cast<size_t>(tt) * P.energy_stride + static_cast<size_t>(c) * g.Kall + g.ks_cont[k]] =
+              b.params.penalty;
+        double2* dst = reinterpret_cast<double2*>(b.kdat + static_cast<size_t>(tt) * P.kdat_stride +
+                                                  static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(k) * rs);
+#pragma unroll
+        for (int i = 0; i < kStride / 2; ++i)
+          if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+        dlmax = fmax(dlmax, fabs(row[0] - P.alpha0[tt][k]));
+        for (int q = 0; q < r; ++q) rqmax[q] = fmax(rqmax[q], fabs(row[1 + q]));
+      }
+      // fold into the bounds profile 0 wrote (tiles of 128: a warp is 32
+      // consecutive contingencies of one tile, half a warp one sub-tile)
+      const int tile = k >> 7, sub = (k & 127) >> 4;
+#pragma unroll
+      for (int o = 8; o > 0; o >>= 1) dlmax = fmax(dlmax, __shfl_xor_sync(0xffffffffu, dlmax, o));
+      if ((threadIdx.x & 15) == 0)
+        atomicMax(b.amx_mt + (static_cast<size_t>(c) * ntiles + tile) * kTmaxSub + sub, dbits(dlmax));
+      for (int q = 0; q < r; ++q) {
+        double rq = rqmax[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) rq = fmax(rq, __shfl_xor_sync(0xffffffffu, rq, o));
+        if (lane == 0) atomicMax(b.rmx_mt + (static_cast<size_t>(c) * ntiles + tile) * kStride + 1 + q, dbits(rq));
+      }
+    }
+    __syncthreads();
+  }
+}
+
 // ---------------------------------------------------------------- K4 special outages
 // Multi-branch / injection contingencies and busbar outages: the outage is
 // folded into the topology (extra removals, omitted injections) and the flows
@@ -707,6 +876,16 @@ int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch&
   else
     k_prep<false><<<prep_grid, kPrepCta, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
                                                                             zsm_doubles);
+  return 1;
+}
+
+int launch_prep_mt(const DevGrid& g, Batch& b, const MtProfiles& p, cudaStream_t stream) {
+  if (p.n_t < 2 || b.n == 0) return 0;
+  const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
+  const size_t smem = ((bits_bytes + 15) & ~size_t{15}) + static_cast<size_t>(p.n_t) * (kMaxSplits + kMaxCols) * 8 +
+                      static_cast<size_t>(p.n_t) * sizeof(int);
+  if (smem > 48 * 1024) cudaFuncSetAttribute(k_prep_mt, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+  k_prep_mt<<<b.n, kPrepCta, smem, stream>>>(g, b, p);
   return 1;
 }
 

@@ -120,6 +120,19 @@ void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, co
 int launch_eval_reset(const DevGrid& g, Batch& b, cudaStream_t stream);
 int launch_analyze(const DevGrid& g, Batch& b, int n_a, int n_d, cudaStream_t stream);
 int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch& s, cudaStream_t stream);
+// Multi-timestep screening: the candidate rows of profiles 1..n_t-1 in one pass
+// (after launch_prep of profile 0 with t_index 0): per-profile base tables and
+// the element strides between the profiles' row / contingency / energy / nc0
+// arrays (profile 0 at the Batch pointers).
+struct MtProfiles {
+  const double* const* f0;       // [n_t] base flows
+  const double* const* theta0;   // [n_t] base angles (reduced)
+  const double* const* inj_net;  // [n_t] injections
+  const double* const* alpha0;   // [n_t] unchanged-topology flow factors
+  int n_t;
+  size_t feat_stride, kdat_stride, energy_stride, nc0_stride;
+};
+int launch_prep_mt(const DevGrid& g, Batch& b, const MtProfiles& p, cudaStream_t stream);
 int launch_special_finish(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
                           cudaStream_t stream);
 void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_out, double* fbus_out,

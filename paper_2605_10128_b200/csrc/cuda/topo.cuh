@@ -503,14 +503,14 @@ __device__ inline void small_solve(Topo& t, const double* G, int ldg, const doub
 // Injection side of the small solve (the only part that depends on the
 // injection profile): phi_p = U^T theta' - p_psi, rho_p = V^T theta' + Y^T phi_p,
 // Rp = [S^-1 phi_p ; -C^-1 rho_p].
-__device__ inline void small_rhs(Topo& t, const double* th) {
+__device__ inline void small_rhs_into(const Topo& t, const double* th, const double* ppsi, double* Rp) {
   const int ns = t.ns, nv = t.nv;
   const double* S = t.Sinv;
   const double* C = t.Cinv;
   double php[kMaxSplits], rhp[kMaxCols];
   for (int c = 0; c < ns + nv; ++c) {
     if (c < ns)
-      php[c] = th[c] - t.ppsi[c];
+      php[c] = th[c] - ppsi[c];
     else
       rhp[c - ns] = th[c];
   }
@@ -519,14 +519,15 @@ __device__ inline void small_rhs(Topo& t, const double* th) {
   for (int q = 0; q < ns; ++q) {
     double acc = 0.0;
     for (int q2 = 0; q2 < ns; ++q2) acc += S[q * kMaxSplits + q2] * php[q2];
-    t.Rp[q] = acc;
+    Rp[q] = acc;
   }
   for (int m = 0; m < nv; ++m) {
     double acc = 0.0;
     for (int m2 = 0; m2 < nv; ++m2) acc += C[m * kMaxCols + m2] * rhp[m2];
-    t.Rp[ns + m] = -acc;
+    Rp[ns + m] = -acc;
   }
 }
+__device__ inline void small_rhs(Topo& t, const double* th) { small_rhs_into(t, th, t.ppsi, t.Rp); }
 
 // Branch features phi_e (ns) and rho_e (nv); returns false for inactive e.
 __device__ inline bool branch_features(const DevGrid& g, const Topo& t, const uint32_t* mv_bits,
