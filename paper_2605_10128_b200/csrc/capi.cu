@@ -448,9 +448,6 @@ int tg_context::enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed
     b.kdat = mt_kdat + static_cast<size_t>(t) * mt_kdat_sz;
     b.energy = mt_energy + static_cast<size_t>(t) * n * Ka;
     b.nc0 = mt_nc0 + static_cast<size_t>(t) * n;
-    b.t_index = t;
-    b.prep_lite = t > 0;  // later profiles reuse the first profile's topology factors and L rows
-    b.feat_ref = mt_feat;
     return b;
   };
   tgb::Batch b0 = view(0);

@@ -53,7 +53,6 @@ __global__ void __launch_bounds__(kAnalyzeThreads) k_analyze(DevGrid g, Batch b,
 // One CTA per candidate (grid-stride over candidates). Z = X [U | V] lives in
 // shared memory (row stride row_stride(r)) when it fits in `zsm_doubles`, else
 // in the CTA's global scratch slot.
-template <bool LITE>  // LITE: a later injection profile reusing the first profile's factors and rows
 __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch,
                                                        int zslots, int zsm_doubles) {
   extern __shared__ __align__(16) uint32_t bits[];
@@ -75,35 +74,18 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
     for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = tb[i];
     __syncthreads();
     if (threadIdx.x == 0) moved_injections(g, t);  // this profile's injections (the analysis may be shared)
-    constexpr bool lite = LITE;
-    if (lite && b.status[c] != 0) {  // islanded by the first profile's prep (structure only)
-      __syncthreads();
-      continue;
-    }
     double* sol = b.topo_sol ? b.topo_sol + static_cast<size_t>(c) * kTopoSol : nullptr;
-    if (lite) {
-      // later profiles: the topology factors of the first profile's prep, only
-      // the injection side of the small solve and the rows are recomputed
-      copy_block(t.Sinv, sol, kTopoSol * sizeof(double), threadIdx.x, blockDim.x);
-      __syncthreads();
-      if (threadIdx.x == 0) {
-        theta_terms(g, t, thv);
-        small_rhs(t, thv);
-      }
-      __syncthreads();
-    }
     const int ldz = row_stride(t.ns + t.nv);
     double* zbuf = static_cast<size_t>(g.Nr) * ldz <= static_cast<size_t>(zsm_doubles) ? zsm : zglob;
-    if (!lite) {
-      __syncthreads();
-      build_z(g, t, zbuf, ldz);
-      __syncthreads();
-      gram_terms(g, t, zbuf, ldz, gram, kSweepRank, thv);
-      __syncthreads();
-      if (threadIdx.x == 0) small_solve(t, gram, kSweepRank, thv);
-      __syncthreads();
-      if (sol && !t.islanded) copy_block(sol, t.Sinv, kTopoSol * sizeof(double), threadIdx.x, blockDim.x);
-    }
+    __syncthreads();
+    build_z(g, t, zbuf, ldz);
+    __syncthreads();
+    gram_terms(g, t, zbuf, ldz, gram, kSweepRank, thv);
+    __syncthreads();
+    if (threadIdx.x == 0) small_solve(t, gram, kSweepRank, thv);
+    __syncthreads();
+    // the topology factors for k_prep_mt (later injection profiles)
+    if (sol && !t.islanded) copy_block(sol, t.Sinv, kTopoSol * sizeof(double), threadIdx.x, blockDim.x);
     if (t.islanded) {
       if (threadIdx.x == 0) {
         b.status[c] = t.islanded;
@@ -118,16 +100,7 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
     int nc0 = 0;
     for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
       double phi[kMaxSplits], rho[kMaxCols];
-      bool on;
-      if (lite) {  // phi, rho from the first profile's branch row (L = b_e [phi; rho])
-        on = g.br_on[e] && !bit_get(rm_bits, e);
-        const double* fr0 = b.feat_ref + feat_index(slot, b.nchunks, e, r);
-        const double ib = 1.0 / g.br_b[e];
-        for (int q = 0; q < ns; ++q) phi[q] = on ? fr0[1 + q] * ib : 0.0;
-        for (int m = 0; m < nv; ++m) rho[m] = on ? fr0[1 + ns + m] * ib : 0.0;
-      } else {
-        on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
-      }
+      const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
       double row[kStride];
 #pragma unroll
       for (int i = 0; i < kStride; ++i) row[i] = 0.0;
@@ -138,18 +111,13 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
         for (int q = 0; q < ns; ++q) row[1 + q] = be * phi[q];
         for (int m = 0; m < nv; ++m) row[1 + ns + m] = be * rho[m];
       }
-      if (b.feat_mt) {  // multi-timestep bounds: max / min of f_c over profiles, L (profile-independent)
+      if (b.feat_mt) {  // multi-timestep bounds (profile 0; k_prep_mt folds the later profiles in)
         unsigned long long* m = reinterpret_cast<unsigned long long*>(b.feat_mt + feat_index(slot, b.nchunks, e, r + 1));
         const unsigned long long key = order_key(row[0]);
-        if (b.t_index == 0) {
-          m[0] = key;
-          m[1] = key;
-          double* l = reinterpret_cast<double*>(m) + 2;
-          for (int q = 0; q < r; ++q) l[q] = row[1 + q];
-        } else {
-          atomicMax(m, key);
-          atomicMin(m + 1, key);
-        }
+        m[0] = key;
+        m[1] = key;
+        double* l = reinterpret_cast<double*>(m) + 2;
+        for (int q = 0; q < r; ++q) l[q] = row[1 + q];
       }
       double2* dst = reinterpret_cast<double2*>(b.feat + feat_index(slot, b.nchunks, e, r));
 #pragma unroll
@@ -867,15 +835,10 @@ int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch&
   const size_t zsm_bytes = std::min<size_t>(static_cast<size_t>(g.Nr) * kStride * sizeof(double), kPrepZsmBytes);
   const int zsm_doubles = static_cast<int>(zsm_bytes / sizeof(double));
   if (bits_al + zsm_bytes > 48 * 1024)  // (per launch: the size depends on the grid)
-    cudaFuncSetAttribute(b.prep_lite ? k_prep<true> : k_prep<false>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(bits_al + zsm_bytes));
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
-  if (b.prep_lite)
-    k_prep<true><<<prep_grid, kPrepCta, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
-                                                                           zsm_doubles);
-  else
-    k_prep<false><<<prep_grid, kPrepCta, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots,
-                                                                            zsm_doubles);
+  k_prep<<<prep_grid, kPrepCta, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots, zsm_doubles);
   return 1;
 }
 

@@ -81,21 +81,18 @@ struct Batch {
   unsigned long long* fbus;   // [n][E] max |f| over busbar outages
   double* energy;             // [n][Kall] outage energy per contingency
   int* nc0;                   // [n] lambda_c0 of the candidate flows (k_prep)
-  // Multi-timestep screening (capi.cu, n_t > 1 profiles): k_prep of profile
-  // t_index folds every profile's candidate flows and flow factors into
-  // bounds over all profiles; k_sweep in mask mode (t_mode 1) marks the rows
+  // Multi-timestep screening (capi.cu, n_t > 1 profiles): k_prep (profile 0)
+  // and k_prep_mt (the others) fold every profile's candidate flows and flow
+  // factors into bounds over all profiles; k_sweep in mask mode (t_mode 1) marks the rows
   // of each (candidate, tile) that can overload at some profile, k_sweep in
   // masked mode (t_mode 2) then visits only those rows per profile.
   int t_mode;                 // 0 single profile, 1 mask generation, 2 masked sweep
-  int t_index;                // profile of this prep pass (0 writes the bounds, > 0 folds)
   double* feat_mt;            // rows [key(max_t f_c), key(min_t f_c), L...] at row_stride(r + 1), feat_index layout;
                               // keys are the ordered bit patterns of doubles (order_key)
   unsigned long long* amx_mt; // [n][ntiles][kTmaxSub] max_t max |alpha_t - alpha0_t| per sub-tile (bits)
   unsigned long long* rmx_mt; // [n][ntiles][kStride] max_t max_k |R'_t[q, k]| per tile (bits, slot 1 + q)
   uint32_t* mask;             // [n][ntiles][nchunks] rows that can overload at some profile
-  int prep_lite;              // k_prep reuses topo_sol and feat_ref (profiles after the first)
   double* topo_sol;           // [n][kTopoSol] S^-1, Y, C^-1 of the first profile's small solve
-  const double* feat_ref;     // the first profile's candidate rows (L)
   int* isl_out;               // [n] islanded special contingencies
   int* isl_bus;               // [n]
   int* wl_list;               // [n] candidates bucketed by rank
