@@ -22,7 +22,9 @@ def main(rep, cfg, note=""):
     sweeps = [r for r in rows[2:] if "k_sweep" in r[hdr.index("Kernel Name")]]
     if not sweeps:
         raise SystemExit("no k_sweep launch in the report")
-    r = sweeps[-1]
+    TSCALE = {"ns": 1e-6, "usecond": 1e-3, "us": 1e-3, "msecond": 1.0, "ms": 1.0, "s": 1e3, "second": 1e3}
+    ti = hdr.index("gpu__time_duration.sum")
+    r = max(sweeps, key=lambda x: float(x[ti]) * TSCALE.get(units[ti], 1.0))  # the main sweep launch
 
     def val(name):
         i = hdr.index(name)
@@ -31,7 +33,8 @@ def main(rep, cfg, note=""):
 
     rec = {
         "report": os.path.basename(rep), "note": note,
-        "duration_ms": val("gpu__time_duration.sum") / (1e6 if units[hdr.index("gpu__time_duration.sum")] == "ns" else 1),
+        "kernel": r[hdr.index("Kernel Name")].split("(")[0],
+        "duration_ms": float(r[ti]) * TSCALE.get(units[ti], 1.0),
         "dram_bytes_per_launch": val("dram__bytes_read.sum") + val("dram__bytes_write.sum"),
         "fp64_pipe_pct": val("sm__pipe_fp64_cycles_active.avg.pct_of_peak_sustained_active"),
         "issue_active_pct": val("smsp__issue_active.avg.pct_of_peak_sustained_active"),
@@ -41,8 +44,6 @@ def main(rep, cfg, note=""):
         "warps_active_pct": val("sm__warps_active.avg.pct_of_peak_sustained_active"),
         "registers": val("launch__registers_per_thread"),
     }
-    if units[hdr.index("gpu__time_duration.sum")] == "ms":
-        rec["duration_ms"] = val("gpu__time_duration.sum")
     doc = json.load(open(OUT)) if os.path.exists(OUT) else {}
     doc[cfg] = rec
     json.dump(doc, open(OUT, "w"), indent=1)
