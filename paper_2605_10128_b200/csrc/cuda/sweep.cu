@@ -558,7 +558,8 @@ __host__ __device__ inline MaskedPlan masked_plan(int E, int S) {
 
 template <int R>
 __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile,
-                                           uint8_t* smem, uint64_t* full_bar, uint64_t* empty_bar, int nunion) {
+                                           uint8_t* smem, uint64_t* full_bar, uint64_t* empty_bar, int nunion,
+                                           double* rmax_s, float* amax_s) {
   constexpr int S = row_stride(R);
   const MaskedPlan plan = masked_plan(g.E, S);
   const int NST = plan.stages;
@@ -604,12 +605,38 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
   };
   if (threadIdx.x == 0)
     for (int j = 0; j < NST && j < nb; ++j) issue(j);
-  // this lane's union row of batch j: own mask bit, candidate row and limit,
-  // gathered one batch ahead (registers) while the current batch computes
+  // this profile's stage-1 bound operands (sweep_cta): max |alpha - alpha0| per
+  // sub-tile (float, rounded up) and max |R'_q| over the tile, per warp
+  float* asub = amax_s + warp * kTmaxSub;
+  double* rms = rmax_s + warp * kStride;
+  {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[k] - g.alpha0[kb + k]));
+#pragma unroll
+    for (int o = kSubLanes / 2; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane % kSubLanes == 0) asub[lane / kSubLanes] = __double2float_ru(a * (1.0 + 1e-12));
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      double r = 0.0;
+#pragma unroll
+      for (int k = 0; k < kKpl; ++k) r = fmax(r, fabs(rr[k][q]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+      if (lane == 0) rms[q] = r * (1.0 + 1e-12);
+    }
+    __syncwarp();
+  }
+  // this lane's union row of batch j: own mask bit, candidate row, limit and
+  // skip record, gathered one batch ahead (registers) while the current batch
+  // computes; the row is kept only if this profile's own stage-1 bound (the
+  // all-profile mask is the union over the day) cannot prove it safe
   int e_n = -1;
   bool marked_n = false;
   double lim_n = 0.0;
   double2 fr_n[S / 2];
+  float4 rec_n[kRec / 4];
+  const float* rec_tile = g.Tmax + static_cast<size_t>(tile) * (g.E + kChunk) * kRec;
   auto gather = [&](int j) {
     const int idx = j * kMaskBatch + lane;
     e_n = j < nb && idx < nunion ? ul[idx] : -1;
@@ -619,13 +646,43 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
 #pragma unroll
       for (int q = 0; q < S / 2; ++q) fr_n[q] = fr[q];
       lim_n = g.br_lim[e_n];
+      const float4* rc = reinterpret_cast<const float4*>(rec_tile + static_cast<size_t>(e_n) * kRec);
+#pragma unroll
+      for (int q = 0; q < kRec / 4; ++q) rec_n[q] = rc[q];
     }
+  };
+  // stage 1 of sweep_cta on the gathered row (same rigorous bound)
+  auto profile_hot = [&]() {
+    const double lim = lim_n * (1.0 - 1e-12);
+    const double* fl = reinterpret_cast<const double*>(fr_n);
+    double l0 = 0.0, l1 = 0.0;
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      if (q & 1)
+        l1 = fma(fabs(fl[1 + q]), rms[q], l1);
+      else
+        l0 = fma(fabs(fl[1 + q]), rms[q], l0);
+    }
+    const double lrb = l0 + l1, fc = fl[0];
+    const float4* ar = reinterpret_cast<const float4*>(asub);
+    float taf = 0.0f;
+#pragma unroll
+    for (int q = 0; q < kTmaxSub / 4; ++q) {
+      const float4 t4 = rec_n[q], a4 = ar[q];
+      taf = fmaxf(taf, fmaxf(fmaxf(__fmul_ru(t4.x, a4.x), __fmul_ru(t4.y, a4.y)),
+                             fmaxf(__fmul_ru(t4.z, a4.z), __fmul_ru(t4.w, a4.w))));
+    }
+    const double2 d0 = reinterpret_cast<const double2*>(rec_n)[kTmaxSub / 4];
+    const double gap = lim - fmax(fc + d0.x, -(fc + d0.y));
+    const double s0 = 1e-12 * (fabs(fc) + fabs(d0.x) + fabs(d0.y));
+    const double wd = static_cast<double>(taf) + lrb;
+    return fma(wd, 1.0 + 1e-12, s0) >= gap;
   };
   gather(0);
   for (int j = 0; j < nb; ++j) {
     const int s = j % NST;
     const int e_l = e_n;
-    const bool marked = marked_n;
+    const bool marked = marked_n && profile_hot();
     const double lim_l = lim_n;
     if (marked) {
       double2* dst = reinterpret_cast<double2*>(scr + lane * S);
@@ -697,8 +754,9 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
 
 template <int R>
 __device__ __noinline__ void masked_cta_call(const DevGrid& g, const Batch& b, const CtaWork& w, int tile,
-                                             uint8_t* smem, uint64_t* full_bar, uint64_t* empty_bar, int nunion) {
-  masked_cta<R>(g, b, w, tile, smem, full_bar, empty_bar, nunion);
+                                             uint8_t* smem, uint64_t* full_bar, uint64_t* empty_bar, int nunion,
+                                             double* rmax_s, float* amax_s) {
+  masked_cta<R>(g, b, w, tile, smem, full_bar, empty_bar, nunion, rmax_s, amax_s);
 }
 
 __global__ void __launch_bounds__(kThreads, 1) k_sweep_masked(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
@@ -707,6 +765,8 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep_masked(DevGrid g, Batch b
   __shared__ int r_s, nunion_s;
   __shared__ int wsum[kWarps];
   __shared__ __align__(8) uint64_t bars[2 * kMaskMaxStages];
+  __shared__ __align__(16) double rmax_s[kWarps * kStride];
+  __shared__ __align__(16) float amax_s[kWarps * kTmaxSub];
   const int per_sb = gblock * ntiles;
   const int sb = static_cast<int>(blockIdx.x) / per_sb, rr = static_cast<int>(blockIdx.x) % per_sb;
   const int g0 = sb * gblock, gg = min(gblock, ngroups - g0);
@@ -779,19 +839,19 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep_masked(DevGrid g, Batch b
   uint64_t* eb = bars + kMaskMaxStages;
   const int nu = nunion_s;
   switch (r_s) {
-    case 0: masked_cta<0>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 1: masked_cta<1>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 2: masked_cta<2>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 3: masked_cta<3>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 4: masked_cta<4>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 5: masked_cta<5>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 0: masked_cta<0>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 1: masked_cta<1>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 2: masked_cta<2>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 3: masked_cta<3>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 4: masked_cta<4>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 5: masked_cta<5>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
     // higher ranks in their own call frames (register pressure of the common ones)
-    case 6: masked_cta_call<6>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 7: masked_cta_call<7>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 8: masked_cta_call<8>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 9: masked_cta_call<9>(g, b, w, tile, sm, fb, eb, nu); break;
-    case 10: masked_cta_call<10>(g, b, w, tile, sm, fb, eb, nu); break;
-    default: masked_cta_call<11>(g, b, w, tile, sm, fb, eb, nu); break;
+    case 6: masked_cta_call<6>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 7: masked_cta_call<7>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 8: masked_cta_call<8>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 9: masked_cta_call<9>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 10: masked_cta_call<10>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    default: masked_cta_call<11>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
   }
 }
 
