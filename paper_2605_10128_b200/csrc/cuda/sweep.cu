@@ -860,41 +860,60 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep_masked(DevGrid g, Batch b
 // (group * kGroupSlots + position) so k_prep writes straight into the layout
 // the sweep streams.
 __global__ void k_bucket(Batch b) {
-  __shared__ int warp_tot[32];
+  // two passes over the batch in 1024-candidate chunks: per-rank counts, then
+  // stable positions (rank bucket, then candidate order); one ballot per rank
+  // per warp and one barrier per chunk and pass
+  constexpr int NR = kSweepRank + 1;
+  __shared__ int warp_tot[NR][32];
+  __shared__ int run_s[NR], base_s[NR], gbase_s[NR];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
-  for (int c = threadIdx.x; c < b.n; c += blockDim.x) b.slot[c] = -1;
+  if (threadIdx.x < NR) run_s[threadIdx.x] = 0;
   __syncthreads();
-  int base = 0, group_base = 0;
-  for (int r = 0; r <= kSweepRank; ++r) {
-    int running = 0;
+  for (int pass = 0; pass < 2; ++pass) {
     for (int c0 = 0; c0 < b.n; c0 += blockDim.x) {
       const int c = c0 + threadIdx.x;
-      const bool mine = c < b.n && b.rank[c] == r;
-      const unsigned m = __ballot_sync(0xffffffffu, mine);
-      if (lane == 0) warp_tot[wid] = __popc(m);
+      const int rk = c < b.n ? b.rank[c] : -1;
+      unsigned mine_m = 0u;
+#pragma unroll
+      for (int r = 0; r < NR; ++r) {
+        const unsigned m = __ballot_sync(0xffffffffu, rk == r);
+        if (rk == r) mine_m = m;
+        if (lane == 0) warp_tot[r][wid] = __popc(m);
+      }
       __syncthreads();
-      int off = 0, tot = 0;
-      for (int x = 0; x < nw; ++x) {
-        if (x < wid) off += warp_tot[x];
-        tot += warp_tot[x];
+      if (pass == 1 && rk >= 0 && rk < NR) {
+        int off = 0;
+        for (int x = 0; x < wid; ++x) off += warp_tot[rk][x];
+        const int pos = run_s[rk] + off + __popc(mine_m & ((1u << lane) - 1));
+        b.wl_list[base_s[rk] + pos] = c;
+        b.slot[c] = (gbase_s[rk] + pos / cand_per_cta(rk)) * kGroupSlots + pos % cand_per_cta(rk);
+      } else if (c < b.n && (rk < 0 || rk >= NR)) {
+        b.slot[c] = -1;
       }
-      if (mine) {
-        const int pos = running + off + __popc(m & ((1u << lane) - 1));
-        b.wl_list[base + pos] = c;
-        b.slot[c] = (group_base + pos / cand_per_cta(r)) * kGroupSlots + pos % cand_per_cta(r);
+      __syncthreads();
+      if (threadIdx.x < NR) {
+        int tot = 0;
+        for (int x = 0; x < nw; ++x) tot += warp_tot[threadIdx.x][x];
+        run_s[threadIdx.x] += tot;
       }
-      running += tot;
       __syncthreads();
     }
-    if (threadIdx.x == 0) {
-      b.wl_start[r] = base;
-      b.wl_count[r] = running;
-      b.wl_group0[r] = group_base;
+    if (pass == 0 && threadIdx.x == 0) {
+      int base = 0, group_base = 0;
+      for (int r = 0; r < NR; ++r) {
+        base_s[r] = base;
+        gbase_s[r] = group_base;
+        b.wl_start[r] = base;
+        b.wl_count[r] = run_s[r];
+        b.wl_group0[r] = group_base;
+        base += run_s[r];
+        group_base += (run_s[r] + cand_per_cta(r) - 1) / cand_per_cta(r);
+        run_s[r] = 0;
+      }
+      b.wl_group0[NR] = group_base;
     }
-    base += running;
-    group_base += (running + cand_per_cta(r) - 1) / cand_per_cta(r);
+    __syncthreads();
   }
-  if (threadIdx.x == 0) b.wl_group0[kSweepRank + 1] = group_base;
 }
 
 }  // namespace
