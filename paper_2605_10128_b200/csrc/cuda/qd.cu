@@ -523,14 +523,22 @@ __global__ void k_insert(QdParams p, Archive a, const int* genomes, Scores sc, c
       int ck[kMaxSlots];
 #pragma unroll
       for (int k = 0; k < kMaxSlots; ++k) ck[k] = -1;
-      if (mine) {
-        cf = sc.fitness[cbase + lane];
-        canonical_key(genomes + static_cast<size_t>(cbase + lane) * ns, p.n_a, p.n_d, ck);
+      if (mine) cf = sc.fitness[cbase + lane];
+      // a full cell only takes a strictly better entry and its worst never
+      // decreases while it stays full: lanes not above the current worst are
+      // rejected whatever comes before them
+      if (cnt >= p.cap) {
+        const double worst0 = __shfl_sync(0xffffffffu, efit, cnt - 1);
+        m &= __ballot_sync(0xffffffffu, mine && cf > worst0);
+        if (!m) continue;
       }
+      if ((m >> lane) & 1u) canonical_key(genomes + static_cast<size_t>(cbase + lane) * ns, p.n_a, p.n_d, ck);
       while (m) {
         const int bit = __ffs(m) - 1;
         m &= m - 1;
         const double fit = __shfl_sync(0xffffffffu, cf, bit);
+        const double worst = __shfl_sync(0xffffffffu, efit, cnt > 0 ? cnt - 1 : 0);
+        if (cnt >= p.cap && fit <= worst) continue;  // rejected before the duplicate test (same outcome)
         int key[kMaxSlots];
         bool same = lane < cnt;
 #pragma unroll
@@ -538,9 +546,7 @@ __global__ void k_insert(QdParams p, Archive a, const int* genomes, Scores sc, c
           key[k] = __shfl_sync(0xffffffffu, ck[k], bit);
           same = same && (k >= ns || ekey[k] == key[k]);
         }
-        bool ok = !__any_sync(0xffffffffu, same);
-        const double worst = __shfl_sync(0xffffffffu, efit, cnt > 0 ? cnt - 1 : 0);
-        if (ok && cnt >= p.cap && fit <= worst) ok = false;
+        const bool ok = !__any_sync(0xffffffffu, same);
         if (ok) {
           const int pos = __popc(__ballot_sync(0xffffffffu, lane < cnt && !(fit > efit)));
           const double uf = __shfl_up_sync(0xffffffffu, efit, 1);
