@@ -235,11 +235,11 @@ struct tg_context {
   bool mt_pattern_ok = false;  // injection zero pattern identical across profiles
   tgb::MtProfiles mt_prof{};   // per-profile table pointers (device arrays)
   tgb::DevGrid g_mt{};          // t = 0 view with the all-profile skip records
-  double* mt_feat = nullptr;    // [n_t] candidate branch rows
-  double* mt_kdat = nullptr;    // [n_t] contingency rows
+  double* mt_fc = nullptr;      // [n_t][n][E] candidate flows per profile
+  double* mt_al = nullptr;      // [n_t][n][Kpad] alpha per profile
+  double* mt_rk = nullptr;      // [cap][Kpad][kStride] profile-independent contingency factors
   double* mt_energy = nullptr;  // [n_t][cap][Kall]
   int* mt_nc0 = nullptr;        // [n_t][cap]
-  size_t mt_feat_sz = 0, mt_kdat_sz = 0;
   // island merge buffers (allocated on the first merge)
   std::unique_ptr<DeviceArena> merge_arena;
   tgb::MergeBuffers merge{};
@@ -361,8 +361,8 @@ void tg_context::ensure_capacity(int n) {
                            tgb::kChunkRows * tgb::kStride;
     const size_t kdat_sz = static_cast<size_t>(cap) * std::max<size_t>(Kp, 1) * tgb::kStride;
     const size_t ntiles = std::max<size_t>(Kp / tgb::sweep_tile_k(), 1);
-    const size_t need = sizeof(double) * (static_cast<size_t>(n_t) * (feat_sz + kdat_sz + static_cast<size_t>(cap) * Ka) +
-                                          feat_sz) +
+    const size_t need = sizeof(double) * (static_cast<size_t>(n_t) * cap * (static_cast<size_t>(E) + Kp + Ka) +
+                                          feat_sz + kdat_sz) +
                         static_cast<size_t>(n_t) * cap * sizeof(int) +
                         static_cast<size_t>(cap) * ntiles * (tgb::kTmaxSub + tgb::kStride) * 8 +
                         static_cast<size_t>(cap) * ntiles * b.nchunks * 4;
@@ -371,10 +371,9 @@ void tg_context::ensure_capacity(int n) {
     static const bool mt_disabled = std::getenv("TGB_NO_MT_SCREEN") != nullptr;  // A/B switch
     mt_ok = mt_pattern_ok && !mt_disabled && need < free_b / 2 && tgb::masked_sweep_fits(g.E);
     if (mt_ok) {
-      mt_feat_sz = feat_sz;
-      mt_kdat_sz = kdat_sz;
-      mt_feat = A.alloc<double>(static_cast<size_t>(n_t) * feat_sz);
-      mt_kdat = A.alloc<double>(static_cast<size_t>(n_t) * kdat_sz);
+      mt_fc = A.alloc<double>(static_cast<size_t>(n_t) * cap * std::max<size_t>(E, 1));
+      mt_al = A.alloc<double>(static_cast<size_t>(n_t) * cap * std::max<size_t>(Kp, 1));
+      mt_rk = A.alloc<double>(kdat_sz);
       mt_energy = A.alloc<double>(static_cast<size_t>(n_t) * cap * Ka);
       mt_nc0 = A.alloc<int>(static_cast<size_t>(n_t) * cap);
       b.feat_mt = A.alloc<double>(feat_sz);
@@ -443,9 +442,10 @@ int tg_context::enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed
   const size_t Ka = std::max(g.Kall, 1);
   int kernels = 0;
   auto view = [&](int t) {
-    tgb::Batch b = bv;
-    b.feat = mt_feat + static_cast<size_t>(t) * mt_feat_sz;
-    b.kdat = mt_kdat + static_cast<size_t>(t) * mt_kdat_sz;
+    tgb::Batch b = bv;  // feat / kdat: profile 0's rows (the batch's own arrays)
+    b.fc_t = mt_fc + static_cast<size_t>(t) * n * g.E;
+    b.al_t = mt_al + static_cast<size_t>(t) * n * g.Kpad;
+    b.rk_mt = mt_rk;
     b.energy = mt_energy + static_cast<size_t>(t) * n * Ka;
     b.nc0 = mt_nc0 + static_cast<size_t>(t) * n;
     return b;
@@ -461,8 +461,11 @@ int tg_context::enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed
     tgb::Batch b0p = view(0);
     kernels += tgb::launch_prep(gt[0], b0p, n_a, n_d, scratch, stream);
     tgb::MtProfiles P = mt_prof;
-    P.feat_stride = mt_feat_sz;
-    P.kdat_stride = mt_kdat_sz;
+    P.fc = mt_fc;
+    P.al = mt_al;
+    P.rk = mt_rk;
+    P.fc_stride = static_cast<size_t>(n) * g.E;
+    P.al_stride = static_cast<size_t>(n) * g.Kpad;
     P.energy_stride = static_cast<size_t>(n) * Ka;
     P.nc0_stride = static_cast<size_t>(n);
     kernels += tgb::launch_prep_mt(g, b0p, P, stream);

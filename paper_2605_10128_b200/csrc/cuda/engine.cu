@@ -219,13 +219,15 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
 }
 
 // ---------------------------------------------------------------- K2b prep, profiles 1..n_t-1
-// Multi-timestep screening (capi.cu enqueue_evaluate_mt): the topology factors
-// and the L rows are profile-independent, only f_c and alpha change with the
-// injections. One CTA per candidate computes every later profile's rows in one
-// pass: the per-profile small right-hand sides in parallel (one thread per
-// profile), then each thread reads its branch's L row once (profile 0, written
-// by k_prep) and emits f_c for all profiles; the bounds of the mask pass are
-// folded over the profiles in registers (no per-profile atomics).
+// Multi-timestep screening (capi.cu enqueue_evaluate_mt): the topology factors,
+// the L rows and the unscaled contingency factors rk are profile-independent,
+// only f_c and alpha change with the injections. One CTA per candidate writes
+// the compact per-profile arrays in one pass: the per-profile small right-hand
+// sides in parallel (one thread per profile), then each thread reads its
+// branch's L row once (profile 0, written by k_prep) and emits f_c for all
+// profiles, and each contingency's rk row once and its alpha per profile
+// (R'_t = rk * alpha_t is formed by the masked sweep); the bounds of the mask
+// pass are folded over the profiles in registers (no per-profile atomics).
 __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProfiles P) {
   extern __shared__ __align__(16) uint32_t bits[];
   __shared__ Topo t;
@@ -264,25 +266,23 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
       small_rhs_into(t, th, ppsi, rp_all + static_cast<size_t>(tt) * kRp);
     }
     __syncthreads();
-    // branch rows of every later profile from the L row of profile 0
+    // f_c of every profile from the L row of profile 0 (compact per-profile
+    // arrays [t][n][E]; profile 0's value is its row's)
     const int e_end = (g.E + 31) & ~31;
     for (int e0 = threadIdx.x; e0 < e_end; e0 += blockDim.x) {
       const int e = e0 < g.E ? e0 : g.E - 1;
       const bool valid = e0 < g.E;
-      const size_t fi = feat_index(slot, b.nchunks, e, r);
-      const double* fr0 = b.feat + fi;
-      double row[kStride];
-#pragma unroll
-      for (int i = 0; i < kStride; ++i) row[i] = 0.0;
-      for (int i = 1; i < rs; ++i) row[i] = fr0[i];
+      const double* fr0 = b.feat + feat_index(slot, b.nchunks, e, r);
+      const double fc0 = fr0[0];
       const bool on = g.br_on[e] && !bit_get(rm_bits, e);
       double phi[kMaxSplits], rho[kMaxCols];
       const double be = g.br_b[e], ib = 1.0 / be;
-      for (int q = 0; q < ns; ++q) phi[q] = on ? row[1 + q] * ib : 0.0;
-      for (int m = 0; m < nv; ++m) rho[m] = on ? row[1 + ns + m] * ib : 0.0;
+      for (int q = 0; q < ns; ++q) phi[q] = on ? fr0[1 + q] * ib : 0.0;
+      for (int m = 0; m < nv; ++m) rho[m] = on ? fr0[1 + ns + m] * ib : 0.0;
       unsigned long long* mk = reinterpret_cast<unsigned long long*>(b.feat_mt + feat_index(slot, b.nchunks, e, r + 1));
       unsigned long long kmax = 0ull, kmin = ~0ull;
       const double lim = g.br_lim[e];
+      if (valid) P.fc[static_cast<size_t>(c) * g.E + e] = fc0;
       for (int tt = 1; tt < P.n_t; ++tt) {
         const double* rp = rp_all + static_cast<size_t>(tt) * kRp;
         double fc = 0.0;
@@ -295,14 +295,10 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
         const unsigned cnt = __popc(__ballot_sync(0xffffffffu, valid && fabs(fc) > lim));
         if (lane == 0 && cnt) atomicAdd(nc0_s + tt, static_cast<int>(cnt));
         if (valid) {
-          row[0] = fc;
           const unsigned long long key = order_key(fc);
           kmax = max(kmax, key);
           kmin = min(kmin, key);
-          double2* dst = reinterpret_cast<double2*>(b.feat + static_cast<size_t>(tt) * P.feat_stride + fi);
-#pragma unroll
-          for (int i = 0; i < kStride / 2; ++i)
-            if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+          P.fc[static_cast<size_t>(tt) * P.fc_stride + static_cast<size_t>(c) * g.E + e] = fc;
         }
       }
       if (valid) {
@@ -313,7 +309,8 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
     __syncthreads();
     if (threadIdx.x == 0)
       for (int tt = 1; tt < P.n_t; ++tt) b.nc0[static_cast<size_t>(tt) * P.nc0_stride + c] = nc0_s[tt];
-    // contingency rows: the topology part once, alpha per profile
+    // contingencies: the topology part once (rk rows [0, S^-1 phi, -C^-1 rho]
+    // at row_stride(r), profile-independent), alpha per profile ([t][n][Kpad])
     for (int k = threadIdx.x; k < g.Kpad; k += blockDim.x) {
       double rk[kSweepRank];
       double den = 1.0;
@@ -346,28 +343,33 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
           live = !(fabs(den) < 1e-8);  // a bridge with flag 0 is a dead stub: flows unchanged
         }
       }
-      double dlmax = 0.0, rqmax[kSweepRank];
-      for (int q = 0; q < r; ++q) rqmax[q] = 0.0;
-      for (int tt = 1; tt < P.n_t; ++tt) {
+      {
         double row[kStride];
 #pragma unroll
         for (int i = 0; i < kStride; ++i) row[i] = 0.0;
-        if (live) {
-          const double fcb = b.feat[static_cast<size_t>(tt) * P.feat_stride + feat_index(slot, b.nchunks, beta, r)];
-          const double alpha = fcb / den;
-          row[0] = alpha;
-          for (int i = 0; i < r; ++i) row[1 + i] = rk[i] * alpha;
-        }
-        if (k < g.Ks && flag == 1)
-          b.energy[static_cast<size_t>(tt) * P.energy_stride + static_cast<size_t>(c) * g.Kall + g.ks_cont[k]] =
-              b.params.penalty;
-        double2* dst = reinterpret_cast<double2*>(b.kdat + static_cast<size_t>(tt) * P.kdat_stride +
-                                                  static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(k) * rs);
+        if (live)
+          for (int i = 0; i < r; ++i) row[1 + i] = rk[i];
+        double2* dst = reinterpret_cast<double2*>(P.rk + static_cast<size_t>(c) * g.Kpad * kStride +
+                                                  static_cast<size_t>(k) * rs);
 #pragma unroll
         for (int i = 0; i < kStride / 2; ++i)
           if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
-        dlmax = fmax(dlmax, fabs(row[0] - P.alpha0[tt][k]));
-        for (int q = 0; q < r; ++q) rqmax[q] = fmax(rqmax[q], fabs(row[1 + q]));
+      }
+      double dlmax = 0.0, rqmax[kSweepRank];
+      for (int q = 0; q < r; ++q) rqmax[q] = 0.0;
+      for (int tt = 0; tt < P.n_t; ++tt) {
+        double alpha = 0.0;
+        if (live) {
+          const double fcb = P.fc[static_cast<size_t>(tt) * P.fc_stride + static_cast<size_t>(c) * g.E + beta];
+          alpha = fcb / den;
+        }
+        P.al[static_cast<size_t>(tt) * P.al_stride + static_cast<size_t>(c) * g.Kpad + k] = alpha;
+        if (tt == 0) continue;  // profile 0: penalties and bounds written by k_prep
+        if (k < g.Ks && flag == 1)
+          b.energy[static_cast<size_t>(tt) * P.energy_stride + static_cast<size_t>(c) * g.Kall + g.ks_cont[k]] =
+              b.params.penalty;
+        dlmax = fmax(dlmax, fabs(alpha - P.alpha0[tt][k]));
+        for (int q = 0; q < r; ++q) rqmax[q] = fmax(rqmax[q], fabs(rk[q] * alpha));
       }
       // fold into the bounds profile 0 wrote (tiles of 128: a warp is 32
       // consecutive contingencies of one tile, half a warp one sub-tile)

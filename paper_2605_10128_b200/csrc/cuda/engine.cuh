@@ -93,6 +93,9 @@ struct Batch {
   unsigned long long* rmx_mt; // [n][ntiles][kStride] max_t max_k |R'_t[q, k]| per tile (bits, slot 1 + q)
   uint32_t* mask;             // [n][ntiles][nchunks] rows that can overload at some profile
   double* topo_sol;           // [n][kTopoSol] S^-1, Y, C^-1 of the first profile's small solve
+  const double* fc_t;         // masked sweep: this profile's f_c [n][E] (k_prep_mt), L from feat (profile 0)
+  const double* al_t;         // masked sweep: this profile's alpha [n][Kpad]
+  const double* rk_mt;        // masked sweep: rk rows (MtProfiles::rk); R'_t = rk * alpha_t
   int* isl_out;               // [n] islanded special contingencies
   int* isl_bus;               // [n]
   int* wl_list;               // [n] candidates bucketed by rank
@@ -127,7 +130,10 @@ struct MtProfiles {
   const double* const* inj_net;  // [n_t] injections
   const double* const* alpha0;   // [n_t] unchanged-topology flow factors
   int n_t;
-  size_t feat_stride, kdat_stride, energy_stride, nc0_stride;
+  double* fc;  // [n_t][n][E] candidate flows per profile (compact)
+  double* al;  // [n_t][n][Kpad] alpha per profile
+  double* rk;  // [n][Kpad][kStride] rows [0, rk_0..rk_{r-1}] at row_stride(r), profile-independent
+  size_t fc_stride, al_stride, energy_stride, nc0_stride;
 };
 int launch_prep_mt(const DevGrid& g, Batch& b, const MtProfiles& p, cudaStream_t stream);
 int launch_special_finish(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,

@@ -534,6 +534,8 @@ static_assert(kSweepRank == 11 && kFastRank == 7, "k_sweep / k_sweep_hi rank swi
 // ~8x fewer rows than the sum at cfg3); the T_base rows of the union are
 // staged once per CTA by TMA bulk copies (1 KB per row) into a ring of
 // 32-row batches, and each warp gathers only its own marked candidate rows.
+// Per-profile data is compact (k_prep_mt): f_c and alpha of this profile, the
+// L rows (profile 0) and the unscaled contingency factors rk are shared.
 constexpr int kMaskBatch = 32;                               // union rows per ring stage
 constexpr size_t kMaskStageBytes = kMaskBatch * kTileK * 8;  // T_base rows of one stage
 constexpr int kMaskMaxStages = 4;
@@ -574,15 +576,17 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
   int cid = warp < w.ncand ? w.cand[warp] : -1;
   if (cid >= 0 && b.status[cid] != 0) cid = -1;
   {
+    // this profile's alpha and the shared rk rows: R'_t = rk * alpha_t (as k_prep)
     const int c = cid >= 0 ? cid : w.cand[0];
-    const double* kd = b.kdat + static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(kb) * S;
+    const double* kr = b.rk_mt + static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(kb) * S;
+    const double* al = b.al_t + static_cast<size_t>(c) * g.Kpad + kb;
     const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad + kb;
 #pragma unroll
     for (int i = 0; i < kKpl; ++i) {
       kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
-      alpha[i] = kd[i * S];
+      alpha[i] = al[i];
 #pragma unroll
-      for (int q = 0; q < R; ++q) rr[i][q] = kd[i * S + 1 + q];
+      for (int q = 0; q < R; ++q) rr[i][q] = kr[i * S + 1 + q] * alpha[i];
       energy[i] = 0.0;
       kval[i] = cid >= 0 && kf[i] == 0;
     }
@@ -642,9 +646,11 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
     e_n = j < nb && idx < nunion ? ul[idx] : -1;
     marked_n = e_n >= 0 && cid >= 0 && ((mw[e_n >> 5] >> (e_n & 31)) & 1u);
     if (marked_n) {
+      // L from profile 0's row, f_c of this profile
       const double2* fr = reinterpret_cast<const double2*>(b.feat + feat_index(static_cast<int>(slot), b.nchunks, e_n, R));
 #pragma unroll
       for (int q = 0; q < S / 2; ++q) fr_n[q] = fr[q];
+      fr_n[0].x = b.fc_t[static_cast<size_t>(cid) * g.E + e_n];
       lim_n = g.br_lim[e_n];
       const float4* rc = reinterpret_cast<const float4*>(rec_tile + static_cast<size_t>(e_n) * kRec);
 #pragma unroll
