@@ -120,6 +120,7 @@ struct CtaWork {
   int cand[kMaxCand];
   int ncand;
   int group;
+  int half;  // k_sweep_masked: which half of the group (kMaskWarps candidates)
 };
 
 // Producer: stage <- stage-chunk i = 32-row chunks [H i, H i + H) (T tile rows
@@ -539,6 +540,9 @@ static_assert(kSweepRank == 11 && kFastRank == 7, "k_sweep / k_sweep_hi rank swi
 constexpr int kMaskBatch = 32;                               // union rows per ring stage
 constexpr size_t kMaskStageBytes = kMaskBatch * kTileK * 8;  // T_base rows of one stage
 constexpr int kMaskMaxStages = 4;
+constexpr int kMaskWarps = kWarps / 2;       // half a candidate group per CTA, two CTAs per SM
+constexpr int kMaskThreads = 32 * kMaskWarps;
+constexpr size_t kMaskBudget = 110 * 1024;  // dynamic shared memory per CTA (two per SM)
 
 // shared-memory plan of k_sweep_masked for E rows at row stride S
 struct MaskedPlan {
@@ -551,8 +555,8 @@ __host__ __device__ inline MaskedPlan masked_plan(int E, int S) {
   p.su = 0;
   p.ul = (static_cast<size_t>(nch) * 4 + 15) & ~size_t{15};
   p.scr = (p.ul + static_cast<size_t>(E) * 4 + 15) & ~size_t{15};
-  p.ring = (p.scr + static_cast<size_t>(kWarps) * 32 * S * 8 + 127) & ~size_t{127};
-  const size_t left = kStageBudget > p.ring ? kStageBudget - p.ring : 0;
+  p.ring = (p.scr + static_cast<size_t>(kMaskWarps) * 32 * S * 8 + 127) & ~size_t{127};
+  const size_t left = kMaskBudget > p.ring ? kMaskBudget - p.ring : 0;
   const size_t st = left / kMaskStageBytes;
   p.stages = static_cast<int>(st < kMaskMaxStages ? st : kMaskMaxStages);
   return p;
@@ -595,7 +599,7 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
   }
   const int ntiles = g.Kpad / kTileK;
   const uint32_t* mw = b.mask + (static_cast<size_t>(cid >= 0 ? cid : 0) * ntiles + tile) * b.nchunks;
-  const size_t slot = static_cast<size_t>(w.group) * kGroupSlots + warp;
+  const size_t slot = static_cast<size_t>(w.group) * kGroupSlots + w.half * kMaskWarps + warp;
   unsigned long long* fmx = b.fmax + static_cast<size_t>(cid >= 0 ? cid : 0) * g.E;
   const double* tk_tile = g.TK + static_cast<size_t>(tile) * g.E * kTileK;
   const int nb = (nunion + kMaskBatch - 1) / kMaskBatch;
@@ -765,36 +769,40 @@ __device__ __noinline__ void masked_cta_call(const DevGrid& g, const Batch& b, c
   masked_cta<R>(g, b, w, tile, smem, full_bar, empty_bar, nunion, rmax_s, amax_s);
 }
 
-__global__ void __launch_bounds__(kThreads, 1) k_sweep_masked(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
+__global__ void __launch_bounds__(kMaskThreads, 2) k_sweep_masked(DevGrid g, Batch b, int ntiles, int ngroups,
+                                                                  int gblock) {
   extern __shared__ __align__(128) uint8_t msm[];
   __shared__ CtaWork w;
   __shared__ int r_s, nunion_s;
-  __shared__ int wsum[kWarps];
+  __shared__ int wsum[kMaskWarps];
   __shared__ __align__(8) uint64_t bars[2 * kMaskMaxStages];
-  __shared__ __align__(16) double rmax_s[kWarps * kStride];
-  __shared__ __align__(16) float amax_s[kWarps * kTmaxSub];
-  const int per_sb = gblock * ntiles;
+  __shared__ __align__(16) double rmax_s[kMaskWarps * kStride];
+  __shared__ __align__(16) float amax_s[kMaskWarps * kTmaxSub];
+  const int per_sb = gblock * ntiles * 2;
   const int sb = static_cast<int>(blockIdx.x) / per_sb, rr = static_cast<int>(blockIdx.x) % per_sb;
   const int g0 = sb * gblock, gg = min(gblock, ngroups - g0);
-  const int tile = rr / gg, group = g0 + rr % gg;
+  const int half = rr & 1, tile = (rr >> 1) / gg, group = g0 + (rr >> 1) % gg;
   if (group >= b.wl_group0[kSweepRank + 1]) return;
   if (threadIdx.x == 0) {
     int r = 0;
     while (r < kSweepRank && group >= b.wl_group0[r + 1]) ++r;
     r_s = r;
     const int per = cand_per_cta(r);
-    const int first = (group - b.wl_group0[r]) * per;
+    const int first = (group - b.wl_group0[r]) * per + half * kMaskWarps;
     int n = 0;
-    for (int j = 0; j < per; ++j)
+    for (int j = 0; j < kMaskWarps; ++j)
       if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
     w.ncand = n;
     w.group = group;
+    w.half = half;
     for (int s = 0; s < kMaskMaxStages; ++s) {
       mbar_init(bars + s, 1);
-      mbar_init(bars + kMaskMaxStages + s, kWarps);
+      mbar_init(bars + kMaskMaxStages + s, kMaskWarps);
     }
     asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
   }
+  __syncthreads();
+  if (w.ncand == 0) return;  // the group's second half can be empty
   // union of the CTA's masks for this tile, then the union row list
   const int nch = b.nchunks;
   uint32_t* su = reinterpret_cast<uint32_t*>(msm);
@@ -940,7 +948,7 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     cudaFuncSetAttribute(k_sweep_hi<true, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmMask>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_sweep_masked, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kStageBudget));
+    cudaFuncSetAttribute(k_sweep_masked, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaskBudget));
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
   static const int gblock_env = [] {
@@ -959,7 +967,7 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     k_sweep<false, kTmMask><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
     k_sweep_hi<false, kTmMask><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
   } else if (b.t_mode == kTmMasked) {
-    k_sweep_masked<<<grid, kThreads, kStageBudget, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_masked<<<2 * grid, kMaskThreads, kMaskBudget, stream>>>(g, b, ntiles, ngroups, gblock);
   } else {
     k_sweep<false, kTmSingle><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
     k_sweep_hi<false, kTmSingle><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
