@@ -54,7 +54,8 @@ constexpr int kChunk = 32;               // branches per pipeline stage
 constexpr int kMaxCand = kWarps;         // one candidate per warp
 constexpr int kGroupBlock = 8;           // candidate groups per CTA super-block (L2 reuse)
 constexpr int kMaxStages = 8;
-constexpr size_t kStageBudget = 216 * 1024;  // dynamic shared memory for the stage ring
+constexpr size_t kStageBudget = 216 * 1024;  // dynamic shared memory for the stage ring (one CTA per SM)
+constexpr size_t kHalfBudget = 104 * 1024;   // the same for half-group CTAs (two per SM)
 constexpr int kSubLanes = 32 / kTmaxSub;     // lanes per skip sub-tile
 static_assert(kTileK % kTmaxSub == 0 && kSubLanes * kTmaxSub == 32, "sub-tile layout");
 static_assert(kMaxCand == kGroupSlots && kChunk == kChunkRows, "sweep tiles must match the row layout");
@@ -67,21 +68,30 @@ __host__ __device__ constexpr int cand_per_cta(int) { return kWarps; }
 // masked sweep of one profile (k_sweep_masked: only the rows marked by mode 1).
 constexpr int kTmSingle = 0, kTmMask = 1, kTmMasked = 2;
 
-template <int R, bool FULL, int TM = kTmSingle>
+// Warps (candidates) per sweep CTA: a whole group of 16 at one CTA per SM, or
+// (HALF, scores-only kernels on grids with few row chunks) half a group at two
+// CTAs per SM, so one CTA's prologue, barrier waits and tail overlap the other's
+// rows; on long sweeps the whole-group CTA streams the skip records once.
+template <bool HALF>
+__host__ __device__ constexpr int cta_warps() { return HALF ? kWarps / 2 : kWarps; }
+constexpr int kHalfMaxRows = 4096;  // branch rows up to which the scores-only sweep uses half-group CTAs
+
+template <int R, bool FULL, int TM = kTmSingle, bool HALF = false>
 struct Ring {
   static constexpr int S = row_stride(TM == kTmMask ? R + 1 : R);
   static constexpr int H = FULL ? 1 : (S <= 4 ? 4 : (S <= 10 ? 2 : 1));          // 32-row chunks per stage
-  static constexpr size_t FH = static_cast<size_t>(kMaxCand) * kChunk * S;       // one chunk of candidate rows
+  static constexpr size_t FH = static_cast<size_t>(cta_warps<HALF>()) * kChunk * S;  // one chunk of candidate rows
   static constexpr size_t T = FULL ? static_cast<size_t>(kChunk) * kTileK : 0;  // T_base tile rows
   static constexpr size_t F = H * FH;                                           // candidate rows
   static constexpr size_t L = H * kChunk;                                       // limits
   static constexpr size_t M = FULL ? 0 : static_cast<size_t>(H) * kChunk * kRec / 2;  // skip records (floats)
   static constexpr size_t doubles = T + F + L + M;
-  static constexpr size_t fit = kStageBudget / (doubles * sizeof(double));
+  static constexpr size_t fit = (HALF ? kHalfBudget : kStageBudget) / (doubles * sizeof(double));
   static constexpr int stages = fit < static_cast<size_t>(kMaxStages) ? static_cast<int>(fit) : kMaxStages;
   static_assert(stages >= 2, "stage ring too small");
 };
 constexpr size_t kSmemBytes = kStageBudget + 128;
+constexpr size_t kHalfSmemBytes = kHalfBudget + 128;
 
 __device__ __forceinline__ uint32_t smem_u32(const void* p) {
   return static_cast<uint32_t>(__cvta_generic_to_shared(p));
@@ -120,27 +130,33 @@ struct CtaWork {
   int cand[kMaxCand];
   int ncand;
   int group;
-  int half;  // k_sweep_masked: which half of the group (kMaskWarps candidates)
+  int half;  // which part of the group a half-group CTA takes (k_sweep scores-only, k_sweep_masked)
 };
 
 // Producer: stage <- stage-chunk i = 32-row chunks [H i, H i + H) (T tile rows
 // when FULL, the group's candidate rows, limits, skip records when not FULL).
-template <int R, bool FULL, int TM>
+template <int R, bool FULL, int TM, bool HALF>
 __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, int i,
                                            double* stage, uint64_t* bar) {
-  using Rg = Ring<R, FULL, TM>;
+  using Rg = Ring<R, FULL, TM, HALF>;
   const int e0 = i * Rg::H * kChunk;
   const int rows = min(Rg::H * kChunk, g.E - e0);
   const int nch = (rows + kChunk - 1) / kChunk;
   const uint32_t bt = FULL ? rows * kTileK * sizeof(double) : 0;
-  const uint32_t bf = nch * Rg::FH * sizeof(double);  // the group's rows of these chunks: one contiguous block
+  const uint32_t bf = nch * Rg::FH * sizeof(double);
   const uint32_t bl = ((rows + 1) & ~1) * sizeof(double);
   const uint32_t bm = Rg::M ? rows * kRec * sizeof(float) : 0;
   mbar_expect_tx(bar, bt + bf + bl + bm);
   if (FULL) bulk_g2s(stage, g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK, bt, bar);
   const double* rows_src = TM == kTmMask ? b.feat_mt : b.feat;
-  bulk_g2s(stage + Rg::T, rows_src + feat_index(w.group * kGroupSlots, b.nchunks, e0, TM == kTmMask ? R + 1 : R), bf,
-           bar);
+  const int rl = TM == kTmMask ? R + 1 : R, slot0 = w.group * kGroupSlots + w.half * cta_warps<HALF>();
+  if (cta_warps<HALF>() == kGroupSlots) {  // the whole group's rows of these chunks: one contiguous block
+    bulk_g2s(stage + Rg::T, rows_src + feat_index(slot0, b.nchunks, e0, rl), bf, bar);
+  } else {  // half a group: one block per chunk
+    for (int h = 0; h < nch; ++h)
+      bulk_g2s(stage + Rg::T + h * Rg::FH, rows_src + feat_index(slot0, b.nchunks, e0 + h * kChunk, rl),
+               static_cast<uint32_t>(Rg::FH * sizeof(double)), bar);
+  }
   bulk_g2s(stage + Rg::T + Rg::F, g.br_lim + e0, bl, bar);
   if (Rg::M)
     bulk_g2s(stage + Rg::T + Rg::F + Rg::L, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kRec, bm,
@@ -148,10 +164,10 @@ __device__ __forceinline__ void issue_chunk(const DevGrid& g, const Batch& b, co
   static_assert(kRec % 4 == 0, "skip records are whole float4");
 }
 
-template <int R, bool FULL, int TM = kTmSingle>
+template <int R, bool FULL, int TM = kTmSingle, bool HALF = false>
 __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile, double* smem,
                                           uint64_t* bars, double* rmax_s, float* amax_s) {
-  using Rg = Ring<R, FULL, TM>;
+  using Rg = Ring<R, FULL, TM, HALF>;
   constexpr int S = Rg::S, NST = Rg::stages;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int kb = tile * kTileK + lane * kKpl;
@@ -230,7 +246,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
   unsigned rows_computed = 0, rows_offered = 0, rows_exact = 0, rows_partial = 0;  // skip statistics
   if (threadIdx.x == 0)
     for (int s = 0; s < NST && s < nchunks; ++s)
-      issue_chunk<R, FULL, TM>(g, b, w, tile, s, smem + s * Rg::doubles, bars + s);
+      issue_chunk<R, FULL, TM, HALF>(g, b, w, tile, s, smem + s * Rg::doubles, bars + s);
 
   // exact path for one branch row: energies (registers) and fmax (atomicMax)
   auto exact_row = [&](int e, double lim, const double (&f1)[kKpl]) {
@@ -423,7 +439,7 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     if (threadIdx.x == 0 && i + NST < nchunks) {
       mbar_wait(bars + kMaxStages + s, (i / NST) & 1);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue_chunk<R, FULL, TM>(g, b, w, tile, i + NST, smem + s * Rg::doubles, bars + s);
+      issue_chunk<R, FULL, TM, HALF>(g, b, w, tile, i + NST, smem + s * Rg::doubles, bars + s);
     }
     __syncwarp();
   }
@@ -447,49 +463,54 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
 // while the super-block's candidate rows stay in L2 across its tiles.
 constexpr int kFastRank = 7;
 
-// CTA setup for (group, rank r): the candidate list and fresh stage barriers.
-__device__ __forceinline__ void cta_setup(const Batch& b, int group, int r, CtaWork& w, uint64_t* bars) {
-  const int per = cand_per_cta(r);
-  const int first = (group - b.wl_group0[r]) * per;
+// CTA setup for (group, half, rank r): the candidate list and fresh stage barriers.
+template <bool HALF>
+__device__ __forceinline__ void cta_setup(const Batch& b, int group, int half, int r, CtaWork& w, uint64_t* bars) {
+  constexpr int W = cta_warps<HALF>();
+  const int first = (group - b.wl_group0[r]) * cand_per_cta(r) + half * W;
   int n = 0;
-  for (int j = 0; j < per; ++j)
+  for (int j = 0; j < W; ++j)
     if (first + j < b.wl_count[r]) w.cand[n++] = b.wl_list[b.wl_start[r] + first + j];
   w.ncand = n;
   w.group = group;
-  for (int s = 0; s < kMaxStages; ++s) mbar_init(bars + s, 1), mbar_init(bars + kMaxStages + s, kWarps);
+  w.half = half;
+  for (int s = 0; s < kMaxStages; ++s) mbar_init(bars + s, 1), mbar_init(bars + kMaxStages + s, W);
   asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
 }
 
-template <bool FULL, int TM>
-__global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
+template <bool FULL, int TM, bool HALF>
+__global__ void __launch_bounds__(32 * cta_warps<HALF>(), HALF ? 2 : 1)
+    k_sweep(DevGrid g, Batch b, int ntiles, int ngroups, int gblock) {
+  constexpr int W = cta_warps<HALF>(), halves = kGroupSlots / W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CtaWork w;
   __shared__ int r_s;
-  __shared__ __align__(16) double rmax_s[kWarps * kStride];
-  __shared__ __align__(16) float amax_s[kWarps * kTmaxSub];
+  __shared__ __align__(16) double rmax_s[W * kStride];
+  __shared__ __align__(16) float amax_s[W * kTmaxSub];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* smem = reinterpret_cast<double*>(smem_raw + 128);
-  const int per_sb = gblock * ntiles;
+  const int per_sb = gblock * ntiles * halves;
   const int sb = static_cast<int>(blockIdx.x) / per_sb, rr = static_cast<int>(blockIdx.x) % per_sb;
   const int g0 = sb * gblock, gg = min(gblock, ngroups - g0);
-  const int tile = rr / gg, group = g0 + rr % gg;
+  const int half = rr % halves, tile = (rr / halves) / gg, group = g0 + (rr / halves) % gg;
   if (group >= b.wl_group0[kFastRank + 1]) return;  // higher ranks: k_sweep_hi
   if (threadIdx.x == 0) {
     int r = 0;
     while (r < kFastRank && group >= b.wl_group0[r + 1]) ++r;
     r_s = r;
-    cta_setup(b, group, r, w, bars);
+    cta_setup<HALF>(b, group, half, r, w, bars);
   }
   __syncthreads();
+  if (w.ncand == 0) return;  // a group's second half can be empty
   switch (r_s) {
-    case 0: sweep_cta<0, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 1: sweep_cta<1, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 2: sweep_cta<2, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 3: sweep_cta<3, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 4: sweep_cta<4, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 5: sweep_cta<5, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    case 6: sweep_cta<6, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-    default: sweep_cta<7, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 0: sweep_cta<0, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 1: sweep_cta<1, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 2: sweep_cta<2, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 3: sweep_cta<3, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 4: sweep_cta<4, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 5: sweep_cta<5, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    case 6: sweep_cta<6, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+    default: sweep_cta<7, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
   }
 }
 
@@ -497,32 +518,36 @@ __global__ void __launch_bounds__(kThreads, 1) k_sweep(DevGrid g, Batch b, int n
 // nodes; rare): a persistent kernel over their (tile, group) items, so its
 // register allocation stays out of the common kernel and an empty bucket
 // costs one short launch.
-template <bool FULL, int TM>
-__global__ void __launch_bounds__(kThreads, 1) k_sweep_hi(DevGrid g, Batch b, int ntiles) {
+template <bool FULL, int TM, bool HALF>
+__global__ void __launch_bounds__(32 * cta_warps<HALF>(), HALF ? 2 : 1) k_sweep_hi(DevGrid g, Batch b, int ntiles) {
+  constexpr int W = cta_warps<HALF>(), halves = kGroupSlots / W;
   extern __shared__ __align__(128) unsigned char smem_raw[];
   __shared__ CtaWork w;
   __shared__ int r_s;
-  __shared__ __align__(16) double rmax_s[kWarps * kStride];
-  __shared__ __align__(16) float amax_s[kWarps * kTmaxSub];
+  __shared__ __align__(16) double rmax_s[W * kStride];
+  __shared__ __align__(16) float amax_s[W * kTmaxSub];
   uint64_t* bars = reinterpret_cast<uint64_t*>(smem_raw);
   double* smem = reinterpret_cast<double*>(smem_raw + 128);
   const int gbeg = b.wl_group0[kFastRank + 1], gend = b.wl_group0[kSweepRank + 1];
-  const long items = static_cast<long>(gend - gbeg) * ntiles;
+  const long items = static_cast<long>(gend - gbeg) * ntiles * halves;
   for (long it = blockIdx.x; it < items; it += gridDim.x) {
-    const int group = gbeg + static_cast<int>(it / ntiles), tile = static_cast<int>(it % ntiles);
+    const int half = static_cast<int>(it % halves);
+    const long gi = it / halves;
+    const int group = gbeg + static_cast<int>(gi / ntiles), tile = static_cast<int>(gi % ntiles);
     __syncthreads();  // the previous item is done with the barriers and shared state
     if (threadIdx.x == 0) {
       int r = kFastRank + 1;
       while (r < kSweepRank && group >= b.wl_group0[r + 1]) ++r;
       r_s = r;
-      cta_setup(b, group, r, w, bars);
+      cta_setup<HALF>(b, group, half, r, w, bars);
     }
     __syncthreads();
+    if (w.ncand == 0) continue;
     switch (r_s) {
-      case 8: sweep_cta<8, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-      case 9: sweep_cta<9, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-      case 10: sweep_cta<10, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
-      default: sweep_cta<11, FULL, TM>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      case 8: sweep_cta<8, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      case 9: sweep_cta<9, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      case 10: sweep_cta<10, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
+      default: sweep_cta<11, FULL, TM, HALF>(g, b, w, tile, smem, bars, rmax_s, amax_s); break;
     }
   }
 }
@@ -941,13 +966,17 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
                   int* launched) {
   static std::atomic<unsigned long long> configured{0};
   if (first_use_on_device(configured)) {
-    const int sm = static_cast<int>(kSmemBytes);
-    cudaFuncSetAttribute(k_sweep<true, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_sweep<false, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_sweep<false, kTmMask>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_sweep_hi<true, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
-    cudaFuncSetAttribute(k_sweep_hi<false, kTmMask>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    const int sm = static_cast<int>(kSmemBytes), hm = static_cast<int>(kHalfSmemBytes);
+    cudaFuncSetAttribute(k_sweep<true, kTmSingle, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep<false, kTmSingle, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep<false, kTmSingle, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
+    cudaFuncSetAttribute(k_sweep<false, kTmMask, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep<false, kTmMask, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
+    cudaFuncSetAttribute(k_sweep_hi<true, kTmSingle, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
+    cudaFuncSetAttribute(k_sweep_hi<false, kTmMask, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
+    cudaFuncSetAttribute(k_sweep_hi<false, kTmMask, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
     cudaFuncSetAttribute(k_sweep_masked, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaskBudget));
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
@@ -959,18 +988,28 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
   const int gblock = std::min(ngroups, gblock_env ? gblock_env : kGroupBlock);
   const unsigned grid = static_cast<unsigned>(ntiles) * ngroups;
   if (ev0) cudaEventRecord(ev0, stream);
-  constexpr int kHiCtas = 148;  // persistent: one CTA per SM
+  constexpr int kHiCtas = 148;  // persistent: one CTA per SM (two half-group CTAs)
+  constexpr int hw = 32 * cta_warps<true>(), hh = kGroupSlots / cta_warps<true>();
+  const bool half = g.E <= kHalfMaxRows;
   if (full) {
-    k_sweep<true, kTmSingle><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
-    k_sweep_hi<true, kTmSingle><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
-  } else if (b.t_mode == kTmMask) {
-    k_sweep<false, kTmMask><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
-    k_sweep_hi<false, kTmMask><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+    k_sweep<true, kTmSingle, false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_hi<true, kTmSingle, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
   } else if (b.t_mode == kTmMasked) {
     k_sweep_masked<<<2 * grid, kMaskThreads, kMaskBudget, stream>>>(g, b, ntiles, ngroups, gblock);
+  } else if (b.t_mode == kTmMask) {
+    if (half) {
+      k_sweep<false, kTmMask, true><<<grid * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+      k_sweep_hi<false, kTmMask, true><<<kHiCtas * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles);
+    } else {
+      k_sweep<false, kTmMask, false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+      k_sweep_hi<false, kTmMask, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+    }
+  } else if (half) {
+    k_sweep<false, kTmSingle, true><<<grid * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_hi<false, kTmSingle, true><<<kHiCtas * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles);
   } else {
-    k_sweep<false, kTmSingle><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
-    k_sweep_hi<false, kTmSingle><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
+    k_sweep<false, kTmSingle, false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
+    k_sweep_hi<false, kTmSingle, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
   }
   if (ev1) cudaEventRecord(ev1, stream);
   *launched += 2;
