@@ -238,6 +238,7 @@ struct tg_context {
   double* mt_fc = nullptr;      // [n_t][n][E] candidate flows per profile
   double* mt_al = nullptr;      // [n_t][n][Kpad] alpha per profile
   double* mt_rk = nullptr;      // [cap][Kpad][kStride] profile-independent contingency factors
+  unsigned long long* mt_fmax = nullptr;  // [kMaskProfiles][cap][E] max |f| per profile of one masked launch
   double* mt_energy = nullptr;  // [n_t][cap][Kall]
   int* mt_nc0 = nullptr;        // [n_t][cap]
   // island merge buffers (allocated on the first merge)
@@ -362,7 +363,7 @@ void tg_context::ensure_capacity(int n) {
     const size_t kdat_sz = static_cast<size_t>(cap) * std::max<size_t>(Kp, 1) * tgb::kStride;
     const size_t ntiles = std::max<size_t>(Kp / tgb::sweep_tile_k(), 1);
     const size_t need = sizeof(double) * (static_cast<size_t>(n_t) * cap * (static_cast<size_t>(E) + Kp + Ka) +
-                                          feat_sz + kdat_sz) +
+                                          feat_sz + kdat_sz + static_cast<size_t>(tgb::kMaskProfiles) * cap * E) +
                         static_cast<size_t>(n_t) * cap * sizeof(int) +
                         static_cast<size_t>(cap) * ntiles * (tgb::kTmaxSub + tgb::kStride) * 8 +
                         static_cast<size_t>(cap) * ntiles * b.nchunks * 4;
@@ -374,6 +375,7 @@ void tg_context::ensure_capacity(int n) {
       mt_fc = A.alloc<double>(static_cast<size_t>(n_t) * cap * std::max<size_t>(E, 1));
       mt_al = A.alloc<double>(static_cast<size_t>(n_t) * cap * std::max<size_t>(Kp, 1));
       mt_rk = A.alloc<double>(kdat_sz);
+      mt_fmax = A.alloc<unsigned long long>(static_cast<size_t>(tgb::kMaskProfiles) * cap * std::max<size_t>(E, 1));
       mt_energy = A.alloc<double>(static_cast<size_t>(n_t) * cap * Ka);
       mt_nc0 = A.alloc<int>(static_cast<size_t>(n_t) * cap);
       b.feat_mt = A.alloc<double>(feat_sz);
@@ -474,22 +476,35 @@ int tg_context::enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed
   bm.t_mode = 1;
   if (g.Ks > 0) tgb::launch_sweep(g_mt, bm, false, stream, timed ? sw0 : nullptr, timed ? sw1 : nullptr, &kernels);
   if (timed && g.Ks > 0) time_sweep_done();
-  for (int t = 0; t < n_t; ++t) {
-    tgb::Batch bt = view(t);
-    bt.out = tscores;
-    bt.t_mode = 2;
-    bt.feat_mt = nullptr;
-    bt.amx_mt = nullptr;
-    bt.rmx_mt = nullptr;
-    check(cudaMemsetAsync(bt.fmax, 0, static_cast<size_t>(n) * g.E * sizeof(unsigned long long), stream), "memset");
-    check(cudaMemsetAsync(bt.fbus, 0, static_cast<size_t>(n) * g.E * sizeof(unsigned long long), stream), "memset");
-    check(cudaMemsetAsync(bt.isl_out, 0, n * sizeof(int), stream), "memset");
-    check(cudaMemsetAsync(bt.isl_bus, 0, n * sizeof(int), stream), "memset");
-    if (g.Ks > 0)
-      tgb::launch_sweep(gt[t], bt, false, stream, timed ? sw0 : nullptr, timed ? sw1 : nullptr, &kernels);
-    if (timed && g.Ks > 0) time_sweep_done();
-    kernels += tgb::launch_special_finish(gt[t], bt, n_a, n_d, false, scratch, stream);
-    kernels += tgb::launch_accumulate_timestep(bt, bv.out, bv.energy, g.Kall, t == 0, stream);
+  // masked sweeps of kMaskProfiles profiles per launch (per-profile fmax
+  // buffers), then per profile special outages, scores, accumulation
+  const size_t fmax_n = static_cast<size_t>(n) * g.E;
+  for (int t0 = 0; t0 < n_t; t0 += tgb::kMaskProfiles) {
+    const int np = std::min(tgb::kMaskProfiles, n_t - t0);
+    tgb::Batch bs = view(t0);
+    bs.t_mode = 2;
+    bs.fmax = mt_fmax;
+    check(cudaMemsetAsync(mt_fmax, 0, np * fmax_n * sizeof(unsigned long long), stream), "memset");
+    if (g.Ks > 0) {
+      tgb::MtMask mm{t0, np, static_cast<size_t>(n) * g.E, static_cast<size_t>(n) * g.Kpad,
+                     static_cast<size_t>(n) * Ka, fmax_n, mt_prof.tmax, mt_prof.alpha0};
+      tgb::launch_sweep_masked(gt[t0], bs, mm, stream, timed ? sw0 : nullptr, timed ? sw1 : nullptr, &kernels);
+      if (timed) time_sweep_done();
+    }
+    for (int p = 0; p < np; ++p) {
+      const int t = t0 + p;
+      tgb::Batch bt = view(t);
+      bt.out = tscores;
+      bt.feat_mt = nullptr;
+      bt.amx_mt = nullptr;
+      bt.rmx_mt = nullptr;
+      bt.fmax = mt_fmax + p * fmax_n;
+      check(cudaMemsetAsync(bt.fbus, 0, fmax_n * sizeof(unsigned long long), stream), "memset");
+      check(cudaMemsetAsync(bt.isl_out, 0, n * sizeof(int), stream), "memset");
+      check(cudaMemsetAsync(bt.isl_bus, 0, n * sizeof(int), stream), "memset");
+      kernels += tgb::launch_special_finish(gt[t], bt, n_a, n_d, false, scratch, stream);
+      kernels += tgb::launch_accumulate_timestep(bt, bv.out, bv.energy, g.Kall, t == 0, stream);
+    }
   }
   kernels += tgb::launch_finish_aggregate(bv, g.Kall, stream);
   return kernels;
@@ -850,12 +865,15 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     {
       // per-profile table pointers for k_prep_mt
       std::vector<const double*> f0p, thp, injp, a0p;
+      std::vector<const float*> tmp;
       for (const auto& gv : ctx->gt) {
         f0p.push_back(gv.f0);
         thp.push_back(gv.theta0);
         injp.push_back(gv.inj_net);
         a0p.push_back(gv.alpha0);
+        tmp.push_back(gv.Tmax);
       }
+      ctx->mt_prof.tmax = A.upload(tmp, s);
       ctx->mt_prof.f0 = A.upload(f0p, s);
       ctx->mt_prof.theta0 = A.upload(thp, s);
       ctx->mt_prof.inj_net = A.upload(injp, s);

@@ -129,6 +129,7 @@ struct MtProfiles {
   const double* const* theta0;   // [n_t] base angles (reduced)
   const double* const* inj_net;  // [n_t] injections
   const double* const* alpha0;   // [n_t] unchanged-topology flow factors
+  const float* const* tmax;      // [n_t] skip records
   int n_t;
   double* fc;  // [n_t][n][E] candidate flows per profile (compact)
   double* al;  // [n_t][n][Kpad] alpha per profile
@@ -151,6 +152,18 @@ int sweep_chunk();
 bool masked_sweep_fits(int E);  // k_sweep_masked's shared-memory plan holds for E rows
 void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cudaEvent_t ev0, cudaEvent_t ev1,
                   int* launched);
+// Masked timestep sweep (Batch::t_mode 2) of profiles [t0, t0 + np): b's fc_t,
+// al_t, energy and fmax point at profile t0's arrays, profile t0 + p at
+// + p * the strides; per-profile skip records and alpha0 through device arrays.
+struct MtMask {
+  int t0, np;
+  size_t fc_stride, al_stride, energy_stride, fmax_stride;
+  const float* const* tmax;
+  const double* const* alpha0;
+};
+constexpr int kMaskProfiles = 8;  // profiles per masked launch
+void launch_sweep_masked(const DevGrid& g, Batch& b, const MtMask& mm, cudaStream_t stream, cudaEvent_t ev0,
+                         cudaEvent_t ev1, int* launched);
 // Rank buckets -> sweep groups; assigns every swept candidate its row slot.
 void launch_bucket(Batch& b, cudaStream_t stream, int* launched);
 // Upper bound on sweep groups for n candidates (every rank bucket rounds up).

@@ -65,8 +65,9 @@ __host__ __device__ constexpr int cand_per_cta(int) { return kWarps; }
 // Stage ring geometry for rank R (doubles per stage, number of stages).
 // Timestep modes (Batch::t_mode): 0 one profile, 1 mask generation over all
 // profiles (k_sweep with rows [max f_c, min f_c, L...], no element work), 2
-// masked sweep of one profile (k_sweep_masked: only the rows marked by mode 1).
-constexpr int kTmSingle = 0, kTmMask = 1, kTmMasked = 2;
+// masked sweep (k_sweep_masked, launch_sweep_masked: only the rows marked by
+// mode 1, kMaskProfiles profiles per launch).
+constexpr int kTmSingle = 0, kTmMask = 1;
 
 // Warps (candidates) per sweep CTA: a whole group of 16 at one CTA per SM, or
 // (HALF, scores-only kernels on grids with few row chunks) half a group at two
@@ -590,7 +591,7 @@ __host__ __device__ inline MaskedPlan masked_plan(int E, int S) {
 template <int R>
 __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, const CtaWork& w, int tile,
                                            uint8_t* smem, uint64_t* full_bar, uint64_t* empty_bar, int nunion,
-                                           double* rmax_s, float* amax_s) {
+                                           double* rmax_s, float* amax_s, const MtMask& mm) {
   constexpr int S = row_stride(R);
   const MaskedPlan plan = masked_plan(g.E, S);
   const int NST = plan.stages;
@@ -604,19 +605,12 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
   int kbr[kKpl], rem[kMaxRemovedSweep];
   int cid = warp < w.ncand ? w.cand[warp] : -1;
   if (cid >= 0 && b.status[cid] != 0) cid = -1;
+  const int c = cid >= 0 ? cid : w.cand[0];
   {
-    // this profile's alpha and the shared rk rows: R'_t = rk * alpha_t (as k_prep)
-    const int c = cid >= 0 ? cid : w.cand[0];
-    const double* kr = b.rk_mt + static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(kb) * S;
-    const double* al = b.al_t + static_cast<size_t>(c) * g.Kpad + kb;
     const uint8_t* kf = b.kflag + static_cast<size_t>(c) * g.Kpad + kb;
 #pragma unroll
     for (int i = 0; i < kKpl; ++i) {
       kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
-      alpha[i] = al[i];
-#pragma unroll
-      for (int q = 0; q < R; ++q) rr[i][q] = kr[i * S + 1 + q] * alpha[i];
-      energy[i] = 0.0;
       kval[i] = cid >= 0 && kf[i] == 0;
     }
 #pragma unroll
@@ -625,11 +619,11 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
   const int ntiles = g.Kpad / kTileK;
   const uint32_t* mw = b.mask + (static_cast<size_t>(cid >= 0 ? cid : 0) * ntiles + tile) * b.nchunks;
   const size_t slot = static_cast<size_t>(w.group) * kGroupSlots + w.half * kMaskWarps + warp;
-  unsigned long long* fmx = b.fmax + static_cast<size_t>(cid >= 0 ? cid : 0) * g.E;
+  unsigned long long* fmx = b.fmax;
   const double* tk_tile = g.TK + static_cast<size_t>(tile) * g.E * kTileK;
-  const int nb = (nunion + kMaskBatch - 1) / kMaskBatch;
-  auto issue = [&](int j) {
-    const int s = j % NST, r0 = j * kMaskBatch, nr = min(kMaskBatch, nunion - r0);
+  const int nb = (nunion + kMaskBatch - 1) / kMaskBatch, nJ = nb * mm.np;  // batches over all profiles
+  auto issue = [&](int J) {
+    const int s = J % NST, r0 = (J % nb) * kMaskBatch, nr = min(kMaskBatch, nunion - r0);
     uint64_t* bar = full_bar + s;
     mbar_expect_tx(bar, static_cast<uint32_t>(nr * kTileK * 8));
     double* dst = const_cast<double*>(ring) + static_cast<size_t>(s) * kMaskBatch * kTileK;
@@ -637,15 +631,32 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
       bulk_g2s(dst + r * kTileK, tk_tile + static_cast<size_t>(ul[r0 + r]) * kTileK, kTileK * 8, bar);
   };
   if (threadIdx.x == 0)
-    for (int j = 0; j < NST && j < nb; ++j) issue(j);
-  // this profile's stage-1 bound operands (sweep_cta): max |alpha - alpha0| per
-  // sub-tile (float, rounded up) and max |R'_q| over the tile, per warp
+    for (int J = 0; J < NST && J < nJ; ++J) issue(J);
   float* asub = amax_s + warp * kTmaxSub;
   double* rms = rmax_s + warp * kStride;
-  {
+  const double* fc_p = b.fc_t;
+  const float* rec_tile = nullptr;
+  // per profile: alpha and R' = rk * alpha (k_prep's rounding), the stage-1
+  // bound operands (sweep_cta: max |alpha - alpha0| per sub-tile as a float
+  // rounded up, max |R'_q| over the tile, per warp)
+  auto profile_setup = [&](int p) {
+    const int t = mm.t0 + p;
+    const double* kr = b.rk_mt + static_cast<size_t>(c) * g.Kpad * kStride + static_cast<size_t>(kb) * S;
+    const double* al = b.al_t + p * mm.al_stride + static_cast<size_t>(c) * g.Kpad + kb;
+#pragma unroll
+    for (int i = 0; i < kKpl; ++i) {
+      alpha[i] = al[i];
+#pragma unroll
+      for (int q = 0; q < R; ++q) rr[i][q] = kr[i * S + 1 + q] * alpha[i];
+      energy[i] = 0.0;
+    }
+    fc_p = b.fc_t + p * mm.fc_stride;
+    rec_tile = mm.tmax[t] + static_cast<size_t>(tile) * (g.E + kChunk) * kRec;
+    fmx = b.fmax + p * mm.fmax_stride + static_cast<size_t>(cid >= 0 ? cid : 0) * g.E;
+    const double* a0 = mm.alpha0[t];
     double a = 0.0;
 #pragma unroll
-    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[k] - g.alpha0[kb + k]));
+    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[k] - a0[kb + k]));
 #pragma unroll
     for (int o = kSubLanes / 2; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
     if (lane % kSubLanes == 0) asub[lane / kSubLanes] = __double2float_ru(a * (1.0 + 1e-12));
@@ -659,7 +670,7 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
       if (lane == 0) rms[q] = r * (1.0 + 1e-12);
     }
     __syncwarp();
-  }
+  };
   // this lane's union row of batch j: own mask bit, candidate row, limit and
   // skip record, gathered one batch ahead (registers) while the current batch
   // computes; the row is kept only if this profile's own stage-1 bound (the
@@ -669,7 +680,6 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
   double lim_n = 0.0;
   double2 fr_n[S / 2];
   float4 rec_n[kRec / 4];
-  const float* rec_tile = g.Tmax + static_cast<size_t>(tile) * (g.E + kChunk) * kRec;
   auto gather = [&](int j) {
     const int idx = j * kMaskBatch + lane;
     e_n = j < nb && idx < nunion ? ul[idx] : -1;
@@ -679,7 +689,7 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
       const double2* fr = reinterpret_cast<const double2*>(b.feat + feat_index(static_cast<int>(slot), b.nchunks, e_n, R));
 #pragma unroll
       for (int q = 0; q < S / 2; ++q) fr_n[q] = fr[q];
-      fr_n[0].x = b.fc_t[static_cast<size_t>(cid) * g.E + e_n];
+      fr_n[0].x = fc_p[static_cast<size_t>(cid) * g.E + e_n];
       lim_n = g.br_lim[e_n];
       const float4* rc = reinterpret_cast<const float4*>(rec_tile + static_cast<size_t>(e_n) * kRec);
 #pragma unroll
@@ -713,9 +723,11 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
     const double wd = static_cast<double>(taf) + lrb;
     return fma(wd, 1.0 + 1e-12, s0) >= gap;
   };
+  for (int p = 0; p < mm.np; ++p) {
+  profile_setup(p);
   gather(0);
   for (int j = 0; j < nb; ++j) {
-    const int s = j % NST;
+    const int J = p * nb + j, s = J % NST;
     const int e_l = e_n;
     const bool marked = marked_n && profile_hot();
     const double lim_l = lim_n;
@@ -727,7 +739,7 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
     __syncwarp();
     gather(j + 1);
     unsigned need = __ballot_sync(0xffffffffu, marked);
-    mbar_wait(full_bar + s, (j / NST) & 1);
+    mbar_wait(full_bar + s, (J / NST) & 1);
     const double* st = ring + static_cast<size_t>(s) * kMaskBatch * kTileK + lane * kKpl;
     while (need) {
       const int u = __ffs(need) - 1;
@@ -772,30 +784,31 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
     // release the stage; thread 0 refills it once every warp has left it
     __syncwarp();
     if (lane == 0) mbar_arrive(empty_bar + s);
-    if (threadIdx.x == 0 && j + NST < nb) {
-      mbar_wait(empty_bar + s, (j / NST) & 1);
+    if (threadIdx.x == 0 && J + NST < nJ) {
+      mbar_wait(empty_bar + s, (J / NST) & 1);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
-      issue(j + NST);
+      issue(J + NST);
     }
     __syncwarp();
   }
   if (cid >= 0) {
-    double* en = b.energy + static_cast<size_t>(cid) * g.Kall;
+    double* en = b.energy + p * mm.energy_stride + static_cast<size_t>(cid) * g.Kall;
 #pragma unroll
     for (int k = 0; k < kKpl; ++k)
       if (kval[k] && kb + k < g.Ks) en[g.ks_cont[kb + k]] = energy[k];
   }
+  }  // profiles
 }
 
 template <int R>
 __device__ __noinline__ void masked_cta_call(const DevGrid& g, const Batch& b, const CtaWork& w, int tile,
                                              uint8_t* smem, uint64_t* full_bar, uint64_t* empty_bar, int nunion,
-                                             double* rmax_s, float* amax_s) {
-  masked_cta<R>(g, b, w, tile, smem, full_bar, empty_bar, nunion, rmax_s, amax_s);
+                                             double* rmax_s, float* amax_s, const MtMask& mm) {
+  masked_cta<R>(g, b, w, tile, smem, full_bar, empty_bar, nunion, rmax_s, amax_s, mm);
 }
 
 __global__ void __launch_bounds__(kMaskThreads, 2) k_sweep_masked(DevGrid g, Batch b, int ntiles, int ngroups,
-                                                                  int gblock) {
+                                                                  int gblock, MtMask mm) {
   extern __shared__ __align__(128) uint8_t msm[];
   __shared__ CtaWork w;
   __shared__ int r_s, nunion_s;
@@ -878,19 +891,19 @@ __global__ void __launch_bounds__(kMaskThreads, 2) k_sweep_masked(DevGrid g, Bat
   uint64_t* eb = bars + kMaskMaxStages;
   const int nu = nunion_s;
   switch (r_s) {
-    case 0: masked_cta<0>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 1: masked_cta<1>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 2: masked_cta<2>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 3: masked_cta<3>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 4: masked_cta<4>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 5: masked_cta<5>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 0: masked_cta<0>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 1: masked_cta<1>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 2: masked_cta<2>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 3: masked_cta<3>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 4: masked_cta<4>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 5: masked_cta<5>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
     // higher ranks in their own call frames (register pressure of the common ones)
-    case 6: masked_cta_call<6>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 7: masked_cta_call<7>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 8: masked_cta_call<8>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 9: masked_cta_call<9>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    case 10: masked_cta_call<10>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
-    default: masked_cta_call<11>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s); break;
+    case 6: masked_cta_call<6>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 7: masked_cta_call<7>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 8: masked_cta_call<8>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 9: masked_cta_call<9>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    case 10: masked_cta_call<10>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
+    default: masked_cta_call<11>(g, b, w, tile, sm, fb, eb, nu, rmax_s, amax_s, mm); break;
   }
 }
 
@@ -977,7 +990,6 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmMask, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmMask, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
-    cudaFuncSetAttribute(k_sweep_masked, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaskBudget));
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
   static const int gblock_env = [] {
@@ -994,8 +1006,6 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
   if (full) {
     k_sweep<true, kTmSingle, false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
     k_sweep_hi<true, kTmSingle, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
-  } else if (b.t_mode == kTmMasked) {
-    k_sweep_masked<<<2 * grid, kMaskThreads, kMaskBudget, stream>>>(g, b, ntiles, ngroups, gblock);
   } else if (b.t_mode == kTmMask) {
     if (half) {
       k_sweep<false, kTmMask, true><<<grid * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
@@ -1013,6 +1023,20 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
   }
   if (ev1) cudaEventRecord(ev1, stream);
   *launched += 2;
+}
+
+void launch_sweep_masked(const DevGrid& g, Batch& b, const MtMask& mm, cudaStream_t stream, cudaEvent_t ev0,
+                         cudaEvent_t ev1, int* launched) {
+  static std::atomic<unsigned long long> configured{0};
+  if (first_use_on_device(configured))
+    cudaFuncSetAttribute(k_sweep_masked, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(kMaskBudget));
+  const int ntiles = g.Kpad / kTileK, ngroups = max_sweep_groups(b.n);
+  const int gblock = std::min(ngroups, kGroupBlock);
+  const unsigned grid = 2u * static_cast<unsigned>(ntiles) * ngroups;  // half-group CTAs
+  if (ev0) cudaEventRecord(ev0, stream);
+  k_sweep_masked<<<grid, kMaskThreads, kMaskBudget, stream>>>(g, b, ntiles, ngroups, gblock, mm);
+  if (ev1) cudaEventRecord(ev1, stream);
+  *launched += 1;
 }
 
 void launch_bucket(Batch& b, cudaStream_t stream, int* launched) {
