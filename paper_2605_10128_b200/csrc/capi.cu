@@ -424,6 +424,7 @@ int tg_context::enqueue_evaluate(tgb::Batch& bv, int n_a, int n_d, bool full, bo
   tgb::Batch bt = bv;
   bt.out = tscores;
   bt.energy = tenergy;
+  bt.no_worst = 1;
   for (int t = 0; t < n_t; ++t) {
     int k = 0;
     tgb::launch_evaluate(gt[t], bt, n_a, n_d, false, scratch, stream, &k, timed ? sw0 : nullptr,
@@ -495,6 +496,7 @@ int tg_context::enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed
       const int t = t0 + p;
       tgb::Batch bt = view(t);
       bt.out = tscores;
+      bt.no_worst = 1;
       bt.feat_mt = nullptr;
       bt.amx_mt = nullptr;
       bt.rmx_mt = nullptr;

@@ -707,6 +707,10 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_finish(DevGrid g, Batch b
     o.isl_out[c] = iso;
     o.isl_bus[c] = isb;
   }
+  if (b.no_worst) {  // one profile of a timestep grid: the worst list is ranked on the summed energies
+    if (lane == 0) o.worst_n[c] = 0;
+    return;
+  }
   warp_worst(b.energy + static_cast<size_t>(c) * g.Kall, g.Kall, b.params.worst_k, wl_v[wid], wl_i[wid],
              o.worst_idx + static_cast<size_t>(c) * b.params.worst_k,
              o.worst_val + static_cast<size_t>(c) * b.params.worst_k, o.worst_n + c, lane);

@@ -87,6 +87,7 @@ struct Batch {
   // of each (candidate, tile) that can overload at some profile, k_sweep in
   // masked mode (t_mode 2) then visits only those rows per profile.
   int t_mode;                 // 0 single profile, 1 mask generation, 2 masked sweep
+  int no_worst;               // k_finish: skip the worst list (per-profile pass of a timestep grid)
   double* feat_mt;            // rows [key(max_t f_c), key(min_t f_c), L...] at row_stride(r + 1), feat_index layout;
                               // keys are the ordered bit patterns of doubles (order_key)
   unsigned long long* amx_mt; // [n][ntiles][kTmaxSub] max_t max |alpha_t - alpha0_t| per sub-tile (bits)
