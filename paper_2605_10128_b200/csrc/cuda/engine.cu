@@ -15,7 +15,6 @@ namespace {
 
 constexpr int kPrepThreads = 256;
 constexpr int kPrepCta = 512;  // k_prep block size (a multiple of 128: the timestep bound folds)
-constexpr size_t kPrepZsmBytes = 0;  // Z = X [U | V] kept in shared memory up to this size
 
 // ---------------------------------------------------------------- K2a analysis
 // Topology analysis (one warp-sized CTA per candidate, thread 0 serial, so a
@@ -51,10 +50,9 @@ __global__ void __launch_bounds__(kAnalyzeThreads) k_analyze(DevGrid g, Batch b,
 
 // ---------------------------------------------------------------- K2 prep
 // One CTA per candidate (grid-stride over candidates). Z = X [U | V] lives in
-// shared memory (row stride row_stride(r)) when it fits in `zsm_doubles`, else
-// in the CTA's global scratch slot.
-__global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch,
-                                                       int zslots, int zsm_doubles) {
+// the CTA's global scratch slot (row stride row_stride(r); L2-resident at cfg2:
+// keeping it in shared memory measured slower, 2 CTAs per SM either way).
+__global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch) {
   extern __shared__ __align__(16) uint32_t bits[];
   __shared__ Topo t;
   __shared__ double gram[kSweepRank * kSweepRank];
@@ -64,7 +62,6 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
   const int words = (g.E + 31) >> 5;
   uint32_t* mv_bits = bits;
   uint32_t* rm_bits = bits + words;
-  double* zsm = reinterpret_cast<double*>(bits + ((2 * words + 3) & ~3));
   double* zglob = zscratch + static_cast<size_t>(blockIdx.x) * g.Nr * kStride;
   for (int c = blockIdx.x; c < b.n; c += gridDim.x) {
     const int slot = b.slot[c];
@@ -76,7 +73,7 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
     if (threadIdx.x == 0) moved_injections(g, t);  // this profile's injections (the analysis may be shared)
     double* sol = b.topo_sol ? b.topo_sol + static_cast<size_t>(c) * kTopoSol : nullptr;
     const int ldz = row_stride(t.ns + t.nv);
-    double* zbuf = static_cast<size_t>(g.Nr) * ldz <= static_cast<size_t>(zsm_doubles) ? zsm : zglob;
+    double* zbuf = zglob;
     __syncthreads();
     build_z(g, t, zbuf, ldz);
     __syncthreads();
@@ -835,16 +832,10 @@ int launch_analyze(const DevGrid& g, Batch& b, int n_a, int n_d, cudaStream_t st
 
 int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch& s, cudaStream_t stream) {
   const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
-  // Z in shared memory up to kPrepZsmBytes (0: Z in the global scratch slots,
-  // measured faster: the small serial solve needs many resident CTAs per SM)
-  const size_t bits_al = (bits_bytes + 15) & ~size_t{15};
-  const size_t zsm_bytes = std::min<size_t>(static_cast<size_t>(g.Nr) * kStride * sizeof(double), kPrepZsmBytes);
-  const int zsm_doubles = static_cast<int>(zsm_bytes / sizeof(double));
-  if (bits_al + zsm_bytes > 48 * 1024)  // (per launch: the size depends on the grid)
-    cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(bits_al + zsm_bytes));
+  if (bits_bytes > 48 * 1024)  // (per launch: the size depends on the grid)
+    cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bits_bytes));
   const int prep_grid = b.n < s.zslots ? b.n : s.zslots;
-  k_prep<<<prep_grid, kPrepCta, bits_al + zsm_bytes, stream>>>(g, b, n_a, n_d, s.zprep, s.zslots, zsm_doubles);
+  k_prep<<<prep_grid, kPrepCta, bits_bytes, stream>>>(g, b, n_a, n_d, s.zprep);
   return 1;
 }
 
