@@ -69,3 +69,17 @@ def test_timestep_scale_equals_sum_of_single_profile_contexts():
         want = sum(getattr(p, f) for p in parts)[live]
         got = getattr(agg, f)[live]
         assert np.max(np.abs(got - want) / np.maximum(1.0, np.abs(want))) <= 1e-12, f
+
+
+def test_more_profiles_than_one_masked_launch():
+    """10 profiles: the masked sweep runs kMaskProfiles (8) profiles per launch,
+    so this covers a full launch plus a partial one; against the oracle run per
+    timestep and summed."""
+    text = json.dumps(synth_grid(150, n_stations=8, seed=31, n_timesteps=10))
+    ctx = _ctx(text)
+    orcs = [OracleContext(t) for t in timestep_grids(text)]
+    assert len(orcs) == 10
+    genomes = orcs[0].random_genomes(300, 3, 2, seed=7)
+    sc = ctx.evaluate_arrays(genomes, 3, 2)
+    ref = oracle_timesteps(orcs, genomes, 3, 2)
+    compare_scores(sc, ref, 20)
