@@ -19,7 +19,7 @@ done
 NCU="ncu --set full --import-source on --clock-control none"
 $NCU -k k_sweep --launch-skip 3 -c 1 -o $OUT/sweep_cfg2_$TAG python tools/step_timing.py cfg2 4096 > /dev/null 2>&1
 $NCU -k k_sweep --launch-skip 3 -c 1 -o $OUT/sweep_cfg4_$TAG python tools/step_timing.py cfg4 16384 > /dev/null 2>&1
-$NCU -k k_sweep_masked --launch-skip 100 -c 1 -o $OUT/masked_cfg3_$TAG python tools/step_timing.py cfg3 4096 > /dev/null 2>&1
+$NCU -k k_sweep_masked --launch-skip 10 -c 1 -o $OUT/masked_cfg3_$TAG python tools/step_timing.py cfg3 4096 > /dev/null 2>&1
 $NCU -k k_prep --launch-skip 3 -c 1 -o $OUT/prep_cfg2_$TAG python tools/step_timing.py cfg2 4096 > /dev/null 2>&1
 $NCU -k k_prep --launch-skip 3 -c 1 -o $OUT/prep_cfg4_$TAG python tools/step_timing.py cfg4 16384 > /dev/null 2>&1
 ls -la $OUT
