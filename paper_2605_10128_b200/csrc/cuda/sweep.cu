@@ -682,7 +682,7 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
   float4 rec_n[kRec / 4];
   auto gather = [&](int j) {
     const int idx = j * kMaskBatch + lane;
-    e_n = j < nb && idx < nunion ? ul[idx] : -1;
+    e_n = j < nb && lane < kMaskBatch && idx < nunion ? ul[idx] : -1;
     marked_n = e_n >= 0 && cid >= 0 && ((mw[e_n >> 5] >> (e_n & 31)) & 1u);
     if (marked_n) {
       // L from profile 0's row, f_c of this profile
