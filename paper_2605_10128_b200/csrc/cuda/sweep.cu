@@ -10,11 +10,12 @@
 // branch order) and the per-(c,e) max (atomicMax on the ordered bit pattern).
 //
 // One CTA = one 128-contingency tile x one group of 16 candidates of equal
-// update rank R (one candidate per warp). Each lane owns 4 contingencies:
-// alpha / R' live in registers for the whole sweep. Candidate rows are
-// row_stride(R) doubles (f_c, L[0..R-1]), contingency rows likewise.
+// update rank R (one candidate per warp), or half a group (8 warps, two CTAs
+// per SM: k_sweep<..., HALF> on grids up to kHalfMaxRows rows). Each lane owns
+// 4 contingencies: alpha / R' live in registers for the whole sweep. Candidate
+// rows are row_stride(R) doubles (f_c, L[0..R-1]), contingency rows likewise.
 //
-// Scores-only kernel (k_sweep<false, kTmSingle>, the MapElites path): branch
+// Scores-only kernel (k_sweep<false, kTmSingle, *>, the MapElites path): branch
 // rows are streamed in stages of 1-4 chunks of 32 by TMA bulk copies
 // (cp.async.bulk + mbarrier complete_tx) into a 2-8 stage ring: the group's
 // candidate rows, the limits and the per-(tile, row) skip record (sub-tile max
@@ -34,8 +35,9 @@
 // Flows kernel (k_sweep<true>, FlowResult requested): every element computed,
 // T_base tiles streamed with the rows, max |f1| folded for every branch.
 // Ranks 8..11 run in the persistent k_sweep_hi (own register allocation).
-// Timestep grids: k_sweep<false, kTmMask> marks the rows that can overload at
-// some injection profile, k_sweep_masked visits only those per profile.
+// Timestep grids: k_sweep<false, kTmMask, *> marks the rows that can overload at
+// some injection profile; k_sweep_masked visits only those, 8 profiles per
+// launch, keeping a row for a profile only if that profile's own bound fails.
 #include <algorithm>
 #include <cstdint>
 #include <cstdlib>
