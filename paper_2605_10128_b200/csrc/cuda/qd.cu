@@ -375,22 +375,29 @@ __device__ const int* member(const Archive& a, const QdParams& p, int ns, int fl
   return a.genome + (static_cast<size_t>(lo) * p.cap + pos) * ns;
 }
 
+// Block = kOffspringLanes lane threads + one extra warp whose first thread draws
+// the iteration's mutation/crossover split, so that draw's engine seeding runs
+// beside the lanes' own seeding instead of before it.
+constexpr int kOffspringLanes = 64;
+
 template <class Rng>
 __global__ void k_offspring(DevGrid g, QdParams p, Archive a, int* genomes) {
   __shared__ int b_mc;
   const long long it = a.iter[0];
-  if (threadIdx.x == 0) {
+  const int lane = blockIdx.x * kOffspringLanes + static_cast<int>(threadIdx.x);
+  const bool is_lane = threadIdx.x < kOffspringLanes && lane < p.batch;
+  Rng r;
+  if (threadIdx.x == kOffspringLanes) {
     Rng ir;
     ir.seed(derive_seed(p.seed, 0x17e7ull, static_cast<unsigned long long>(it)));
     b_mc = uniform_int(ir, 0, p.batch);
+  } else if (is_lane) {
+    r.seed(derive_seed(p.seed, static_cast<unsigned long long>(it), static_cast<unsigned long long>(lane) + 1ull));
   }
   __syncthreads();
-  const int lane = blockIdx.x * blockDim.x + threadIdx.x;
-  if (lane >= p.batch) return;
+  if (!is_lane) return;
   const int ns = p.n_a + p.n_d;
   Ops o{g, p};
-  Rng r;
-  r.seed(derive_seed(p.seed, static_cast<unsigned long long>(it), static_cast<unsigned long long>(lane) + 1ull));
   const int total = a.flat_start[p.cells];
   int child[kMaxSlots];
   if (lane < b_mc) {
@@ -739,12 +746,12 @@ void launch_archive_reset(const QdState& q, cudaStream_t s) {
 }
 
 void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStream_t s) {
-  constexpr int kThreads = 64;  // lanes carry a 2.5 KB engine state in local memory
-  const int blocks = (q.p.batch + kThreads - 1) / kThreads;
+  // lanes carry a 2.5 KB engine state in local memory
+  const int blocks = (q.p.batch + kOffspringLanes - 1) / kOffspringLanes;
   if (q.p.rng == kRngPhilox)
-    k_offspring<Philox><<<blocks, kThreads, 0, s>>>(g, q.p, q.a, genomes);
+    k_offspring<Philox><<<blocks, kOffspringLanes + 32, 0, s>>>(g, q.p, q.a, genomes);
   else
-    k_offspring<Mt64><<<blocks, kThreads, 0, s>>>(g, q.p, q.a, genomes);
+    k_offspring<Mt64><<<blocks, kOffspringLanes + 32, 0, s>>>(g, q.p, q.a, genomes);
 }
 
 namespace {
