@@ -523,16 +523,22 @@ __device__ void warp_worst(const double* en, int K, int wk, double* lv, int* li,
                            int* out_n, int lane) {
   int npos = 0;
   unsigned long long maxbits = 0ull;  // positive doubles order like their bit patterns
-  for (int k0 = 0; k0 < K; k0 += 32) {
-    const int k = k0 + lane;
-    const double v = k < K ? en[k] : 0.0;
-    const unsigned m = __ballot_sync(0xffffffffu, v > 0.0);
-    const int at = npos + __popc(m & ((1u << lane) - 1u));
-    if (v > 0.0) {
-      if (at < kFinishList) lv[at] = v, li[at] = k;
-      maxbits = max(maxbits, static_cast<unsigned long long>(__double_as_longlong(v)));
+  for (int k0 = 0; k0 < K; k0 += 128) {
+    double vv[4];  // four blocks of 32 in flight, compacted in index order
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vv[u] = k0 + 32 * u + lane < K ? en[k0 + 32 * u + lane] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 32 * u + lane;
+      const double v = vv[u];
+      const unsigned m = __ballot_sync(0xffffffffu, v > 0.0);
+      const int at = npos + __popc(m & ((1u << lane) - 1u));
+      if (v > 0.0) {
+        if (at < kFinishList) lv[at] = v, li[at] = k;
+        maxbits = max(maxbits, static_cast<unsigned long long>(__double_as_longlong(v)));
+      }
+      npos += __popc(m);
     }
-    npos += __popc(m);
   }
   __syncwarp();
   bool listed = npos <= kFinishList;
@@ -665,13 +671,20 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_finish(DevGrid g, Batch b
   const unsigned long long* fb = b.fbus + static_cast<size_t>(c) * g.E;
   double so = 0.0, sb = 0.0;
   int nc = 0, nc0 = lane == 0 ? b.nc0[c] : 0;  // counted by k_prep
-  for (int e = lane; e < g.E; e += 32) {
-    const double lim = g.br_lim[e];
-    const double m = __longlong_as_double(static_cast<long long>(fm[e]));
-    if (m > lim) so += m - lim, ++nc;
-    if (g.Kb > 0) {  // no busbar outages: fbus stays 0
-      const double mb = __longlong_as_double(static_cast<long long>(fb[e]));
-      if (mb > lim) sb += mb - lim;
+  // four rows per lane in flight (loads first), summed in branch order per lane
+  for (int e0 = lane; e0 < g.E; e0 += 128) {
+    double lim[4], m[4], mb[4];
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int e = e0 + 32 * u;
+      lim[u] = e < g.E ? g.br_lim[e] : CUDART_INF;
+      m[u] = e < g.E ? __longlong_as_double(static_cast<long long>(fm[e])) : 0.0;
+      mb[u] = e < g.E && g.Kb > 0 ? __longlong_as_double(static_cast<long long>(fb[e])) : 0.0;  // no busbar outages: 0
+    }
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      if (m[u] > lim[u]) so += m[u] - lim[u], ++nc;
+      if (mb[u] > lim[u]) sb += mb[u] - lim[u];
     }
   }
   int isl = 0;
