@@ -7,7 +7,7 @@ set -u
 TAG=${1:-v}
 OUT=gpurun_out
 mkdir -p $OUT
-for c in cfg2 cfg3 cfg4; do
+for c in cfg1 cfg2 cfg3 cfg4; do
   python bench.py --config $c --steps 30 --warmup 5 > $OUT/bench_${c}_$TAG.json 2> $OUT/bench_${c}_$TAG.err
 done
 for cb in "cfg2 4096" "cfg3 4096" "cfg4 16384"; do
