@@ -505,9 +505,11 @@ int tg_context::enqueue_evaluate_mt(tgb::Batch& bv, int n_a, int n_d, bool timed
       check(cudaMemsetAsync(bt.isl_out, 0, n * sizeof(int), stream), "memset");
       check(cudaMemsetAsync(bt.isl_bus, 0, n * sizeof(int), stream), "memset");
       kernels += tgb::launch_special_finish(gt[t], bt, n_a, n_d, false, scratch, stream);
-      kernels += tgb::launch_accumulate_timestep(bt, bv.out, bv.energy, g.Kall, t == 0, stream);
+      kernels += tgb::launch_accumulate_timestep(bt, bv.out, nullptr, g.Kall, t == 0, stream);
     }
   }
+  kernels += tgb::launch_sum_profiles(mt_energy, n_t, static_cast<size_t>(n) * Ka, static_cast<size_t>(n) * g.Kall,
+                                      bv.energy, stream);
   kernels += tgb::launch_finish_aggregate(bv, g.Kall, stream);
   return kernels;
 }

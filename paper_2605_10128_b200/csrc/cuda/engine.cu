@@ -734,7 +734,7 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_finish(DevGrid g, Batch b
 // worst list ranks the sums), islanded if islanded at any t. With T == 1 this
 // is exactly the reference's evaluate.
 __global__ void k_accum_t(Batch bt, Scores agg, double* agg_energy, int Kall, int first) {
-  const size_t n_en = static_cast<size_t>(bt.n) * Kall;
+  const size_t n_en = agg_energy ? static_cast<size_t>(bt.n) * Kall : 0;  // null: energies summed by k_sum_profiles
   for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n_en;
        i += static_cast<size_t>(gridDim.x) * blockDim.x)
     agg_energy[i] = first ? bt.energy[i] : agg_energy[i] + bt.energy[i];
@@ -892,6 +892,23 @@ int launch_accumulate_timestep(const Batch& bt, Scores& agg, double* agg_energy,
   const size_t work = static_cast<size_t>(bt.n) * (Kall > 0 ? Kall : 1);
   const int grid = static_cast<int>(std::min<size_t>((work + 255) / 256, 148 * 8));
   k_accum_t<<<grid, 256, 0, stream>>>(bt, agg, agg_energy, Kall, first ? 1 : 0);
+  return 1;
+}
+
+// Sum of the per-profile energy arrays in profile order (the same additions as
+// k_accum_t's running sum), one pass over all profiles.
+__global__ void k_sum_profiles(const double* e, int n_t, size_t stride, size_t n, double* out) {
+  for (size_t i = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; i < n;
+       i += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    double acc = e[i];
+    for (int t = 1; t < n_t; ++t) acc = acc + e[static_cast<size_t>(t) * stride + i];
+    out[i] = acc;
+  }
+}
+
+int launch_sum_profiles(const double* e, int n_t, size_t stride, size_t n, double* out, cudaStream_t stream) {
+  const int grid = static_cast<int>(std::min<size_t>((n + 255) / 256, 148 * 8));
+  k_sum_profiles<<<grid > 0 ? grid : 1, 256, 0, stream>>>(e, n_t, stride, n, out);
   return 1;
 }
 

@@ -148,6 +148,7 @@ void launch_extract(const DevGrid& g, Batch& b, double* base_out, double* fmax_o
 int launch_accumulate_timestep(const Batch& bt, Scores& agg, double* agg_energy, int Kall, bool first,
                                cudaStream_t stream);
 int launch_finish_aggregate(Batch& b, int Kall, cudaStream_t stream);
+int launch_sum_profiles(const double* e, int n_t, size_t stride, size_t n, double* out, cudaStream_t stream);
 int sweep_tile_k();
 int sweep_chunk();
 bool masked_sweep_fits(int E);  // k_sweep_masked's shared-memory plan holds for E rows
