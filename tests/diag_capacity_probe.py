@@ -1,3 +1,4 @@
+"""Diagnostic (not collected by pytest): capacity errors of random genomes at n_a/n_d = 3/2 and 4/4 on cfg2, the failing ones checked against the oracle. Run on a GPU: python tests/diag_capacity_probe.py"""
 import sys, json, numpy as np
 sys.path.insert(0, '.')
 import paper_2605_10128_b200 as P
