@@ -261,8 +261,13 @@ __device__ __forceinline__ void sweep_cta(const DevGrid& g, const Batch& b, cons
     for (int k = 0; k < kKpl; ++k) {
       if (!kval[k] || skip_row || e == kbr[k]) continue;  // the outaged branch carries 0
       const double a = fabs(f1[k]);
-      if (a > lim) energy[k] += a - lim;
-      m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+      if (FULL) {
+        if (a > lim) energy[k] += a - lim;
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+      } else if (a > lim) {  // only a max above the limit is folded: track overloaded elements only
+        energy[k] += a - lim;
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+      }
     }
     if (cid < 0) return;
     unsigned long long* fmx = b.fmax + static_cast<size_t>(cid) * g.E;
@@ -778,8 +783,10 @@ __device__ __forceinline__ void masked_cta(const DevGrid& g, const Batch& b, con
       for (int k = 0; k < kKpl; ++k) {
         if (!kval[k] || skip_row || e == kbr[k]) continue;
         const double a = fabs(f1[k]);
-        if (a > lim) energy[k] += a - lim;
-        m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+        if (a > lim) {  // only a max above the limit is folded
+          energy[k] += a - lim;
+          m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+        }
       }
       if (m > static_cast<unsigned long long>(__double_as_longlong(lim))) atomicMax(fmx + e, m);
     }
