@@ -1,12 +1,14 @@
 """Benchmark: N-1-evaluated topologies/s of the device-resident MapElites loop.
 
-Workload (BASELINE.json configs[1]): synthetic 1k-bus / 1.5k-branch grid, a
-4096-candidate batch per generation, full single-branch N-1 over every
+Workload (default, BASELINE.json configs[3], the largest single-GPU config):
+synthetic TSO-scale 7k-bus / 10.5k-branch grid with 500 splittable stations,
+a 16384-candidate batch per generation, full single-branch N-1 over every
 listed contingency, 1 timestep. One step = one MapElites generation: device
-mutation/crossover of 4096 lanes, DC N-1 evaluation of every lane, archive
-insert (qd_optimizer.cpp:376-401), launched as one CUDA graph.
+mutation/crossover of every lane, DC N-1 evaluation of every lane, archive
+insert (qd_optimizer.cpp:376-401), launched as one CUDA graph. --config
+cfg1|cfg2|cfg3 select the other BASELINE configs.
 
-  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg2|cfg4|cfg1] [--impl b200|reference]
+  python bench.py [--gpus N] [--steps K] [--warmup W] [--config cfg4|cfg3|cfg2|cfg1] [--impl b200|reference]
 
 Multi-GPU (torchrun): one island per rank (own seed, own archive), archives
 merged every --merge-every generations (NCCL allgather of the archive blobs +
@@ -139,24 +141,40 @@ class ClockSampler:
                 "samples": len(sm)}
 
 
-def cpu_baseline(text: str, n_target_s: float = 12.0, world: int = 1):
-    """The reference algorithm (oracle restatement) on this host's cores: a
-    bounded sample of the same workload's genomes through
-    DcContext::evaluate_batch with threads = hardware concurrency."""
-    from oracle.oracle import OracleContext
+def _reference_loop(text: str, gens_warm: int, gens_timed: int, gen_seconds: float, batch_cap: int):
+    """The reference's own MapElites loop (run_optimizer, qd_optimizer.cpp:344-417,
+    restated in oracle/) on this host: mutate / crossover from its archive,
+    DcContext::evaluate_batch on all host threads (dc_engine.cpp:446-465),
+    Repertoire::insert. The per-generation batch is a bounded sample of the
+    workload's batch, sized from a probe so one generation takes about
+    gen_seconds. Returns (topologies/s over the timed generations, lanes per
+    generation, timed seconds, cores)."""
+    from oracle.oracle import OracleContext, qd_config
     orc = OracleContext(text)
     cores = os.cpu_count() or 1
-    probe = orc.random_genomes(32, 3, 2, seed=11)
-    t = orc.time_evaluate_batch(probe, 3, 2, 1)
-    n = int(max(32, min(20000, 32 * n_target_s / max(t, 1e-6))))
-    sample = orc.random_genomes(n, 3, 2, seed=12)
-    dt = orc.time_evaluate_batch(sample, 3, 2, 1)
+    probe = orc.random_genomes(max(16, cores), 3, 2, seed=11)
+    t = orc.time_evaluate_batch(probe, 3, 2, 1) / len(probe)  # seconds per lane, threaded
+    lanes = int(max(16, min(batch_cap, gen_seconds / max(t, 1e-9))))
+    lanes = min(batch_cap, -(-lanes // cores) * cores)  # whole rounds of the thread fan-out
+    gens = gens_warm + gens_timed
+    cfg = qd_config(batch_size=lanes, iters_per_epoch=1 << 30, seed=1, max_evaluations=1 + gens * lanes)
+    stamps, _ = orc.run_optimizer_timed(cfg)
+    assert len(stamps) == gens, (len(stamps), gens)
+    dt = float(stamps[-1] - stamps[gens_warm - 1])
+    T = n_timesteps(text)  # the reference evaluates one injection vector: one evaluation per timestep
+    return lanes * gens_timed / dt / T, lanes, dt * T, cores
+
+
+def cpu_baseline(text: str, batch_cap: int):
+    """cpu_baseline leg (rank 0, N=1): ~10-15 s of the reference loop."""
+    value, lanes, dt, cores = _reference_loop(text, 1, 8, 1.5, batch_cap)
     T = n_timesteps(text)
-    note = (f"; {T} timesteps = {T} reference evaluations per topology (the reference evaluates one injection "
-            f"vector; timed on one profile, rate / {T})") if T > 1 else ""
-    return {"value": n / dt / T, "unit": "topologies/s", "cores": cores, "kind": "port",
-            "sample": f"{n} random genomes (helpers.hpp random_genome, n_a=3, n_d=2) of this workload's grid, "
-                      f"full N-1, DcContext::evaluate_batch on {cores} threads, {dt:.1f} s{note}"}
+    note = (f"; {T} timesteps = {T} reference evaluations per topology (timed on one profile, rate / {T})"
+            if T > 1 else "")
+    return {"value": value, "unit": "topologies/s", "cores": cores, "kind": "port",
+            "sample": f"the reference's MapElites loop (oracle restatement of run_optimizer): 8 timed generations of "
+                      f"{lanes} lanes (bounded sample of the {batch_cap}-lane batch) after 1 warm-up generation, "
+                      f"full N-1, evaluate_batch on {cores} threads, {dt:.1f} s{note}"}
 
 
 def n_timesteps(text: str) -> int:
@@ -164,36 +182,27 @@ def n_timesteps(text: str) -> int:
 
 
 def run_reference(args, world, rank):
-    """--impl reference: the reference's CPU path on this host (rank 0 only)."""
+    """--impl reference: the reference's CPU path on this host (rank 0 only):
+    its own MapElites loop, each step one generation of a bounded lane sample."""
     if rank != 0:
         return
     text = grid_text(args.config)
-    from oracle.oracle import OracleContext
-    orc = OracleContext(text)
-    cores = os.cpu_count() or 1
-    probe = orc.random_genomes(16, 3, 2, seed=21)
-    t = orc.time_evaluate_batch(probe, 3, 2, 1)
-    per_step = int(max(16, min(CONFIGS[args.config]["batch"], 16 * 2.0 / max(t, 1e-6))))
-    for w in range(args.warmup):
-        orc.time_evaluate_batch(orc.random_genomes(per_step, 3, 2, seed=100 + w), 3, 2, 1)
-    total_n, total_t = 0, 0.0
-    for k in range(args.steps):
-        g = orc.random_genomes(per_step, 3, 2, seed=1000 + k)
-        total_t += orc.time_evaluate_batch(g, 3, 2, 1) * n_timesteps(text)  # one reference evaluation per profile
-        total_n += per_step
-    value = total_n / total_t
+    B = CONFIGS[args.config]["batch"]
+    value, lanes, dt, cores = _reference_loop(text, args.warmup, args.steps, 2.0, B)
+    T = n_timesteps(text)
     line = {"metric": "N-1-evaluated topologies/sec (DC)", "value": value, "unit": "topologies/s",
             "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
-            "ms_per_step": 1000.0 * total_t / args.steps, "higher_is_better": True, "scaling": "weak",
+            "ms_per_step": 1000.0 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (seeded generator, reference JSON format)",
             "impl": "reference",
-            "config": {"workload": CONFIGS[args.config]["workload"], "batch_per_step": per_step,
-                       "note": "each step is a bounded sample of the workload's batch"},
+            "config": {"workload": CONFIGS[args.config]["workload"], "batch_per_step": lanes,
+                       "note": f"each step is one generation of the reference's MapElites loop over a bounded "
+                               f"sample of {lanes} lanes (of the {B}-lane batch)"},
             "cpu_baseline": {"value": value, "unit": "topologies/s", "cores": cores, "kind": "port",
-                             "sample": f"{per_step} genomes per step x {args.steps} steps, DcContext::evaluate_batch "
-                                       f"(threads = {cores})" + (f", x {n_timesteps(text)} profiles (one reference "
-                                                                  "evaluation per timestep, timed on one)"
-                                                                  if n_timesteps(text) > 1 else "")},
+                             "sample": f"run_optimizer (oracle restatement): {args.warmup} warm-up + {args.steps} "
+                                       f"timed generations of {lanes} lanes, evaluate_batch on {cores} threads"
+                                       + (f", x {T} profiles (one reference evaluation per timestep, timed on one)"
+                                          if T > 1 else "")},
             "e2e": {"value": value, "unit": "topologies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -203,7 +212,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg2", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rng", default="replay", choices=["replay", "philox"],
@@ -346,9 +355,15 @@ def main():
     #      (DcContext::evaluate_batch: H2D genomes, evaluate, D2H scores each step)
     rng = np.random.default_rng(7 + rank)
     pool = np.array([e.genome.action_slots + e.genome.disconnection_slots for e in snap.entries], np.int32)
-    parents = pool[rng.integers(0, len(pool), B)]
-    genomes = P.mutate_lanes(ctx, cfg, parents, rng.integers(1, 2 ** 62, B, dtype=np.uint64))
-    g_pin = torch.from_numpy(genomes.reshape(-1)).pin_memory()
+    e2e_steps = max(3, min(args.steps, 10))
+    # a distinct batch of mutated archive genomes per timed step (each step
+    # copies its own genomes host -> device and its scores device -> host)
+    batches = []
+    for k in range(e2e_steps + 2):
+        parents = pool[rng.integers(0, len(pool), B)]
+        batches.append(P.mutate_lanes(ctx, cfg, parents, rng.integers(1, 2 ** 62, B, dtype=np.uint64)))
+    g_pin = torch.from_numpy(np.stack(batches).reshape(-1)).pin_memory()
+    per = B * (cfg.n_a + cfg.n_d)
     wk = ctx.config.worst_k
     outs = {k: torch.zeros(B * m, dtype=t).pin_memory() for k, t, m in [
         ("lambda_o", torch.float64, 1), ("lambda_c", torch.int32, 1), ("lambda_c0", torch.int32, 1),
@@ -359,15 +374,14 @@ def main():
     import ctypes as C
     sc = P.api.L.ScoresC(*[C.cast(C.c_void_p(outs[f].data_ptr()), t) for f, t in P.api.L.ScoresC._fields_])
     d2h = sum(v.numel() * v.element_size() for v in outs.values())
-    h2d = g_pin.numel() * 4
-    for _ in range(2):
-        P.evaluate_raw(ctx, g_pin.data_ptr(), B, 3, 2, sc)
+    h2d = per * 4
+    for k in range(2):
+        P.evaluate_raw(ctx, g_pin.data_ptr() + (e2e_steps + k) * per * 4, B, 3, 2, sc)
     torch.cuda.synchronize()
     barrier()
     t0 = time.perf_counter()
-    e2e_steps = max(3, min(args.steps, 20))
-    for _ in range(e2e_steps):
-        P.evaluate_raw(ctx, g_pin.data_ptr(), B, 3, 2, sc)
+    for k in range(e2e_steps):
+        P.evaluate_raw(ctx, g_pin.data_ptr() + k * per * 4, B, 3, 2, sc)
     torch.cuda.synchronize()
     e2e_s = time.perf_counter() - t0
     e2e_s = max_over_ranks(e2e_s, world, dev)
@@ -375,7 +389,7 @@ def main():
 
     base = None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
-        base = cpu_baseline(text)
+        base = cpu_baseline(text, B)
 
     work_bytes = B * (E * 64 + info["k_padded"] * 64)  # per-step candidate rows (feat + contingency rows)
     if rank == 0:

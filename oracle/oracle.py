@@ -74,6 +74,8 @@ def lib() -> C.CDLL:
         L.oc_run_optimizer.restype = vp
         L.oc_run_optimizer_trace.argtypes = [vp, C.POINTER(QdConfigC)]
         L.oc_run_optimizer_trace.restype = vp
+        L.oc_run_optimizer_timed.argtypes = [vp, C.POINTER(QdConfigC), f64p, C.c_int, C.POINTER(C.c_int64)]
+        L.oc_run_optimizer_timed.restype = C.c_int
         L.oc_random_grid_json.argtypes = [C.c_uint64, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]
         L.oc_random_grid_json.restype = vp
         L.oc_random_genomes.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_int, i32p]
@@ -188,6 +190,16 @@ class OracleContext:
     def run_optimizer_trace(self, cfg: QdConfigC) -> dict:
         """run_optimizer with each iteration's offspring and scores (lockstep parity)."""
         return json.loads(_take_string(lib().oc_run_optimizer_trace(self.h, C.byref(cfg))))
+
+    def run_optimizer_timed(self, cfg: QdConfigC):
+        """run_optimizer; returns (per-iteration end stamps in seconds, evaluations)."""
+        cap = 1 << 16
+        st = np.zeros(cap)
+        ev = C.c_int64()
+        n = lib().oc_run_optimizer_timed(self.h, C.byref(cfg), _p(st, C.c_double), cap, C.byref(ev))
+        if n < 0:
+            raise RuntimeError(lib().oc_last_error().decode())
+        return st[:n], int(ev.value)
 
     def rebuild_flows(self, genome, n_a: int, n_d: int):
         g = np.ascontiguousarray(genome, np.int32)

@@ -327,6 +327,24 @@ char* oc_run_optimizer_trace(void* h, const oc_qd_config* cfg) {
   return rc == 0 ? out : nullptr;
 }
 
+// run_optimizer with a wall-clock stamp (seconds since the call) after each
+// iteration's inserts: the reference arm of bench.py times the reference's own
+// MapElites loop per generation. Returns the number of stamps written.
+int oc_run_optimizer_timed(void* h, const oc_qd_config* cfg, double* stamps, int cap, int64_t* evaluations) {
+  int n = 0;
+  int rc = guarded([&] {
+    auto* c = static_cast<Ctx*>(h);
+    QdConfig q = to_qd(cfg);
+    const auto t0 = std::chrono::steady_clock::now();
+    IterationTrace tr = [&](std::int64_t, const std::vector<Genome>&, const std::vector<ScoreVector>&) {
+      if (n < cap) stamps[n++] = std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    };
+    auto r = run_optimizer(*c->dc, q, nullptr, nullptr, &tr);
+    *evaluations = r.stats.evaluations;
+  });
+  return rc == 0 ? n : -1;
+}
+
 // Seeded fixtures (tests/helpers.hpp:435-581).
 char* oc_random_grid_json(uint64_t seed, int n_nodes, int extra_edges, int n_outages, int n_stations, int multi,
                           int injection_outages, int busbar_outages) {

@@ -13,6 +13,7 @@ the evaluation runs on the GPU and there is no CPU fallback.
 from __future__ import annotations
 
 import ctypes as C
+import threading
 import math
 from dataclasses import dataclass, field
 from typing import Callable, List, Optional, Sequence, Tuple
@@ -587,10 +588,38 @@ def run_optimizer(ctx: DcContext, cfg: QdConfig, sink: Optional[Callable[[Repert
     cap = 1 << 16
     tev = np.zeros(cap, np.int64)
     tbest = np.zeros(cap)
-    stop_arr = stop if stop is not None else None
+    # `stop` (the reference's std::atomic<bool>*, qd_optimizer.hpp:116-118) is
+    # polled by the native loop: a threading.Event is mirrored into a private
+    # int32 flag; an array must already be a contiguous int32 buffer (a copy
+    # would never see the caller's store)
+    watcher = None
+    done = None
+    if stop is None:
+        stop_arr = None
+    elif isinstance(stop, threading.Event):
+        stop_arr = np.zeros(1, np.int32)
+        done = threading.Event()
+
+        def _mirror():
+            while not done.is_set():
+                if stop.wait(0.005):
+                    stop_arr[0] = 1
+                    return
+        watcher = threading.Thread(target=_mirror, daemon=True)
+        watcher.start()
+    else:
+        if not (isinstance(stop, np.ndarray) and stop.dtype == np.int32 and stop.size >= 1
+                and stop.flags["C_CONTIGUOUS"]):
+            raise ConfigError("stop must be a threading.Event or a contiguous numpy int32 array")
+        stop_arr = stop
     stop_p = _ptr(stop_arr, C.c_int32) if stop_arr is not None else C.POINTER(C.c_int32)()
-    _check(LIB.tg_optimizer_run(ctx._h, C.byref(ccfg), cb, user, stop_p, C.byref(stats), _ptr(tev, C.c_int64),
-                                _ptr(tbest, C.c_double), cap))
+    try:
+        _check(LIB.tg_optimizer_run(ctx._h, C.byref(ccfg), cb, user, stop_p, C.byref(stats), _ptr(tev, C.c_int64),
+                                    _ptr(tbest, C.c_double), cap))
+    finally:
+        if watcher is not None:
+            done.set()
+            watcher.join()
     if errors:
         raise errors[0]
     view = L.SnapshotView()

@@ -216,6 +216,19 @@ struct tg_context {
   void snap_buffers(size_t bytes);
   void free_snap_buffers();
   int n_a_cap = 4, n_d_cap = 4;
+  // grid-dependent sizes checked against the engine's compile-time capacities
+  // (common.cuh): outage removal sets (multi-branch contingencies, busbar
+  // implied sets), outage injection sets, per-station injection / branch
+  // terminals (moved by one split)
+  int max_outage_removed = 0, max_outage_inj = 0, max_station_inj = 0, max_station_br = 0;
+  int* err_sticky = nullptr;  // device word: a capacity error happened in some lane since the last check
+  int* err_host = nullptr;    // pinned mirror of err_sticky, copied after every enqueued loop step
+  cudaEvent_t err_ev = nullptr;
+  bool err_pending = false;
+  void check_capacity(int n_a, int n_d) const;
+  void check_sticky();  // synchronizing check
+  void poll_sticky();   // non-blocking: raises if an earlier step's mirror landed with an error
+  void mirror_sticky(); // enqueue the mirror copy after the steps just enqueued
   // live timing of the fused sweep (bench.py roofline)
   bool time_sweep = false;
   cudaEvent_t sw0 = nullptr, sw1 = nullptr;
@@ -261,6 +274,54 @@ struct tg_context {
   void time_sweep_done();
 };
 
+void tg_context::check_capacity(int n_a, int n_d) const {
+  auto fail = [](const std::string& what) {
+    throw CapacityFailure(what + " exceeds the engine's compile-time capacity (common.cuh)");
+  };
+  if (max_outage_removed + n_d > tgb::kMaxRemoved)
+    fail("an outage removal set of " + std::to_string(max_outage_removed) + " branches plus " + std::to_string(n_d) +
+         " genome disconnections (limit " + std::to_string(tgb::kMaxRemoved) + ")");
+  if (n_a * max_station_inj > tgb::kMaxInjMoved)
+    fail(std::to_string(n_a) + " splits of stations with " + std::to_string(max_station_inj) +
+         " injection terminals (limit " + std::to_string(tgb::kMaxInjMoved) + " moved injections)");
+  if (n_a * max_station_br > tgb::kMaxMoved)
+    fail(std::to_string(n_a) + " splits of stations with " + std::to_string(max_station_br) +
+         " branch terminals (limit " + std::to_string(tgb::kMaxMoved) + " moved branch ends)");
+}
+
+// Capacity errors of lanes evaluated inside the device loop (k_finish ORs
+// them into err_sticky): raised by the next host-visible call, never dropped.
+void tg_context::check_sticky() {
+  int v = 0;
+  check(cudaMemcpyAsync(&v, err_sticky, sizeof(int), cudaMemcpyDeviceToHost, stream), "error word D2H");
+  check(cudaStreamSynchronize(stream), "error word");
+  if (v) {
+    check(cudaMemsetAsync(err_sticky, 0, sizeof(int), stream), "error word reset");
+    throw CapacityFailure("a candidate exceeded the engine's compile-time capacity (rank/removed/moved limits) "
+                          "during the optimizer loop");
+  }
+}
+
+void tg_context::poll_sticky() {
+  if (!err_pending) return;
+  const cudaError_t r = cudaEventQuery(err_ev);
+  if (r == cudaErrorNotReady) return;
+  check(r, "error word");
+  err_pending = false;
+  if (*err_host) check_sticky();
+}
+
+void tg_context::mirror_sticky() {
+  if (!err_host) {
+    check(cudaMallocHost(reinterpret_cast<void**>(&err_host), sizeof(int)), "cudaMallocHost");
+    *err_host = 0;
+    check(cudaEventCreateWithFlags(&err_ev, cudaEventDisableTiming), "event");
+  }
+  check(cudaMemcpyAsync(err_host, err_sticky, sizeof(int), cudaMemcpyDeviceToHost, stream), "error word D2H");
+  check(cudaEventRecord(err_ev, stream), "event record");
+  err_pending = true;
+}
+
 void tg_context::snap_buffers(size_t bytes) {
   if (bytes <= snap_bytes) return;
   check(cudaStreamSynchronize(stream), "snapshot buffers");
@@ -296,6 +357,7 @@ void tg_context::ensure_capacity(int n) {
   DeviceArena& A = *batch_arena;
   tgb::Batch& b = batch;
   b = tgb::Batch{};  // every pointer below is reallocated or stays null
+  b.err_sticky = err_sticky;
   mt_ok = false;
   const size_t E = g.E, Kp = g.Kpad, Ka = std::max(g.Kall, 1);
   d_genomes = A.alloc<int>(static_cast<size_t>(cap) * tgb::kMaxSlots);
@@ -552,6 +614,8 @@ void check_errors(tg_context* ctx, int n) {
   check(cudaMemcpyAsync(err.data(), ctx->batch.out.error, n * sizeof(int), cudaMemcpyDeviceToHost, ctx->stream),
         "error D2H");
   check(cudaStreamSynchronize(ctx->stream), "evaluate");
+  // this call reports its own lanes: the loop's sticky word starts clean
+  check(cudaMemsetAsync(ctx->err_sticky, 0, sizeof(int), ctx->stream), "error word reset");
   for (int i = 0; i < n; ++i)
     if (err[i] != 0)
       throw CapacityFailure("candidate " + std::to_string(i) +
@@ -733,6 +797,35 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
       ks_cont.swap(c2);
       ks_br.swap(b2);
     }
+    // capacities (common.cuh) against this grid: checked here and per call
+    for (size_t c = 0; c + 1 < kx_bptr.size(); ++c) {
+      ctx->max_outage_removed = std::max(ctx->max_outage_removed, kx_bptr[c + 1] - kx_bptr[c]);
+      ctx->max_outage_inj = std::max(ctx->max_outage_inj, kx_iptr[c + 1] - kx_iptr[c]);
+    }
+    for (int bo = 0; bo < gd->n_busbar_outages; ++bo)
+      ctx->max_outage_removed = std::max(ctx->max_outage_removed, gd->bo_implied_ptr[bo + 1] - gd->bo_implied_ptr[bo]);
+    if (ad && ad->n_actions > 0 && gd->n_busbar_outages > 0) {
+      const int nslots = ad->action_busbar_ptr[ad->n_actions];
+      for (int i = 0; i < nslots; ++i)
+        ctx->max_outage_removed =
+            std::max(ctx->max_outage_removed, ad->action_implied_ptr[i + 1] - ad->action_implied_ptr[i]);
+    }
+    for (int st = 0; st < gd->n_substations; ++st) {
+      int ni = 0, nb = 0;
+      for (int q = gd->sub_term_ptr[st]; q < gd->sub_term_ptr[st + 1]; ++q) (gd->term_kind[q] == 2 ? ni : nb) += 1;
+      ctx->max_station_inj = std::max(ctx->max_station_inj, ni);
+      ctx->max_station_br = std::max(ctx->max_station_br, nb);
+    }
+    if (ctx->max_outage_removed > tgb::kMaxRemoved)
+      throw CapacityFailure("an outage removes " + std::to_string(ctx->max_outage_removed) +
+                            " branches; the engine's compile-time capacity is " + std::to_string(tgb::kMaxRemoved));
+    if (ctx->max_outage_inj > tgb::kMaxPMod)
+      throw CapacityFailure("a contingency drops " + std::to_string(ctx->max_outage_inj) +
+                            " injections; the engine's compile-time capacity is " + std::to_string(tgb::kMaxPMod));
+    if (ctx->max_station_inj > tgb::kMaxInjMoved || ctx->max_station_br > tgb::kMaxMoved)
+      throw CapacityFailure("a substation has more terminals than the engine's compile-time capacity");
+    ctx->err_sticky = A.alloc<int>(1);
+    check(cudaMemsetAsync(ctx->err_sticky, 0, sizeof(int), s), "error word");
     const int tile = tgb::sweep_tile_k();
     g.Ks = static_cast<int>(ks_cont.size());
     g.Kpad = ((g.Ks + tile - 1) / tile) * tile;
@@ -941,6 +1034,7 @@ void tg_context_destroy(tg_context* ctx) {
   ctx->free_snap_buffers();
   cudaStream_t s = ctx->stream;
   if (ctx->sw0) cudaEventDestroy(ctx->sw0), cudaEventDestroy(ctx->sw1);
+  if (ctx->err_host) cudaFreeHost(ctx->err_host), cudaEventDestroy(ctx->err_ev);
   delete ctx;
   cudaStreamDestroy(s);
 }
@@ -959,6 +1053,7 @@ tg_status tg_evaluate_batch(tg_context* ctx, const int32_t* genomes, int32_t n, 
       if (v < -1 || (slot < n_a && v >= ctx->g.A) || (slot >= n_a && v >= ctx->g.D))
         throw tgb::ValidationError("genome slot value out of range");
     }
+    ctx->check_capacity(n_a, n_d);
     (void)batch_size;  // padding lanes are empty genomes whose scores are dropped
     ctx->ensure_capacity(n);
     check(cudaMemcpyAsync(ctx->d_genomes, genomes, static_cast<size_t>(n) * (n_a + n_d) * sizeof(int),
@@ -1010,6 +1105,7 @@ tg_status tg_evaluate_batch_device(tg_context* ctx, const int32_t* d_genomes, in
       throw tgb::ConfigError("genome slots exceed the engine capacity (n_a <= 4, n_d <= 4)");
     if (n <= 0) return;
     check(cudaSetDevice(ctx->device), "cudaSetDevice");
+    ctx->check_capacity(n_a, n_d);
     ctx->ensure_capacity(n);
     check(cudaMemcpyAsync(ctx->d_genomes, d_genomes, static_cast<size_t>(n) * (n_a + n_d) * sizeof(int),
                           cudaMemcpyDeviceToDevice, ctx->stream),
@@ -1076,6 +1172,7 @@ tgb::QdParams qd_params(tg_context* ctx, const tg_qd_config* c) {
   if (!(c->mutation_mean < 12.0))
     throw tgb::ConfigError("mutation_mean >= 12 (libstdc++ rejection sampler) is not replayed on the device");
   if (c->d_max < 0 || c->s_max < 0 || c->r_max < 0) throw tgb::ConfigError("descriptor bounds must be >= 0");
+  ctx->check_capacity(c->n_a, c->n_d);
   tgb::QdParams p{};
   p.n_a = c->n_a;
   p.n_d = c->n_d;
@@ -1190,6 +1287,8 @@ tg_status tg_qd_begin(tg_context* ctx, const tg_qd_config* cfg) {
     qd_setup(ctx, p);
     tgb::QdState& q = *ctx->qd;
     ctx->ensure_capacity(p.batch);
+    check(cudaMemsetAsync(ctx->err_sticky, 0, sizeof(int), ctx->stream), "error word reset");
+    ctx->err_pending = false;
     cudaStream_t s = ctx->stream;
     // seed the archive with the unchanged topology (qd_optimizer.cpp:361-363)
     tgb::launch_archive_reset(q, s);
@@ -1215,6 +1314,7 @@ tg_status tg_qd_begin(tg_context* ctx, const tg_qd_config* cfg) {
 tg_status tg_qd_step(tg_context* ctx, int32_t n_iters) {
   return guarded([&] {
     if (!ctx->qd || !ctx->qd->graph) throw tgb::ConfigError("call tg_qd_begin first");
+    ctx->poll_sticky();  // an earlier step's capacity error surfaces here (no synchronization)
     if (ctx->time_sweep) {
       // instrumented path: same kernels launched directly, sweep bracketed by events
       tgb::QdState& q = *ctx->qd;
@@ -1225,11 +1325,13 @@ tg_status tg_qd_step(tg_context* ctx, int32_t n_iters) {
                                                 ctx->stream);
       }
       ctx->qd_evaluations += static_cast<int64_t>(n_iters) * q.p.batch;
+      ctx->mirror_sticky();
       return;
     }
     for (int i = 0; i < n_iters; ++i) check(cudaGraphLaunch(ctx->qd->graph, ctx->stream), "graph launch");
     ctx->launches += static_cast<int64_t>(n_iters) * ctx->qd->kernels_per_iter;
     ctx->qd_evaluations += static_cast<int64_t>(n_iters) * ctx->qd->p.batch;
+    ctx->mirror_sticky();
   });
 }
 
@@ -1307,12 +1409,15 @@ tg_status tg_qd_generation_end(tg_context* ctx) {
                                         ctx->stream);
     ctx->qd_evaluations += q.p.batch;
     check(cudaGetLastError(), "insert");
+    ctx->poll_sticky();
+    ctx->mirror_sticky();
   });
 }
 
 tg_status tg_qd_fetch(tg_context* ctx, int32_t final_snapshot, tg_snapshot_view* out) {
   return guarded([&] {
     if (!ctx->qd) throw tgb::ConfigError("call tg_qd_begin first");
+    ctx->check_sticky();
     fetch_archive(ctx, ctx->qd_epoch, ctx->qd_evaluations, final_snapshot != 0);
     if (out) *out = ctx->snap.view;
   });
@@ -1567,11 +1672,8 @@ tg_status tg_optimizer_run(tg_context* ctx, const tg_qd_config* cfg, tg_snapshot
     if (!emitted_final) snapshot(true);
     deliver(true);
     for (auto& e : ev) cudaEventDestroy(e);
-    // capacity errors raised inside the loop surface here
-    std::vector<int> err(q.p.batch);
-    check(cudaMemcpy(err.data(), ctx->batch.out.error, q.p.batch * sizeof(int), cudaMemcpyDeviceToHost), "D2H");
-    for (int e : err)
-      if (e) throw CapacityFailure("a candidate exceeded the engine's compile-time capacity during the run");
+    // capacity errors of any generation of the run surface here (sticky word)
+    ctx->check_sticky();
     if (stats) {
       stats->evaluations = ctx->qd_evaluations;
       stats->epochs = ctx->qd_epoch;

@@ -20,7 +20,7 @@ constexpr int kMaxGround = 8;      // dead base nodes grounded
 constexpr int kMaxCols = kMaxSplits + kMaxRemoved + kMaxGround;  // Z columns for the outage rebuild
 constexpr int kTopoSol = kMaxSplits * kMaxSplits + kMaxSplits * kMaxCols + kMaxCols * kMaxCols;  // S^-1, Y, C^-1
 constexpr int kMaxTerms = 512;     // sparse coefficients over all Z columns
-constexpr int kMaxPMod = 16;       // omitted injections (p modifications)
+constexpr int kMaxPMod = 32;       // omitted injections (p modifications)
 constexpr int kMaxInjMoved = 64;   // injections moved to new nodes
 constexpr int kTmaxSub = 8;        // sub-tiles of a sweep tile carrying their own max |T_base| per row
 constexpr int kRec = kTmaxSub + 4; // floats per (tile, row) skip record: kTmaxSub sub-tile maxima of |T_base| (float,

@@ -397,7 +397,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_special(DevGrid g, Batch b, in
   __shared__ Topo t;
   __shared__ int extra[kMaxRemoved];
   __shared__ int omit[kMaxPMod];
-  __shared__ int n_extra, n_omit, skip;
+  __shared__ int n_extra, n_omit, skip, overflow;
   __shared__ double red_sum[kPrepThreads / 32];
   __shared__ double gram[kMaxCols * kMaxCols];
   __shared__ double thv[kMaxCols];
@@ -414,13 +414,15 @@ __global__ void __launch_bounds__(kPrepThreads) k_special(DevGrid g, Batch b, in
       skip = b.status[c] != 0;
       n_extra = 0;
       n_omit = 0;
+      overflow = 0;
       if (!skip) {
         if (cs < g.Kx) {
+          // lists longer than the capacities are rejected at context creation;
+          // never truncated here (an overflow is a capacity error for the lane)
+          if (g.kx_br_ptr[cs + 1] - g.kx_br_ptr[cs] > kMaxRemoved || g.kx_inj_ptr[cs + 1] - g.kx_inj_ptr[cs] > kMaxPMod)
+            overflow = 1;
           for (int p = g.kx_br_ptr[cs]; p < g.kx_br_ptr[cs + 1] && n_extra < kMaxRemoved; ++p) extra[n_extra++] = g.kx_br[p];
-          for (int p = g.kx_inj_ptr[cs]; p < g.kx_inj_ptr[cs + 1] && n_omit < kMaxPMod; ++p) {
-            // injection outages only matter when the injection carries power
-            omit[n_omit++] = g.kx_inj[p];
-          }
+          for (int p = g.kx_inj_ptr[cs]; p < g.kx_inj_ptr[cs + 1] && n_omit < kMaxPMod; ++p) omit[n_omit++] = g.kx_inj[p];
         } else {
           // busbar outage: implied set of the station's action or the default (dc_engine.cpp:373-379)
           const int bo = cs - g.Kx;
@@ -440,6 +442,7 @@ __global__ void __launch_bounds__(kPrepThreads) k_special(DevGrid g, Batch b, in
             hi = g.bo_def_ptr[bo + 1];
             src = g.bo_def;
           }
+          if (hi - lo > kMaxRemoved) overflow = 1;
           for (int p = lo; p < hi && n_extra < kMaxRemoved; ++p) extra[n_extra++] = src[p];
         }
       }
@@ -451,7 +454,10 @@ __global__ void __launch_bounds__(kPrepThreads) k_special(DevGrid g, Batch b, in
     }
     for (int i = threadIdx.x; i < 2 * words; i += blockDim.x) bits[i] = 0u;
     __syncthreads();
-    if (threadIdx.x == 0) analyze(g, t, mv_bits, rm_bits, slots, n_a, n_d, extra, n_extra, omit, n_omit);
+    if (threadIdx.x == 0) {
+      analyze(g, t, mv_bits, rm_bits, slots, n_a, n_d, extra, n_extra, omit, n_omit);
+      if (overflow) t.islanded = 2;
+    }
     __syncthreads();
     if (!t.islanded) {
       build_z(g, t, zbuf, kMaxCols);
@@ -661,6 +667,7 @@ __global__ void __launch_bounds__(32 * kFinishWarps) k_finish(DevGrid g, Batch b
       o.fitness[c] = -CUDART_INF;
       o.islanded[c] = st == 1 ? 1 : 0;
       o.error[c] = st == 1 ? 0 : st;
+      if (st != 1 && b.err_sticky) atomicOr(b.err_sticky, 1);
       o.worst_n[c] = 0;
       o.isl_out[c] = 0;
       o.isl_bus[c] = 0;

@@ -63,6 +63,8 @@ struct Batch {
   const int* genomes;         // [n][n_a+n_d]
   DcParams params;
   int* status;                // 0 ok, 1 islanded, 2/3 capacity error
+  int* err_sticky;            // per-context capacity-error word: k_finish ORs 1 into it for every lane whose
+                              // status is a capacity error; the host checks it after loop steps and clears it
   TopoCore* topo;             // [n] topology analysis of k_analyze, reloaded by k_prep
   uint32_t* tbits;            // [n][2 * words] moved / removed branch bitmaps of the analysis
   int* rank;                  // low-rank update size, -1 when not swept
@@ -77,7 +79,11 @@ struct Batch {
   double* kdat;               // [n][Kpad * kStride]: Kpad rows of row_stride(r) doubles alpha, R'
                               // (single-branch contingencies)
   uint8_t* kflag;             // [n][Kpad] 0 ok, 1 islanded, 2 padding
-  unsigned long long* fmax;   // [n][E] max |f| over contingencies (bits of a non-negative double)
+  unsigned long long* fmax;   // [n][E] max |f| over contingencies (bits of a non-negative double). The FULL
+                              // (FlowResult) sweep folds every element; the scores-only and masked sweeps fold
+                              // only elements above the branch limit (the only values a score reads), so there
+                              // an entry at or below the limit means "not overloaded", not the maximum: only
+                              // FULL-path fmax may be exported as FlowResult::max_contingency (launch_extract)
   unsigned long long* fbus;   // [n][E] max |f| over busbar outages
   double* energy;             // [n][Kall] outage energy per contingency
   int* nc0;                   // [n] lambda_c0 of the candidate flows (k_prep)

@@ -199,7 +199,11 @@ __device__ inline void analyze(const DevGrid& g, TopoCore& t, uint32_t* mv_bits,
     if (d >= 0) add_removed(g.disc[d]);
   }
   for (int k = 0; k < n_extra; ++k) add_removed(extra_rem[k]);
-  for (int k = 0; k < n_omit && t.nom < kMaxPMod; ++k) t.omit[t.nom++] = omit_inj[k];
+  if (n_omit > kMaxPMod) {
+    t.islanded = 2;  // capacity exceeded (never truncated)
+    return;
+  }
+  for (int k = 0; k < n_omit; ++k) t.omit[t.nom++] = omit_inj[k];
 
   // splits: one new node per non-empty action slot, in slot order (genome.cpp:90-108)
   for (int k = 0; k < n_a; ++k) {
@@ -214,10 +218,12 @@ __device__ inline void analyze(const DevGrid& g, TopoCore& t, uint32_t* mv_bits,
       if (!grp[q]) continue;
       const int kind = g.term_kind[t0 + q], el = g.term_elem[t0 + q];
       if (kind == 2) {
-        if (t.ninj < kMaxInjMoved) {
-          t.inj_id[t.ninj] = el;
-          t.inj_new[t.ninj++] = j;
+        if (t.ninj >= kMaxInjMoved) {
+          t.islanded = 2;  // capacity exceeded (never truncated)
+          return;
         }
+        t.inj_id[t.ninj] = el;
+        t.inj_new[t.ninj++] = j;
         continue;
       }
       int slot = moved_slot(t, mv_bits, el);
