@@ -304,6 +304,10 @@ tg_status tg_sweep_timing(tg_context* ctx, int32_t enable, double* total_ms, int
  * last call: offered, passing the per-row bound (first FMA computed), fully
  * computed (passing the per-element bound), holding at least one overload. */
 tg_status tg_sweep_rows(tg_context* ctx, int64_t* computed, int64_t* offered, int64_t* overloaded, int64_t* partial);
+/* Chunk-level skip statistics of the chunked scores-only sweep since the last
+ * call: (candidate, tile, 32-row chunk) tests run and chunks that failed the
+ * bound (their rows went to the row-level stages). Resets the counters. */
+tg_status tg_sweep_chunks(tg_context* ctx, int64_t* tested, int64_t* hot);
 /* Low-rank update size of each candidate of the last evaluated batch (-1 = not swept). */
 tg_status tg_batch_ranks(tg_context* ctx, int32_t n, int32_t* ranks);
 /* Measured FP64 FMA throughput of `device` (TFLOP/s) from a DFMA microbenchmark. */

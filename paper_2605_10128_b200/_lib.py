@@ -118,6 +118,7 @@ SIGNATURES = [
     ("tg_sweep_timing", C.c_int, [C.c_void_p, C.c_int32, f64p, i64p]),
     ("tg_batch_ranks", C.c_int, [C.c_void_p, C.c_int32, i32p]),
     ("tg_sweep_rows", C.c_int, [C.c_void_p, i64p, i64p, i64p, i64p]),
+    ("tg_sweep_chunks", C.c_int, [C.c_void_p, i64p, i64p]),
     ("tg_fp64_peak", C.c_int, [C.c_int, f64p]),
     ("tg_channel_create", C.c_void_p, [C.c_int64]),
     ("tg_channel_destroy", None, [C.c_void_p]),

@@ -777,3 +777,10 @@ def sweep_rows(ctx: DcContext) -> Tuple[int, int, int, int]:
     p = C.c_int64()
     _check(LIB.tg_sweep_rows(ctx._h, C.byref(a), C.byref(b), C.byref(o), C.byref(p)))
     return a.value, b.value, o.value, p.value
+
+
+def sweep_chunks(ctx: DcContext) -> Tuple[int, int]:
+    """(chunk tests, hot chunks) of the chunked scores-only sweep since the last call (resets)."""
+    a, h = C.c_int64(), C.c_int64()
+    _check(LIB.tg_sweep_chunks(ctx._h, C.byref(a), C.byref(h)))
+    return a.value, h.value

@@ -9,6 +9,7 @@
 #include <deque>
 #include <memory>
 #include <string>
+#include <tuple>
 #include <vector>
 
 #include "../../include/topopt_b200.h"
@@ -221,6 +222,7 @@ struct tg_context {
   // implied sets), outage injection sets, per-station injection / branch
   // terminals (moved by one split)
   int max_outage_removed = 0, max_outage_inj = 0, max_station_inj = 0, max_station_br = 0;
+  std::vector<int> br_perm;   // internal branch index -> the grid's (empty: identity); see sweep_row_order
   int* err_sticky = nullptr;  // device word: a capacity error happened in some lane since the last check
   int* err_host = nullptr;    // pinned mirror of err_sticky, copied after every enqueued loop step
   cudaEvent_t err_ev = nullptr;
@@ -370,8 +372,10 @@ void tg_context::ensure_capacity(int n) {
   b.feat = A.alloc<double>(static_cast<size_t>(tgb::max_sweep_groups(cap)) * b.nchunks * tgb::kGroupSlots *
                            tgb::kChunkRows * tgb::kStride);
   b.slot = A.alloc<int>(cap);
-  b.rows_done = A.alloc<unsigned long long>(4);
-  check(cudaMemset(b.rows_done, 0, 4 * sizeof(unsigned long long)), "rows_done");
+  b.rows_done = A.alloc<unsigned long long>(8);
+  check(cudaMemset(b.rows_done, 0, 8 * sizeof(unsigned long long)), "memset");
+  b.csum = A.alloc<float>(static_cast<size_t>(cap) * b.nchunks * tgb::kCsum);
+  b.item_ctr = A.alloc<unsigned int>(4);
   b.kdat = A.alloc<double>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1) * tgb::kStride);
   b.kflag = A.alloc<uint8_t>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1));
   b.fmax = A.alloc<unsigned long long>(static_cast<size_t>(cap) * E);
@@ -720,18 +724,146 @@ tg_status tg_actionset_describe(const tg_actionset* a, const tg_grid*, tg_action
   });
 }
 
-tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad, const tg_dc_config* cfg, int device,
-                            tg_context** out) {
-  return guarded([&] {
-    auto ctx = std::make_unique<tg_context>();
-    ctx->device = device;
-    check(cudaSetDevice(device), "cudaSetDevice");
-    check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+}  // extern "C"
+
+namespace {
+
+// B_red^-1 of the grid (dc_engine.cpp:88-116): assembled on the host in the
+// grid's own branch order, inverted on the device. Node space only, so it is
+// shared by every branch (row) order.
+double* base_inverse(tg_context* ctx, const tg_grid_desc* gd) {
+  const int N = gd->n_nodes, E = gd->n_branches, Nr = N - 1;
+  std::vector<int> red(N, -1);
+  for (int v = 0, r = 0; v < N; ++v)
+    if (v != gd->slack) red[v] = r++;
+  std::vector<double> bred(static_cast<size_t>(Nr) * Nr, 0.0);
+  for (int e = 0; e < E; ++e) {
+    if (!gd->branch_in_service[e]) continue;
+    const double b = 1.0 / gd->branch_x[e];
+    const int i = red[gd->branch_from[e]], j = red[gd->branch_to[e]];
+    if (i >= 0) bred[static_cast<size_t>(i) * Nr + i] += b;
+    if (j >= 0) bred[static_cast<size_t>(j) * Nr + j] += b;
+    if (i >= 0 && j >= 0) bred[static_cast<size_t>(i) * Nr + j] -= b, bred[static_cast<size_t>(j) * Nr + i] -= b;
+  }
+  double* X = ctx->arena.upload(bred, ctx->stream);
+  if (!tgb::device_spd_inverse(X, Nr, ctx->stream))
+    throw tgb::SingularSystem("susceptance matrix is singular; the grid is disconnected");
+  return X;
+}
+
+// Sweep row order: the engine numbers branches internally so that each
+// 32-row chunk of the sweep holds electrically close branches (recursive
+// bisection of the node graph, tgb::locality_rank), with the rows whose base
+// N-1 headroom is under 5 % of their limit (near-overloaded in the unchanged
+// topology) last. A chunk far from a candidate's changes is then proved safe
+// by one chunk-level bound (sweep.cu). Returns internal -> original branch
+// index; empty (identity) for grids below the sweep's scale.
+std::vector<int> sweep_row_order(tg_context* ctx, const tg_grid_desc* gd, const double* X) {
+  const int N = gd->n_nodes, E = gd->n_branches, I = gd->n_injections;
+  if (E < 512 || getenv("TGB_NO_ROW_ORDER")) return {};
+  cudaStream_t s = ctx->stream;
+  DeviceArena tmp;
+  std::vector<int> red(N, -1);
+  for (int v = 0, r = 0; v < N; ++v)
+    if (v != gd->slack) red[v] = r++;
+  std::vector<int> ks;
+  for (int c = 0; c < gd->n_contingencies; ++c)
+    if (gd->cont_branch_ptr[c + 1] - gd->cont_branch_ptr[c] == 1 && gd->cont_inj_ptr[c + 1] == gd->cont_inj_ptr[c])
+      ks.push_back(gd->cont_branch[gd->cont_branch_ptr[c]]);
+  std::vector<double> b(E), p(N, 0.0);
+  for (int e = 0; e < E; ++e) b[e] = 1.0 / gd->branch_x[e];
+  for (int i = 0; i < I; ++i) p[gd->injection_node[i]] += gd->injection_net_mw[i];
+  double tot = 0.0;
+  for (double v : p) tot += v;
+  p[gd->slack] -= tot;
+  std::vector<double> pr(N - 1);
+  for (int v = 0; v < N; ++v)
+    if (red[v] >= 0) pr[red[v]] = p[v];
+  tgb::DevGrid g{};
+  g.N = N;
+  g.Nr = N - 1;
+  g.E = E;
+  g.Ks = static_cast<int>(ks.size());
+  g.red = tmp.upload(red, s);
+  g.br_from = tmp.upload(std::vector<int>(gd->branch_from, gd->branch_from + E), s);
+  g.br_to = tmp.upload(std::vector<int>(gd->branch_to, gd->branch_to + E), s);
+  g.br_b = tmp.upload(b, s);
+  g.br_lim = tmp.upload(std::vector<double>(gd->branch_limit, gd->branch_limit + E), s);
+  g.br_on = tmp.upload(std::vector<uint8_t>(gd->branch_in_service, gd->branch_in_service + E), s);
+  g.ks_branch = tmp.upload(ks.empty() ? std::vector<int>{0} : ks, s);
+  g.X = X;
+  double* h = tmp.alloc<double>(E);
+  tgb::launch_row_headroom(g, tmp.upload(pr, s), tmp.alloc<double>(N), tmp.alloc<double>(E), tmp.alloc<double>(E), h,
+                           s);
+  check(cudaGetLastError(), "row headroom");
+  std::vector<double> hh(E);
+  check(cudaMemcpyAsync(hh.data(), h, E * sizeof(double), cudaMemcpyDeviceToHost, s), "headroom D2H");
+  check(cudaStreamSynchronize(s), "row headroom");
+  std::vector<std::pair<int, int>> edges;
+  for (int e = 0; e < E; ++e)
+    if (gd->branch_in_service[e]) edges.emplace_back(gd->branch_from[e], gd->branch_to[e]);
+  const std::vector<int> rank = tgb::locality_rank(N, edges);
+  std::vector<int> perm(E);
+  for (int e = 0; e < E; ++e) perm[e] = e;
+  auto key = [&](int e) {
+    const int tight = hh[e] < 0.05 * gd->branch_limit[e] ? 1 : 0;
+    const int a = rank[gd->branch_from[e]], c = rank[gd->branch_to[e]];
+    return std::make_tuple(tight, std::min(a, c), std::max(a, c));
+  };
+  std::stable_sort(perm.begin(), perm.end(), [&](int x, int y) { return key(x) < key(y); });
+  return perm;
+}
+
+// Grid / action descriptors with branches renumbered (internal e = original
+// perm[e]); every branch reference is mapped, everything else is shared.
+struct PermutedDesc {
+  tg_grid_desc gd;
+  tg_actionset_desc ad{};
+  std::vector<int32_t> from, to, cont_branch, term_element, bo_implied, act_implied, disc;
+  std::vector<double> x, lim;
+  std::vector<uint8_t> on;
+  PermutedDesc(const tg_grid_desc& g, const tg_actionset_desc* a, const std::vector<int>& perm) : gd(g) {
+    const int E = g.n_branches;
+    std::vector<int> inv(E);
+    for (int e = 0; e < E; ++e) inv[perm[e]] = e;
+    for (int e = 0; e < E; ++e) {
+      from.push_back(g.branch_from[perm[e]]);
+      to.push_back(g.branch_to[perm[e]]);
+      x.push_back(g.branch_x[perm[e]]);
+      lim.push_back(g.branch_limit[perm[e]]);
+      on.push_back(g.branch_in_service[perm[e]]);
+    }
+    for (int i = 0; i < g.cont_branch_ptr[g.n_contingencies]; ++i) cont_branch.push_back(inv[g.cont_branch[i]]);
+    const int nterm = g.sub_term_ptr[g.n_substations];
+    for (int q = 0; q < nterm; ++q)
+      term_element.push_back(g.term_kind[q] == 2 ? g.term_element[q] : inv[g.term_element[q]]);
+    for (int i = 0; i < g.bo_implied_ptr[g.n_busbar_outages]; ++i) bo_implied.push_back(inv[g.bo_implied[i]]);
+    gd.branch_from = from.data();
+    gd.branch_to = to.data();
+    gd.branch_x = x.data();
+    gd.branch_limit = lim.data();
+    gd.branch_in_service = on.data();
+    gd.cont_branch = cont_branch.data();
+    gd.term_element = term_element.data();
+    gd.bo_implied = bo_implied.data();
+    if (a) {
+      ad = *a;
+      const int nslots = a->n_actions > 0 ? a->action_busbar_ptr[a->n_actions] : 0;
+      const int nimp = a->n_actions > 0 ? a->action_implied_ptr[nslots] : 0;
+      for (int i = 0; i < nimp; ++i) act_implied.push_back(inv[a->action_implied[i]]);
+      for (int d = 0; d < a->n_disconnectables; ++d) disc.push_back(inv[a->disconnectables[d]]);
+      ad.action_implied = act_implied.data();
+      ad.disconnectables = disc.data();
+    }
+  }
+};
+
+void context_build(tg_context* ctx, const tg_grid_desc* gd, const tg_actionset_desc* ad, const tg_dc_config* cfg,
+                   double* X_base) {
     cudaStream_t s = ctx->stream;
     DeviceArena& A = ctx->arena;
     tgb::DevGrid& g = ctx->g;
     const int N = gd->n_nodes, E = gd->n_branches, I = gd->n_injections;
-    if (N < 2) throw tgb::ValidationError("grid needs at least two nodes");
     g.N = N;
     g.Nr = N - 1;
     g.E = E;
@@ -898,20 +1030,9 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     }
     g.disc = g.D > 0 ? A.upload(v32(ad->disconnectables, g.D), s) : A.alloc<int>(1);
 
-    // base factorization: B_red assembled on the host, inverted on the device
+    // base factorization (base_inverse, in the grid's own branch order)
     const int Nr = g.Nr;
-    std::vector<double> bred(static_cast<size_t>(Nr) * Nr, 0.0);
-    for (int e = 0; e < E; ++e) {
-      if (!gd->branch_in_service[e]) continue;
-      const int i = red[gd->branch_from[e]], j = red[gd->branch_to[e]];
-      if (i >= 0) bred[static_cast<size_t>(i) * Nr + i] += b[e];
-      if (j >= 0) bred[static_cast<size_t>(j) * Nr + j] += b[e];
-      if (i >= 0 && j >= 0) bred[static_cast<size_t>(i) * Nr + j] -= b[e], bred[static_cast<size_t>(j) * Nr + i] -= b[e];
-    }
-    double* X = A.upload(bred, s);
-    if (!tgb::device_spd_inverse(X, Nr, s))
-      throw tgb::SingularSystem("susceptance matrix is singular; the grid is disconnected");
-    g.X = X;
+    g.X = X_base;
     // base tables per injection profile (timestep extension; T = 1 is the reference)
     const int T = std::max(1, gd->n_timesteps);
     if (T > 1 && !gd->injection_net_mw_t) throw tgb::ConfigError("n_timesteps > 1 needs injection_net_mw_t");
@@ -955,6 +1076,13 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
       gv.alpha0 = alpha0;
       tgb::launch_base_tables(gv, d_pr, theta0, f0, tdiag, tk, tmax, alpha0, s);
       check(cudaGetLastError(), "base tables");
+      if (g.Kpad > 0) {
+        float* crec = A.alloc<float>(static_cast<size_t>(ntiles) * ((E + tgb::kChunkRows - 1) / tgb::kChunkRows) *
+                                     tgb::kRec);
+        tgb::launch_chunk_records(gv, crec, s);
+        check(cudaGetLastError(), "chunk records");
+        gv.Crec = crec;
+      }
       ctx->gt.push_back(gv);
     }
     g = ctx->gt[0];
@@ -1005,7 +1133,7 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     ctx->params.variant = 1;
     ctx->run_batch(1, 1, 0, false);
     ctx->params.variant = variant;
-    check_errors(ctx.get(), 1);
+    check_errors(ctx, 1);
     double lo_ = 0, lb_ = 0, fit = 0;
     int lc = 0, lc0 = 0;
     const tgb::Scores& o = ctx->batch.out;
@@ -1017,6 +1145,28 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     ctx->lambda_b_pre = lb_;
     ctx->params.lambda_b_pre = lb_;
     ctx->pre = {lo_, static_cast<double>(lc), static_cast<double>(lc0), lb_, fit};
+}
+
+}  // namespace
+
+extern "C" {
+tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad, const tg_dc_config* cfg, int device,
+                            tg_context** out) {
+  return guarded([&] {
+    auto ctx = std::make_unique<tg_context>();
+    ctx->device = device;
+    check(cudaSetDevice(device), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    if (gd->n_nodes < 2) throw tgb::ValidationError("grid needs at least two nodes");
+    double* X = base_inverse(ctx.get(), gd);
+    std::vector<int> perm = sweep_row_order(ctx.get(), gd, X);
+    if (perm.empty()) {
+      context_build(ctx.get(), gd, ad, cfg, X);
+    } else {
+      PermutedDesc pd(*gd, ad, perm);
+      context_build(ctx.get(), &pd.gd, ad ? &pd.ad : nullptr, cfg, X);
+      ctx->br_perm = std::move(perm);
+    }
     *out = ctx.release();
   });
 }
@@ -1065,20 +1215,30 @@ tg_status tg_evaluate_batch(tg_context* ctx, const int32_t* genomes, int32_t n, 
     const size_t ne = static_cast<size_t>(n) * ctx->g.E;
     if (base_flows || max_contingency || max_busbar) {
       tgb::DeviceScratchGuard tmp(ne);
+      std::vector<double> stage(ctx->br_perm.empty() ? 0 : ne);
+      // per-branch outputs leave in the grid's branch order (internal rows: sweep_row_order)
+      auto fetch = [&](double* dst) {
+        double* land = ctx->br_perm.empty() ? dst : stage.data();
+        check(cudaMemcpyAsync(land, tmp.ptr, ne * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+        check(cudaStreamSynchronize(ctx->stream), "sync");
+        if (!ctx->br_perm.empty()) {
+          const int E = ctx->g.E;
+          for (int i = 0; i < n; ++i)
+            for (int e = 0; e < E; ++e)
+              dst[static_cast<size_t>(i) * E + ctx->br_perm[e]] = stage[static_cast<size_t>(i) * E + e];
+        }
+      };
       if (base_flows) {
         tgb::launch_extract(ctx->g, ctx->batch, tmp.ptr, nullptr, nullptr, ctx->stream);
-        check(cudaMemcpyAsync(base_flows, tmp.ptr, ne * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-        check(cudaStreamSynchronize(ctx->stream), "sync");
+        fetch(base_flows);
       }
       if (max_contingency) {
         tgb::launch_extract(ctx->g, ctx->batch, nullptr, tmp.ptr, nullptr, ctx->stream);
-        check(cudaMemcpyAsync(max_contingency, tmp.ptr, ne * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-        check(cudaStreamSynchronize(ctx->stream), "sync");
+        fetch(max_contingency);
       }
       if (max_busbar) {
         tgb::launch_extract(ctx->g, ctx->batch, nullptr, nullptr, tmp.ptr, ctx->stream);
-        check(cudaMemcpyAsync(max_busbar, tmp.ptr, ne * sizeof(double), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
-        check(cudaStreamSynchronize(ctx->stream), "sync");
+        fetch(max_busbar);
       }
     }
     if (outage_energy && ctx->g.Kall > 0)
@@ -1575,6 +1735,19 @@ tg_status tg_sweep_rows(tg_context* ctx, int64_t* computed, int64_t* offered, in
     if (offered) *offered = static_cast<int64_t>(v[1]);
     if (overloaded) *overloaded = static_cast<int64_t>(v[2]);
     if (partial) *partial = static_cast<int64_t>(v[3]);
+  });
+}
+
+tg_status tg_sweep_chunks(tg_context* ctx, int64_t* tested, int64_t* hot) {
+  return guarded([&] {
+    unsigned long long v[2] = {0, 0};
+    if (ctx->batch.rows_done) {
+      check(cudaMemcpyAsync(v, ctx->batch.rows_done + 4, sizeof(v), cudaMemcpyDeviceToHost, ctx->stream), "D2H");
+      check(cudaMemsetAsync(ctx->batch.rows_done + 4, 0, sizeof(v), ctx->stream), "chunks reset");
+      check(cudaStreamSynchronize(ctx->stream), "chunks");
+    }
+    if (tested) *tested = static_cast<int64_t>(v[0]);
+    if (hot) *hot = static_cast<int64_t>(v[1]);
   });
 }
 

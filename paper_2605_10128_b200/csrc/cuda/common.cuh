@@ -57,6 +57,10 @@ struct DevGrid {
   const float* Tmax;       // [Kpad/128][E + 32][kRec] skip record per (tile, row): max over each sub-tile of
                            // |T_base[e, k]|, then max_k and min_k of T_base[e, k] * alpha0[k] over the tile
   const double* alpha0;    // [Kpad] alpha of the unchanged topology, f0[beta] / (1 - Tdiag[beta]) (0 padding)
+  const float* Crec;       // [Kpad/128][ceil(E/32)][kRec] chunk record per (tile, 32-row chunk): the max over the
+                           // chunk's rows of each sub-tile maximum of Tmax (floats), then the chunk's base N-1
+                           // headroom min_e (lim_e - max(f0_e + D0max, -(f0_e + D0min))) minus a rounding slack
+                           // (double); the chunk-level skip bound of the scores-only sweep (sweep.cu)
   const int* kx_cont;      // [Kx]
   const int* kx_br_ptr;    // [Kx+1]
   const int* kx_br;

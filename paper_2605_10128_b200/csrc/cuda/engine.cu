@@ -95,19 +95,44 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
     // branch rows: [f_c, b_e*phi_e, b_e*rho_e, 0...]; lambda_c0 = #(|f_c| > limit)
     // (dc_engine.cpp:397) counted on the way
     int nc0 = 0;
-    for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
-      double phi[kMaxSplits], rho[kMaxCols];
-      const bool on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
+    // a warp covers 32 consecutive rows (one sweep chunk) per pass, so the
+    // chunk summaries of the chunked sweep are warp reductions
+    float* csum = r <= kChunkedMaxRank ? b.csum + static_cast<size_t>(c) * b.nchunks * kCsum : nullptr;
+    for (int e0 = threadIdx.x & ~31; e0 < g.E; e0 += blockDim.x) {
+      const int e = e0 + (threadIdx.x & 31);
       double row[kStride];
 #pragma unroll
       for (int i = 0; i < kStride; ++i) row[i] = 0.0;
-      row[0] = cand_flow(g, t, e, phi, rho, on);
-      nc0 += fabs(row[0]) > g.br_lim[e];
-      if (on) {
-        const double be = g.br_b[e];
-        for (int q = 0; q < ns; ++q) row[1 + q] = be * phi[q];
-        for (int m = 0; m < nv; ++m) row[1 + ns + m] = be * rho[m];
+      bool on = false;
+      if (e < g.E) {
+        double phi[kMaxSplits], rho[kMaxCols];
+        on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
+        row[0] = cand_flow(g, t, e, phi, rho, on);
+        nc0 += fabs(row[0]) > g.br_lim[e];
+        if (on) {
+          const double be = g.br_b[e];
+          for (int q = 0; q < ns; ++q) row[1 + q] = be * phi[q];
+          for (int m = 0; m < nv; ++m) row[1 + ns + m] = be * rho[m];
+        }
       }
+      if (csum) {
+        // live rows only: removed / out-of-service rows carry no flow in the
+        // exact path (their elements are never scored)
+        float v[kCsum];
+        v[0] = on ? __double2float_ru(fabs(row[0] - g.f0[e])) : 0.0f;
+#pragma unroll
+        for (int q = 0; q + 1 < kCsum; ++q) v[1 + q] = on && q < r ? __double2float_ru(fabs(row[1 + q])) : 0.0f;
+#pragma unroll
+        for (int q = 0; q < kCsum; ++q)
+#pragma unroll
+          for (int o = 16; o > 0; o >>= 1) v[q] = fmaxf(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+        if ((threadIdx.x & 31) == 0) {
+          float4* dst = reinterpret_cast<float4*>(csum + static_cast<size_t>(e0 >> 5) * kCsum);
+          dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+          dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+        }
+      }
+      if (e >= g.E) continue;
       if (b.feat_mt) {  // multi-timestep bounds (profile 0; k_prep_mt folds the later profiles in)
         unsigned long long* m = reinterpret_cast<unsigned long long*>(b.feat_mt + feat_index(slot, b.nchunks, e, r + 1));
         const unsigned long long key = order_key(row[0]);

@@ -14,6 +14,8 @@ size_t topo_core_bytes();
 constexpr int kMaxRemovedSweep = 4;  // genome disconnections skipped in the sweep (n_d <= 4)
 constexpr int kGroupSlots = 16;      // candidates per sweep CTA group (8 warps x 2)
 constexpr int kChunkRows = 32;       // branch rows per sweep pipeline stage
+constexpr int kCsum = 8;             // floats per (candidate, chunk) summary: max |f_c - f0|, max |L_0..6|
+constexpr int kChunkedMaxRank = 7;   // ranks handled by the chunked sweep (higher ranks: k_sweep_hi)
 
 // Ordered-integer key of a double (any sign): keys compare like the values.
 __device__ inline unsigned long long order_key(double x) {
@@ -75,7 +77,11 @@ struct Batch {
   double* feat;
   int* slot;                  // [n] group * kGroupSlots + position, -1 when not swept
   int nchunks;                // ceil(E / kChunkRows)
-  unsigned long long* rows_done;  // [4] sweep stats: blocks computed / offered / overloaded / first FMA only
+  unsigned long long* rows_done;  // [8] sweep stats: blocks computed / offered / overloaded / first FMA only,
+                                  // chunk tests / hot chunks (chunked sweep)
+  float* csum;                // [n][nchunks][kCsum] per (candidate, 32-row chunk): max |f_c - f0| and max |L_q|
+                              // (q < rank) over the chunk's live rows, floats rounded up (k_prep; ranks <= 7)
+  unsigned int* item_ctr;     // [4] work counters of the persistent chunked sweep (zeroed per evaluation)
   double* kdat;               // [n][Kpad * kStride]: Kpad rows of row_stride(r) doubles alpha, R'
                               // (single-branch contingencies)
   uint8_t* kflag;             // [n][Kpad] 0 ok, 1 islanded, 2 padding
@@ -184,6 +190,12 @@ bool device_spd_inverse(double* a, int n, cudaStream_t stream);
 // Skip records of n_t profiles (contiguous, rec_floats each) combined into
 // bounds over all profiles (multi-timestep screening).
 void launch_rec_combine(const float* recs, size_t rec_floats, int n_t, float* out, cudaStream_t stream);
+// Base N-1 headroom per branch row (lim - max_k |f0 + T_base alpha0|) for the
+// sweep row order; needs g.{E, Nr, Ks, red, br_*, X, ks_branch}.
+void launch_row_headroom(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* h,
+                         cudaStream_t stream);
+// Chunk records (DevGrid::Crec) from a profile's skip records, base flows and limits.
+void launch_chunk_records(const DevGrid& g, float* crec, cudaStream_t stream);
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
                         float* tmax, double* alpha0, cudaStream_t stream);
 

@@ -167,7 +167,79 @@ __global__ void k_rec_combine(const float* recs, size_t rec_floats, int n_t, flo
   }
 }
 
+// Base N-1 headroom of every branch row: lim_e - max_k |f0_e + T_base[e,k] alpha0_k|
+// over the single-branch contingencies (own outage excluded), one warp per row.
+// Used once at context creation to order the sweep rows (near-overloaded rows
+// last). X is symmetric: x(r_e, c) is read along row r_e (contiguous).
+__global__ void k_row_headroom(DevGrid g, double* h) {
+  const int lane = threadIdx.x & 31;
+  for (int e = (blockIdx.x * blockDim.x + threadIdx.x) >> 5; e < g.E; e += (gridDim.x * blockDim.x) >> 5) {
+    const int ri = g.red[g.br_from[e]], rj = g.red[g.br_to[e]];
+    const double b = g.br_b[e], fe = g.f0[e];
+    const double* xi = ri >= 0 ? g.X + static_cast<size_t>(ri) * g.Nr : nullptr;
+    const double* xj = rj >= 0 ? g.X + static_cast<size_t>(rj) * g.Nr : nullptr;
+    double m = fabs(fe);
+    for (int k = lane; k < g.Ks && g.br_on[e]; k += 32) {
+      const int beta = g.ks_branch[k];
+      if (beta == e) continue;
+      const int fk = g.red[g.br_from[beta]], tk = g.red[g.br_to[beta]];
+      const double ai = xi ? (fk >= 0 ? xi[fk] : 0.0) - (tk >= 0 ? xi[tk] : 0.0) : 0.0;
+      const double aj = xj ? (fk >= 0 ? xj[fk] : 0.0) - (tk >= 0 ? xj[tk] : 0.0) : 0.0;
+      const double den = 1.0 - g.Tdiag[beta];
+      const double a0 = fabs(den) >= 1e-8 ? g.f0[beta] / den : 0.0;
+      m = fmax(m, fabs(fe + b * (ai - aj) * a0));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if (lane == 0) h[e] = g.br_lim[e] - m;
+  }
+}
+
+// Chunk record per (tile, 32-row chunk), one thread each: the chunk-level
+// relaxation of the row records. For every row e of the chunk and element k of
+// the tile, |f1| <= max(f0_e + D0max, -(f0_e + D0min)) + |f_c - f0|_e + w_e, so
+// a chunk whose rows all satisfy  max|f_c - f0| + max w < min_e headroom_e
+// cannot overload (sweep.cu, chunked sweep). The headroom is lowered by
+// 1e-9 (lim + |f0| + |D0max| + |D0min|) over the chunk: far more than the
+// rounding of any computed f1 (FP64, a few ulps).
+__global__ void k_chunk_rec(DevGrid g, float* crec, int W, int ld) {
+  const int ntiles = g.Kpad / W, nch = (g.E + kChunkRows - 1) / kChunkRows;
+  for (int idx = blockIdx.x * blockDim.x + threadIdx.x; idx < ntiles * nch; idx += gridDim.x * blockDim.x) {
+    const int tile = idx / nch, ch = idx % nch;
+    float tm[kTmaxSub];
+    for (int q = 0; q < kTmaxSub; ++q) tm[q] = 0.0f;
+    double h = CUDART_INF, sl = 0.0;
+    for (int e = ch * kChunkRows; e < min(g.E, (ch + 1) * kChunkRows); ++e) {
+      const float* rec = g.Tmax + (static_cast<size_t>(tile) * ld + e) * kRec;
+      for (int q = 0; q < kTmaxSub; ++q) tm[q] = fmaxf(tm[q], rec[q]);
+      const double2 d0 = *reinterpret_cast<const double2*>(rec + kTmaxSub);
+      const double f = g.f0[e], lim = g.br_lim[e];
+      h = fmin(h, lim - fmax(f + d0.x, -(f + d0.y)));
+      sl = fmax(sl, fabs(lim) + fabs(f) + fabs(d0.x) + fabs(d0.y));
+    }
+    float* out = crec + static_cast<size_t>(idx) * kRec;
+    for (int q = 0; q < kTmaxSub; ++q) out[q] = tm[q];
+    *reinterpret_cast<double2*>(out + kTmaxSub) = make_double2(h - 1e-9 * sl, 0.0);
+  }
+}
+
 }  // namespace
+
+void launch_chunk_records(const DevGrid& g, float* crec, cudaStream_t stream) {
+  const int n = (g.Kpad / sweep_tile_k()) * ((g.E + kChunkRows - 1) / kChunkRows);
+  if (n > 0) k_chunk_rec<<<(n + 255) / 256, 256, 0, stream>>>(g, crec, sweep_tile_k(), g.E + sweep_chunk());
+}
+
+void launch_row_headroom(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* h,
+                         cudaStream_t stream) {
+  k_theta<<<(g.Nr + 255) / 256 + 1, 256, 0, stream>>>(g, p_red, theta0);
+  DevGrid g2 = g;
+  g2.theta0 = theta0;
+  k_branch_base<<<(g.E + 255) / 256 + 1, 256, 0, stream>>>(g2, theta0, f0, tdiag);
+  g2.f0 = f0;
+  g2.Tdiag = tdiag;
+  k_row_headroom<<<148 * 8, 256, 0, stream>>>(g2, h);
+}
 
 void launch_rec_combine(const float* recs, size_t rec_floats, int n_t, float* out, cudaStream_t stream) {
   k_rec_combine<<<1024, 256, 0, stream>>>(recs, rec_floats, n_t, out);

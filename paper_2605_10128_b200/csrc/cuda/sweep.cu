@@ -916,6 +916,351 @@ __global__ void __launch_bounds__(kMaskThreads, 2) k_sweep_masked(DevGrid g, Bat
   }
 }
 
+// ---------------------------------------------------------------- chunked sweep
+// Scores-only sweep for ranks <= kChunkedMaxRank on one injection profile
+// (the MapElites path). Persistent: every warp takes (candidate, tile) work
+// items from a global counter (candidate-major, so concurrently running warps
+// share the candidate's rows in L2) and runs them on its own, with no CTA-wide
+// synchronization:
+//   1. the candidate's alpha / R' of the tile in registers (4 contingencies per
+//      lane), the bound operands max |alpha - alpha0| per sub-tile and max |R'_q|
+//      per tile as in sweep_cta;
+//   2. chunk test, one lane per 32-row chunk: every element of the chunk and
+//      tile satisfies |f1| <= (base N-1 flow) + |f_c - f0| + |T_base||delta| +
+//      sum_q |L_q||R'_q|, so the chunk is safe when
+//        max|f_c - f0| + max_s Tmc_s delta_s + sum_q Lmax_q Rmax_q < Hc
+//      (Crec: Tmc, Hc per (tile, chunk); csum: max|f_c - f0|, Lmax per
+//      (candidate, chunk); FP32 with upward rounding and a 1e-6 relative
+//      margin against a headroom already lowered for FP64 rounding). With the
+//      rows in locality order (capi.cu sweep_row_order) most chunks of a tile
+//      are far from the candidate's changes and pass;
+//   3. the hot chunks' rows (candidate rows, limits, row skip records) are
+//      staged by TMA bulk copies into a per-warp ring (lane 0 refills a stage
+//      once the warp has left it) and run the row-level stages 1-3 of
+//      sweep_cta unchanged (same arithmetic, so the result equals the dense
+//      sweep bit for bit).
+constexpr int kCkWarps = 8;                   // warps per CTA (independent), 2 CTAs per SM
+constexpr int kCkThreads = 32 * kCkWarps;
+constexpr int kCkMaxChunks = 512;             // E <= 16384 rows (16-bit hot-chunk list)
+constexpr size_t kCkWarpBytes = 13 * 1024 + 512;  // shared memory per warp
+constexpr size_t kCkHead = 64 + 128 + 32 + 2 * kCkMaxChunks;  // barriers, rms, asub, hot list
+constexpr int kCkMaxStages = 4;
+
+template <int R>
+struct CkRing {
+  static constexpr int S = row_stride(R);
+  static constexpr size_t F = static_cast<size_t>(kChunk) * S * 8;  // candidate rows of one chunk
+  static constexpr size_t L = kChunk * 8;                            // limits
+  static constexpr size_t M = static_cast<size_t>(kChunk) * kRec * 4;  // row skip records
+  static constexpr size_t stage = F + L + M;
+  static constexpr size_t fit = (kCkWarpBytes - kCkHead) / stage;
+  static constexpr int stages = fit < static_cast<size_t>(kCkMaxStages) ? static_cast<int>(fit) : kCkMaxStages;
+  static_assert(stages >= 2, "chunked ring too small");
+  static_assert(F % 16 == 0 && M % 16 == 0 && kCkHead % 16 == 0, "bulk copies move 16-byte multiples");
+};
+constexpr size_t kCkSmemBytes = kCkWarps * kCkWarpBytes;
+
+template <int R>
+__device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int cid, int tile, uint8_t* ws,
+                                        uint32_t& phase, unsigned (&stats)[6]) {
+  using Rg = CkRing<R>;
+  constexpr int S = Rg::S, NST = Rg::stages;
+  const int lane = threadIdx.x & 31;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ws);
+  double* rms = reinterpret_cast<double*>(ws + 64);
+  float* asub = reinterpret_cast<float*>(ws + 64 + 128);
+  uint16_t* list = reinterpret_cast<uint16_t*>(ws + 64 + 128 + 32);
+  uint8_t* ring = ws + kCkHead;
+  const int kb = tile * kTileK + lane * kKpl;
+  const int nch = b.nchunks;
+  double alpha[kKpl], rr[kKpl][R > 0 ? R : 1], energy[kKpl];
+  bool kval[kKpl];
+  int kbr[kKpl], rem[kMaxRemovedSweep];
+  {
+    const double* kd = b.kdat + static_cast<size_t>(cid) * g.Kpad * kStride + static_cast<size_t>(kb) * S;
+    const uint8_t* kf = b.kflag + static_cast<size_t>(cid) * g.Kpad + kb;
+#pragma unroll
+    for (int i = 0; i < kKpl; ++i) {
+      kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
+      alpha[i] = kd[i * S];
+#pragma unroll
+      for (int q = 0; q < R; ++q) rr[i][q] = kd[i * S + 1 + q];
+      energy[i] = 0.0;
+      kval[i] = kf[i] == 0;
+    }
+#pragma unroll
+    for (int q = 0; q < kMaxRemovedSweep; ++q) rem[q] = b.removed[static_cast<size_t>(cid) * kMaxRemovedSweep + q];
+  }
+  // bound operands (sweep_cta): asub per sub-tile, rms per tile
+  if (lane < kStride) rms[lane] = 0.0;
+  __syncwarp();
+  {
+    double a = 0.0;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[k] - g.alpha0[kb + k]));
+#pragma unroll
+    for (int o = kSubLanes / 2; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
+    if (lane % kSubLanes == 0) asub[lane / kSubLanes] = __double2float_ru(a * (1.0 + 1e-12));
+#pragma unroll
+    for (int q = 0; q < R; ++q) {
+      double r = 0.0;
+#pragma unroll
+      for (int k = 0; k < kKpl; ++k) r = fmax(r, fabs(rr[k][q]));
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
+      if (lane == 0) rms[1 + q] = r * (1.0 + 1e-12);
+    }
+  }
+  __syncwarp();
+  constexpr bool kRegW = R <= 3;
+  float areg[kRegW ? kTmaxSub : 1];
+  double wreg[kRegW ? S : 1];
+  if (kRegW) {
+#pragma unroll
+    for (int q = 0; q < kTmaxSub; ++q) areg[q] = asub[q];
+#pragma unroll
+    for (int q = 0; q < S; ++q) wreg[q] = rms[q];
+  }
+  // chunk tests -> hot-chunk list
+  int nlist = 0;
+  {
+    float af[kTmaxSub], rf[R > 0 ? R : 1];
+#pragma unroll
+    for (int q = 0; q < kTmaxSub; ++q) af[q] = asub[q];
+#pragma unroll
+    for (int q = 0; q < R; ++q) rf[q] = __double2float_ru(rms[1 + q]);
+    const float* crec = g.Crec + static_cast<size_t>(tile) * nch * kRec;
+    const float* cs = b.csum + static_cast<size_t>(cid) * nch * kCsum;
+    for (int cb = 0; cb < nch; cb += 32) {
+      const int ch = cb + lane;
+      bool hot = false;
+      if (ch < nch) {
+        const float4* rc = reinterpret_cast<const float4*>(crec + static_cast<size_t>(ch) * kRec);
+        const float4 t0 = __ldg(rc), t1 = __ldg(rc + 1);
+        const double hc = __ldg(reinterpret_cast<const double*>(rc + 2));
+        const float4 c0 = __ldg(reinterpret_cast<const float4*>(cs + static_cast<size_t>(ch) * kCsum));
+        const float4 c1 = __ldg(reinterpret_cast<const float4*>(cs + static_cast<size_t>(ch) * kCsum) + 1);
+        const float cv[kCsum] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
+        float td = fmaxf(fmaxf(fmaxf(__fmul_ru(t0.x, af[0]), __fmul_ru(t0.y, af[1])),
+                               fmaxf(__fmul_ru(t0.z, af[2]), __fmul_ru(t0.w, af[3]))),
+                         fmaxf(fmaxf(__fmul_ru(t1.x, af[4]), __fmul_ru(t1.y, af[5])),
+                               fmaxf(__fmul_ru(t1.z, af[6]), __fmul_ru(t1.w, af[7]))));
+        float bnd = __fadd_ru(cv[0], td);
+#pragma unroll
+        for (int q = 0; q < R; ++q) bnd = __fmaf_ru(cv[1 + q], rf[q], bnd);
+        hot = static_cast<double>(__fmul_ru(bnd, 1.000001f)) >= hc;
+      }
+      const unsigned m = __ballot_sync(0xffffffffu, hot);
+      if (hot) list[nlist + __popc(m & ((1u << lane) - 1))] = static_cast<uint16_t>(ch);
+      nlist += __popc(m);
+    }
+    stats[4] += static_cast<unsigned>(nch);
+    stats[5] += static_cast<unsigned>(nlist);
+    stats[1] += static_cast<unsigned>(g.E);  // rows offered (every row of the tile)
+  }
+  __syncwarp();
+  // stage of list entry j: j % NST; each stage barrier completes one phase per
+  // fill and the warp waits for every fill, so the per-stage parity bits in
+  // `phase` stay valid across items of different ring geometry
+  auto issue = [&](int j) {  // lane 0
+    const int st = j % NST;
+    const int e0 = list[j] * kChunk;
+    uint8_t* dst = ring + static_cast<size_t>(st) * Rg::stage;
+    uint64_t* bar = bars + st;
+    mbar_expect_tx(bar, static_cast<uint32_t>(Rg::stage));
+    const int slot = b.slot[cid];
+    bulk_g2s(dst, b.feat + feat_index(slot, nch, e0, R), static_cast<uint32_t>(Rg::F), bar);
+    bulk_g2s(dst + Rg::F, g.br_lim + e0, static_cast<uint32_t>(Rg::L), bar);
+    bulk_g2s(dst + Rg::F + Rg::L, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kRec,
+             static_cast<uint32_t>(Rg::M), bar);
+  };
+  if (lane == 0)
+    for (int j = 0; j < NST && j < nlist; ++j) issue(j);
+
+  auto exact_row = [&](int e, double lim, const double (&f1)[kKpl]) {
+    bool skip_row = false;
+#pragma unroll
+    for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[q];
+    unsigned long long m = 0ull;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k) {
+      if (!kval[k] || skip_row || e == kbr[k]) continue;
+      const double a = fabs(f1[k]);
+      if (a > lim) {
+        energy[k] += a - lim;
+        m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
+      }
+    }
+    if (m > static_cast<unsigned long long>(__double_as_longlong(lim))) atomicMax(b.fmax + static_cast<size_t>(cid) * g.E + e, m);
+  };
+  auto finish_row = [&](int e, double lim, const double* fr, double (&f1)[kKpl]) {
+    double fl[R > 0 ? R : 1];
+#pragma unroll
+    for (int q = 0; q < R; ++q) fl[q] = fr[1 + q];
+    uint32_t mx = 0u;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k) {
+      double acc = f1[k];
+#pragma unroll
+      for (int q = 0; q < R; ++q) acc = fma(fl[q], rr[k][q], acc);
+      f1[k] = acc;
+      mx = max(mx, hi_abs(acc));
+    }
+    if (__any_sync(0xffffffffu, mx >= hi_abs(lim))) {
+      exact_row(e, lim, f1);
+      return true;
+    }
+    return false;
+  };
+
+  for (int j = 0; j < nlist; ++j) {
+    const int st = j % NST;
+    const uint8_t* sb = ring + static_cast<size_t>(st) * Rg::stage;
+    mbar_wait(bars + st, (phase >> st) & 1u);
+    phase ^= 1u << st;
+    const int e0 = list[j] * kChunk;
+    const int rows = min(kChunk, g.E - e0);
+    const double* sF = reinterpret_cast<const double*>(sb);
+    const double* sL = reinterpret_cast<const double*>(sb + Rg::F);
+    const float* sM = reinterpret_cast<const float*>(sb + Rg::F + Rg::L);
+    // stage 1 (sweep_cta, same arithmetic): one lane per row
+    bool hot = false;
+    uint32_t thr_lane = 0u;
+    if (lane < rows) {
+      const double lim = sL[lane] * (1.0 - 1e-12);
+      const float4* rec = reinterpret_cast<const float4*>(sM) + lane * (kRec / 4);
+      const double2* fr = reinterpret_cast<const double2*>(sF + lane * S);
+      const double2* wr = reinterpret_cast<const double2*>(rms);
+      double l0 = 0.0, l1 = 0.0, fc = 0.0;
+#pragma unroll
+      for (int q = 0; q < S / 2; ++q) {
+        const double2 p2 = fr[q];
+        const double2 w2 = kRegW ? make_double2(wreg[kRegW ? 2 * q : 0], wreg[kRegW ? 2 * q + 1 : 0]) : wr[q];
+        l0 = fma(fabs(p2.x), w2.x, l0);
+        l1 = fma(fabs(p2.y), w2.y, l1);
+        if (q == 0) fc = p2.x;
+      }
+      const double flo = fc;
+      const double lrb = l0 + l1;
+      const float4* ar = reinterpret_cast<const float4*>(asub);
+      float taf = 0.0f;
+#pragma unroll
+      for (int q = 0; q < kTmaxSub / 4; ++q) {
+        const float4 t4 = rec[q];
+        const float4 a4 = kRegW ? make_float4(areg[kRegW ? 4 * q : 0], areg[kRegW ? 4 * q + 1 : 0],
+                                              areg[kRegW ? 4 * q + 2 : 0], areg[kRegW ? 4 * q + 3 : 0])
+                                : ar[q];
+        taf = fmaxf(taf, fmaxf(fmaxf(__fmul_ru(t4.x, a4.x), __fmul_ru(t4.y, a4.y)),
+                               fmaxf(__fmul_ru(t4.z, a4.z), __fmul_ru(t4.w, a4.w))));
+      }
+      const double2 d0 = reinterpret_cast<const double2*>(rec)[kTmaxSub / 4];
+      const double thr = lim - lrb;
+      thr_lane = thr > 0.0 ? hi_abs(thr) : 0u;
+      const double gap = lim - fmax(fc + d0.x, -(flo + d0.y));
+      const double s0 = 1e-12 * (fmax(fabs(fc), fabs(flo)) + fabs(d0.x) + fabs(d0.y));
+      const double wd = static_cast<double>(taf) + lrb;
+      hot = fma(wd, 1.0 + 1e-12, s0) >= gap;
+    }
+    unsigned need = __ballot_sync(0xffffffffu, hot);
+    stats[3] += __popc(need);
+    // stage 2 / 3 (sweep_cta)
+    constexpr int NB = R >= 6 ? 1 : (R >= 4 ? 2 : 4);
+    const double* tk_rows = g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK + lane * kKpl;
+    while (need) {
+      int els[NB];
+      int nu = 0;
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        els[u] = need ? __ffs(need) - 1 : -1;
+        if (need) need &= need - 1, ++nu;
+      }
+      double2 t[NB][2];
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        const int el = els[u] >= 0 ? els[u] : els[0];
+        const double2* src = reinterpret_cast<const double2*>(tk_rows + static_cast<size_t>(el) * kTileK);
+        t[u][0] = __ldg(src);
+        t[u][1] = __ldg(src + 1);
+      }
+#pragma unroll
+      for (int u = 0; u < NB; ++u) {
+        if (u >= nu) break;
+        const int el = els[u];
+        const double fc = sF[el * S];
+        const uint32_t thr = __shfl_sync(0xffffffffu, thr_lane, el);
+        const double tv[kKpl] = {t[u][0].x, t[u][0].y, t[u][1].x, t[u][1].y};
+        double f1[kKpl];
+        uint32_t m = 0u;
+#pragma unroll
+        for (int k = 0; k < kKpl; ++k) {
+          f1[k] = fma(tv[k], alpha[k], fc);
+          m = max(m, hi_abs(f1[k]));
+        }
+        if (!__any_sync(0xffffffffu, m >= thr)) continue;
+        ++stats[0];
+        stats[2] += finish_row(e0 + el, sL[el], sF + el * S, f1) ? 1u : 0u;
+      }
+    }
+    __syncwarp();
+    if (lane == 0 && j + NST < nlist) {
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      issue(j + NST);
+    }
+    __syncwarp();
+  }
+  double* en = b.energy + static_cast<size_t>(cid) * g.Kall;
+#pragma unroll
+  for (int k = 0; k < kKpl; ++k)
+    if (kval[k] && kb + k < g.Ks) en[g.ks_cont[kb + k]] = energy[k];
+}
+
+template <int RLO, int RHI>
+__device__ __forceinline__ void ck_dispatch(const DevGrid& g, const Batch& b, int r, int cid, int tile, uint8_t* ws,
+                                            uint32_t& phase, unsigned (&stats)[6]) {
+  if constexpr (RLO <= RHI) {
+    if (r == RLO || RLO == RHI) {
+      ck_item<RLO>(g, b, cid, tile, ws, phase, stats);
+    } else {
+      ck_dispatch<RLO + 1, RHI>(g, b, r, cid, tile, ws, phase, stats);
+    }
+  }
+}
+
+// ranks RLO..RHI (one kernel per rank class: each gets its own register allocation)
+template <int RLO, int RHI>
+__global__ void __launch_bounds__(kCkThreads, 2) k_sweep_chunked(DevGrid g, Batch b, int ntiles, unsigned* ctr) {
+  extern __shared__ __align__(128) uint8_t ck_smem[];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  uint8_t* ws = ck_smem + static_cast<size_t>(warp) * kCkWarpBytes;
+  uint64_t* bars = reinterpret_cast<uint64_t*>(ws);
+  if (lane == 0) {
+    for (int s = 0; s < kCkMaxStages; ++s) mbar_init(bars + s, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+  }
+  __syncwarp();
+  const int first = b.wl_start[RLO];
+  const int ncand = b.wl_start[RHI] + b.wl_count[RHI] - first;
+  const long items = static_cast<long>(ncand) * ntiles;
+  uint32_t phase = 0;
+  unsigned stats[6] = {0, 0, 0, 0, 0, 0};
+  for (;;) {
+    long it = 0;
+    if (lane == 0) it = atomicAdd(ctr, 1u);
+    it = __shfl_sync(0xffffffffu, it, 0);
+    if (it >= items) break;
+    const int cid = b.wl_list[first + static_cast<int>(it / ntiles)];
+    const int tile = static_cast<int>(it % ntiles);
+    if (b.status[cid] != 0) continue;
+    ck_dispatch<RLO, RHI>(g, b, b.rank[cid], cid, tile, ws, phase, stats);
+  }
+  if (lane == 0) {
+    for (int i = 0; i < 6; ++i)
+      if (stats[i]) atomicAdd(b.rows_done + i, static_cast<unsigned long long>(stats[i]));
+  }
+}
+constexpr int kCkSplit = 4;  // rank classes [0, kCkSplit] and [kCkSplit + 1, kChunkedMaxRank]
+static_assert(kChunkedMaxRank == 7, "k_sweep_chunked rank switch");
+
 // Stable per-rank lists of swept candidates; bucket r is cut into CTA groups
 // of cand_per_cta(r), and every swept candidate gets its row slot
 // (group * kGroupSlots + position) so k_prep writes straight into the layout
@@ -999,6 +1344,10 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmMask, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmMask, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
+    cudaFuncSetAttribute(k_sweep_chunked<0, kCkSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kCkSmemBytes));
+    cudaFuncSetAttribute(k_sweep_chunked<kCkSplit + 1, kChunkedMaxRank>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                         static_cast<int>(kCkSmemBytes));
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
   static const int gblock_env = [] {
@@ -1012,6 +1361,8 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
   constexpr int kHiCtas = 148;  // persistent: one CTA per SM (two half-group CTAs)
   constexpr int hw = 32 * cta_warps<true>(), hh = kGroupSlots / cta_warps<true>();
   const bool half = g.E <= kHalfMaxRows;
+  static const bool v1 = std::getenv("TGB_SWEEP_V1") != nullptr;  // A/B: the tile-streaming sweep for every rank
+  const bool chunked = !v1 && g.Crec && b.csum && g.E <= kCkMaxChunks * kChunk;
   if (full) {
     k_sweep<true, kTmSingle, false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
     k_sweep_hi<true, kTmSingle, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
@@ -1023,6 +1374,13 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
       k_sweep<false, kTmMask, false><<<grid, kThreads, kSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
       k_sweep_hi<false, kTmMask, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
     }
+  } else if (chunked) {
+    cudaMemsetAsync(b.item_ctr, 0, 2 * sizeof(unsigned int), stream);
+    k_sweep_chunked<0, kCkSplit><<<148 * 2, kCkThreads, kCkSmemBytes, stream>>>(g, b, ntiles, b.item_ctr);
+    k_sweep_chunked<kCkSplit + 1, kChunkedMaxRank><<<148 * 2, kCkThreads, kCkSmemBytes, stream>>>(g, b, ntiles,
+                                                                                                  b.item_ctr + 1);
+    *launched += 1;  // three sweep kernels on this path
+    k_sweep_hi<false, kTmSingle, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
   } else if (half) {
     k_sweep<false, kTmSingle, true><<<grid * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
     k_sweep_hi<false, kTmSingle, true><<<kHiCtas * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles);
