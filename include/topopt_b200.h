@@ -178,6 +178,11 @@ const char* tg_version(void);
 /* load_grid / grid_from_json_text, grid_model.hpp:130-131 */
 tg_status tg_grid_from_json(const char* text, size_t len, tg_grid** out);
 void tg_grid_destroy(tg_grid* grid);
+/* grid_to_json_text, grid_model.cpp:423-485 (the canonical dump; free with tg_free) */
+tg_status tg_grid_to_json(const tg_grid* grid, char** text_out);
+/* grid_content_hash, grid_model.cpp:494-503: FNV-1a of the canonical dump, the
+ * key of the action cache (importer.cpp:407-479) */
+tg_status tg_grid_content_hash(const tg_grid* grid, uint64_t* hash);
 /* fills a desc whose arrays point into the grid object (valid while it lives) */
 tg_status tg_grid_describe(const tg_grid* grid, tg_grid_desc* out);
 /* build_action_set, importer.hpp:80 (EnumerationConfig seed/cap, importer.hpp:68-71) */

@@ -80,6 +80,14 @@ def lib() -> C.CDLL:
         L.oc_random_grid_json.restype = vp
         L.oc_random_genomes.argtypes = [vp, C.c_int, C.c_int, C.c_uint64, C.c_int, i32p]
         L.oc_rebuild_flows.argtypes = [vp, i32p, C.c_int, C.c_int, f64p, i32p]
+        L.oc_grid_json.argtypes = [vp]
+        L.oc_grid_json.restype = vp
+        L.oc_grid_hash.argtypes = [vp]
+        L.oc_grid_hash.restype = C.c_uint64
+        L.oc_action_cache.argtypes = [vp]
+        L.oc_action_cache.restype = vp
+        L.oc_action_cache_load.argtypes = [vp, C.c_char_p]
+        L.oc_action_cache_load.restype = C.c_int64
         _lib = L
     return _lib
 
@@ -116,6 +124,22 @@ class OracleContext:
             raise RuntimeError(f"oracle error {rc}: {lib().oc_last_error().decode()}")
         self.worst_k = worst_k
         self.info = json.loads(_take_string(lib().oc_context_info(self.h)))
+
+    def grid_json(self) -> str:
+        """grid_to_json_text (grid_model.cpp:423-485)."""
+        return _take_string(lib().oc_grid_json(self.h))
+
+    def grid_hash(self) -> int:
+        """grid_content_hash (grid_model.cpp:494-503)."""
+        return int(lib().oc_grid_hash(self.h))
+
+    def action_cache(self) -> str:
+        """save_action_set's text (importer.cpp:407-430)."""
+        return _take_string(lib().oc_action_cache(self.h))
+
+    def load_action_cache(self, text: str) -> int:
+        """load_action_set (importer.cpp:432-479): action count, -1 if rejected."""
+        return int(lib().oc_action_cache_load(self.h, text.encode()))
 
     def __del__(self):
         if getattr(self, "h", None):

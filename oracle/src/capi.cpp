@@ -123,6 +123,22 @@ int oc_context_create(const char* grid_json, uint64_t enum_seed, int64_t enum_ca
 
 void oc_context_destroy(void* h) { delete static_cast<Ctx*>(h); }
 
+// grid_to_json_text / grid_content_hash (grid_model.cpp:423-503) and the
+// action cache text (importer.cpp:407-430) of the context's grid / action set
+char* oc_grid_json(void* h) { return dup_str(grid_to_json_text(static_cast<Ctx*>(h)->grid)); }
+uint64_t oc_grid_hash(void* h) { return grid_content_hash(static_cast<Ctx*>(h)->grid); }
+char* oc_action_cache(void* h) {
+  auto* c = static_cast<Ctx*>(h);
+  return dup_str(action_set_to_json_text(c->actions, c->grid));
+}
+// load_action_set (importer.cpp:432-479) of `text` against the context's grid:
+// number of actions, -1 when the cache is rejected (hash or ids)
+int64_t oc_action_cache_load(void* h, const char* text) {
+  auto* c = static_cast<Ctx*>(h);
+  auto s = action_set_from_json_text(c->grid, text);
+  return s ? static_cast<int64_t>(s->actions.size()) : -1;
+}
+
 // JSON: {"n_nodes","n_branches","n_contingencies","n_busbar_outages","n_actions",
 //        "disconnectables":[...],"actions":[{substation,group,busbars,open_couplers,lambda_r}],
 //        "station_ranges":{sub:[b,e]}, "pre_score":{...}, "lambda_b_pre"}

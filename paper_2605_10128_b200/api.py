@@ -98,6 +98,21 @@ class GridModel:
         self.branch_from = np.ctypeslib.as_array(d.branch_from, shape=(E,)).copy() if E else np.zeros(0, np.int32)
         self.branch_to = np.ctypeslib.as_array(d.branch_to, shape=(E,)).copy() if E else np.zeros(0, np.int32)
 
+    def to_json_text(self) -> str:
+        """grid_to_json_text (grid_model.cpp:423-485): the canonical dump."""
+        p = C.c_void_p()
+        _check(LIB.tg_grid_to_json(self._h, C.byref(p)))
+        try:
+            return C.string_at(p).decode()
+        finally:
+            LIB.tg_free(p)
+
+    def content_hash(self) -> int:
+        """grid_content_hash (grid_model.cpp:494-503), the action-cache key."""
+        h = C.c_uint64()
+        _check(LIB.tg_grid_content_hash(self._h, C.byref(h)))
+        return int(h.value)
+
     def __del__(self):
         if getattr(self, "_h", None):
             LIB.tg_grid_destroy(self._h)

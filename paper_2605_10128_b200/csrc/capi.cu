@@ -645,6 +645,19 @@ tg_status tg_grid_from_json(const char* text, size_t len, tg_grid** out) {
 
 void tg_grid_destroy(tg_grid* grid) { delete grid; }
 
+tg_status tg_grid_to_json(const tg_grid* grid, char** text_out) {
+  return guarded([&] {
+    const std::string s = tgb::grid_to_json_text(grid->g);
+    char* p = static_cast<char*>(std::malloc(s.size() + 1));
+    std::memcpy(p, s.c_str(), s.size() + 1);
+    *text_out = p;
+  });
+}
+
+tg_status tg_grid_content_hash(const tg_grid* grid, uint64_t* hash) {
+  return guarded([&] { *hash = tgb::grid_content_hash(grid->g); });
+}
+
 tg_status tg_grid_describe(const tg_grid* h, tg_grid_desc* d) {
   return guarded([&] {
     const tgb::Grid& g = h->g;
@@ -691,7 +704,7 @@ tg_status tg_actionset_build(const tg_grid* grid, uint64_t seed, int64_t cap, tg
 tg_status tg_actionset_from_json(const tg_grid* grid, const char* text, size_t len, tg_actionset** out) {
   return guarded([&] {
     auto a = std::make_unique<tg_actionset>();
-    if (!tgb::actions_from_json(std::string(text, len), grid->g, tgb::grid_fingerprint(grid->g), a->t))
+    if (!tgb::actions_from_json(std::string(text, len), grid->g, tgb::grid_content_hash(grid->g), a->t))
       throw tgb::IoError("action cache does not match this grid");
     flatten_actions(*a, grid->g);
     *out = a.release();
@@ -700,7 +713,7 @@ tg_status tg_actionset_from_json(const tg_grid* grid, const char* text, size_t l
 
 tg_status tg_actionset_to_json(const tg_actionset* set, const tg_grid* grid, char** text_out) {
   return guarded([&] {
-    std::string s = tgb::actions_to_json(set->t, grid->g, tgb::grid_fingerprint(grid->g));
+    std::string s = tgb::actions_to_json(set->t, grid->g, tgb::grid_content_hash(grid->g));
     char* p = static_cast<char*>(std::malloc(s.size() + 1));
     std::memcpy(p, s.c_str(), s.size() + 1);
     *text_out = p;

@@ -282,7 +282,9 @@ Grid load_grid_json(const std::string& text) {
   Grid g;
   for (const Value& jn : field(doc, "nodes", "grid").arr) {
     std::string id = get_string(jn, "id", "node");
-    opt_number(jn, "shunt_b_pu", 0.0, "node '" + id + "'");
+    g.node_shunt.push_back(opt_number(jn, "shunt_b_pu", 0.0, "node '" + id + "'"));
+    const Value* sub = jn.find("substation");
+    g.node_sub.push_back(sub && sub->is_string() ? sub->str : std::string());
     if (!g.node_lookup.emplace(id, g.n_nodes()).second) throw ValidationError("duplicate node id '" + id + "'");
     g.node_id.push_back(std::move(id));
   }
@@ -298,9 +300,9 @@ Grid load_grid_json(const std::string& text) {
     g.br_to.push_back(node_of(get_string(jb, "to", w), w));
     g.br_x.push_back(get_number(jb, "x_pu", w));
     g.br_limit.push_back(get_number(jb, "limit_mw", w));
-    opt_number(jb, "r_pu", 0.0, w);
-    opt_number(jb, "b_pu", 0.0, w);
-    opt_number(jb, "tap", 1.0, w);
+    g.br_r.push_back(opt_number(jb, "r_pu", 0.0, w));
+    g.br_bc.push_back(opt_number(jb, "b_pu", 0.0, w));
+    g.br_tap.push_back(opt_number(jb, "tap", 1.0, w));
     const Value* on = jb.find("in_service");
     g.br_on.push_back(on && on->is_bool() ? on->b : 1);
     if (!g.branch_lookup.emplace(id, g.n_branches() - 1).second) throw ValidationError("duplicate branch id '" + id + "'");
@@ -311,11 +313,14 @@ Grid load_grid_json(const std::string& text) {
     const std::string w = "injection '" + id + "'";
     g.inj_node.push_back(node_of(get_string(ji, "node", w), w));
     g.inj_p.push_back(get_number(ji, "p_mw", w));
-    opt_number(ji, "q_mvar", 0.0, w);
+    g.inj_q.push_back(opt_number(ji, "q_mvar", 0.0, w));
     const std::string kind = get_string(ji, "kind", w);
     if (kind != "generator" && kind != "load") throw ParseError(w + ": kind must be 'generator' or 'load'");
     g.inj_gen.push_back(kind == "generator");
-    if (const Value* v = ji.find("v_setpoint_pu")) {
+    const Value* vs = ji.find("v_setpoint_pu");
+    g.inj_has_vset.push_back(vs != nullptr);
+    g.inj_vset.push_back(vs ? vs->num : 0.0);
+    if (const Value* v = vs) {
       if (kind == "load") throw ValidationError("load '" + id + "' carries a voltage setpoint");
       if (!(v->num > 0.0)) throw ValidationError("generator '" + id + "' has a non-positive voltage setpoint");
     }
@@ -712,52 +717,7 @@ ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap) {
   return t;
 }
 
-// Canonical, order-stable dump used only to key the action cache.
-std::uint64_t grid_fingerprint(const Grid& g) {
-  std::string s;
-  char buf[64];
-  auto num = [&](double v) {
-    std::snprintf(buf, sizeof buf, "%.17g;", v);
-    s += buf;
-  };
-  for (const auto& id : g.node_id) s += id + ";";
-  for (int e = 0; e < g.n_branches(); ++e) {
-    s += g.branch_id[e] + ";" + std::to_string(g.br_from[e]) + ";" + std::to_string(g.br_to[e]) + ";";
-    num(g.br_x[e]);
-    num(g.br_limit[e]);
-    s += g.br_on[e] ? "1;" : "0;";
-  }
-  for (int i = 0; i < g.n_injections(); ++i) {
-    s += g.inj_id[i] + ";" + std::to_string(g.inj_node[i]) + ";";
-    num(g.inj_net(i));
-  }
-  for (std::size_t c = 0; c < g.cont_id.size(); ++c) {
-    s += g.cont_id[c] + ":";
-    for (int e : g.cont_branches[c]) s += std::to_string(e) + ",";
-    for (int i : g.cont_injections[c]) s += "i" + std::to_string(i) + ",";
-  }
-  for (const Station& st : g.stations) {
-    s += "S" + std::to_string(st.node) + ";";
-    for (const auto& b : st.busbars) s += b + ",";
-    for (auto [a, b] : st.couplers) s += std::to_string(a) + "-" + std::to_string(b) + ",";
-    for (std::size_t t = 0; t < st.term_kind.size(); ++t) {
-      s += st.term_element[t] + "@" + std::to_string(st.term_default[t]) + "[";
-      for (int r : st.term_reach[t]) s += std::to_string(r) + ",";
-      s += "]";
-    }
-  }
-  for (std::size_t b = 0; b < g.bo_id.size(); ++b)
-    s += g.bo_id[b] + std::to_string(g.bo_station[b]) + "/" + std::to_string(g.bo_busbar[b]) + ";";
-  s += "slack" + std::to_string(g.slack);
-  std::uint64_t h = 14695981039346656037ull;
-  for (unsigned char c : s) {
-    h ^= c;
-    h *= 1099511628211ull;
-  }
-  return h;
-}
-
-// Cache schema of importer.cpp:407-430 (grid_hash is this engine's fingerprint).
+// Cache schema of importer.cpp:407-430 (grid_hash = grid_content_hash, grid_model.cpp:494-503).
 std::string actions_to_json(const ActionTable& t, const Grid& g, std::uint64_t hash) {
   std::string o = "{\"grid_hash\":" + std::to_string(hash) + ",\"disconnectables\":[";
   for (std::size_t i = 0; i < t.disconnectables.size(); ++i)

@@ -61,6 +61,12 @@ struct Grid {
   std::vector<int> bo_station, bo_busbar;
   std::vector<Station> stations;
   int slack = -1;
+  // fields that enter only the canonical dump (grid_to_json_text /
+  // grid_content_hash, grid_model.cpp:423-503): node substation names and
+  // shunts, branch r / charging / tap, injection q and voltage setpoints
+  std::vector<std::string> node_sub;
+  std::vector<double> node_shunt, br_r, br_bc, br_tap, inj_q, inj_vset;
+  std::vector<char> inj_has_vset;
   // Timestep extension (not in the reference, whose GridModel carries one
   // injection vector, grid_model.hpp:36-46): top-level key
   //   "timesteps": {"count": T, "injections": {"<injection id>": [p_mw x T], ...}}
@@ -128,6 +134,11 @@ std::vector<int> enumerate_disconnectables(const Grid& g);
 ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap);
 std::string actions_to_json(const ActionTable& t, const Grid& g, std::uint64_t grid_hash);
 bool actions_from_json(const std::string& text, const Grid& g, std::uint64_t grid_hash, ActionTable& out);
-std::uint64_t grid_fingerprint(const Grid& g);  // FNV-1a over a canonical dump
+// grid_model.cpp:423-485: the reference's canonical serialization (nlohmann
+// ordered_json, dump(2)); grid_model.cpp:494-503: FNV-1a over it, the key of
+// the action cache (importer.cpp:407-479), so caches written by either side
+// load on the other. host/grid_json.cpp.
+std::string grid_to_json_text(const Grid& g);
+std::uint64_t grid_content_hash(const Grid& g);
 
 }  // namespace tgb
