@@ -310,6 +310,7 @@ def main():
     # ---- live roofline of the fused sweep (same loop, sweep bracketed by events)
     P.sweep_timing(ctx, True)
     P.sweep_rows(ctx)  # reset the skip counters
+    P.sweep_chunks(ctx)
     flops = 0.0
     E, Ks, Kp = info["n_branches"], info["n_single"], info["k_padded"]
     T = int(json.loads(text).get("timesteps", {}).get("count", 1))
@@ -328,6 +329,7 @@ def main():
         alg_bytes += T * (8.0 * float(np.sum(stride)) * (E + Kp) + 8.0 * E * Kp * (1 + 10 / 128))
     sweep_ms, sweep_n = P.sweep_timing(ctx, False)
     rows_done, rows_offered, rows_overloaded, rows_partial = P.sweep_rows(ctx)
+    chunk_tests, chunk_hot = P.sweep_chunks(ctx)
     torch.cuda.synchronize()
     avg_ms = sweep_ms / max(sweep_n, 1)  # one sweep launch (one per timestep per generation)
     step_sweep_ms = sweep_ms / n_prof
@@ -437,7 +439,10 @@ def main():
                                       "flop_fraction": executed_frac, "first_fma_block_fraction": partial_frac,
                                       "computed_block_fraction": computed_frac,
                                       "overloaded_block_fraction": rows_overloaded / rows_offered if rows_offered
-                                      else 0.0, "ncu": ncu or None}},
+                                      else 0.0,
+                                      "chunk_tests": chunk_tests,
+                                      "hot_chunk_fraction": chunk_hot / chunk_tests if chunk_tests else None,
+                                      "ncu": ncu or None}},
             "e2e": {"value": e2e_value, "unit": "topologies/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "call": "tg_evaluate_batch (DcContext::evaluate_batch) on pinned host buffers"},

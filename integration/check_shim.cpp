@@ -1,0 +1,15 @@
+// Compile check of the reference-side shim against the reference's own headers
+// (tests/test_integration_shim.py): instantiates every entry point.
+#include "dc_engine_b200.hpp"
+
+void shim_entry_points(const topopt::GridModel& g, const topopt::ActionSet& a, const topopt::QdConfig& q) {
+  topopt::b200::GpuDcContext ctx(g, a, topopt::DcConfig{});
+  std::vector<topopt::Genome> gs{topopt::Genome::empty(q.n_a, q.n_d)};
+  std::vector<topopt::ScoreVector> s = ctx.evaluate_batch(gs, q.batch_size);
+  topopt::ScoreVector one = ctx.evaluate(gs[0]);
+  std::atomic<bool> stop{false};
+  topopt::OptimizerStats st = topopt::b200::run_optimizer_gpu(ctx, q, [](topopt::RepertoireSnapshot) {}, &stop);
+  (void)s;
+  (void)one;
+  (void)st;
+}

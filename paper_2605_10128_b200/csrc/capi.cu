@@ -1046,6 +1046,32 @@ void context_build(tg_context* ctx, const tg_grid_desc* gd, const tg_actionset_d
     // base factorization (base_inverse, in the grid's own branch order)
     const int Nr = g.Nr;
     g.X = X_base;
+    // branch-space columns of every action / disconnectable (topo.cuh
+    // column_sources): k_prep reads a candidate's update columns instead of
+    // building Z = X [U | V]; skipped when they would take more than 1/8 of
+    // the free memory (k_prep then builds Z)
+    g.PhiA = nullptr;
+    g.PsiD = nullptr;
+    {
+      std::vector<int> dob(E, -1);
+      for (int d = 0; d < g.D; ++d) dob[ad->disconnectables[d]] = d;
+      g.disc_of_br = A.upload(dob, s);
+      size_t free_b = 0, total_b = 0;
+      check(cudaMemGetInfo(&free_b, &total_b), "cudaMemGetInfo");
+      const size_t need = static_cast<size_t>(g.A + g.D) * E * sizeof(double);
+      static const bool off = std::getenv("TGB_NO_PHI_COLUMNS") != nullptr;  // A/B switch
+      if (!off && g.A + g.D > 0 && need <= free_b / 8) {
+        double* phi = A.alloc<double>(static_cast<size_t>(g.A + g.D) * E);
+        int* nmv = A.alloc<int>(std::max(g.A, 1));
+        g.PhiA = phi;
+        g.PsiD = phi + static_cast<size_t>(g.A) * E;
+        g.act_nmv = nmv;
+        tgb::launch_phi_columns(g, phi, nmv, phi + static_cast<size_t>(g.A) * E, s);
+        check(cudaGetLastError(), "phi columns");
+      } else {
+        g.act_nmv = A.alloc<int>(1);
+      }
+    }
     // base tables per injection profile (timestep extension; T = 1 is the reference)
     const int T = std::max(1, gd->n_timesteps);
     if (T > 1 && !gd->injection_net_mw_t) throw tgb::ConfigError("n_timesteps > 1 needs injection_net_mw_t");

@@ -84,6 +84,15 @@ struct DevGrid {
   const int* act_bb_ptr;   // [A+1]
   const int* act_imp;
   const int* disc;         // [D] branch index of each disconnectable
+  // Branch-space columns of the low-rank update, precomputed once per context
+  // (setup.cu k_phi_cols; null when they do not fit the memory budget):
+  // PhiA[a][e] = (X u_a)[from_e] - (X u_a)[to_e] for the split column u_a of
+  // action a (all its base-active moved branch ends), PsiD[d][e] the same for
+  // the removal column a_d of disconnectable d (topo.cuh column_sources).
+  const double* PhiA;      // [A][E]
+  const int* act_nmv;      // [A] base-active moved branch ends of each action (-1: no column)
+  const double* PsiD;      // [D][E]
+  const int* disc_of_br;   // [E] disconnectable index of a branch, -1
 };
 
 struct DcParams {

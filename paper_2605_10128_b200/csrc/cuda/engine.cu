@@ -57,6 +57,7 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
   __shared__ Topo t;
   __shared__ double gram[kSweepRank * kSweepRank];
   __shared__ double thv[kSweepRank];
+  __shared__ const double* cbase[kSweepRank];
   __shared__ int nc0_s;
   if (threadIdx.x == 0) nc0_s = 0;
   const int words = (g.E + 31) >> 5;
@@ -74,10 +75,16 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
     double* sol = b.topo_sol ? b.topo_sol + static_cast<size_t>(c) * kTopoSol : nullptr;
     const int ldz = row_stride(t.ns + t.nv);
     double* zbuf = zglob;
+    const bool pc = g.PhiA != nullptr;  // branch-space columns: no Z = X [U | V] per candidate
     __syncthreads();
-    build_z(g, t, zbuf, ldz);
-    __syncthreads();
-    gram_terms(g, t, zbuf, ldz, gram, kSweepRank, thv);
+    if (pc) {
+      if (threadIdx.x == 0) column_sources(g, t, rm_bits, cbase);
+      gram_terms_x(g, t, gram, kSweepRank, thv);
+    } else {
+      build_z(g, t, zbuf, ldz);
+      __syncthreads();
+      gram_terms(g, t, zbuf, ldz, gram, kSweepRank, thv);
+    }
     __syncthreads();
     if (threadIdx.x == 0) small_solve(t, gram, kSweepRank, thv);
     __syncthreads();
@@ -106,7 +113,8 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
       bool on = false;
       if (e < g.E) {
         double phi[kMaxSplits], rho[kMaxCols];
-        on = branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
+        on = pc ? branch_features_pc(g, t, mv_bits, rm_bits, cbase, e, phi, rho)
+                : branch_features(g, t, mv_bits, rm_bits, zbuf, ldz, e, phi, rho);
         row[0] = cand_flow(g, t, e, phi, rho, on);
         nc0 += fabs(row[0]) > g.br_lim[e];
         if (on) {

@@ -194,6 +194,8 @@ void launch_rec_combine(const float* recs, size_t rec_floats, int n_t, float* ou
 // sweep row order; needs g.{E, Nr, Ks, red, br_*, X, ks_branch}.
 void launch_row_headroom(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* h,
                          cudaStream_t stream);
+// Branch-space columns PhiA [A][E], act_nmv [A], PsiD [D][E] (DevGrid) from X.
+void launch_phi_columns(const DevGrid& g, double* phiA, int* act_nmv, double* psiD, cudaStream_t stream);
 // Chunk records (DevGrid::Crec) from a profile's skip records, base flows and limits.
 void launch_chunk_records(const DevGrid& g, float* crec, cudaStream_t stream);
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,

@@ -223,7 +223,64 @@ __global__ void k_chunk_rec(DevGrid g, float* crec, int W, int ld) {
   }
 }
 
+// Branch-space columns (DevGrid::PhiA / PsiD): one CTA per column, columns
+// [0, A) the actions' split columns u_a (moved base-active branch ends, the
+// U-column terms of topo.cuh analyze for a split whose moved branches are all
+// live), [A, A + D) the disconnectables' removal columns a_d. Row e holds
+// (X u)[from_e] - (X u)[to_e] with X u evaluated by build_z's term formula.
+__global__ void k_phi_cols(DevGrid g, double* phiA, int* act_nmv, double* psiD) {
+  __shared__ int tidx[kMaxTerms];
+  __shared__ double tcoef[kMaxTerms];
+  __shared__ int nt_s;
+  const int col = blockIdx.x;
+  if (threadIdx.x == 0) {
+    int nt = 0;
+    if (col < g.A) {
+      const int a = col, s = g.act_station[a], t0 = g.st_term_ptr[s], nterm = g.st_term_ptr[s + 1] - t0;
+      const uint8_t* grp = g.act_group + g.act_group_ptr[a];
+      int nmv = 0;
+      for (int q = 0; q < nterm; ++q) {
+        const int kind = g.term_kind[t0 + q], el = g.term_elem[t0 + q];
+        if (!grp[q] || kind == 2 || !g.br_on[el]) continue;
+        ++nmv;
+        const double coef = g.br_b[el] * (kind == 0 ? 1.0 : -1.0);
+        const int ri = g.red[g.br_from[el]], rj = g.red[g.br_to[el]];
+        if (nt + 2 > kMaxTerms) {
+          nt = -1;
+          break;
+        }
+        if (ri >= 0) tidx[nt] = ri, tcoef[nt++] = coef;
+        if (rj >= 0) tidx[nt] = rj, tcoef[nt++] = -coef;
+      }
+      act_nmv[a] = nt < 0 ? -1 : nmv;
+    } else {
+      const int e = g.disc[col - g.A];
+      const int ri = g.red[g.br_from[e]], rj = g.red[g.br_to[e]];
+      if (ri >= 0) tidx[nt] = ri, tcoef[nt++] = 1.0;
+      if (rj >= 0) tidx[nt] = rj, tcoef[nt++] = -1.0;
+    }
+    nt_s = nt;
+  }
+  __syncthreads();
+  const int nt = nt_s;
+  if (nt < 0) return;
+  double* out = col < g.A ? phiA + static_cast<size_t>(col) * g.E : psiD + static_cast<size_t>(col - g.A) * g.E;
+  for (int e = threadIdx.x; e < g.E; e += blockDim.x) {
+    const int rf = g.red[g.br_from[e]], rt = g.red[g.br_to[e]];
+    double zf = 0.0, zt = 0.0;
+    if (rf >= 0)
+      for (int p = 0; p < nt; ++p) zf = fma(tcoef[p], g.X[static_cast<size_t>(tidx[p]) * g.Nr + rf], zf);
+    if (rt >= 0)
+      for (int p = 0; p < nt; ++p) zt = fma(tcoef[p], g.X[static_cast<size_t>(tidx[p]) * g.Nr + rt], zt);
+    out[e] = zf - zt;
+  }
+}
+
 }  // namespace
+
+void launch_phi_columns(const DevGrid& g, double* phiA, int* act_nmv, double* psiD, cudaStream_t stream) {
+  if (g.A + g.D > 0) k_phi_cols<<<g.A + g.D, 256, 0, stream>>>(g, phiA, act_nmv, psiD);
+}
 
 void launch_chunk_records(const DevGrid& g, float* crec, cudaStream_t stream) {
   const int n = (g.Kpad / sweep_tile_k()) * ((g.E + kChunkRows - 1) / kChunkRows);

@@ -558,6 +558,83 @@ __device__ inline bool branch_features(const DevGrid& g, const Topo& t, const ui
   return active_branch(g, rm_bits, e);
 }
 
+// ---- precomputed branch-space columns (no per-candidate Z) -------------------
+// With DevGrid::PhiA / PsiD a column of [U | V] is read in branch space: the
+// split column of action a (all its base-active moved ends) is PhiA[a], a
+// removed disconnectable d is PsiD[d]; any other column (a split whose moved
+// branch is also removed, a grounded dead node) is evaluated from its sparse
+// node-space terms by X gathers. Same values as build_z + branch_features
+// (up to the summation order of the terms).
+
+// Z value of column c at reduced node v: sum_p coef_p X[term_p, v] (build_z's row formula).
+__device__ __forceinline__ double zval(const DevGrid& g, const TopoCore& t, int c, int v) {
+  double acc = 0.0;
+  for (int p = t.col_ptr[c]; p < t.col_ptr[c + 1]; ++p)
+    acc = fma(t.term_coef[p], g.X[static_cast<size_t>(t.term_idx[p]) * g.Nr + v], acc);
+  return acc;
+}
+
+// Gram entries G = [U|V]^T X [U|V] and th = [U|V]^T theta' from X gathers
+// (all threads of the block; gram_terms without Z).
+__device__ inline void gram_terms_x(const DevGrid& g, const TopoCore& t, double* G, int ldg, double* th) {
+  const int ncol = t.ns + t.nv;
+  for (int i = threadIdx.x; i < ncol * ncol + ncol; i += blockDim.x) {
+    if (i < ncol * ncol) {
+      const int c = i / ncol, c2 = i % ncol;
+      double acc = 0.0;
+      for (int p = t.col_ptr[c]; p < t.col_ptr[c + 1]; ++p) acc = fma(t.term_coef[p], zval(g, t, c2, t.term_idx[p]), acc);
+      G[c * ldg + c2] = acc;
+    } else {
+      const int c = i - ncol * ncol;
+      double acc = 0.0;
+      for (int p = t.col_ptr[c]; p < t.col_ptr[c + 1]; ++p) acc = fma(t.term_coef[p], theta_mod(g, t, t.term_idx[p]), acc);
+      th[c] = acc;
+    }
+  }
+}
+
+// Branch-space source of each column (thread 0): PhiA / PsiD row, or null
+// for the gather path.
+__device__ inline void column_sources(const DevGrid& g, const TopoCore& t, const uint32_t* rm_bits,
+                                      const double** base) {
+  for (int q = 0; q < t.ns; ++q) {
+    const int j = t.node_of_q[q], a = t.action_of_new[j];
+    int cnt = 0;
+    for (int i = 0; i < t.nmv; ++i) cnt += t.mv_c[i][j] != 0 && active_branch(g, rm_bits, t.mv_branch[i]);
+    base[q] = g.act_nmv[a] == cnt ? g.PhiA + static_cast<size_t>(a) * g.E : nullptr;
+  }
+  for (int m = 0; m < t.nv; ++m) {
+    const int d = m < t.nrem ? g.disc_of_br[t.rem[m]] : -1;
+    base[t.ns + m] = d >= 0 ? g.PsiD + static_cast<size_t>(d) * g.E : nullptr;
+  }
+}
+
+// branch_features with the branch-space column sources.
+__device__ inline bool branch_features_pc(const DevGrid& g, const Topo& t, const uint32_t* mv_bits,
+                                          const uint32_t* rm_bits, const double* const* base, int e, double* phi,
+                                          double* rho) {
+  const int ns = t.ns, nv = t.nv;
+  const int rf = g.red[g.br_from[e]], rt = g.red[g.br_to[e]];
+  for (int c = 0; c < ns + nv; ++c) {
+    double d;
+    if (base[c]) {
+      d = base[c][e];
+    } else {
+      d = (rf >= 0 ? zval(g, t, c, rf) : 0.0) - (rt >= 0 ? zval(g, t, c, rt) : 0.0);
+    }
+    if (c < ns)
+      phi[c] = d;
+    else
+      rho[c - ns] = d;
+  }
+  const int s = moved_slot(t, mv_bits, e);
+  if (s >= 0)
+    for (int q = 0; q < ns; ++q) phi[q] -= t.mv_c[s][t.node_of_q[q]];
+  for (int m = 0; m < nv; ++m)
+    for (int q = 0; q < ns; ++q) rho[m] += t.Y[q * kMaxCols + m] * phi[q];
+  return active_branch(g, rm_bits, e);
+}
+
 // Base flow of e under the (possibly omitted-injection) base injections.
 __device__ inline double base_flow_mod(const DevGrid& g, const TopoCore& t, int e) {
   double f = g.f0[e];
