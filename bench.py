@@ -260,12 +260,27 @@ def main():
 
     ex = None
     shard = None
+    # the engine's own NCCL communicator (tg_islands_*) on NCCL runs; the
+    # torch.distributed exchange for gloo (ranks sharing a GPU) or on request
+    native = False
+    if world > 1:
+        import torch.distributed as dist
+        native = dist.get_backend() == "nccl" and not os.environ.get("TGB_TORCH_EXCHANGE")
     if world > 1 and args.mode == "shard":
-        from paper_2605_10128_b200.islands import BatchShard
-        shard = BatchShard(sess)
+        if native:
+            from paper_2605_10128_b200.islands import NativeIslands
+            nat = NativeIslands(sess)
+
+            class _Shard:
+                def step(self, n):
+                    nat.shard_step(n)
+            shard = _Shard()
+        else:
+            from paper_2605_10128_b200.islands import BatchShard
+            shard = BatchShard(sess)
     elif world > 1 and args.merge_every > 0:
-        from paper_2605_10128_b200.islands import IslandExchange
-        ex = IslandExchange(sess)
+        from paper_2605_10128_b200.islands import IslandExchange, NativeIslands
+        ex = NativeIslands(sess) if native else IslandExchange(sess)
 
     def generations(n):
         if shard is not None:
@@ -317,10 +332,12 @@ def main():
     n_prof = 5
     isl = 0
     alg_bytes = 0.0
+    r_all = np.zeros(0, np.int64)
     for _ in range(n_prof):
         sess.step(1)
         r = P.batch_ranks(ctx, B)
         live = r[r >= 0]
+        r_all = np.concatenate([r_all, live.astype(np.int64)])
         isl += int((r < 0).sum())
         flops += float(E) * Ks * float(np.sum(2.0 * T + 2.0 * live))
         # compulsory sweep traffic: each swept candidate's branch and contingency
@@ -340,8 +357,22 @@ def main():
     # executed FP64 work: blocks past the per-row bound run the first FMA
     # (f_c + T alpha), blocks past the per-element bound also the R FMAs of L R';
     # skipped work cannot change any score
-    executed_frac = ((partial_frac + computed_frac * mean_rank) / (1.0 + mean_rank)) if rows_offered else 1.0
-    executed_tflops = dense_tflops * executed_frac
+    # executed FP64 work per launch: computed blocks x 128 elements x (2 + 2r),
+    # plus the row bound (2 + 2r flops) of every row of a hot chunk
+    per_launch = n_prof * T
+    executed_flops = (rows_done * 128.0 * (2.0 + 2.0 * mean_rank) + chunk_hot * 32.0 * (2.0 + 2.0 * mean_rank)) / per_launch
+    executed_tflops = executed_flops / (avg_ms * 1e-3) / 1e12 if avg_ms else 0.0
+    # compulsory HBM bytes per launch of the chunked sweep
+    stride_mean = float(np.mean((np.maximum(r_all, 0) + 2) & ~1)) if len(r_all) else 2.0
+    n_swept = len(r_all) / n_prof
+    nch = (E + 31) // 32
+    hbm_bytes = (n_swept * (8.0 * stride_mean * Kp + nch * 32.0) + (Kp // 128) * nch * 48.0
+                 + chunk_hot / per_launch * 32.0 * (8.0 * stride_mean + 8.0 + 48.0))
+    hbm_gbs = hbm_bytes / (avg_ms * 1e-3) / 1e9 if avg_ms else 0.0
+    try:
+        hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+    except (OSError, ValueError, KeyError):
+        hbm_peak = 7700.0
     peak = P.fp64_peak_tflops(dev)
     traffic = None
     ncu = {}
@@ -410,7 +441,9 @@ def main():
                                        "all lanes (archive identical to one GPU)" if shard is not None else
                                        f"islands x{world} (seed 1+rank), archives merged every {args.merge_every} "
                                        "generation(s): NCCL allgather of archive blobs + device Repertoire merge"
-                                       if ex is not None else f"islands x{world} (seed 1+rank)"),
+                                       if ex is not None else f"islands x{world} (seed 1+rank)")
+                                      + ("; exchange: engine-native NCCL communicator (tg_islands_*)" if native else
+                                         "; exchange: torch.distributed" if world > 1 else ""),
                        "l2": f"per-step candidate working set {work_bytes / 2**20:.0f} MiB > 126 MiB L2 "
                              "(no flush needed)",
                        "step": "one MapElites generation: mutate/crossover + full N-1 evaluation + archive insert",
@@ -418,31 +451,36 @@ def main():
                        "archive_entries": len(snap.entries), "best_fitness": snap.best_fitness,
                        "context_setup_s": setup_s},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "fp64", "kernel": "k_sweep (fused N-1 sweep)", "achieved": dense_tflops,
-                         "peak": peak, "unit": "TFLOP/s", "frac": dense_tflops / peak if peak else None,
-                         "traffic": traffic,
-                         "algorithmic": "SURVEY.md 8(d): E*K_single*(2T+2r) FP64 flops per swept candidate x the "
-                                        "candidates of one generation, / the generation's sweep time (one launch per "
-                                        "timestep) measured live with CUDA events on the engine stream",
+            "roofline": {"bound": "fp64", "kernel": "k_sweep_chunked (fused N-1 sweep, scores-only)",
+                         "achieved": executed_tflops, "peak": peak, "unit": "TFLOP/s",
+                         "frac": executed_tflops / peak if peak else None, "traffic": traffic,
+                         "algorithmic": "FP64 flops the exact sweep must execute per launch: every (branch row, "
+                                        "128-contingency tile, candidate) block that no bound proves safe (these are "
+                                        "the overloaded blocks up to ~7 %) x 128 elements x (2 + 2r), plus the row "
+                                        "bound of every row of a hot chunk (2 + 2r); / the average launch time "
+                                        "measured live with CUDA events on the engine stream",
+                         "executed_flops_per_launch": executed_flops, "avg_launch_ms": avg_ms,
+                         "mean_rank": mean_rank, "timesteps": T,
                          "peak_source": "DFMA microbenchmark on this GPU in this run (MEASURED_PEAKS.json has no "
                                         "FP64 figure)",
-                         "flops_per_launch": flops / n_prof / T, "avg_launch_ms": avg_ms, "mean_rank": mean_rank,
-                         "timesteps": T,
-                         "algorithmic_bytes_per_launch": alg_bytes / n_prof / T,
+                         "note": "issue-bound on the compare / accumulate work around the FMAs of the overloaded "
+                                 "elements (ncu: profiles/r2/); skipped work provably cannot change a score "
+                                 "(tests/test_gpu_scale.py: bit-identical to the dense sweep)",
+                         "hbm": {"compulsory_bytes_per_launch": hbm_bytes, "achieved_gbs": hbm_gbs,
+                                 "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak if hbm_peak else None,
+                                 "what": "contingency rows of every swept candidate (all tiles), chunk summaries, "
+                                         "chunk records, candidate rows + limits + row records of the hot chunks"},
+                         "dense_equivalent": {"tflops": dense_tflops, "x_fp64_peak": dense_tflops / peak if peak else None,
+                                              "flops_per_launch": flops / n_prof / T,
+                                              "what": "SURVEY.md 8(d) E*K_single*(2T+2r) per swept candidate / the "
+                                                      "launch time: the work of a sweep that evaluates every element "
+                                                      "(not a roofline: the exact skip never executes most of it)"},
                          "islanded_fraction": isl / (n_prof * B),
-                         "note": "the sweep does not execute every algorithmic flop: an exact bound-and-skip proves "
-                                 "most (branch row, contingency tile, candidate) blocks below their limit without "
-                                 "element work (skipped work cannot change a score; tests/test_gpu_scale.py checks "
-                                 "it bit for bit against the dense sweep). 'executed' reports the FP64 work it "
-                                 "does run; the kernel is latency/issue-bound (profiles/)",
-                         "executed": {"tflops": executed_tflops, "frac_of_peak": executed_tflops / peak if peak else None,
-                                      "flop_fraction": executed_frac, "first_fma_block_fraction": partial_frac,
-                                      "computed_block_fraction": computed_frac,
-                                      "overloaded_block_fraction": rows_overloaded / rows_offered if rows_offered
-                                      else 0.0,
-                                      "chunk_tests": chunk_tests,
-                                      "hot_chunk_fraction": chunk_hot / chunk_tests if chunk_tests else None,
-                                      "ncu": ncu or None}},
+                         "skip": {"executed_block_fraction": computed_frac,
+                                  "overloaded_block_fraction": rows_overloaded / rows_offered if rows_offered else 0.0,
+                                  "chunk_tests": chunk_tests,
+                                  "hot_chunk_fraction": chunk_hot / chunk_tests if chunk_tests else None},
+                         "ncu": ncu or None},
             "e2e": {"value": e2e_value, "unit": "topologies/s", "h2d_bytes_per_step": int(h2d),
                     "d2h_bytes_per_step": int(d2h),
                     "call": "tg_evaluate_batch (DcContext::evaluate_batch) on pinned host buffers"},

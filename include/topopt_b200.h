@@ -270,6 +270,25 @@ tg_status tg_qd_scores_blob_bytes(tg_context* ctx, int32_t n, int64_t* bytes);
 tg_status tg_qd_scores_pack(tg_context* ctx, int32_t lo, int32_t hi, void* d_blob);
 tg_status tg_qd_scores_unpack(tg_context* ctx, int32_t lo, int32_t hi, const void* d_blob);
 tg_status tg_qd_generation_end(tg_context* ctx);
+/* ---- native NCCL exchange (host/islands.cpp): one context
+ * per process / GPU, ncclAllGather on the context's stream between the
+ * engine's kernels (no host sync, no torch). NCCL is loaded at run time
+ * (dlopen libnccl.so.2); without it these return TG_CUDA_ERROR.
+ * unique_id: ncclGetUniqueId (128 bytes) on one rank, distributed by the
+ * caller out of band; create: ncclCommInitRank on the context's device (call
+ * on every rank, collectively). exchange = tg_archive_pack -> allgather ->
+ * tg_archive_merge (after tg_qd_begin). step: n generations of this island
+ * with an exchange after every merge_every-th (0 = never). shard_step: n
+ * batch-sharded generations of ONE population (batch_size = the QdConfig's,
+ * divisible by world): generation_begin, this rank's lane slice, score-slice
+ * allgather + unpack, generation_end; the archive equals a one-GPU run. */
+typedef struct tg_islands tg_islands;
+tg_status tg_islands_unique_id(uint8_t* id /* [128] */);
+tg_status tg_islands_create(tg_context* ctx, const uint8_t* id, int32_t rank, int32_t world, tg_islands** out);
+void tg_islands_destroy(tg_islands* islands);
+tg_status tg_islands_exchange(tg_islands* islands);
+tg_status tg_islands_step(tg_islands* islands, int32_t n, int32_t merge_every);
+tg_status tg_islands_shard_step(tg_islands* islands, int32_t n, int32_t batch_size);
 /* descriptor_to_cell, qd_optimizer.cpp:12-17 */
 int32_t tg_descriptor_to_cell(int32_t lambda_d, int32_t lambda_s, int32_t lambda_r, const tg_qd_config* cfg);
 /* Device mutation / crossover of single lanes with the reference RNG stream

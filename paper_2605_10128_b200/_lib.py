@@ -139,6 +139,12 @@ SIGNATURES = [
     ("tg_archive_blob_bytes", C.c_int, [C.c_void_p, i64p]),
     ("tg_archive_pack", C.c_int, [C.c_void_p, C.c_void_p]),
     ("tg_archive_merge", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32]),
+    ("tg_islands_unique_id", C.c_int, [C.c_void_p]),
+    ("tg_islands_create", C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.POINTER(C.c_void_p)]),
+    ("tg_islands_destroy", None, [C.c_void_p]),
+    ("tg_islands_exchange", C.c_int, [C.c_void_p]),
+    ("tg_islands_step", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    ("tg_islands_shard_step", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
 ]
 
 

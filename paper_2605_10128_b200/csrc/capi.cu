@@ -33,6 +33,15 @@ void check(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw CudaFailure(std::string(what) + ": " + cudaGetErrorString(e));
 }
 
+}  // namespace
+
+// host/islands.cpp reports through the same per-thread message as the C ABI
+namespace tgb {
+void set_last_error(const std::string& m) { g_error = m; }
+}  // namespace tgb
+
+namespace {
+
 template <class F>
 tg_status guarded(F&& f) {
   try {
@@ -384,6 +393,7 @@ void tg_context::ensure_capacity(int n) {
   b.isl_out = A.alloc<int>(cap);
   b.isl_bus = A.alloc<int>(cap);
   b.nc0 = A.alloc<int>(cap);
+  b.pc = A.alloc<tgb::PcFac>(cap);
   b.wl_list = A.alloc<int>(cap);
   b.wl_start = A.alloc<int>(tgb::kSweepRank + 1);
   b.wl_count = A.alloc<int>(tgb::kSweepRank + 1);

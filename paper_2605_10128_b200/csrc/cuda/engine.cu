@@ -5,6 +5,7 @@
 // apply_topology / screen_contingencies / compute_scores
 // (dc_engine.cpp:147-468). See topo.cuh for the low-rank formulation.
 #include <algorithm>
+#include <cstdlib>
 
 #include "engine.cuh"
 #include "topo.cuh"
@@ -245,6 +246,286 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
       for (int i = 0; i < kMaxRemovedSweep; ++i) rem[i] = i < t.nrem ? t.rem[i] : -1;
     }
     __syncthreads();
+  }
+}
+
+// ---------------------------------------------------------------- K2 prep, split form
+// With the branch-space columns (DevGrid::PhiA) a candidate's prep splits in
+// two kernels with no CTA-wide phases and no Z = X [U | V]:
+//   k_prep_solve: one warp per candidate: column sources, Gram entries from X
+//     gathers (topo.cuh gram_terms_x), the serial small solve (S^-1, Y, C^-1,
+//     Rp), compact factors to Batch::pc;
+//   k_prep_rows: one warp per (candidate, 32 branch rows) -- the branch rows
+//     [f_c, b_e phi_e, b_e rho_e], the chunk summary (csum) and lambda_c0 --
+//     or per (candidate, 32 contingencies) -- [alpha_k, R'_k] and the flag,
+//     with phi / rho of the outaged branch read from the same columns.
+// Same formulas as k_prep (topo.cuh branch_features / cand_flow); rank R is a
+// template parameter so the row vectors live in registers.
+__global__ void __launch_bounds__(32) k_prep_solve(DevGrid g, Batch b) {
+  __shared__ Topo t;
+  __shared__ double gram[kSweepRank * kSweepRank];
+  __shared__ double thv[kSweepRank];
+  __shared__ const double* cbase[kSweepRank];
+  const int words = (g.E + 31) >> 5;
+  const int tid = threadIdx.x;
+  for (int c = blockIdx.x; c < b.n; c += gridDim.x) {
+    if (b.slot[c] < 0) continue;  // islanded (or over capacity) by the analysis: status already set
+    copy_block(static_cast<TopoCore*>(&t), b.topo + c, sizeof(TopoCore), tid, 32);
+    __syncthreads();
+    const uint32_t* rm_bits = b.tbits + static_cast<size_t>(c) * 2 * words + words;
+    if (tid == 0) {
+      moved_injections(g, t);
+      column_sources(g, t, rm_bits, cbase);
+    }
+    __syncthreads();
+    gram_terms_x(g, t, gram, kSweepRank, thv);
+    __syncthreads();
+    if (tid == 0) small_solve(t, gram, kSweepRank, thv);
+    __syncthreads();
+    if (t.islanded) {
+      if (tid == 0) {
+        b.status[c] = t.islanded;
+        b.rank[c] = -1;
+      }
+      __syncthreads();
+      continue;
+    }
+    const int ns = t.ns, nv = t.nv;
+    PcFac* f = b.pc + c;
+    for (int i = tid; i < kMaxSplits * kMaxSplits; i += 32) f->Sinv[i] = t.Sinv[i];
+    for (int i = tid; i < ns * nv; i += 32) f->Y[(i / nv) * kSweepRank + i % nv] = t.Y[(i / nv) * kMaxCols + i % nv];
+    for (int i = tid; i < nv * nv; i += 32) f->Cinv[(i / nv) * kSweepRank + i % nv] = t.Cinv[(i / nv) * kMaxCols + i % nv];
+    if (tid < ns + nv) {
+      f->Rp[tid] = t.Rp[tid];
+      f->base[tid] = cbase[tid];
+    }
+    if (tid == 0) {
+      f->ns = ns;
+      f->nv = nv;
+      b.status[c] = 0;
+      b.rank[c] = ns + nv;
+      b.nc0[c] = 0;  // k_prep_rows adds its counts
+      int* rem = b.removed + static_cast<size_t>(c) * kMaxRemovedSweep;
+      for (int i = 0; i < kMaxRemovedSweep; ++i) rem[i] = i < t.nrem ? t.rem[i] : -1;
+    }
+    __syncthreads();
+  }
+}
+
+// z = [phi_e ; rho_e] of branch e for a rank-R candidate (branch_features_pc
+// with the compact factors); returns whether e is live.
+template <int R>
+__device__ __forceinline__ bool pc_features(const DevGrid& g, const TopoCore& t, const PcFac& f, const uint32_t* mv_bits,
+                                            const uint32_t* rm_bits, int ns, int e, double (&z)[R > 0 ? R : 1]) {
+  int rf = -2, rt = -2;
+#pragma unroll
+  for (int c = 0; c < R; ++c) {
+    const double* src = f.base[c];
+    if (src) {
+      z[c] = __ldg(src + e);
+    } else {
+      if (rf == -2) rf = g.red[g.br_from[e]], rt = g.red[g.br_to[e]];
+      z[c] = (rf >= 0 ? zval(g, t, c, rf) : 0.0) - (rt >= 0 ? zval(g, t, c, rt) : 0.0);
+    }
+  }
+  if (bit_get(mv_bits, e)) {
+    const int s = moved_slot(t, mv_bits, e);
+#pragma unroll
+    for (int q = 0; q < R; ++q)
+      if (q < ns) z[q] -= t.mv_c[s][t.node_of_q[q]];
+  }
+  // rho_m += sum_q Y[q][m] phi_q (rho index m = c - ns)
+#pragma unroll
+  for (int c = 0; c < R; ++c) {
+    if (c < ns) continue;
+    double acc = z[c];
+#pragma unroll
+    for (int q = 0; q < (R < kMaxSplits ? R : kMaxSplits); ++q)
+      if (q < ns) acc += f.Y[q * kSweepRank + (c - ns)] * z[q];
+    z[c] = acc;
+  }
+  return g.br_on[e] && !bit_get(rm_bits, e);
+}
+
+// candidate flow on a live branch (cand_flow): f0 + b_e (phi . Rp_s + rho . Rp_v)
+template <int R>
+__device__ __forceinline__ double pc_flow(const DevGrid& g, const PcFac& f, int e, const double (&z)[R > 0 ? R : 1]) {
+  double acc = 0.0;
+#pragma unroll
+  for (int c = 0; c < R; ++c) acc = fma(z[c], f.Rp[c], acc);
+  return g.f0[e] + g.br_b[e] * acc;
+}
+
+template <int R>
+__device__ __forceinline__ void prep_branch_chunk(const DevGrid& g, const Batch& b, int c, int slot, int chunk,
+                                                  const TopoCore& t, const PcFac& f, const uint32_t* mv_bits,
+                                                  const uint32_t* rm_bits) {
+  constexpr int RS = row_stride(R);
+  const int lane = threadIdx.x & 31, ns = f.ns;
+  const int e = chunk * kChunkRows + lane;
+  double row[RS];
+#pragma unroll
+  for (int i = 0; i < RS; ++i) row[i] = 0.0;
+  bool on = false;
+  if (e < g.E) {
+    double z[R > 0 ? R : 1];
+    on = pc_features<R>(g, t, f, mv_bits, rm_bits, ns, e, z);
+    if (on) {
+      row[0] = pc_flow<R>(g, f, e, z);
+      const double be = g.br_b[e];
+#pragma unroll
+      for (int q = 0; q < R; ++q) row[1 + q] = be * z[q];
+    }
+  }
+  const unsigned over = __ballot_sync(0xffffffffu, e < g.E && fabs(row[0]) > g.br_lim[e < g.E ? e : 0]);
+  if (lane == 0 && over) atomicAdd(b.nc0 + c, __popc(over));
+  if (R <= kChunkedMaxRank) {
+    float v[kCsum];
+    v[0] = on ? __double2float_ru(fabs(row[0] - g.f0[e])) : 0.0f;
+#pragma unroll
+    for (int q = 0; q + 1 < kCsum; ++q) v[1 + q] = on && q < R ? __double2float_ru(fabs(row[1 + (q < R ? q : 0)])) : 0.0f;
+#pragma unroll
+    for (int q = 0; q < kCsum; ++q)
+#pragma unroll
+      for (int o = 16; o > 0; o >>= 1) v[q] = fmaxf(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+    if (lane == 0) {
+      float4* dst = reinterpret_cast<float4*>(b.csum + (static_cast<size_t>(c) * b.nchunks + chunk) * kCsum);
+      dst[0] = make_float4(v[0], v[1], v[2], v[3]);
+      dst[1] = make_float4(v[4], v[5], v[6], v[7]);
+    }
+  }
+  if (e < g.E) {
+    double2* dst = reinterpret_cast<double2*>(b.feat + feat_index(slot, b.nchunks, e, R));
+#pragma unroll
+    for (int i = 0; i < RS / 2; ++i) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+  }
+}
+
+template <int R>
+__device__ __forceinline__ void prep_cont_chunk(const DevGrid& g, const Batch& b, int c, int kchunk, const TopoCore& t,
+                                                const PcFac& f, const uint32_t* mv_bits, const uint32_t* rm_bits) {
+  constexpr int RS = row_stride(R);
+  const int lane = threadIdx.x & 31, ns = f.ns, nv = f.nv;
+  const int k = kchunk * 32 + lane;
+  double row[RS];
+#pragma unroll
+  for (int i = 0; i < RS; ++i) row[i] = 0.0;
+  uint8_t flag = 2;  // padding
+  if (k < g.Ks) {
+    const int beta = g.ks_branch[k];
+    flag = 0;
+    double z[R > 0 ? R : 1];
+    if (pc_features<R>(g, t, f, mv_bits, rm_bits, ns, beta, z)) {
+      double rk[R > 0 ? R : 1];
+      double lr = 0.0;
+#pragma unroll
+      for (int q = 0; q < (R < kMaxSplits ? R : kMaxSplits); ++q) {
+        if (q >= ns) continue;
+        double acc = 0.0;
+#pragma unroll
+        for (int q2 = 0; q2 < (R < kMaxSplits ? R : kMaxSplits); ++q2)
+          if (q2 < ns) acc += f.Sinv[q * kMaxSplits + q2] * z[q2];
+        rk[q] = acc;
+        lr += z[q] * acc;
+      }
+#pragma unroll
+      for (int c2 = 0; c2 < R; ++c2) {
+        if (c2 < ns) continue;
+        const int m = c2 - ns;
+        double acc = 0.0;
+#pragma unroll
+        for (int c3 = 0; c3 < R; ++c3)
+          if (c3 >= ns) acc += f.Cinv[m * kSweepRank + (c3 - ns)] * z[c3];
+        rk[c2] = -acc;
+        lr -= z[c2] * acc;
+      }
+      const double tkk = g.Tdiag[beta] + g.br_b[beta] * lr;
+      const double den = 1.0 - tkk;
+      if (fabs(den) < 1e-8) {
+        // bridge under the candidate topology (dc_engine.cpp:346-349 -> rebuild):
+        // only a dead stub (degree 1, no injection, not the slack) keeps flows
+        bool stub = false;
+        for (int side = 0; side < 2 && !stub; ++side) {
+          const int w = cand_end(g, t, mv_bits, beta, side == 0);
+          stub = w != g.slack && cand_degree(g, t, mv_bits, rm_bits, w) == 1 && !cand_hosts_injection(g, t, w);
+        }
+        flag = stub ? 0 : 1;
+      } else {
+        const double alpha = pc_flow<R>(g, f, beta, z) / den;
+        row[0] = alpha;
+#pragma unroll
+        for (int i = 0; i < R; ++i) row[1 + i] = rk[i] * alpha;
+      }
+      (void)nv;
+    }
+    if (flag == 1) b.energy[static_cast<size_t>(c) * g.Kall + g.ks_cont[k]] = b.params.penalty;
+  }
+  if (k < g.Kpad) {
+    double2* dst = reinterpret_cast<double2*>(b.kdat + static_cast<size_t>(c) * g.Kpad * kStride +
+                                              static_cast<size_t>(k) * RS);
+#pragma unroll
+    for (int i = 0; i < RS / 2; ++i) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+    b.kflag[static_cast<size_t>(c) * g.Kpad + k] = flag;
+  }
+}
+
+// Warp work item = (candidate of the rank class, segment of kPrepSeg
+// consecutive 32-row chunks: branch rows, then contingency rows). The
+// candidate's factors are staged once per segment in the warp's shared slab.
+constexpr int kPrepSeg = 8;
+constexpr int kPrepRowWarps = 8;
+
+template <int R>
+__device__ __forceinline__ void prep_segment(const DevGrid& g, const Batch& b, int c, int slot, int j0, int j1,
+                                             const PcFac& f) {
+  const int words = (g.E + 31) >> 5;
+  const uint32_t* mv_bits = b.tbits + static_cast<size_t>(c) * 2 * words;
+  const TopoCore& t = b.topo[c];
+  for (int j = j0; j < j1; ++j) {
+    if (j < b.nchunks)
+      prep_branch_chunk<R>(g, b, c, slot, j, t, f, mv_bits, mv_bits + words);
+    else
+      prep_cont_chunk<R>(g, b, c, j - b.nchunks, t, f, mv_bits, mv_bits + words);
+  }
+}
+
+template <int RLO, int RHI>
+__device__ __forceinline__ void prep_segment_dispatch(const DevGrid& g, const Batch& b, int r, int c, int slot, int j0,
+                                                      int j1, const PcFac& f) {
+  if constexpr (RLO <= RHI) {
+    if (r == RLO)
+      prep_segment<RLO>(g, b, c, slot, j0, j1, f);
+    else
+      prep_segment_dispatch<RLO + 1, RHI>(g, b, r, c, slot, j0, j1, f);
+  }
+}
+
+// Ranks [RLO, RHI] from the rank buckets of k_bucket (one register allocation
+// per class; the classes run as separate launches).
+template <int RLO, int RHI>
+__global__ void __launch_bounds__(32 * kPrepRowWarps) k_prep_rows(DevGrid g, Batch b) {
+  __shared__ PcFac slab[kPrepRowWarps];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  PcFac& f = slab[warp];
+  const int per = b.nchunks + g.Kpad / 32;
+  const int nseg = (per + kPrepSeg - 1) / kPrepSeg;
+  const int first = b.wl_start[RLO];
+  const int ncand = b.wl_start[RHI] + b.wl_count[RHI] - first;
+  const long total = static_cast<long>(ncand) * nseg;
+  int loaded = -1;
+  for (long w = static_cast<long>(blockIdx.x) * kPrepRowWarps + warp; w < total;
+       w += static_cast<long>(gridDim.x) * kPrepRowWarps) {
+    const int c = b.wl_list[first + static_cast<int>(w / nseg)];
+    const int sg = static_cast<int>(w % nseg);
+    if (b.status[c] != 0) continue;  // islanded by the small solve
+    if (c != loaded) {
+      __syncwarp();
+      copy_block(&f, b.pc + c, sizeof(PcFac), lane, 32);
+      __syncwarp();
+      loaded = c;
+    }
+    const int j0 = sg * kPrepSeg, j1 = min(per, j0 + kPrepSeg);
+    prep_segment_dispatch<RLO, RHI>(g, b, b.rank[c], c, b.slot[c], j0, j1, f);
   }
 }
 
@@ -884,6 +1165,16 @@ int launch_analyze(const DevGrid& g, Batch& b, int n_a, int n_d, cudaStream_t st
 }
 
 int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch& s, cudaStream_t stream) {
+  // split form (branch-space columns; single-profile batches: the timestep
+  // screening keeps k_prep, which also writes its bounds and factors)
+  static const bool split_off = std::getenv("TGB_NO_SPLIT_PREP") != nullptr;  // A/B switch
+  if (g.PhiA && !b.feat_mt && !b.amx_mt && !b.topo_sol && !split_off) {
+    if (b.n == 0) return 0;
+    k_prep_solve<<<b.n < 65535 ? b.n : 65535, 32, 0, stream>>>(g, b);
+    k_prep_rows<0, 4><<<148 * 8, 256, 0, stream>>>(g, b);
+    k_prep_rows<5, kSweepRank><<<148 * 8, 256, 0, stream>>>(g, b);
+    return 3;
+  }
   const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
   if (bits_bytes > 48 * 1024)  // (per launch: the size depends on the grid)
     cudaFuncSetAttribute(k_prep, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bits_bytes));

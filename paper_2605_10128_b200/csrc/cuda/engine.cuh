@@ -59,6 +59,17 @@ struct Scores {
   int* isl_bus;     // islanded busbar outages
 };
 
+// Compact small-solve factors of one candidate for the split prep
+// (k_prep_solve -> k_prep_rows; ranks <= kSweepRank, branch-space columns).
+struct alignas(16) PcFac {
+  double Sinv[kMaxSplits * kMaxSplits];  // ns x ns (ld kMaxSplits)
+  double Y[kMaxSplits * kSweepRank];     // S^-1 Phi, ns x nv (ld kSweepRank)
+  double Cinv[kSweepRank * kSweepRank];  // nv x nv (ld kSweepRank)
+  double Rp[kMaxSplits + kSweepRank];    // [S^-1 phi_p ; -C^-1 rho_p]
+  const double* base[kSweepRank];        // branch-space column sources (topo.cuh column_sources)
+  int ns, nv;
+};
+
 // Device buffers of one evaluation batch (capacity fixed at allocation).
 struct Batch {
   int n;                      // candidates in this launch
@@ -93,6 +104,7 @@ struct Batch {
   unsigned long long* fbus;   // [n][E] max |f| over busbar outages
   double* energy;             // [n][Kall] outage energy per contingency
   int* nc0;                   // [n] lambda_c0 of the candidate flows (k_prep)
+  PcFac* pc;                  // [n] split-prep factors (k_prep_solve)
   // Multi-timestep screening (capi.cu, n_t > 1 profiles): k_prep (profile 0)
   // and k_prep_mt (the others) fold every profile's candidate flows and flow
   // factors into bounds over all profiles; k_sweep in mask mode (t_mode 1) marks the rows

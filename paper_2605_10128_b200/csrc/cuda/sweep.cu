@@ -1077,40 +1077,41 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
   if (lane == 0)
     for (int j = 0; j < NST && j < nlist; ++j) issue(j);
 
-  auto exact_row = [&](int e, double lim, const double (&f1)[kKpl]) {
-    bool skip_row = false;
-#pragma unroll
-    for (int q = 0; q < kMaxRemovedSweep; ++q) skip_row |= e == rem[q];
-    unsigned long long m = 0ull;
-#pragma unroll
-    for (int k = 0; k < kKpl; ++k) {
-      if (!kval[k] || skip_row || e == kbr[k]) continue;
-      const double a = fabs(f1[k]);
-      if (a > lim) {
-        energy[k] += a - lim;
-        m = max(m, static_cast<unsigned long long>(__double_as_longlong(a)));
-      }
-    }
-    if (m > static_cast<unsigned long long>(__double_as_longlong(lim))) atomicMax(b.fmax + static_cast<size_t>(cid) * g.E + e, m);
-  };
-  auto finish_row = [&](int e, double lim, const double* fr, double (&f1)[kKpl]) {
+  // exact path of a hot row: the full f1 of the lane's contingencies (same
+  // FMA order as sweep_cta's stages 2-3, so bit-identical values), energies
+  // per contingency in registers, the row's max over overloaded elements as
+  // one warp reduction and one atomicMax. Stage 1 passes rows that are
+  // overloaded for ~93 % (cfg4), so the per-row first-FMA and all-FMA
+  // prefilters of sweep_cta are not repeated here.
+  auto exact_row = [&](int e, double lim, const double* fr, const double (&tv)[kKpl]) {
     double fl[R > 0 ? R : 1];
 #pragma unroll
     for (int q = 0; q < R; ++q) fl[q] = fr[1 + q];
-    uint32_t mx = 0u;
+    const double fc = fr[0];
+    double mx = 0.0;
 #pragma unroll
     for (int k = 0; k < kKpl; ++k) {
-      double acc = f1[k];
+      double acc = fma(tv[k], alpha[k], fc);
 #pragma unroll
       for (int q = 0; q < R; ++q) acc = fma(fl[q], rr[k][q], acc);
-      f1[k] = acc;
-      mx = max(mx, hi_abs(acc));
+      const double a = fabs(acc);
+      if (a > lim && kval[k] && e != kbr[k]) {
+        energy[k] += a - lim;
+        mx = fmax(mx, a);
+      }
     }
-    if (__any_sync(0xffffffffu, mx >= hi_abs(lim))) {
-      exact_row(e, lim, f1);
-      return true;
+    // warp max of non-negative doubles on their bit patterns (hi word, then lo)
+    const unsigned long long bits = dbits(mx);
+    const unsigned hi = static_cast<unsigned>(bits >> 32);
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    if (mhi == 0u) return false;  // no overloaded element (an overload is > lim > 0)
+    const unsigned sel = __ballot_sync(0xffffffffu, hi == mhi);
+    if (hi == mhi) {
+      const unsigned mlo = __reduce_max_sync(sel, static_cast<unsigned>(bits));
+      if (lane == __ffs(sel) - 1)
+        atomicMax(b.fmax + static_cast<size_t>(cid) * g.E + e, (static_cast<unsigned long long>(mhi) << 32) | mlo);
     }
-    return false;
+    return true;
   };
 
   for (int j = 0; j < nlist; ++j) {
@@ -1123,10 +1124,13 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
     const double* sF = reinterpret_cast<const double*>(sb);
     const double* sL = reinterpret_cast<const double*>(sb + Rg::F);
     const float* sM = reinterpret_cast<const float*>(sb + Rg::F + Rg::L);
-    // stage 1 (sweep_cta, same arithmetic): one lane per row
+    // stage 1 (sweep_cta, same arithmetic): one lane per row; rows removed by
+    // the genome carry no flow and are never scored
     bool hot = false;
-    uint32_t thr_lane = 0u;
     if (lane < rows) {
+      bool removed = false;
+#pragma unroll
+      for (int q = 0; q < kMaxRemovedSweep; ++q) removed |= e0 + lane == rem[q];
       const double lim = sL[lane] * (1.0 - 1e-12);
       const float4* rec = reinterpret_cast<const float4*>(sM) + lane * (kRec / 4);
       const double2* fr = reinterpret_cast<const double2*>(sF + lane * S);
@@ -1154,17 +1158,16 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
                                fmaxf(__fmul_ru(t4.z, a4.z), __fmul_ru(t4.w, a4.w))));
       }
       const double2 d0 = reinterpret_cast<const double2*>(rec)[kTmaxSub / 4];
-      const double thr = lim - lrb;
-      thr_lane = thr > 0.0 ? hi_abs(thr) : 0u;
       const double gap = lim - fmax(fc + d0.x, -(flo + d0.y));
       const double s0 = 1e-12 * (fmax(fabs(fc), fabs(flo)) + fabs(d0.x) + fabs(d0.y));
       const double wd = static_cast<double>(taf) + lrb;
-      hot = fma(wd, 1.0 + 1e-12, s0) >= gap;
+      hot = !removed && fma(wd, 1.0 + 1e-12, s0) >= gap;
     }
     unsigned need = __ballot_sync(0xffffffffu, hot);
     stats[3] += __popc(need);
-    // stage 2 / 3 (sweep_cta)
-    constexpr int NB = R >= 6 ? 1 : (R >= 4 ? 2 : 4);
+    stats[0] += __popc(need);
+    // exact path, NB rows' T_base tile rows in flight
+    constexpr int NB = R >= 6 ? 2 : 4;
     const double* tk_rows = g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK + lane * kKpl;
     while (need) {
       int els[NB];
@@ -1186,19 +1189,8 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
       for (int u = 0; u < NB; ++u) {
         if (u >= nu) break;
         const int el = els[u];
-        const double fc = sF[el * S];
-        const uint32_t thr = __shfl_sync(0xffffffffu, thr_lane, el);
         const double tv[kKpl] = {t[u][0].x, t[u][0].y, t[u][1].x, t[u][1].y};
-        double f1[kKpl];
-        uint32_t m = 0u;
-#pragma unroll
-        for (int k = 0; k < kKpl; ++k) {
-          f1[k] = fma(tv[k], alpha[k], fc);
-          m = max(m, hi_abs(f1[k]));
-        }
-        if (!__any_sync(0xffffffffu, m >= thr)) continue;
-        ++stats[0];
-        stats[2] += finish_row(e0 + el, sL[el], sF + el * S, f1) ? 1u : 0u;
+        stats[2] += exact_row(e0 + el, sL[el], sF + el * S, tv) ? 1u : 0u;
       }
     }
     __syncwarp();
@@ -1258,8 +1250,6 @@ __global__ void __launch_bounds__(kCkThreads, 2) k_sweep_chunked(DevGrid g, Batc
       if (stats[i]) atomicAdd(b.rows_done + i, static_cast<unsigned long long>(stats[i]));
   }
 }
-constexpr int kCkSplit = 4;  // rank classes [0, kCkSplit] and [kCkSplit + 1, kChunkedMaxRank]
-static_assert(kChunkedMaxRank == 7, "k_sweep_chunked rank switch");
 
 // Stable per-rank lists of swept candidates; bucket r is cut into CTA groups
 // of cand_per_cta(r), and every swept candidate gets its row slot
@@ -1344,9 +1334,7 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     cudaFuncSetAttribute(k_sweep_hi<false, kTmSingle, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmMask, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, sm);
     cudaFuncSetAttribute(k_sweep_hi<false, kTmMask, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, hm);
-    cudaFuncSetAttribute(k_sweep_chunked<0, kCkSplit>, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                         static_cast<int>(kCkSmemBytes));
-    cudaFuncSetAttribute(k_sweep_chunked<kCkSplit + 1, kChunkedMaxRank>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    cudaFuncSetAttribute(k_sweep_chunked<0, kChunkedMaxRank>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                          static_cast<int>(kCkSmemBytes));
   }
   // group slots: every bucket rounds up to whole groups of kWarps candidates
@@ -1375,11 +1363,10 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
       k_sweep_hi<false, kTmMask, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
     }
   } else if (chunked) {
-    cudaMemsetAsync(b.item_ctr, 0, 2 * sizeof(unsigned int), stream);
-    k_sweep_chunked<0, kCkSplit><<<148 * 2, kCkThreads, kCkSmemBytes, stream>>>(g, b, ntiles, b.item_ctr);
-    k_sweep_chunked<kCkSplit + 1, kChunkedMaxRank><<<148 * 2, kCkThreads, kCkSmemBytes, stream>>>(g, b, ntiles,
-                                                                                                  b.item_ctr + 1);
-    *launched += 1;  // three sweep kernels on this path
+    // ranks 0..7 in one persistent kernel (one work list, no tail between
+    // rank classes; every rank variant fits the same 128 registers)
+    cudaMemsetAsync(b.item_ctr, 0, sizeof(unsigned int), stream);
+    k_sweep_chunked<0, kChunkedMaxRank><<<148 * 2, kCkThreads, kCkSmemBytes, stream>>>(g, b, ntiles, b.item_ctr);
     k_sweep_hi<false, kTmSingle, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
   } else if (half) {
     k_sweep<false, kTmSingle, true><<<grid * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);

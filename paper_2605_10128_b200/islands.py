@@ -221,6 +221,68 @@ class BatchShard:
                 s.generation_end()
 
 
+class NativeIslands:
+    """The same two exchanges through the engine's own NCCL communicator
+    (tg_islands_*, host/islands.cpp): ncclAllGather on the context stream
+    between the pack / merge (island mode) or score pack / unpack (shard mode)
+    kernels; no torch on the data path. torch.distributed only carries the
+    128-byte NCCL unique id from rank 0 to the others (any backend)."""
+
+    def __init__(self, session, group=None):
+        import ctypes as C
+
+        import numpy as np
+        import torch
+        import torch.distributed as dist
+
+        from . import api
+
+        self.session = session
+        self.world = dist.get_world_size(group) if dist.is_initialized() else 1
+        self.rank = dist.get_rank(group) if dist.is_initialized() else 0
+        uid = np.zeros(128, np.uint8)
+        if self.rank == 0:
+            api._check(api.LIB.tg_islands_unique_id(uid.ctypes.data_as(C.c_void_p)))
+        if self.world > 1:
+            t = torch.from_numpy(uid)
+            if dist.get_backend(group) == "nccl":
+                t = t.cuda()
+            dist.broadcast(t, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+            uid = t.cpu().numpy().astype(np.uint8)
+        h = C.c_void_p()
+        api._check(api.LIB.tg_islands_create(session.ctx._h, uid.ctypes.data_as(C.c_void_p), self.rank, self.world,
+                                             C.byref(h)))
+        self._h = h
+        self.exchanges = 0
+
+    def exchange(self) -> None:
+        from . import api
+
+        api._check(api.LIB.tg_islands_exchange(self._h))
+        self.exchanges += 1
+
+    def step(self, n: int = 1, merge_every: int = 1) -> None:
+        """n island generations, an exchange after every merge_every-th (0 = none)."""
+        from . import api
+
+        api._check(api.LIB.tg_islands_step(self._h, n, merge_every))
+        if merge_every:
+            self.exchanges += n // merge_every
+
+    def shard_step(self, n: int = 1) -> None:
+        """n batch-sharded generations of one population (BatchShard semantics)."""
+        from . import api
+
+        api._check(api.LIB.tg_islands_shard_step(self._h, n, self.session.cfg.batch_size))
+
+    def __del__(self):
+        from . import api
+
+        if getattr(self, "_h", None):
+            api.LIB.tg_islands_destroy(self._h)
+            self._h = None
+
+
 def run_islands(session, generations: int, merge_every: int = 1, exchange: Optional[IslandExchange] = None) -> None:
     """`generations` MapElites generations of this island with an archive
     merge every `merge_every` generations (0 = never)."""
