@@ -1018,6 +1018,15 @@ void context_build(tg_context* ctx, const tg_grid_desc* gd, const tg_actionset_d
     g.inj_net = A.upload(std::vector<double>(gd->injection_net_mw, gd->injection_net_mw + I), s);
     g.ks_cont = A.upload(ks_cont, s);
     g.ks_branch = A.upload(ks_br, s);
+    {
+      // rows that are the outaged branch of some contingency of a sweep tile
+      // (the chunked sweep's exact path checks its diagonal only there)
+      const int tk = tgb::sweep_tile_k(), nt = std::max(g.Kpad / tk, 1), nw = (E + 31) / 32;
+      std::vector<uint32_t> diag(static_cast<size_t>(nt) * nw, 0u);
+      for (int k = 0; k < static_cast<int>(ks_br.size()); ++k)
+        diag[static_cast<size_t>(k / tk) * nw + ks_br[k] / 32] |= 1u << (ks_br[k] % 32);
+      g.diag_bits = A.upload(diag, s);
+    }
     g.kx_cont = A.upload(kx_cont, s);
     g.kx_br_ptr = A.upload(kx_bptr, s);
     g.kx_br = A.upload(kx_b, s);

@@ -61,6 +61,8 @@ struct DevGrid {
                            // chunk's rows of each sub-tile maximum of Tmax (floats), then the chunk's base N-1
                            // headroom min_e (lim_e - max(f0_e + D0max, -(f0_e + D0min))) minus a rounding slack
                            // (double); the chunk-level skip bound of the scores-only sweep (sweep.cu)
+  const uint32_t* diag_bits;  // [Kpad/128][ceil(E/32)] bit e%32 of word e/32: row e is the outaged branch of a
+                              // contingency of the tile (the only rows with a diagonal element to exclude)
   const int* kx_cont;      // [Kx]
   const int* kx_br_ptr;    // [Kx+1]
   const int* kx_br;

@@ -89,6 +89,12 @@ __global__ void k_branch_base(DevGrid g, const double* theta, double* f0, double
 
 // T_base[e, k] = b_e a_e^T X a_beta(k), stored in sweep tiles [k / W][e][k % W]
 // (W = sweep_tile_k()) so one pipeline stage of the sweep is one contiguous block.
+// The diagonal (e = beta(k), the outaged branch itself) is stored as 0: its
+// element is never scored (dc_engine.cpp:328-343 removes the branch; every
+// sweep excludes e == beta(k)), and its LODF value f_c / (1 - T_ee) would
+// otherwise dominate the skip records of row e in its own tile (at cfg4 it
+// made ~90 % of the blocks that passed the bounds). The true diagonal stays in
+// Tdiag for alpha.
 __global__ void k_tk(DevGrid g, double* tk, int W) {
   const size_t total = static_cast<size_t>(g.E) * g.Kpad;
   for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
@@ -97,7 +103,7 @@ __global__ void k_tk(DevGrid g, double* tk, int W) {
     const size_t rest = idx / W;
     const int e = static_cast<int>(rest % g.E), k = static_cast<int>(rest / g.E) * W + kk;
     double v = 0.0;
-    if (k < g.Ks && g.br_on[e]) {
+    if (k < g.Ks && g.br_on[e] && g.ks_branch[k] != e) {
       const int beta = g.ks_branch[k];
       const int fk = g.red[g.br_from[beta]], tk2 = g.red[g.br_to[beta]];
       const int ri = g.red[g.br_from[e]], rj = g.red[g.br_to[e]];

@@ -960,6 +960,14 @@ struct CkRing {
 };
 constexpr size_t kCkSmemBytes = kCkWarps * kCkWarpBytes;
 
+// acc += d when d > 0 (a predicated add: the conditional add of the exact
+// path without a select)
+__device__ __forceinline__ void add_if_positive(double& acc, double d) {
+  asm("{\n\t.reg .pred p;\n\tsetp.gt.f64 p, %1, 0d0000000000000000;\n\t@p add.rn.f64 %0, %0, %1;\n\t}"
+      : "+d"(acc)
+      : "d"(d));
+}
+
 template <int R>
 __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int cid, int tile, uint8_t* ws,
                                         uint32_t& phase, unsigned (&stats)[6]) {
@@ -1114,6 +1122,40 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
     return true;
   };
 
+  // fast form of exact_row when every contingency of the warp is valid and
+  // row e is not the outaged branch of any of them (no per-element validity
+  // tests): energies by a predicated add of a - lim > 0 (the same additions),
+  // the row maximum over all elements (it is the maximum over the overloaded
+  // ones whenever one exists, and then the only one stored)
+  auto exact_row_fast = [&](int e, double lim, const double* fr, const double (&tv)[kKpl]) {
+    double fl[R > 0 ? R : 1];
+#pragma unroll
+    for (int q = 0; q < R; ++q) fl[q] = fr[1 + q];
+    const double fc = fr[0];
+    double ma = 0.0;
+#pragma unroll
+    for (int k = 0; k < kKpl; ++k) {
+      double acc = fma(tv[k], alpha[k], fc);
+#pragma unroll
+      for (int q = 0; q < R; ++q) acc = fma(fl[q], rr[k][q], acc);
+      const double a = fabs(acc);
+      add_if_positive(energy[k], a - lim);
+      ma = a > ma ? a : ma;
+    }
+    const unsigned long long bits = dbits(ma);
+    const unsigned hi = static_cast<unsigned>(bits >> 32);
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned sel = __ballot_sync(0xffffffffu, hi == mhi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? static_cast<unsigned>(bits) : 0u);
+    const unsigned long long m = (static_cast<unsigned long long>(mhi) << 32) | mlo;
+    if (m <= dbits(lim)) return false;  // no overloaded element
+    if (lane == __ffs(sel) - 1) atomicMax(b.fmax + static_cast<size_t>(cid) * g.E + e, m);
+    return true;
+  };
+  const bool all_valid = __all_sync(0xffffffffu, kval[0] && kval[1] && kval[2] && kval[3]);
+  static_assert(kKpl == 4, "all_valid covers four contingencies per lane");
+  const uint32_t* diag_tile = g.diag_bits + static_cast<size_t>(tile) * nch;
+
   for (int j = 0; j < nlist; ++j) {
     const int st = j % NST;
     const uint8_t* sb = ring + static_cast<size_t>(st) * Rg::stage;
@@ -1167,6 +1209,7 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
     stats[3] += __popc(need);
     stats[0] += __popc(need);
     // exact path, NB rows' T_base tile rows in flight
+    const uint32_t dword = need ? __ldg(diag_tile + list[j]) : 0u;
     constexpr int NB = R >= 6 ? 2 : 4;
     const double* tk_rows = g.TK + (static_cast<size_t>(tile) * g.E + e0) * kTileK + lane * kKpl;
     while (need) {
@@ -1190,7 +1233,9 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
         if (u >= nu) break;
         const int el = els[u];
         const double tv[kKpl] = {t[u][0].x, t[u][0].y, t[u][1].x, t[u][1].y};
-        stats[2] += exact_row(e0 + el, sL[el], sF + el * S, tv) ? 1u : 0u;
+        const bool ok = all_valid && !((dword >> el) & 1u);
+        stats[2] += (ok ? exact_row_fast(e0 + el, sL[el], sF + el * S, tv)
+                        : exact_row(e0 + el, sL[el], sF + el * S, tv)) ? 1u : 0u;
       }
     }
     __syncwarp();
