@@ -183,6 +183,11 @@ tg_status tg_grid_to_json(const tg_grid* grid, char** text_out);
 /* grid_content_hash, grid_model.cpp:494-503: FNV-1a of the canonical dump, the
  * key of the action cache (importer.cpp:407-479) */
 tg_status tg_grid_content_hash(const tg_grid* grid, uint64_t* hash);
+/* build_ptdf, importer.cpp:358-401 (PTDFMatrix::sensitivities): computed on
+ * `device` from the device inverse of B_red; out [n_branches][n_nodes]
+ * row-major, slack column and out-of-service rows zero. SingularSystem on a
+ * disconnected grid. */
+tg_status tg_build_ptdf(const tg_grid* grid, int device, double* out);
 /* fills a desc whose arrays point into the grid object (valid while it lives) */
 tg_status tg_grid_describe(const tg_grid* grid, tg_grid_desc* out);
 /* build_action_set, importer.hpp:80 (EnumerationConfig seed/cap, importer.hpp:68-71) */

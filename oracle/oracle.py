@@ -88,6 +88,7 @@ def lib() -> C.CDLL:
         L.oc_action_cache.restype = vp
         L.oc_action_cache_load.argtypes = [vp, C.c_char_p]
         L.oc_action_cache_load.restype = C.c_int64
+        L.oc_build_ptdf.argtypes = [vp, f64p]
         _lib = L
     return _lib
 
@@ -128,6 +129,14 @@ class OracleContext:
     def grid_json(self) -> str:
         """grid_to_json_text (grid_model.cpp:423-485)."""
         return _take_string(lib().oc_grid_json(self.h))
+
+    def build_ptdf(self) -> np.ndarray:
+        """build_ptdf (importer.cpp:358-401): [E, N]."""
+        E, N = self.info["n_branches"], self.info["n_nodes"]
+        out = np.zeros((E, N))
+        if lib().oc_build_ptdf(self.h, _p(out, C.c_double)) != 0:
+            raise RuntimeError(lib().oc_last_error().decode())
+        return out
 
     def grid_hash(self) -> int:
         """grid_content_hash (grid_model.cpp:494-503)."""

@@ -127,6 +127,15 @@ void oc_context_destroy(void* h) { delete static_cast<Ctx*>(h); }
 // action cache text (importer.cpp:407-430) of the context's grid / action set
 char* oc_grid_json(void* h) { return dup_str(grid_to_json_text(static_cast<Ctx*>(h)->grid)); }
 uint64_t oc_grid_hash(void* h) { return grid_content_hash(static_cast<Ctx*>(h)->grid); }
+// build_ptdf (importer.cpp:358-401) of the context's grid: out [E][N] row-major
+int oc_build_ptdf(void* h, double* out) {
+  return guarded([&] {
+    const PTDFMatrix p = build_ptdf(static_cast<Ctx*>(h)->grid);
+    const int E = p.sensitivities.rows, N = p.sensitivities.cols;
+    for (int e = 0; e < E; ++e)
+      for (int v = 0; v < N; ++v) out[static_cast<size_t>(e) * N + v] = p.sensitivities(e, v);
+  });
+}
 char* oc_action_cache(void* h) {
   auto* c = static_cast<Ctx*>(h);
   return dup_str(action_set_to_json_text(c->actions, c->grid));

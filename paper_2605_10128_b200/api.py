@@ -185,6 +185,14 @@ def build_action_set(grid: GridModel, seed: int = 0, cap: int = 1 << 23) -> Acti
     return ActionSet(h, grid)
 
 
+def build_ptdf(grid: GridModel, device: int = 0) -> np.ndarray:
+    """build_ptdf (importer.cpp:358-401): PTDFMatrix::sensitivities [E, N]
+    computed on the GPU (slack column and out-of-service rows zero)."""
+    out = np.zeros((grid.n_branches, grid.n_nodes))
+    _check(LIB.tg_build_ptdf(grid._h, device, _ptr(out, C.c_double)))
+    return out
+
+
 def save_action_set(actions: ActionSet, grid: GridModel, path: str) -> None:
     try:
         with open(path, "w", encoding="utf-8") as f:

@@ -664,6 +664,44 @@ tg_status tg_grid_to_json(const tg_grid* grid, char** text_out) {
   });
 }
 
+tg_status tg_build_ptdf(const tg_grid* grid, int device, double* out) {
+  return guarded([&] {
+    const tgb::Grid& g = grid->g;
+    const int N = g.n_nodes(), E = g.n_branches(), Nr = N - 1;
+    check(cudaSetDevice(device), "cudaSetDevice");
+    cudaStream_t s = nullptr;
+    check(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+    DeviceArena A;
+    std::vector<int> red(N, -1);
+    for (int v = 0, r = 0; v < N; ++v)
+      if (v != g.slack) red[v] = r++;
+    std::vector<double> b(E), bred(static_cast<size_t>(Nr) * Nr, 0.0);
+    for (int e = 0; e < E; ++e) {
+      b[e] = 1.0 / g.br_x[e];
+      if (!g.br_on[e]) continue;
+      const int i = red[g.br_from[e]], j = red[g.br_to[e]];
+      if (i >= 0) bred[static_cast<size_t>(i) * Nr + i] += b[e];
+      if (j >= 0) bred[static_cast<size_t>(j) * Nr + j] += b[e];
+      if (i >= 0 && j >= 0) bred[static_cast<size_t>(i) * Nr + j] -= b[e], bred[static_cast<size_t>(j) * Nr + i] -= b[e];
+    }
+    double* X = A.upload(bred, s);
+    const bool ok = tgb::device_spd_inverse(X, Nr, s);
+    if (!ok) {
+      cudaStreamDestroy(s);
+      throw tgb::SingularSystem("susceptance matrix is singular; the grid is disconnected");
+    }
+    std::vector<uint8_t> on(g.br_on.begin(), g.br_on.end());
+    double* d_out = A.alloc<double>(static_cast<size_t>(E) * N);
+    tgb::launch_ptdf(N, E, Nr, A.upload(red, s), A.upload(std::vector<int>(g.br_from.begin(), g.br_from.end()), s),
+                     A.upload(std::vector<int>(g.br_to.begin(), g.br_to.end()), s), A.upload(b, s), A.upload(on, s), X,
+                     d_out, s);
+    check(cudaGetLastError(), "ptdf");
+    check(cudaMemcpyAsync(out, d_out, static_cast<size_t>(E) * N * sizeof(double), cudaMemcpyDeviceToHost, s), "D2H");
+    check(cudaStreamSynchronize(s), "ptdf");
+    cudaStreamDestroy(s);
+  });
+}
+
 tg_status tg_grid_content_hash(const tg_grid* grid, uint64_t* hash) {
   return guarded([&] { *hash = tgb::grid_content_hash(grid->g); });
 }

@@ -199,6 +199,9 @@ inline int max_sweep_groups(int n) { return (n + kGroupSlots - 1) / kGroupSlots 
 // X = B_red^-1 by in-place Gauss-Jordan (B_red is SPD; no pivoting needed).
 // Returns false when a pivot is not positive (disconnected grid).
 bool device_spd_inverse(double* a, int n, cudaStream_t stream);
+// build_ptdf (importer.cpp:358-401) from X = B_red^-1: out [E][N], slack column 0.
+void launch_ptdf(int N, int E, int Nr, const int* red, const int* from, const int* to, const double* b,
+                 const uint8_t* on, const double* X, double* out, cudaStream_t stream);
 // Skip records of n_t profiles (contiguous, rec_floats each) combined into
 // bounds over all profiles (multi-timestep screening).
 void launch_rec_combine(const float* recs, size_t rec_floats, int n_t, float* out, cudaStream_t stream);

@@ -308,6 +308,34 @@ void launch_rec_combine(const float* recs, size_t rec_floats, int n_t, float* ou
   k_rec_combine<<<1024, 256, 0, stream>>>(recs, rec_floats, n_t, out);
 }
 
+// PTDF of importer.cpp:358-401: row e = b_e (X[red(from_e), :] - X[red(to_e), :])
+// over the full node index (slack column zero), 0 rows for out-of-service
+// branches; out is [E][N] row-major.
+__global__ void k_ptdf(int N, int E, int Nr, const int* red, const int* from, const int* to, const double* b,
+                       const uint8_t* on, const double* X, double* out) {
+  const size_t total = static_cast<size_t>(E) * N;
+  for (size_t idx = blockIdx.x * static_cast<size_t>(blockDim.x) + threadIdx.x; idx < total;
+       idx += static_cast<size_t>(gridDim.x) * blockDim.x) {
+    const int e = static_cast<int>(idx / N), v = static_cast<int>(idx % N);
+    const int rv = red[v], i = red[from[e]], j = red[to[e]];
+    double val = 0.0;
+    if (on[e] && rv >= 0) {
+      const double xi = i >= 0 ? X[static_cast<size_t>(rv) * Nr + i] : 0.0;  // X symmetric
+      const double xj = j >= 0 ? X[static_cast<size_t>(rv) * Nr + j] : 0.0;
+      val = b[e] * (xi - xj);
+    }
+    out[idx] = val;
+  }
+}
+
+void launch_ptdf(int N, int E, int Nr, const int* red, const int* from, const int* to, const double* b,
+                 const uint8_t* on, const double* X, double* out, cudaStream_t stream) {
+  const size_t total = static_cast<size_t>(E) * N;
+  if (total == 0) return;
+  k_ptdf<<<static_cast<int>(std::min<size_t>((total + 255) / 256, 148 * 16)), 256, 0, stream>>>(N, E, Nr, red, from, to,
+                                                                                                  b, on, X, out);
+}
+
 bool device_spd_inverse(double* a, int n, cudaStream_t stream) {
   if (n == 0) return true;
   double *row = nullptr, *col = nullptr, *dmax = nullptr;

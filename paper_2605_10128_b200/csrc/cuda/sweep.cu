@@ -1248,7 +1248,7 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
   double* en = b.energy + static_cast<size_t>(cid) * g.Kall;
 #pragma unroll
   for (int k = 0; k < kKpl; ++k)
-    if (kval[k] && kb + k < g.Ks) en[g.ks_cont[kb + k]] = energy[k];
+    if (kval[k] && kb + k < g.Ks && energy[k] != 0.0) en[g.ks_cont[kb + k]] = energy[k];  // zeroed per evaluation
 }
 
 template <int RLO, int RHI>
