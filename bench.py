@@ -331,7 +331,6 @@ def main():
     T = int(json.loads(text).get("timesteps", {}).get("count", 1))
     n_prof = 5
     isl = 0
-    alg_bytes = 0.0
     r_all = np.zeros(0, np.int64)
     for _ in range(n_prof):
         sess.step(1)
@@ -340,10 +339,6 @@ def main():
         r_all = np.concatenate([r_all, live.astype(np.int64)])
         isl += int((r < 0).sum())
         flops += float(E) * Ks * float(np.sum(2.0 * T + 2.0 * live))
-        # compulsory sweep traffic: each swept candidate's branch and contingency
-        # rows (row_stride(r) doubles each) + the skip records + T_base read once
-        stride = (live + 2) & ~1
-        alg_bytes += T * (8.0 * float(np.sum(stride)) * (E + Kp) + 8.0 * E * Kp * (1 + 10 / 128))
     sweep_ms, sweep_n = P.sweep_timing(ctx, False)
     rows_done, rows_offered, rows_overloaded, rows_partial = P.sweep_rows(ctx)
     chunk_tests, chunk_hot = P.sweep_chunks(ctx)
@@ -362,17 +357,26 @@ def main():
     per_launch = n_prof * T
     executed_flops = (rows_done * 128.0 * (2.0 + 2.0 * mean_rank) + chunk_hot * 32.0 * (2.0 + 2.0 * mean_rank)) / per_launch
     executed_tflops = executed_flops / (avg_ms * 1e-3) / 1e12 if avg_ms else 0.0
-    # compulsory HBM bytes per launch of the chunked sweep
-    stride_mean = float(np.mean((np.maximum(r_all, 0) + 2) & ~1)) if len(r_all) else 2.0
+    # SURVEY.md 8(d) compulsory bytes per sweep launch: T_base read once
+    # (8 E K), every swept candidate's per-candidate vectors in (8 (E + K)(T + r)
+    # with T = 1 per launch) and its folded outputs out (8 (E + K): fmax per
+    # branch, energy per contingency)
     n_swept = len(r_all) / n_prof
+    r_mean = float(np.mean(np.maximum(r_all, 0))) if len(r_all) else 0.0
+    alg_bytes = 8.0 * E * Ks + n_swept * 8.0 * (E + Ks) * (1.0 + r_mean) + n_swept * 8.0 * (E + Ks)
+    hbm_gbs = alg_bytes / (avg_ms * 1e-3) / 1e9 if avg_ms else 0.0
+    # bytes the chunked sweep stages through L2 / shared memory per launch
+    # (mostly L2 hits: ncu DRAM traffic is the `traffic` figure)
+    stride_mean = float(np.mean((np.maximum(r_all, 0) + 2) & ~1)) if len(r_all) else 2.0
     nch = (E + 31) // 32
-    hbm_bytes = (n_swept * (8.0 * stride_mean * Kp + nch * 32.0) + (Kp // 128) * nch * 48.0
-                 + chunk_hot / per_launch * 32.0 * (8.0 * stride_mean + 8.0 + 48.0))
-    hbm_gbs = hbm_bytes / (avg_ms * 1e-3) / 1e9 if avg_ms else 0.0
+    staged_bytes = (n_swept * (8.0 * stride_mean * Kp + nch * 32.0) + (Kp // 128) * nch * 48.0
+                    + chunk_hot / per_launch * 32.0 * (8.0 * stride_mean + 8.0 + 48.0))
     try:
         hbm_peak = float(json.load(open(os.path.join(ROOT, "MEASURED_PEAKS.json")))["hbm_gbs"])
+        hbm_src = "MEASURED_PEAKS.json hbm_gbs"
     except (OSError, ValueError, KeyError):
         hbm_peak = 7700.0
+        hbm_src = "B200_PROFILING.md fallback"
     peak = P.fp64_peak_tflops(dev)
     traffic = None
     ncu = {}
@@ -451,25 +455,30 @@ def main():
                        "archive_entries": len(snap.entries), "best_fitness": snap.best_fitness,
                        "context_setup_s": setup_s},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "fp64", "kernel": "k_sweep_chunked (fused N-1 sweep, scores-only)",
-                         "achieved": executed_tflops, "peak": peak, "unit": "TFLOP/s",
-                         "frac": executed_tflops / peak if peak else None, "traffic": traffic,
-                         "algorithmic": "FP64 flops the exact sweep must execute per launch: every (branch row, "
-                                        "128-contingency tile, candidate) block that no bound proves safe (these are "
-                                        "the overloaded blocks up to ~7 %) x 128 elements x (2 + 2r), plus the row "
-                                        "bound of every row of a hot chunk (2 + 2r); / the average launch time "
+            "roofline": {"bound": "hbm", "kernel": "k_sweep_chunked (fused N-1 sweep, scores-only)",
+                         "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
+                         "frac": hbm_gbs / hbm_peak if hbm_peak else None, "traffic": traffic,
+                         "algorithmic": "SURVEY.md 8(d) compulsory bytes per launch: 8*E*K (T_base once) + per "
+                                        "swept candidate 8*(E+K)*(1+r) in (candidate flows + low-rank factors) "
+                                        "and 8*(E+K) out (folded maxima, energies); / the average launch time "
                                         "measured live with CUDA events on the engine stream",
-                         "executed_flops_per_launch": executed_flops, "avg_launch_ms": avg_ms,
-                         "mean_rank": mean_rank, "timesteps": T,
-                         "peak_source": "DFMA microbenchmark on this GPU in this run (MEASURED_PEAKS.json has no "
-                                        "FP64 figure)",
-                         "note": "issue-bound on the compare / accumulate work around the FMAs of the overloaded "
-                                 "elements (ncu: profiles/r2/); skipped work provably cannot change a score "
-                                 "(tests/test_gpu_scale.py: bit-identical to the dense sweep)",
-                         "hbm": {"compulsory_bytes_per_launch": hbm_bytes, "achieved_gbs": hbm_gbs,
-                                 "peak_gbs": hbm_peak, "frac": hbm_gbs / hbm_peak if hbm_peak else None,
-                                 "what": "contingency rows of every swept candidate (all tiles), chunk summaries, "
-                                         "chunk records, candidate rows + limits + row records of the hot chunks"},
+                         "alg_bytes_per_launch": alg_bytes, "avg_launch_ms": avg_ms, "mean_rank": mean_rank,
+                         "timesteps": T, "peak_source": hbm_src,
+                         "traffic_source": "ncu --set full dram__bytes_read.sum + dram__bytes_write.sum of one "
+                                           "launch (profiles/sweep_ncu_summary.json)",
+                         "note": "latency / issue-bound (ncu: issue active ~42 %, warps active ~25 %): the "
+                                 "work is the chunk and row bounds plus the exact path of the few overloaded "
+                                 "blocks; skipped work provably cannot change a score (tests/test_gpu_scale.py: "
+                                 "bit-identical to the dense sweep)",
+                         "fp64_executed": {"tflops": executed_tflops, "peak": peak,
+                                           "frac": executed_tflops / peak if peak else None,
+                                           "flops_per_launch": executed_flops,
+                                           "peak_source": "DFMA microbenchmark on this GPU in this run "
+                                                          "(MEASURED_PEAKS.json has no FP64 figure)",
+                                           "what": "FP64 flops executed: every (row, 128-contingency tile) block "
+                                                   "no bound proves safe x 128 x (2 + 2r), plus the row bound "
+                                                   "(2 + 2r) of every row of a hot chunk"},
+                         "staged_bytes_per_launch": staged_bytes,
                          "dense_equivalent": {"tflops": dense_tflops, "x_fp64_peak": dense_tflops / peak if peak else None,
                                               "flops_per_launch": flops / n_prof / T,
                                               "what": "SURVEY.md 8(d) E*K_single*(2T+2r) per swept candidate / the "
@@ -478,7 +487,7 @@ def main():
                          "islanded_fraction": isl / (n_prof * B),
                          "skip": {"executed_block_fraction": computed_frac,
                                   "overloaded_block_fraction": rows_overloaded / rows_offered if rows_offered else 0.0,
-                                  "chunk_tests": chunk_tests,
+                                  "chunk_tests": chunk_tests / per_launch,
                                   "hot_chunk_fraction": chunk_hot / chunk_tests if chunk_tests else None},
                          "ncu": ncu or None},
             "e2e": {"value": e2e_value, "unit": "topologies/s", "h2d_bytes_per_step": int(h2d),

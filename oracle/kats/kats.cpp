@@ -4,8 +4,10 @@
 // block cites the reference test it re-checks (proj/tests/*.cpp). Runs as a
 // plain binary (no doctest in this image): prints one line per check group and
 // exits non-zero on any failure. Driven by tests/test_oracle_kats.py.
+#include <algorithm>
 #include <chrono>
 #include <cmath>
+#include <complex>
 #include <cstdio>
 #include <functional>
 #include <map>
@@ -1046,6 +1048,253 @@ KAT(acceptance_7_progress) {
   const double best = r.repertoire.best_fitness();
   std::printf("  criterion 7: optimum %.3f reached %.3f, drop %.0f%%\n", opt, best, 100 * drop);
   expect(best >= opt - 0.05 * std::abs(opt), "criterion 7");
+}
+
+
+// ------------------------------------------------------------ AC validation
+// test_ac_validator.cpp:15-395
+namespace {
+AppliedTopology no_split(const GridModel& g, const ActionSet& a) { return apply_genome(g, a, Genome::empty(0, 0)); }
+json two_bus_json(double x, double r, double p, double q) {
+  return {{"nodes", {{{"id", "s"}}, {{"id", "b"}}}},
+          {"branches", {{{"id", "sb"}, {"from", "s"}, {"to", "b"}, {"x_pu", x}, {"r_pu", r}, {"limit_mw", 100.0}}}},
+          {"injections", {{{"id", "l"}, {"node", "b"}, {"p_mw", p}, {"q_mvar", q}, {"kind", "load"}}}},
+          {"slack", "s"}};
+}
+int slot_of_disconnectable(const GridModel& g, const ActionSet& a, const char* id) {
+  for (int d = 0; d < static_cast<int>(a.disconnectables.size()); ++d)
+    if (g.branches[a.disconnectables[d]].id == id) return d;
+  return -1;
+}
+}  // namespace
+
+KAT(ac_flat_and_two_bus) {
+  {  // zero load: converges on the first mismatch test (test_ac_validator.cpp:31-47)
+    GridModel g = grid_from_json(two_bus_json(0.1, 0.01, 0.0, 0.0));
+    ActionSet a = build_action_set(g);
+    AcCaseResult r = ac_power_flow(g, no_split(g, a));
+    expect(r.converged && r.iterations == 1, "zero load converges in one iteration");
+    expect(*std::max_element(r.loading_mva.begin(), r.loading_mva.end()) < 1e-9, "zero flows");
+    expect(std::abs(r.vm_pu[g.node_index("b")] - 1.0) < 1e-12, "flat magnitude");
+  }
+  {  // two-bus load vs the Z-bus fixed point (49-75)
+    GridModel g = grid_from_json(two_bus_json(0.1, 0.01, 50.0, 10.0));
+    ActionSet a = build_action_set(g);
+    AcCaseResult r = ac_power_flow(g, no_split(g, a));
+    expect(r.converged, "two-bus converges");
+    std::complex<double> v1(1.0, 0.0), z(0.01, 0.1), s(0.5, 0.1), v2 = v1;
+    for (int i = 0; i < 500; ++i) v2 = v1 - z * std::conj(s / v2);
+    const int b = g.node_index("b");
+    expect(std::abs(std::polar(r.vm_pu[b], r.va_rad[b]) - v2) < 1e-6, "two-bus voltage = fixed point");
+    const std::complex<double> sf = v1 * std::conj((v1 - v2) / z) * 100.0;
+    expect(sf.real() > 50.0, "sending end covers losses");
+    expect(std::abs(r.loading_mva[0] - std::abs(sf)) <= 1e-6 * std::abs(sf), "loading = |S_from|");
+  }
+  {  // beyond transfer capacity (170-184)
+    GridModel g = grid_from_json(two_bus_json(0.5, 0.05, 400.0, 100.0));
+    ActionSet a = build_action_set(g);
+    expect(!ac_power_flow(g, no_split(g, a)).converged, "heavy load does not converge");
+  }
+}
+
+KAT(ac_grid14_published) {  // test_ac_validator.cpp:77-134
+  GridModel g = data_grid("grid14.json");
+  ActionSet a;
+  AcCaseResult r = ac_power_flow(g, no_split(g, a));
+  expect(r.converged && r.iterations <= 10, "grid14 converges within 10 iterations");
+  const std::vector<std::pair<const char*, double>> pub = {
+      {"1", 1.060}, {"2", 1.045}, {"3", 1.010}, {"4", 1.018}, {"5", 1.020}, {"6", 1.070}, {"7", 1.062},
+      {"8", 1.090}, {"9", 1.056}, {"10", 1.051}, {"11", 1.057}, {"12", 1.055}, {"13", 1.050}, {"14", 1.036}};
+  for (auto& [bus, vm] : pub) expect(std::abs(r.vm_pu[g.node_index(bus)] - vm) < 1e-3, std::string("published vm ") + bus);
+  // bus power balance against an independent Ybus (90-134)
+  const int n = static_cast<int>(g.nodes.size());
+  std::vector<std::complex<double>> V(n), S(n, 0.0);
+  for (int v = 0; v < n; ++v) V[v] = std::polar(r.vm_pu[v], r.va_rad[v]);
+  for (const Branch& br : g.branches) {
+    const std::complex<double> y = 1.0 / std::complex<double>(br.resistance, br.reactance), ysh(0.0, br.charging_b / 2);
+    const std::complex<double> i_f = (y + ysh) / (br.tap * br.tap) * V[br.from] - y / br.tap * V[br.to];
+    const std::complex<double> i_t = -y / br.tap * V[br.from] + (y + ysh) * V[br.to];
+    S[br.from] += V[br.from] * std::conj(i_f);
+    S[br.to] += V[br.to] * std::conj(i_t);
+  }
+  for (int v = 0; v < n; ++v) S[v] += V[v] * std::conj(std::complex<double>(0.0, g.nodes[v].shunt_b_pu) * V[v]);
+  for (int v = 0; v < n; ++v) {
+    if (v == g.slack) continue;
+    double p = 0, q = 0;
+    bool pv = false;
+    for (const Injection& inj : g.injections) {
+      if (inj.node != v) continue;
+      if (inj.kind == InjectionKind::Generator) {
+        p += inj.p_mw / 100.0;
+        pv = pv || inj.v_setpoint_pu.has_value();
+      } else {
+        p -= inj.p_mw / 100.0;
+        q -= inj.q_mvar / 100.0;
+      }
+    }
+    expect(std::abs(S[v].real() - p) < 1e-6, "P balance");
+    if (!pv) expect(std::abs(S[v].imag() - q) < 1e-6, "Q balance");
+  }
+}
+
+KAT(ac_islanding_contingency) {  // test_ac_validator.cpp:136-168
+  GridModel g = mini_congestion_grid();
+  ActionSet a = build_action_set(g);
+  int pick = -1;
+  for (const Action& act : a.actions) {
+    const SubstationDetail& st = g.substations[act.substation];
+    if (st.node != g.node_index("f")) continue;
+    bool load_stays = false, mf_moves = true;
+    for (int t = 0; t < static_cast<int>(st.terminals.size()); ++t) {
+      if (st.terminals[t].element == "load" && !act.group[t]) load_stays = true;
+      if ((st.terminals[t].element == "mf" || st.terminals[t].element == "mf2") && !act.group[t]) mf_moves = false;
+    }
+    if (load_stays && mf_moves) pick = act.id;
+  }
+  if (pick >= 0) {
+    Genome gen = Genome::empty(3, 2);
+    gen.action_slots[0] = pick;
+    AcNetwork net(g, apply_genome(g, a, gen));
+    expect(net.run_case(-1).converged, "split base converges");
+    int af = -1;
+    for (int k = 0; k < static_cast<int>(g.contingencies.size()); ++k)
+      if (g.contingencies[k].id == "o-af") af = k;
+    expect(af >= 0 && !net.run_case(af).converged, "stranding contingency does not converge");
+  }
+}
+
+KAT(ac_validator_congestion) {  // test_ac_validator.cpp:186-233, 235-262
+  GridModel g = mini_congestion_grid();
+  ActionSet a = build_action_set(g);
+  DcContext dc(g, a);
+  AcValidator val(g, a, dc, {});
+  expect(val.baseline_lambda_o() > 0.0, "baseline overload");
+  const int mf = slot_of_disconnectable(g, a, "mf");
+  expect(mf >= 0, "mf disconnectable");
+  Genome clear = Genome::empty(3, 2);
+  clear.disconnection_slots[0] = mf;
+  const ScoreVector cs = dc.evaluate(clear);
+  expect(std::abs(cs.fitness) < 1e-9, "clearing DC fitness 0");
+  Genome none = Genome::empty(3, 2);
+  expect(val.worst_k_check(none, dc.evaluate(none)) == RejectionReason::OverloadNotImproved, "unchanged never improves");
+  expect(val.worst_k_check(clear, cs) == RejectionReason::None, "worst-k passes clearing");
+  ValidationRecord rec = val.full_validation(clear, cs);
+  expect(rec.accepted && rec.ac_lambda_o < val.baseline_lambda_o() && rec.stage == ValidationStage::FullN1,
+         "full validation accepts clearing");
+  AcValidator hist(g, a, dc, {});
+  expect(hist.validate({clear, cs}).accepted, "validate accepts");
+  EliminationOutcome out = hist.eliminate({{clear, cs}});
+  expect(out.pruned.size() == 1 && out.pruned[0].second == RejectionReason::EliminatedSimilar && out.queue.empty(),
+         "validated genome pruned as similar");
+  for (double scale : {1.0, 0.9, 0.8}) {  // monotone in loading (235-262)
+    json j = json::parse(grid_to_json_text(mini_congestion_grid()));
+    for (json& inj : j["injections"]) {
+      if (inj["kind"] != "load") continue;
+      inj["p_mw"] = inj["p_mw"].get<double>() * scale;
+      inj["q_mvar"] = inj["q_mvar"].get<double>() * scale;
+    }
+    GridModel gs = grid_from_json(j);
+    ActionSet as = build_action_set(gs);
+    DcContext dcs(gs, as);
+    AcValidator vs(gs, as, dcs, {});
+    if (vs.baseline_lambda_o() == 0.0) continue;
+    Genome gg = Genome::empty(3, 2);
+    gg.disconnection_slots[0] = slot_of_disconnectable(gs, as, "mf");
+    ValidationRecord r = vs.full_validation(gg, dcs.evaluate(gg));
+    expect(r.reason != RejectionReason::OverloadNotImproved && r.accepted, "accepted at smaller loads");
+  }
+  const std::string line = record_to_json(rec, g, a);  // 374-395
+  json p = json::parse(line);
+  expect(p.contains("verdict") && p.contains("reason") && p.contains("ac_lambda_o") && p["stage"] == "full_n1" &&
+             p["lambda_d"] == 1,
+         "record serializes");
+}
+
+KAT(ac_critical_count_rejection) {  // test_ac_validator.cpp:264-298
+  json j = {{"nodes", {{{"id", "a"}}, {{"id", "m"}}, {{"id", "f"}}}},
+            {"branches",
+             {{{"id", "af"}, {"from", "a"}, {"to", "f"}, {"x_pu", 0.3}, {"limit_mw", 200.0}},
+              {{"id", "am"}, {"from", "a"}, {"to", "m"}, {"x_pu", 0.05}, {"limit_mw", 107.0}},
+              {{"id", "mf"}, {"from", "m"}, {"to", "f"}, {"x_pu", 0.05}, {"limit_mw", 45.0}},
+              {{"id", "mf2"}, {"from", "m"}, {"to", "f"}, {"x_pu", 0.2}, {"limit_mw", 100.0}}}},
+            {"injections",
+             {{{"id", "g"}, {"node", "a"}, {"p_mw", 100.0}, {"kind", "generator"}, {"v_setpoint_pu", 1.02}},
+              {{"id", "load"}, {"node", "f"}, {"p_mw", 100.0}, {"q_mvar", 20.0}, {"kind", "load"}}}},
+            {"contingencies", {{{"id", "o-af"}, {"branches", {"af"}}}, {{"id", "o-am"}, {"branches", {"am"}}}}},
+            {"slack", "a"}};
+  GridModel g = grid_from_json(j);
+  ActionSet a = build_action_set(g);
+  DcContext dc(g, a);
+  AcValidator val(g, a, dc, {});
+  expect(val.baseline_critical_count() == 1, "one baseline critical branch");
+  Genome gen = Genome::empty(3, 2);
+  gen.disconnection_slots[0] = slot_of_disconnectable(g, a, "mf");
+  ValidationRecord r = val.full_validation(gen, dc.evaluate(gen));
+  expect(!r.accepted && r.reason == RejectionReason::CriticalCountIncreased && r.ac_lambda_o < val.baseline_lambda_o(),
+         "criticals increased -> rejected");
+}
+
+KAT(ac_elimination) {  // test_ac_validator.cpp:300-372
+  GridModel g = mini_congestion_grid();
+  ActionSet a = build_action_set(g);
+  DcContext dc(g, a);
+  AcValidator val(g, a, dc, {});
+  const double pre = dc.pre_optimization_score().fitness;
+  expect(pre < 0.0, "congested pre fitness");
+  auto make = [&](double fit, int d, int s, int r) {
+    Candidate c;
+    c.genome = Genome::empty(3, 2);
+    c.genome.disconnection_slots[0] = d % 2;
+    c.dc_score.fitness = fit;
+    c.dc_score.lambda_d = d;
+    c.dc_score.lambda_s = s;
+    c.dc_score.lambda_r = r;
+    return c;
+  };
+  {
+    Candidate simple = make(-10.0, 1, 0, 0), twin = make(-10.0, 1, 1, 3);
+    twin.genome.disconnection_slots[0] = 1;
+    EliminationOutcome o = val.eliminate({simple, twin});
+    expect(o.pruned.size() == 1 && o.pruned[0].first == 1 && o.pruned[0].second == RejectionReason::EliminatedDominated &&
+               o.queue.size() == 1 && o.queue[0] == 0,
+           "dominated pruned");
+  }
+  {
+    EliminationOutcome o = val.eliminate({make(pre + 0.01 * std::abs(pre), 1, 0, 0)});
+    expect(o.pruned.size() == 1 && o.pruned[0].second == RejectionReason::EliminatedBelowThreshold, "below threshold");
+  }
+  {
+    Candidate good = make(-5.0, 1, 0, 0), better = make(-1.0, 1, 0, 0);
+    better.genome.disconnection_slots[0] = 1;
+    EliminationOutcome o = val.eliminate({good, better});
+    expect(o.queue.size() == 2 && o.queue[0] == 1 && o.queue[1] == 0, "queue by DC fitness");
+  }
+  {
+    std::mt19937_64 rng(42);
+    std::uniform_real_distribution<double> uf(pre, 0.0);
+    std::uniform_int_distribution<int> ui(0, 3);
+    std::vector<Candidate> pool;
+    for (int i = 0; i < 60; ++i) {
+      Candidate c;
+      c.genome = random_genome(a, 3, 2, rng);
+      c.dc_score.fitness = uf(rng);
+      c.dc_score.lambda_d = c.genome.disconnection_count();
+      c.dc_score.lambda_s = c.genome.split_count();
+      c.dc_score.lambda_r = ui(rng);
+      pool.push_back(c);
+    }
+    EliminationOutcome o = val.eliminate(pool);
+    const double eps = val.config().dominance_fitness_frac * std::abs(pre);
+    const double theta = val.config().improvement_threshold_frac * std::abs(pre);
+    auto swd = [](const ScoreVector& s) { return s.lambda_d + s.lambda_s + s.lambda_r; };
+    bool ok = o.queue.size() + o.pruned.size() == pool.size();
+    for (int i : o.queue) {
+      ok = ok && pool[i].dc_score.fitness - pre >= theta;
+      for (const Candidate& other : pool)
+        ok = ok && !(swd(other.dc_score) < swd(pool[i].dc_score) && other.dc_score.fitness >= pool[i].dc_score.fitness - eps);
+    }
+    expect(ok, "survivors fail every pruning predicate");
+  }
 }
 
 }  // namespace

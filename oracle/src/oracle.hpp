@@ -403,3 +403,105 @@ OptimizerResult run_optimizer(const DcContext& ctx, const QdConfig& cfg, const S
                               const std::atomic<bool>* stop = nullptr, const IterationTrace* trace = nullptr);
 
 }  // namespace oracle
+
+// ---- ac_validator.hpp:18-140 (restated in ac.cpp) ----------------------------
+namespace oracle {
+
+struct AcConfig {
+  double tolerance_pu = 1e-6;
+  int max_iterations = 30;
+  int worst_k_nonconverged = 2;
+  double nonconverged_fraction = 0.05;
+  int similarity_distance = 1;
+  double dominance_fitness_frac = 0.01;
+  double improvement_threshold_frac = 0.05;
+};
+
+struct AcCaseResult {
+  bool converged = false;
+  int iterations = 0;
+  Vec loading_mva;  // per branch, MVA (max of both ends); zero unless converged
+  Vec vm_pu, va_rad;  // per bus (base nodes, then split sections)
+};
+
+class AcNetwork {
+ public:
+  AcNetwork(const GridModel& grid, const AppliedTopology& topology, AcConfig config = {});
+  AcCaseResult run_case(int contingency) const;  // -1 = base case
+  double overload_energy(const AcCaseResult& r) const;
+  int critical_count(const AcCaseResult& r) const;
+
+ private:
+  const GridModel* grid_;
+  AppliedTopology topo_;
+  AcConfig cfg_;
+  int n_buses_ = 0;
+  AcCaseResult solve(const std::vector<char>& branch_out, const std::vector<char>& injection_out) const;
+};
+
+AcCaseResult ac_power_flow(const GridModel& grid, const AppliedTopology& topology, AcConfig config = {});
+
+enum class RejectionReason {
+  None, Nonconvergence, OverloadNotImproved, CriticalCountIncreased,
+  EliminatedSimilar, EliminatedDominated, EliminatedBelowThreshold,
+};
+std::string to_string(RejectionReason reason);
+enum class ValidationStage { None, WorstK, FullN1 };
+
+struct ValidationRecord {
+  Genome genome;
+  ScoreVector dc_score;
+  ValidationStage stage = ValidationStage::None;
+  bool accepted = false;
+  RejectionReason reason = RejectionReason::None;
+  double ac_lambda_o = 0.0;
+};
+struct Candidate {
+  Genome genome;
+  ScoreVector dc_score;
+};
+struct EliminationOutcome {
+  std::vector<int> queue;
+  std::vector<std::pair<int, RejectionReason>> pruned;
+};
+
+class AcValidator {
+ public:
+  AcValidator(const GridModel& grid, const ActionSet& actions, const DcContext& dc, AcConfig config = {});
+  const AcConfig& config() const { return cfg_; }
+  double baseline_lambda_o() const { return base_lambda_o_; }
+  int baseline_critical_count() const { return base_critical_; }
+  bool baseline_base_converged() const { return base_converged_; }
+  double baseline_base_energy() const { return base_energy_; }
+  const std::vector<char>& baseline_case_converged() const { return case_converged_; }
+  const std::vector<double>& baseline_case_energy() const { return case_energy_; }
+  EliminationOutcome eliminate(const std::vector<Candidate>& candidates) const;
+  RejectionReason worst_k_check(const Genome& genome, const ScoreVector& dc_score) const;
+  ValidationRecord full_validation(const Genome& genome, const ScoreVector& dc_score) const;
+  ValidationRecord validate(const Candidate& candidate);
+  void record_elimination(const Candidate& candidate, RejectionReason reason);
+  const std::vector<ValidationRecord>& records() const { return records_; }
+
+ private:
+  const GridModel* grid_;
+  const ActionSet* actions_;
+  AcConfig cfg_;
+  double pre_fitness_ = 0.0;
+  double base_lambda_o_ = 0.0;
+  int base_critical_ = 0;
+  bool base_converged_ = false;
+  double base_energy_ = 0.0;
+  std::vector<char> case_converged_;
+  std::vector<double> case_energy_;
+  struct Validated {
+    Genome genome;
+    int swd = 0;
+    double fitness = 0.0;
+  };
+  std::vector<Validated> validated_;
+  std::vector<ValidationRecord> records_;
+};
+
+std::string record_to_json(const ValidationRecord& record, const GridModel& grid, const ActionSet& actions);
+
+}  // namespace oracle
