@@ -344,6 +344,81 @@ tg_status tg_fp64_peak(int device, double* tflops);
 tg_status tg_context_info(tg_context* ctx, int64_t* values, int32_t n_values); /* see capi.cu */
 int64_t tg_kernel_launches(tg_context* ctx);  /* engine kernels launched so far */
 
+/* ---- AC validation: batched Newton-Raphson on the device.
+ * Replaces AcNetwork / AcValidator (ac_validator.hpp:18-140, ac_validator.cpp:26-495):
+ * every (genome, contingency) case is one CTA running the reference's polar
+ * Newton-Raphson from a flat start (dense Jacobian, LU with partial pivoting),
+ * in shared memory for small networks, in a per-CTA HBM scratch slot otherwise. */
+typedef struct tg_ac_context tg_ac_context;
+
+/* AcConfig, ac_validator.hpp:18-26 */
+typedef struct tg_ac_config {
+  double tolerance_pu;               /* 1e-6 */
+  int32_t max_iterations;            /* 30 */
+  int32_t worst_k_nonconverged;      /* q = 2 */
+  double nonconverged_fraction;      /* 0.05 */
+  int32_t similarity_distance;       /* 1   (host-side eliminate) */
+  double dominance_fitness_frac;     /* 0.01 (host-side eliminate) */
+  double improvement_threshold_frac; /* 0.05 (host-side eliminate) */
+} tg_ac_config;
+
+/* RejectionReason, ac_validator.hpp:63-71 */
+typedef enum tg_ac_reason {
+  TG_AC_NONE = 0,
+  TG_AC_NONCONVERGENCE = 1,
+  TG_AC_OVERLOAD_NOT_IMPROVED = 2,
+  TG_AC_CRITICAL_COUNT_INCREASED = 3,
+  TG_AC_ELIMINATED_SIMILAR = 4,
+  TG_AC_ELIMINATED_DOMINATED = 5,
+  TG_AC_ELIMINATED_BELOW_THRESHOLD = 6
+} tg_ac_reason;
+
+/* Baseline metrics of the unchanged grid (AcValidator::AcValidator, ac_validator.cpp:313-343). */
+typedef struct tg_ac_baseline {
+  double lambda_o;          /* baseline_lambda_o() */
+  int32_t critical_count;   /* baseline_critical_count() */
+  uint8_t base_converged;
+  double base_energy;
+  double pre_fitness;       /* DcContext::pre_optimization_score().fitness */
+} tg_ac_baseline;
+
+/* AcCaseResult per case (ac_validator.hpp:28-36) plus overload_energy /
+ * critical_count (ac_validator.cpp:274-288). Any pointer may be NULL;
+ * loading_mva is [n_cases][n_branches], vm_pu / va_rad [n_cases][n_nodes + n_a]. */
+typedef struct tg_ac_case_out {
+  uint8_t* converged;
+  int32_t* iterations;
+  double* overload_energy;
+  int32_t* critical_count;
+  double* loading_mva;
+  double* vm_pu;
+  double* va_rad;
+} tg_ac_case_out;
+
+/* AcValidator(grid, actions, dc, config): device tables + the baseline (base case and
+ * every contingency of the unchanged grid) computed on `device`. cfg NULL = defaults.
+ * dc supplies the pre-optimization DC fitness (may be NULL: 0). */
+tg_status tg_ac_context_create(const tg_grid* grid, const tg_actionset* actions, tg_context* dc,
+                               const tg_ac_config* cfg, int device, tg_ac_context** out);
+void tg_ac_context_destroy(tg_ac_context* ctx);
+/* baseline values; case_converged / case_energy: [n_contingencies] or NULL */
+tg_status tg_ac_baseline_get(tg_ac_context* ctx, tg_ac_baseline* out, uint8_t* case_converged, double* case_energy);
+/* AcNetwork(grid, apply_genome(genome)).run_case(k) for a batch of cases
+ * (ac_validator.cpp:26-272): case i solves genome case_genome[i] under contingency
+ * case_contingency[i] (-1 = base case). genomes: [n_genomes][n_a + n_d], -1 = empty slot. */
+tg_status tg_ac_run_cases(tg_ac_context* ctx, const int32_t* genomes, int32_t n_genomes, int32_t n_a, int32_t n_d,
+                          const int32_t* case_genome, const int32_t* case_contingency, int32_t n_cases,
+                          tg_ac_case_out* out);
+/* AcValidator::worst_k_check for n genomes at once (ac_validator.cpp:399-425): base case
+ * plus each genome's DC worst contingencies worst_idx[i][0 .. worst_n[i]); reason[i] = tg_ac_reason. */
+tg_status tg_ac_worst_k_check(tg_ac_context* ctx, const int32_t* genomes, int32_t n, int32_t n_a, int32_t n_d,
+                              const int32_t* worst_idx, const int32_t* worst_n, int32_t worst_stride, int32_t* reason);
+/* AcValidator::full_validation for n genomes at once (ac_validator.cpp:427-473): base case
+ * and every contingency; reason / accepted / ac_lambda_o per genome (accepted, ac_lambda_o may be NULL). */
+tg_status tg_ac_full_validation(tg_ac_context* ctx, const int32_t* genomes, int32_t n, int32_t n_a, int32_t n_d,
+                                int32_t* reason, uint8_t* accepted, double* ac_lambda_o);
+int64_t tg_ac_kernel_launches(tg_ac_context* ctx);  /* AC kernels launched so far */
+
 #ifdef __cplusplus
 }
 #endif

@@ -89,6 +89,15 @@ def lib() -> C.CDLL:
         L.oc_action_cache_load.argtypes = [vp, C.c_char_p]
         L.oc_action_cache_load.restype = C.c_int64
         L.oc_build_ptdf.argtypes = [vp, f64p]
+        L.oc_ac_cases.argtypes = [vp, C.c_double, C.c_int, i32p, C.c_int, C.c_int, i32p, i32p, C.c_int, C.c_int,
+                                  u8p, i32p, f64p, i32p, f64p, f64p, f64p]
+        L.oc_ac_validator_create.argtypes = [vp, C.c_double, C.c_int, C.c_int, C.c_double, C.c_int, C.c_double,
+                                             C.c_double, C.POINTER(vp)]
+        L.oc_ac_validator_destroy.argtypes = [vp]
+        L.oc_ac_baseline.argtypes = [vp, f64p, i32p, u8p, f64p, u8p, f64p]
+        L.oc_ac_worst_k.argtypes = [vp, i32p, C.c_int, C.c_int, C.c_int, i32p, i32p, C.c_int, i32p]
+        L.oc_mini_congestion_json.restype = vp
+        L.oc_ac_full.argtypes = [vp, i32p, C.c_int, C.c_int, C.c_int, i32p, u8p, f64p]
         _lib = L
     return _lib
 
@@ -111,6 +120,11 @@ def random_grid_json(seed, n_nodes=20, extra_edges=10, n_outages=5, n_stations=2
     """tests/helpers.hpp:435-553 random_grid, serialized."""
     return _take_string(lib().oc_random_grid_json(seed, n_nodes, extra_edges, n_outages, n_stations, int(multi),
                                                   int(injection), int(busbar)))
+
+
+def mini_congestion_json() -> str:
+    """tests/helpers.hpp:83-103 mini_congestion_grid as grid JSON."""
+    return _take_string(lib().oc_mini_congestion_json())
 
 
 class OracleContext:
@@ -242,3 +256,68 @@ class OracleContext:
         if rc != 0:
             raise RuntimeError(lib().oc_last_error().decode())
         return None if sing.value else f
+
+
+class OracleAc:
+    """AcNetwork / AcValidator of the restated reference (oracle/src/ac.cpp) on an OracleContext."""
+
+    def __init__(self, orc: "OracleContext", tol=1e-6, max_iter=30, q=2, frac=0.05, sim=1, dom=0.01, thr=0.05):
+        self.orc, self.tol, self.max_iter = orc, tol, max_iter
+        self.h = C.c_void_p()
+        if lib().oc_ac_validator_create(orc.h, tol, max_iter, q, frac, sim, dom, thr, C.byref(self.h)) != 0:
+            raise RuntimeError(lib().oc_last_error().decode())
+        K = orc.info["n_contingencies"]
+        lo, cr, bc, be = C.c_double(), C.c_int32(), C.c_uint8(), C.c_double()
+        cc, ce = np.zeros(max(K, 1), np.uint8), np.zeros(max(K, 1))
+        lib().oc_ac_baseline(self.h, C.byref(lo), C.byref(cr), C.byref(bc), C.byref(be), _p(cc, C.c_uint8),
+                             _p(ce, C.c_double))
+        self.baseline = dict(lambda_o=lo.value, critical=cr.value, base_converged=bool(bc.value),
+                             base_energy=be.value, case_converged=cc[:K].astype(bool), case_energy=ce[:K])
+
+    def __del__(self):
+        if getattr(self, "h", None):
+            lib().oc_ac_validator_destroy(self.h)
+            self.h = None
+
+    def cases(self, genomes, n_a, n_d, case_genome, case_cont, threads=0, loading=True) -> dict:
+        g = np.ascontiguousarray(genomes, np.int32).reshape(-1, n_a + n_d)
+        cg = np.ascontiguousarray(case_genome, np.int32)
+        ck = np.ascontiguousarray(case_cont, np.int32)
+        n = len(cg)
+        E, V = self.orc.info["n_branches"], self.orc.info["n_nodes"] + n_a
+        out = dict(converged=np.zeros(n, np.uint8), iterations=np.zeros(n, np.int32), overload_energy=np.zeros(n),
+                   critical_count=np.zeros(n, np.int32))
+        nul = C.POINTER(C.c_double)()
+        if loading:
+            out.update(loading_mva=np.zeros((n, E)), vm_pu=np.zeros((n, V)), va_rad=np.zeros((n, V)))
+        f64 = C.c_double
+        rc = lib().oc_ac_cases(self.orc.h, self.tol, self.max_iter, _p(g, C.c_int32), n_a, n_d, _p(cg, C.c_int32),
+                               _p(ck, C.c_int32), n, threads or (os.cpu_count() or 1), _p(out["converged"], C.c_uint8),
+                               _p(out["iterations"], C.c_int32), _p(out["overload_energy"], f64),
+                               _p(out["critical_count"], C.c_int32),
+                               _p(out["loading_mva"], f64) if loading else nul,
+                               _p(out["vm_pu"], f64) if loading else nul, _p(out["va_rad"], f64) if loading else nul)
+        if rc != 0:
+            raise RuntimeError(lib().oc_last_error().decode())
+        out["converged"] = out["converged"].astype(bool)
+        return out
+
+    def worst_k_check(self, genomes, n_a, n_d, worst_idx, worst_n) -> np.ndarray:
+        g = np.ascontiguousarray(genomes, np.int32).reshape(-1, n_a + n_d)
+        n = g.shape[0]
+        wi = np.ascontiguousarray(worst_idx, np.int32).reshape(n, -1)
+        wn = np.ascontiguousarray(worst_n, np.int32)
+        reason = np.zeros(n, np.int32)
+        if lib().oc_ac_worst_k(self.h, _p(g, C.c_int32), n_a, n_d, n, _p(wi, C.c_int32), _p(wn, C.c_int32),
+                               wi.shape[1], _p(reason, C.c_int32)) != 0:
+            raise RuntimeError(lib().oc_last_error().decode())
+        return reason
+
+    def full_validation(self, genomes, n_a, n_d):
+        g = np.ascontiguousarray(genomes, np.int32).reshape(-1, n_a + n_d)
+        n = g.shape[0]
+        reason, acc, lo = np.zeros(n, np.int32), np.zeros(n, np.uint8), np.zeros(n)
+        if lib().oc_ac_full(self.h, _p(g, C.c_int32), n_a, n_d, n, _p(reason, C.c_int32), _p(acc, C.c_uint8),
+                            _p(lo, C.c_double)) != 0:
+            raise RuntimeError(lib().oc_last_error().decode())
+        return reason, acc.astype(bool), lo

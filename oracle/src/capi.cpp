@@ -1,6 +1,8 @@
 // CPU ORACLE — TEST INFRASTRUCTURE ONLY (see oracle.hpp).
 // extern "C" surface so pytest / bench.py (cpu_baseline) can drive the oracle
 // through ctypes. Structured results are returned as JSON text (oc_free them).
+#include <algorithm>
+#include <atomic>
 #include <chrono>
 #include <cmath>
 #include <cstdlib>
@@ -414,4 +416,114 @@ int oc_rebuild_flows(void* h, const int32_t* genome, int na, int nd, double* flo
   });
 }
 
+
+// ---- AC validation (ac_validator.cpp) --------------------------------------
+// Cases (genome index, contingency or -1) of a genome batch on `threads` host
+// threads; any output pointer may be null (loading [n][E], vm / va [n][N + na]).
+int oc_ac_cases(void* h, double tol, int max_iter, const int32_t* genomes, int na, int nd, const int32_t* case_g,
+                const int32_t* case_k, int n, int threads, uint8_t* conv, int32_t* iters, double* energy,
+                int32_t* crit, double* loading, double* vm, double* va) {
+  return guarded([&] {
+    Ctx* c = static_cast<Ctx*>(h);
+    AcConfig cfg;
+    cfg.tolerance_pu = tol;
+    cfg.max_iterations = max_iter;
+    const int E = static_cast<int>(c->grid.branches.size());
+    const int V = static_cast<int>(c->grid.nodes.size()) + na;
+    std::atomic<int> next{0};
+    auto work = [&] {
+      for (int i; (i = next.fetch_add(1)) < n;) {
+        const AcNetwork net(c->grid, apply_genome(c->grid, c->actions, genome_at(genomes, na, nd, case_g[i])), cfg);
+        const AcCaseResult r = net.run_case(case_k[i]);
+        if (conv) conv[i] = r.converged;
+        if (iters) iters[i] = r.iterations;
+        if (energy) energy[i] = r.converged ? net.overload_energy(r) : 0.0;
+        if (crit) crit[i] = r.converged ? net.critical_count(r) : 0;
+        if (loading) std::copy(r.loading_mva.begin(), r.loading_mva.end(), loading + static_cast<size_t>(i) * E);
+        if (vm)
+          for (int v = 0; v < V; ++v) {
+            vm[static_cast<size_t>(i) * V + v] = v < static_cast<int>(r.vm_pu.size()) ? r.vm_pu[v] : 0.0;
+            va[static_cast<size_t>(i) * V + v] = v < static_cast<int>(r.va_rad.size()) ? r.va_rad[v] : 0.0;
+          }
+      }
+    };
+    const int T = std::max(1, threads);
+    std::vector<std::thread> pool;
+    for (int t = 1; t < T; ++t) pool.emplace_back(work);
+    work();
+    for (auto& t : pool) t.join();
+  });
+}
+
+struct OcAc {
+  Ctx* ctx;
+  std::unique_ptr<AcValidator> val;
+};
+
+int oc_ac_validator_create(void* h, double tol, int max_iter, int q, double frac, int sim, double dom, double thr,
+                           void** out) {
+  return guarded([&] {
+    Ctx* c = static_cast<Ctx*>(h);
+    AcConfig cfg;
+    cfg.tolerance_pu = tol;
+    cfg.max_iterations = max_iter;
+    cfg.worst_k_nonconverged = q;
+    cfg.nonconverged_fraction = frac;
+    cfg.similarity_distance = sim;
+    cfg.dominance_fitness_frac = dom;
+    cfg.improvement_threshold_frac = thr;
+    auto v = std::make_unique<OcAc>();
+    v->ctx = c;
+    v->val = std::make_unique<AcValidator>(c->grid, c->actions, *c->dc, cfg);
+    *out = v.release();
+  });
+}
+
+void oc_ac_validator_destroy(void* v) { delete static_cast<OcAc*>(v); }
+
+// lambda_o, critical, base_converged, base_energy; per contingency converged / energy
+int oc_ac_baseline(void* v, double* lambda_o, int32_t* crit, uint8_t* base_conv, double* base_energy,
+                   uint8_t* case_conv, double* case_energy) {
+  return guarded([&] {
+    const AcValidator& a = *static_cast<OcAc*>(v)->val;
+    *lambda_o = a.baseline_lambda_o();
+    *crit = a.baseline_critical_count();
+    *base_conv = a.baseline_base_converged();
+    *base_energy = a.baseline_base_energy();
+    for (std::size_t k = 0; k < a.baseline_case_converged().size(); ++k) {
+      case_conv[k] = a.baseline_case_converged()[k];
+      case_energy[k] = a.baseline_case_energy()[k];
+    }
+  });
+}
+
+// worst_k_check per genome; worst lists [n][stride] with lengths worst_n
+int oc_ac_worst_k(void* v, const int32_t* genomes, int na, int nd, int n, const int32_t* worst_idx,
+                  const int32_t* worst_n, int stride, int32_t* reason) {
+  return guarded([&] {
+    const AcValidator& a = *static_cast<OcAc*>(v)->val;
+    for (int i = 0; i < n; ++i) {
+      ScoreVector s;
+      for (int j = 0; j < worst_n[i]; ++j) s.worst_contingencies.emplace_back(worst_idx[i * stride + j], 1.0);
+      reason[i] = static_cast<int32_t>(a.worst_k_check(genome_at(genomes, na, nd, i), s));
+    }
+  });
+}
+
+// full_validation per genome
+int oc_ac_full(void* v, const int32_t* genomes, int na, int nd, int n, int32_t* reason, uint8_t* accepted,
+               double* lambda_o) {
+  return guarded([&] {
+    const AcValidator& a = *static_cast<OcAc*>(v)->val;
+    for (int i = 0; i < n; ++i) {
+      const ValidationRecord r = a.full_validation(genome_at(genomes, na, nd, i), ScoreVector{});
+      reason[i] = static_cast<int32_t>(r.reason);
+      accepted[i] = r.accepted;
+      lambda_o[i] = r.ac_lambda_o;
+    }
+  });
+}
+
+// tests/helpers.hpp:83-103 mini_congestion_grid, serialized (grid_to_json_text)
+char* oc_mini_congestion_json() { return dup_str(grid_to_json_text(oracle::fx::mini_congestion_grid())); }
 }  // extern "C"

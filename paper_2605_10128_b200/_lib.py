@@ -77,6 +77,22 @@ class OptStats(C.Structure):
     _fields_ = [("evaluations", C.c_int64), ("epochs", C.c_int32), ("n_trace", C.c_int32)]
 
 
+class AcConfigC(C.Structure):
+    _fields_ = [("tolerance_pu", C.c_double), ("max_iterations", C.c_int32), ("worst_k_nonconverged", C.c_int32),
+                ("nonconverged_fraction", C.c_double), ("similarity_distance", C.c_int32),
+                ("dominance_fitness_frac", C.c_double), ("improvement_threshold_frac", C.c_double)]
+
+
+class AcBaselineC(C.Structure):
+    _fields_ = [("lambda_o", C.c_double), ("critical_count", C.c_int32), ("base_converged", C.c_uint8),
+                ("base_energy", C.c_double), ("pre_fitness", C.c_double)]
+
+
+class AcCaseOutC(C.Structure):
+    _fields_ = [("converged", u8p), ("iterations", i32p), ("overload_energy", f64p), ("critical_count", i32p),
+                ("loading_mva", f64p), ("vm_pu", f64p), ("va_rad", f64p)]
+
+
 SNAPSHOT_CB = C.CFUNCTYPE(None, C.POINTER(SnapshotView), C.c_void_p)
 
 # (name, restype, argtypes) for every entry point of include/topopt_b200.h
@@ -146,6 +162,16 @@ SIGNATURES = [
     ("tg_islands_exchange", C.c_int, [C.c_void_p]),
     ("tg_islands_step", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
     ("tg_islands_shard_step", C.c_int, [C.c_void_p, C.c_int32, C.c_int32]),
+    ("tg_ac_context_create", C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.POINTER(AcConfigC), C.c_int,
+                                       C.POINTER(C.c_void_p)]),
+    ("tg_ac_context_destroy", None, [C.c_void_p]),
+    ("tg_ac_baseline_get", C.c_int, [C.c_void_p, C.POINTER(AcBaselineC), u8p, f64p]),
+    ("tg_ac_run_cases", C.c_int, [C.c_void_p, i32p, C.c_int32, C.c_int32, C.c_int32, i32p, i32p, C.c_int32,
+                                  C.POINTER(AcCaseOutC)]),
+    ("tg_ac_worst_k_check", C.c_int, [C.c_void_p, i32p, C.c_int32, C.c_int32, C.c_int32, i32p, i32p, C.c_int32,
+                                      i32p]),
+    ("tg_ac_full_validation", C.c_int, [C.c_void_p, i32p, C.c_int32, C.c_int32, C.c_int32, i32p, u8p, f64p]),
+    ("tg_ac_kernel_launches", C.c_int64, [C.c_void_p]),
 ]
 
 

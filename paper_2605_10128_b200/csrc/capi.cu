@@ -13,6 +13,7 @@
 #include <vector>
 
 #include "../../include/topopt_b200.h"
+#include "cuda/ac.cuh"
 #include "cuda/engine.cuh"
 #include "cuda/qd.cuh"
 #include "host/model.hpp"
@@ -2059,3 +2060,384 @@ extern "C" tg_status tg_fp64_peak(int device, double* tflops) {
     check(cudaGetLastError(), "fp64 peak");
   });
 }
+
+// ---------------------------------------------------------------- AC validation
+// AcValidator (ac_validator.hpp:93-140) on the device: the baseline at
+// creation, then worst-k and full N-1 stages for whole batches of genomes.
+struct tg_ac_context {
+  int device = 0;
+  cudaStream_t stream = nullptr;
+  DeviceArena arena;
+  tgb::AcGrid g{};
+  tg_ac_config cfg{};
+  int N = 0, E = 0, I = 0, K = 0, A = 0, D = 0;
+  double pre_fitness = 0.0;
+  // baseline of the unchanged grid (ac_validator.cpp:313-343)
+  double base_lambda_o = 0.0;
+  int base_critical = 0;
+  bool base_converged = false;
+  double base_energy = 0.0;
+  std::vector<uint8_t> case_conv;
+  std::vector<double> case_energy;
+  int64_t launches = 0;
+  // per-call buffers (grow only)
+  std::unique_ptr<DeviceArena> work;
+  size_t cap_genomes = 0, cap_cases = 0, cap_scratch = 0, cap_rows = 0;
+  int cap_slots = 0;
+  int *d_genomes = nullptr, *d_case_g = nullptr, *d_case_k = nullptr, *d_iters = nullptr, *d_crit = nullptr,
+      *d_nonconv = nullptr, *d_fcrit = nullptr;
+  int *t_from = nullptr, *t_to = nullptr, *t_inode = nullptr, *t_nnew = nullptr;
+  uint8_t *t_rem = nullptr, *d_conv = nullptr, *d_foldcase = nullptr;
+  double *d_energy = nullptr, *d_flo = nullptr, *d_loading = nullptr, *d_vm = nullptr, *d_va = nullptr;
+  unsigned long long* d_fold = nullptr;
+  unsigned char* d_scratch = nullptr;
+
+  struct Result {
+    std::vector<uint8_t> conv;
+    std::vector<int32_t> iters, crit;
+    std::vector<double> energy;
+    std::vector<int32_t> nonconv, fold_crit;  // per genome (fold runs)
+    std::vector<double> fold_lambda_o;
+  };
+  // Runs cases (genome index, contingency index) of a genome batch; with
+  // `fold`, contingency cases (k >= 0) fold their loadings per genome.
+  Result run(const int32_t* genomes, int n_genomes, int n_a, int n_d, const std::vector<int32_t>& cg,
+             const std::vector<int32_t>& ck, bool fold, double* loading, double* vm, double* va);
+};
+
+namespace {
+constexpr size_t kAcSmemMax = 200 * 1024;
+constexpr size_t kAcScratchBudget = size_t(4) << 30;
+
+tgb::AcSolver ac_solver(const tg_ac_context& ctx, int n_a) {
+  tgb::AcSolver sv{};
+  sv.tol = ctx.cfg.tolerance_pu;
+  sv.max_iter = ctx.cfg.max_iterations;
+  sv.n_bus = ctx.N + n_a;
+  sv.nu = 2 * (sv.n_bus - 1);
+  if (static_cast<double>(sv.nu) * sv.nu * 8.0 > double(size_t(1) << 30))
+    throw CapacityFailure("dense AC Jacobian of " + std::to_string(sv.nu) +
+                          " unknowns exceeds the 1 GiB per-case workspace of the batched solver");
+  sv.ws_bytes = tgb::ac_workspace_bytes(sv.n_bus, sv.nu, ctx.E);
+  sv.in_smem = sv.ws_bytes <= kAcSmemMax;
+  return sv;
+}
+}  // namespace
+
+tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, int n_a, int n_d,
+                                         const std::vector<int32_t>& cg, const std::vector<int32_t>& ck, bool fold,
+                                         double* loading, double* vm, double* va) {
+  if (n_a < 0 || n_d < 0 || n_a > 64 || n_d > 64) throw tgb::ValidationError("bad genome slot counts");
+  for (int i = 0; i < n_genomes; ++i) {
+    for (int s = 0; s < n_a; ++s) {
+      const int a = genomes[static_cast<size_t>(i) * (n_a + n_d) + s];
+      if (a < -1 || a >= A) throw tgb::ValidationError("action id out of range in genome " + std::to_string(i));
+    }
+    for (int s = 0; s < n_d; ++s) {
+      const int d = genomes[static_cast<size_t>(i) * (n_a + n_d) + n_a + s];
+      if (d < -1 || d >= D) throw tgb::ValidationError("disconnection id out of range in genome " + std::to_string(i));
+    }
+  }
+  const int nc = static_cast<int>(cg.size());
+  for (int c = 0; c < nc; ++c)
+    if (cg[c] < 0 || cg[c] >= n_genomes || ck[c] < -1 || ck[c] >= K)
+      throw tgb::ValidationError("AC case " + std::to_string(c) + " out of range");
+  const tgb::AcSolver sv0 = ac_solver(*this, n_a);
+  int slots = sv0.in_smem ? std::min(nc, 148 * 32)
+                          : std::max(1, std::min<int>({nc, 148 * 2, static_cast<int>(kAcScratchBudget / sv0.ws_bytes)}));
+  const size_t scratch = sv0.in_smem ? 0 : static_cast<size_t>(slots) * sv0.ws_bytes;
+  const size_t rows = loading ? static_cast<size_t>(nc) * E : 0;
+  const size_t vrows = vm ? static_cast<size_t>(nc) * (N + n_a) : 0;
+  check(cudaSetDevice(device), "cudaSetDevice");
+  if (!work || static_cast<size_t>(n_genomes) > cap_genomes || static_cast<size_t>(nc) > cap_cases ||
+      scratch > cap_scratch || rows + 2 * vrows > cap_rows || n_a + n_d > cap_slots) {
+    check(cudaStreamSynchronize(stream), "AC sync");
+    work.reset(new DeviceArena);
+    cap_genomes = std::max<size_t>(n_genomes, 2 * cap_genomes);
+    cap_cases = std::max<size_t>(nc, 2 * cap_cases);
+    cap_scratch = std::max(scratch, cap_scratch);
+    cap_rows = std::max(rows + 2 * vrows, cap_rows);
+    cap_slots = std::max(n_a + n_d, std::max(cap_slots, 8));
+    d_genomes = work->alloc<int>(cap_genomes * cap_slots);
+    t_from = work->alloc<int>(cap_genomes * E);
+    t_to = work->alloc<int>(cap_genomes * E);
+    t_rem = work->alloc<uint8_t>(cap_genomes * E);
+    t_inode = work->alloc<int>(cap_genomes * std::max(I, 1));
+    t_nnew = work->alloc<int>(cap_genomes);
+    d_fold = work->alloc<unsigned long long>(cap_genomes * E);
+    d_nonconv = work->alloc<int>(cap_genomes);
+    d_flo = work->alloc<double>(cap_genomes);
+    d_fcrit = work->alloc<int>(cap_genomes);
+    d_case_g = work->alloc<int>(cap_cases);
+    d_case_k = work->alloc<int>(cap_cases);
+    d_foldcase = work->alloc<uint8_t>(cap_cases);
+    d_conv = work->alloc<uint8_t>(cap_cases);
+    d_iters = work->alloc<int>(cap_cases);
+    d_crit = work->alloc<int>(cap_cases);
+    d_energy = work->alloc<double>(cap_cases);
+    d_loading = work->alloc<double>(std::max<size_t>(cap_rows, 1));
+    d_scratch = cap_scratch ? work->alloc<unsigned char>(cap_scratch) : nullptr;
+  }
+  std::vector<uint8_t> fc(nc);
+  for (int c = 0; c < nc; ++c) fc[c] = fold && ck[c] >= 0;
+  if (n_genomes)
+    check(cudaMemcpyAsync(d_genomes, genomes, sizeof(int32_t) * n_genomes * (n_a + n_d), cudaMemcpyHostToDevice,
+                          stream), "AC genomes H2D");
+  check(cudaMemcpyAsync(d_case_g, cg.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, stream), "AC cases");
+  check(cudaMemcpyAsync(d_case_k, ck.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, stream), "AC cases");
+  check(cudaMemcpyAsync(d_foldcase, fc.data(), nc, cudaMemcpyHostToDevice, stream), "AC cases");
+  if (fold) {
+    check(cudaMemsetAsync(d_fold, 0, sizeof(unsigned long long) * n_genomes * E, stream), "AC fold reset");
+    check(cudaMemsetAsync(d_nonconv, 0, sizeof(int) * n_genomes, stream), "AC fold reset");
+  }
+  tgb::AcTopo tp{t_from, t_to, t_rem, t_inode, t_nnew};
+  tgb::ac_launch_topo(g, d_genomes, n_genomes, n_a, n_d, tp, stream);
+  tgb::AcCases io{};
+  io.genome = d_case_g;
+  io.cont = d_case_k;
+  io.n = nc;
+  io.converged = d_conv;
+  io.iterations = d_iters;
+  io.energy = d_energy;
+  io.critical = d_crit;
+  io.loading = loading ? d_loading : nullptr;
+  io.vm_stride = N + n_a;
+  io.vm = vm ? d_loading + rows : nullptr;
+  io.va = vm ? d_loading + rows + vrows : nullptr;
+  io.fold_case = d_foldcase;
+  io.fold = fold ? d_fold : nullptr;
+  io.nonconverged = fold ? d_nonconv : nullptr;
+  tgb::AcSolver sv = sv0;
+  sv.scratch = d_scratch;
+  tgb::ac_launch_cases(g, tp, io, sv, slots, stream);
+  launches += 2;
+  if (fold) {
+    tgb::ac_launch_fold_finish(g, d_fold, n_genomes, d_flo, d_fcrit, stream);
+    ++launches;
+  }
+  check(cudaGetLastError(), "AC launch");
+  Result r;
+  r.conv.resize(nc);
+  r.iters.resize(nc);
+  r.crit.resize(nc);
+  r.energy.resize(nc);
+  check(cudaMemcpyAsync(r.conv.data(), d_conv, nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  check(cudaMemcpyAsync(r.iters.data(), d_iters, sizeof(int) * nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  check(cudaMemcpyAsync(r.crit.data(), d_crit, sizeof(int) * nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  check(cudaMemcpyAsync(r.energy.data(), d_energy, sizeof(double) * nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  if (loading)
+    check(cudaMemcpyAsync(loading, d_loading, sizeof(double) * rows, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  if (vm) {
+    check(cudaMemcpyAsync(vm, d_loading + rows, sizeof(double) * vrows, cudaMemcpyDeviceToHost, stream), "AC D2H");
+    check(cudaMemcpyAsync(va, d_loading + rows + vrows, sizeof(double) * vrows, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  }
+  if (fold) {
+    r.nonconv.resize(n_genomes);
+    r.fold_crit.resize(n_genomes);
+    r.fold_lambda_o.resize(n_genomes);
+    check(cudaMemcpyAsync(r.nonconv.data(), d_nonconv, sizeof(int) * n_genomes, cudaMemcpyDeviceToHost, stream), "AC D2H");
+    check(cudaMemcpyAsync(r.fold_crit.data(), d_fcrit, sizeof(int) * n_genomes, cudaMemcpyDeviceToHost, stream), "AC D2H");
+    check(cudaMemcpyAsync(r.fold_lambda_o.data(), d_flo, sizeof(double) * n_genomes, cudaMemcpyDeviceToHost, stream),
+          "AC D2H");
+  }
+  check(cudaStreamSynchronize(stream), "AC cases");
+  return r;
+}
+
+extern "C" {
+
+tg_status tg_ac_context_create(const tg_grid* grid, const tg_actionset* actions, tg_context* dc,
+                               const tg_ac_config* cfg, int device, tg_ac_context** out) {
+  return guarded([&] {
+    if (!grid || !actions || !out) throw tgb::ConfigError("null argument");
+    *out = nullptr;
+    std::unique_ptr<tg_ac_context> ctx(new tg_ac_context);
+    ctx->device = device;
+    ctx->cfg = cfg ? *cfg : tg_ac_config{1e-6, 30, 2, 0.05, 1, 0.01, 0.05};
+    if (ctx->cfg.max_iterations < 1 || !(ctx->cfg.tolerance_pu > 0.0)) throw tgb::ConfigError("bad AcConfig");
+    check(cudaSetDevice(device), "cudaSetDevice");
+    check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    const tgb::Grid& G = grid->g;
+    ctx->N = G.n_nodes();
+    ctx->E = G.n_branches();
+    ctx->I = G.n_injections();
+    ctx->K = static_cast<int>(G.cont_id.size());
+    ctx->A = actions->t.n_actions();
+    ctx->D = static_cast<int>(actions->t.disconnectables.size());
+    cudaStream_t s = ctx->stream;
+    DeviceArena& ar = ctx->arena;
+    tgb::AcGrid& g = ctx->g;
+    g.N = ctx->N, g.E = ctx->E, g.I = ctx->I, g.K = ctx->K, g.slack = G.slack;
+    g.br_from = ar.upload(grid->br_from, s);
+    g.br_to = ar.upload(grid->br_to, s);
+    g.br_on = ar.upload(grid->br_on, s);
+    g.br_lim = ar.upload(grid->br_lim, s);
+    g.br_r = ar.upload(G.br_r, s);
+    g.br_x = ar.upload(G.br_x, s);
+    g.br_bc = ar.upload(G.br_bc, s);
+    g.br_tap = ar.upload(G.br_tap, s);
+    g.node_shunt = ar.upload(G.node_shunt, s);
+    g.inj_node = ar.upload(grid->inj_node, s);
+    g.inj_p = ar.upload(G.inj_p, s);
+    g.inj_q = ar.upload(G.inj_q, s);
+    g.inj_vset = ar.upload(G.inj_vset, s);
+    std::vector<uint8_t> gen(G.inj_gen.begin(), G.inj_gen.end()), hv(G.inj_has_vset.begin(), G.inj_has_vset.end());
+    g.inj_gen = ar.upload(gen, s);
+    g.inj_has_vset = ar.upload(hv, s);
+    g.cont_br_ptr = ar.upload(grid->cont_bptr, s);
+    g.cont_br = ar.upload(grid->cont_b, s);
+    g.cont_inj_ptr = ar.upload(grid->cont_iptr, s);
+    g.cont_inj = ar.upload(grid->cont_i, s);
+    g.st_term_ptr = ar.upload(grid->sub_tptr, s);
+    g.term_kind = ar.upload(grid->tkind, s);
+    g.term_elem = ar.upload(grid->telem, s);
+    g.act_station = ar.upload(actions->station, s);
+    g.act_group_ptr = ar.upload(actions->gptr, s);
+    g.act_group = ar.upload(actions->group, s);
+    g.disc = ar.upload(actions->disc, s);
+    // pre-optimization DC fitness (ac_validator.cpp:315), from the DC context
+    if (dc) {
+      ctx->pre_fitness = dc->pre.size() > 4 ? dc->pre[4] : 0.0;
+    }
+    // baseline: the unchanged grid's base case and every contingency
+    const int K = ctx->K;
+    std::vector<int32_t> cg(K + 1, 0), ck(K + 1);
+    for (int k = 0; k <= K; ++k) ck[k] = k - 1;
+    const tg_ac_context::Result r = ctx->run(nullptr, 1, 0, 0, cg, ck, true, nullptr, nullptr, nullptr);
+    ctx->base_converged = r.conv[0];
+    ctx->base_energy = r.conv[0] ? r.energy[0] : 0.0;
+    ctx->case_conv.assign(r.conv.begin() + 1, r.conv.end());
+    ctx->case_energy.assign(K, 0.0);
+    for (int k = 0; k < K; ++k)
+      if (ctx->case_conv[k]) ctx->case_energy[k] = r.energy[k + 1];
+    ctx->base_lambda_o = r.fold_lambda_o[0];
+    ctx->base_critical = r.fold_crit[0];
+    *out = ctx.release();
+  });
+}
+
+void tg_ac_context_destroy(tg_ac_context* ctx) {
+  if (!ctx) return;
+  cudaSetDevice(ctx->device);
+  if (ctx->stream) cudaStreamSynchronize(ctx->stream);
+  ctx->work.reset();
+  if (ctx->stream) cudaStreamDestroy(ctx->stream);
+  delete ctx;
+}
+
+tg_status tg_ac_baseline_get(tg_ac_context* ctx, tg_ac_baseline* out, uint8_t* case_converged, double* case_energy) {
+  return guarded([&] {
+    if (!ctx || !out) throw tgb::ConfigError("null argument");
+    out->lambda_o = ctx->base_lambda_o;
+    out->critical_count = ctx->base_critical;
+    out->base_converged = ctx->base_converged;
+    out->base_energy = ctx->base_energy;
+    out->pre_fitness = ctx->pre_fitness;
+    if (case_converged) std::copy(ctx->case_conv.begin(), ctx->case_conv.end(), case_converged);
+    if (case_energy) std::copy(ctx->case_energy.begin(), ctx->case_energy.end(), case_energy);
+  });
+}
+
+tg_status tg_ac_run_cases(tg_ac_context* ctx, const int32_t* genomes, int32_t n_genomes, int32_t n_a, int32_t n_d,
+                          const int32_t* case_genome, const int32_t* case_contingency, int32_t n_cases,
+                          tg_ac_case_out* out) {
+  return guarded([&] {
+    if (!ctx || !out || n_cases < 0 || n_genomes < 0 || (n_genomes && !genomes) ||
+        (n_cases && (!case_genome || !case_contingency)))
+      throw tgb::ConfigError("bad argument");
+    if (n_cases == 0) return;
+    std::vector<int32_t> cg(case_genome, case_genome + n_cases), ck(case_contingency, case_contingency + n_cases);
+    if ((out->vm_pu == nullptr) != (out->va_rad == nullptr)) throw tgb::ConfigError("vm_pu and va_rad go together");
+    const tg_ac_context::Result r =
+        ctx->run(genomes, n_genomes, n_a, n_d, cg, ck, false, out->loading_mva, out->vm_pu, out->va_rad);
+    if (out->converged) std::copy(r.conv.begin(), r.conv.end(), out->converged);
+    if (out->iterations) std::copy(r.iters.begin(), r.iters.end(), out->iterations);
+    if (out->overload_energy) std::copy(r.energy.begin(), r.energy.end(), out->overload_energy);
+    if (out->critical_count) std::copy(r.crit.begin(), r.crit.end(), out->critical_count);
+  });
+}
+
+tg_status tg_ac_worst_k_check(tg_ac_context* ctx, const int32_t* genomes, int32_t n, int32_t n_a, int32_t n_d,
+                              const int32_t* worst_idx, const int32_t* worst_n, int32_t worst_stride, int32_t* reason) {
+  return guarded([&] {
+    if (!ctx || n < 0 || (n && (!genomes || !worst_idx || !worst_n || !reason)) || worst_stride < 0)
+      throw tgb::ConfigError("bad argument");
+    if (n == 0) return;
+    // cases: per genome the base case, then its worst contingencies in list order
+    std::vector<int32_t> cg, ck, first(n);
+    for (int i = 0; i < n; ++i) {
+      if (worst_n[i] < 0 || worst_n[i] > worst_stride) throw tgb::ValidationError("bad worst list length");
+      first[i] = static_cast<int32_t>(cg.size());
+      cg.push_back(i), ck.push_back(-1);
+      for (int j = 0; j < worst_n[i]; ++j) cg.push_back(i), ck.push_back(worst_idx[static_cast<size_t>(i) * worst_stride + j]);
+    }
+    const tg_ac_context::Result r = ctx->run(genomes, n, n_a, n_d, cg, ck, false, nullptr, nullptr, nullptr);
+    // ac_validator.cpp:399-425, summed in list order
+    for (int i = 0; i < n; ++i) {
+      const int b = first[i];
+      if (!r.conv[b]) {
+        reason[i] = TG_AC_NONCONVERGENCE;
+        continue;
+      }
+      if (worst_n[i] == 0) {
+        reason[i] = TG_AC_NONE;
+        continue;
+      }
+      double mine = r.energy[b], ref = ctx->base_energy;
+      int failed = 0;
+      int verdict = -1;
+      for (int j = 0; j < worst_n[i]; ++j) {
+        const int k = ck[b + 1 + j];
+        if (!r.conv[b + 1 + j]) {
+          if (++failed > ctx->cfg.worst_k_nonconverged) {
+            verdict = TG_AC_NONCONVERGENCE;
+            break;
+          }
+          continue;
+        }
+        if (!ctx->case_conv[k]) continue;
+        mine += r.energy[b + 1 + j];
+        ref += ctx->case_energy[k];
+      }
+      if (verdict < 0) verdict = (ctx->base_converged && mine >= ref) ? TG_AC_OVERLOAD_NOT_IMPROVED : TG_AC_NONE;
+      reason[i] = verdict;
+    }
+  });
+}
+
+tg_status tg_ac_full_validation(tg_ac_context* ctx, const int32_t* genomes, int32_t n, int32_t n_a, int32_t n_d,
+                                int32_t* reason, uint8_t* accepted, double* ac_lambda_o) {
+  return guarded([&] {
+    if (!ctx || n < 0 || (n && (!genomes || !reason))) throw tgb::ConfigError("bad argument");
+    if (n == 0) return;
+    const int K = ctx->K;
+    std::vector<int32_t> cg, ck;
+    cg.reserve(static_cast<size_t>(n) * (K + 1));
+    ck.reserve(cg.capacity());
+    for (int i = 0; i < n; ++i)
+      for (int k = -1; k < K; ++k) cg.push_back(i), ck.push_back(k);
+    const tg_ac_context::Result r = ctx->run(genomes, n, n_a, n_d, cg, ck, true, nullptr, nullptr, nullptr);
+    // ac_validator.cpp:445-472
+    for (int i = 0; i < n; ++i) {
+      const bool base_ok = r.conv[static_cast<size_t>(i) * (K + 1)];
+      int why = TG_AC_NONE;
+      double lo = 0.0;
+      if (!base_ok || r.nonconv[i] > ctx->cfg.nonconverged_fraction * K) {
+        why = TG_AC_NONCONVERGENCE;
+      } else {
+        lo = r.fold_lambda_o[i];
+        if (!(lo < ctx->base_lambda_o))
+          why = TG_AC_OVERLOAD_NOT_IMPROVED;
+        else if (r.fold_crit[i] > ctx->base_critical)
+          why = TG_AC_CRITICAL_COUNT_INCREASED;
+      }
+      reason[i] = why;
+      if (accepted) accepted[i] = why == TG_AC_NONE;
+      if (ac_lambda_o) ac_lambda_o[i] = lo;
+    }
+  });
+}
+
+int64_t tg_ac_kernel_launches(tg_ac_context* ctx) { return ctx ? ctx->launches : 0; }
+
+}  // extern "C"

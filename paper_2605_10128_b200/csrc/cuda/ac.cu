@@ -1,0 +1,534 @@
+// Batched AC Newton-Raphson cases (see ac.cuh). One CTA per case; the
+// reference's per-case algorithm (ac_validator.cpp:37-272) with the case's
+// dense Ybus / Jacobian in the CTA's workspace.
+#include <cfloat>
+
+#include "ac.cuh"
+
+namespace tgb {
+
+namespace {
+
+constexpr double kBaseMva = 100.0;  // ac_validator.cpp:14
+
+// Workspace of one case (offsets in bytes, 16-byte aligned sections).
+struct AcWs {
+  double *J, *G, *B, *vm, *va, *P, *Q, *psp, *qsp, *vset, *dx, *lm, *red;
+  int *bus_of, *node_of, *ang, *mag, *pv, *reach, *ired;
+  uint8_t* live;
+};
+
+__host__ __device__ inline size_t align16(size_t b) { return (b + 15) & ~size_t(15); }
+
+__host__ __device__ inline size_t ws_layout(int n_bus, int nu, int E, unsigned char* base, AcWs* w) {
+  size_t off = 0;
+  auto take_d = [&](size_t n) {
+    double* p = reinterpret_cast<double*>(base + off);
+    off = align16(off + n * sizeof(double));
+    return p;
+  };
+  auto take_i = [&](size_t n) {
+    int* p = reinterpret_cast<int*>(base + off);
+    off = align16(off + n * sizeof(int));
+    return p;
+  };
+  const size_t nb = static_cast<size_t>(n_bus), nn = static_cast<size_t>(nu);
+  AcWs t{};
+  t.J = take_d(nn * nn);
+  t.G = take_d(nb * nb);
+  t.B = take_d(nb * nb);
+  t.vm = take_d(nb);
+  t.va = take_d(nb);
+  t.P = take_d(nb);
+  t.Q = take_d(nb);
+  t.psp = take_d(nb);
+  t.qsp = take_d(nb);
+  t.vset = take_d(nb);
+  t.dx = take_d(nn);
+  t.lm = take_d(nn);
+  t.red = take_d(64);
+  t.bus_of = take_i(nb);
+  t.node_of = take_i(nb);
+  t.ang = take_i(nn);
+  t.mag = take_i(nn);
+  t.pv = take_i(nb);
+  t.reach = take_i(nb);
+  t.ired = take_i(64);
+  t.live = reinterpret_cast<uint8_t*>(base + off);
+  off = align16(off + static_cast<size_t>(E));
+  if (w) *w = t;
+  return off;
+}
+
+// ---- block reductions (every thread calls; deterministic order) -----------
+template <int NT>
+__device__ double block_max(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v = fmax(v, __shfl_xor_sync(0xffffffffu, v, o));
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int i = 1; i < NT / 32; ++i) r = fmax(r, red[i]);
+  return r;
+}
+
+template <int NT>
+__device__ double block_sum(double v, double* red) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v;
+  __syncthreads();
+  double r = red[0];
+  for (int i = 1; i < NT / 32; ++i) r += red[i];
+  return r;
+}
+
+template <int NT>
+__device__ int block_sum_int(int v, int* ired) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) ired[w] = v;
+  __syncthreads();
+  int r = 0;
+  for (int i = 0; i < NT / 32; ++i) r += ired[i];
+  return r;
+}
+
+// first index of the largest value (values < 0 never win: the caller passes -1
+// for no candidate)
+template <int NT>
+__device__ int block_argmax(double v, int idx, double* red, int* ired) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) v = ov, idx = oi;
+  }
+  const int w = threadIdx.x >> 5;
+  __syncthreads();
+  if ((threadIdx.x & 31) == 0) red[w] = v, ired[w] = idx;
+  __syncthreads();
+  double bv = red[0];
+  int bi = ired[0];
+  for (int i = 1; i < NT / 32; ++i)
+    if (red[i] > bv || (red[i] == bv && ired[i] < bi)) bv = red[i], bi = ired[i];
+  return bi;
+}
+
+__device__ __forceinline__ bool in_list(const int* lo, const int* hi, int x) {
+  for (const int* p = lo; p < hi; ++p)
+    if (*p == x) return true;
+  return false;
+}
+
+// Series and shunt admittances of branch e in the pi model with the tap on the
+// from side: yff = (ys + j bc/2) / t^2, yft = ytf = -ys / t, ytt = ys + j bc/2
+// (ac_validator.cpp:123-133).
+struct BranchY {
+  double ffr, ffi, ftr, fti, ttr, tti;
+};
+__device__ __forceinline__ BranchY branch_y(const AcGrid& g, int e) {
+  const double r = g.br_r[e], x = g.br_x[e], t = g.br_tap[e];
+  const double d = r * r + x * x;
+  const double ysr = r / d, ysi = -x / d;  // 1 / (r + j x)
+  const double shi = g.br_bc[e] / 2.0;
+  BranchY y;
+  y.ffr = ysr / (t * t);
+  y.ffi = (ysi + shi) / (t * t);
+  y.ftr = -ysr / t;
+  y.fti = -ysi / t;
+  y.ttr = ysr;
+  y.tti = ysi + shi;
+  return y;
+}
+
+// LU with row partial pivoting of the nu x nu row-major J, solving J x = dx in
+// place (dx <- x). Eigen::PartialPivLU's pivot rule (first largest |a_ik|);
+// a zero pivot leaves non-finite entries, tested by the caller like the
+// reference's step.allFinite() (ac_validator.cpp:239-241).
+template <int NT>
+__device__ void lu_solve(double* J, double* dx, double* lm, int nu, double* red, int* ired) {
+  const int tid = threadIdx.x;
+  for (int k = 0; k < nu; ++k) {
+    double best = -1.0;
+    int bi = nu;
+    for (int i = k + tid; i < nu; i += NT) {
+      const double a = fabs(J[static_cast<size_t>(i) * nu + k]);
+      if (a > best) best = a, bi = i;
+    }
+    int p = block_argmax<NT>(best, bi, red, ired);
+    if (p >= nu) p = k;
+    if (p != k) {
+      for (int j = k + tid; j < nu; j += NT) {
+        const double t = J[static_cast<size_t>(k) * nu + j];
+        J[static_cast<size_t>(k) * nu + j] = J[static_cast<size_t>(p) * nu + j];
+        J[static_cast<size_t>(p) * nu + j] = t;
+      }
+      if (tid == 0) {
+        const double t = dx[k];
+        dx[k] = dx[p];
+        dx[p] = t;
+      }
+    }
+    __syncthreads();
+    const double piv = J[static_cast<size_t>(k) * nu + k];
+    const double bk = dx[k];
+    for (int i = k + 1 + tid; i < nu; i += NT) {
+      const double l = J[static_cast<size_t>(i) * nu + k] / piv;
+      lm[i] = l;
+      dx[i] -= l * bk;
+    }
+    __syncthreads();
+    const int m = nu - k - 1;
+    for (int idx = tid; idx < m * m; idx += NT) {
+      const int i = k + 1 + idx / m, j = k + 1 + idx % m;
+      const double l = lm[i];
+      if (l != 0.0) J[static_cast<size_t>(i) * nu + j] -= l * J[static_cast<size_t>(k) * nu + j];
+    }
+    __syncthreads();
+  }
+  for (int i = nu - 1; i >= 0; --i) {
+    if (tid == 0) dx[i] = dx[i] / J[static_cast<size_t>(i) * nu + i];
+    __syncthreads();
+    const double xi = dx[i];
+    for (int r = tid; r < i; r += NT) dx[r] -= J[static_cast<size_t>(r) * nu + i] * xi;
+    __syncthreads();
+  }
+}
+
+template <int NT>
+__device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io, const AcSolver& sv, int c,
+                           const AcWs& w) {
+  const int tid = threadIdx.x;
+  const int E = g.E, I = g.I;
+  const int gi = io.genome[c], ci = io.cont[c];
+  const int nnew = tp.n_new[gi];
+  const int nbus = g.N + nnew;
+  const int* ef = tp.from + static_cast<size_t>(gi) * E;
+  const int* et = tp.to + static_cast<size_t>(gi) * E;
+  const uint8_t* rem = tp.removed + static_cast<size_t>(gi) * E;
+  const int* inode = tp.inj_node + static_cast<size_t>(gi) * I;
+  const int* cb0 = ci >= 0 ? g.cont_br + g.cont_br_ptr[ci] : nullptr;
+  const int* cb1 = ci >= 0 ? g.cont_br + g.cont_br_ptr[ci + 1] : nullptr;
+  const int* cj0 = ci >= 0 ? g.cont_inj + g.cont_inj_ptr[ci] : nullptr;
+  const int* cj1 = ci >= 0 ? g.cont_inj + g.cont_inj_ptr[ci + 1] : nullptr;
+  const bool fold = io.fold != nullptr && io.fold_case != nullptr && io.fold_case[c];
+
+  // live branches (ac_validator.cpp:45-49) and reachability from the slack
+  // (52-73) by label propagation over the live edges
+  for (int e = tid; e < E; e += NT) w.live[e] = g.br_on[e] && !rem[e] && !in_list(cb0, cb1, e);
+  for (int v = tid; v < nbus; v += NT) w.reach[v] = v == g.slack;
+  __syncthreads();
+  for (;;) {
+    bool changed = false;
+    for (int e = tid; e < E; e += NT) {
+      if (!w.live[e]) continue;
+      const int a = ef[e], b = et[e];
+      if (w.reach[a] != w.reach[b]) {
+        w.reach[a] = 1;
+        w.reach[b] = 1;
+        changed = true;
+      }
+    }
+    if (!__syncthreads_or(changed)) break;
+  }
+  // a live component without the slack, or a stranded nonzero injection:
+  // not converged after zero iterations (ac_validator.cpp:74-82)
+  bool bad = false;
+  for (int e = tid; e < E; e += NT)
+    if (w.live[e] && !w.reach[ef[e]]) bad = true;
+  for (int i = tid; i < I; i += NT)
+    if ((g.inj_p[i] != 0.0 || g.inj_q[i] != 0.0) && !w.reach[inode[i]] && !in_list(cj0, cj1, i)) bad = true;
+  const bool floating = __syncthreads_or(bad);
+
+  int* sh = w.ired + 32;  // n, slack bus, n angles, n magnitudes
+  if (!floating) {
+    // bus numbering, specified injections, PV buses (ac_validator.cpp:84-115),
+    // Ybus in branch order (117-141), flat start and unknown order (143-156)
+    const int nmax = sv.n_bus;
+    for (int i = tid; i < nmax * nmax; i += NT) w.G[i] = 0.0, w.B[i] = 0.0;
+    __syncthreads();
+    if (tid == 0) {
+      int n = 0;
+      for (int v = 0; v < nbus; ++v) {
+        w.bus_of[v] = w.reach[v] ? n : -1;
+        if (w.reach[v]) w.node_of[n++] = v;
+      }
+      for (int b = 0; b < n; ++b) w.psp[b] = 0.0, w.qsp[b] = 0.0, w.vset[b] = 1.0, w.pv[b] = 0;
+      for (int i = 0; i < I; ++i) {
+        if (in_list(cj0, cj1, i)) continue;
+        const int b = w.bus_of[inode[i]];
+        if (b < 0) continue;
+        if (g.inj_gen[i]) {
+          w.psp[b] += g.inj_p[i] / kBaseMva;
+          if (g.inj_has_vset[i]) {
+            if (!w.pv[b]) w.vset[b] = g.inj_vset[i];
+            w.pv[b] = 1;
+          } else {
+            w.qsp[b] += g.inj_q[i] / kBaseMva;
+          }
+        } else {
+          w.psp[b] -= g.inj_p[i] / kBaseMva;
+          w.qsp[b] -= g.inj_q[i] / kBaseMva;
+        }
+      }
+      for (int e = 0; e < E; ++e) {
+        if (!w.live[e]) continue;
+        const BranchY y = branch_y(g, e);
+        const int f = w.bus_of[ef[e]], t = w.bus_of[et[e]];
+        w.G[f * n + f] += y.ffr, w.B[f * n + f] += y.ffi;
+        w.G[f * n + t] += y.ftr, w.B[f * n + t] += y.fti;
+        w.G[t * n + f] += y.ftr, w.B[t * n + f] += y.fti;
+        w.G[t * n + t] += y.ttr, w.B[t * n + t] += y.tti;
+      }
+      for (int v = 0; v < g.N; ++v)
+        if (w.bus_of[v] >= 0 && g.node_shunt[v] != 0.0) w.B[w.bus_of[v] * n + w.bus_of[v]] += g.node_shunt[v];
+      const int sl = w.bus_of[g.slack];
+      int na = 0, nm = 0;
+      for (int b = 0; b < n; ++b) {
+        w.vm[b] = (w.pv[b] || b == sl) ? w.vset[b] : 1.0;
+        w.va[b] = 0.0;
+        if (b == sl) continue;
+        w.ang[na++] = b;
+      }
+      for (int b = 0; b < n; ++b)
+        if (b != sl && !w.pv[b]) w.mag[nm++] = b;
+      sh[0] = n, sh[1] = sl, sh[2] = na, sh[3] = nm;
+    }
+    __syncthreads();
+  }
+  const int n = floating ? 0 : sh[0];
+  const int na = floating ? 0 : sh[2], nm = floating ? 0 : sh[3], nu = na + nm;
+
+  bool ok = false;
+  int iters = 0;
+  if (!floating) {
+    for (int it = 1; it <= sv.max_iter; ++it) {  // ac_validator.cpp:175-244
+      // bus injections (159-173)
+      for (int i = tid; i < n; i += NT) {
+        double p = 0.0, q = 0.0;
+        const double vi = w.vm[i], ai = w.va[i];
+        for (int k = 0; k < n; ++k) {
+          const double gik = w.G[i * n + k], bik = w.B[i * n + k];
+          if (gik == 0.0 && bik == 0.0) continue;
+          double s, co;
+          sincos(ai - w.va[k], &s, &co);
+          p += vi * w.vm[k] * (gik * co + bik * s);
+          q += vi * w.vm[k] * (gik * s - bik * co);
+        }
+        w.P[i] = p;
+        w.Q[i] = q;
+      }
+      __syncthreads();
+      double wl = 0.0;
+      for (int r = tid; r < nu; r += NT) {
+        const double m = r < na ? w.psp[w.ang[r]] - w.P[w.ang[r]] : w.qsp[w.mag[r - na]] - w.Q[w.mag[r - na]];
+        w.dx[r] = m;
+        wl = fmax(wl, fabs(m));  // std::max(worst, |m|): a NaN mismatch is skipped, like the reference
+      }
+      const double worst = block_max<NT>(wl, w.red);
+      iters = it;
+      if (!isfinite(worst) || worst > 1e8) break;
+      if (worst < sv.tol) {
+        ok = true;
+        break;
+      }
+      if (it == sv.max_iter) break;
+      // Jacobian (186-236)
+      for (int idx = tid; idx < nu * nu; idx += NT) {
+        const int r = idx / nu, cc = idx % nu;
+        const int i = r < na ? w.ang[r] : w.mag[r - na];
+        const int k = cc < na ? w.ang[cc] : w.mag[cc - na];
+        const double vi = w.vm[i];
+        double v;
+        if (i == k) {
+          const double gii = w.G[i * n + i], bii = w.B[i * n + i];
+          if (r < na)
+            v = cc < na ? -w.Q[i] - bii * vi * vi : w.P[i] / vi + gii * vi;
+          else
+            v = cc < na ? w.P[i] - gii * vi * vi : w.Q[i] / vi - bii * vi;
+        } else {
+          const double gik = w.G[i * n + k], bik = w.B[i * n + k];
+          if (gik == 0.0 && bik == 0.0) {
+            v = 0.0;
+          } else {
+            double s, co;
+            sincos(w.va[i] - w.va[k], &s, &co);
+            const double vk = w.vm[k];
+            if (r < na)
+              v = cc < na ? vi * vk * (gik * s - bik * co) : vi * (gik * co + bik * s);
+            else
+              v = cc < na ? -vi * vk * (gik * co + bik * s) : vi * (gik * s - bik * co);
+          }
+        }
+        w.J[idx] = v;
+      }
+      __syncthreads();
+      lu_solve<NT>(w.J, w.dx, w.lm, nu, w.red, w.ired);
+      bool fin = true;
+      for (int r = tid; r < nu; r += NT) fin = fin && isfinite(w.dx[r]);
+      if (!__syncthreads_and(fin)) break;
+      for (int r = tid; r < nu; r += NT) {
+        if (r < na)
+          w.va[w.ang[r]] += w.dx[r];
+        else
+          w.vm[w.mag[r - na]] += w.dx[r];
+      }
+      __syncthreads();
+    }
+  }
+
+  // outputs (ac_validator.cpp:246-272, 274-288)
+  if (io.vm)
+    for (int v = tid; v < io.vm_stride; v += NT) {
+      const int b = ok && v < nbus ? w.bus_of[v] : -1;
+      io.vm[static_cast<size_t>(c) * io.vm_stride + v] = b >= 0 ? w.vm[b] : 0.0;
+      io.va[static_cast<size_t>(c) * io.vm_stride + v] = b >= 0 ? w.va[b] : 0.0;
+    }
+  double en = 0.0;
+  int cr = 0;
+  for (int e = tid; e < E; e += NT) {
+    double load = 0.0;
+    if (ok && w.live[e]) {
+      const BranchY y = branch_y(g, e);
+      const int f = w.bus_of[ef[e]], t = w.bus_of[et[e]];
+      double sf, cf, st, ct;
+      sincos(w.va[f], &sf, &cf);
+      sincos(w.va[t], &st, &ct);
+      const double vfr = w.vm[f] * cf, vfi = w.vm[f] * sf, vtr = w.vm[t] * ct, vti = w.vm[t] * st;
+      // I_f = yff V_f + yft V_t, I_t = ytf V_f + ytt V_t; S = V conj(I)
+      const double ifr = y.ffr * vfr - y.ffi * vfi + y.ftr * vtr - y.fti * vti;
+      const double ifi = y.ffr * vfi + y.ffi * vfr + y.ftr * vti + y.fti * vtr;
+      const double itr = y.ftr * vfr - y.fti * vfi + y.ttr * vtr - y.tti * vti;
+      const double iti = y.ftr * vfi + y.fti * vfr + y.ttr * vti + y.tti * vtr;
+      const double sfr = vfr * ifr + vfi * ifi, sfi = vfi * ifr - vfr * ifi;
+      const double str = vtr * itr + vti * iti, sti = vti * itr - vtr * iti;
+      load = fmax(hypot(sfr, sfi), hypot(str, sti)) * kBaseMva;
+    }
+    if (io.loading) io.loading[static_cast<size_t>(c) * E + e] = load;
+    if (ok) {
+      const double d = load - g.br_lim[e];
+      en += d > 0.0 ? d : 0.0;
+      cr += load > g.br_lim[e];
+    }
+    if (fold && ok) atomicMax(io.fold + static_cast<size_t>(gi) * E + e, static_cast<unsigned long long>(__double_as_longlong(load)));
+  }
+  const double energy = block_sum<NT>(en, w.red);
+  const int crit = block_sum_int<NT>(cr, w.ired);
+  if (tid == 0) {
+    io.converged[c] = ok;
+    io.iterations[c] = iters;
+    if (io.energy) io.energy[c] = ok ? energy : 0.0;
+    if (io.critical) io.critical[c] = ok ? crit : 0;
+    if (fold && !ok && io.nonconverged) atomicAdd(io.nonconverged + gi, 1);
+  }
+  __syncthreads();
+}
+
+template <int NT>
+__global__ void __launch_bounds__(NT) k_ac_case(AcGrid g, AcTopo tp, AcCases io, AcSolver sv) {
+  extern __shared__ __align__(16) unsigned char ac_smem[];
+  unsigned char* base = sv.in_smem ? ac_smem : sv.scratch + static_cast<size_t>(blockIdx.x) * sv.ws_bytes;
+  AcWs w;
+  ws_layout(sv.n_bus, sv.nu, g.E, base, &w);
+  for (int c = blockIdx.x; c < io.n; c += gridDim.x) solve_case<NT>(g, tp, io, sv, c, w);
+}
+
+// apply_genome (genome.cpp:76-110): base endpoints, disconnections removed,
+// then each split slot in order moves its group's terminals to node N + j.
+__global__ void k_ac_topo(AcGrid g, const int* genomes, int n_a, int n_d, AcTopo t) {
+  const int gi = blockIdx.x, E = g.E, I = g.I;
+  const int* gen = genomes + static_cast<size_t>(gi) * (n_a + n_d);
+  int* from = t.from + static_cast<size_t>(gi) * E;
+  int* to = t.to + static_cast<size_t>(gi) * E;
+  uint8_t* rem = t.removed + static_cast<size_t>(gi) * E;
+  int* inode = t.inj_node + static_cast<size_t>(gi) * I;
+  for (int e = threadIdx.x; e < E; e += blockDim.x) from[e] = g.br_from[e], to[e] = g.br_to[e], rem[e] = 0;
+  for (int i = threadIdx.x; i < I; i += blockDim.x) inode[i] = g.inj_node[i];
+  __syncthreads();
+  if (threadIdx.x < n_d) {
+    const int d = gen[n_a + threadIdx.x];
+    if (d >= 0) rem[g.disc[d]] = 1;
+  }
+  int nn = 0;
+  for (int s = 0; s < n_a; ++s) {
+    const int a = gen[s];
+    if (a < 0) continue;
+    const int st = g.act_station[a];
+    const int t0 = g.st_term_ptr[st], nt = g.st_term_ptr[st + 1] - t0;
+    const uint8_t* grp = g.act_group + g.act_group_ptr[a];
+    const int node = g.N + nn;
+    for (int k = threadIdx.x; k < nt; k += blockDim.x) {
+      if (!grp[k]) continue;
+      const int kind = g.term_kind[t0 + k], el = g.term_elem[t0 + k];
+      if (kind == 2)
+        inode[el] = node;
+      else if (kind == 0)
+        from[el] = node;
+      else
+        to[el] = node;
+    }
+    ++nn;
+  }
+  if (threadIdx.x == 0) t.n_new[gi] = nn;
+}
+
+// one warp per genome: lambda_o and critical count over the folded maxima
+// (ac_validator.cpp:451-456); lane partial sums then a fixed shuffle tree
+__global__ void k_ac_fold_finish(AcGrid g, const unsigned long long* fold, int n, double* lambda_o, int* critical) {
+  const int gi = blockIdx.x * (blockDim.x / 32) + threadIdx.x / 32, lane = threadIdx.x & 31;
+  if (gi >= n) return;
+  double s = 0.0;
+  int cnt = 0;
+  for (int e = lane; e < g.E; e += 32) {
+    const double m = __longlong_as_double(static_cast<long long>(fold[static_cast<size_t>(gi) * g.E + e]));
+    const double d = m - g.br_lim[e];
+    s += d > 0.0 ? d : 0.0;
+    cnt += m > g.br_lim[e];
+  }
+  for (int o = 16; o > 0; o >>= 1) {
+    s += __shfl_xor_sync(0xffffffffu, s, o);
+    cnt += __shfl_xor_sync(0xffffffffu, cnt, o);
+  }
+  if (lane == 0) lambda_o[gi] = s, critical[gi] = cnt;
+}
+
+}  // namespace
+
+size_t ac_workspace_bytes(int n_bus, int nu, int E) { return ws_layout(n_bus, nu, E, nullptr, nullptr); }
+
+int ac_threads(int nu) { return nu <= 48 ? 64 : (nu <= 160 ? 256 : 512); }
+
+void ac_launch_topo(const AcGrid& g, const int* genomes, int n_genomes, int n_a, int n_d, const AcTopo& t,
+                    cudaStream_t s) {
+  if (n_genomes > 0) k_ac_topo<<<n_genomes, 128, 0, s>>>(g, genomes, n_a, n_d, t);
+}
+
+void ac_launch_cases(const AcGrid& g, const AcTopo& t, const AcCases& c, const AcSolver& sv, int ctas,
+                     cudaStream_t s) {
+  if (c.n <= 0) return;
+  const size_t smem = sv.in_smem ? sv.ws_bytes : 0;
+  switch (ac_threads(sv.nu)) {
+    case 64:
+      cudaFuncSetAttribute(k_ac_case<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_ac_case<64><<<ctas, 64, smem, s>>>(g, t, c, sv);
+      break;
+    case 256:
+      cudaFuncSetAttribute(k_ac_case<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_ac_case<256><<<ctas, 256, smem, s>>>(g, t, c, sv);
+      break;
+    default:
+      cudaFuncSetAttribute(k_ac_case<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+      k_ac_case<512><<<ctas, 512, smem, s>>>(g, t, c, sv);
+      break;
+  }
+}
+
+void ac_launch_fold_finish(const AcGrid& g, const unsigned long long* fold, int n_genomes, double* lambda_o,
+                           int* critical, cudaStream_t s) {
+  if (n_genomes > 0) k_ac_fold_finish<<<(n_genomes + 3) / 4, 128, 0, s>>>(g, fold, n_genomes, lambda_o, critical);
+}
+
+}  // namespace tgb
