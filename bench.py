@@ -207,12 +207,171 @@ def run_reference(args, world, rank):
     print(json.dumps(line), flush=True)
 
 
+# ---------------------------------------------------------------- AC stage (--stage ac)
+AC_CONFIGS = {
+    "cfg1": dict(workload="grid14_congested (bundled), 2048 DC-proposed topologies, full AC N-1 validation "
+                          "(base case + every contingency)", genomes=2048),
+    "ac118": dict(workload="synthetic 118-bus grid with AC data (tools/synth_grid.py with_ac_data), 256 topologies, "
+                           "full AC N-1 validation", genomes=256),
+}
+
+
+def ac_grid_text(cfg: str) -> str:
+    if cfg == "cfg1":
+        return open(os.path.join(ROOT, "tests", "golden", "data", "grid14_congested.json")).read()
+    from tools.synth_grid import synth_grid, with_ac_data
+    return json.dumps(with_ac_data(synth_grid(118, seed=7, n_stations=6)))
+
+
+def random_valid_genomes(actions, n: int, n_a: int = 3, n_d: int = 2, seed: int = 5) -> np.ndarray:
+    """Valid genomes (distinct stations, distinct disconnections; genome.cpp:41-62)."""
+    rng = np.random.default_rng(seed)
+    ranges = sorted(actions.station_ranges.items())
+    D = len(actions.disconnectables)
+    out = np.full((n, n_a + n_d), -1, np.int32)
+    for i in range(n):
+        ns = int(rng.integers(0, min(n_a, len(ranges)) + 1))
+        for j, k in enumerate(rng.choice(len(ranges), ns, replace=False)):
+            lo, hi = ranges[k][1]
+            out[i, j] = int(rng.integers(lo, hi))
+        nd = int(rng.integers(0, min(n_d, D) + 1))
+        for j, d in enumerate(rng.choice(D, nd, replace=False)):
+            out[i, n_a + j] = int(d)
+    return out
+
+
+def run_ac(args, world, rank):
+    """AC validation stage (SURVEY 8(f) row 4): AcValidator::full_validation for a batch of
+    topologies, every (topology, contingency) case solved by the batched device Newton-Raphson.
+    One step = one full_validation call through the C ABI with host genomes in and verdicts
+    out. --impl reference: the reference algorithm (oracle restatement) on all host cores."""
+    cfgname = args.config if args.config in AC_CONFIGS else "cfg1"
+    text = ac_grid_text(cfgname)
+    n_gen = AC_CONFIGS[cfgname]["genomes"]
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from oracle.oracle import OracleAc, OracleContext
+        orc = OracleContext(text)
+        oac = OracleAc(orc)
+        import paper_2605_10128_b200  # noqa: F401  (not used: genomes below come from numpy)
+        K = orc.info["n_contingencies"]
+        gen = orc.random_genomes(n_gen, 3, 2, seed=5)
+        cores = os.cpu_count() or 1
+        cg = np.repeat(np.arange(n_gen), K + 1).astype(np.int32)
+        ck = np.tile(np.arange(-1, K, dtype=np.int32), n_gen)
+        t0 = time.perf_counter()
+        oac.cases(gen, 3, 2, cg[:cores * (K + 1)], ck[:cores * (K + 1)], threads=cores, loading=False)
+        per = (time.perf_counter() - t0) / (cores * (K + 1))
+        m = int(max(cores * (K + 1), min(len(cg), 2.0 / max(per, 1e-9))))
+        times = []
+        for _ in range(args.warmup + args.steps):
+            t0 = time.perf_counter()
+            oac.cases(gen, 3, 2, cg[:m], ck[:m], threads=cores, loading=False)
+            times.append(time.perf_counter() - t0)
+        dt = sum(times[args.warmup:])
+        value = m * args.steps / dt / (K + 1)
+        line = {"metric": "AC N-1 validated topologies/sec", "value": value, "unit": "topologies/s",
+                "n_gpus": args.gpus, "steps": args.steps, "warmup": args.warmup,
+                "ms_per_step": 1000 * dt / args.steps, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f64", "data": "synthetic genomes", "impl": "reference",
+                "config": {"workload": AC_CONFIGS[cfgname]["workload"], "cases_per_step": m},
+                "cpu_baseline": {"value": value, "unit": "topologies/s", "cores": cores, "kind": "port",
+                                 "sample": f"{m} AcNetwork::run_case solves per step (bounded sample) on {cores} "
+                                           "threads"},
+                "e2e": {"value": value, "unit": "topologies/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+        print(json.dumps(line), flush=True)
+        return
+
+    import torch
+    import paper_2605_10128_b200 as P
+    from paper_2605_10128_b200.ac import AcContext
+
+    dev = local_device = int(os.environ.get("LOCAL_RANK", "0")) % max(1, torch.cuda.device_count())
+    torch.cuda.set_device(dev)
+    grid = P.grid_from_json_text(text)
+    actions = P.build_action_set(grid)
+    dc = P.DcContext(grid, actions, P.DcConfig(), device=local_device)
+    t_setup = time.perf_counter()
+    ac = AcContext(grid, actions, dc, device=dev)
+    setup_s = time.perf_counter() - t_setup
+    K = grid.n_contingencies
+    genomes = random_valid_genomes(actions, n_gen, seed=5 + rank)
+    for _ in range(args.warmup):
+        ac.full_validation_arrays(genomes, 3, 2)
+    l0 = ac.kernel_launches()
+    with ClockSampler(dev) as clk:
+        clk.mark()
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            reason, acc, lo = ac.full_validation_arrays(genomes, 3, 2)
+        torch.cuda.synchronize()
+        dt = time.perf_counter() - t0
+    dt = max_over_ranks(dt, world, dev)
+    launches = ac.kernel_launches() - l0
+    value = n_gen * args.steps * world / dt
+    # iterations per case for the work estimate (one extra probe call)
+    cg = np.repeat(np.arange(n_gen), K + 1).astype(np.int32)
+    ck = np.tile(np.arange(-1, K, dtype=np.int32), n_gen)
+    r = ac.run_cases(genomes, cg, ck, 3, 2, loading=False, voltages=False)
+    nb = grid.n_nodes + 3
+    nu = 2 * (nb - 1)
+    # dense LU (2/3 nu^3) + Jacobian and injections (~ 12 nu^2) per Newton step
+    flops = float(np.sum(np.maximum(r["iterations"] - 1, 0))) * (2.0 / 3.0 * nu ** 3 + 12.0 * nu ** 2)
+    tflops = flops * args.steps / dt / 1e12
+    peak = P.fp64_peak_tflops(dev)
+    base = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        from oracle.oracle import OracleAc, OracleContext
+        oac = OracleAc(OracleContext(text))
+        cores = os.cpu_count() or 1
+        m = min(len(cg), max(cores * (K + 1), 4000))
+        t0 = time.perf_counter()
+        oac.cases(genomes, 3, 2, cg[:m], ck[:m], threads=cores, loading=False)
+        m = int(min(len(cg), max(m, m * 3.0 / max(time.perf_counter() - t0, 1e-6))))  # ~3 s sample
+        t0 = time.perf_counter()
+        oac.cases(genomes, 3, 2, cg[:m], ck[:m], threads=cores, loading=False)
+        cdt = time.perf_counter() - t0
+        base = {"value": m / cdt / (K + 1), "unit": "topologies/s", "cores": cores, "kind": "port",
+                "sample": f"{m} AcNetwork::run_case solves of the same topologies (oracle restatement of "
+                          f"ac_validator.cpp) on {cores} threads, {cdt:.1f} s"}
+    if rank == 0:
+        line = {"metric": "AC N-1 validated topologies/sec", "value": value, "unit": "topologies/s",
+                "n_gpus": world, "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1000 * dt / args.steps,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic genomes (seeded, valid), grid as named",
+                "config": {"workload": AC_CONFIGS[cfgname]["workload"], "topologies_per_step": n_gen,
+                           "cases_per_step": n_gen * (K + 1), "n_buses": grid.n_nodes, "n_contingencies": K,
+                           "dense_unknowns_max": nu, "context_setup_s": setup_s,
+                           "converged_fraction": float(np.mean(r["converged"])),
+                           "mean_iterations": float(np.mean(r["iterations"])),
+                           "accepted": int(np.sum(acc)), "l2": "inputs are genomes (KB); no flush needed"},
+                "gpu_launches": int(launches),
+                "roofline": {"bound": "fp64", "kernel": "k_ac_case (one CTA per case: Newton-Raphson, dense LU)",
+                             "achieved": tflops, "peak": peak, "unit": "TFLOP/s",
+                             "frac": tflops / peak if peak else None, "traffic": None,
+                             "algorithmic": "per Newton step of every case 2/3 nu^3 (partial-pivot LU) + 12 nu^2 "
+                                            "(injections, Jacobian), nu = 2 (buses - 1); / the step time",
+                             "note": "latency-bound: the LU of a few-dozen-unknown Jacobian is a chain of "
+                                     "CTA barriers; the throughput comes from thousands of cases in flight"},
+                "e2e": {"value": value, "unit": "topologies/s", "h2d_bytes_per_step": int(genomes.nbytes),
+                        "d2h_bytes_per_step": int(n_gen * (4 + 1 + 8)),
+                        "call": "tg_ac_full_validation (AcValidator::full_validation for the batch) on host buffers"},
+                "clocks": clk.summary()}
+        if base is not None:
+            line["cpu_baseline"] = base
+        print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
-    ap.add_argument("--config", default="cfg4", choices=sorted(CONFIGS))
+    ap.add_argument("--config", default="cfg4", choices=sorted(set(CONFIGS) | set(AC_CONFIGS)))
+    ap.add_argument("--stage", default="dc", choices=["dc", "ac"],
+                    help="dc: the MapElites DC N-1 loop (north_star); ac: the AC validation stage")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rng", default="replay", choices=["replay", "philox"],
@@ -226,6 +385,9 @@ def main():
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3)
     world, rank, local = dist_setup()
+    if args.stage == "ac":
+        run_ac(args, world, rank)
+        return
     if args.impl == "reference":
         run_reference(args, world, rank)
         if world > 1:

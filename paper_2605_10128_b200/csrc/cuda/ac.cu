@@ -181,11 +181,14 @@ __device__ void lu_solve(double* J, double* dx, double* lm, int nu, double* red,
       dx[i] -= l * bk;
     }
     __syncthreads();
-    const int m = nu - k - 1;
-    for (int idx = tid; idx < m * m; idx += NT) {
-      const int i = k + 1 + idx / m, j = k + 1 + idx % m;
+    // trailing update: warps over rows, lanes over columns (row-major J, so a
+    // warp touches consecutive words)
+    const double* rk = J + static_cast<size_t>(k) * nu;
+    for (int i = k + 1 + (tid >> 5); i < nu; i += NT / 32) {
       const double l = lm[i];
-      if (l != 0.0) J[static_cast<size_t>(i) * nu + j] -= l * J[static_cast<size_t>(k) * nu + j];
+      if (l == 0.0) continue;
+      double* ri = J + static_cast<size_t>(i) * nu;
+      for (int j = k + 1 + (tid & 31); j < nu; j += 32) ri[j] -= l * rk[j];
     }
     __syncthreads();
   }

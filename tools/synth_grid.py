@@ -236,3 +236,23 @@ def config_json(name: str) -> str:
 if __name__ == "__main__":
     name = sys.argv[1] if len(sys.argv) > 1 else "cfg2"
     print(config_json(name))
+
+
+def with_ac_data(grid: dict, r_ratio: float = 0.1, charging: float = 0.02, q_ratio: float = 0.25,
+                 v_set: float = 1.02, p_scale: float = 0.5) -> dict:
+    """AC fields for a synthetic grid (the configs above are DC-only): r = r_ratio x,
+    line charging, load q = q_ratio p, generators regulate to v_set (PV buses), every
+    injection scaled by p_scale (the DC configs load their branches near the limits;
+    at full load most of them have no AC solution)."""
+    g = json.loads(json.dumps(grid))
+    for inj in g["injections"]:
+        inj["p_mw"] *= p_scale
+    for b in g["branches"]:
+        b["r_pu"] = r_ratio * b["x_pu"]
+        b["b_pu"] = charging
+    for inj in g["injections"]:
+        if inj["kind"] == "load":
+            inj["q_mvar"] = q_ratio * inj["p_mw"]
+        else:
+            inj["v_setpoint_pu"] = v_set
+    return g
