@@ -192,6 +192,11 @@ tg_status tg_build_ptdf(const tg_grid* grid, int device, double* out);
 tg_status tg_grid_describe(const tg_grid* grid, tg_grid_desc* out);
 /* build_action_set, importer.hpp:80 (EnumerationConfig seed/cap, importer.hpp:68-71) */
 tg_status tg_actionset_build(const tg_grid* grid, uint64_t seed, int64_t cap, tg_actionset** out);
+/* build_action_set with the islanding validation of every candidate split
+ * (validate_action_islanding, importer.cpp:314-339) on `device`: one CTA per split
+ * (BFS connectivity + bridges by tree-path covering); same action ids as
+ * tg_actionset_build. */
+tg_status tg_actionset_build_device(const tg_grid* grid, uint64_t seed, int64_t cap, int device, tg_actionset** out);
 /* load_action_set / save_action_set, importer.hpp:91-94 (JSON text in memory) */
 tg_status tg_actionset_from_json(const tg_grid* grid, const char* text, size_t len, tg_actionset** out);
 tg_status tg_actionset_to_json(const tg_actionset* set, const tg_grid* grid, char** text_out); /* free with tg_free */

@@ -179,9 +179,14 @@ class ActionSet:
             self._h = None
 
 
-def build_action_set(grid: GridModel, seed: int = 0, cap: int = 1 << 23) -> ActionSet:
+def build_action_set(grid: GridModel, seed: int = 0, cap: int = 1 << 23, device: Optional[int] = None) -> ActionSet:
+    """build_action_set (importer.cpp:341-356). device=None: islanding validation on the
+    host threads; device=k: on GPU k (tg_actionset_build_device). Same ids either way."""
     h = C.c_void_p()
-    _check(LIB.tg_actionset_build(grid._h, seed, cap, C.byref(h)))
+    if device is None:
+        _check(LIB.tg_actionset_build(grid._h, seed, cap, C.byref(h)))
+    else:
+        _check(LIB.tg_actionset_build_device(grid._h, seed, cap, device, C.byref(h)))
     return ActionSet(h, grid)
 
 

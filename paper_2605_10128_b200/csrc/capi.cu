@@ -390,6 +390,8 @@ void tg_context::ensure_capacity(int n) {
   b.kflag = A.alloc<uint8_t>(static_cast<size_t>(cap) * std::max<size_t>(Kp, 1));
   b.fmax = A.alloc<unsigned long long>(static_cast<size_t>(cap) * E);
   b.fbus = A.alloc<unsigned long long>(static_cast<size_t>(cap) * E);
+  // zero once: grids without busbar outages never write it (no per-evaluation reset)
+  check(cudaMemset(b.fbus, 0, static_cast<size_t>(cap) * E * sizeof(unsigned long long)), "memset");
   b.energy = A.alloc<double>(static_cast<size_t>(cap) * Ka);
   b.isl_out = A.alloc<int>(cap);
   b.isl_bus = A.alloc<int>(cap);
@@ -745,6 +747,21 @@ tg_status tg_actionset_build(const tg_grid* grid, uint64_t seed, int64_t cap, tg
   return guarded([&] {
     auto a = std::make_unique<tg_actionset>();
     a->t = tgb::build_actions(grid->g, seed, cap > 0 ? cap : (int64_t{1} << 23));
+    flatten_actions(*a, grid->g);
+    *out = a.release();
+  });
+}
+
+tg_status tg_actionset_build_device(const tg_grid* grid, uint64_t seed, int64_t cap, int device, tg_actionset** out) {
+  return guarded([&] {
+    if (device < 0) throw tgb::ConfigError("device must be >= 0");
+    auto a = std::make_unique<tg_actionset>();
+    try {
+      a->t = tgb::build_actions(grid->g, seed, cap > 0 ? cap : (int64_t{1} << 23), device);
+    } catch (const std::runtime_error& e) {
+      if (dynamic_cast<const tgb::ParseError*>(&e) || dynamic_cast<const tgb::ValidationError*>(&e)) throw;
+      throw CudaFailure(e.what());
+    }
     flatten_actions(*a, grid->g);
     *out = a.release();
   });

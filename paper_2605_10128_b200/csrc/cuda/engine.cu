@@ -1145,7 +1145,8 @@ size_t topo_core_bytes() { return sizeof(TopoCore); }
 // multi-timestep path of capi.cu interleaves them across profiles).
 int launch_eval_reset(const DevGrid& g, Batch& b, cudaStream_t stream) {
   cudaMemsetAsync(b.fmax, 0, static_cast<size_t>(b.n) * g.E * sizeof(unsigned long long), stream);
-  cudaMemsetAsync(b.fbus, 0, static_cast<size_t>(b.n) * g.E * sizeof(unsigned long long), stream);
+  if (g.Kb > 0)  // only busbar outages fold into fbus (k_special); k_finish reads it only then
+    cudaMemsetAsync(b.fbus, 0, static_cast<size_t>(b.n) * g.E * sizeof(unsigned long long), stream);
   cudaMemsetAsync(b.energy, 0, static_cast<size_t>(b.n) * g.Kall * sizeof(double), stream);
   cudaMemsetAsync(b.isl_out, 0, b.n * sizeof(int), stream);
   cudaMemsetAsync(b.isl_bus, 0, b.n * sizeof(int), stream);

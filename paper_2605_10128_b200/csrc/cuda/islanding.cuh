@@ -1,0 +1,32 @@
+// Device islanding validation of candidate station splits (islanding.cu).
+#pragma once
+
+#include <cstdint>
+#include <vector>
+
+namespace tgb {
+
+// Base branch graph and the listed contingencies (grid order).
+struct SplitGraphDesc {
+  int n_nodes = 0;
+  std::vector<int> br_from, br_to;
+  std::vector<uint8_t> br_on;
+  std::vector<int> node_ptr, node_br;    // CSR: every branch at both ends
+  std::vector<int> single_br;            // branch of each single-branch contingency
+  std::vector<int> multi_ptr{0}, multi_br;  // CSR of the multi-branch contingencies
+};
+
+// Candidate splits: split node, moved branch ends (+1 + e from end, -(1 + e)
+// to end), whether the fresh node carries a terminal that counts
+// (split_edges' new_node_used, importer.cpp:288-312).
+struct SplitCandidates {
+  std::vector<int> station_node;
+  std::vector<int> moved_ptr{0}, moved;
+  std::vector<uint8_t> fresh_used;
+};
+
+// keep[i] = validate_action_islanding (importer.cpp:314-339) of candidate i,
+// computed on `device`.
+void validate_splits_device(const SplitGraphDesc& g, const SplitCandidates& c, int device, std::vector<char>& keep);
+
+}  // namespace tgb

@@ -1,5 +1,6 @@
 // Host-side network model and import step (see model.hpp for the reference map).
 #include "model.hpp"
+#include "../cuda/islanding.cuh"
 
 #include <algorithm>
 #include <array>
@@ -640,7 +641,7 @@ bool split_keeps_connected(const Grid& g, int s, const std::vector<char>& grp) {
 }  // namespace
 
 // importer.cpp:239-282 + 341-356. Ids: station order, then enumeration order.
-ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap) {
+ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap, int device) {
   ActionTable t;
   t.disconnectables = enumerate_disconnectables(g);
   t.station_range.assign(g.stations.size(), {-1, -1});
@@ -688,7 +689,59 @@ ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap) {
   // assigned afterwards in (station, enumeration) order as the reference does
   std::vector<Realized> real(pending.size());
   std::vector<char> keep(pending.size(), 0);
-  {
+  if (device >= 0) {
+    // realization on the host, islanding validation of every realized split
+    // on the device (cuda/islanding.cu), one CTA per split
+    std::vector<char> realized(pending.size(), 0);
+    for (std::size_t i = 0; i < pending.size(); ++i)
+      realized[i] = realize(g.stations[pending[i].first], pending[i].second, real[i]);
+    SplitGraphDesc gd;
+    gd.n_nodes = g.n_nodes();
+    gd.br_from.assign(g.br_from.begin(), g.br_from.end());
+    gd.br_to.assign(g.br_to.begin(), g.br_to.end());
+    gd.br_on.assign(g.br_on.begin(), g.br_on.end());
+    std::vector<int> deg(g.n_nodes() + 1, 0);
+    for (int e = 0; e < g.n_branches(); ++e) ++deg[g.br_from[e] + 1], ++deg[g.br_to[e] + 1];
+    for (int v = 0; v < g.n_nodes(); ++v) deg[v + 1] += deg[v];
+    gd.node_ptr = deg;
+    gd.node_br.assign(deg.back(), 0);
+    {
+      std::vector<int> fill(deg.begin(), deg.end() - 1);
+      for (int e = 0; e < g.n_branches(); ++e) gd.node_br[fill[g.br_from[e]]++] = e, gd.node_br[fill[g.br_to[e]]++] = e;
+    }
+    for (const auto& brs : g.cont_branches) {
+      if (brs.size() == 1) gd.single_br.push_back(brs[0]);
+      if (brs.size() > 1) {
+        gd.multi_br.insert(gd.multi_br.end(), brs.begin(), brs.end());
+        gd.multi_ptr.push_back(static_cast<int>(gd.multi_br.size()));
+      }
+    }
+    SplitCandidates cd;
+    std::vector<std::size_t> idx;
+    for (std::size_t i = 0; i < pending.size(); ++i) {
+      if (!realized[i]) continue;
+      const Station& st = g.stations[pending[i].first];
+      const auto& grp = pending[i].second;
+      bool fresh = false;
+      for (int k = 0; k < static_cast<int>(st.term_kind.size()); ++k) {
+        if (!grp[k]) continue;
+        if (st.term_kind[k] == kInjection) {
+          fresh = true;
+          continue;
+        }
+        const int e = st.term_index[k];
+        cd.moved.push_back(st.term_kind[k] == kFromEnd ? 1 + e : -(1 + e));
+        fresh = fresh || g.br_on[e];
+      }
+      cd.moved_ptr.push_back(static_cast<int>(cd.moved.size()));
+      cd.station_node.push_back(st.node);
+      cd.fresh_used.push_back(fresh);
+      idx.push_back(i);
+    }
+    std::vector<char> ok;
+    validate_splits_device(gd, cd, device, ok);
+    for (std::size_t j = 0; j < idx.size(); ++j) keep[idx[j]] = ok[j];
+  } else {
     std::atomic<std::size_t> next{0};
     auto work = [&] {
       for (std::size_t i; (i = next.fetch_add(1)) < pending.size();) {

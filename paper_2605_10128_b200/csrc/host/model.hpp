@@ -131,7 +131,9 @@ struct ActionTable {
 std::vector<int> locality_rank(int n, const std::vector<std::pair<int, int>>& edges, int leaf = 48);
 
 std::vector<int> enumerate_disconnectables(const Grid& g);
-ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap);
+// device >= 0: the islanding validation of the candidate splits runs on that
+// GPU (cuda/islanding.cu) instead of the host threads; same ids.
+ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap, int device = -1);
 std::string actions_to_json(const ActionTable& t, const Grid& g, std::uint64_t grid_hash);
 bool actions_from_json(const std::string& text, const Grid& g, std::uint64_t grid_hash, ActionTable& out);
 // grid_model.cpp:423-485: the reference's canonical serialization (nlohmann
