@@ -131,6 +131,8 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
         v[0] = on ? __double2float_ru(fabs(row[0] - g.f0[e])) : 0.0f;
 #pragma unroll
         for (int q = 0; q + 1 < kCsum; ++q) v[1 + q] = on && q < r ? __double2float_ru(fabs(row[1 + q])) : 0.0f;
+        if (r + 2 <= kCsum)  // row-coupled chunk test slot, as in prep_branch_chunk
+          v[kCsum - 1] = on ? __double2float_ru(fabs(row[0] - g.f0[e]) - (g.br_lim[e] - fabs(g.f0[e]))) : -CUDART_INF_F;
 #pragma unroll
         for (int q = 0; q < kCsum; ++q)
 #pragma unroll
@@ -384,6 +386,10 @@ __device__ __forceinline__ void prep_branch_chunk(const DevGrid& g, const Batch&
     v[0] = on ? __double2float_ru(fabs(row[0] - g.f0[e])) : 0.0f;
 #pragma unroll
     for (int q = 0; q + 1 < kCsum; ++q) v[1 + q] = on && q < R ? __double2float_ru(fabs(row[1 + (q < R ? q : 0)])) : 0.0f;
+    // ranks <= kCsum - 2: the last slot carries max_e (|f_c - f0|_e - (lim_e - |f0_e|))
+    // for the row-coupled chunk test (setup.cu k_chunk_rec); dead rows never overload
+    if (R + 2 <= kCsum)
+      v[kCsum - 1] = on ? __double2float_ru(fabs(row[0] - g.f0[e]) - (g.br_lim[e] - fabs(g.f0[e]))) : -CUDART_INF_F;
 #pragma unroll
     for (int q = 0; q < kCsum; ++q)
 #pragma unroll

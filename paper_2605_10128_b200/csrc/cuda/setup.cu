@@ -205,7 +205,11 @@ __global__ void k_row_headroom(DevGrid g, double* h) {
 // relaxation of the row records. For every row e of the chunk and element k of
 // the tile, |f1| <= max(f0_e + D0max, -(f0_e + D0min)) + |f_c - f0|_e + w_e, so
 // a chunk whose rows all satisfy  max|f_c - f0| + max w < min_e headroom_e
-// cannot overload (sweep.cu, chunked sweep). The headroom is lowered by
+// cannot overload (sweep.cu, chunked sweep). Writing the base term as
+// |f0_e| + d_e, the same inequality also holds when
+//   max_e (|f_c - f0|_e - (lim_e - |f0_e|)) + max_e d_e + max w < 0,
+// which ties each row's flow change to its own static headroom; the record
+// carries max_e d_e for that second test. The headroom is lowered by
 // 1e-9 (lim + |f0| + |D0max| + |D0min|) over the chunk: far more than the
 // rounding of any computed f1 (FP64, a few ulps).
 __global__ void k_chunk_rec(DevGrid g, float* crec, int W, int ld) {
@@ -214,18 +218,22 @@ __global__ void k_chunk_rec(DevGrid g, float* crec, int W, int ld) {
     const int tile = idx / nch, ch = idx % nch;
     float tm[kTmaxSub];
     for (int q = 0; q < kTmaxSub; ++q) tm[q] = 0.0f;
-    double h = CUDART_INF, sl = 0.0;
+    double h = CUDART_INF, sl = 0.0, dm = 0.0;
     for (int e = ch * kChunkRows; e < min(g.E, (ch + 1) * kChunkRows); ++e) {
       const float* rec = g.Tmax + (static_cast<size_t>(tile) * ld + e) * kRec;
       for (int q = 0; q < kTmaxSub; ++q) tm[q] = fmaxf(tm[q], rec[q]);
       const double2 d0 = *reinterpret_cast<const double2*>(rec + kTmaxSub);
       const double f = g.f0[e], lim = g.br_lim[e];
-      h = fmin(h, lim - fmax(f + d0.x, -(f + d0.y)));
+      const double base = fmax(f + d0.x, -(f + d0.y));  // max_k |f0_e + T_base[e,k] alpha0_k| over the tile
+      h = fmin(h, lim - base);
+      dm = fmax(dm, base - fabs(f));
       sl = fmax(sl, fabs(lim) + fabs(f) + fabs(d0.x) + fabs(d0.y));
     }
     float* out = crec + static_cast<size_t>(idx) * kRec;
     for (int q = 0; q < kTmaxSub; ++q) out[q] = tm[q];
-    *reinterpret_cast<double2*>(out + kTmaxSub) = make_double2(h - 1e-9 * sl, 0.0);
+    // second double: the tile's largest base flow change over |f0| in the chunk,
+    // raised by the same rounding margin (the row-coupled test of the chunked sweep)
+    *reinterpret_cast<double2*>(out + kTmaxSub) = make_double2(h - 1e-9 * sl, dm + 1e-9 * sl);
   }
 }
 

@@ -1045,7 +1045,7 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
       if (ch < nch) {
         const float4* rc = reinterpret_cast<const float4*>(crec + static_cast<size_t>(ch) * kRec);
         const float4 t0 = __ldg(rc), t1 = __ldg(rc + 1);
-        const double hc = __ldg(reinterpret_cast<const double*>(rc + 2));
+        const double2 hd = __ldg(reinterpret_cast<const double2*>(rc + 2));  // (min headroom, max d_e)
         const float4 c0 = __ldg(reinterpret_cast<const float4*>(cs + static_cast<size_t>(ch) * kCsum));
         const float4 c1 = __ldg(reinterpret_cast<const float4*>(cs + static_cast<size_t>(ch) * kCsum) + 1);
         const float cv[kCsum] = {c0.x, c0.y, c0.z, c0.w, c1.x, c1.y, c1.z, c1.w};
@@ -1053,10 +1053,15 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
                                fmaxf(__fmul_ru(t0.z, af[2]), __fmul_ru(t0.w, af[3]))),
                          fmaxf(fmaxf(__fmul_ru(t1.x, af[4]), __fmul_ru(t1.y, af[5])),
                                fmaxf(__fmul_ru(t1.z, af[6]), __fmul_ru(t1.w, af[7]))));
-        float bnd = __fadd_ru(cv[0], td);
+        float wb = td;  // bound of |T_base||delta| + sum_q |L_q||R'_q| over the chunk and tile
 #pragma unroll
-        for (int q = 0; q < R; ++q) bnd = __fmaf_ru(cv[1 + q], rf[q], bnd);
-        hot = static_cast<double>(__fmul_ru(bnd, 1.000001f)) >= hc;
+        for (int q = 0; q < R; ++q) wb = __fmaf_ru(cv[1 + q], rf[q], wb);
+        const float bnd = __fadd_ru(cv[0], wb);
+        hot = static_cast<double>(__fmul_ru(bnd, 1.000001f)) >= hd.x;
+        // row-coupled test (setup.cu k_chunk_rec): safe when
+        // max_e (|f_c - f0|_e - H0_e) + max_e d_e + w < 0
+        if (R + 2 <= kCsum && hot)
+          hot = static_cast<double>(cv[kCsum - 1]) + static_cast<double>(__fmul_ru(wb, 1.000001f)) + hd.y >= 0.0;
       }
       const unsigned m = __ballot_sync(0xffffffffu, hot);
       if (hot) list[nlist + __popc(m & ((1u << lane) - 1))] = static_cast<uint16_t>(ch);
