@@ -53,6 +53,19 @@ __global__ void __launch_bounds__(kAnalyzeThreads) k_analyze(DevGrid g, Batch b,
 // One CTA per candidate (grid-stride over candidates). Z = X [U | V] lives in
 // the CTA's global scratch slot (row stride row_stride(r); L2-resident at cfg2:
 // keeping it in shared memory measured slower, 2 CTAs per SM either way).
+// Warp-wide maximum of a chunk summary, one REDUX per slot: floats compared
+// through an order-preserving unsigned key (non-negative floats are their bit
+// patterns; the last slot may be negative or -inf).
+__device__ __forceinline__ void warp_max_summary(float (&v)[kCsum]) {
+#pragma unroll
+  for (int q = 0; q < kCsum; ++q) {
+    const unsigned b = __float_as_uint(v[q]);
+    const unsigned key = (b >> 31) ? ~b : (b | 0x80000000u);
+    const unsigned m = __reduce_max_sync(0xffffffffu, key);
+    v[q] = __uint_as_float((m >> 31) ? (m & 0x7fffffffu) : ~m);
+  }
+}
+
 __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, int n_d, double* zscratch) {
   extern __shared__ __align__(16) uint32_t bits[];
   __shared__ Topo t;
@@ -133,10 +146,7 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
         for (int q = 0; q + 1 < kCsum; ++q) v[1 + q] = on && q < r ? __double2float_ru(fabs(row[1 + q])) : 0.0f;
         if (r + 2 <= kCsum)  // row-coupled chunk test slot, as in prep_branch_chunk
           v[kCsum - 1] = on ? __double2float_ru(fabs(row[0] - g.f0[e]) - (g.br_lim[e] - fabs(g.f0[e]))) : -CUDART_INF_F;
-#pragma unroll
-        for (int q = 0; q < kCsum; ++q)
-#pragma unroll
-          for (int o = 16; o > 0; o >>= 1) v[q] = fmaxf(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+        warp_max_summary(v);
         if ((threadIdx.x & 31) == 0) {
           float4* dst = reinterpret_cast<float4*>(csum + static_cast<size_t>(e0 >> 5) * kCsum);
           dst[0] = make_float4(v[0], v[1], v[2], v[3]);
@@ -390,10 +400,7 @@ __device__ __forceinline__ void prep_branch_chunk(const DevGrid& g, const Batch&
     // for the row-coupled chunk test (setup.cu k_chunk_rec); dead rows never overload
     if (R + 2 <= kCsum)
       v[kCsum - 1] = on ? __double2float_ru(fabs(row[0] - g.f0[e]) - (g.br_lim[e] - fabs(g.f0[e]))) : -CUDART_INF_F;
-#pragma unroll
-    for (int q = 0; q < kCsum; ++q)
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) v[q] = fmaxf(v[q], __shfl_xor_sync(0xffffffffu, v[q], o));
+    warp_max_summary(v);
     if (lane == 0) {
       float4* dst = reinterpret_cast<float4*>(b.csum + (static_cast<size_t>(c) * b.nchunks + chunk) * kCsum);
       dst[0] = make_float4(v[0], v[1], v[2], v[3]);
