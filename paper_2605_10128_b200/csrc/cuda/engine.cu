@@ -849,109 +849,23 @@ __device__ __forceinline__ bool worst_before(double v, int k, double u, int j) {
 }
 
 // One warp: the first wk entries with energy > 0 of en[0..K) in the order
-// (energy desc, index asc). Positive energies are compacted into the warp's
-// shared list (lv, li; kFinishList entries), selection rounds then scan the
-// list (or all K when it overflows).
-__device__ void warp_worst(const double* en, int K, int wk, double* lv, int* li, int* out_idx, double* out_val,
-                           int* out_n, int lane) {
-  int npos = 0;
-  unsigned long long maxbits = 0ull;  // positive doubles order like their bit patterns
-  for (int k0 = 0; k0 < K; k0 += 128) {
-    double vv[4];  // four blocks of 32 in flight, compacted in index order
-#pragma unroll
-    for (int u = 0; u < 4; ++u) vv[u] = k0 + 32 * u + lane < K ? en[k0 + 32 * u + lane] : 0.0;
-#pragma unroll
-    for (int u = 0; u < 4; ++u) {
-      const int k = k0 + 32 * u + lane;
-      const double v = vv[u];
-      const unsigned m = __ballot_sync(0xffffffffu, v > 0.0);
-      const int at = npos + __popc(m & ((1u << lane) - 1u));
-      if (v > 0.0) {
-        if (at < kFinishList) lv[at] = v, li[at] = k;
-        maxbits = max(maxbits, static_cast<unsigned long long>(__double_as_longlong(v)));
-      }
-      npos += __popc(m);
-    }
-  }
-  __syncwarp();
-  bool listed = npos <= kFinishList;
-  int n_scan = listed ? npos : K;
-  if (!listed) {
-    // Too many positive energies for the list: a histogram over (exponent, 3
-    // mantissa bits) below the maximum finds the bucket holding the wk-th
-    // largest; only entries at or above it are collected (3 passes over K
-    // instead of wk).
-    for (int o = 16; o > 0; o >>= 1) maxbits = max(maxbits, __shfl_xor_sync(0xffffffffu, maxbits, o));
-    const long long maxkey = static_cast<long long>(maxbits >> 49);
-    int* hist = li;  // kFinishList >= 256 buckets
-    for (int i = lane; i < 256; i += 32) hist[i] = 0;
-    __syncwarp();
-    for (int k = lane; k < K; k += 32) {
-      const double v = en[k];
-      if (!(v > 0.0)) continue;
-      const long long d = maxkey - static_cast<long long>(static_cast<unsigned long long>(__double_as_longlong(v)) >> 49);
-      atomicAdd(&hist[d < 255 ? d : 255], 1);
-    }
-    __syncwarp();
-    int local = 0;
-#pragma unroll
-    for (int q = 0; q < 8; ++q) local += hist[lane * 8 + q];
-    int incl = local;
-#pragma unroll
-    for (int o = 1; o < 32; o <<= 1) {
-      const int y = __shfl_up_sync(0xffffffffu, incl, o);
-      if (lane >= o) incl += y;
-    }
-    const int excl = incl - local;
-    int jb = 255, cum = npos;  // bucket of the wk-th largest, count at or above it
-    if (excl < wk && incl >= wk) {
-      int run = excl;
-      for (int q = 0; q < 8; ++q) {
-        run += hist[lane * 8 + q];
-        if (run >= wk) {
-          jb = lane * 8 + q;
-          cum = run;
-          break;
-        }
-      }
-    }
-    const unsigned who = __ballot_sync(0xffffffffu, excl < wk && incl >= wk);
-    if (who) {
-      const int src = __ffs(who) - 1;
-      jb = __shfl_sync(0xffffffffu, jb, src);
-      cum = __shfl_sync(0xffffffffu, cum, src);
-    }
-    __syncwarp();
-    if (cum <= kFinishList) {
-      int n = 0;
-      for (int k0 = 0; k0 < K; k0 += 32) {
-        const int k = k0 + lane;
-        const double v = k < K ? en[k] : 0.0;
-        bool take = false;
-        if (v > 0.0) {
-          const long long d =
-              maxkey - static_cast<long long>(static_cast<unsigned long long>(__double_as_longlong(v)) >> 49);
-          take = (d < 255 ? d : 255) <= jb;
-        }
-        const unsigned m = __ballot_sync(0xffffffffu, take);
-        const int at = n + __popc(m & ((1u << lane) - 1u));
-        if (take) lv[at] = v, li[at] = k;
-        n += __popc(m);
-      }
-      __syncwarp();
-      listed = true;
-      n_scan = n;
-    }
-  }
+// (energy desc, index asc) -- the reference's worst list (dc_engine.cpp:398-419).
+// One pass over en: positive energies are appended to the warp's shared list
+// (lv, li; kFinishList entries); when the list would overflow it is cut to its
+// wk best entries, and from then on only entries ranked before the wk-th best
+// seen so far are appended (later indices lose ties, so "before" is a strict
+// energy comparison there). Selection rounds then rank the list.
+__device__ void warp_select(const double* lv, const int* li, int n, int wk, int lane, int* sel_idx, double* sel_val,
+                            int* n_sel, double* last_v, int* last_i) {
   double pv = CUDART_INF;
   int pi = -1, nsel = 0;
   for (int round = 0; round < wk; ++round) {
     double bv = 0.0;
     int bi = -1;
-    for (int i = lane; i < n_scan; i += 32) {
-      const double v = listed ? lv[i] : en[i];
-      const int k = listed ? li[i] : i;
-      if (!(v > 0.0) || !worst_before(pv, pi, v, k)) continue;  // already selected
+    for (int i = lane; i < n; i += 32) {
+      const double v = lv[i];
+      const int k = li[i];
+      if (!worst_before(pv, pi, v, k)) continue;  // already selected
       if (bi < 0 || worst_before(v, k, bv, bi)) bv = v, bi = k;
     }
 #pragma unroll
@@ -961,11 +875,100 @@ __device__ void warp_worst(const double* en, int K, int wk, double* lv, int* li,
       if (oi >= 0 && (bi < 0 || worst_before(ov, oi, bv, bi))) bv = ov, bi = oi;
     }
     if (bi < 0) break;
-    if (lane == 0) out_idx[round] = bi, out_val[round] = bv;
+    if (sel_idx && lane == 0) sel_idx[round] = bi, sel_val[round] = bv;
     pv = bv;
     pi = bi;
     ++nsel;
   }
+  *n_sel = nsel;
+  *last_v = pv;
+  *last_i = pi;
+}
+
+__device__ void warp_worst(const double* en, int K, int wk, double* lv, int* li, int* out_idx, double* out_val,
+                           int* out_n, int lane) {
+  if (2 * wk > kFinishList) {  // long worst lists: rank the energies in place (no list)
+    double pv = CUDART_INF;
+    int pi = -1, nsel = 0;
+    for (int round = 0; round < wk; ++round) {
+      double bv = 0.0;
+      int bi = -1;
+      for (int k = lane; k < K; k += 32) {
+        const double v = en[k];
+        if (!(v > 0.0) || !worst_before(pv, pi, v, k)) continue;
+        if (bi < 0 || worst_before(v, k, bv, bi)) bv = v, bi = k;
+      }
+#pragma unroll
+      for (int d = 16; d > 0; d >>= 1) {
+        const double ov = __shfl_xor_sync(0xffffffffu, bv, d);
+        const int oi = __shfl_xor_sync(0xffffffffu, bi, d);
+        if (oi >= 0 && (bi < 0 || worst_before(ov, oi, bv, bi))) bv = ov, bi = oi;
+      }
+      if (bi < 0) break;
+      if (lane == 0) out_idx[round] = bi, out_val[round] = bv;
+      pv = bv;
+      pi = bi;
+      ++nsel;
+    }
+    if (lane == 0) *out_n = nsel;
+    return;
+  }
+  int npos = 0;
+  double tv = 0.0;  // entries must rank before (tv, ti); ti < 0: any positive energy
+  int ti = -1;
+  for (int k0 = 0; k0 < K; k0 += 128) {
+    double vv[4];  // four blocks of 32 in flight
+#pragma unroll
+    for (int u = 0; u < 4; ++u) vv[u] = k0 + 32 * u + lane < K ? en[k0 + 32 * u + lane] : 0.0;
+#pragma unroll
+    for (int u = 0; u < 4; ++u) {
+      const int k = k0 + 32 * u + lane;
+      const double v = vv[u];
+      bool take = v > 0.0 && (ti < 0 || worst_before(v, k, tv, ti));
+      unsigned m = __ballot_sync(0xffffffffu, take);
+      if (npos + __popc(m) > kFinishList) {
+        // cut the list to its wk best entries (stable, in place: writes trail reads)
+        __syncwarp();
+        int ns;
+        warp_select(lv, li, npos, wk, lane, nullptr, nullptr, &ns, &tv, &ti);
+        int kept = 0;
+        for (int i0 = 0; i0 < npos; i0 += 32) {
+          const int i = i0 + lane;
+          double x = 0.0;
+          int xi = 0;
+          bool keep = false;
+          if (i < npos) {
+            x = lv[i];
+            xi = li[i];
+            keep = ti >= 0 && !worst_before(tv, ti, x, xi);  // ranked at or before the wk-th best
+          }
+          const unsigned km = __ballot_sync(0xffffffffu, keep);
+          if (keep) {
+            const int at = kept + __popc(km & ((1u << lane) - 1u));
+            lv[at] = x;
+            li[at] = xi;
+          }
+          kept += __popc(km);
+        }
+        __syncwarp();
+        npos = kept;
+        if (ti < 0) npos = 0;  // wk == 0: nothing is ever kept
+        take = v > 0.0 && ti >= 0 && worst_before(v, k, tv, ti);
+        m = __ballot_sync(0xffffffffu, take);
+      }
+      if (take) {
+        const int at = npos + __popc(m & ((1u << lane) - 1u));
+        lv[at] = v;
+        li[at] = k;
+      }
+      npos += __popc(m);
+    }
+  }
+  __syncwarp();
+  int nsel;
+  double lvv;
+  int lii;
+  warp_select(lv, li, npos, wk, lane, out_idx, out_val, &nsel, &lvv, &lii);
   if (lane == 0) *out_n = nsel;
 }
 
