@@ -1189,8 +1189,9 @@ int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch&
     if (b.n == 0) return 0;
     k_prep_solve<<<b.n < 65535 ? b.n : 65535, 32, 0, stream>>>(g, b);
     k_prep_rows<0, 4><<<148 * 8, 256, 0, stream>>>(g, b);
-    k_prep_rows<5, kSweepRank><<<148 * 8, 256, 0, stream>>>(g, b);
-    return 3;
+    k_prep_rows<5, kChunkedMaxRank><<<148 * 8, 256, 0, stream>>>(g, b);  // without the rank 8-11 registers
+    k_prep_rows<kChunkedMaxRank + 1, kSweepRank><<<148 * 8, 256, 0, stream>>>(g, b);
+    return 4;
   }
   const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
   if (bits_bytes > 48 * 1024)  // (per launch: the size depends on the grid)
