@@ -516,7 +516,7 @@ __device__ __forceinline__ void prep_segment_dispatch(const DevGrid& g, const Ba
 // Ranks [RLO, RHI] from the rank buckets of k_bucket (one register allocation
 // per class; the classes run as separate launches).
 template <int RLO, int RHI>
-__global__ void __launch_bounds__(32 * kPrepRowWarps, RHI <= 4 ? 4 : 2) k_prep_rows(DevGrid g, Batch b) {
+__global__ void __launch_bounds__(32 * kPrepRowWarps, RHI <= 4 ? 4 : (RHI <= 7 ? 3 : 2)) k_prep_rows(DevGrid g, Batch b) {
   __shared__ PcFac slab[kPrepRowWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PcFac& f = slab[warp];
