@@ -183,6 +183,8 @@ tg_status tg_grid_to_json(const tg_grid* grid, char** text_out);
 /* grid_content_hash, grid_model.cpp:494-503: FNV-1a of the canonical dump, the
  * key of the action cache (importer.cpp:407-479) */
 tg_status tg_grid_content_hash(const tg_grid* grid, uint64_t* hash);
+/* Branch id string of branch e (grid_model.hpp:37 Branch::id); valid while the grid lives. NULL if e is out of range. */
+const char* tg_grid_branch_id(const tg_grid* grid, int32_t e);
 /* build_ptdf, importer.cpp:358-401 (PTDFMatrix::sensitivities): computed on
  * `device` from the device inverse of B_red; out [n_branches][n_nodes]
  * row-major, slack column and out-of-service rows zero. SingularSystem on a

@@ -12,6 +12,8 @@
  *   genome.hpp:13-46         Genome (canonical_key, counts), genome_valid, genome_distance
  *   dc_engine.hpp:16-150     DcConfig, ScoreVector, FlowResult, DcContext::{evaluate,
  *                            evaluate_batch, evaluate_flows, pre_optimization_score, lambda_b_pre}
+ *   ac_validator.hpp:18-140  AcConfig, AcCaseResult, RejectionReason, ValidationRecord, Candidate,
+ *                            EliminationOutcome, AcValidator (GPU batches), record_to_json
  *   qd_optimizer.hpp:15-118  QdConfig, cell_count, descriptor_to_cell, RepertoireEntry,
  *                            Repertoire (read side), SnapshotEntry, RepertoireSnapshot,
  *                            SnapshotSink, OptimizerStats, OptimizerResult, run_optimizer
@@ -29,6 +31,7 @@
 #include <array>
 #include <atomic>
 #include <chrono>
+#include <cmath>
 #include <cstdint>
 #include <filesystem>
 #include <fstream>
@@ -411,6 +414,279 @@ class DcContext {
   ScoreVector pre_score_;
   double lambda_b_pre_ = 0.0;
 };
+
+
+// ---- ac_validator.hpp:18-140 ---------------------------------------------------
+// The AC validation stage on the GPU (tg_ac_*): every power flow of a call is
+// solved in one batch, one CTA per (genome, contingency) case. eliminate() and
+// the validation history are host logic, as in the reference.
+struct AcConfig {
+  double tolerance_pu = 1e-6;
+  int max_iterations = 30;
+  int worst_k_nonconverged = 2;
+  double nonconverged_fraction = 0.05;
+  int similarity_distance = 1;
+  double dominance_fitness_frac = 0.01;
+  double improvement_threshold_frac = 0.05;
+};
+
+struct AcCaseResult {
+  bool converged = false;
+  int iterations = 0;
+  std::vector<double> loading_mva;  // per branch, MVA
+  std::vector<double> vm_pu, va_rad;  // per bus (base nodes, then split sections)
+};
+
+enum class RejectionReason {
+  None, Nonconvergence, OverloadNotImproved, CriticalCountIncreased,
+  EliminatedSimilar, EliminatedDominated, EliminatedBelowThreshold,
+};
+inline std::string to_string(RejectionReason r) {
+  static const char* names[] = {"none", "nonconvergence", "overload_not_improved", "critical_count_increased",
+                                "eliminated_similar", "eliminated_dominated", "eliminated_below_threshold"};
+  return names[static_cast<int>(r)];
+}
+enum class ValidationStage { None, WorstK, FullN1 };
+
+struct ValidationRecord {
+  Genome genome;
+  ScoreVector dc_score;
+  ValidationStage stage = ValidationStage::None;
+  bool accepted = false;
+  RejectionReason reason = RejectionReason::None;
+  double ac_lambda_o = 0.0;
+};
+struct Candidate {
+  Genome genome;
+  ScoreVector dc_score;
+};
+struct EliminationOutcome {
+  std::vector<int> queue;
+  std::vector<std::pair<int, RejectionReason>> pruned;
+};
+
+class AcValidator {
+ public:
+  AcValidator(const GridModel& grid, const ActionSet& actions, const DcContext& dc, AcConfig config = {},
+              int device = 0)
+      : grid_(grid), actions_(actions), config_(config) {
+    const tg_ac_config c{config.tolerance_pu, config.max_iterations, config.worst_k_nonconverged,
+                         config.nonconverged_fraction, config.similarity_distance, config.dominance_fitness_frac,
+                         config.improvement_threshold_frac};
+    check(tg_ac_context_create(grid.handle(), actions.handle(), dc.handle(), &c, device, &h_));
+    tg_ac_baseline b{};
+    check(tg_ac_baseline_get(h_, &b, nullptr, nullptr));
+    baseline_lambda_o_ = b.lambda_o;
+    baseline_critical_ = b.critical_count;
+    pre_fitness_ = dc.pre_optimization_score().fitness;
+  }
+  ~AcValidator() {
+    if (h_) tg_ac_context_destroy(h_);
+  }
+  AcValidator(const AcValidator&) = delete;
+  AcValidator& operator=(const AcValidator&) = delete;
+
+  const AcConfig& config() const { return config_; }
+  double baseline_lambda_o() const { return baseline_lambda_o_; }
+  int baseline_critical_count() const { return baseline_critical_; }
+  tg_ac_context* handle() const { return h_; }
+
+  // AcNetwork(grid, apply_genome(genome)).run_case(k) for every k (-1 = base case)
+  std::vector<AcCaseResult> run_cases(const Genome& g, const std::vector<int>& contingencies) const {
+    int na = static_cast<int>(g.action_slots.size()), nd = static_cast<int>(g.disconnection_slots.size());
+    std::vector<int32_t> flat(g.action_slots.begin(), g.action_slots.end());
+    flat.insert(flat.end(), g.disconnection_slots.begin(), g.disconnection_slots.end());
+    const int n = static_cast<int>(contingencies.size()), E = grid_.n_branches(), V = grid_.n_nodes() + na;
+    std::vector<int32_t> cg(n, 0), ck(contingencies.begin(), contingencies.end());
+    std::vector<uint8_t> conv(n);
+    std::vector<int32_t> it(n);
+    std::vector<double> load(static_cast<size_t>(n) * E), vm(static_cast<size_t>(n) * V), va(vm.size());
+    tg_ac_case_out o{conv.data(), it.data(), nullptr, nullptr, load.data(), vm.data(), va.data()};
+    if (n) check(tg_ac_run_cases(h_, flat.data(), 1, na, nd, cg.data(), ck.data(), n, &o));
+    std::vector<AcCaseResult> out(n);
+    for (int i = 0; i < n; ++i) {
+      out[i].converged = conv[i] != 0;
+      out[i].iterations = it[i];
+      out[i].loading_mva.assign(load.begin() + static_cast<size_t>(i) * E, load.begin() + static_cast<size_t>(i + 1) * E);
+      out[i].vm_pu.assign(vm.begin() + static_cast<size_t>(i) * V, vm.begin() + static_cast<size_t>(i + 1) * V);
+      out[i].va_rad.assign(va.begin() + static_cast<size_t>(i) * V, va.begin() + static_cast<size_t>(i + 1) * V);
+    }
+    return out;
+  }
+  AcCaseResult run_case(const Genome& g, int contingency) const { return run_cases(g, {contingency}).front(); }
+
+  // ac_validator.cpp:345-397
+  EliminationOutcome eliminate(const std::vector<Candidate>& cands) const {
+    const double eps = config_.dominance_fitness_frac * std::abs(pre_fitness_);
+    const double theta = config_.improvement_threshold_frac * std::abs(pre_fitness_);
+    auto swd = [](const ScoreVector& s) { return s.lambda_d + s.lambda_s + s.lambda_r; };
+    EliminationOutcome out;
+    for (int i = 0; i < static_cast<int>(cands.size()); ++i) {
+      const Candidate& c = cands[i];
+      auto dominated_by = [&](int osw, double ofit) { return osw < swd(c.dc_score) && ofit >= c.dc_score.fitness - eps; };
+      RejectionReason why = RejectionReason::None;
+      for (const auto& v : validated_)
+        if (genome_distance(c.genome, v.genome) <= config_.similarity_distance) {
+          why = RejectionReason::EliminatedSimilar;
+          break;
+        }
+      if (why == RejectionReason::None)
+        for (const Candidate& o : cands)
+          if (dominated_by(swd(o.dc_score), o.dc_score.fitness)) {
+            why = RejectionReason::EliminatedDominated;
+            break;
+          }
+      if (why == RejectionReason::None)
+        for (const auto& v : validated_)
+          if (dominated_by(v.swd, v.fitness)) {
+            why = RejectionReason::EliminatedDominated;
+            break;
+          }
+      if (why == RejectionReason::None &&
+          (!std::isfinite(c.dc_score.fitness) || c.dc_score.fitness - pre_fitness_ < theta))
+        why = RejectionReason::EliminatedBelowThreshold;
+      if (why == RejectionReason::None)
+        out.queue.push_back(i);
+      else
+        out.pruned.emplace_back(i, why);
+    }
+    std::sort(out.queue.begin(), out.queue.end(), [&](int a, int b) {
+      if (cands[a].dc_score.fitness != cands[b].dc_score.fitness) return cands[a].dc_score.fitness > cands[b].dc_score.fitness;
+      return cands[a].genome.canonical_key() < cands[b].genome.canonical_key();
+    });
+    return out;
+  }
+
+  // ac_validator.cpp:399-425, for a batch of genomes (one device batch)
+  std::vector<RejectionReason> worst_k_check(const std::vector<Candidate>& cs) const {
+    if (cs.empty()) return {};
+    int na = 0, nd = 0, wk = 1;
+    for (const Candidate& c : cs) {
+      na = std::max(na, static_cast<int>(c.genome.action_slots.size()));
+      nd = std::max(nd, static_cast<int>(c.genome.disconnection_slots.size()));
+      wk = std::max(wk, static_cast<int>(c.dc_score.worst_contingencies.size()));
+    }
+    const int n = static_cast<int>(cs.size());
+    std::vector<int32_t> flat = pad(cs, na, nd), wi(static_cast<size_t>(n) * wk, -1), wn(n), reason(n);
+    for (int i = 0; i < n; ++i) {
+      wn[i] = static_cast<int32_t>(cs[i].dc_score.worst_contingencies.size());
+      for (int j = 0; j < wn[i]; ++j) wi[static_cast<size_t>(i) * wk + j] = cs[i].dc_score.worst_contingencies[j].first;
+    }
+    check(tg_ac_worst_k_check(h_, flat.data(), n, na, nd, wi.data(), wn.data(), wk, reason.data()));
+    std::vector<RejectionReason> out(n);
+    for (int i = 0; i < n; ++i) out[i] = static_cast<RejectionReason>(reason[i]);
+    return out;
+  }
+  RejectionReason worst_k_check(const Genome& g, const ScoreVector& s) const { return worst_k_check({{g, s}}).front(); }
+
+  // ac_validator.cpp:427-473, for a batch of genomes (one device batch)
+  std::vector<ValidationRecord> full_validation(const std::vector<Candidate>& cs) const {
+    if (cs.empty()) return {};
+    int na = 0, nd = 0;
+    for (const Candidate& c : cs) {
+      na = std::max(na, static_cast<int>(c.genome.action_slots.size()));
+      nd = std::max(nd, static_cast<int>(c.genome.disconnection_slots.size()));
+    }
+    const int n = static_cast<int>(cs.size());
+    std::vector<int32_t> flat = pad(cs, na, nd), reason(n);
+    std::vector<uint8_t> acc(n);
+    std::vector<double> lo(n);
+    check(tg_ac_full_validation(h_, flat.data(), n, na, nd, reason.data(), acc.data(), lo.data()));
+    std::vector<ValidationRecord> out(n);
+    for (int i = 0; i < n; ++i)
+      out[i] = {cs[i].genome, cs[i].dc_score, ValidationStage::FullN1, acc[i] != 0,
+                static_cast<RejectionReason>(reason[i]), lo[i]};
+    return out;
+  }
+  ValidationRecord full_validation(const Genome& g, const ScoreVector& s) const { return full_validation({{g, s}}).front(); }
+
+  // validate() for each candidate in order (ac_validator.cpp:475-495): the
+  // worst-k stage of all of them as one device batch, the full N-1 stage of
+  // the survivors as a second; the records equal a loop of validate calls.
+  std::vector<ValidationRecord> validate_queue(const std::vector<Candidate>& cs) {
+    for (const Candidate& c : cs)
+      validated_.push_back({c.genome, c.dc_score.lambda_d + c.dc_score.lambda_s + c.dc_score.lambda_r, c.dc_score.fitness});
+    const std::vector<RejectionReason> early = worst_k_check(cs);
+    std::vector<Candidate> go;
+    for (size_t i = 0; i < cs.size(); ++i)
+      if (early[i] == RejectionReason::None) go.push_back(cs[i]);
+    const std::vector<ValidationRecord> full = full_validation(go);
+    std::vector<ValidationRecord> out;
+    size_t j = 0;
+    for (size_t i = 0; i < cs.size(); ++i) {
+      if (early[i] == RejectionReason::None)
+        out.push_back(full[j++]);
+      else
+        out.push_back({cs[i].genome, cs[i].dc_score, ValidationStage::WorstK, false, early[i], 0.0});
+      records_.push_back(out.back());
+    }
+    return out;
+  }
+  ValidationRecord validate(const Candidate& c) { return validate_queue({c}).front(); }
+  void record_elimination(const Candidate& c, RejectionReason reason) {
+    records_.push_back({c.genome, c.dc_score, ValidationStage::None, false, reason, 0.0});
+  }
+  const std::vector<ValidationRecord>& records() const { return records_; }
+  const GridModel& grid() const { return grid_; }
+  const ActionSet& actions() const { return actions_; }
+
+ private:
+  static std::vector<int32_t> pad(const std::vector<Candidate>& cs, int na, int nd) {
+    std::vector<int32_t> flat;
+    for (const Candidate& c : cs) {
+      flat.insert(flat.end(), c.genome.action_slots.begin(), c.genome.action_slots.end());
+      flat.insert(flat.end(), na - c.genome.action_slots.size(), -1);
+      flat.insert(flat.end(), c.genome.disconnection_slots.begin(), c.genome.disconnection_slots.end());
+      flat.insert(flat.end(), nd - c.genome.disconnection_slots.size(), -1);
+    }
+    return flat;
+  }
+  struct Validated {
+    Genome genome;
+    int swd = 0;
+    double fitness = 0.0;
+  };
+  GridModel grid_;
+  ActionSet actions_;
+  AcConfig config_;
+  tg_ac_context* h_ = nullptr;
+  double baseline_lambda_o_ = 0.0, pre_fitness_ = 0.0;
+  int baseline_critical_ = 0;
+  std::vector<Validated> validated_;
+  std::vector<ValidationRecord> records_;
+};
+
+// ac_validator.cpp:497-534 (nlohmann ordered_json dump: compact, key order kept)
+inline std::string record_to_json(const ValidationRecord& r, const GridModel& grid, const ActionSet& actions) {
+  std::ostringstream o;
+  o.precision(17);
+  auto ids = [](std::vector<int> v) {
+    std::sort(v.begin(), v.end());
+    return v;
+  };
+  std::vector<int> acts, discs;
+  for (int a : r.genome.action_slots)
+    if (a >= 0) acts.push_back(a);
+  for (int d : r.genome.disconnection_slots)
+    if (d >= 0) discs.push_back(d);
+  o << "{\"actions\":[";
+  bool first = true;
+  for (int a : ids(acts)) o << (first ? "" : ",") << a, first = false;
+  o << "],\"disconnections\":[";
+  first = true;
+  for (int d : ids(discs)) {
+    const char* id = tg_grid_branch_id(grid.handle(), actions.disconnectable(d));
+    o << (first ? "" : ",") << '"' << (id ? id : "") << '"';
+    first = false;
+  }
+  const double fit = std::isfinite(r.dc_score.fitness) ? r.dc_score.fitness : -1e30;
+  const char* stage = r.stage == ValidationStage::None ? "eliminated" : r.stage == ValidationStage::WorstK ? "worst_k" : "full_n1";
+  o << "],\"lambda_d\":" << r.dc_score.lambda_d << ",\"lambda_s\":" << r.dc_score.lambda_s
+    << ",\"lambda_r\":" << r.dc_score.lambda_r << ",\"dc_fitness\":" << fit << ",\"dc_lambda_o\":" << r.dc_score.lambda_o
+    << ",\"stage\":\"" << stage << "\",\"verdict\":\"" << (r.accepted ? "accepted" : "rejected")
+    << "\",\"reason\":\"" << (r.accepted ? "" : to_string(r.reason)) << "\",\"ac_lambda_o\":" << r.ac_lambda_o << "}";
+  return o.str();
+}
 
 // ---- qd_optimizer.hpp:15-118 -------------------------------------------------
 struct QdConfig {

@@ -105,6 +105,7 @@ SIGNATURES = [
     ("tg_grid_describe", C.c_int, [C.c_void_p, C.POINTER(GridDesc)]),
     ("tg_grid_to_json", C.c_int, [C.c_void_p, C.POINTER(C.c_void_p)]),
     ("tg_grid_content_hash", C.c_int, [C.c_void_p, C.POINTER(C.c_uint64)]),
+    ("tg_grid_branch_id", C.c_char_p, [C.c_void_p, C.c_int32]),
     ("tg_build_ptdf", C.c_int, [C.c_void_p, C.c_int, C.POINTER(C.c_double)]),
     ("tg_actionset_build", C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.POINTER(C.c_void_p)]),
     ("tg_actionset_build_device", C.c_int, [C.c_void_p, C.c_uint64, C.c_int64, C.c_int, C.POINTER(C.c_void_p)]),

@@ -709,6 +709,11 @@ tg_status tg_grid_content_hash(const tg_grid* grid, uint64_t* hash) {
   return guarded([&] { *hash = tgb::grid_content_hash(grid->g); });
 }
 
+const char* tg_grid_branch_id(const tg_grid* grid, int32_t e) {
+  if (!grid || e < 0 || e >= grid->g.n_branches()) return nullptr;
+  return grid->g.branch_id[e].c_str();
+}
+
 tg_status tg_grid_describe(const tg_grid* h, tg_grid_desc* d) {
   return guarded([&] {
     const tgb::Grid& g = h->g;

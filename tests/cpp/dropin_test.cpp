@@ -226,6 +226,40 @@ static void gpu_checks(const std::filesystem::path& golden, const std::filesyste
   CHECK(throws<tb::ConfigError>([&] { tb::run_optimizer(ctx, bad, {}); }));
   // a sink exception propagates to the caller (no exception crosses the C ABI)
   CHECK(throws<std::logic_error>([&] { tb::run_optimizer(ctx, q, [](tb::RepertoireSnapshot) { throw std::logic_error("x"); }); }));
+  // AcValidator (ac_validator.hpp:93-140) on the GPU: baseline, worst-k and full
+  // N-1 verdicts of the golden genomes (compared with the oracle by the caller),
+  // the unchanged topology never improves on itself, validate_queue == stages
+  {
+    tb::AcValidator val(g, a, ctx);
+    CHECK(val.baseline_lambda_o() > 0.0 && val.baseline_critical_count() >= 0);
+    std::vector<tb::Candidate> cs;
+    for (size_t i = 0; i < gs.size(); ++i) cs.push_back({gs[i], sc[i]});
+    const auto wk = val.worst_k_check(cs);
+    const auto full = val.full_validation(cs);
+    CHECK(wk.size() == cs.size() && full.size() == cs.size());
+    CHECK(val.worst_k_check(tb::Genome::empty(3, 2), sc[0]) == tb::RejectionReason::OverloadNotImproved);
+    const tb::AcCaseResult base = val.run_case(tb::Genome::empty(3, 2), -1);
+    CHECK(base.converged && base.iterations > 0 && static_cast<int>(base.loading_mva.size()) == g.n_branches());
+    const auto recs = val.validate_queue(cs);
+    for (size_t i = 0; i < cs.size(); ++i) {
+      if (wk[i] == tb::RejectionReason::None)
+        CHECK(recs[i].stage == tb::ValidationStage::FullN1 && recs[i].reason == full[i].reason);
+      else
+        CHECK(recs[i].stage == tb::ValidationStage::WorstK && recs[i].reason == wk[i]);
+    }
+    CHECK(val.records().size() == cs.size());
+    const json rj = json::parse(tb::record_to_json(full[0], g, a));
+    CHECK(rj["stage"] == "full_n1" && rj.contains("ac_lambda_o") && rj.contains("verdict"));
+    json acj;
+    acj["baseline_lambda_o"] = val.baseline_lambda_o();
+    acj["baseline_critical"] = val.baseline_critical_count();
+    for (size_t i = 0; i < cs.size(); ++i) {
+      acj["worst_k"].push_back(static_cast<int>(wk[i]));
+      acj["full_reason"].push_back(static_cast<int>(full[i].reason));
+      acj["full_lambda_o"].push_back(full[i].ac_lambda_o);
+    }
+    out["ac"] = acj;
+  }
   std::ofstream(out_path) << out.dump() << "\n";
 }
 

@@ -8,7 +8,9 @@ the C ABI) driven from a compiled C++ test binary (tests/cpp/dropin_test.cpp):
   golden vectors (1e-9), mixed slot counts in one batch, pre-optimization
   score, run_optimizer with a sink, the std::atomic<bool> stop flag,
   ConfigError and sink exceptions; the optimizer run is compared here with the
-  oracle's run_optimizer (qd_optimizer.cpp:344-417).
+  oracle's run_optimizer (qd_optimizer.cpp:344-417); AcValidator (baseline,
+  worst-k and full N-1 verdicts of the golden genomes, validate_queue) against the
+  oracle's ac_validator.cpp restatement.
 """
 import json
 import os
@@ -47,3 +49,20 @@ def test_cpp_dropin_gpu(tmp_path):
     assert got["evaluations"] == ref["stats"]["evaluations"] == 3201
     assert got["epochs"] == ref["stats"]["epochs"] == got["n_snapshots"]
     assert abs(got["best_fitness"] - ref["snapshots"][-1]["best_fitness"]) <= 1e-6
+    # AcValidator through the C++ API vs the oracle's restatement of ac_validator.cpp
+    import numpy as np
+    from oracle.oracle import OracleAc
+    gold = json.loads(open(GOLDEN).read())
+    orc = OracleContext(text)
+    oac = OracleAc(orc)
+    ac = got["ac"]
+    assert abs(ac["baseline_lambda_o"] - oac.baseline["lambda_o"]) <= 1e-8 * max(1.0, oac.baseline["lambda_o"])
+    assert ac["baseline_critical"] == oac.baseline["critical"]
+    gen = np.array(gold["genomes"], np.int32)
+    n_a = gold["n_a"]
+    n_d = gen.shape[1] - n_a
+    sc = orc.evaluate(gen, n_a, n_d)
+    assert ac["worst_k"] == oac.worst_k_check(gen, n_a, n_d, sc["worst_idx"], sc["worst_n"]).tolist()
+    reason, acc, lo = oac.full_validation(gen, n_a, n_d)
+    assert ac["full_reason"] == reason.tolist()
+    assert np.allclose(ac["full_lambda_o"], lo, rtol=1e-8, atol=1e-8)
