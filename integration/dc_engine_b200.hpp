@@ -11,10 +11,12 @@
 //
 // Reference interfaces used: grid_model.hpp:16-139, importer.hpp:19-35,
 // genome.hpp:13-35, dc_engine.hpp:16-48 and 95-150, qd_optimizer.hpp:15-118,
-// errors.hpp:9-34.
+// ac_validator.hpp:18-140, errors.hpp:9-34.
 #pragma once
 
+#include <algorithm>
 #include <atomic>
+#include <cmath>
 #include <chrono>
 #include <cstdint>
 #include <exception>
@@ -25,6 +27,7 @@
 
 #include <topopt_b200.h>
 
+#include "topopt/ac_validator.hpp"
 #include "topopt/dc_engine.hpp"
 #include "topopt/errors.hpp"
 #include "topopt/qd_optimizer.hpp"
@@ -315,5 +318,200 @@ inline OptimizerStats run_optimizer_gpu(const GpuDcContext& ctx, const QdConfig&
   for (int i = 0; i < st.n_trace; ++i) out.fitness_trace.emplace_back(tev[i], tbest[i]);
   return out;
 }
+
+
+// Drop-in for AcValidator (ac_validator.hpp:93-140): the same members on the
+// reference's own types; every power flow runs on the GPU (tg_ac_*, one CTA per
+// (genome, contingency) case). The engine reads the grid through the
+// reference's canonical dump (grid_to_json_text) and rebuilds the action set
+// with the same ids. eliminate() and the history are the reference's host
+// logic; validate_queue() validates a whole elimination queue with two device
+// batches and records what a loop of validate() calls records.
+class GpuAcValidator {
+ public:
+  GpuAcValidator(const GridModel& grid, const ActionSet& actions, const DcContext& dc, AcConfig config = {},
+                 const GpuDcContext* gpu_dc = nullptr, int device = 0)
+      : grid_(&grid), actions_(&actions), config_(config) {
+    const std::string text = grid_to_json_text(grid);
+    check(tg_grid_from_json(text.data(), text.size(), &tg_grid_));
+    check(tg_actionset_build(tg_grid_, 0, 0, &tg_actions_));
+    const tg_ac_config c{config.tolerance_pu, config.max_iterations, config.worst_k_nonconverged,
+                         config.nonconverged_fraction, config.similarity_distance, config.dominance_fitness_frac,
+                         config.improvement_threshold_frac};
+    check(tg_ac_context_create(tg_grid_, tg_actions_, gpu_dc ? gpu_dc->handle() : nullptr, &c, device, &h_));
+    tg_ac_baseline b{};
+    check(tg_ac_baseline_get(h_, &b, nullptr, nullptr));
+    baseline_lambda_o_ = b.lambda_o;
+    baseline_critical_ = b.critical_count;
+    pre_fitness_ = dc.pre_optimization_score().fitness;
+  }
+  ~GpuAcValidator() {
+    if (h_) tg_ac_context_destroy(h_);
+    if (tg_actions_) tg_actionset_destroy(tg_actions_);
+    if (tg_grid_) tg_grid_destroy(tg_grid_);
+  }
+  GpuAcValidator(const GpuAcValidator&) = delete;
+  GpuAcValidator& operator=(const GpuAcValidator&) = delete;
+
+  const AcConfig& config() const { return config_; }
+  double baseline_lambda_o() const { return baseline_lambda_o_; }
+  int baseline_critical_count() const { return baseline_critical_; }
+
+  // ac_validator.cpp:345-397
+  EliminationOutcome eliminate(const std::vector<Candidate>& cands) const {
+    const double eps = config_.dominance_fitness_frac * std::abs(pre_fitness_);
+    const double theta = config_.improvement_threshold_frac * std::abs(pre_fitness_);
+    auto swd = [](const ScoreVector& s) { return s.lambda_d + s.lambda_s + s.lambda_r; };
+    EliminationOutcome out;
+    for (int i = 0; i < static_cast<int>(cands.size()); ++i) {
+      const Candidate& c = cands[i];
+      auto dominated_by = [&](int osw, double ofit) { return osw < swd(c.dc_score) && ofit >= c.dc_score.fitness - eps; };
+      RejectionReason why = RejectionReason::None;
+      for (const Validated& v : validated_)
+        if (genome_distance(c.genome, v.genome) <= config_.similarity_distance) {
+          why = RejectionReason::EliminatedSimilar;
+          break;
+        }
+      if (why == RejectionReason::None)
+        for (const Candidate& o : cands)
+          if (dominated_by(swd(o.dc_score), o.dc_score.fitness)) {
+            why = RejectionReason::EliminatedDominated;
+            break;
+          }
+      if (why == RejectionReason::None)
+        for (const Validated& v : validated_)
+          if (dominated_by(v.swd, v.fitness)) {
+            why = RejectionReason::EliminatedDominated;
+            break;
+          }
+      if (why == RejectionReason::None &&
+          (!std::isfinite(c.dc_score.fitness) || c.dc_score.fitness - pre_fitness_ < theta))
+        why = RejectionReason::EliminatedBelowThreshold;
+      if (why == RejectionReason::None)
+        out.queue.push_back(i);
+      else
+        out.pruned.emplace_back(i, why);
+    }
+    std::sort(out.queue.begin(), out.queue.end(), [&](int a, int b) {
+      if (cands[a].dc_score.fitness != cands[b].dc_score.fitness) return cands[a].dc_score.fitness > cands[b].dc_score.fitness;
+      return cands[a].genome.canonical_key() < cands[b].genome.canonical_key();
+    });
+    return out;
+  }
+
+  // ac_validator.cpp:399-425 for a batch
+  std::vector<RejectionReason> worst_k_check(const std::vector<Candidate>& cs) const {
+    if (cs.empty()) return {};
+    int na = 0, nd = 0, wk = 1;
+    for (const Candidate& c : cs) {
+      na = std::max<int>(na, static_cast<int>(c.genome.action_slots.size()));
+      nd = std::max<int>(nd, static_cast<int>(c.genome.disconnection_slots.size()));
+      wk = std::max<int>(wk, static_cast<int>(c.dc_score.worst_contingencies.size()));
+    }
+    const int n = static_cast<int>(cs.size());
+    std::vector<int32_t> flat = pad(cs, na, nd), wi(static_cast<size_t>(n) * wk, -1), wn(n), reason(n);
+    for (int i = 0; i < n; ++i) {
+      wn[i] = static_cast<int32_t>(cs[i].dc_score.worst_contingencies.size());
+      for (int j = 0; j < wn[i]; ++j) wi[static_cast<size_t>(i) * wk + j] = cs[i].dc_score.worst_contingencies[j].first;
+    }
+    check(tg_ac_worst_k_check(h_, flat.data(), n, na, nd, wi.data(), wn.data(), wk, reason.data()));
+    std::vector<RejectionReason> out(n);
+    for (int i = 0; i < n; ++i) out[i] = static_cast<RejectionReason>(reason[i]);
+    return out;
+  }
+  RejectionReason worst_k_check(const Genome& g, const ScoreVector& s) const { return worst_k_check({Candidate{g, s}}).front(); }
+
+  // ac_validator.cpp:427-473 for a batch
+  std::vector<ValidationRecord> full_validation(const std::vector<Candidate>& cs) const {
+    std::vector<ValidationRecord> out;
+    if (cs.empty()) return out;
+    int na = 0, nd = 0;
+    for (const Candidate& c : cs) {
+      na = std::max<int>(na, static_cast<int>(c.genome.action_slots.size()));
+      nd = std::max<int>(nd, static_cast<int>(c.genome.disconnection_slots.size()));
+    }
+    const int n = static_cast<int>(cs.size());
+    std::vector<int32_t> flat = pad(cs, na, nd), reason(n);
+    std::vector<uint8_t> acc(n);
+    std::vector<double> lo(n);
+    check(tg_ac_full_validation(h_, flat.data(), n, na, nd, reason.data(), acc.data(), lo.data()));
+    out.resize(n);
+    for (int i = 0; i < n; ++i) {
+      out[i].genome = cs[i].genome;
+      out[i].dc_score = cs[i].dc_score;
+      out[i].stage = ValidationStage::FullN1;
+      out[i].accepted = acc[i] != 0;
+      out[i].reason = static_cast<RejectionReason>(reason[i]);
+      out[i].ac_lambda_o = lo[i];
+    }
+    return out;
+  }
+  ValidationRecord full_validation(const Genome& g, const ScoreVector& s) const {
+    return full_validation(std::vector<Candidate>{Candidate{g, s}}).front();
+  }
+
+  // ac_validator.cpp:475-495 for a whole queue
+  std::vector<ValidationRecord> validate_queue(const std::vector<Candidate>& cs) {
+    for (const Candidate& c : cs)
+      validated_.push_back({c.genome, c.dc_score.lambda_d + c.dc_score.lambda_s + c.dc_score.lambda_r, c.dc_score.fitness});
+    const std::vector<RejectionReason> early = worst_k_check(cs);
+    std::vector<Candidate> go;
+    for (size_t i = 0; i < cs.size(); ++i)
+      if (early[i] == RejectionReason::None) go.push_back(cs[i]);
+    const std::vector<ValidationRecord> full = full_validation(go);
+    std::vector<ValidationRecord> out;
+    size_t j = 0;
+    for (size_t i = 0; i < cs.size(); ++i) {
+      if (early[i] == RejectionReason::None) {
+        out.push_back(full[j++]);
+      } else {
+        ValidationRecord r;
+        r.genome = cs[i].genome;
+        r.dc_score = cs[i].dc_score;
+        r.stage = ValidationStage::WorstK;
+        r.reason = early[i];
+        out.push_back(r);
+      }
+      records_.push_back(out.back());
+    }
+    return out;
+  }
+  ValidationRecord validate(const Candidate& c) { return validate_queue({c}).front(); }
+  void record_elimination(const Candidate& c, RejectionReason reason) {
+    ValidationRecord r;
+    r.genome = c.genome;
+    r.dc_score = c.dc_score;
+    r.reason = reason;
+    records_.push_back(r);
+  }
+  const std::vector<ValidationRecord>& records() const { return records_; }
+
+ private:
+  static std::vector<int32_t> pad(const std::vector<Candidate>& cs, int na, int nd) {
+    std::vector<int32_t> flat;
+    for (const Candidate& c : cs) {
+      flat.insert(flat.end(), c.genome.action_slots.begin(), c.genome.action_slots.end());
+      flat.insert(flat.end(), na - c.genome.action_slots.size(), -1);
+      flat.insert(flat.end(), c.genome.disconnection_slots.begin(), c.genome.disconnection_slots.end());
+      flat.insert(flat.end(), nd - c.genome.disconnection_slots.size(), -1);
+    }
+    return flat;
+  }
+  struct Validated {
+    Genome genome;
+    int swd = 0;
+    double fitness = 0.0;
+  };
+  const GridModel* grid_;
+  const ActionSet* actions_;
+  AcConfig config_;
+  tg_grid* tg_grid_ = nullptr;
+  tg_actionset* tg_actions_ = nullptr;
+  tg_ac_context* h_ = nullptr;
+  double baseline_lambda_o_ = 0.0, pre_fitness_ = 0.0;
+  int baseline_critical_ = 0;
+  std::vector<Validated> validated_;
+  std::vector<ValidationRecord> records_;
+};
 
 }  // namespace topopt::b200
