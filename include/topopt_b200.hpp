@@ -152,6 +152,7 @@ inline std::uint64_t grid_content_hash(const GridModel& g) {
 struct EnumerationConfig {
   std::int64_t cap = std::int64_t{1} << 23;
   std::uint64_t seed = 0;
+  int device = -1;  // >= 0: islanding validation of the candidate splits on that GPU (same ids)
 };
 
 class ActionSet {
@@ -175,7 +176,10 @@ class ActionSet {
 
 inline ActionSet build_action_set(const GridModel& g, const EnumerationConfig& cfg = {}) {
   tg_actionset* h = nullptr;
-  check(tg_actionset_build(g.handle(), cfg.seed, cfg.cap, &h));
+  if (cfg.device >= 0)
+    check(tg_actionset_build_device(g.handle(), cfg.seed, cfg.cap, cfg.device, &h));
+  else
+    check(tg_actionset_build(g.handle(), cfg.seed, cfg.cap, &h));
   return ActionSet(h, g);
 }
 inline void save_action_set(const ActionSet& a, const GridModel& g, const std::filesystem::path& path) {
