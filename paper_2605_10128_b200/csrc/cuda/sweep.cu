@@ -1003,20 +1003,22 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
   if (lane < kStride) rms[lane] = 0.0;
   __syncwarp();
   {
+    // maxima as floats rounded up (looser by at most one float ulp: the bounds
+    // stay rigorous), reduced with one REDUX each (non-negative float bits
+    // order like the values)
     double a = 0.0;
 #pragma unroll
     for (int k = 0; k < kKpl; ++k) a = fmax(a, fabs(alpha[k] - g.alpha0[kb + k]));
-#pragma unroll
-    for (int o = kSubLanes / 2; o > 0; o >>= 1) a = fmax(a, __shfl_xor_sync(0xffffffffu, a, o));
-    if (lane % kSubLanes == 0) asub[lane / kSubLanes] = __double2float_ru(a * (1.0 + 1e-12));
+    const unsigned gmask = ((1u << kSubLanes) - 1u) << (lane & ~(kSubLanes - 1));
+    const unsigned am = __reduce_max_sync(gmask, __float_as_uint(__double2float_ru(a * (1.0 + 1e-12))));
+    if (lane % kSubLanes == 0) asub[lane / kSubLanes] = __uint_as_float(am);
 #pragma unroll
     for (int q = 0; q < R; ++q) {
       double r = 0.0;
 #pragma unroll
       for (int k = 0; k < kKpl; ++k) r = fmax(r, fabs(rr[k][q]));
-#pragma unroll
-      for (int o = 16; o > 0; o >>= 1) r = fmax(r, __shfl_xor_sync(0xffffffffu, r, o));
-      if (lane == 0) rms[1 + q] = r * (1.0 + 1e-12);
+      const unsigned m = __reduce_max_sync(0xffffffffu, __float_as_uint(__double2float_ru(r * (1.0 + 1e-12))));
+      if (lane == 0) rms[1 + q] = static_cast<double>(__uint_as_float(m));
     }
   }
   __syncwarp();
