@@ -410,7 +410,7 @@ __device__ __forceinline__ void prep_branch_chunk(const DevGrid& g, const Batch&
   if (e < g.E) {
     double2* dst = reinterpret_cast<double2*>(b.feat + feat_index(slot, b.nchunks, e, R));
 #pragma unroll
-    for (int i = 0; i < RS / 2; ++i) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+    for (int i = 0; i < RS / 2; ++i) __stcs(dst + i, make_double2(row[2 * i], row[2 * i + 1]));  // streaming: read back by the sweep, not by this kernel
   }
 }
 
@@ -477,7 +477,7 @@ __device__ __forceinline__ void prep_cont_chunk(const DevGrid& g, const Batch& b
     double2* dst = reinterpret_cast<double2*>(b.kdat + static_cast<size_t>(c) * g.Kpad * kStride +
                                               static_cast<size_t>(k) * RS);
 #pragma unroll
-    for (int i = 0; i < RS / 2; ++i) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
+    for (int i = 0; i < RS / 2; ++i) __stcs(dst + i, make_double2(row[2 * i], row[2 * i + 1]));
     b.kflag[static_cast<size_t>(c) * g.Kpad + k] = flag;
   }
 }
