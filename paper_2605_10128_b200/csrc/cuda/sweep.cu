@@ -990,9 +990,9 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
 #pragma unroll
     for (int i = 0; i < kKpl; ++i) {
       kbr[i] = kb + i < g.Ks ? g.ks_branch[kb + i] : -1;
-      alpha[i] = kd[i * S];
+      alpha[i] = __ldcs(kd + i * S);  // read once per launch: streaming
 #pragma unroll
-      for (int q = 0; q < R; ++q) rr[i][q] = kd[i * S + 1 + q];
+      for (int q = 0; q < R; ++q) rr[i][q] = __ldcs(kd + i * S + 1 + q);
       energy[i] = 0.0;
       kval[i] = kf[i] == 0;
     }
