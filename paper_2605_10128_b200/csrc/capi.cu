@@ -2108,7 +2108,7 @@ struct tg_ac_context {
   int cap_slots = 0;
   int *d_genomes = nullptr, *d_case_g = nullptr, *d_case_k = nullptr, *d_iters = nullptr, *d_crit = nullptr,
       *d_nonconv = nullptr, *d_fcrit = nullptr;
-  int *t_from = nullptr, *t_to = nullptr, *t_inode = nullptr, *t_nnew = nullptr;
+  int *t_from = nullptr, *t_to = nullptr, *t_inode = nullptr, *t_nnew = nullptr, *t_split = nullptr;
   uint8_t *t_rem = nullptr, *d_conv = nullptr, *d_foldcase = nullptr;
   double *d_energy = nullptr, *d_flo = nullptr, *d_loading = nullptr, *d_vm = nullptr, *d_va = nullptr;
   unsigned long long* d_fold = nullptr;
@@ -2188,6 +2188,7 @@ tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, 
     t_rem = work->alloc<uint8_t>(cap_genomes * E);
     t_inode = work->alloc<int>(cap_genomes * std::max(I, 1));
     t_nnew = work->alloc<int>(cap_genomes);
+    t_split = work->alloc<int>(cap_genomes * cap_slots);
     d_fold = work->alloc<unsigned long long>(cap_genomes * E);
     d_nonconv = work->alloc<int>(cap_genomes);
     d_flo = work->alloc<double>(cap_genomes);
@@ -2214,7 +2215,7 @@ tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, 
     check(cudaMemsetAsync(d_fold, 0, sizeof(unsigned long long) * n_genomes * E, stream), "AC fold reset");
     check(cudaMemsetAsync(d_nonconv, 0, sizeof(int) * n_genomes, stream), "AC fold reset");
   }
-  tgb::AcTopo tp{t_from, t_to, t_rem, t_inode, t_nnew};
+  tgb::AcTopo tp{t_from, t_to, t_rem, t_inode, t_nnew, t_split, std::max(n_a, 1)};
   tgb::ac_launch_topo(g, d_genomes, n_genomes, n_a, n_d, tp, stream);
   tgb::AcCases io{};
   io.genome = d_case_g;
@@ -2301,6 +2302,18 @@ tg_status tg_ac_context_create(const tg_grid* grid, const tg_actionset* actions,
     g.br_bc = ar.upload(G.br_bc, s);
     g.br_tap = ar.upload(G.br_tap, s);
     g.node_shunt = ar.upload(G.node_shunt, s);
+    {
+      // CSR of every branch at both of its ends, grid order (the sparse Ybus of k_ac_case)
+      std::vector<int32_t> ptr(ctx->N + 1, 0), br;
+      for (int e = 0; e < ctx->E; ++e) ++ptr[G.br_from[e] + 1], ++ptr[G.br_to[e] + 1];
+      for (int v = 0; v < ctx->N; ++v) ptr[v + 1] += ptr[v];
+      br.assign(ptr.back(), 0);
+      std::vector<int32_t> fill(ptr.begin(), ptr.end() - 1);
+      for (int e = 0; e < ctx->E; ++e) br[fill[G.br_from[e]]++] = e, br[fill[G.br_to[e]]++] = e;
+      g.node_ptr = ar.upload(ptr, s);
+      g.node_br = ar.upload(br, s);
+    }
+    g.st_node = ar.upload(grid->sub_node, s);
     g.inj_node = ar.upload(grid->inj_node, s);
     g.inj_p = ar.upload(G.inj_p, s);
     g.inj_q = ar.upload(G.inj_q, s);

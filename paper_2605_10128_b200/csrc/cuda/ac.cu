@@ -13,8 +13,8 @@ constexpr double kBaseMva = 100.0;  // ac_validator.cpp:14
 
 // Workspace of one case (offsets in bytes, 16-byte aligned sections).
 struct AcWs {
-  double *J, *G, *B, *vm, *va, *P, *Q, *psp, *qsp, *vset, *dx, *lm, *red;
-  int *bus_of, *node_of, *ang, *mag, *pv, *reach, *ired;
+  double *J, *Gd, *Bd, *vm, *va, *P, *Q, *psp, *qsp, *vset, *dx, *lm, *red;
+  int *bus_of, *node_of, *ang, *mag, *ang_pos, *mag_pos, *pv, *reach, *ired;
   uint8_t* live;
 };
 
@@ -35,8 +35,8 @@ __host__ __device__ inline size_t ws_layout(int n_bus, int nu, int E, unsigned c
   const size_t nb = static_cast<size_t>(n_bus), nn = static_cast<size_t>(nu);
   AcWs t{};
   t.J = take_d(nn * nn);
-  t.G = take_d(nb * nb);
-  t.B = take_d(nb * nb);
+  t.Gd = take_d(nb);
+  t.Bd = take_d(nb);
   t.vm = take_d(nb);
   t.va = take_d(nb);
   t.P = take_d(nb);
@@ -51,6 +51,8 @@ __host__ __device__ inline size_t ws_layout(int n_bus, int nu, int E, unsigned c
   t.node_of = take_i(nb);
   t.ang = take_i(nn);
   t.mag = take_i(nn);
+  t.ang_pos = take_i(nb);
+  t.mag_pos = take_i(nb);
   t.pv = take_i(nb);
   t.reach = take_i(nb);
   t.ired = take_i(64);
@@ -183,12 +185,19 @@ __device__ void lu_solve(double* J, double* dx, double* lm, int nu, double* red,
     __syncthreads();
     // trailing update: warps over rows, lanes over columns (row-major J, so a
     // warp touches consecutive words)
+    // (two rows per warp: each pivot-row element is loaded once for both)
     const double* rk = J + static_cast<size_t>(k) * nu;
-    for (int i = k + 1 + (tid >> 5); i < nu; i += NT / 32) {
-      const double l = lm[i];
-      if (l == 0.0) continue;
-      double* ri = J + static_cast<size_t>(i) * nu;
-      for (int j = k + 1 + (tid & 31); j < nu; j += 32) ri[j] -= l * rk[j];
+    for (int i = k + 1 + 2 * (tid >> 5); i < nu; i += 2 * (NT / 32)) {
+      const bool two = i + 1 < nu;
+      const double l0 = lm[i], l1 = two ? lm[i + 1] : 0.0;
+      if (l0 == 0.0 && l1 == 0.0) continue;
+      double* r0 = J + static_cast<size_t>(i) * nu;
+      double* r1 = r0 + nu;
+      for (int j = k + 1 + (tid & 31); j < nu; j += 32) {
+        const double x = rk[j];
+        if (l0 != 0.0) r0[j] -= l0 * x;
+        if (l1 != 0.0) r1[j] -= l1 * x;
+      }
     }
     __syncthreads();
   }
@@ -198,6 +207,26 @@ __device__ void lu_solve(double* J, double* dx, double* lm, int nu, double* red,
     const double xi = dx[i];
     for (int r = tid; r < i; r += NT) dx[r] -= J[static_cast<size_t>(r) * nu + i] * xi;
     __syncthreads();
+  }
+}
+
+// The Ybus off-diagonal terms of bus i as a sum over its live branches
+// (sparse form of ac_validator.cpp:117-141; parallel branches add up like the
+// dense matrix's entries): fn(k, g_ik, b_ik) for every branch to bus k. The
+// candidates are the base node's incident branches (a split section's: the
+// station node's), kept if one of their current ends is bus i's node.
+template <class F>
+__device__ __forceinline__ void for_each_branch_of_bus(const AcGrid& g, const AcWs& w, const int* ef, const int* et,
+                                                       const int* split_node, int i, F&& fn) {
+  const int v = w.node_of[i];
+  const int base = v < g.N ? v : split_node[v - g.N];
+  for (int p = g.node_ptr[base]; p < g.node_ptr[base + 1]; ++p) {
+    const int e = g.node_br[p];
+    if (!w.live[e]) continue;
+    const int a = ef[e], b = et[e];
+    if (a != v && b != v) continue;  // this end moved to another section
+    const BranchY y = branch_y(g, e);  // y_ft = y_tf
+    fn(w.bus_of[a == v ? b : a], y.ftr, y.fti);
   }
 }
 
@@ -213,6 +242,7 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
   const int* et = tp.to + static_cast<size_t>(gi) * E;
   const uint8_t* rem = tp.removed + static_cast<size_t>(gi) * E;
   const int* inode = tp.inj_node + static_cast<size_t>(gi) * I;
+  const int* split_node = tp.split_node + static_cast<size_t>(gi) * tp.split_stride;
   const int* cb0 = ci >= 0 ? g.cont_br + g.cont_br_ptr[ci] : nullptr;
   const int* cb1 = ci >= 0 ? g.cont_br + g.cont_br_ptr[ci + 1] : nullptr;
   const int* cj0 = ci >= 0 ? g.cont_inj + g.cont_inj_ptr[ci] : nullptr;
@@ -250,9 +280,6 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
   if (!floating) {
     // bus numbering, specified injections, PV buses (ac_validator.cpp:84-115),
     // Ybus in branch order (117-141), flat start and unknown order (143-156)
-    const int nmax = sv.n_bus;
-    for (int i = tid; i < nmax * nmax; i += NT) w.G[i] = 0.0, w.B[i] = 0.0;
-    __syncthreads();
     if (tid == 0) {
       int n = 0;
       for (int v = 0; v < nbus; ++v) {
@@ -277,27 +304,31 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
           w.qsp[b] -= g.inj_q[i] / kBaseMva;
         }
       }
+      // Ybus diagonal in branch order (the off-diagonal terms are summed per bus
+      // over its branches, for_each_branch_of_bus)
+      for (int b = 0; b < n; ++b) w.Gd[b] = 0.0, w.Bd[b] = 0.0;
       for (int e = 0; e < E; ++e) {
         if (!w.live[e]) continue;
         const BranchY y = branch_y(g, e);
         const int f = w.bus_of[ef[e]], t = w.bus_of[et[e]];
-        w.G[f * n + f] += y.ffr, w.B[f * n + f] += y.ffi;
-        w.G[f * n + t] += y.ftr, w.B[f * n + t] += y.fti;
-        w.G[t * n + f] += y.ftr, w.B[t * n + f] += y.fti;
-        w.G[t * n + t] += y.ttr, w.B[t * n + t] += y.tti;
+        w.Gd[f] += y.ffr, w.Bd[f] += y.ffi;
+        w.Gd[t] += y.ttr, w.Bd[t] += y.tti;
       }
       for (int v = 0; v < g.N; ++v)
-        if (w.bus_of[v] >= 0 && g.node_shunt[v] != 0.0) w.B[w.bus_of[v] * n + w.bus_of[v]] += g.node_shunt[v];
+        if (w.bus_of[v] >= 0 && g.node_shunt[v] != 0.0) w.Bd[w.bus_of[v]] += g.node_shunt[v];
       const int sl = w.bus_of[g.slack];
       int na = 0, nm = 0;
       for (int b = 0; b < n; ++b) {
         w.vm[b] = (w.pv[b] || b == sl) ? w.vset[b] : 1.0;
         w.va[b] = 0.0;
+        w.ang_pos[b] = -1;
+        w.mag_pos[b] = -1;
         if (b == sl) continue;
+        w.ang_pos[b] = na;
         w.ang[na++] = b;
       }
       for (int b = 0; b < n; ++b)
-        if (b != sl && !w.pv[b]) w.mag[nm++] = b;
+        if (b != sl && !w.pv[b]) w.mag_pos[b] = nm, w.mag[nm++] = b;
       sh[0] = n, sh[1] = sl, sh[2] = na, sh[3] = nm;
     }
     __syncthreads();
@@ -311,16 +342,14 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
     for (int it = 1; it <= sv.max_iter; ++it) {  // ac_validator.cpp:175-244
       // bus injections (159-173)
       for (int i = tid; i < n; i += NT) {
-        double p = 0.0, q = 0.0;
         const double vi = w.vm[i], ai = w.va[i];
-        for (int k = 0; k < n; ++k) {
-          const double gik = w.G[i * n + k], bik = w.B[i * n + k];
-          if (gik == 0.0 && bik == 0.0) continue;
+        double p = vi * vi * w.Gd[i], q = -vi * vi * w.Bd[i];
+        for_each_branch_of_bus(g, w, ef, et, split_node, i, [&](int k, double gik, double bik) {
           double s, co;
           sincos(ai - w.va[k], &s, &co);
           p += vi * w.vm[k] * (gik * co + bik * s);
           q += vi * w.vm[k] * (gik * s - bik * co);
-        }
+        });
         w.P[i] = p;
         w.Q[i] = q;
       }
@@ -339,34 +368,38 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
         break;
       }
       if (it == sv.max_iter) break;
-      // Jacobian (186-236)
-      for (int idx = tid; idx < nu * nu; idx += NT) {
-        const int r = idx / nu, cc = idx % nu;
-        const int i = r < na ? w.ang[r] : w.mag[r - na];
-        const int k = cc < na ? w.ang[cc] : w.mag[cc - na];
-        const double vi = w.vm[i];
-        double v;
-        if (i == k) {
-          const double gii = w.G[i * n + i], bii = w.B[i * n + i];
-          if (r < na)
-            v = cc < na ? -w.Q[i] - bii * vi * vi : w.P[i] / vi + gii * vi;
-          else
-            v = cc < na ? w.P[i] - gii * vi * vi : w.Q[i] / vi - bii * vi;
-        } else {
-          const double gik = w.G[i * n + k], bik = w.B[i * n + k];
-          if (gik == 0.0 && bik == 0.0) {
-            v = 0.0;
-          } else {
-            double s, co;
-            sincos(w.va[i] - w.va[k], &s, &co);
-            const double vk = w.vm[k];
-            if (r < na)
-              v = cc < na ? vi * vk * (gik * s - bik * co) : vi * (gik * co + bik * s);
-            else
-              v = cc < na ? -vi * vk * (gik * co + bik * s) : vi * (gik * s - bik * co);
-          }
+      // Jacobian (186-236): zeroed, then each bus fills its own rows (diagonal
+      // terms, and one term per branch for the neighbour's columns)
+      for (int idx = tid; idx < nu * nu; idx += NT) w.J[idx] = 0.0;
+      __syncthreads();
+      for (int i = tid; i < n; i += NT) {
+        const int rp = w.ang_pos[i], rq = w.mag_pos[i] >= 0 ? na + w.mag_pos[i] : -1;
+        if (rp < 0 && rq < 0) continue;  // the slack bus has no row
+        const double vi = w.vm[i], gii = w.Gd[i], bii = w.Bd[i];
+        double* JP = rp >= 0 ? w.J + static_cast<size_t>(rp) * nu : nullptr;
+        double* JQ = rq >= 0 ? w.J + static_cast<size_t>(rq) * nu : nullptr;
+        if (JP) {
+          JP[rp] = -w.Q[i] - bii * vi * vi;
+          if (rq >= 0) JP[rq] = w.P[i] / vi + gii * vi;
         }
-        w.J[idx] = v;
+        if (JQ) {
+          if (rp >= 0) JQ[rp] = w.P[i] - gii * vi * vi;
+          JQ[rq] = w.Q[i] / vi - bii * vi;
+        }
+        for_each_branch_of_bus(g, w, ef, et, split_node, i, [&](int k, double gik, double bik) {
+          const int ct = w.ang_pos[k], cv = w.mag_pos[k] >= 0 ? na + w.mag_pos[k] : -1;
+          double s, co;
+          sincos(w.va[i] - w.va[k], &s, &co);
+          const double vk = w.vm[k];
+          if (JP) {
+            if (ct >= 0) JP[ct] += vi * vk * (gik * s - bik * co);
+            if (cv >= 0) JP[cv] += vi * (gik * co + bik * s);
+          }
+          if (JQ) {
+            if (ct >= 0) JQ[ct] += -vi * vk * (gik * co + bik * s);
+            if (cv >= 0) JQ[cv] += vi * (gik * s - bik * co);
+          }
+        });
       }
       __syncthreads();
       lu_solve<NT>(w.J, w.dx, w.lm, nu, w.red, w.ired);
@@ -461,6 +494,7 @@ __global__ void k_ac_topo(AcGrid g, const int* genomes, int n_a, int n_d, AcTopo
     if (a < 0) continue;
     const int st = g.act_station[a];
     const int t0 = g.st_term_ptr[st], nt = g.st_term_ptr[st + 1] - t0;
+    if (threadIdx.x == 0) t.split_node[static_cast<size_t>(gi) * t.split_stride + nn] = g.st_node[st];
     const uint8_t* grp = g.act_group + g.act_group_ptr[a];
     const int node = g.N + nn;
     for (int k = threadIdx.x; k < nt; k += blockDim.x) {

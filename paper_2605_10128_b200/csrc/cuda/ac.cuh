@@ -29,6 +29,8 @@ struct AcGrid {
   const double* br_bc;       // [E] total line charging p.u.
   const double* br_tap;      // [E] off-nominal ratio, from side
   const double* node_shunt;  // [N] shunt susceptance p.u.
+  const int* node_ptr;       // [N+1] CSR of every branch at each of its ends (grid order)
+  const int* node_br;
   const int* inj_node;       // [I]
   const double* inj_p;       // [I] MW
   const double* inj_q;       // [I] Mvar
@@ -39,6 +41,7 @@ struct AcGrid {
   const int* cont_br;
   const int* cont_inj_ptr;   // [K+1] CSR of contingency injections
   const int* cont_inj;
+  const int* st_node;        // [S] the station's node
   const int* st_term_ptr;    // [S+1] station terminals
   const int* term_kind;      // 0 branch from-end, 1 branch to-end, 2 injection
   const int* term_elem;
@@ -55,6 +58,8 @@ struct AcTopo {
   uint8_t* removed;  // [G][E]
   int* inj_node;     // [G][I]
   int* n_new;        // [G]
+  int* split_node;   // [G][split_stride] base node of each split section (slot order)
+  int split_stride;
 };
 
 // One validation batch of cases (genome index, contingency index or -1 for
