@@ -617,7 +617,10 @@ def main():
                        "archive_entries": len(snap.entries), "best_fitness": snap.best_fitness,
                        "context_setup_s": setup_s},
             "gpu_launches": int(launches),
-            "roofline": {"bound": "hbm", "kernel": "k_sweep_chunked (fused N-1 sweep, scores-only)",
+            "roofline": {"bound": "hbm",
+                         "kernel": ("k_sweep_chunked (fused N-1 sweep, scores-only)" if T == 1 else
+                                    "mask pass + k_sweep_masked (timestep screening, 8 profiles per launch); "
+                                    "bytes per profile"),
                          "achieved": hbm_gbs, "peak": hbm_peak, "unit": "GB/s",
                          "frac": hbm_gbs / hbm_peak if hbm_peak else None, "traffic": traffic,
                          "algorithmic": "SURVEY.md 8(d) compulsory bytes per launch: 8*E*K (T_base once) + per "
