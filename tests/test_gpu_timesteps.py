@@ -83,3 +83,22 @@ def test_more_profiles_than_one_masked_launch():
     sc = ctx.evaluate_arrays(genomes, 3, 2)
     ref = oracle_timesteps(orcs, genomes, 3, 2)
     compare_scores(sc, ref, 20)
+
+
+def test_cfg3_against_the_oracle_per_profile():
+    """The bench's configs[2] grid itself (2k buses, 100 split stations, 24
+    timesteps: mask pass + three masked launches of 8 profiles) on 64 MapElites
+    loop candidates, against the oracle run on each of the 24 single-profile
+    grids and aggregated (not only against the engine's own per-profile path)."""
+    from tools.synth_grid import config_json
+
+    text = config_json("cfg3")
+    ctx = _ctx(text)
+    sess = P.QdSession(ctx, P.QdConfig(batch_size=512, seed=9, iters_per_epoch=1 << 30))
+    sess.step(3)
+    genomes = sess.offspring()[:64]
+    sc = ctx.evaluate_arrays(genomes, 3, 2)
+    orcs = [OracleContext(t) for t in timestep_grids(text)]
+    assert len(orcs) == 24
+    ref = oracle_timesteps(orcs, genomes, 3, 2)
+    compare_scores(sc, ref, 20)
