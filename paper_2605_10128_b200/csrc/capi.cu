@@ -204,6 +204,7 @@ struct tg_context {
   int n_cont = 0;
   int worst_k = 20;
   int64_t launches = 0;
+  tgb::SideStream side{nullptr, nullptr, nullptr};  // special outages beside the prep / sweep (launch_evaluate)
   // evaluation batch buffers
   int capacity = 0;
   std::unique_ptr<DeviceArena> batch_arena;
@@ -491,7 +492,7 @@ int tg_context::enqueue_evaluate(tgb::Batch& bv, int n_a, int n_d, bool full, bo
   }
   if (n_t == 1) {
     tgb::launch_evaluate(g, bv, n_a, n_d, full, scratch, stream, &kernels, timed ? sw0 : nullptr,
-                         timed ? sw1 : nullptr);
+                         timed ? sw1 : nullptr, &side);
     if (timed) time_sweep_done();
     return kernels;
   }
@@ -1276,6 +1277,11 @@ tg_status tg_context_create(const tg_grid_desc* gd, const tg_actionset_desc* ad,
     ctx->device = device;
     check(cudaSetDevice(device), "cudaSetDevice");
     check(cudaStreamCreateWithFlags(&ctx->stream, cudaStreamNonBlocking), "stream");
+    // side stream of launch_evaluate (special outages beside the prep / sweep);
+    // created here, not inside a graph capture
+    check(cudaStreamCreateWithFlags(&ctx->side.stream, cudaStreamNonBlocking), "side stream");
+    check(cudaEventCreateWithFlags(&ctx->side.fork, cudaEventDisableTiming), "event");
+    check(cudaEventCreateWithFlags(&ctx->side.join, cudaEventDisableTiming), "event");
     if (gd->n_nodes < 2) throw tgb::ValidationError("grid needs at least two nodes");
     double* X = base_inverse(ctx.get(), gd);
     std::vector<int> perm = sweep_row_order(ctx.get(), gd, X);
@@ -1303,6 +1309,12 @@ void tg_context_destroy(tg_context* ctx) {
   ctx->free_snap_buffers();
   cudaStream_t s = ctx->stream;
   if (ctx->sw0) cudaEventDestroy(ctx->sw0), cudaEventDestroy(ctx->sw1);
+  if (ctx->side.stream) {
+    cudaStreamSynchronize(ctx->side.stream);
+    cudaStreamDestroy(ctx->side.stream);
+    cudaEventDestroy(ctx->side.fork);
+    cudaEventDestroy(ctx->side.join);
+  }
   if (ctx->err_host) cudaFreeHost(ctx->err_host), cudaEventDestroy(ctx->err_ev);
   delete ctx;
   cudaStreamDestroy(s);

@@ -252,8 +252,7 @@ __global__ void __launch_bounds__(kPrepCta) k_prep(DevGrid g, Batch b, int n_a, 
       }
     }
     if (threadIdx.x == 0) {
-      b.status[c] = 0;
-      b.rank[c] = r;
+      b.rank[c] = r;  // status stays k_analyze's 0 (k_special may run beside this kernel)
       int* rem = b.removed + static_cast<size_t>(c) * kMaxRemovedSweep;
       for (int i = 0; i < kMaxRemovedSweep; ++i) rem[i] = i < t.nrem ? t.rem[i] : -1;
     }
@@ -314,8 +313,7 @@ __global__ void __launch_bounds__(32) k_prep_solve(DevGrid g, Batch b) {
     if (tid == 0) {
       f->ns = ns;
       f->nv = nv;
-      b.status[c] = 0;
-      b.rank[c] = ns + nv;
+      b.rank[c] = ns + nv;  // status stays k_analyze's 0 (k_special may run beside this kernel)
       b.nc0[c] = 0;  // k_prep_rows adds its counts
       int* rem = b.removed + static_cast<size_t>(c) * kMaxRemovedSweep;
       for (int i = 0; i < kMaxRemovedSweep; ++i) rem[i] = i < t.nrem ? t.rem[i] : -1;
@@ -1211,28 +1209,48 @@ int launch_prep_mt(const DevGrid& g, Batch& b, const MtProfiles& p, cudaStream_t
   return 1;
 }
 
+int launch_special(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
+                   cudaStream_t stream) {
+  if (g.Kx + g.Kb == 0 || b.n == 0) return 0;
+  const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
+  const long total = static_cast<long>(b.n) * (g.Kx + g.Kb);
+  const int grid = static_cast<int>(total < s.zslots_special ? total : s.zslots_special);
+  k_special<<<grid, kPrepThreads, bits_bytes, stream>>>(g, b, n_a, n_d, full ? 1 : 0, s.zspecial);
+  return 1;
+}
+
 int launch_special_finish(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
                           cudaStream_t stream) {
-  int launched = 0;
-  const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
-  if (g.Kx + g.Kb > 0) {
-    const long total = static_cast<long>(b.n) * (g.Kx + g.Kb);
-    const int grid = static_cast<int>(total < s.zslots_special ? total : s.zslots_special);
-    k_special<<<grid, kPrepThreads, bits_bytes, stream>>>(g, b, n_a, n_d, full ? 1 : 0, s.zspecial);
-    ++launched;
-  }
+  int launched = launch_special(g, b, n_a, n_d, full, s, stream);
   k_finish<<<(b.n + kFinishWarps - 1) / kFinishWarps, 32 * kFinishWarps, 0, stream>>>(g, b, n_a, n_d);
   ++launched;
   return launched;
 }
 
 void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
-                     cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin, cudaEvent_t sweep_end) {
+                     cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin, cudaEvent_t sweep_end,
+                     const SideStream* side) {
   int launched = launch_eval_reset(g, b, stream);
   launched += launch_analyze(g, b, n_a, n_d, stream);
+  // the special outages (multi-branch / injection contingencies, busbar
+  // outages) only need the analysis: on the side stream they run beside the
+  // prep and the sweep (they write their own energies and fold atomically)
+  const bool fork = side && side->stream && g.Kx + g.Kb > 0;
+  if (fork) {
+    cudaEventRecord(side->fork, stream);
+    cudaStreamWaitEvent(side->stream, side->fork, 0);
+    launched += launch_special(g, b, n_a, n_d, full, s, side->stream);
+    cudaEventRecord(side->join, side->stream);
+  }
   launched += launch_prep(g, b, n_a, n_d, s, stream);
   if (g.Ks > 0) launch_sweep(g, b, full, stream, sweep_begin, sweep_end, &launched);
-  launched += launch_special_finish(g, b, n_a, n_d, full, s, stream);
+  if (fork) {
+    cudaStreamWaitEvent(stream, side->join, 0);
+    k_finish<<<(b.n + kFinishWarps - 1) / kFinishWarps, 32 * kFinishWarps, 0, stream>>>(g, b, n_a, n_d);
+    ++launched;
+  } else {
+    launched += launch_special_finish(g, b, n_a, n_d, full, s, stream);
+  }
   if (kernels) *kernels = launched;
 }
 

@@ -138,9 +138,15 @@ struct EvalScratch {
 };
 
 // sweep_begin / sweep_end (optional) bracket the fused sweep launch for live timing.
+// A second stream with fork / join events: launch_evaluate runs the special
+// outages there, beside the prep and the sweep.
+struct SideStream {
+  cudaStream_t stream;
+  cudaEvent_t fork, join;
+};
 void launch_evaluate(const DevGrid& g, Batch& b, int n_a, int n_d, bool full, const EvalScratch& s,
                      cudaStream_t stream, int* kernels, cudaEvent_t sweep_begin = nullptr,
-                     cudaEvent_t sweep_end = nullptr);
+                     cudaEvent_t sweep_end = nullptr, const SideStream* side = nullptr);
 // The phases launch_evaluate runs (returning kernels launched).
 int launch_eval_reset(const DevGrid& g, Batch& b, cudaStream_t stream);
 int launch_analyze(const DevGrid& g, Batch& b, int n_a, int n_d, cudaStream_t stream);
