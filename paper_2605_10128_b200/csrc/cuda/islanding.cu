@@ -216,6 +216,69 @@ __global__ void __launch_bounds__(kIslThreads) k_split_valid(IslGraph g, IslCand
   }
 }
 
+
+// Bridges of the base graph without each contingency's branches
+// (enumerate_disconnectables, importer.cpp:42-70): one CTA per case (case
+// n_cases = the base graph itself), BFS from node 0 over the live,
+// non-excluded branches, tree-path covering by the non-tree ones; every
+// uncovered tree edge is a bridge of that graph and is OR-ed into `bridges`.
+// A case whose graph leaves a live branch unreached from node 0 (a second
+// component) is flagged for the host's general bridge pass.
+__global__ void __launch_bounds__(kIslThreads) k_cont_bridges(IslGraph g, const int* cptr, const int* cbr, int n_cases,
+                                                              IslScratch sc, uint32_t* bridges, int* fallback) {
+  __shared__ int shv[2];
+  __shared__ int mv_dummy[1];
+  extern __shared__ uint32_t mb_zero[];  // no moved ends: an all-zero bitmap over the branches
+  const int tid = threadIdx.x, nn = g.N + 1, words = (g.E + 31) >> 5;
+  int* dist = sc.dist + static_cast<size_t>(blockIdx.x) * nn;
+  int* pe = sc.par_edge + static_cast<size_t>(blockIdx.x) * nn;
+  int* q0 = sc.queue + static_cast<size_t>(blockIdx.x) * 2 * nn;
+  int* q1 = q0 + nn;
+  uint8_t* cov = sc.cov + static_cast<size_t>(blockIdx.x) * g.E;
+  for (int w = tid; w < words; w += kIslThreads) mb_zero[w] = 0u;
+  __syncthreads();
+  // no split: a graph with no moved ends (the fresh node n = N stays isolated)
+  Split sp{-1, g.N, 0, mv_dummy, mb_zero};
+  for (int ci = blockIdx.x; ci <= n_cases; ci += gridDim.x) {
+    const int* x0 = ci < n_cases ? cbr + cptr[ci] : nullptr;
+    const int* x1 = ci < n_cases ? cbr + cptr[ci + 1] : nullptr;
+    if (ci < n_cases && x0 == x1) continue;  // empty contingency: nothing removed
+    bfs(g, sp, x0, x1, false, dist, pe, q0, q1, shv);
+    for (int e = tid; e < g.E; e += kIslThreads) cov[e] = 0;
+    __syncthreads();
+    bool stray = false;
+    for (int e = tid; e < g.E; e += kIslThreads) {
+      if (!g.br_on[e] || (x0 && excluded(x0, x1, e))) continue;
+      int a = g.br_from[e], b = g.br_to[e];
+      if (dist[a] < 0 || dist[b] < 0) {
+        stray = true;
+        continue;
+      }
+      if (pe[a] == e || pe[b] == e) continue;  // tree edge
+      while (a != b) {
+        if (dist[a] >= dist[b]) {
+          const int pa = pe[a];
+          cov[pa] = 1;
+          a = g.br_from[pa] == a ? g.br_to[pa] : g.br_from[pa];
+        } else {
+          const int pb = pe[b];
+          cov[pb] = 1;
+          b = g.br_from[pb] == b ? g.br_to[pb] : g.br_from[pb];
+        }
+      }
+    }
+    if (__syncthreads_or(stray)) {
+      if (tid == 0) fallback[ci] = 1;
+      continue;
+    }
+    for (int v = tid; v < nn; v += kIslThreads) {
+      const int e = pe[v];
+      if (e >= 0 && !cov[e]) atomicOr(bridges + (e >> 5), 1u << (e & 31));
+    }
+    __syncthreads();
+  }
+}
+
 void ck(cudaError_t e, const char* what) {
   if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
 }
@@ -287,6 +350,59 @@ void validate_splits_device(const SplitGraphDesc& gd, const SplitCandidates& cd,
   std::vector<uint8_t> out(n);
   ck(cudaMemcpy(out.data(), c.keep, n, cudaMemcpyDeviceToHost), "D2H keep");
   for (int i = 0; i < n; ++i) keep[i] = out[i];
+}
+
+
+void contingency_bridges_device(const SplitGraphDesc& gd, int device, std::vector<char>& is_bridge_any,
+                                std::vector<int>& fallback_cases) {
+  const int E = static_cast<int>(gd.br_from.size());
+  const int n_cases = static_cast<int>(gd.cont_ptr.size()) - 1;
+  is_bridge_any.assign(E, 0);
+  fallback_cases.clear();
+  ck(cudaSetDevice(device), "cudaSetDevice");
+  std::vector<void*> owned;
+  struct Free {
+    std::vector<void*>& o;
+    ~Free() {
+      for (void* p : o) cudaFree(p);
+    }
+  } guard{owned};
+  IslGraph g{};
+  g.N = gd.n_nodes;
+  g.E = E;
+  g.br_from = up(gd.br_from, owned);
+  g.br_to = up(gd.br_to, owned);
+  g.br_on = up(gd.br_on, owned);
+  g.node_ptr = up(gd.node_ptr, owned);
+  g.node_br = up(gd.node_br, owned);
+  const int* cptr = up(gd.cont_ptr, owned);
+  const int* cbr = up(gd.cont_br, owned);
+  const int slots = std::min(n_cases + 1, 148 * 4);
+  const size_t nn = static_cast<size_t>(g.N) + 1;
+  IslScratch sc{};
+  void* p = nullptr;
+  ck(cudaMalloc(&p, slots * nn * sizeof(int) * 4 + static_cast<size_t>(slots) * std::max(E, 1)), "cudaMalloc");
+  owned.push_back(p);
+  sc.dist = static_cast<int*>(p);
+  sc.par_edge = sc.dist + slots * nn;
+  sc.queue = sc.par_edge + slots * nn;
+  sc.cov = reinterpret_cast<uint8_t*>(sc.queue + 2 * slots * nn);
+  const int words = (E + 31) / 32;
+  std::vector<uint32_t> zeros(std::max(words, 1), 0u);
+  uint32_t* bits = up(zeros, owned);
+  std::vector<int> fz(n_cases + 1, 0);
+  int* fb = up(fz, owned);
+  const size_t smem = static_cast<size_t>((E + 31) / 32) * 4;
+  if (smem > 48 * 1024) ck(cudaFuncSetAttribute(k_cont_bridges, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                static_cast<int>(smem)), "smem attribute");
+  k_cont_bridges<<<slots, kIslThreads, smem>>>(g, cptr, cbr, n_cases, sc, bits, fb);
+  ck(cudaGetLastError(), "k_cont_bridges launch");
+  std::vector<uint32_t> hb(std::max(words, 1));
+  ck(cudaMemcpy(hb.data(), bits, hb.size() * sizeof(uint32_t), cudaMemcpyDeviceToHost), "D2H bridges");
+  ck(cudaMemcpy(fz.data(), fb, fz.size() * sizeof(int), cudaMemcpyDeviceToHost), "D2H fallback");
+  for (int e = 0; e < E; ++e) is_bridge_any[e] = (hb[e >> 5] >> (e & 31)) & 1u;
+  for (int c = 0; c <= n_cases; ++c)
+    if (fz[c]) fallback_cases.push_back(c);
 }
 
 }  // namespace tgb

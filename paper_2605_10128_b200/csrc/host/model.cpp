@@ -1,4 +1,6 @@
 // Host-side network model and import step (see model.hpp for the reference map).
+#include <chrono>
+#include <cstdlib>
 #include "model.hpp"
 #include "../cuda/islanding.cuh"
 
@@ -498,20 +500,63 @@ std::vector<int> locality_rank(int n, const std::vector<std::pair<int, int>>& ed
 }
 
 // ---------------------------------------------------------------- import
-std::vector<int> enumerate_disconnectables(const Grid& g) {
+// Base branch graph, node CSR and contingency lists for the device graph kernels
+// (cuda/islanding.cu).
+SplitGraphDesc split_graph_desc(const Grid& g) {
+  SplitGraphDesc gd;
+  gd.n_nodes = g.n_nodes();
+  gd.br_from.assign(g.br_from.begin(), g.br_from.end());
+  gd.br_to.assign(g.br_to.begin(), g.br_to.end());
+  gd.br_on.assign(g.br_on.begin(), g.br_on.end());
+  std::vector<int> deg(g.n_nodes() + 1, 0);
+  for (int e = 0; e < g.n_branches(); ++e) ++deg[g.br_from[e] + 1], ++deg[g.br_to[e] + 1];
+  for (int v = 0; v < g.n_nodes(); ++v) deg[v + 1] += deg[v];
+  gd.node_ptr = deg;
+  gd.node_br.assign(deg.back(), 0);
+  std::vector<int> fill(deg.begin(), deg.end() - 1);
+  for (int e = 0; e < g.n_branches(); ++e) gd.node_br[fill[g.br_from[e]]++] = e, gd.node_br[fill[g.br_to[e]]++] = e;
+  for (const auto& brs : g.cont_branches) {
+    if (brs.size() == 1) gd.single_br.push_back(brs[0]);
+    if (brs.size() > 1) {
+      gd.multi_br.insert(gd.multi_br.end(), brs.begin(), brs.end());
+      gd.multi_ptr.push_back(static_cast<int>(gd.multi_br.size()));
+    }
+    gd.cont_br.insert(gd.cont_br.end(), brs.begin(), brs.end());
+    gd.cont_ptr.push_back(static_cast<int>(gd.cont_br.size()));
+  }
+  return gd;
+}
+
+// importer.cpp:42-70. device >= 0: the bridge passes (the base graph and the
+// graph without each contingency's branches) run on that GPU, one CTA per pass
+// (cuda/islanding.cu); a pass whose graph splits into components falls back to
+// the host's general bridge search.
+std::vector<int> enumerate_disconnectables(const Grid& g, int device) {
   const int ne = g.n_branches(), n = g.n_nodes();
   std::vector<Edge> edges;
   for (int e = 0; e < ne; ++e) edges.push_back({g.br_from[e], g.br_to[e], g.br_on[e] != 0});
   std::vector<char> out_of_play(ne, 0);
   for (int e = 0; e < ne; ++e) out_of_play[e] = !g.br_on[e];
-  for (int e : bridges(n, edges)) out_of_play[e] = 1;
   for (const auto& brs : g.cont_branches)
     for (int e : brs) out_of_play[e] = 1;
-  for (const auto& brs : g.cont_branches) {
-    if (brs.empty()) continue;
+  auto host_pass = [&](int c) {  // c = contingency, or -1: the base graph
     auto cut = edges;
-    for (int e : brs) cut[e].on = false;
+    if (c >= 0)
+      for (int e : g.cont_branches[c]) cut[e].on = false;
     for (int e : bridges(n, cut)) out_of_play[e] = 1;
+  };
+  if (device >= 0) {
+    std::vector<char> any;
+    std::vector<int> fb;
+    contingency_bridges_device(split_graph_desc(g), device, any, fb);
+    for (int e = 0; e < ne; ++e)
+      if (any[e]) out_of_play[e] = 1;
+    const int K = static_cast<int>(g.cont_branches.size());
+    for (int c : fb) host_pass(c < K ? c : -1);
+  } else {
+    host_pass(-1);
+    for (int c = 0; c < static_cast<int>(g.cont_branches.size()); ++c)
+      if (!g.cont_branches[c].empty()) host_pass(c);
   }
   std::vector<int> d;
   for (int e = 0; e < ne; ++e)
@@ -643,7 +688,16 @@ bool split_keeps_connected(const Grid& g, int s, const std::vector<char>& grp) {
 // importer.cpp:239-282 + 341-356. Ids: station order, then enumeration order.
 ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap, int device) {
   ActionTable t;
-  t.disconnectables = enumerate_disconnectables(g);
+  static const bool timing = std::getenv("TGB_IMPORT_TIMING") != nullptr;
+  auto t0 = std::chrono::steady_clock::now();
+  auto lap = [&](const char* what) {
+    if (!timing) return;
+    const auto t1 = std::chrono::steady_clock::now();
+    std::fprintf(stderr, "import %s: %.3f s\n", what, std::chrono::duration<double>(t1 - t0).count());
+    t0 = t1;
+  };
+  t.disconnectables = enumerate_disconnectables(g, device);
+  lap("disconnectables");
   t.station_range.assign(g.stations.size(), {-1, -1});
   std::vector<std::pair<int, std::vector<char>>> pending;  // (station, group) in enumeration order
   for (int s = 0; s < static_cast<int>(g.stations.size()); ++s) {
@@ -684,6 +738,7 @@ ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap, i
     }
     for (auto& grp : cands) pending.push_back({s, std::move(grp)});
   }
+  lap("enumeration");
   // realization + islanding validation of every candidate split are
   // independent (importer.cpp:288-356): fanned out over the host cores, ids
   // assigned afterwards in (station, enumeration) order as the reference does
@@ -695,27 +750,7 @@ ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap, i
     std::vector<char> realized(pending.size(), 0);
     for (std::size_t i = 0; i < pending.size(); ++i)
       realized[i] = realize(g.stations[pending[i].first], pending[i].second, real[i]);
-    SplitGraphDesc gd;
-    gd.n_nodes = g.n_nodes();
-    gd.br_from.assign(g.br_from.begin(), g.br_from.end());
-    gd.br_to.assign(g.br_to.begin(), g.br_to.end());
-    gd.br_on.assign(g.br_on.begin(), g.br_on.end());
-    std::vector<int> deg(g.n_nodes() + 1, 0);
-    for (int e = 0; e < g.n_branches(); ++e) ++deg[g.br_from[e] + 1], ++deg[g.br_to[e] + 1];
-    for (int v = 0; v < g.n_nodes(); ++v) deg[v + 1] += deg[v];
-    gd.node_ptr = deg;
-    gd.node_br.assign(deg.back(), 0);
-    {
-      std::vector<int> fill(deg.begin(), deg.end() - 1);
-      for (int e = 0; e < g.n_branches(); ++e) gd.node_br[fill[g.br_from[e]]++] = e, gd.node_br[fill[g.br_to[e]]++] = e;
-    }
-    for (const auto& brs : g.cont_branches) {
-      if (brs.size() == 1) gd.single_br.push_back(brs[0]);
-      if (brs.size() > 1) {
-        gd.multi_br.insert(gd.multi_br.end(), brs.begin(), brs.end());
-        gd.multi_ptr.push_back(static_cast<int>(gd.multi_br.size()));
-      }
-    }
+    const SplitGraphDesc gd = split_graph_desc(g);
     SplitCandidates cd;
     std::vector<std::size_t> idx;
     for (std::size_t i = 0; i < pending.size(); ++i) {

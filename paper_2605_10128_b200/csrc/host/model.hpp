@@ -130,7 +130,8 @@ struct ActionTable {
 // contingency tiles of the sweep so each tile is electrically compact.
 std::vector<int> locality_rank(int n, const std::vector<std::pair<int, int>>& edges, int leaf = 48);
 
-std::vector<int> enumerate_disconnectables(const Grid& g);
+// device >= 0: the bridge passes on that GPU (cuda/islanding.cu), same result
+std::vector<int> enumerate_disconnectables(const Grid& g, int device = -1);
 // device >= 0: the islanding validation of the candidate splits runs on that
 // GPU (cuda/islanding.cu) instead of the host threads; same ids.
 ActionTable build_actions(const Grid& g, std::uint64_t seed, std::int64_t cap, int device = -1);
