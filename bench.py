@@ -364,14 +364,51 @@ def run_ac(args, world, rank):
         print(json.dumps(line), flush=True)
 
 
+def run_import(args, world, rank):
+    """Import stage: build_action_set (importer.cpp:42-70, 239-356) of the
+    config's grid with the bridge passes and the split islanding validation on the GPU
+    (tg_actionset_build_device), against the same algorithm on the host cores."""
+    if rank != 0:
+        return
+    import paper_2605_10128_b200 as P
+    cfgname = args.config if args.config in CONFIGS else "cfg4"
+    text = grid_text(cfgname)
+    grid = P.grid_from_json_text(text)
+    P.build_action_set(grid, device=0)  # warm-up (context, module load)
+    times = []
+    for _ in range(max(args.steps, 1)):
+        t0 = time.perf_counter()
+        acts = P.build_action_set(grid, device=0)
+        times.append(time.perf_counter() - t0)
+    dev_s = statistics.median(times)
+    t0 = time.perf_counter()
+    host = P.build_action_set(grid)
+    host_s = time.perf_counter() - t0
+    same = (host.n_actions == acts.n_actions and host.groups == acts.groups
+            and host.disconnectables.tolist() == acts.disconnectables.tolist())
+    line = {"metric": "action-set import time", "value": dev_s, "unit": "s", "n_gpus": 1, "steps": len(times),
+            "warmup": 1, "ms_per_step": 1000 * dev_s, "higher_is_better": False, "scaling": "strong",
+            "vs_baseline": None, "dtype": "int32", "data": "synthetic grid as named",
+            "config": {"workload": CONFIGS[cfgname]["workload"] + "; build_action_set only",
+                       "n_actions": acts.n_actions, "n_disconnectables": len(acts.disconnectables),
+                       "identical_to_host": bool(same)},
+            "gpu_launches": 2,
+            "cpu_baseline": {"value": host_s, "unit": "s", "cores": os.cpu_count() or 1, "kind": "port",
+                             "sample": "the same build_action_set on the host (enumerate_disconnectables on one "
+                                       "thread as in importer.cpp:42-70, split validation on all threads)"},
+            "e2e": {"value": dev_s, "unit": "s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=50)
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--config", default="cfg4", choices=sorted(set(CONFIGS) | set(AC_CONFIGS)))
-    ap.add_argument("--stage", default="dc", choices=["dc", "ac"],
-                    help="dc: the MapElites DC N-1 loop (north_star); ac: the AC validation stage")
+    ap.add_argument("--stage", default="dc", choices=["dc", "ac", "import"],
+                    help="dc: the MapElites DC N-1 loop (north_star); ac: the AC validation stage; "
+                         "import: build_action_set with the graph passes on the GPU")
     ap.add_argument("--impl", default="b200", choices=["b200", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--rng", default="replay", choices=["replay", "philox"],
@@ -387,6 +424,9 @@ def main():
     world, rank, local = dist_setup()
     if args.stage == "ac":
         run_ac(args, world, rank)
+        return
+    if args.stage == "import":
+        run_import(args, world, rank)
         return
     if args.impl == "reference":
         run_reference(args, world, rank)
