@@ -464,7 +464,7 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
 }
 
 template <int NT>
-__global__ void __launch_bounds__(NT) k_ac_case(AcGrid g, AcTopo tp, AcCases io, AcSolver sv) {
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? 2 : 14)) k_ac_case(AcGrid g, AcTopo tp, AcCases io, AcSolver sv) {
   extern __shared__ __align__(16) unsigned char ac_smem[];
   unsigned char* base = sv.in_smem ? ac_smem : sv.scratch + static_cast<size_t>(blockIdx.x) * sv.ws_bytes;
   AcWs w;
