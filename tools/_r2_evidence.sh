@@ -18,3 +18,5 @@ NCU="timeout 900 ncu --set full --import-source on --clock-control none"
 $NCU -k regex:k_sweep_chunked --launch-skip 4 -c 1 -o gpurun_out/chunked_cfg4_${TAG} python tools/step_timing.py cfg4 16384 > /dev/null 2>&1
 $NCU -k regex:"k_prep_rows|k_finish" --launch-skip 8 -c 4 -o gpurun_out/prepfin_cfg4_${TAG} python tools/step_timing.py cfg4 16384 > /dev/null 2>&1
 $NCU -k regex:k_sweep_chunked --launch-skip 4 -c 1 -o gpurun_out/chunked_cfg2_${TAG} python tools/step_timing.py cfg2 4096 > /dev/null 2>&1
+timeout 600 python bench.py --stage import --config cfg4 --steps 5 > gpurun_out/${TAG}_bench_import_cfg4.json 2> gpurun_out/${TAG}_bench_import_cfg4.err
+timeout 2000 python -m pytest tests -m gpu -q > gpurun_out/${TAG}_pytest.log 2>&1; echo "pytest rc=$?" >> gpurun_out/${TAG}_pytest.log
