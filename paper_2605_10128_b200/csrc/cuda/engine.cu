@@ -1186,9 +1186,13 @@ int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch&
   if (g.PhiA && !b.feat_mt && !b.amx_mt && !b.topo_sol && !split_off) {
     if (b.n == 0) return 0;
     k_prep_solve<<<b.n < 65535 ? b.n : 65535, 32, 0, stream>>>(g, b);
-    k_prep_rows<0, 4><<<148 * 8, 256, 0, stream>>>(g, b);
-    k_prep_rows<5, kChunkedMaxRank><<<148 * 8, 256, 0, stream>>>(g, b);  // without the rank 8-11 registers
-    k_prep_rows<kChunkedMaxRank + 1, kSweepRank><<<148 * 8, 256, 0, stream>>>(g, b);
+    // grid: the warp work items a class can have at most (small batches launch
+    // few CTAs), at most 8 CTAs per SM
+    const long seg = (b.nchunks + g.Kpad / 32 + kPrepSeg - 1) / kPrepSeg;
+    const int rows_grid = static_cast<int>(std::min<long>(148 * 8, (static_cast<long>(b.n) * seg + 7) / 8));
+    k_prep_rows<0, 4><<<rows_grid, 256, 0, stream>>>(g, b);
+    k_prep_rows<5, kChunkedMaxRank><<<rows_grid, 256, 0, stream>>>(g, b);  // without the rank 8-11 registers
+    k_prep_rows<kChunkedMaxRank + 1, kSweepRank><<<rows_grid, 256, 0, stream>>>(g, b);
     return 4;
   }
   const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);

@@ -50,6 +50,37 @@ struct Mt64 {
   }
 };
 
+// The same engine with its 312-word state in shared memory (k_offspring: the
+// per-lane state in local memory spilled to L2, and every lazily twisted draw
+// waited on it)
+struct Mt64S {
+  static constexpr int kN = Mt64::kN, kM = Mt64::kM;
+  unsigned long long* mt;
+  int i;
+  __device__ void bind(unsigned long long* state) { mt = state; }
+  __device__ void seed(unsigned long long s) {
+    unsigned long long x = s;
+    mt[0] = x;
+    for (int k = 1; k < kN; ++k) {
+      x = 6364136223846793005ull * (x ^ (x >> 62)) + k;
+      mt[k] = x;
+    }
+    i = 0;
+  }
+  __device__ unsigned long long next() {
+    const int k = i;
+    const unsigned long long x = (mt[k] & 0xFFFFFFFF80000000ull) | (mt[k + 1 < kN ? k + 1 : 0] & 0x7FFFFFFFull);
+    unsigned long long y = mt[k + kM < kN ? k + kM : k + kM - kN] ^ (x >> 1) ^ ((x & 1ull) ? 0xB5026F5AA96619E9ull : 0ull);
+    mt[k] = y;
+    i = k + 1 < kN ? k + 1 : 0;
+    y ^= (y >> 29) & 0x5555555555555555ull;
+    y ^= (y << 17) & 0x71D67FFFEDA60000ull;
+    y ^= (y << 37) & 0xFFF7EEE000000000ull;
+    y ^= y >> 43;
+    return y;
+  }
+};
+
 // Philox4x32-10 (Salmon et al., SC'11): counter-based, stateless per draw; the
 // lane key is the same derive_seed(seed, iter, lane + 1) the replay mode seeds
 // mt19937_64 with, the counter is the draw index. Two 64-bit draws per block.
@@ -58,6 +89,7 @@ struct Philox {
   uint32_t ctr = 0;
   unsigned long long buf = 0;
   bool have = false;
+  __device__ void bind(unsigned long long*) {}
   __device__ void seed(unsigned long long s) {
     k0 = static_cast<uint32_t>(s);
     k1 = static_cast<uint32_t>(s >> 32);
@@ -380,15 +412,18 @@ __device__ const int* member(const Archive& a, const QdParams& p, int ns, int fl
 // beside the lanes' own seeding instead of before it.
 constexpr int kOffspringLanes = 64;
 
-template <class Rng>
+template <class Rng, int L = kOffspringLanes>
 __global__ void k_offspring(DevGrid g, QdParams p, Archive a, int* genomes) {
   __shared__ int b_mc;
+  extern __shared__ unsigned long long rng_state[];  // Mt64S: (L + 1) x 312 words
   const long long it = a.iter[0];
-  const int lane = blockIdx.x * kOffspringLanes + static_cast<int>(threadIdx.x);
-  const bool is_lane = threadIdx.x < kOffspringLanes && lane < p.batch;
+  const int lane = blockIdx.x * L + static_cast<int>(threadIdx.x);
+  const bool is_lane = threadIdx.x < L && lane < p.batch;
   Rng r;
-  if (threadIdx.x == kOffspringLanes) {
+  r.bind(rng_state + static_cast<size_t>(threadIdx.x < L ? threadIdx.x : L) * Mt64::kN);
+  if (threadIdx.x == L) {
     Rng ir;
+    ir.bind(rng_state + static_cast<size_t>(L) * Mt64::kN);
     ir.seed(derive_seed(p.seed, 0x17e7ull, static_cast<unsigned long long>(it)));
     b_mc = uniform_int(ir, 0, p.batch);
   } else if (is_lane) {
@@ -751,7 +786,15 @@ void launch_offspring(const DevGrid& g, const QdState& q, int* genomes, cudaStre
   if (q.p.rng == kRngPhilox)
     k_offspring<Philox><<<blocks, kOffspringLanes + 32, 0, s>>>(g, q.p, q.a, genomes);
   else
-    k_offspring<Mt64><<<blocks, kOffspringLanes + 32, 0, s>>>(g, q.p, q.a, genomes);
+  {
+    // replay engine: 32 lanes per block with their states in shared memory
+    constexpr int kL = 32;
+    const size_t smem = static_cast<size_t>(kL + 1) * Mt64::kN * sizeof(unsigned long long);
+    static std::atomic<unsigned long long> configured{0};
+    if (first_use_on_device(configured))
+      cudaFuncSetAttribute(k_offspring<Mt64S, kL>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    k_offspring<Mt64S, kL><<<(q.p.batch + kL - 1) / kL, kL + 32, smem, s>>>(g, q.p, q.a, genomes);
+  }
 }
 
 namespace {

@@ -1418,7 +1418,9 @@ void launch_sweep(const DevGrid& g, Batch& b, bool full, cudaStream_t stream, cu
     // ranks 0..7 in one persistent kernel (one work list, no tail between
     // rank classes; every rank variant fits the same 128 registers)
     cudaMemsetAsync(b.item_ctr, 0, sizeof(unsigned int), stream);
-    k_sweep_chunked<0, kChunkedMaxRank><<<148 * 2, kCkThreads, kCkSmemBytes, stream>>>(g, b, ntiles, b.item_ctr);
+    // persistent: 2 CTAs per SM, fewer when the batch has fewer (candidate, tile) items than warps
+    const int ck_grid = static_cast<int>(std::max<long>(1, std::min<long>(148 * 2, (static_cast<long>(b.n) * ntiles + kCkWarps - 1) / kCkWarps)));
+    k_sweep_chunked<0, kChunkedMaxRank><<<ck_grid, kCkThreads, kCkSmemBytes, stream>>>(g, b, ntiles, b.item_ctr);
     k_sweep_hi<false, kTmSingle, false><<<kHiCtas, kThreads, kSmemBytes, stream>>>(g, b, ntiles);
   } else if (half) {
     k_sweep<false, kTmSingle, true><<<grid * hh, hw, kHalfSmemBytes, stream>>>(g, b, ntiles, ngroups, gblock);
