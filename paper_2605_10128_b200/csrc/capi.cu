@@ -1196,6 +1196,9 @@ void context_build(tg_context* ctx, const tg_grid_desc* gd, const tg_actionset_d
       gv.alpha0 = alpha0;
       tgb::launch_base_tables(gv, d_pr, theta0, f0, tdiag, tk, tmax, alpha0, s);
       check(cudaGetLastError(), "base tables");
+      double4* rstat = A.alloc<double4>(std::max(E, 1));
+      tgb::launch_row_static(gv, f0, rstat, s);
+      gv.row_static = rstat;
       if (g.Kpad > 0) {
         float* crec = A.alloc<float>(static_cast<size_t>(ntiles) * ((E + tgb::kChunkRows - 1) / tgb::kChunkRows) *
                                      tgb::kRec);

@@ -44,6 +44,7 @@ struct DevGrid {
   const double* X;         // [Nr*Nr] inverse reduced susceptance (symmetric)
   const double* theta0;    // [Nr]  base angles X * p_red
   const double* f0;        // [E]   base flows
+  const double4* row_static;  // [E] (f0, b, limit, in service) packed: one load per row in k_prep_rows
   const double* Tdiag;     // [E]   b_e a_e^T X a_e
   const int* node_ptr;     // [N+1] in-service incident branches
   const int* node_br;

@@ -377,27 +377,37 @@ __device__ __forceinline__ void prep_branch_chunk(const DevGrid& g, const Batch&
 #pragma unroll
   for (int i = 0; i < RS; ++i) row[i] = 0.0;
   bool on = false;
+  // the row's static data (f0, b, limit, in service) in one load, issued first
+  double4 rs = make_double4(0.0, 0.0, 0.0, 0.0);
+  if (e < g.E) {
+    const double2* p = reinterpret_cast<const double2*>(g.row_static + e);
+    const double2 a = __ldg(p), b2 = __ldg(p + 1);
+    rs = make_double4(a.x, a.y, b2.x, b2.y);
+  }
   if (e < g.E) {
     double z[R > 0 ? R : 1];
-    on = pc_features<R>(g, t, f, mv_bits, rm_bits, ns, e, z);
+    pc_features<R>(g, t, f, mv_bits, rm_bits, ns, e, z);  // (its live flag: rs.w and rm_bits, below)
+    on = rs.w != 0.0 && !bit_get(rm_bits, e);
     if (on) {
-      row[0] = pc_flow<R>(g, f, e, z);
-      const double be = g.br_b[e];
+      double acc = 0.0;
 #pragma unroll
-      for (int q = 0; q < R; ++q) row[1 + q] = be * z[q];
+      for (int q = 0; q < R; ++q) acc = fma(z[q], f.Rp[q], acc);
+      row[0] = rs.x + rs.y * acc;  // pc_flow
+#pragma unroll
+      for (int q = 0; q < R; ++q) row[1 + q] = rs.y * z[q];
     }
   }
-  const unsigned over = __ballot_sync(0xffffffffu, e < g.E && fabs(row[0]) > g.br_lim[e < g.E ? e : 0]);
+  const unsigned over = __ballot_sync(0xffffffffu, e < g.E && fabs(row[0]) > rs.z);
   if (lane == 0 && over) atomicAdd(b.nc0 + c, __popc(over));
   if (R <= kChunkedMaxRank) {
     float v[kCsum];
-    v[0] = on ? __double2float_ru(fabs(row[0] - g.f0[e])) : 0.0f;
+    v[0] = on ? __double2float_ru(fabs(row[0] - rs.x)) : 0.0f;
 #pragma unroll
     for (int q = 0; q + 1 < kCsum; ++q) v[1 + q] = on && q < R ? __double2float_ru(fabs(row[1 + (q < R ? q : 0)])) : 0.0f;
     // ranks <= kCsum - 2: the last slot carries max_e (|f_c - f0|_e - (lim_e - |f0_e|))
     // for the row-coupled chunk test (setup.cu k_chunk_rec); dead rows never overload
     if (R + 2 <= kCsum)
-      v[kCsum - 1] = on ? __double2float_ru(fabs(row[0] - g.f0[e]) - (g.br_lim[e] - fabs(g.f0[e]))) : -CUDART_INF_F;
+      v[kCsum - 1] = on ? __double2float_ru(fabs(row[0] - rs.x) - (rs.z - fabs(rs.x))) : -CUDART_INF_F;
     warp_max_summary(v);
     if (lane == 0) {
       float4* dst = reinterpret_cast<float4*>(b.csum + (static_cast<size_t>(c) * b.nchunks + chunk) * kCsum);

@@ -219,6 +219,8 @@ void launch_row_headroom(const DevGrid& g, const double* p_red, double* theta0, 
 void launch_phi_columns(const DevGrid& g, double* phiA, int* act_nmv, double* psiD, cudaStream_t stream);
 // Chunk records (DevGrid::Crec) from a profile's skip records, base flows and limits.
 void launch_chunk_records(const DevGrid& g, float* crec, cudaStream_t stream);
+// DevGrid::row_static from the profile's base flows
+void launch_row_static(const DevGrid& g, const double* f0, double4* out, cudaStream_t stream);
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
                         float* tmax, double* alpha0, cudaStream_t stream);
 

@@ -77,6 +77,11 @@ __global__ void k_theta(DevGrid g, const double* p_red, double* theta) {
   }
 }
 
+__global__ void k_row_static(DevGrid g, const double* f0, double4* out) {
+  for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < g.E; e += gridDim.x * blockDim.x)
+    out[e] = make_double4(f0[e], g.br_b[e], g.br_lim[e], g.br_on[e] ? 1.0 : 0.0);
+}
+
 __global__ void k_branch_base(DevGrid g, const double* theta, double* f0, double* tdiag) {
   for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < g.E; e += gridDim.x * blockDim.x) {
     const int ri = g.red[g.br_from[e]], rj = g.red[g.br_to[e]];
@@ -373,6 +378,10 @@ bool device_spd_inverse(double* a, int n, cudaStream_t stream) {
   cudaFree(dmax);
   cudaFree(bad);
   return hbad == 0;
+}
+
+void launch_row_static(const DevGrid& g, const double* f0, double4* out, cudaStream_t stream) {
+  if (g.E > 0) k_row_static<<<(g.E + 255) / 256, 256, 0, stream>>>(g, f0, out);
 }
 
 void launch_base_tables(const DevGrid& g, const double* p_red, double* theta0, double* f0, double* tdiag, double* tk,
