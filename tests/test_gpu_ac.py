@@ -319,3 +319,56 @@ def test_stages_vs_oracle(data_dir):
                 assert rec.stage == 2 and rec.reason == r2[i] and rec.accepted == acc[i]
         assert len(val.records()) == 40
         assert val.ctx.kernel_launches() > 0
+
+
+def test_pipeline_snapshot_to_ac_hand_off(data_dir):
+    """The consumer side of the hot path (pipeline.cpp:380-425): the DC loop's
+    snapshots feed the AC validator — candidates deduplicated by canonical key,
+    eliminate(), the queue validated (two device batches), pruned ones
+    recorded — and every verdict equals the oracle's worst_k_check /
+    full_validation of the same genome."""
+    import paper_2605_10128_b200 as P
+    from paper_2605_10128_b200.ac import Candidate, RejectionReason, ValidationStage, record_to_json
+
+    text = open(os.path.join(data_dir, "grid14_congested.json")).read()
+    val, dc, orc, oac = _pair(text)
+    snaps = []
+    P.run_optimizer(dc, P.QdConfig(seed=3, batch_size=64, iters_per_epoch=5, max_evaluations=641),
+                    sink=lambda s: snaps.append(s))
+    assert snaps and snaps[-1].final
+    resolved = set()
+    n_val = 0
+    for snap in snaps:
+        cands, seen = [], set()
+        for e in snap.entries:
+            if e.genome.is_empty():
+                continue
+            key = e.genome.canonical_key()
+            if key in resolved or key in seen:
+                continue
+            seen.add(key)
+            cands.append(Candidate(e.genome, e.score))
+        if not cands:
+            continue
+        out = val.eliminate(cands)
+        queue = [cands[i] for i in out.queue]
+        recs = val.validate_queue(queue)
+        for c, rec in zip(queue, recs):
+            g = np.array([c.genome.action_slots + c.genome.disconnection_slots], np.int32)
+            wi = np.array([[k for k, _ in c.dc_score.worst_contingencies] or [-1]], np.int32)
+            wn = np.array([len(c.dc_score.worst_contingencies)], np.int32)
+            early = int(oac.worst_k_check(g, 3, 2, wi, wn)[0])
+            if early != RejectionReason.None_:
+                assert rec.stage == ValidationStage.WorstK and int(rec.reason) == early
+            else:
+                reason, acc, lo = oac.full_validation(g, 3, 2)
+                assert rec.stage == ValidationStage.FullN1 and int(rec.reason) == int(reason[0])
+                assert rec.accepted == bool(acc[0])
+                assert abs(rec.ac_lambda_o - lo[0]) <= TOL * max(1.0, abs(lo[0]))
+            json.loads(record_to_json(rec, val.grid, val.actions))
+            resolved.add(c.genome.canonical_key())
+            n_val += 1
+        for i, why in out.pruned:
+            val.record_elimination(cands[i], why)
+            resolved.add(cands[i].genome.canonical_key())
+    assert n_val > 0 and len(val.records()) == len(resolved)
