@@ -15,6 +15,7 @@
 #include "../../include/topopt_b200.h"
 #include "cuda/ac.cuh"
 #include "cuda/engine.cuh"
+#include "cuda/islanding.cuh"
 #include "cuda/qd.cuh"
 #include "host/model.hpp"
 #include "host/snapshot.hpp"
@@ -764,6 +765,8 @@ tg_status tg_actionset_build_device(const tg_grid* grid, uint64_t seed, int64_t 
     auto a = std::make_unique<tg_actionset>();
     try {
       a->t = tgb::build_actions(grid->g, seed, cap > 0 ? cap : (int64_t{1} << 23), device);
+    } catch (const tgb::SplitCapacityError& e) {
+      throw CapacityFailure(e.what());
     } catch (const std::runtime_error& e) {
       if (dynamic_cast<const tgb::ParseError*>(&e) || dynamic_cast<const tgb::ValidationError*>(&e)) throw;
       throw CudaFailure(e.what());

@@ -302,7 +302,7 @@ void validate_splits_device(const SplitGraphDesc& gd, const SplitCandidates& cd,
   int max_moved = 0;
   for (int i = 0; i < n; ++i) max_moved = std::max(max_moved, cd.moved_ptr[i + 1] - cd.moved_ptr[i]);
   if (max_moved > kIslMaxMoved)
-    throw std::runtime_error("a station split moves " + std::to_string(max_moved) + " branch ends (device limit " +
+    throw SplitCapacityError("a station split moves " + std::to_string(max_moved) + " branch ends (device limit " +
                              std::to_string(kIslMaxMoved) + ")");
   std::vector<void*> owned;
   struct Free {

@@ -2,9 +2,16 @@
 #pragma once
 
 #include <cstdint>
+#include <stdexcept>
 #include <vector>
 
 namespace tgb {
+
+// a candidate split beyond the kernel's shared-memory capacity (reported as
+// TG_CAPACITY_ERROR by the C ABI, never truncated)
+struct SplitCapacityError : std::runtime_error {
+  using std::runtime_error::runtime_error;
+};
 
 // Base branch graph and the listed contingencies (grid order).
 struct SplitGraphDesc {
