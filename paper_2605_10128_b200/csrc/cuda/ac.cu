@@ -119,6 +119,32 @@ __device__ int block_argmax(double v, int idx, double* red, int* ired) {
   return bi;
 }
 
+// block_argmax for the LU's column loop: the LU's own barriers already order
+// the previous column's reads of red / ired before this write, and the
+// per-warp winners are reduced by shuffles (one total order on (value, index),
+// so the result is block_argmax's)
+template <int NT>
+__device__ int lu_argmax(double v, int idx, double* red, int* ired) {
+  for (int o = 16; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) v = ov, idx = oi;
+  }
+  const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  constexpr int NW = NT / 32;
+  static_assert(NW >= 2 && (NW & (NW - 1)) == 0, "warps per CTA: a power of two");
+  if (lane == 0) red[w] = v, ired[w] = idx;
+  __syncthreads();
+  v = red[lane & (NW - 1)];  // every group of NW lanes reduces a full copy
+  idx = ired[lane & (NW - 1)];
+  for (int o = NW / 2; o > 0; o >>= 1) {
+    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
+    if (ov > v || (ov == v && oi < idx)) v = ov, idx = oi;
+  }
+  return idx;
+}
+
 __device__ __forceinline__ bool in_list(const int* lo, const int* hi, int x) {
   for (const int* p = lo; p < hi; ++p)
     if (*p == x) return true;
@@ -160,7 +186,7 @@ __device__ void lu_solve(double* J, double* dx, double* lm, int nu, double* red,
       const double a = fabs(J[static_cast<size_t>(i) * nu + k]);
       if (a > best) best = a, bi = i;
     }
-    int p = block_argmax<NT>(best, bi, red, ired);
+    int p = lu_argmax<NT>(best, bi, red, ired);
     if (p >= nu) p = k;
     if (p != k) {
       for (int j = k + tid; j < nu; j += NT) {
@@ -193,10 +219,39 @@ __device__ void lu_solve(double* J, double* dx, double* lm, int nu, double* red,
       if (l0 == 0.0 && l1 == 0.0) continue;
       double* r0 = J + static_cast<size_t>(i) * nu;
       double* r1 = r0 + nu;
-      for (int j = k + 1 + (tid & 31); j < nu; j += 32) {
-        const double x = rk[j];
-        if (l0 != 0.0) r0[j] -= l0 * x;
-        if (l1 != 0.0) r1[j] -= l1 * x;
+      if constexpr (NT >= 256) {
+        // four column groups per pass, all loads issued before the stores (the
+        // rows may alias as far as the compiler knows, so a plain loop would wait
+        // out each load's latency: the scratch path's rows live in L1 / L2)
+        for (int jb = k + 1 + (tid & 31); jb < nu; jb += 4 * 32) {
+          double x[4], a0[4], a1[4];
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = jb + 32 * u;
+            x[u] = j < nu ? rk[j] : 0.0;
+            a0[u] = j < nu ? r0[j] : 0.0;
+            a1[u] = two && j < nu ? r1[j] : 0.0;
+          }
+#pragma unroll
+          for (int u = 0; u < 4; ++u) {
+            const int j = jb + 32 * u;
+            if (j >= nu) break;
+            if (l0 != 0.0) {
+              a0[u] -= l0 * x[u];
+              r0[j] = a0[u];
+            }
+            if (l1 != 0.0) {
+              a1[u] -= l1 * x[u];
+              r1[j] = a1[u];
+            }
+          }
+        }
+      } else {
+        for (int j = k + 1 + (tid & 31); j < nu; j += 32) {
+          const double x = rk[j];
+          if (l0 != 0.0) r0[j] -= l0 * x;
+          if (l1 != 0.0) r1[j] -= l1 * x;
+        }
       }
     }
     __syncthreads();
