@@ -518,12 +518,29 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
   __syncthreads();
 }
 
+// the workspace sections at base, from the layout's offsets (rel = the layout
+// at address 0, computed on the host: a kernel parameter, so the section
+// pointers cost one add wherever the compiler rematerializes them)
+__device__ __forceinline__ AcWs rebase(const AcWs& rel, unsigned char* base) {
+  auto d = [&](double* p) { return reinterpret_cast<double*>(base + reinterpret_cast<size_t>(p)); };
+  auto i = [&](int* p) { return reinterpret_cast<int*>(base + reinterpret_cast<size_t>(p)); };
+  AcWs w;
+  w.J = d(rel.J), w.Gd = d(rel.Gd), w.Bd = d(rel.Bd), w.vm = d(rel.vm), w.va = d(rel.va), w.P = d(rel.P);
+  w.Q = d(rel.Q), w.psp = d(rel.psp), w.qsp = d(rel.qsp), w.vset = d(rel.vset), w.dx = d(rel.dx);
+  w.lm = d(rel.lm), w.red = d(rel.red);
+  w.bus_of = i(rel.bus_of), w.node_of = i(rel.node_of), w.ang = i(rel.ang), w.mag = i(rel.mag);
+  w.ang_pos = i(rel.ang_pos), w.mag_pos = i(rel.mag_pos), w.pv = i(rel.pv), w.reach = i(rel.reach);
+  w.ired = i(rel.ired);
+  w.live = base + reinterpret_cast<size_t>(rel.live);
+  return w;
+}
+
 template <int NT>
-__global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? 2 : 14)) k_ac_case(AcGrid g, AcTopo tp, AcCases io, AcSolver sv) {
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? 2 : 14))
+    k_ac_case(AcGrid g, AcTopo tp, AcCases io, AcSolver sv, AcWs rel) {
   extern __shared__ __align__(16) unsigned char ac_smem[];
   unsigned char* base = sv.in_smem ? ac_smem : sv.scratch + static_cast<size_t>(blockIdx.x) * sv.ws_bytes;
-  AcWs w;
-  ws_layout(sv.n_bus, sv.nu, g.E, base, &w);
+  const AcWs w = rebase(rel, base);
   for (int c = blockIdx.x; c < io.n; c += gridDim.x) solve_case<NT>(g, tp, io, sv, c, w);
 }
 
@@ -602,18 +619,20 @@ void ac_launch_cases(const AcGrid& g, const AcTopo& t, const AcCases& c, const A
                      cudaStream_t s) {
   if (c.n <= 0) return;
   const size_t smem = sv.in_smem ? sv.ws_bytes : 0;
+  AcWs rel;
+  ws_layout(sv.n_bus, sv.nu, g.E, nullptr, &rel);
   switch (ac_threads(sv.nu)) {
     case 64:
       cudaFuncSetAttribute(k_ac_case<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_ac_case<64><<<ctas, 64, smem, s>>>(g, t, c, sv);
+      k_ac_case<64><<<ctas, 64, smem, s>>>(g, t, c, sv, rel);
       break;
     case 256:
       cudaFuncSetAttribute(k_ac_case<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_ac_case<256><<<ctas, 256, smem, s>>>(g, t, c, sv);
+      k_ac_case<256><<<ctas, 256, smem, s>>>(g, t, c, sv, rel);
       break;
     default:
       cudaFuncSetAttribute(k_ac_case<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_ac_case<512><<<ctas, 512, smem, s>>>(g, t, c, sv);
+      k_ac_case<512><<<ctas, 512, smem, s>>>(g, t, c, sv, rel);
       break;
   }
 }
