@@ -1284,16 +1284,17 @@ __global__ void __launch_bounds__(kCkThreads, 2) k_sweep_chunked(DevGrid g, Batc
   __syncwarp();
   const int first = b.wl_start[RLO];
   const int ncand = b.wl_start[RHI] + b.wl_count[RHI] - first;
-  const long items = static_cast<long>(ncand) * ntiles;
+  const unsigned items = static_cast<unsigned>(ncand) * static_cast<unsigned>(ntiles);  // the item counter is 32-bit
   uint32_t phase = 0;
   unsigned stats[6] = {0, 0, 0, 0, 0, 0};
   for (;;) {
-    long it = 0;
+    unsigned it = 0;
     if (lane == 0) it = atomicAdd(ctr, 1u);
     it = __shfl_sync(0xffffffffu, it, 0);
     if (it >= items) break;
-    const int cid = b.wl_list[first + static_cast<int>(it / ntiles)];
-    const int tile = static_cast<int>(it % ntiles);
+    const unsigned ci = it / static_cast<unsigned>(ntiles);  // 32-bit division
+    const int cid = b.wl_list[first + static_cast<int>(ci)];
+    const int tile = static_cast<int>(it - ci * static_cast<unsigned>(ntiles));
     if (b.status[cid] != 0) continue;
     ck_dispatch<RLO, RHI>(g, b, b.rank[cid], cid, tile, ws, phase, stats);
   }
