@@ -532,12 +532,12 @@ __global__ void __launch_bounds__(32 * kPrepRowWarps, RHI <= 4 ? 4 : (RHI <= 7 ?
   const int nseg = (per + kPrepSeg - 1) / kPrepSeg;
   const int first = b.wl_start[RLO];
   const int ncand = b.wl_start[RHI] + b.wl_count[RHI] - first;
-  const long total = static_cast<long>(ncand) * nseg;
+  const unsigned total = static_cast<unsigned>(ncand) * static_cast<unsigned>(nseg);  // 32-bit: cheap division
   int loaded = -1;
-  for (long w = static_cast<long>(blockIdx.x) * kPrepRowWarps + warp; w < total;
-       w += static_cast<long>(gridDim.x) * kPrepRowWarps) {
-    const int c = b.wl_list[first + static_cast<int>(w / nseg)];
-    const int sg = static_cast<int>(w % nseg);
+  for (unsigned w = blockIdx.x * kPrepRowWarps + warp; w < total; w += gridDim.x * kPrepRowWarps) {
+    const unsigned ci = w / static_cast<unsigned>(nseg);
+    const int c = b.wl_list[first + static_cast<int>(ci)];
+    const int sg = static_cast<int>(w - ci * static_cast<unsigned>(nseg));
     if (b.status[c] != 0) continue;  // islanded by the small solve
     if (c != loaded) {
       __syncwarp();

@@ -981,6 +981,9 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
   uint8_t* ring = ws + kCkHead;
   const int kb = tile * kTileK + lane * kKpl;
   const int nch = b.nchunks;
+  // the candidate's row block (chunk 0; chunk j at + j * kGroupSlots * kChunkRows * S),
+  // its slot loaded at the item's start so the ring fills do not wait on it
+  const double* fbase = b.feat + feat_index(b.slot[cid], nch, 0, R);
   double alpha[kKpl], rr[kKpl][R > 0 ? R : 1], energy[kKpl];
   bool kval[kKpl];
   int kbr[kKpl], rem[kMaxRemovedSweep];
@@ -1083,8 +1086,8 @@ __device__ __forceinline__ void ck_item(const DevGrid& g, const Batch& b, int ci
     uint8_t* dst = ring + static_cast<size_t>(st) * Rg::stage;
     uint64_t* bar = bars + st;
     mbar_expect_tx(bar, static_cast<uint32_t>(Rg::stage));
-    const int slot = b.slot[cid];
-    bulk_g2s(dst, b.feat + feat_index(slot, nch, e0, R), static_cast<uint32_t>(Rg::F), bar);
+    bulk_g2s(dst, fbase + static_cast<size_t>(list[j]) * (kGroupSlots * kChunkRows * S), static_cast<uint32_t>(Rg::F),
+             bar);
     bulk_g2s(dst + Rg::F, g.br_lim + e0, static_cast<uint32_t>(Rg::L), bar);
     bulk_g2s(dst + Rg::F + Rg::L, g.Tmax + (static_cast<size_t>(tile) * (g.E + kChunk) + e0) * kRec,
              static_cast<uint32_t>(Rg::M), bar);
