@@ -493,7 +493,7 @@ __device__ __forceinline__ void prep_cont_chunk(const DevGrid& g, const Batch& b
 // Warp work item = (candidate of the rank class, segment of kPrepSeg
 // consecutive 32-row chunks: branch rows, then contingency rows). The
 // candidate's factors are staged once per segment in the warp's shared slab.
-constexpr int kPrepSeg = 8;
+constexpr int kPrepSeg = 16;
 constexpr int kPrepRowWarps = 8;
 
 template <int R>
