@@ -14,6 +14,7 @@ constexpr double kBaseMva = 100.0;  // ac_validator.cpp:14
 // Workspace of one case (offsets in bytes, 16-byte aligned sections).
 struct AcWs {
   double *J, *Gd, *Bd, *vm, *va, *P, *Q, *psp, *qsp, *vset, *dx, *lm, *red;
+  double *yb, *sc;  // [2E] y_ft of each live branch; [2 * 2E] sin / cos per branch-end slot of the grid CSR
   int *bus_of, *node_of, *ang, *mag, *ang_pos, *mag_pos, *pv, *reach, *ired;
   uint8_t* live;
 };
@@ -47,6 +48,8 @@ __host__ __device__ inline size_t ws_layout(int n_bus, int nu, int E, unsigned c
   t.dx = take_d(nn);
   t.lm = take_d(nn);
   t.red = take_d(64);
+  t.yb = take_d(2 * static_cast<size_t>(E));
+  t.sc = take_d(4 * static_cast<size_t>(E));
   t.bus_of = take_i(nb);
   t.node_of = take_i(nb);
   t.ang = take_i(nn);
@@ -280,8 +283,7 @@ __device__ __forceinline__ void for_each_branch_of_bus(const AcGrid& g, const Ac
     if (!w.live[e]) continue;
     const int a = ef[e], b = et[e];
     if (a != v && b != v) continue;  // this end moved to another section
-    const BranchY y = branch_y(g, e);  // y_ft = y_tf
-    fn(w.bus_of[a == v ? b : a], y.ftr, y.fti);
+    fn(w.bus_of[a == v ? b : a], w.yb[2 * e], w.yb[2 * e + 1], p);  // y_ft = y_tf
   }
 }
 
@@ -394,14 +396,25 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
   bool ok = false;
   int iters = 0;
   if (!floating) {
+    // the live branches' y_ft, formed once per case (the Newton loop reads them
+    // twice per iteration)
+    for (int e = tid; e < E; e += NT) {
+      if (!w.live[e]) continue;
+      const BranchY y = branch_y(g, e);
+      w.yb[2 * e] = y.ftr;
+      w.yb[2 * e + 1] = y.fti;
+    }
+    __syncthreads();
     for (int it = 1; it <= sv.max_iter; ++it) {  // ac_validator.cpp:175-244
       // bus injections (159-173)
       for (int i = tid; i < n; i += NT) {
         const double vi = w.vm[i], ai = w.va[i];
         double p = vi * vi * w.Gd[i], q = -vi * vi * w.Bd[i];
-        for_each_branch_of_bus(g, w, ef, et, split_node, i, [&](int k, double gik, double bik) {
+        for_each_branch_of_bus(g, w, ef, et, split_node, i, [&](int k, double gik, double bik, int slot) {
           double s, co;
           sincos(ai - w.va[k], &s, &co);
+          w.sc[2 * slot] = s;  // reused by the Jacobian (same angles)
+          w.sc[2 * slot + 1] = co;
           p += vi * w.vm[k] * (gik * co + bik * s);
           q += vi * w.vm[k] * (gik * s - bik * co);
         });
@@ -441,10 +454,9 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
           if (rp >= 0) JQ[rp] = w.P[i] - gii * vi * vi;
           JQ[rq] = w.Q[i] / vi - bii * vi;
         }
-        for_each_branch_of_bus(g, w, ef, et, split_node, i, [&](int k, double gik, double bik) {
+        for_each_branch_of_bus(g, w, ef, et, split_node, i, [&](int k, double gik, double bik, int slot) {
           const int ct = w.ang_pos[k], cv = w.mag_pos[k] >= 0 ? na + w.mag_pos[k] : -1;
-          double s, co;
-          sincos(w.va[i] - w.va[k], &s, &co);
+          const double s = w.sc[2 * slot], co = w.sc[2 * slot + 1];  // sincos(va_i - va_k) of the injections
           const double vk = w.vm[k];
           if (JP) {
             if (ct >= 0) JP[ct] += vi * vk * (gik * s - bik * co);
@@ -527,7 +539,7 @@ __device__ __forceinline__ AcWs rebase(const AcWs& rel, unsigned char* base) {
   AcWs w;
   w.J = d(rel.J), w.Gd = d(rel.Gd), w.Bd = d(rel.Bd), w.vm = d(rel.vm), w.va = d(rel.va), w.P = d(rel.P);
   w.Q = d(rel.Q), w.psp = d(rel.psp), w.qsp = d(rel.qsp), w.vset = d(rel.vset), w.dx = d(rel.dx);
-  w.lm = d(rel.lm), w.red = d(rel.red);
+  w.lm = d(rel.lm), w.red = d(rel.red), w.yb = d(rel.yb), w.sc = d(rel.sc);
   w.bus_of = i(rel.bus_of), w.node_of = i(rel.node_of), w.ang = i(rel.ang), w.mag = i(rel.mag);
   w.ang_pos = i(rel.ang_pos), w.mag_pos = i(rel.mag_pos), w.pv = i(rel.pv), w.reach = i(rel.reach);
   w.ired = i(rel.ired);
