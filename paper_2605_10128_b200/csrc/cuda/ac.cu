@@ -128,24 +128,29 @@ __device__ int block_argmax(double v, int idx, double* red, int* ired) {
 // so the result is block_argmax's)
 template <int NT>
 __device__ int lu_argmax(double v, int idx, double* red, int* ired) {
-  for (int o = 16; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-    if (ov > v || (ov == v && oi < idx)) v = ov, idx = oi;
-  }
+  // (value, index) as an ordered key: v is -1 (no candidate) or some |a_ik|
+  // (never NaN), whose bit pattern orders like the value; + 1 puts 0.0 above
+  // "no candidate". The largest key, then the smallest index among its
+  // holders: three REDUX steps per warp (the shuffle butterfly's result).
+  const unsigned long long key = v >= 0.0 ? static_cast<unsigned long long>(__double_as_longlong(v)) + 1ull : 0ull;
+  auto warp_pick = [](unsigned long long k, unsigned i, unsigned long long& wk) {
+    const unsigned hi = static_cast<unsigned>(k >> 32), lo = static_cast<unsigned>(k);
+    const unsigned mhi = __reduce_max_sync(0xffffffffu, hi);
+    const unsigned mlo = __reduce_max_sync(0xffffffffu, hi == mhi ? lo : 0u);
+    wk = (static_cast<unsigned long long>(mhi) << 32) | mlo;
+    return __reduce_min_sync(0xffffffffu, hi == mhi && lo == mlo ? i : 0xffffffffu);
+  };
+  unsigned long long wk;
+  unsigned wi = warp_pick(key, static_cast<unsigned>(idx), wk);
   const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
   constexpr int NW = NT / 32;
   static_assert(NW >= 2 && (NW & (NW - 1)) == 0, "warps per CTA: a power of two");
-  if (lane == 0) red[w] = v, ired[w] = idx;
+  unsigned long long* rk = reinterpret_cast<unsigned long long*>(red);
+  if (lane == 0) rk[w] = wk, ired[w] = static_cast<int>(wi);
   __syncthreads();
-  v = red[lane & (NW - 1)];  // every group of NW lanes reduces a full copy
-  idx = ired[lane & (NW - 1)];
-  for (int o = NW / 2; o > 0; o >>= 1) {
-    const double ov = __shfl_xor_sync(0xffffffffu, v, o);
-    const int oi = __shfl_xor_sync(0xffffffffu, idx, o);
-    if (ov > v || (ov == v && oi < idx)) v = ov, idx = oi;
-  }
-  return idx;
+  // every group of NW lanes holds a full copy of the per-warp winners
+  wi = warp_pick(rk[lane & (NW - 1)], static_cast<unsigned>(ired[lane & (NW - 1)]), wk);
+  return static_cast<int>(wi);
 }
 
 __device__ __forceinline__ bool in_list(const int* lo, const int* hi, int x) {
