@@ -560,7 +560,7 @@ __global__ void __launch_bounds__(32 * kPrepRowWarps, RHI <= 4 ? 4 : (RHI <= 7 ?
 // profiles, and each contingency's rk row once and its alpha per profile
 // (R'_t = rk * alpha_t is formed by the masked sweep); the bounds of the mask
 // pass are folded over the profiles in registers (no per-profile atomics).
-__global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProfiles P) {
+__global__ void __launch_bounds__(kPrepCta, 2) k_prep_mt(DevGrid g, Batch b, MtProfiles P) {
   extern __shared__ __align__(16) uint32_t bits[];
   __shared__ Topo t;
   constexpr int kRp = kMaxSplits + kMaxCols;
@@ -607,10 +607,20 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
       const double* fr0 = b.feat + feat_index(slot, b.nchunks, e, r);
       const double fc0 = fr0[0];
       const bool on = g.br_on[e] && !bit_get(rm_bits, e);
-      double phi[kMaxSplits], rho[kMaxCols];
+      // phi / rho in registers: unrolled loops with a CTA-uniform exit (ns, nv
+      // are the candidate's), so every index is static
+      double phi[kMaxSplits], rho[kSweepRank];
       const double be = g.br_b[e], ib = 1.0 / be;
-      for (int q = 0; q < ns; ++q) phi[q] = on ? fr0[1 + q] * ib : 0.0;
-      for (int m = 0; m < nv; ++m) rho[m] = on ? fr0[1 + ns + m] * ib : 0.0;
+#pragma unroll
+      for (int q = 0; q < kMaxSplits; ++q) {
+        if (q >= ns) break;
+        phi[q] = on ? fr0[1 + q] * ib : 0.0;
+      }
+#pragma unroll
+      for (int m = 0; m < kSweepRank; ++m) {
+        if (m >= nv) break;
+        rho[m] = on ? fr0[1 + ns + m] * ib : 0.0;
+      }
       unsigned long long* mk = reinterpret_cast<unsigned long long*>(b.feat_mt + feat_index(slot, b.nchunks, e, r + 1));
       unsigned long long kmax = 0ull, kmin = ~0ull;
       const double lim = g.br_lim[e];
@@ -620,8 +630,16 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
         double fc = 0.0;
         if (on) {  // cand_flow (topo.cuh) with this profile's base flow and Rp
           double acc = 0.0;
-          for (int q = 0; q < ns; ++q) acc = fma(phi[q], rp[q], acc);
-          for (int m = 0; m < nv; ++m) acc = fma(rho[m], rp[ns + m], acc);
+#pragma unroll
+          for (int q = 0; q < kMaxSplits; ++q) {
+            if (q >= ns) break;
+            acc = fma(phi[q], rp[q], acc);
+          }
+#pragma unroll
+          for (int m = 0; m < kSweepRank; ++m) {
+            if (m >= nv) break;
+            acc = fma(rho[m], rp[ns + m], acc);
+          }
           fc = P.f0[tt][e] + be * acc;
         }
         const unsigned cnt = __popc(__ballot_sync(0xffffffffu, valid && fabs(fc) > lim));
@@ -644,7 +662,7 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
     // contingencies: the topology part once (rk rows [0, S^-1 phi, -C^-1 rho]
     // at row_stride(r), profile-independent), alpha per profile ([t][n][Kpad])
     for (int k = threadIdx.x; k < g.Kpad; k += blockDim.x) {
-      double rk[kSweepRank];
+      double rks[kMaxSplits], rkv[kSweepRank];  // rk = [S^-1 phi, -C^-1 rho]
       double den = 1.0;
       bool live = false;  // regular contingency with an active outaged branch
       int beta = -1;
@@ -655,20 +673,40 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
         if (on) {
           const double* fr = b.feat + feat_index(slot, b.nchunks, beta, r);
           const double ib = 1.0 / g.br_b[beta];
-          double phi[kMaxSplits], rho[kMaxCols];
-          for (int q = 0; q < ns; ++q) phi[q] = fr[1 + q] * ib;
-          for (int m = 0; m < nv; ++m) rho[m] = fr[1 + ns + m] * ib;
+          double phi[kMaxSplits], rho[kSweepRank];
+#pragma unroll
+          for (int q = 0; q < kMaxSplits; ++q) {
+            if (q >= ns) break;
+            phi[q] = fr[1 + q] * ib;
+          }
+#pragma unroll
+          for (int m = 0; m < kSweepRank; ++m) {
+            if (m >= nv) break;
+            rho[m] = fr[1 + ns + m] * ib;
+          }
           double lr = 0.0;
-          for (int q = 0; q < ns; ++q) {
+#pragma unroll
+          for (int q = 0; q < kMaxSplits; ++q) {
+            if (q >= ns) break;
             double acc = 0.0;
-            for (int q2 = 0; q2 < ns; ++q2) acc += t.Sinv[q * kMaxSplits + q2] * phi[q2];
-            rk[q] = acc;
+#pragma unroll
+            for (int q2 = 0; q2 < kMaxSplits; ++q2) {
+              if (q2 >= ns) break;
+              acc += t.Sinv[q * kMaxSplits + q2] * phi[q2];
+            }
+            rks[q] = acc;
             lr += phi[q] * acc;
           }
-          for (int m = 0; m < nv; ++m) {
+#pragma unroll
+          for (int m = 0; m < kSweepRank; ++m) {
+            if (m >= nv) break;
             double acc = 0.0;
-            for (int m2 = 0; m2 < nv; ++m2) acc += t.Cinv[m * kMaxCols + m2] * rho[m2];
-            rk[ns + m] = -acc;
+#pragma unroll
+            for (int m2 = 0; m2 < kSweepRank; ++m2) {
+              if (m2 >= nv) break;
+              acc += t.Cinv[m * kMaxCols + m2] * rho[m2];
+            }
+            rkv[m] = -acc;
             lr -= rho[m] * acc;
           }
           den = 1.0 - (g.Tdiag[beta] + g.br_b[beta] * lr);
@@ -679,16 +717,29 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
         double row[kStride];
 #pragma unroll
         for (int i = 0; i < kStride; ++i) row[i] = 0.0;
-        if (live)
-          for (int i = 0; i < r; ++i) row[1 + i] = rk[i];
+        if (live) {
+#pragma unroll
+          for (int q = 0; q < kMaxSplits; ++q) {
+            if (q >= ns) break;
+            row[1 + q] = rks[q];
+          }
+#pragma unroll
+          for (int m = 0; m < kSweepRank; ++m) {
+            if (m >= nv) break;
+            row[1 + ns + m] = rkv[m];
+          }
+        }
         double2* dst = reinterpret_cast<double2*>(P.rk + static_cast<size_t>(c) * g.Kpad * kStride +
                                                   static_cast<size_t>(k) * rs);
 #pragma unroll
         for (int i = 0; i < kStride / 2; ++i)
           if (2 * i < rs) dst[i] = make_double2(row[2 * i], row[2 * i + 1]);
       }
-      double dlmax = 0.0, rqmax[kSweepRank];
-      for (int q = 0; q < r; ++q) rqmax[q] = 0.0;
+      double dlmax = 0.0, rqs[kMaxSplits], rqv[kSweepRank];  // max_t |rk alpha_t| per column
+#pragma unroll
+      for (int q = 0; q < kMaxSplits; ++q) rqs[q] = 0.0;
+#pragma unroll
+      for (int m = 0; m < kSweepRank; ++m) rqv[m] = 0.0;
       for (int tt = 0; tt < P.n_t; ++tt) {
         double alpha = 0.0;
         if (live) {
@@ -701,7 +752,18 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
           b.energy[static_cast<size_t>(tt) * P.energy_stride + static_cast<size_t>(c) * g.Kall + g.ks_cont[k]] =
               b.params.penalty;
         dlmax = fmax(dlmax, fabs(alpha - P.alpha0[tt][k]));
-        for (int q = 0; q < r; ++q) rqmax[q] = fmax(rqmax[q], fabs(rk[q] * alpha));
+        if (live) {  // (rk is zero otherwise: the maxima stay 0)
+#pragma unroll
+          for (int q = 0; q < kMaxSplits; ++q) {
+            if (q >= ns) break;
+            rqs[q] = fmax(rqs[q], fabs(rks[q] * alpha));
+          }
+#pragma unroll
+          for (int m = 0; m < kSweepRank; ++m) {
+            if (m >= nv) break;
+            rqv[m] = fmax(rqv[m], fabs(rkv[m] * alpha));
+          }
+        }
       }
       // fold into the bounds profile 0 wrote (tiles of 128: a warp is 32
       // consecutive contingencies of one tile, half a warp one sub-tile)
@@ -711,7 +773,13 @@ __global__ void __launch_bounds__(kPrepCta) k_prep_mt(DevGrid g, Batch b, MtProf
       if ((threadIdx.x & 15) == 0)
         atomicMax(b.amx_mt + (static_cast<size_t>(c) * ntiles + tile) * kTmaxSub + sub, dbits(dlmax));
       for (int q = 0; q < r; ++q) {
-        double rq = rqmax[q];
+        double rq = 0.0;  // rqmax[q] (static register indices)
+#pragma unroll
+        for (int i = 0; i < kMaxSplits; ++i)
+          if (i == q) rq = rqs[i];
+#pragma unroll
+        for (int m = 0; m < kSweepRank; ++m)
+          if (ns + m == q) rq = rqv[m];
 #pragma unroll
         for (int o = 16; o > 0; o >>= 1) rq = fmax(rq, __shfl_xor_sync(0xffffffffu, rq, o));
         if (lane == 0) atomicMax(b.rmx_mt + (static_cast<size_t>(c) * ntiles + tile) * kStride + 1 + q, dbits(rq));
