@@ -475,16 +475,19 @@ __device__ void solve_case(const AcGrid& g, const AcTopo& tp, const AcCases& io,
       }
       __syncthreads();
       lu_solve<NT>(w.J, w.dx, w.lm, nu, w.red, w.ired);
+      // step.allFinite() (ac_validator.cpp:239-241) tested with the update's
+      // barrier: a non-finite step ends the case unconverged, whose voltages
+      // are never reported, so applying it first changes no output
       bool fin = true;
-      for (int r = tid; r < nu; r += NT) fin = fin && isfinite(w.dx[r]);
-      if (!__syncthreads_and(fin)) break;
       for (int r = tid; r < nu; r += NT) {
+        const double d = w.dx[r];
+        fin = fin && isfinite(d);
         if (r < na)
-          w.va[w.ang[r]] += w.dx[r];
+          w.va[w.ang[r]] += d;
         else
-          w.vm[w.mag[r - na]] += w.dx[r];
+          w.vm[w.mag[r - na]] += d;
       }
-      __syncthreads();
+      if (!__syncthreads_and(fin)) break;
     }
   }
 
