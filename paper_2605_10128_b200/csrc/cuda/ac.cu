@@ -185,7 +185,7 @@ __device__ __forceinline__ BranchY branch_y(const AcGrid& g, int e) {
 // a zero pivot leaves non-finite entries, tested by the caller like the
 // reference's step.allFinite() (ac_validator.cpp:239-241).
 template <int NT>
-__device__ void lu_solve(double* J, double* dx, double* lm, int nu, double* red, int* ired) {
+__device__ __forceinline__ void lu_solve(double* J, double* dx, double* lm, int nu, double* red, int* ired) {
   const int tid = threadIdx.x;
   for (int k = 0; k < nu; ++k) {
     double best = -1.0;
@@ -555,11 +555,17 @@ __device__ __forceinline__ AcWs rebase(const AcWs& rel, unsigned char* base) {
   return w;
 }
 
-template <int NT>
+// SMEM: the workspace is the dynamic shared memory (a separate instantiation,
+// so every workspace pointer is provably shared: LDS / STS with 32-bit
+// addresses instead of generic loads), else the CTA's HBM scratch slot
+template <int NT, bool SMEM>
 __global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? 2 : 14))
     k_ac_case(AcGrid g, AcTopo tp, AcCases io, AcSolver sv, AcWs rel) {
   extern __shared__ __align__(16) unsigned char ac_smem[];
-  unsigned char* base = sv.in_smem ? ac_smem : sv.scratch + static_cast<size_t>(blockIdx.x) * sv.ws_bytes;
+  // (the scratch instantiation keeps the runtime choice: its generic-pointer
+  // code measured faster on the 118-bus case than a provably global base)
+  unsigned char* base =
+      SMEM || sv.in_smem ? ac_smem : sv.scratch + static_cast<size_t>(blockIdx.x) * sv.ws_bytes;
   const AcWs w = rebase(rel, base);
   for (int c = blockIdx.x; c < io.n; c += gridDim.x) solve_case<NT>(g, tp, io, sv, c, w);
 }
@@ -641,18 +647,28 @@ void ac_launch_cases(const AcGrid& g, const AcTopo& t, const AcCases& c, const A
   const size_t smem = sv.in_smem ? sv.ws_bytes : 0;
   AcWs rel;
   ws_layout(sv.n_bus, sv.nu, g.E, nullptr, &rel);
+  auto launch = [&](auto kern, int nt) {
+    cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
+    kern<<<ctas, nt, smem, s>>>(g, t, c, sv, rel);
+  };
   switch (ac_threads(sv.nu)) {
     case 64:
-      cudaFuncSetAttribute(k_ac_case<64>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_ac_case<64><<<ctas, 64, smem, s>>>(g, t, c, sv, rel);
+      if (sv.in_smem)
+        launch(k_ac_case<64, true>, 64);
+      else
+        launch(k_ac_case<64, false>, 64);
       break;
     case 256:
-      cudaFuncSetAttribute(k_ac_case<256>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_ac_case<256><<<ctas, 256, smem, s>>>(g, t, c, sv, rel);
+      if (sv.in_smem)
+        launch(k_ac_case<256, true>, 256);
+      else
+        launch(k_ac_case<256, false>, 256);
       break;
     default:
-      cudaFuncSetAttribute(k_ac_case<512>, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
-      k_ac_case<512><<<ctas, 512, smem, s>>>(g, t, c, sv, rel);
+      if (sv.in_smem)
+        launch(k_ac_case<512, true>, 512);
+      else
+        launch(k_ac_case<512, false>, 512);
       break;
   }
 }
