@@ -2131,6 +2131,10 @@ struct tg_ac_context {
   double *d_energy = nullptr, *d_flo = nullptr, *d_loading = nullptr, *d_vm = nullptr, *d_va = nullptr;
   unsigned long long* d_fold = nullptr;
   unsigned char* d_scratch = nullptr;
+  unsigned* d_next_case = nullptr;
+  // pinned host staging of one call's inputs and per-case outputs (grow only)
+  unsigned char* h_stage = nullptr;
+  size_t h_stage_cap = 0;
 
   struct Result {
     std::vector<uint8_t> conv;
@@ -2185,7 +2189,7 @@ tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, 
   const tgb::AcSolver sv0 = ac_solver(*this, n_a);
   // HBM-scratch path: two 512-thread CTAs per SM (64 registers), the slots' Jacobians (the LU's
   // working set) stay within L2 for mid-size networks
-  int slots = sv0.in_smem ? std::min(nc, 148 * 32)
+  int slots = sv0.in_smem ? nc  // one CTA per case: the block scheduler balances the uneven Newton runs
                           : std::max(1, std::min<int>({nc, 148 * 2, static_cast<int>(kAcScratchBudget / sv0.ws_bytes)}));
   const size_t scratch = sv0.in_smem ? 0 : static_cast<size_t>(slots) * sv0.ws_bytes;
   const size_t rows = loading ? static_cast<size_t>(nc) * E : 0;
@@ -2220,15 +2224,34 @@ tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, 
     d_energy = work->alloc<double>(cap_cases);
     d_loading = work->alloc<double>(std::max<size_t>(cap_rows, 1));
     d_scratch = cap_scratch ? work->alloc<unsigned char>(cap_scratch) : nullptr;
+    d_next_case = work->alloc<unsigned>(1);
   }
-  std::vector<uint8_t> fc(nc);
+  // inputs and per-case outputs through one pinned staging block (pageable
+  // copies would each be staged by the driver synchronously)
+  const size_t gbytes = sizeof(int32_t) * n_genomes * (n_a + n_d), cbytes = sizeof(int32_t) * nc;
+  auto up16 = [](size_t b) { return (b + 15) & ~size_t(15); };
+  const size_t o_g = 0, o_cg = up16(gbytes), o_ck = o_cg + up16(cbytes), o_fc = o_ck + up16(cbytes);
+  const size_t o_conv = o_fc + up16(nc), o_iters = o_conv + up16(nc), o_crit = o_iters + up16(cbytes);
+  const size_t o_energy = o_crit + up16(cbytes), o_nonconv = o_energy + up16(sizeof(double) * nc);
+  const size_t o_fcrit = o_nonconv + up16(sizeof(int) * n_genomes), o_flo = o_fcrit + up16(sizeof(int) * n_genomes);
+  const size_t stage_bytes = o_flo + up16(sizeof(double) * n_genomes);
+  if (stage_bytes > h_stage_cap) {
+    check(cudaStreamSynchronize(stream), "AC sync");
+    if (h_stage) cudaFreeHost(h_stage);
+    h_stage = nullptr;
+    h_stage_cap = std::max(stage_bytes, 2 * h_stage_cap);
+    check(cudaMallocHost(reinterpret_cast<void**>(&h_stage), h_stage_cap), "cudaMallocHost");
+  }
+  if (n_genomes) std::memcpy(h_stage + o_g, genomes, gbytes);
+  std::memcpy(h_stage + o_cg, cg.data(), cbytes);
+  std::memcpy(h_stage + o_ck, ck.data(), cbytes);
+  uint8_t* fc = h_stage + o_fc;
   for (int c = 0; c < nc; ++c) fc[c] = fold && ck[c] >= 0;
   if (n_genomes)
-    check(cudaMemcpyAsync(d_genomes, genomes, sizeof(int32_t) * n_genomes * (n_a + n_d), cudaMemcpyHostToDevice,
-                          stream), "AC genomes H2D");
-  check(cudaMemcpyAsync(d_case_g, cg.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, stream), "AC cases");
-  check(cudaMemcpyAsync(d_case_k, ck.data(), sizeof(int32_t) * nc, cudaMemcpyHostToDevice, stream), "AC cases");
-  check(cudaMemcpyAsync(d_foldcase, fc.data(), nc, cudaMemcpyHostToDevice, stream), "AC cases");
+    check(cudaMemcpyAsync(d_genomes, h_stage + o_g, gbytes, cudaMemcpyHostToDevice, stream), "AC genomes H2D");
+  check(cudaMemcpyAsync(d_case_g, h_stage + o_cg, cbytes, cudaMemcpyHostToDevice, stream), "AC cases");
+  check(cudaMemcpyAsync(d_case_k, h_stage + o_ck, cbytes, cudaMemcpyHostToDevice, stream), "AC cases");
+  check(cudaMemcpyAsync(d_foldcase, fc, nc, cudaMemcpyHostToDevice, stream), "AC cases");
   if (fold) {
     check(cudaMemsetAsync(d_fold, 0, sizeof(unsigned long long) * n_genomes * E, stream), "AC fold reset");
     check(cudaMemsetAsync(d_nonconv, 0, sizeof(int) * n_genomes, stream), "AC fold reset");
@@ -2252,6 +2275,8 @@ tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, 
   io.nonconverged = fold ? d_nonconv : nullptr;
   tgb::AcSolver sv = sv0;
   sv.scratch = d_scratch;
+  sv.next_case = sv.in_smem ? nullptr : d_next_case;
+  if (!sv.in_smem) check(cudaMemsetAsync(d_next_case, 0, sizeof(unsigned), stream), "AC case counter");
   tgb::ac_launch_cases(g, tp, io, sv, slots, stream);
   launches += 2;
   if (fold) {
@@ -2260,14 +2285,10 @@ tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, 
   }
   check(cudaGetLastError(), "AC launch");
   Result r;
-  r.conv.resize(nc);
-  r.iters.resize(nc);
-  r.crit.resize(nc);
-  r.energy.resize(nc);
-  check(cudaMemcpyAsync(r.conv.data(), d_conv, nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
-  check(cudaMemcpyAsync(r.iters.data(), d_iters, sizeof(int) * nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
-  check(cudaMemcpyAsync(r.crit.data(), d_crit, sizeof(int) * nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
-  check(cudaMemcpyAsync(r.energy.data(), d_energy, sizeof(double) * nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  check(cudaMemcpyAsync(h_stage + o_conv, d_conv, nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  check(cudaMemcpyAsync(h_stage + o_iters, d_iters, cbytes, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  check(cudaMemcpyAsync(h_stage + o_crit, d_crit, cbytes, cudaMemcpyDeviceToHost, stream), "AC D2H");
+  check(cudaMemcpyAsync(h_stage + o_energy, d_energy, sizeof(double) * nc, cudaMemcpyDeviceToHost, stream), "AC D2H");
   if (loading)
     check(cudaMemcpyAsync(loading, d_loading, sizeof(double) * rows, cudaMemcpyDeviceToHost, stream), "AC D2H");
   if (vm) {
@@ -2275,15 +2296,26 @@ tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, 
     check(cudaMemcpyAsync(va, d_loading + rows + vrows, sizeof(double) * vrows, cudaMemcpyDeviceToHost, stream), "AC D2H");
   }
   if (fold) {
-    r.nonconv.resize(n_genomes);
-    r.fold_crit.resize(n_genomes);
-    r.fold_lambda_o.resize(n_genomes);
-    check(cudaMemcpyAsync(r.nonconv.data(), d_nonconv, sizeof(int) * n_genomes, cudaMemcpyDeviceToHost, stream), "AC D2H");
-    check(cudaMemcpyAsync(r.fold_crit.data(), d_fcrit, sizeof(int) * n_genomes, cudaMemcpyDeviceToHost, stream), "AC D2H");
-    check(cudaMemcpyAsync(r.fold_lambda_o.data(), d_flo, sizeof(double) * n_genomes, cudaMemcpyDeviceToHost, stream),
+    check(cudaMemcpyAsync(h_stage + o_nonconv, d_nonconv, sizeof(int) * n_genomes, cudaMemcpyDeviceToHost, stream),
           "AC D2H");
+    check(cudaMemcpyAsync(h_stage + o_fcrit, d_fcrit, sizeof(int) * n_genomes, cudaMemcpyDeviceToHost, stream), "AC D2H");
+    check(cudaMemcpyAsync(h_stage + o_flo, d_flo, sizeof(double) * n_genomes, cudaMemcpyDeviceToHost, stream), "AC D2H");
   }
   check(cudaStreamSynchronize(stream), "AC cases");
+  auto take = [&](auto& v, size_t off, size_t count) {
+    using T = typename std::decay_t<decltype(v)>::value_type;
+    v.resize(count);
+    std::memcpy(v.data(), h_stage + off, sizeof(T) * count);
+  };
+  take(r.conv, o_conv, nc);
+  take(r.iters, o_iters, nc);
+  take(r.crit, o_crit, nc);
+  take(r.energy, o_energy, nc);
+  if (fold) {
+    take(r.nonconv, o_nonconv, n_genomes);
+    take(r.fold_crit, o_fcrit, n_genomes);
+    take(r.fold_lambda_o, o_flo, n_genomes);
+  }
   return r;
 }
 
@@ -2376,6 +2408,7 @@ void tg_ac_context_destroy(tg_ac_context* ctx) {
   cudaSetDevice(ctx->device);
   if (ctx->stream) cudaStreamSynchronize(ctx->stream);
   ctx->work.reset();
+  if (ctx->h_stage) cudaFreeHost(ctx->h_stage);
   if (ctx->stream) cudaStreamDestroy(ctx->stream);
   delete ctx;
 }

@@ -567,7 +567,22 @@ __global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? 2 : 14))
   unsigned char* base =
       SMEM || sv.in_smem ? ac_smem : sv.scratch + static_cast<size_t>(blockIdx.x) * sv.ws_bytes;
   const AcWs w = rebase(rel, base);
-  for (int c = blockIdx.x; c < io.n; c += gridDim.x) solve_case<NT>(g, tp, io, sv, c, w);
+  if (SMEM || sv.next_case == nullptr) {
+    // shared-memory workspace: one CTA per case (the block scheduler balances
+    // the uneven Newton runs)
+    for (int c = blockIdx.x; c < io.n; c += gridDim.x) solve_case<NT>(g, tp, io, sv, c, w);
+  } else {
+    // scratch slots (one per resident CTA): cases claimed dynamically
+    __shared__ int next_s;
+    for (;;) {
+      if (threadIdx.x == 0) next_s = static_cast<int>(atomicAdd(sv.next_case, 1u));
+      __syncthreads();
+      const int c = next_s;
+      __syncthreads();
+      if (c >= io.n) break;
+      solve_case<NT>(g, tp, io, sv, c, w);
+    }
+  }
 }
 
 // apply_genome (genome.cpp:76-110): base endpoints, disconnections removed,

@@ -89,6 +89,7 @@ struct AcSolver {
   int in_smem;      // workspace in dynamic shared memory (else scratch + blockIdx.x * ws_bytes)
   size_t ws_bytes;  // per-CTA workspace
   unsigned char* scratch;
+  unsigned* next_case;  // scratch path: dynamic case counter (zeroed per launch)
 };
 
 size_t ac_workspace_bytes(int n_bus, int nu, int E);
