@@ -524,7 +524,8 @@ __device__ __forceinline__ void prep_segment_dispatch(const DevGrid& g, const Ba
 // Ranks [RLO, RHI] from the rank buckets of k_bucket (one register allocation
 // per class; the classes run as separate launches).
 template <int RLO, int RHI>
-__global__ void __launch_bounds__(32 * kPrepRowWarps, RHI <= 4 ? 4 : (RHI <= 7 ? 3 : 2)) k_prep_rows(DevGrid g, Batch b) {
+__global__ void __launch_bounds__(32 * kPrepRowWarps, RHI <= 4 ? 4 : (RHI <= 7 ? 3 : 2))
+    k_prep_rows(DevGrid g, Batch b, unsigned* ctr) {
   __shared__ PcFac slab[kPrepRowWarps];
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   PcFac& f = slab[warp];
@@ -534,7 +535,13 @@ __global__ void __launch_bounds__(32 * kPrepRowWarps, RHI <= 4 ? 4 : (RHI <= 7 ?
   const int ncand = b.wl_start[RHI] + b.wl_count[RHI] - first;
   const unsigned total = static_cast<unsigned>(ncand) * static_cast<unsigned>(nseg);  // 32-bit: cheap division
   int loaded = -1;
-  for (unsigned w = blockIdx.x * kPrepRowWarps + warp; w < total; w += gridDim.x * kPrepRowWarps) {
+  for (;;) {
+    // items claimed from a counter (a static striding leaves the last CTA wave
+    // partly filled)
+    unsigned w = 0;
+    if (lane == 0) w = atomicAdd(ctr, 1u);
+    w = __shfl_sync(0xffffffffu, w, 0);
+    if (w >= total) break;
     const unsigned ci = w / static_cast<unsigned>(nseg);
     const int c = b.wl_list[first + static_cast<int>(ci)];
     const int sg = static_cast<int>(w - ci * static_cast<unsigned>(nseg));
@@ -1268,9 +1275,10 @@ int launch_prep(const DevGrid& g, Batch& b, int n_a, int n_d, const EvalScratch&
     // few CTAs), at most 8 CTAs per SM
     const long seg = (b.nchunks + g.Kpad / 32 + kPrepSeg - 1) / kPrepSeg;
     const int rows_grid = static_cast<int>(std::min<long>(148 * 8, (static_cast<long>(b.n) * seg + 7) / 8));
-    k_prep_rows<0, 4><<<rows_grid, 256, 0, stream>>>(g, b);
-    k_prep_rows<5, kChunkedMaxRank><<<rows_grid, 256, 0, stream>>>(g, b);  // without the rank 8-11 registers
-    k_prep_rows<kChunkedMaxRank + 1, kSweepRank><<<rows_grid, 256, 0, stream>>>(g, b);
+    cudaMemsetAsync(b.item_ctr + 1, 0, 3 * sizeof(unsigned int), stream);  // the classes' item counters
+    k_prep_rows<0, 4><<<rows_grid, 256, 0, stream>>>(g, b, b.item_ctr + 1);
+    k_prep_rows<5, kChunkedMaxRank><<<rows_grid, 256, 0, stream>>>(g, b, b.item_ctr + 2);  // without the rank 8-11 registers
+    k_prep_rows<kChunkedMaxRank + 1, kSweepRank><<<rows_grid, 256, 0, stream>>>(g, b, b.item_ctr + 3);
     return 4;
   }
   const size_t bits_bytes = 2 * static_cast<size_t>((g.E + 31) >> 5) * sizeof(uint32_t);
