@@ -2187,10 +2187,9 @@ tg_ac_context::Result tg_ac_context::run(const int32_t* genomes, int n_genomes, 
     if (cg[c] < 0 || cg[c] >= n_genomes || ck[c] < -1 || ck[c] >= K)
       throw tgb::ValidationError("AC case " + std::to_string(c) + " out of range");
   const tgb::AcSolver sv0 = ac_solver(*this, n_a);
-  // HBM-scratch path: two 512-thread CTAs per SM (64 registers), the slots' Jacobians (the LU's
-  // working set) stay within L2 for mid-size networks
+  // HBM-scratch path: one slot per resident CTA, four 256-thread CTAs per SM (64 registers)
   int slots = sv0.in_smem ? nc  // one CTA per case: the block scheduler balances the uneven Newton runs
-                          : std::max(1, std::min<int>({nc, 148 * 2, static_cast<int>(kAcScratchBudget / sv0.ws_bytes)}));
+                          : std::max(1, std::min<int>({nc, 148 * 4, static_cast<int>(kAcScratchBudget / sv0.ws_bytes)}));
   const size_t scratch = sv0.in_smem ? 0 : static_cast<size_t>(slots) * sv0.ws_bytes;
   const size_t rows = loading ? static_cast<size_t>(nc) * E : 0;
   const size_t vrows = vm ? static_cast<size_t>(nc) * (N + n_a) : 0;

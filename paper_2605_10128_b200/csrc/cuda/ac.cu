@@ -559,7 +559,7 @@ __device__ __forceinline__ AcWs rebase(const AcWs& rel, unsigned char* base) {
 // so every workspace pointer is provably shared: LDS / STS with 32-bit
 // addresses instead of generic loads), else the CTA's HBM scratch slot
 template <int NT, bool SMEM>
-__global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? 2 : 14))
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? (SMEM ? 2 : 4) : 14))
     k_ac_case(AcGrid g, AcTopo tp, AcCases io, AcSolver sv, AcWs rel) {
   extern __shared__ __align__(16) unsigned char ac_smem[];
   // (the scratch instantiation keeps the runtime choice: its generic-pointer
@@ -666,7 +666,9 @@ void ac_launch_cases(const AcGrid& g, const AcTopo& t, const AcCases& c, const A
     cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(smem));
     kern<<<ctas, nt, smem, s>>>(g, t, c, sv, rel);
   };
-  switch (ac_threads(sv.nu)) {
+  // scratch: four 256-thread CTAs per SM at 64 registers (cases claimed from a
+  // counter; 4 x 256 measured 719 /s on the 118-bus case, 2 x 512: 525, 8 x 128: 679)
+  switch (sv.in_smem ? ac_threads(sv.nu) : 256) {
     case 64:
       if (sv.in_smem)
         launch(k_ac_case<64, true>, 64);
