@@ -559,7 +559,7 @@ __device__ __forceinline__ AcWs rebase(const AcWs& rel, unsigned char* base) {
 // so every workspace pointer is provably shared: LDS / STS with 32-bit
 // addresses instead of generic loads), else the CTA's HBM scratch slot
 template <int NT, bool SMEM>
-__global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? (SMEM ? 2 : 4) : 14))
+__global__ void __launch_bounds__(NT, NT == 512 ? 2 : (NT == 256 ? (SMEM ? 2 : 4) : 16))
     k_ac_case(AcGrid g, AcTopo tp, AcCases io, AcSolver sv, AcWs rel) {
   extern __shared__ __align__(16) unsigned char ac_smem[];
   // (the scratch instantiation keeps the runtime choice: its generic-pointer
